@@ -1,0 +1,316 @@
+#!/usr/bin/env python
+"""GDP policy-step benchmark (BASELINE.json metric: sampled placements/sec for the full
+policy step -- embed -> place -> sample -> cost -> grad -> allreduce -- on the synthetic
+50k-node 8-layer-GNMT-shaped graph).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4] [--batch B] [--impl reference]
+
+One process per GPU (torchrun for N > 1, NCCL).  Placements are sharded across ranks
+(each rank samples B_g = --batch placements with global indices rank*B_g + b), rewards
+are all-gathered for the advantage baseline, gradients all-reduced.  Rank 0 prints one
+JSON line.  --impl reference times the CPU oracle (oracle/, the plain fp64 reference)
+on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import workloads  # noqa: E402
+
+METRIC = "sampled placements/sec (policy fwd+bwd+cost) on 50k-node GNMT graph at 1/2/4/8 B200"
+UNIT = "placements/s"
+
+
+def peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "sm_max_mhz": 1965.0, "_fallback": True}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.lines, self.proc = index, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.Q,
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for ln in self.proc.stdout:
+            self.lines.append(ln.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- CPU oracle timing
+def oracle_placements_per_s(W, B_total: int, n_cost: int, threads: int):
+    """Time the oracle (as it stands) on a bounded sample of the workload: one full fp64
+    policy fwd+bwd per graph plus the cost model on n_cost placements per graph over
+    `threads` host threads; the step time is extrapolated to B_total placements."""
+    import oracle
+    from oracle import sampling as Osa
+    from oracle import simulate as Osim
+    t_net = 0.0
+    t_cost_per = 0.0
+    for g in W.graphs:
+        X = workloads.features(g)
+        pg = oracle.prepare(g, X)
+        th = workloads.init_theta(workloads.F, W.d, seed=7)
+        t0 = time.perf_counter()
+        E = oracle.embed(pg, th, W.d)
+        z = oracle.place(pg, th, E, W.d, W.seg_len, W.mem_len, W.superposition)
+        U = Osa.uniforms(g.N, n_cost, W.seed, 0, 0)
+        D, _, _ = Osa.sample(z, U, pg.lead)
+        t1 = time.perf_counter()
+        topo = workloads.topology(g, W.d)
+        r = Osim.simulate_batch(g, topo, D, threads=threads)
+        t2 = time.perf_counter()
+        A, _, _ = Osa.advantage(r["reward"], 0.0, 0)
+        oracle.policy_grad(pg, th, W.d, W.seg_len, W.mem_len, W.superposition, D, A, loss_scale=1.0 / n_cost)
+        t3 = time.perf_counter()
+        t_net += (t1 - t0) + (t3 - t2)
+        t_cost_per += (t2 - t1) / n_cost
+    step = t_net + t_cost_per * B_total
+    return B_total / step, dict(t_net_s=t_net, t_cost_per_placement_s=t_cost_per)
+
+
+def run_reference(args, W, rank: int):
+    """--impl reference: the oracle timed on the host cores, rank 0 only."""
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    n_cost = min(args.batch, 16)
+    vals = []
+    for i in range(args.warmup + args.steps):
+        v, info = oracle_placements_per_s(W, args.batch, n_cost, threads)
+        if i >= args.warmup:
+            vals.append(v)
+    value = statistics.median(vals)
+    sample = (f"per step: full fp64 oracle policy fwd+bwd (N={sum(g.N for g in W.graphs)}) + cost model on "
+              f"{n_cost} of {args.batch} placements over {threads} threads; step time extrapolated to "
+              f"B={args.batch}")
+    out = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * args.batch / value,
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64/i64",
+           "data": "synthetic", "config": config_json(W, args),
+           "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": sample},
+           "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+           "detail": info}
+    print(json.dumps(out), flush=True)
+
+
+def config_json(W, args):
+    g = W.graphs
+    return {"workload": W.name, "graphs": [x.name for x in g], "nodes": [x.N for x in g],
+            "edges": [x.E for x in g], "devices_d": W.d, "seg_len": W.seg_len, "mem_len": W.mem_len,
+            "superposition": W.superposition, "batch_per_gpu": args.batch,
+            "global_batch": args.batch * args.gpus, "parallelism": f"dp{args.gpus} (placements sharded)",
+            "l2": "flushed between timed steps (512 MiB write)"}
+
+
+# ----------------------------------------------------------------------------- GPU arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c4")
+    ap.add_argument("--batch", type=int, default=None)
+    ap.add_argument("--mem-len", type=int, default=None)
+    ap.add_argument("--impl", default="gdp", choices=["gdp", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    W = workloads.config(args.config, batch=args.batch, mem_len=args.mem_len)
+    args.batch = W.batch
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, W, rank)
+        return
+
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    import __graft_entry__
+    if rank == 0:
+        __graft_entry__.build()
+    if world > 1:
+        dist.barrier()
+    import paper_1910_01578_b200 as gdp
+
+    graphs = [(g, workloads.features(g), workloads.topology(g, W.d)) for g in W.graphs]
+    ps = gdp.PolicyStep(graphs, W.d, W.seg_len, W.mem_len, W.superposition, W.batch, seed=W.seed,
+                        mode="samples", rank=rank, world=world, device=dev)
+    th = workloads.init_theta(workloads.F, W.d, seed=7)
+    theta = torch.from_numpy(th).to(dev)
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+
+    def sync():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+            torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        ps.run(theta)
+    sync()
+    ps.events.clear()
+    times = []
+    launches0 = gdp.launch_count()
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            flush.fill_(1.0)
+            sync()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+            ps.run(theta, timed=True)
+            e1.record()
+            sync()
+            times.append(e0.elapsed_time(e1))
+    launches = (gdp.launch_count() - launches0) // args.steps
+    total_ms = sum(times)
+    if world > 1:
+        t = torch.tensor([total_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    placements = W.batch * world * len(W.graphs) * args.steps
+    value = placements / (total_ms / 1000.0)
+
+    # dominant kernel: the cost model (one CTA per placement); per-launch time from events
+    cost_ms = [a.elapsed_time(b) for a, b in zip(ps.events["cost0"], ps.events["cost1"])]
+    grad_ms = [a.elapsed_time(b) for a, b in zip(ps.events["grad0"], ps.events["grad1"])]
+    place_ms = [a.elapsed_time(b) for a, b in zip(ps.events["place0"], ps.events["sample0"])]
+    embed_ms = [a.elapsed_time(b) for a, b in zip(ps.events["embed0"], ps.events["place0"])]
+    sample_ms = [a.elapsed_time(b) for a, b in zip(ps.events["sample0"], ps.events["cost0"])]
+    cost_avg = statistics.mean(cost_ms)
+    # algorithmic work of one cost launch: per placement N + E events,
+    # i.e. one dispatch/finish per op and one relaxation per edge; B placements per launch
+    events_per_launch = sum(g.N + g.E for g in W.graphs) * W.batch / len(W.graphs)
+    achieved = events_per_launch / (cost_avg / 1000.0) / 1e9          # Gevent/s
+    pk = peaks()
+    sm_mhz = pk.get("sm_max_mhz", 1965.0)
+    # ALU roofline of an event: one warp-instruction issue slot per event per SMSP
+    # (148 SMs x 4 schedulers x clock); DESIGN.md §"Roofline of the cost model"
+    peak_gev = 148 * 4 * sm_mhz * 1e6 / 1e9
+    roof = {"kernel": "k_cost", "bound": "alu", "achieved": achieved, "peak": peak_gev, "unit": "Gevent/s",
+            "frac": achieved / peak_gev, "traffic": None,
+            "peak_source": "148 SM x 4 issue/clk x sm_max_mhz (MEASURED_PEAKS.json)",
+            "share_of_step": sum(cost_ms) / sum(times)}
+
+    # e2e through the public API with host buffers: theta H2D, step, grad + rewards D2H
+    e2e = None
+    if not args.no_e2e:
+        th_host = torch.from_numpy(th).pin_memory()
+        g_host = torch.empty(ps.n_params, dtype=torch.float32).pin_memory()
+        r_host = [torch.empty(st.B, dtype=torch.float64).pin_memory() for st in ps.states]
+        theta2 = torch.empty_like(theta)
+        et = []
+        for _ in range(max(2, args.steps // 2)):
+            flush.fill_(1.0)
+            sync()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+            theta2.copy_(th_host, non_blocking=True)
+            ps.run(theta2)
+            g_host.copy_(ps.grad, non_blocking=True)
+            for st, rh in zip(ps.states, r_host):
+                rh.copy_(st.reward, non_blocking=True)
+            e1.record()
+            sync()
+            et.append(e0.elapsed_time(e1))
+        tot = sum(et)
+        if world > 1:
+            t = torch.tensor([tot], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            tot = float(t.item())
+        e2e = {"value": W.batch * world * len(W.graphs) * len(et) / (tot / 1000.0), "unit": UNIT,
+               "h2d_bytes_per_step": th.nbytes, "d2h_bytes_per_step": 4 * ps.n_params + 8 * W.batch * len(W.graphs)}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        n_cost = min(W.batch, 16)
+        v, info = oracle_placements_per_s(W, W.batch, n_cost, threads)
+        cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": "oracle",
+               "sample": (f"one full fp64 oracle policy fwd+bwd (N={sum(g.N for g in W.graphs)}) + cost model on "
+                          f"{n_cost} of {W.batch} placements over {threads} threads; step extrapolated to "
+                          f"B={W.batch}"), "detail": info}
+
+    if rank == 0:
+        st0 = ps.states[0]
+        rep = st0.reports()
+        out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+               "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+               "scaling": "weak", "vs_baseline": None, "dtype": "f32/i32", "data": "synthetic",
+               "config": config_json(W, argparse.Namespace(batch=W.batch, gpus=world)),
+               "clocks": clk.summary(), "gpu_launches": int(launches), "roofline": roof, "e2e": e2e,
+               "cpu_baseline": cpu,
+               "stages_ms": {"embed": statistics.mean(embed_ms), "place": statistics.mean(place_ms),
+                             "sample": statistics.mean(sample_ms), "cost": cost_avg,
+                             "grad": statistics.mean(grad_ms)},
+               "valid_frac": float(np.mean(rep["valid"])), "makespan_mean_ticks": float(np.mean(rep["makespan"]))}
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,249 @@
+/*
+ * gdp.h -- C ABI of libgdp.so, the B200 (sm_100a) hot path of GDP
+ * ("GDP: Generalized Device Placement for Dataflow Graphs", arXiv 1910.01578).
+ *
+ * One batched policy step (§3, Eq. 1-4; §4.1 reward):
+ *   gdp_embed        GraphSAGE max-pool embedding            (§3.1, Eq. 2-3)
+ *   gdp_place        segment-recurrent Transformer-XL placer  (§3.2-3.3, Eq. 4)
+ *                    with superposition conditioning -> per-node device logits
+ *   gdp_sample       B placements D ~ pi_theta(G)             (§3)
+ *   gdp_cost         step-time cost model + reward            (§4.1)
+ *   gdp_advantage    reward minus mean of all previous trials (§4.1)
+ *   gdp_policy_grad  PPO / REINFORCE gradient of theta        (§3, Eq. 1)
+ *
+ * Conventions (all entry points):
+ *   - Plain pointers only.  "dev" pointers are CUDA device memory on the current
+ *     device, "host" pointers are host memory.  The caller owns every buffer passed
+ *     in; the library owns gdp_graph / gdp_topo objects until their destroy call.
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *     Compute calls are asynchronous on `stream`; argument validation is synchronous
+ *     and returns a status.  Device faults surface at the caller's next sync.
+ *   - No allocation happens inside the hot-path calls: all scratch comes from the
+ *     caller's workspace `ws` (size from gdp_workspace_size).
+ *   - Per-node arrays at the boundary are in the CALLER's node-id order.  The
+ *     library computes the Kahn order pi (ties by smallest id) and runs
+ *     the segment-recurrent placer in pi order internally.
+ *   - Same inputs => bit-identical outputs.
+ *   - Errors: a status code (never an exception); gdp_last_error() gives a
+ *     thread-local message.  An invalid placement is a verdict in the report,
+ *     not an error.
+ */
+#ifndef GDP_H_
+#define GDP_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  GDP_OK = 0,
+  GDP_ERR_ARG = 1,        /* bad scalar argument / null pointer / unsupported config */
+  GDP_ERR_GRAPH = 2,      /* edge endpoint out of range, self edge, duplicate edge, negative cost/bytes */
+  GDP_ERR_CYCLE = 3,      /* the edge list is not a DAG */
+  GDP_ERR_SHAPE = 4,      /* sizes disagree (e.g. F or d differs from the graph / config) */
+  GDP_ERR_CUDA = 5,       /* a CUDA call failed (message in gdp_last_error) */
+  GDP_ERR_OVERFLOW = 6,   /* sum of durations + transfers could reach 2^31 ticks (device time is int32) */
+  GDP_ERR_NONFINITE = 7,  /* reserved: non-finite gradient */
+  GDP_ERR_WORKSPACE = 8   /* ws_bytes smaller than gdp_workspace_size */
+} gdp_status;
+
+typedef struct gdp_graph_s *gdp_graph;
+typedef struct gdp_topo_s *gdp_topo;
+
+/* Model configuration.  The network sizes are the SURVEY §8 defaults
+ * (h = 64, 4 heads, 3 GNN rounds, 2 placement layers + 1 conditioner layer,
+ * FFN 4h); other values return GDP_ERR_ARG. */
+typedef struct {
+  int32_t hidden;         /* h, must be 64 */
+  int32_t heads;          /* must be 4 (head dim 16) */
+  int32_t gnn_layers;     /* L, must be 3 */
+  int32_t xl_layers;      /* must be 2 */
+  int32_t ffn;            /* must be 256 */
+  int32_t num_devices;    /* d, 1..8 ("up to eight") */
+  int32_t seg_len;        /* S >= 1: Transformer-XL segment length */
+  int32_t mem_len;        /* M >= 0 cached positions before each segment, or -1 = every earlier segment */
+  int32_t superposition;  /* 1: Eq. 4 gates on every placer dense map and the head; 0: gates == 1 */
+} gdp_config;
+
+/* One cost-model verdict per placement. */
+typedef struct {
+  int64_t makespan;       /* ticks (1 tick = 1 us) */
+  int64_t cross_bytes;    /* sum of output_bytes over cross-device edges */
+  uint8_t valid;          /* 1 iff violation == 0 */
+  uint8_t violation;      /* 0 none, 1 co-location, 2 out of memory, 3 malformed (device id >= d) */
+  uint8_t pad[6];
+} gdp_sim_report;
+
+/* Flat parameter vector theta (fp32), in this order.  Matrices are row-major
+ * fan_in x fan_out; every dense map is y = x W + b.  Gate projections P_j (64 x w_j)
+ * and q_j (w_j) give gamma_j = 2 sigmoid(z P_j + q_j) for the placer's dense maps
+ * (gate0.* for placement layer 0, gate1.* for layer 1, gate.head for the head). */
+typedef enum {
+  GDP_P_GNN_IN_W = 0,   /* F x 64    input projection */
+  GDP_P_GNN_IN_B,       /* 64 */
+  GDP_P_GNN_0_W,        /* 64 x 64   Eq. 2 W^(0) */
+  GDP_P_GNN_0_B,        /* 64        Eq. 2 b^(0) */
+  GDP_P_GNN_0_WF,       /* 128 x 64  Eq. 3 f^(1) on concat(h_v, h_N(v)) */
+  GDP_P_GNN_0_BF,       /* 64 */
+  GDP_P_GNN_1_W, GDP_P_GNN_1_B, GDP_P_GNN_1_WF, GDP_P_GNN_1_BF,
+  GDP_P_GNN_2_W, GDP_P_GNN_2_B, GDP_P_GNN_2_WF, GDP_P_GNN_2_BF,
+  /* three Transformer-XL layers, each: ln1.g, ln1.b (64), Wq (64x64), bq, Wk, bk, Wv, bv,
+     Wo, bo, ln2.g, ln2.b, W1 (64x256), b1 (256), W2 (256x64), b2 (64) */
+  GDP_P_COND_LN1_G, GDP_P_COND_LN1_B, GDP_P_COND_WQ, GDP_P_COND_BQ, GDP_P_COND_WK, GDP_P_COND_BK,
+  GDP_P_COND_WV, GDP_P_COND_BV, GDP_P_COND_WO, GDP_P_COND_BO, GDP_P_COND_LN2_G, GDP_P_COND_LN2_B,
+  GDP_P_COND_W1, GDP_P_COND_B1, GDP_P_COND_W2, GDP_P_COND_B2,
+  GDP_P_XL0_LN1_G, GDP_P_XL0_LN1_B, GDP_P_XL0_WQ, GDP_P_XL0_BQ, GDP_P_XL0_WK, GDP_P_XL0_BK,
+  GDP_P_XL0_WV, GDP_P_XL0_BV, GDP_P_XL0_WO, GDP_P_XL0_BO, GDP_P_XL0_LN2_G, GDP_P_XL0_LN2_B,
+  GDP_P_XL0_W1, GDP_P_XL0_B1, GDP_P_XL0_W2, GDP_P_XL0_B2,
+  GDP_P_XL1_LN1_G, GDP_P_XL1_LN1_B, GDP_P_XL1_WQ, GDP_P_XL1_BQ, GDP_P_XL1_WK, GDP_P_XL1_BK,
+  GDP_P_XL1_WV, GDP_P_XL1_BV, GDP_P_XL1_WO, GDP_P_XL1_BO, GDP_P_XL1_LN2_G, GDP_P_XL1_LN2_B,
+  GDP_P_XL1_W1, GDP_P_XL1_B1, GDP_P_XL1_W2, GDP_P_XL1_B2,
+  /* gates, per placement layer l: q, k, v, o, f1 (P 64x64, q 64), f2 (P 64x256, q 256) */
+  GDP_P_GATE0_Q_P, GDP_P_GATE0_Q_Q, GDP_P_GATE0_K_P, GDP_P_GATE0_K_Q, GDP_P_GATE0_V_P, GDP_P_GATE0_V_Q,
+  GDP_P_GATE0_O_P, GDP_P_GATE0_O_Q, GDP_P_GATE0_F1_P, GDP_P_GATE0_F1_Q, GDP_P_GATE0_F2_P, GDP_P_GATE0_F2_Q,
+  GDP_P_GATE1_Q_P, GDP_P_GATE1_Q_Q, GDP_P_GATE1_K_P, GDP_P_GATE1_K_Q, GDP_P_GATE1_V_P, GDP_P_GATE1_V_Q,
+  GDP_P_GATE1_O_P, GDP_P_GATE1_O_Q, GDP_P_GATE1_F1_P, GDP_P_GATE1_F1_Q, GDP_P_GATE1_F2_P, GDP_P_GATE1_F2_Q,
+  GDP_P_GATE_HEAD_P,    /* 64 x 64 */
+  GDP_P_GATE_HEAD_Q,    /* 64 */
+  GDP_P_HEAD_W,         /* 64 x d   per-node device logits (Fig. 1 "d") */
+  GDP_P_HEAD_B,         /* d */
+  GDP_P_COUNT           /* = 90 tensors */
+} gdp_param_id;
+
+/* ------------------------------------------------------------------ setup (untimed) */
+
+/* Fill *out with the SURVEY §8 defaults for d devices (S = 128, M = 128,
+ * superposition on).  Errors: GDP_ERR_ARG if d is not in 1..8 or out is NULL. */
+gdp_status gdp_default_config(int32_t d, gdp_config *out);
+
+/* Thread-local message describing the last non-OK status (never NULL). */
+const char *gdp_last_error(void);
+
+/* Diagnostic: total number of CUDA kernels this library has launched in this process
+ * (all threads, all devices).  bench.py reads it around the timed region. */
+uint64_t gdp_launch_count(void);
+
+/* Host-only graph check: ids in range, no self or duplicate edges,
+ * acyclic.  edges: host E x 2 int32 (producer, consumer).  topo_order (host, N,
+ * nullable) receives Kahn's order with ties broken by smallest id.
+ * Errors: GDP_ERR_ARG (N <= 0, E < 0, edges NULL with E > 0), GDP_ERR_GRAPH, GDP_ERR_CYCLE. */
+gdp_status gdp_graph_validate(int32_t N, int64_t E, const int32_t *edges, int32_t *topo_order);
+
+/* Create a graph G(V, E): N ops, F meta features per op, E
+ * data-dependency edges.  All inputs are HOST arrays and are copied:
+ *   feat          N x F float32 row-major, the initial representations h_v^(0)
+ *   edges         E x 2 int32 (producer, consumer)
+ *   compute_cost  N int64 ticks (>= 0, <= 2^31-1)
+ *   output_bytes  N int64 (>= 0)
+ *   memory_bytes  N int64 (>= 0), resident on the op's device for the whole step
+ *   coloc_group   N int32 group id or -1, nullable (no co-location constraints)
+ * The device copies (features, symmetric neighbour CSR, in/out CSR, Kahn order,
+ * group leaders) live on the current CUDA device until gdp_graph_destroy.
+ * Synchronous.  Errors: GDP_ERR_ARG, GDP_ERR_GRAPH, GDP_ERR_CYCLE, GDP_ERR_CUDA. */
+gdp_status gdp_graph_create(int32_t N, int32_t F, const float *feat, int64_t E, const int32_t *edges,
+                            const int64_t *compute_cost, const int64_t *output_bytes,
+                            const int64_t *memory_bytes, const int32_t *coloc_group, gdp_graph *out);
+gdp_status gdp_graph_destroy(gdp_graph g);
+
+/* Device topology, all HOST arrays, copied:
+ *   mem_capacity  d int64 bytes;  speed d int32 (> 0) multiplier on compute_cost;
+ *   bytes_per_tick d x d int64 (> 0 off the diagonal, symmetric; diagonal ignored);
+ *   latency d x d int32 ticks (>= 0; diagonal ignored).
+ * Errors: GDP_ERR_ARG (d not in 1..8, bad entries, asymmetric bandwidth). */
+gdp_status gdp_topo_create(int32_t d, const int64_t *mem_capacity, const int32_t *speed,
+                           const int64_t *bytes_per_tick, const int32_t *latency, gdp_topo *out);
+gdp_status gdp_topo_destroy(gdp_topo t);
+
+/* Flat-theta layout for config c and feature width F: *n_params (nullable) and
+ * offsets[GDP_P_COUNT + 1] (nullable; offsets[i] = first element of tensor i,
+ * offsets[GDP_P_COUNT] = n_params).  Errors: GDP_ERR_ARG. */
+gdp_status gdp_param_layout(const gdp_config *c, int32_t F, int64_t *offsets, int64_t *n_params);
+
+/* Bytes of workspace the hot-path calls need for graph g, config c and up to B
+ * placements per gdp_cost / gdp_policy_grad call.  Errors: GDP_ERR_ARG. */
+gdp_status gdp_workspace_size(gdp_graph g, const gdp_config *c, int32_t B, size_t *bytes);
+
+/* ------------------------------------------------------------------ hot path */
+
+/* §3.1 graph embedding (Eq. 2-3): H0 = X W_in + b_in; for l < 3:
+ * Z = sigmoid(H W_l + b_l); a_v = max_{u in N(v)} Z_u (N(v) = preds U succs, first
+ * index on ties, 0 if empty); H = tanh([H | a] W_f,l + b_f,l).
+ *   theta     dev fp32 [n_params]
+ *   node_emb  dev fp32 N x 64 (out), caller node order
+ *   ws        dev workspace; activations saved here are consumed by gdp_policy_grad
+ * Errors: GDP_ERR_ARG, GDP_ERR_WORKSPACE, GDP_ERR_CUDA. */
+gdp_status gdp_embed(gdp_graph g, const gdp_config *c, const float *theta, float *node_emb,
+                     void *ws, size_t ws_bytes, void *stream);
+
+/* §3.2-3.3 placement network on node_emb in Kahn order: conditioner layer ->
+ * z = mean over nodes -> gates gamma_j = 2 sigmoid(z P_j + q_j) (Eq. 4) -> two
+ * Transformer-XL layers (segments of S nodes attending to themselves and to the
+ * stop-gradient cached states of the previous M positions; no positional terms,
+ * P:144-148) -> logits = (gamma_head . y) W_head + b_head.
+ *   node_emb  dev fp32 N x 64 (in, as written by gdp_embed)
+ *   logits    dev fp32 N x d (out), caller node order
+ * Errors: GDP_ERR_ARG (d mismatch, S < 1, M < -1), GDP_ERR_WORKSPACE, GDP_ERR_CUDA. */
+gdp_status gdp_place(gdp_graph g, const gdp_config *c, const float *theta, const float *node_emb,
+                     float *logits, void *ws, size_t ws_bytes, void *stream);
+
+/* D ~ pi_theta(G).  For sample b (global index
+ * gidx = sample_offset + b) and node v: Philox4x32-10 with key (seed mod 2^32,
+ * seed >> 32) and counter (v >> 2, gidx mod 2^32, step mod 2^32, gidx >> 32), word
+ * v & 3, u = (word >> 8) 2^-24; D[b][v] = min{k : u < cdf_v[k]} over the fp32 softmax
+ * CDF of logits row v (fallback: last k with p > 0).  Co-location non-leaders copy
+ * the leader (lowest id in the group).  logprob[b] = sum over leaders of log p_v[D].
+ *   logits      dev fp32 N x d (in);  placements dev uint8 B x N (out, placement-major)
+ *   logprob     dev fp32 B (out)
+ * Errors: GDP_ERR_ARG (B < 1), GDP_ERR_WORKSPACE, GDP_ERR_CUDA. */
+gdp_status gdp_sample(gdp_graph g, const gdp_config *c, const float *logits, int32_t B, uint64_t seed,
+                      uint64_t sample_offset, uint64_t step, uint8_t *placements, float *logprob,
+                      void *ws, size_t ws_bytes, void *stream);
+
+/* Step-time cost model (semantics in DESIGN.md §"Cost model"):
+ * per placement, list scheduling in integer ticks -- duration = compute_cost x
+ * speed[D v]; one transfer per cross-device edge, FIFO on the directed channel
+ * (D u -> D v), ceil(bytes / bytes_per_tick) + latency; each device runs one op at a
+ * time, choosing the smallest (ready time, id); liveness memory model; co-location
+ * and capacity checks.  One CTA per placement.  reward[b] = valid ? -sqrt(makespan /
+ * 1e6) : -10.
+ *   placements dev uint8 B x N (in);  rep dev gdp_sim_report B (out)
+ *   peak_mem   dev int64 B x d (out, nullable);  busy dev int64 B x d (out, nullable)
+ *   reward     dev fp64 B (out)
+ * Errors: GDP_ERR_ARG, GDP_ERR_SHAPE (topology d != config d), GDP_ERR_OVERFLOW,
+ * GDP_ERR_WORKSPACE, GDP_ERR_CUDA.  Invalid placements are verdicts, not errors. */
+gdp_status gdp_cost(gdp_graph g, gdp_topo t, const uint8_t *placements, int32_t B, gdp_sim_report *rep,
+                    int64_t *peak_mem, int64_t *busy, double *reward, void *ws, size_t ws_bytes,
+                    void *stream);
+
+/* Advantage ("average reward of all the previous trials as a bias term"):
+ * for b = 0..B-1 in order, adv[b] = (count == 0) ? 0 : reward[b] - sum / count, then
+ * sum += reward[b], count += 1.  One state per graph.
+ *   reward dev fp64 B;  run_sum dev fp64 [1] (in/out);  run_count dev int64 [1] (in/out)
+ *   adv dev fp64 B (out).  Errors: GDP_ERR_ARG, GDP_ERR_CUDA. */
+gdp_status gdp_advantage(const double *reward, int32_t B, double *run_sum, int64_t *run_count, double *adv,
+                         void *stream);
+
+/* Policy gradient (P:93 PPO; Eq. 1 batch objective):
+ *   L = -loss_scale * sum_b min(rho_b A_b, clip(rho_b, 1-eps, 1+eps) A_b)
+ *       - entropy_coef * (1/N) sum_v H(p_v),
+ * rho_b = exp(logprob_b - old_logprob_b) (rho = 1 with the gradient of log pi when
+ * old_logprob is NULL), log pi_b = sum over co-location leaders of log p_v[D_b v].
+ * The gradient flows end to end through the placer and the GNN; cached
+ * Transformer-XL states are stop-gradient.  grad += dL/dtheta.
+ * Must follow gdp_embed and gdp_place of the same theta with the same ws.
+ *   logits dev fp32 N x d;  placements dev uint8 B x N;  adv dev fp64 B
+ *   logprob dev fp32 B (used only when old_logprob != NULL);  old_logprob dev fp32 B or NULL
+ *   grad dev fp32 [n_params] (accumulated)
+ * Errors: GDP_ERR_ARG, GDP_ERR_WORKSPACE, GDP_ERR_CUDA. */
+gdp_status gdp_policy_grad(gdp_graph g, const gdp_config *c, const float *theta, const float *logits,
+                           const uint8_t *placements, int32_t B, const double *adv, const float *logprob,
+                           const float *old_logprob, float clip_eps, float entropy_coef, float loss_scale,
+                           float *grad, void *ws, size_t ws_bytes, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GDP_H_ */

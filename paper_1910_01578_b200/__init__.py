@@ -1,0 +1,225 @@
+"""paper_1910_01578_b200 -- the B200 hot path of GDP (arXiv 1910.01578) behind a C ABI.
+
+Thin ctypes binding of libgdp.so (include/gdp.h).  Every function here only marshals
+arguments (torch tensors -> raw device pointers, the current CUDA stream); every step
+of the path runs in the CUDA kernels of csrc/.  There is no CPU fallback: importing
+works without a GPU (so the ABI can be inspected), but every compute call requires
+the built library and a CUDA device and raises otherwise.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional, Sequence
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libgdp.so")
+_lib = None
+
+GDP_OK = 0
+STATUS = {0: "GDP_OK", 1: "GDP_ERR_ARG", 2: "GDP_ERR_GRAPH", 3: "GDP_ERR_CYCLE", 4: "GDP_ERR_SHAPE",
+          5: "GDP_ERR_CUDA", 6: "GDP_ERR_OVERFLOW", 7: "GDP_ERR_NONFINITE", 8: "GDP_ERR_WORKSPACE"}
+P_COUNT = 90
+REPORT_BYTES = 24
+
+EXPORTS = ["gdp_default_config", "gdp_last_error", "gdp_launch_count", "gdp_graph_validate", "gdp_graph_create", "gdp_graph_destroy",
+           "gdp_topo_create", "gdp_topo_destroy", "gdp_param_layout", "gdp_workspace_size", "gdp_embed",
+           "gdp_place", "gdp_sample", "gdp_cost", "gdp_advantage", "gdp_policy_grad"]
+
+
+class GdpError(RuntimeError):
+    def __init__(self, status: int, where: str):
+        self.status = status
+        super().__init__(f"{where}: {STATUS.get(status, status)}: {last_error()}")
+
+
+class Config(ctypes.Structure):
+    _fields_ = [("hidden", ctypes.c_int32), ("heads", ctypes.c_int32), ("gnn_layers", ctypes.c_int32),
+                ("xl_layers", ctypes.c_int32), ("ffn", ctypes.c_int32), ("num_devices", ctypes.c_int32),
+                ("seg_len", ctypes.c_int32), ("mem_len", ctypes.c_int32), ("superposition", ctypes.c_int32)]
+
+
+def lib():
+    """Load libgdp.so (built by __graft_entry__.build()); fail loudly if it is missing."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"libgdp.so not built ({LIB_PATH}); run __graft_entry__.build()")
+        L = ctypes.CDLL(LIB_PATH)
+        P, I32, I64, U64, F32, SZ = (ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64,
+                                     ctypes.c_float, ctypes.c_size_t)
+        sig = {
+            "gdp_default_config": [I32, P],
+            "gdp_graph_validate": [I32, I64, P, P],
+            "gdp_graph_create": [I32, I32, P, I64, P, P, P, P, P, P],
+            "gdp_graph_destroy": [P],
+            "gdp_topo_create": [I32, P, P, P, P, P],
+            "gdp_topo_destroy": [P],
+            "gdp_param_layout": [P, I32, P, P],
+            "gdp_workspace_size": [P, P, I32, P],
+            "gdp_embed": [P, P, P, P, P, SZ, P],
+            "gdp_place": [P, P, P, P, P, P, SZ, P],
+            "gdp_sample": [P, P, P, I32, U64, U64, U64, P, P, P, SZ, P],
+            "gdp_cost": [P, P, P, I32, P, P, P, P, P, SZ, P],
+            "gdp_advantage": [P, I32, P, P, P, P],
+            "gdp_policy_grad": [P, P, P, P, P, I32, P, P, P, F32, F32, F32, P, P, SZ, P],
+        }
+        for name, args in sig.items():
+            fn = getattr(L, name)
+            fn.argtypes = args
+            fn.restype = ctypes.c_int
+        L.gdp_launch_count.restype = ctypes.c_uint64
+        L.gdp_launch_count.argtypes = []
+        L.gdp_last_error.restype = ctypes.c_char_p
+        L.gdp_last_error.argtypes = []
+        _lib = L
+    return _lib
+
+
+def last_error() -> str:
+    try:
+        return lib().gdp_last_error().decode()
+    except Exception:  # pragma: no cover
+        return "?"
+
+
+def launch_count() -> int:
+    """Kernels launched by libgdp.so so far in this process."""
+    return int(lib().gdp_launch_count())
+
+
+def _check(st: int, where: str):
+    if st != GDP_OK:
+        raise GdpError(st, where)
+
+
+def _np_ptr(a: Optional[np.ndarray]):
+    return None if a is None else a.ctypes.data_as(ctypes.c_void_p)
+
+
+def _t_ptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(stream=None):
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+# --------------------------------------------------------------------------- setup objects
+def default_config(d: int, seg_len: int = 128, mem_len: int = 128, superposition: bool = True) -> Config:
+    c = Config()
+    _check(lib().gdp_default_config(d, ctypes.byref(c)), "gdp_default_config")
+    c.seg_len, c.mem_len, c.superposition = seg_len, mem_len, int(bool(superposition))
+    return c
+
+
+def graph_validate(N: int, edges: np.ndarray) -> np.ndarray:
+    e = np.ascontiguousarray(edges, dtype=np.int32).reshape(-1, 2)
+    order = np.zeros(N, dtype=np.int32)
+    _check(lib().gdp_graph_validate(N, e.shape[0], _np_ptr(e), _np_ptr(order)), "gdp_graph_validate")
+    return order
+
+
+class Graph:
+    """gdp_graph handle (device copies of the graph).  `src` is any object with
+    N, edges, compute_cost, output_bytes, memory_bytes, coloc (e.g. workloads.Graph)."""
+
+    def __init__(self, src, feat: np.ndarray):
+        self.N = int(src.N)
+        X = np.ascontiguousarray(feat, dtype=np.float32)
+        self.F = int(X.shape[1])
+        e = np.ascontiguousarray(src.edges, dtype=np.int32).reshape(-1, 2)
+        self.E = int(e.shape[0])
+        cc = np.ascontiguousarray(src.compute_cost, dtype=np.int64)
+        ob = np.ascontiguousarray(src.output_bytes, dtype=np.int64)
+        mb = np.ascontiguousarray(src.memory_bytes, dtype=np.int64)
+        co = None if getattr(src, "coloc", None) is None else np.ascontiguousarray(src.coloc, dtype=np.int32)
+        h = ctypes.c_void_p()
+        _check(lib().gdp_graph_create(self.N, self.F, _np_ptr(X), self.E, _np_ptr(e), _np_ptr(cc), _np_ptr(ob),
+                                      _np_ptr(mb), _np_ptr(co), ctypes.byref(h)), "gdp_graph_create")
+        self.h = h
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.gdp_graph_destroy(self.h)
+            self.h = None
+
+
+class Topo:
+    def __init__(self, topo):
+        self.d = int(topo.d)
+        self._a = [np.ascontiguousarray(topo.mem_capacity, dtype=np.int64),
+                   np.ascontiguousarray(topo.speed, dtype=np.int32),
+                   np.ascontiguousarray(topo.bytes_per_tick, dtype=np.int64),
+                   np.ascontiguousarray(topo.latency, dtype=np.int32)]
+        h = ctypes.c_void_p()
+        _check(lib().gdp_topo_create(self.d, *[_np_ptr(a) for a in self._a], ctypes.byref(h)), "gdp_topo_create")
+        self.h = h
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.gdp_topo_destroy(self.h)
+            self.h = None
+
+
+def param_layout(cfg: Config, F: int):
+    off = np.zeros(P_COUNT + 1, dtype=np.int64)
+    n = ctypes.c_int64()
+    _check(lib().gdp_param_layout(ctypes.byref(cfg), F, _np_ptr(off), ctypes.byref(n)), "gdp_param_layout")
+    return off, int(n.value)
+
+
+def workspace_size(g: Graph, cfg: Config, B: int) -> int:
+    n = ctypes.c_size_t()
+    _check(lib().gdp_workspace_size(g.h, ctypes.byref(cfg), B, ctypes.byref(n)), "gdp_workspace_size")
+    return int(n.value)
+
+
+# --------------------------------------------------------------------------- hot path (same names as the C ABI)
+def gdp_embed(g: Graph, cfg: Config, theta, node_emb, ws, stream=None):
+    _check(lib().gdp_embed(g.h, ctypes.byref(cfg), _t_ptr(theta), _t_ptr(node_emb), _t_ptr(ws), ws.numel(),
+                           _stream(stream)), "gdp_embed")
+
+
+def gdp_place(g: Graph, cfg: Config, theta, node_emb, logits, ws, stream=None):
+    _check(lib().gdp_place(g.h, ctypes.byref(cfg), _t_ptr(theta), _t_ptr(node_emb), _t_ptr(logits), _t_ptr(ws),
+                           ws.numel(), _stream(stream)), "gdp_place")
+
+
+def gdp_sample(g: Graph, cfg: Config, logits, B: int, seed: int, sample_offset: int, step: int, placements, logprob,
+               ws, stream=None):
+    _check(lib().gdp_sample(g.h, ctypes.byref(cfg), _t_ptr(logits), B, seed, sample_offset, step,
+                            _t_ptr(placements), _t_ptr(logprob), _t_ptr(ws), ws.numel(), _stream(stream)),
+           "gdp_sample")
+
+
+def gdp_cost(g: Graph, t: Topo, placements, B: int, rep, peak_mem, busy, reward, ws, stream=None):
+    _check(lib().gdp_cost(g.h, t.h, _t_ptr(placements), B, _t_ptr(rep), _t_ptr(peak_mem), _t_ptr(busy),
+                          _t_ptr(reward), _t_ptr(ws), ws.numel(), _stream(stream)), "gdp_cost")
+
+
+def gdp_advantage(reward, B: int, run_sum, run_count, adv, stream=None):
+    _check(lib().gdp_advantage(_t_ptr(reward), B, _t_ptr(run_sum), _t_ptr(run_count), _t_ptr(adv),
+                               _stream(stream)), "gdp_advantage")
+
+
+def gdp_policy_grad(g: Graph, cfg: Config, theta, logits, placements, B: int, adv, logprob, old_logprob,
+                    clip_eps: float, entropy_coef: float, loss_scale: float, grad, ws, stream=None):
+    _check(lib().gdp_policy_grad(g.h, ctypes.byref(cfg), _t_ptr(theta), _t_ptr(logits), _t_ptr(placements), B,
+                                 _t_ptr(adv), _t_ptr(logprob), _t_ptr(old_logprob), clip_eps, entropy_coef,
+                                 loss_scale, _t_ptr(grad), _t_ptr(ws), ws.numel(), _stream(stream)),
+           "gdp_policy_grad")
+
+
+def decode_reports(rep_bytes: np.ndarray):
+    """gdp_sim_report B x 24 bytes -> dict of arrays (makespan, cross_bytes, valid, violation)."""
+    r = np.ascontiguousarray(rep_bytes, dtype=np.uint8).reshape(-1, REPORT_BYTES)
+    return dict(makespan=r[:, 0:8].copy().view(np.int64)[:, 0], cross_bytes=r[:, 8:16].copy().view(np.int64)[:, 0],
+                valid=r[:, 16].copy(), violation=r[:, 17].copy())
+
+
+from .step import PolicyStep  # noqa: E402  (marshalling helper built on the functions above)

@@ -1,0 +1,521 @@
+// C ABI of libgdp.so (include/gdp.h): validation, graph/topology objects, parameter layout,
+// workspace layout and the hot-path entry points.
+#include <algorithm>
+#include <atomic>
+#include <climits>
+#include <cstring>
+#include <functional>
+#include <queue>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+
+namespace gdp {
+
+static thread_local std::string g_err = "ok";
+static std::atomic<unsigned long long> g_launches{0};
+
+void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+void set_error(const std::string &msg) { g_err = msg; }
+
+gdp_status cuda_status(cudaError_t e, const char *what) {
+  set_error(std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e));
+  return GDP_ERR_CUDA;
+}
+
+static gdp_status fail(gdp_status s, const std::string &msg) {
+  set_error(msg);
+  return s;
+}
+
+// parameter tensor shapes in GDP_P_* order
+static void param_shapes(int F, int d, long long *sz) {
+  const long long H = kH, FF = kFFN;
+  int i = 0;
+  sz[i++] = F * H; sz[i++] = H;
+  for (int l = 0; l < kGNN; l++) { sz[i++] = H * H; sz[i++] = H; sz[i++] = 2 * H * H; sz[i++] = H; }
+  for (int l = 0; l < 3; l++) {
+    sz[i++] = H; sz[i++] = H;                       // ln1
+    for (int j = 0; j < 4; j++) { sz[i++] = H * H; sz[i++] = H; }   // q k v o
+    sz[i++] = H; sz[i++] = H;                       // ln2
+    sz[i++] = H * FF; sz[i++] = FF;                 // W1 b1
+    sz[i++] = FF * H; sz[i++] = H;                  // W2 b2
+  }
+  for (int l = 0; l < 2; l++)
+    for (int j = 0; j < 6; j++) {
+      long long w = j == 5 ? FF : H;
+      sz[i++] = H * w; sz[i++] = w;
+    }
+  sz[i++] = H * H; sz[i++] = H;                     // head gate
+  sz[i++] = H * d; sz[i++] = d;                     // head
+}
+
+void param_offsets(int F, int d, long long *off) {
+  long long sz[GDP_P_COUNT];
+  param_shapes(F, d, sz);
+  off[0] = 0;
+  for (int i = 0; i < GDP_P_COUNT; i++) off[i + 1] = off[i] + sz[i];
+}
+
+static gdp_status check_config(const gdp_config *c) {
+  if (!c) return fail(GDP_ERR_ARG, "config is NULL");
+  if (c->hidden != kH || c->heads != kHeads || c->gnn_layers != kGNN || c->xl_layers != 2 || c->ffn != kFFN)
+    return fail(GDP_ERR_ARG, "unsupported network size (need hidden 64, heads 4, gnn_layers 3, xl_layers 2, ffn 256)");
+  if (c->num_devices < 1 || c->num_devices > kMaxD) return fail(GDP_ERR_ARG, "num_devices must be in 1..8");
+  if (c->seg_len < 1) return fail(GDP_ERR_ARG, "seg_len must be >= 1");
+  if (c->mem_len < -1) return fail(GDP_ERR_ARG, "mem_len must be >= -1");
+  return GDP_OK;
+}
+
+// ------------------------------------------------------------------ workspace
+static size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
+
+bool ws_layout(const gdp_graph_s *g, int d, int B, char *base, WS *w) {
+  const size_t N = (size_t)g->N, E = (size_t)(g->E > 0 ? g->E : 1);
+  size_t off = 0;
+  auto take = [&](size_t bytes) -> char * {
+    char *p = base ? base + off : nullptr;
+    off += align_up(bytes);
+    return p;
+  };
+  auto F32 = [&](size_t n) { return reinterpret_cast<float *>(take(n * sizeof(float))); };
+  WS z{};
+  for (int i = 0; i < 4; i++) z.H[i] = F32(N * kH);
+  for (int i = 0; i < 3; i++) {
+    z.Z[i] = F32(N * kH);
+    z.A[i] = F32(N * kH);
+    z.ARG[i] = reinterpret_cast<int *>(take(N * kH * sizeof(int)));
+  }
+  z.Etopo = F32(N * kH);
+  z.zsum = F32(kH);
+  z.z = F32(kH);
+  z.gam = F32(kGamTotal);
+  z.Wh = F32(kH * kMaxD);
+  z.dWh = F32((kH + 1) * kMaxD);
+  z.logits_topo = F32(N * kMaxD);
+  for (int l = 0; l < 3; l++) {
+    Layer &L = z.L[l];
+    L.x = nullptr;
+    L.a = F32(N * kH);
+    L.mu1 = F32(N);
+    L.rs1 = F32(N);
+    L.qkv = F32(N * 192);
+    L.o = F32(N * kH);
+    L.lse = F32(N * kHeads);
+    L.x1 = F32(N * kH);
+    L.c = F32(N * kH);
+    L.mu2 = F32(N);
+    L.rs2 = F32(N);
+    L.m = F32(N * kFFN);
+    L.y = F32(N * kH);
+    L.Wqkv = F32(64 * 192);
+    L.bqkv = F32(192);
+    L.Wo = F32(64 * 64);
+    L.W1 = F32(64 * 256);
+    L.W2 = F32(256 * 64);
+    L.dWqkv = F32(65 * 192);
+    L.dWo = F32(65 * 64);
+    L.dW1 = F32(65 * 256);
+    L.dW2 = F32(257 * 64);
+  }
+  z.dlog = F32(N * kMaxD);
+  z.dlog_topo = F32(N * kMaxD);
+  z.dy = F32(N * kH);
+  z.dx1 = F32(N * kH);
+  z.dm = F32(N * kFFN);
+  z.dc = F32(N * kH);
+  z.dout = F32(N * kH);
+  z.dqkv = F32(N * 192);
+  z.dkvm = F32(N * 128);
+  z.dkvt = F32(N * 192);
+  z.da = F32(N * kH);
+  z.dam = F32(N * kH);
+  z.dxa = F32(N * kH);
+  z.dEt = F32(N * kH);
+  z.dE = F32(N * kH);
+  z.dH = F32(N * kH);
+  z.dHn = F32(N * kH);
+  z.dAg = F32(N * kH);
+  z.dP = F32(N * kH);
+  z.dd = F32(N * kHeads);
+  const size_t chunks = (N + 255) / 256 + 1;
+  z.part_floats = chunks * 257 * 256;
+  z.part = F32(z.part_floats);
+  z.dgam = F32(kGamTotal);
+  z.dz = F32(kH);
+  z.dzp = F32(kH * kGateCount);
+  z.cdf = F32(N * kMaxD);
+  z.logp = F32(N * kMaxD);
+  z.lastpos = reinterpret_cast<int *>(take(N * sizeof(int)));
+  const size_t Bc = (size_t)std::max(B, 1);
+  // everything below depends on B (kept last so the offsets above never move)
+  z.wb = reinterpret_cast<double *>(take(Bc * sizeof(double)));
+  z.c_rem = reinterpret_cast<int *>(take(Bc * N * sizeof(int)));
+  z.c_rcons = reinterpret_cast<int *>(take(Bc * N * sizeof(int)));
+  z.c_new = reinterpret_cast<int *>(take(Bc * 2 * N * sizeof(int)));
+  z.c_fifo = reinterpret_cast<int2 *>(take(Bc * N * sizeof(int2)));
+  z.c_chq = reinterpret_cast<int4 *>(take(Bc * E * sizeof(int4)));
+  z.bytes = off;
+  (void)d;
+  *w = z;
+  return true;
+}
+
+}  // namespace gdp
+
+using namespace gdp;
+
+// per-call workspace check: ws must hold the layout for (graph, B)
+static gdp_status carve(const gdp_graph_s *g, int d, int B, void *ws, size_t ws_bytes, WS *w) {
+  WS probe;
+  ws_layout(g, d, B, nullptr, &probe);
+  if (!ws) return fail(GDP_ERR_ARG, "workspace is NULL");
+  if (ws_bytes < probe.bytes)
+    return fail(GDP_ERR_WORKSPACE, "workspace too small: need " + std::to_string(probe.bytes) + " bytes, got " +
+                                       std::to_string(ws_bytes));
+  ws_layout(g, d, B, static_cast<char *>(ws), w);
+  return GDP_OK;
+}
+
+
+namespace gdp {
+gdp_status run_embed(const gdp_graph_s *g, const float *theta, float *node_emb, const WS &w, int d, cudaStream_t s);
+gdp_status run_place(const gdp_graph_s *g, const gdp_config *c, const float *theta, const float *node_emb,
+                     float *logits, const WS &w, cudaStream_t s);
+gdp_status run_policy_grad(const gdp_graph_s *g, const gdp_config *c, const float *theta, const float *logits,
+                           const uint8_t *D, int B, const double *adv, const float *logprob,
+                           const float *old_logprob, float eps, float beta, float scale, float *grad, const WS &w,
+                           cudaStream_t s);
+}  // namespace gdp
+
+extern "C" {
+
+const char *gdp_last_error(void) { return g_err.c_str(); }
+
+uint64_t gdp_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
+
+gdp_status gdp_default_config(int32_t d, gdp_config *out) {
+  if (!out) return fail(GDP_ERR_ARG, "out is NULL");
+  if (d < 1 || d > kMaxD) return fail(GDP_ERR_ARG, "d must be in 1..8");
+  out->hidden = kH;
+  out->heads = kHeads;
+  out->gnn_layers = kGNN;
+  out->xl_layers = 2;
+  out->ffn = kFFN;
+  out->num_devices = d;
+  out->seg_len = 128;
+  out->mem_len = 128;
+  out->superposition = 1;
+  return GDP_OK;
+}
+
+gdp_status gdp_graph_validate(int32_t N, int64_t E, const int32_t *edges, int32_t *topo_order) {
+  if (N <= 0) return fail(GDP_ERR_ARG, "N must be > 0");
+  if (E < 0) return fail(GDP_ERR_ARG, "E must be >= 0");
+  if (E > 0 && !edges) return fail(GDP_ERR_ARG, "edges is NULL");
+  if (E >= INT_MAX) return fail(GDP_ERR_ARG, "too many edges");
+  std::vector<std::pair<int, int>> es((size_t)E);
+  for (int64_t e = 0; e < E; e++) {
+    int u = edges[2 * e], v = edges[2 * e + 1];
+    if (u < 0 || u >= N || v < 0 || v >= N)
+      return fail(GDP_ERR_GRAPH, "edge " + std::to_string(e) + " has an endpoint out of range");
+    if (u == v) return fail(GDP_ERR_GRAPH, "self edge at node " + std::to_string(u));
+    es[(size_t)e] = {u, v};
+  }
+  std::sort(es.begin(), es.end());
+  for (size_t i = 1; i < es.size(); i++)
+    if (es[i] == es[i - 1])
+      return fail(GDP_ERR_GRAPH, "duplicate edge " + std::to_string(es[i].first) + "->" + std::to_string(es[i].second));
+  std::vector<int> indeg(N, 0), ptr(N + 1, 0);
+  for (auto &p : es) { indeg[p.second]++; ptr[p.first + 1]++; }
+  for (int v = 0; v < N; v++) ptr[v + 1] += ptr[v];
+  std::priority_queue<int, std::vector<int>, std::greater<int>> q;
+  for (int v = 0; v < N; v++)
+    if (!indeg[v]) q.push(v);
+  int n = 0;
+  while (!q.empty()) {
+    int u = q.top();
+    q.pop();
+    if (topo_order) topo_order[n] = u;
+    n++;
+    for (int e = ptr[u]; e < ptr[u + 1]; e++)
+      if (--indeg[es[e].second] == 0) q.push(es[e].second);
+  }
+  if (n != N) return fail(GDP_ERR_CYCLE, "the edge list has a cycle");
+  return GDP_OK;
+}
+
+gdp_status gdp_graph_create(int32_t N, int32_t F, const float *feat, int64_t E, const int32_t *edges,
+                            const int64_t *compute_cost, const int64_t *output_bytes, const int64_t *memory_bytes,
+                            const int32_t *coloc_group, gdp_graph *out) {
+  if (!out) return fail(GDP_ERR_ARG, "out is NULL");
+  *out = nullptr;
+  if (N <= 0 || F <= 0) return fail(GDP_ERR_ARG, "N and F must be > 0");
+  if (!feat || !compute_cost || !output_bytes || !memory_bytes) return fail(GDP_ERR_ARG, "NULL input array");
+  for (int v = 0; v < N; v++) {
+    if (compute_cost[v] < 0 || compute_cost[v] > INT_MAX)
+      return fail(GDP_ERR_GRAPH, "compute_cost out of range at node " + std::to_string(v));
+    if (output_bytes[v] < 0 || memory_bytes[v] < 0)
+      return fail(GDP_ERR_GRAPH, "negative bytes at node " + std::to_string(v));
+  }
+  std::vector<int> order(N);
+  gdp_status st = gdp_graph_validate(N, E, edges, order.data());
+  if (st != GDP_OK) return st;
+  auto *g = new gdp_graph_s();
+  g->N = N;
+  g->F = F;
+  g->E = E;
+  GDP_CUDA_CHECK(cudaGetDevice(&g->device));
+  // out / in CSR
+  std::vector<std::pair<int, int>> es((size_t)E);
+  for (int64_t e = 0; e < E; e++) es[(size_t)e] = {edges[2 * e], edges[2 * e + 1]};
+  std::sort(es.begin(), es.end());
+  std::vector<int> optr(N + 1, 0), iptr(N + 1, 0), oidx((size_t)E), osrc((size_t)E), iidx((size_t)E);
+  for (auto &p : es) { optr[p.first + 1]++; iptr[p.second + 1]++; }
+  for (int v = 0; v < N; v++) { optr[v + 1] += optr[v]; iptr[v + 1] += iptr[v]; }
+  {
+    std::vector<int> fi(iptr.begin(), iptr.end() - 1);
+    for (size_t e = 0; e < es.size(); e++) {
+      oidx[e] = es[e].second;
+      osrc[e] = es[e].first;
+      iidx[fi[es[e].second]++] = es[e].first;   // producers ascending (es sorted by producer)
+    }
+  }
+  // symmetric neighbourhood N(v) = preds U succs, ascending, unique
+  std::vector<std::pair<int, int>> sym;
+  sym.reserve(2 * (size_t)E);
+  for (auto &p : es) { sym.push_back({p.first, p.second}); sym.push_back({p.second, p.first}); }
+  std::sort(sym.begin(), sym.end());
+  sym.erase(std::unique(sym.begin(), sym.end()), sym.end());
+  std::vector<int> nptr(N + 1, 0), nidx(sym.size());
+  for (size_t i = 0; i < sym.size(); i++) { nptr[sym[i].first + 1]++; nidx[i] = sym[i].second; }
+  for (int v = 0; v < N; v++) nptr[v + 1] += nptr[v];
+  g->E_sym = (int64_t)sym.size();
+  // leaders (lowest id of each co-location group)
+  std::vector<int> leader(N);
+  for (int v = 0; v < N; v++) leader[v] = v;
+  if (coloc_group) {
+    std::vector<std::pair<int, int>> first;
+    std::vector<int> gid_first;
+    // map group id -> first member via sorting (ids may be sparse)
+    std::vector<std::pair<int, int>> gm;
+    for (int v = 0; v < N; v++)
+      if (coloc_group[v] >= 0) gm.push_back({coloc_group[v], v});
+    std::sort(gm.begin(), gm.end());
+    for (size_t i = 0; i < gm.size(); i++) {
+      size_t j = i;
+      while (j + 1 < gm.size() && gm[j + 1].first == gm[i].first) j++;
+      for (size_t k = i; k <= j; k++) leader[gm[k].second] = gm[i].second;
+      if (j > i) g->has_coloc = true;
+      i = j;
+    }
+  }
+  std::vector<int> cost(N);
+  long long sum_cost = 0, sum_edge_out = 0;
+  for (int v = 0; v < N; v++) { cost[v] = (int)compute_cost[v]; sum_cost += compute_cost[v]; }
+  for (auto &p : es) sum_edge_out += output_bytes[p.first];
+  g->sum_cost = sum_cost;
+  g->sum_edge_out_bytes = sum_edge_out;
+  bool ident = true;
+  for (int i = 0; i < N; i++)
+    if (order[i] != i) ident = false;
+  g->perm_identity = ident;
+  for (int v = 0; v < N; v++) {
+    g->max_indeg = std::max(g->max_indeg, iptr[v + 1] - iptr[v]);
+    g->max_outdeg = std::max(g->max_outdeg, optr[v + 1] - optr[v]);
+  }
+  auto up = [&](void **dst, const void *src, size_t bytes) -> cudaError_t {
+    cudaError_t e = cudaMalloc(dst, bytes ? bytes : 4);
+    if (e != cudaSuccess) return e;
+    if (bytes) return cudaMemcpy(*dst, src, bytes, cudaMemcpyHostToDevice);
+    return cudaSuccess;
+  };
+#define UP(field, src, bytes)                                                   \
+  do {                                                                          \
+    cudaError_t _e = up(reinterpret_cast<void **>(&g->field), (src), (bytes));  \
+    if (_e != cudaSuccess) { gdp_graph_destroy(g); return cuda_status(_e, "graph upload"); } \
+  } while (0)
+  UP(X, feat, (size_t)N * F * sizeof(float));
+  UP(nbr_ptr, nptr.data(), (N + 1) * sizeof(int));
+  UP(nbr_idx, nidx.data(), nidx.size() * sizeof(int));
+  UP(out_ptr, optr.data(), (N + 1) * sizeof(int));
+  UP(out_idx, oidx.data(), oidx.size() * sizeof(int));
+  UP(out_src, osrc.data(), osrc.size() * sizeof(int));
+  UP(in_ptr, iptr.data(), (N + 1) * sizeof(int));
+  UP(in_idx, iidx.data(), iidx.size() * sizeof(int));
+  UP(cost, cost.data(), N * sizeof(int));
+  UP(out_bytes, output_bytes, N * sizeof(long long));
+  UP(mem_bytes, memory_bytes, N * sizeof(long long));
+  UP(perm, order.data(), N * sizeof(int));
+  UP(leader, leader.data(), N * sizeof(int));
+#undef UP
+  *out = g;
+  return GDP_OK;
+}
+
+gdp_status gdp_graph_destroy(gdp_graph g) {
+  if (!g) return GDP_OK;
+  void *ptrs[] = {g->X, g->nbr_ptr, g->nbr_idx, g->out_ptr, g->out_idx, g->out_src, g->in_ptr, g->in_idx,
+                  g->cost, g->out_bytes, g->mem_bytes, g->perm, g->leader};
+  for (void *p : ptrs)
+    if (p) cudaFree(p);
+  delete g;
+  return GDP_OK;
+}
+
+gdp_status gdp_topo_create(int32_t d, const int64_t *mem_capacity, const int32_t *speed,
+                           const int64_t *bytes_per_tick, const int32_t *latency, gdp_topo *out) {
+  if (!out) return fail(GDP_ERR_ARG, "out is NULL");
+  *out = nullptr;
+  if (d < 1 || d > kMaxD) return fail(GDP_ERR_ARG, "d must be in 1..8");
+  if (!mem_capacity || !speed || !bytes_per_tick || !latency) return fail(GDP_ERR_ARG, "NULL topology array");
+  auto *t = new gdp_topo_s();
+  t->d = d;
+  for (int i = 0; i < 8; i++) { t->cap[i] = 0; t->speed[i] = 1; }
+  for (int i = 0; i < 64; i++) { t->bpt[i] = 1; t->lat[i] = 0; }
+  for (int k = 0; k < d; k++) {
+    if (speed[k] <= 0) { delete t; return fail(GDP_ERR_ARG, "speed must be > 0"); }
+    if (mem_capacity[k] < 0) { delete t; return fail(GDP_ERR_ARG, "mem_capacity must be >= 0"); }
+    t->cap[k] = mem_capacity[k];
+    t->speed[k] = speed[k];
+  }
+  for (int s = 0; s < d; s++)
+    for (int u = 0; u < d; u++) {
+      if (s == u) continue;
+      long long bw = bytes_per_tick[s * d + u];
+      int la = latency[s * d + u];
+      if (bw <= 0 || la < 0) { delete t; return fail(GDP_ERR_ARG, "bandwidth must be > 0 and latency >= 0 off the diagonal"); }
+      if (bw != bytes_per_tick[u * d + s]) { delete t; return fail(GDP_ERR_ARG, "bandwidth must be symmetric"); }
+      t->bpt[s * 8 + u] = bw;
+      t->lat[s * 8 + u] = la;
+    }
+  *out = t;
+  return GDP_OK;
+}
+
+gdp_status gdp_topo_destroy(gdp_topo t) {
+  delete t;
+  return GDP_OK;
+}
+
+gdp_status gdp_param_layout(const gdp_config *c, int32_t F, int64_t *offsets, int64_t *n_params) {
+  gdp_status st = check_config(c);
+  if (st != GDP_OK) return st;
+  if (F <= 0) return fail(GDP_ERR_ARG, "F must be > 0");
+  long long off[GDP_P_COUNT + 1];
+  param_offsets(F, c->num_devices, off);
+  if (offsets)
+    for (int i = 0; i <= GDP_P_COUNT; i++) offsets[i] = off[i];
+  if (n_params) *n_params = off[GDP_P_COUNT];
+  return GDP_OK;
+}
+
+gdp_status gdp_workspace_size(gdp_graph g, const gdp_config *c, int32_t B, size_t *bytes) {
+  if (!g || !bytes) return fail(GDP_ERR_ARG, "NULL argument");
+  gdp_status st = check_config(c);
+  if (st != GDP_OK) return st;
+  if (B < 1) return fail(GDP_ERR_ARG, "B must be >= 1");
+  WS w;
+  ws_layout(g, c->num_devices, B, nullptr, &w);
+  *bytes = w.bytes;
+  return GDP_OK;
+}
+
+// Offsets of everything embed/place save for policy_grad do not depend on B (the B-sized
+// scratch is carved last), so each call carves for the B it is given.
+static gdp_status carve_any(const gdp_graph_s *g, int d, int Bneed, void *ws, size_t ws_bytes, WS *w) {
+  return carve(g, d, Bneed, ws, ws_bytes, w);
+}
+
+gdp_status gdp_embed(gdp_graph g, const gdp_config *c, const float *theta, float *node_emb, void *ws,
+                     size_t ws_bytes, void *stream) {
+  if (!g || !theta || !node_emb) return fail(GDP_ERR_ARG, "NULL argument");
+  gdp_status st = check_config(c);
+  if (st != GDP_OK) return st;
+  WS w;
+  st = carve_any(g, c->num_devices, 1, ws, ws_bytes, &w);
+  if (st != GDP_OK) return st;
+  return run_embed(g, theta, node_emb, w, c->num_devices, static_cast<cudaStream_t>(stream));
+}
+
+gdp_status gdp_place(gdp_graph g, const gdp_config *c, const float *theta, const float *node_emb, float *logits,
+                     void *ws, size_t ws_bytes, void *stream) {
+  if (!g || !theta || !node_emb || !logits) return fail(GDP_ERR_ARG, "NULL argument");
+  gdp_status st = check_config(c);
+  if (st != GDP_OK) return st;
+  WS w;
+  st = carve_any(g, c->num_devices, 1, ws, ws_bytes, &w);
+  if (st != GDP_OK) return st;
+  return run_place(g, c, theta, node_emb, logits, w, static_cast<cudaStream_t>(stream));
+}
+
+gdp_status gdp_sample(gdp_graph g, const gdp_config *c, const float *logits, int32_t B, uint64_t seed,
+                      uint64_t sample_offset, uint64_t step, uint8_t *placements, float *logprob, void *ws,
+                      size_t ws_bytes, void *stream) {
+  if (!g || !logits || !placements || !logprob) return fail(GDP_ERR_ARG, "NULL argument");
+  gdp_status st = check_config(c);
+  if (st != GDP_OK) return st;
+  if (B < 1) return fail(GDP_ERR_ARG, "B must be >= 1");
+  WS w;
+  st = carve_any(g, c->num_devices, 1, ws, ws_bytes, &w);
+  if (st != GDP_OK) return st;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  launch_sample(logits, g->leader, g->has_coloc, g->N, c->num_devices, B, seed, sample_offset, step, w.cdf,
+                w.logp, w.lastpos, placements, logprob, s);
+  GDP_LAUNCH_CHECK("gdp_sample");
+  return GDP_OK;
+}
+
+gdp_status gdp_cost(gdp_graph g, gdp_topo t, const uint8_t *placements, int32_t B, gdp_sim_report *rep,
+                    int64_t *peak_mem, int64_t *busy, double *reward, void *ws, size_t ws_bytes, void *stream) {
+  if (!g || !t || !placements || !rep || !reward) return fail(GDP_ERR_ARG, "NULL argument");
+  if (B < 1) return fail(GDP_ERR_ARG, "B must be >= 1");
+  // int32 device time: the schedule never exceeds sum(durations) + sum(transfers)
+  long long maxspeed = 1, minbw = LLONG_MAX, maxlat = 0;
+  for (int k = 0; k < t->d; k++) maxspeed = std::max<long long>(maxspeed, t->speed[k]);
+  for (int s = 0; s < t->d; s++)
+    for (int u = 0; u < t->d; u++)
+      if (s != u) {
+        minbw = std::min(minbw, t->bpt[s * 8 + u]);
+        maxlat = std::max<long long>(maxlat, t->lat[s * 8 + u]);
+      }
+  double bound = (double)g->sum_cost * (double)maxspeed;
+  if (t->d > 1) bound += (double)g->sum_edge_out_bytes / (double)minbw + (double)g->E * (double)(maxlat + 1);
+  if (bound >= 2147483000.0)
+    return fail(GDP_ERR_OVERFLOW, "sum of durations and transfers may exceed 2^31 ticks");
+  WS w;
+  gdp_status st = carve_any(g, t->d, B, ws, ws_bytes, &w);
+  if (st != GDP_OK) return st;
+  return launch_cost(g, t, placements, B, rep, reinterpret_cast<long long *>(peak_mem),
+                     reinterpret_cast<long long *>(busy), reward, w, static_cast<cudaStream_t>(stream));
+}
+
+gdp_status gdp_advantage(const double *reward, int32_t B, double *run_sum, int64_t *run_count, double *adv,
+                         void *stream) {
+  if (!reward || !run_sum || !run_count || !adv) return fail(GDP_ERR_ARG, "NULL argument");
+  if (B < 1) return fail(GDP_ERR_ARG, "B must be >= 1");
+  launch_advantage(reward, B, run_sum, reinterpret_cast<long long *>(run_count), adv,
+                   static_cast<cudaStream_t>(stream));
+  GDP_LAUNCH_CHECK("gdp_advantage");
+  return GDP_OK;
+}
+
+gdp_status gdp_policy_grad(gdp_graph g, const gdp_config *c, const float *theta, const float *logits,
+                           const uint8_t *placements, int32_t B, const double *adv, const float *logprob,
+                           const float *old_logprob, float clip_eps, float entropy_coef, float loss_scale,
+                           float *grad, void *ws, size_t ws_bytes, void *stream) {
+  if (!g || !theta || !logits || !placements || !adv || !grad) return fail(GDP_ERR_ARG, "NULL argument");
+  if (old_logprob && !logprob) return fail(GDP_ERR_ARG, "logprob is required with old_logprob");
+  gdp_status st = check_config(c);
+  if (st != GDP_OK) return st;
+  if (B < 1) return fail(GDP_ERR_ARG, "B must be >= 1");
+  WS w;
+  st = carve_any(g, c->num_devices, B, ws, ws_bytes, &w);
+  if (st != GDP_OK) return st;
+  return run_policy_grad(g, c, theta, logits, placements, B, adv, logprob, old_logprob, clip_eps, entropy_coef,
+                         loss_scale, grad, w, static_cast<cudaStream_t>(stream));
+}
+
+}  // extern "C"

@@ -1,0 +1,181 @@
+// Internal declarations of libgdp.so (the product).  Shares nothing with oracle/.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "../../include/gdp.h"
+
+namespace gdp {
+
+constexpr int kH = 64;       // hidden size h
+constexpr int kHeads = 4;
+constexpr int kDH = 16;      // head dim
+constexpr int kFFN = 256;
+constexpr int kGNN = 3;
+constexpr int kMaxD = 8;
+constexpr float kLnEps = 1e-5f;
+
+void set_error(const std::string &msg);
+void note_launch();   // counts kernel launches (gdp_launch_count)
+gdp_status cuda_status(cudaError_t e, const char *what);
+
+#define GDP_CUDA_CHECK(expr)                                      \
+  do {                                                            \
+    cudaError_t _e = (expr);                                      \
+    if (_e != cudaSuccess) return gdp::cuda_status(_e, #expr);    \
+  } while (0)
+
+#define GDP_LAUNCH_CHECK(what)                                    \
+  do {                                                            \
+    cudaError_t _e = cudaGetLastError();                          \
+    if (_e != cudaSuccess) return gdp::cuda_status(_e, what);     \
+  } while (0)
+
+}  // namespace gdp
+
+// ------------------------------------------------------------------ graph / topology
+struct gdp_graph_s {
+  int N = 0, F = 0;
+  int64_t E = 0, E_sym = 0;
+  int device = 0;
+  // device arrays (caller node ids)
+  float *X = nullptr;                               // N x F
+  int *nbr_ptr = nullptr, *nbr_idx = nullptr;       // symmetric neighbour CSR (N+1, E_sym)
+  int *out_ptr = nullptr, *out_idx = nullptr, *out_src = nullptr;  // out CSR, consumers ascending
+  int *in_ptr = nullptr, *in_idx = nullptr;         // in CSR, producers ascending
+  int *cost = nullptr;                              // int32 compute cost
+  long long *out_bytes = nullptr, *mem_bytes = nullptr;
+  int *perm = nullptr;                              // Kahn order: perm[i] = node at position i
+  int *leader = nullptr;                            // co-location leader (self if none)
+  bool perm_identity = true, has_coloc = false;
+  // host aggregates (overflow check)
+  long long sum_cost = 0;
+  long long sum_edge_out_bytes = 0;                 // sum over edges of producer output bytes
+  long long n_edges_cross_max = 0;
+  int max_indeg = 0, max_outdeg = 0;
+};
+
+struct gdp_topo_s {
+  int d = 0;
+  long long cap[8];
+  int speed[8];
+  long long bpt[64];
+  int lat[64];
+};
+
+// Topology passed by value to kernels
+struct TopoArgs {
+  int d;
+  long long cap[8];
+  int speed[8];
+  long long bpt[64];
+  int lat[64];
+};
+
+namespace gdp {
+
+// ------------------------------------------------------------------ workspace layout
+struct Layer {       // saved activations of one Transformer-XL layer (topological row order)
+  float *x, *a, *mu1, *rs1, *qkv, *o, *lse, *x1, *c, *mu2, *rs2, *m, *y;
+  // folded (gated) weights
+  float *Wqkv, *bqkv, *Wo, *W1, *W2;
+  // dW' (augmented with the bias row) for the gate backward
+  float *dWqkv, *dWo, *dW1, *dW2;
+};
+
+struct WS {
+  // embed
+  float *H[4], *Z[3], *A[3];
+  int *ARG[3];
+  // place
+  float *Etopo, *zsum, *z, *gam, *Wh, *dWh, *logits_topo;
+  Layer L[3];  // 0 = conditioner, 1 = xl0, 2 = xl1
+  // grad scratch
+  double *wb;
+  float *dlog, *dlog_topo, *dy, *dx1, *dm, *dc, *dout, *dqkv, *dkvm, *dkvt, *da, *dam, *dxa, *dEt, *dE;
+  float *dH, *dHn, *dAg, *dP, *dd;
+  float *part;           // wgrad / column-sum partials
+  float *dgam, *dz, *dzp;
+  size_t part_floats;
+  // sample
+  float *cdf, *logp;
+  int *lastpos;
+  // cost scratch
+  int *c_rem, *c_rcons, *c_new;
+  int2 *c_fifo;
+  int4 *c_chq;
+  size_t bytes;
+};
+
+bool ws_layout(const gdp_graph_s *g, int d, int B, char *base, WS *w);
+
+// Gated dense maps per placement layer, in theta order: q, k, v, o, f1, f2; then head.
+constexpr int kGateCount = 13;
+constexpr int kGamTotal = 2 * (5 * kH + kFFN) + kH;   // 1216
+
+// ------------------------------------------------------------------ kernels (launchers)
+enum Epi { EPI_NONE = 0, EPI_SIGMOID = 1, EPI_TANH = 2, EPI_RELU = 3, EPI_MASK = 4 };
+
+struct GemmArgs {
+  int M, K, Nout;
+  const float *X1; int ldx1; int K1;        // operand columns [0, K1)
+  const float *X2; int ldx2;                // operand columns [K1, K) (nullable)
+  const float *W; int ldw_k, ldw_n;         // W(k, n) = W[k * ldw_k + n * ldw_n]
+  const float *bias;                        // Nout (nullable)
+  const float *R; int ldr;                  // residual added after the activation (nullable)
+  const float *aux; int ldaux;              // EPI_MASK: multiply by (aux > 0)
+  float *Y; int ldy; int split;             // columns < split -> Y
+  float *Y2; int ldy2;                      // columns >= split -> Y2 (col - split)
+  int accumulate;                           // Y = Y + result
+  int epi;
+};
+void launch_gemm(const GemmArgs &a, cudaStream_t s);
+
+// dW_aug[(K + with_bias) x Nout] = [X, 1]^T dY over all M rows, deterministic split-K over rows.
+// Result: out (+)= sum (accumulate flag).  part must hold chunks * (K+1) * Nout floats.
+void launch_wgrad(int M, int K, int Nout, const float *X1, int ldx1, int K1, const float *X2, int ldx2,
+                  const float *dY, int ldy, bool with_bias, float *part, size_t part_floats, float *out,
+                  bool accumulate, cudaStream_t s);
+
+void launch_layernorm(const float *x, const float *g, const float *b, float *y, float *mu, float *rs, int N,
+                      cudaStream_t s);
+// dx (+)= LN backward of da; param grads from (da + da_extra) accumulated into dgb[0..63] (gain) and
+// dgb[64..127] (bias).
+void launch_layernorm_bwd(const float *x, const float *mu, const float *rs, const float *g, const float *da,
+                          const float *da_extra, float *dx, bool dx_accumulate, float *dgb, float *part,
+                          int N, cudaStream_t s);
+void launch_colsum(const float *x, int N, int C, float scale, float *out, float *part, cudaStream_t s);
+
+void launch_gather_max(const float *Z, const int *ptr, const int *idx, float *A, int *ARG, int N, cudaStream_t s);
+void launch_gather_max_bwd(const float *dA, const int *ARG, const float *Z, const int *ptr, const int *idx,
+                           float *dPre, int N, cudaStream_t s);
+
+void launch_attn_fwd(const float *qkv, float *o, float *lse, int N, int S, int M, cudaStream_t s);
+void launch_attn_bwd(const float *qkv, const float *o, const float *lse, const float *dout, float *dqkv,
+                     float *dkvm, float *Dd, int N, int S, int M, cudaStream_t s);
+
+void launch_rows_gather(const float *src, const int *perm, float *dst, int N, int C, cudaStream_t s);
+void launch_rows_scatter(const float *src, const int *perm, float *dst, int N, int C, bool accumulate,
+                         cudaStream_t s);
+void launch_tanh_grad(const float *dHn, const float *Hn, float *dP, int n, cudaStream_t s);
+void launch_add(const float *a, int lda, const float *b, int ldb, float *c, int ldc, int rows, int cols,
+                cudaStream_t s);
+void launch_fill_rows(float *dst, const float *row, float scale, int N, int C, cudaStream_t s);
+
+// sampling / loss
+void launch_sample(const float *logits, const int *leader, bool has_coloc, int N, int d, int B, uint64_t seed,
+                   uint64_t offset, uint64_t step, float *cdf, float *logp, int *lastpos, uint8_t *D,
+                   float *logprob, cudaStream_t s);
+void launch_logit_grad(const float *logits, const uint8_t *D, const int *leader, const double *adv,
+                       const float *logprob, const float *old_logprob, float eps, float beta, float scale,
+                       int N, int d, int B, double *wb, float *dlog, cudaStream_t s);
+
+// cost model
+gdp_status launch_cost(const gdp_graph_s *g, const gdp_topo_s *t, const uint8_t *D, int B,
+                       gdp_sim_report *rep, long long *peak, long long *busy, double *reward, const WS &w,
+                       cudaStream_t s);
+void launch_advantage(const double *r, int B, double *sum, long long *cnt, double *adv, cudaStream_t s);
+
+}  // namespace gdp

@@ -1,0 +1,298 @@
+// Graph aggregation (§3.1 Eq. 2) and segment-recurrent attention
+// (§3.2).
+//
+//  * k_gather_max:      warp per node, lanes own 2 of the 64 channels; neighbour rows
+//                       (256 B, coalesced) are streamed in ascending id, strict '>' keeps
+//                       the first (lowest-id) maximiser.  Empty N(v) -> 0.
+//  * k_gather_max_bwd:  the max-pool backward as a GATHER over the symmetric CSR:
+//                       dZ_u[c] = sum_{v in N(u), argmax_v[c] = u} dA_v[c] (no atomics,
+//                       fixed order), fused with the sigmoid derivative Z(1-Z).
+//  * attention:         one CTA per (segment, head); queries of segment tau attend to
+//                       keys [max(0, tau S - M), min((tau+1) S, N)) with an online softmax;
+//                       the backward splits dK/dV into the own-segment part (flows into x)
+//                       and the memory part (stop-gradient: parameters only).
+#include "common.cuh"
+
+namespace gdp {
+namespace {
+
+__global__ void k_gather_max(const float *__restrict__ Z, const int *__restrict__ ptr,
+                             const int *__restrict__ idx, float *A, int *ARG, int N) {
+  int v = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (v >= N) return;
+  int b = ptr[v], e = ptr[v + 1];
+  float m0 = 0.f, m1 = 0.f;
+  int a0 = -1, a1 = -1;
+  if (b < e) {
+    int u = idx[b];
+    m0 = Z[(size_t)u * kH + lane];
+    m1 = Z[(size_t)u * kH + lane + 32];
+    a0 = a1 = u;
+    for (int j = b + 1; j < e; j++) {
+      u = idx[j];
+      float z0 = Z[(size_t)u * kH + lane], z1 = Z[(size_t)u * kH + lane + 32];
+      if (z0 > m0) { m0 = z0; a0 = u; }
+      if (z1 > m1) { m1 = z1; a1 = u; }
+    }
+  }
+  A[(size_t)v * kH + lane] = m0;
+  A[(size_t)v * kH + lane + 32] = m1;
+  ARG[(size_t)v * kH + lane] = a0;
+  ARG[(size_t)v * kH + lane + 32] = a1;
+}
+
+__global__ void k_gather_max_bwd(const float *__restrict__ dA, const int *__restrict__ ARG,
+                                 const float *__restrict__ Z, const int *__restrict__ ptr,
+                                 const int *__restrict__ idx, float *dPre, int N) {
+  int u = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (u >= N) return;
+  float s0 = 0.f, s1 = 0.f;
+  for (int j = ptr[u]; j < ptr[u + 1]; j++) {
+    int v = idx[j];
+    size_t o = (size_t)v * kH;
+    if (ARG[o + lane] == u) s0 += dA[o + lane];
+    if (ARG[o + lane + 32] == u) s1 += dA[o + lane + 32];
+  }
+  size_t o = (size_t)u * kH;
+  float z0 = Z[o + lane], z1 = Z[o + lane + 32];
+  dPre[o + lane] = s0 * z0 * (1.f - z0);
+  dPre[o + lane + 32] = s1 * z1 * (1.f - z1);
+}
+
+constexpr int AQ = 128;  // queries (or keys) per thread block pass
+constexpr int AK = 64;   // keys (or queries) per shared-memory tile
+constexpr float kScale = 0.25f;   // 1 / sqrt(16)
+
+__device__ __forceinline__ void key_range(int tau, int N, int S, int M, int *lo, int *hi) {
+  long long q0 = (long long)tau * S;
+  *lo = (M < 0) ? 0 : (int)max(0LL, q0 - M);
+  *hi = (int)min((long long)N, q0 + S);
+}
+
+// qkv: N x 192 [Q | K | V], head h uses columns h*16 .. h*16+15 of each block.
+__global__ void __launch_bounds__(AQ) k_attn_fwd(const float *__restrict__ qkv, float *o, float *lse, int N,
+                                                 int S, int M) {
+  __shared__ float Ks[AK][kDH + 1], Vs[AK][kDH + 1];
+  const int tau = blockIdx.x, hd = blockIdx.y;
+  int lo, hi;
+  key_range(tau, N, S, M, &lo, &hi);
+  const int q0 = tau * S, q1 = min(N, q0 + S);
+  for (int qb = q0; qb < q1; qb += AQ) {
+    const int i = qb + threadIdx.x;
+    const bool valid = i < q1;
+    float q[kDH], acc[kDH];
+    float mx = -INFINITY, l = 0.f;
+#pragma unroll
+    for (int c = 0; c < kDH; c++) {
+      q[c] = valid ? qkv[(size_t)i * 192 + hd * kDH + c] : 0.f;
+      acc[c] = 0.f;
+    }
+    for (int kb = lo; kb < hi; kb += AK) {
+      __syncthreads();
+      for (int e = threadIdx.x; e < AK * kDH; e += AQ) {
+        int j = e / kDH, c = e % kDH;
+        int r = kb + j;
+        Ks[j][c] = r < hi ? qkv[(size_t)r * 192 + 64 + hd * kDH + c] : 0.f;
+        Vs[j][c] = r < hi ? qkv[(size_t)r * 192 + 128 + hd * kDH + c] : 0.f;
+      }
+      __syncthreads();
+      const int nk = min(AK, hi - kb);
+      for (int j = 0; j < nk; j++) {
+        float s = 0.f;
+#pragma unroll
+        for (int c = 0; c < kDH; c++) s = fmaf(q[c], Ks[j][c], s);
+        s *= kScale;
+        if (s > mx) {
+          float f = expf(mx - s);
+          l *= f;
+#pragma unroll
+          for (int c = 0; c < kDH; c++) acc[c] *= f;
+          mx = s;
+        }
+        float p = expf(s - mx);
+        l += p;
+#pragma unroll
+        for (int c = 0; c < kDH; c++) acc[c] = fmaf(p, Vs[j][c], acc[c]);
+      }
+    }
+    if (valid) {
+      float inv = 1.f / l;
+#pragma unroll
+      for (int c = 0; c < kDH; c++) o[(size_t)i * kH + hd * kDH + c] = acc[c] * inv;
+      lse[(size_t)i * kHeads + hd] = mx + logf(l);
+    }
+  }
+}
+
+// Dd[i][h] = sum_c dO[i][h*16+c] * O[i][h*16+c]
+__global__ void k_attn_bwd_prep(const float *o, const float *dout, float *Dd, int N) {
+  int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= N * kHeads) return;
+  int i = e / kHeads, h = e % kHeads;
+  float s = 0.f;
+  for (int c = 0; c < kDH; c++) s = fmaf(dout[(size_t)i * kH + h * kDH + c], o[(size_t)i * kH + h * kDH + c], s);
+  Dd[e] = s;
+}
+
+// dQ (query-major): dqkv[:, 0:64]
+__global__ void __launch_bounds__(AQ) k_attn_bwd_dq(const float *__restrict__ qkv, const float *__restrict__ lse,
+                                                    const float *__restrict__ dout, const float *__restrict__ Dd,
+                                                    float *dqkv, int N, int S, int M) {
+  __shared__ float Ks[AK][kDH + 1], Vs[AK][kDH + 1];
+  const int tau = blockIdx.x, hd = blockIdx.y;
+  int lo, hi;
+  key_range(tau, N, S, M, &lo, &hi);
+  const int q0 = tau * S, q1 = min(N, q0 + S);
+  for (int qb = q0; qb < q1; qb += AQ) {
+    const int i = qb + threadIdx.x;
+    const bool valid = i < q1;
+    float q[kDH], dq[kDH], dob[kDH];
+    float L = valid ? lse[(size_t)i * kHeads + hd] : 0.f;
+    float D = valid ? Dd[(size_t)i * kHeads + hd] : 0.f;
+#pragma unroll
+    for (int c = 0; c < kDH; c++) {
+      q[c] = valid ? qkv[(size_t)i * 192 + hd * kDH + c] : 0.f;
+      dob[c] = valid ? dout[(size_t)i * kH + hd * kDH + c] : 0.f;
+      dq[c] = 0.f;
+    }
+    for (int kb = lo; kb < hi; kb += AK) {
+      __syncthreads();
+      for (int e = threadIdx.x; e < AK * kDH; e += AQ) {
+        int j = e / kDH, c = e % kDH;
+        int r = kb + j;
+        Ks[j][c] = r < hi ? qkv[(size_t)r * 192 + 64 + hd * kDH + c] : 0.f;
+        Vs[j][c] = r < hi ? qkv[(size_t)r * 192 + 128 + hd * kDH + c] : 0.f;
+      }
+      __syncthreads();
+      const int nk = min(AK, hi - kb);
+      for (int j = 0; j < nk; j++) {
+        float s = 0.f, dp = 0.f;
+#pragma unroll
+        for (int c = 0; c < kDH; c++) {
+          s = fmaf(q[c], Ks[j][c], s);
+          dp = fmaf(dob[c], Vs[j][c], dp);
+        }
+        float p = expf(s * kScale - L);
+        float ds = p * (dp - D) * kScale;
+#pragma unroll
+        for (int c = 0; c < kDH; c++) dq[c] = fmaf(ds, Ks[j][c], dq[c]);
+      }
+    }
+    if (valid) {
+#pragma unroll
+      for (int c = 0; c < kDH; c++) dqkv[(size_t)i * 192 + hd * kDH + c] = dq[c];
+    }
+  }
+}
+
+__device__ __forceinline__ void dkv_accum(int ni, const float (*Qs)[kDH + 1], const float (*dOs)[kDH + 1],
+                                          const float *Ls, const float *Ds, const float *k, const float *v,
+                                          float *DK, float *DV) {
+  for (int r = 0; r < ni; r++) {
+    float s = 0.f, dp = 0.f;
+#pragma unroll
+    for (int c = 0; c < kDH; c++) {
+      s = fmaf(Qs[r][c], k[c], s);
+      dp = fmaf(dOs[r][c], v[c], dp);
+    }
+    float p = expf(s * kScale - Ls[r]);
+    float ds = p * (dp - Ds[r]) * kScale;
+#pragma unroll
+    for (int c = 0; c < kDH; c++) {
+      DV[c] = fmaf(p, dOs[r][c], DV[c]);
+      DK[c] = fmaf(ds, Qs[r][c], DK[c]);
+    }
+  }
+}
+
+// dK, dV (key-major).  Keys of segment sigma are attended by query segments tau >= sigma
+// whose range starts at or before them.  tau == sigma -> own part (dqkv[:, 64:192]);
+// tau > sigma -> memory part (dkvm[:, 0:128]), which is stop-gradient for x.
+__global__ void __launch_bounds__(AQ) k_attn_bwd_dkv(const float *__restrict__ qkv, const float *__restrict__ lse,
+                                                     const float *__restrict__ dout, const float *__restrict__ Dd,
+                                                     float *dqkv, float *dkvm, int N, int S, int M, int nseg) {
+  __shared__ float Qs[AK][kDH + 1], dOs[AK][kDH + 1], Ls[AK], Ds[AK];
+  const int sig = blockIdx.x, hd = blockIdx.y;
+  const int j0 = sig * S, j1 = min(N, j0 + S);
+  int tau_hi = nseg - 1;
+  if (M >= 0) tau_hi = min(nseg - 1, (int)(((long long)j1 - 1 + M) / S));
+  for (int jb = j0; jb < j1; jb += AQ) {
+    const int j = jb + threadIdx.x;
+    const bool valid = j < j1;
+    float k[kDH], v[kDH], dk[kDH], dv[kDH], dkm[kDH], dvm[kDH];
+#pragma unroll
+    for (int c = 0; c < kDH; c++) {
+      k[c] = valid ? qkv[(size_t)j * 192 + 64 + hd * kDH + c] : 0.f;
+      v[c] = valid ? qkv[(size_t)j * 192 + 128 + hd * kDH + c] : 0.f;
+      dk[c] = dv[c] = dkm[c] = dvm[c] = 0.f;
+    }
+    for (int tau = sig; tau <= tau_hi; tau++) {
+      int lo, hi;
+      key_range(tau, N, S, M, &lo, &hi);
+      const bool inr = valid && j >= lo;
+      const int q0 = tau * S, q1 = min(N, q0 + S);
+      for (int ib = q0; ib < q1; ib += AK) {
+        __syncthreads();
+        for (int e = threadIdx.x; e < AK * kDH; e += AQ) {
+          int r = e / kDH, c = e % kDH;
+          int i = ib + r;
+          Qs[r][c] = i < q1 ? qkv[(size_t)i * 192 + hd * kDH + c] : 0.f;
+          dOs[r][c] = i < q1 ? dout[(size_t)i * kH + hd * kDH + c] : 0.f;
+        }
+        for (int r = threadIdx.x; r < AK; r += AQ) {
+          int i = ib + r;
+          Ls[r] = i < q1 ? lse[(size_t)i * kHeads + hd] : 0.f;
+          Ds[r] = i < q1 ? Dd[(size_t)i * kHeads + hd] : 0.f;
+        }
+        __syncthreads();
+        if (!inr) continue;
+        const int ni = min(AK, q1 - ib);
+        if (tau == sig) dkv_accum(ni, Qs, dOs, Ls, Ds, k, v, dk, dv);
+        else dkv_accum(ni, Qs, dOs, Ls, Ds, k, v, dkm, dvm);
+      }
+    }
+    if (valid) {
+#pragma unroll
+      for (int c = 0; c < kDH; c++) {
+        dqkv[(size_t)j * 192 + 64 + hd * kDH + c] = dk[c];
+        dqkv[(size_t)j * 192 + 128 + hd * kDH + c] = dv[c];
+        dkvm[(size_t)j * 128 + hd * kDH + c] = dkm[c];
+        dkvm[(size_t)j * 128 + 64 + hd * kDH + c] = dvm[c];
+      }
+    }
+  }
+}
+
+}  // namespace
+
+void launch_gather_max(const float *Z, const int *ptr, const int *idx, float *A, int *ARG, int N, cudaStream_t s) {
+  unsigned blocks = (unsigned)(((size_t)N * 32 + 255) / 256);
+  note_launch();
+  k_gather_max<<<blocks, 256, 0, s>>>(Z, ptr, idx, A, ARG, N);
+}
+
+void launch_gather_max_bwd(const float *dA, const int *ARG, const float *Z, const int *ptr, const int *idx,
+                           float *dPre, int N, cudaStream_t s) {
+  unsigned blocks = (unsigned)(((size_t)N * 32 + 255) / 256);
+  note_launch();
+  k_gather_max_bwd<<<blocks, 256, 0, s>>>(dA, ARG, Z, ptr, idx, dPre, N);
+}
+
+void launch_attn_fwd(const float *qkv, float *o, float *lse, int N, int S, int M, cudaStream_t s) {
+  int nseg = (N + S - 1) / S;
+  note_launch();
+  k_attn_fwd<<<dim3(nseg, kHeads), AQ, 0, s>>>(qkv, o, lse, N, S, M);
+}
+
+void launch_attn_bwd(const float *qkv, const float *o, const float *lse, const float *dout, float *dqkv,
+                     float *dkvm, float *Dd, int N, int S, int M, cudaStream_t s) {
+  int nseg = (N + S - 1) / S;
+  note_launch();
+  k_attn_bwd_prep<<<(N * kHeads + 255) / 256, 256, 0, s>>>(o, dout, Dd, N);
+  note_launch();
+  k_attn_bwd_dq<<<dim3(nseg, kHeads), AQ, 0, s>>>(qkv, lse, dout, Dd, dqkv, N, S, M);
+  note_launch();
+  k_attn_bwd_dkv<<<dim3(nseg, kHeads), AQ, 0, s>>>(qkv, lse, dout, Dd, dqkv, dkvm, N, S, M, nseg);
+}
+
+}  // namespace gdp

@@ -1,0 +1,108 @@
+"""One batched GDP policy step over one or more graphs (marshalling only).
+
+Buffers are torch CUDA tensors; every arithmetic step runs in libgdp.so kernels.
+torch.distributed (NCCL) supplies the exchange steps of the data-parallel path, as laid
+out by sharding.plan:
+  * mode 'samples': an all-gather of the rewards (global trial order for the advantage,
+    P:177) and one all-reduce of the flat fp32 gradient;
+  * mode 'graphs': one all-reduce of the gradient.
+"""
+from __future__ import annotations
+
+from typing import Dict, List, Optional
+
+import numpy as np
+
+from . import (Config, Graph, Topo, default_config, gdp_advantage, gdp_cost, gdp_embed, gdp_place,
+               gdp_policy_grad, gdp_sample, param_layout, workspace_size, REPORT_BYTES, decode_reports)
+from .sharding import plan as make_plan
+
+
+class _GraphState:
+    def __init__(self, gsrc, feat, topo_src, cfg: Config, B_local: int, B_total: int, device):
+        import torch
+        self.g = Graph(gsrc, feat)
+        self.t = Topo(topo_src)
+        self.cfg = cfg
+        self.N, self.F = self.g.N, self.g.F
+        self.B, self.B_total = B_local, B_total
+        d = cfg.num_devices
+        self.ws = torch.empty(workspace_size(self.g, cfg, B_local), dtype=torch.uint8, device=device)
+        self.node_emb = torch.empty(self.N, 64, dtype=torch.float32, device=device)
+        self.logits = torch.empty(self.N, d, dtype=torch.float32, device=device)
+        self.placements = torch.empty(B_local, self.N, dtype=torch.uint8, device=device)
+        self.logprob = torch.empty(B_local, dtype=torch.float32, device=device)
+        self.rep = torch.empty(B_local, REPORT_BYTES, dtype=torch.uint8, device=device)
+        self.peak = torch.empty(B_local, d, dtype=torch.int64, device=device)
+        self.busy = torch.empty(B_local, d, dtype=torch.int64, device=device)
+        self.reward = torch.empty(B_local, dtype=torch.float64, device=device)
+        self.reward_all = torch.empty(B_total, dtype=torch.float64, device=device)
+        self.adv_all = torch.empty(B_total, dtype=torch.float64, device=device)
+        self.run_sum = torch.zeros(1, dtype=torch.float64, device=device)
+        self.run_count = torch.zeros(1, dtype=torch.int64, device=device)
+
+    def reports(self) -> Dict[str, np.ndarray]:
+        r = decode_reports(self.rep.cpu().numpy())
+        r["reward"] = self.reward.cpu().numpy()
+        r["peak"] = self.peak.cpu().numpy()
+        return r
+
+
+class PolicyStep:
+    """graphs: list of (workloads.Graph-like, features N x F, workloads.Topology-like)."""
+
+    def __init__(self, graphs: List, d: int, seg_len: int, mem_len: int, superposition: bool, batch: int,
+                 seed: int = 42, clip_eps: float = 0.2, entropy_coef: float = 0.01, mode: str = "samples",
+                 rank: int = 0, world: int = 1, device=None):
+        import torch
+        self.torch = torch
+        self.device = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.cfg = default_config(d, seg_len, mem_len, superposition)
+        self.plan = make_plan(mode, rank, world, batch, len(graphs), entropy_coef,
+                              [g[0].N * batch for g in graphs])
+        self.seed, self.clip_eps = seed, clip_eps
+        self.B_local, self.B_total = self.plan.B_local, self.plan.B_total
+        self.states = [_GraphState(graphs[i][0], graphs[i][1], graphs[i][2], self.cfg, self.B_local,
+                                   self.B_total, self.device) for i in self.plan.graphs]
+        F = graphs[0][1].shape[1]
+        self.offsets, self.n_params = param_layout(self.cfg, F)
+        self.grad = torch.zeros(self.n_params, dtype=torch.float32, device=self.device)
+        self.step_idx = 0
+        self.events: Dict[str, list] = {}
+
+    def _ev(self, name: str, timed: bool):
+        if timed:
+            e = self.torch.cuda.Event(enable_timing=True)
+            e.record()
+            self.events.setdefault(name, []).append(e)
+
+    def run(self, theta, timed: bool = False):
+        """embed -> place -> sample -> cost -> [all-gather rewards] -> advantage -> grad
+        -> [all-reduce]; leaves the summed gradient in self.grad (asynchronous)."""
+        torch, P = self.torch, self.plan
+        step = self.step_idx
+        self.grad.zero_()
+        for st in self.states:
+            self._ev("embed0", timed)
+            gdp_embed(st.g, self.cfg, theta, st.node_emb, st.ws)
+            self._ev("place0", timed)
+            gdp_place(st.g, self.cfg, theta, st.node_emb, st.logits, st.ws)
+            self._ev("sample0", timed)
+            gdp_sample(st.g, self.cfg, st.logits, st.B, self.seed, P.sample_offset, step, st.placements,
+                       st.logprob, st.ws)
+            self._ev("cost0", timed)
+            gdp_cost(st.g, st.t, st.placements, st.B, st.rep, st.peak, st.busy, st.reward, st.ws)
+            self._ev("cost1", timed)
+            if P.mode == "samples" and P.world > 1:
+                torch.distributed.all_gather_into_tensor(st.reward_all, st.reward)
+            else:
+                st.reward_all.copy_(st.reward)
+            gdp_advantage(st.reward_all, st.B_total, st.run_sum, st.run_count, st.adv_all)
+            adv = st.adv_all[P.sample_offset:P.sample_offset + st.B]
+            self._ev("grad0", timed)
+            gdp_policy_grad(st.g, self.cfg, theta, st.logits, st.placements, st.B, adv, st.logprob, None,
+                            self.clip_eps, P.entropy_coef, P.loss_scale, self.grad, st.ws)
+            self._ev("grad1", timed)
+        if P.world > 1:
+            torch.distributed.all_reduce(self.grad)
+        self.step_idx += 1

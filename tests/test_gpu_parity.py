@@ -1,0 +1,290 @@
+"""GPU parity: every C-ABI stage against the oracle on the same seeded inputs.
+
+Tolerances (BASELINE.json north_star; DESIGN.md §"Parity"):
+  * integers (placements, makespans, validity, peaks, busy, cross bytes) bit-exact;
+    sampled placements excused only where the oracle's CDF margin |u - c_k| < 1e-5;
+  * reward / advantage bit-exact (IEEE divide + sqrt, no contraction);
+  * fp32 tensors: |x - r| <= 1e-4 * max(|r|, 1e-2 * max|r|) elementwise.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from oracle import sampling as Osa
+from oracle import simulate as Osim
+import workloads
+from tests.helpers import graph as mkgraph, topo as mktopo
+
+pytestmark = pytest.mark.gpu
+
+RTOL = 1e-4
+
+
+def close(x, r, rtol=RTOL, floor=1e-2):
+    x = np.asarray(x, dtype=np.float64)
+    r = np.asarray(r, dtype=np.float64)
+    scale = np.maximum(np.abs(r), floor * max(np.abs(r).max(), 1e-30))
+    bad = np.abs(x - r) > rtol * scale
+    return (not bad.any()), float((np.abs(x - r) / scale).max()), int(bad.sum())
+
+
+@pytest.fixture(scope="module")
+def gdp():
+    import __graft_entry__
+    __graft_entry__.build()
+    import paper_1910_01578_b200 as m
+    assert torch.cuda.is_available()
+    return m
+
+
+def cost_gpu(gdp, g, t, D):
+    G = gdp.Graph(g, workloads.features(g))
+    T = gdp.Topo(t)
+    B = D.shape[0]
+    cfg = gdp.default_config(t.d)
+    ws = torch.empty(gdp.workspace_size(G, cfg, B), dtype=torch.uint8, device="cuda")
+    Dd = torch.from_numpy(np.ascontiguousarray(D, dtype=np.uint8)).cuda()
+    rep = torch.empty(B, 24, dtype=torch.uint8, device="cuda")
+    peak = torch.empty(B, t.d, dtype=torch.int64, device="cuda")
+    busy = torch.empty(B, t.d, dtype=torch.int64, device="cuda")
+    rew = torch.empty(B, dtype=torch.float64, device="cuda")
+    gdp.gdp_cost(G, T, Dd, B, rep, peak, busy, rew, ws)
+    torch.cuda.synchronize()
+    r = gdp.decode_reports(rep.cpu().numpy())
+    r.update(peak=peak.cpu().numpy(), busy=busy.cpu().numpy(), reward=rew.cpu().numpy())
+    return r
+
+
+def assert_cost_equal(g, t, D, r):
+    o = Osim.simulate_batch(g, t, D)
+    for k in ("makespan", "cross_bytes", "valid", "violation", "peak", "busy", "reward"):
+        a, b = np.asarray(r[k]), np.asarray(o[k])
+        if k in ("valid", "violation"):
+            a, b = a.astype(np.int64), b.astype(np.int64)
+        bad = np.nonzero(~np.all((a == b).reshape(len(D), -1), axis=1))[0]
+        assert bad.size == 0, (k, bad[:5], a[bad[:3]], b[bad[:3]])
+
+
+# ------------------------------------------------------------------ cost model (bit-exact)
+@pytest.mark.parametrize("seed", range(6))
+def test_cost_random_dags(gdp, seed):
+    rng = np.random.default_rng(seed)
+    n = int(rng.integers(1, 300))
+    g = workloads.random_dag(n, p_edge=float(rng.uniform(0.05, 0.5)), max_back=int(rng.integers(1, 40)),
+                             seed=seed, cost_max=int(rng.integers(1, 50)))
+    if seed % 2:
+        g.compute_cost[rng.random(n) < 0.2] = 0            # zero-duration ops
+        g.output_bytes[rng.random(n) < 0.3] = 0            # zero-byte transfers
+    d = [1, 2, 3, 8, 5, 4][seed]
+    t = mktopo(d, bw=int(rng.integers(1, 2000)), lat=int(rng.integers(0, 3)) if seed % 2 else 2,
+               cap=int(rng.integers(500, 5000)))
+    D = rng.integers(0, d, size=(64, n)).astype(np.uint8)
+    assert_cost_equal(g, t, D, cost_gpu(gdp, g, t, D))
+
+
+def test_cost_pins_on_gpu(gdp):
+    # SPEC S:283 diamond and the P11 reading pins, now through the C ABI
+    g = mkgraph(4, [(0, 1), (0, 2), (1, 3), (2, 3)], [1, 1, 1, 1], out=[2, 2, 2, 2])
+    r = cost_gpu(gdp, g, mktopo(2, bw=1, lat=0), np.array([[0, 0, 1, 0]], dtype=np.uint8))
+    assert r["makespan"][0] == 7
+    g = mkgraph(6, [(2, 3), (1, 4), (4, 5)], [5, 2, 1, 1, 1, 1])
+    r = cost_gpu(gdp, g, mktopo(2, bw=1, lat=0), np.array([[0, 1, 1, 0, 0, 1]], dtype=np.uint8))
+    assert r["makespan"][0] == 7
+    g = mkgraph(3, [(0, 1), (0, 2)], [1, 1, 1], out=[2, 0, 0])
+    r = cost_gpu(gdp, g, mktopo(2, bw=1), np.array([[0, 1, 1]], dtype=np.uint8))
+    assert r["makespan"][0] == 6
+
+
+def test_cost_colocation_and_malformed(gdp):
+    g = workloads.with_colocation(workloads.multibranch(blocks=10, seed=3))
+    t = workloads.topology(g, 4)
+    rng = np.random.default_rng(1)
+    D = rng.integers(0, 4, size=(16, g.N)).astype(np.uint8)
+    lead = oracle.model.leaders(g.N, g.coloc)
+    D[:8] = D[:8][:, lead]                      # half respect the groups
+    D[15, 7] = 9                                # malformed entry
+    assert_cost_equal(g, t, D, cost_gpu(gdp, g, t, D))
+
+
+@pytest.mark.parametrize("cfg", ["c1", "c2", "c3"])
+def test_cost_workloads(gdp, cfg):
+    W = workloads.config(cfg)
+    rng = np.random.default_rng(5)
+    for g in W.graphs:
+        t = workloads.topology(g, W.d)
+        D = rng.integers(0, W.d, size=(8, g.N)).astype(np.uint8)
+        D[0] = 0                                # single device: OOM for d >= 2
+        assert_cost_equal(g, t, D, cost_gpu(gdp, g, t, D))
+
+
+def test_cost_full_size_c4(gdp):
+    W = workloads.config("c4")
+    g = W.graphs[0]
+    t = workloads.topology(g, W.d)
+    rng = np.random.default_rng(9)
+    D = rng.integers(0, W.d, size=(6, g.N)).astype(np.uint8)
+    D[1] = 0
+    D[2] = (np.arange(g.N) * W.d // g.N).astype(np.uint8)     # contiguous blocks
+    assert_cost_equal(g, t, D, cost_gpu(gdp, g, t, D))
+
+
+# ------------------------------------------------------------------ policy network stages
+def run_step(gdp, g, W_d, S, M, sup, B, th, seed=42, step=0, old=None, eps=0.2, beta=0.01, scale=None):
+    X = workloads.features(g)
+    G = gdp.Graph(g, X)
+    cfg = gdp.default_config(W_d, S, M, sup)
+    ws = torch.empty(gdp.workspace_size(G, cfg, B), dtype=torch.uint8, device="cuda")
+    theta = torch.from_numpy(th).cuda()
+    emb = torch.empty(g.N, 64, device="cuda")
+    logits = torch.empty(g.N, W_d, device="cuda")
+    gdp.gdp_embed(G, cfg, theta, emb, ws)
+    gdp.gdp_place(G, cfg, theta, emb, logits, ws)
+    Dd = torch.empty(B, g.N, dtype=torch.uint8, device="cuda")
+    lp = torch.empty(B, dtype=torch.float32, device="cuda")
+    gdp.gdp_sample(G, cfg, logits, B, seed, 0, step, Dd, lp, ws)
+    torch.cuda.synchronize()
+    adv = np.random.default_rng(3).normal(size=B)
+    advd = torch.from_numpy(adv).cuda()
+    _, n = gdp.param_layout(cfg, X.shape[1])
+    grad = torch.zeros(n, device="cuda")
+    oldd = None if old is None else torch.from_numpy(np.asarray(old, dtype=np.float32)).cuda()
+    gdp.gdp_policy_grad(G, cfg, theta, logits, Dd, B, advd, lp, oldd, eps, beta,
+                        scale if scale is not None else 1.0 / B, grad, ws)
+    torch.cuda.synchronize()
+    return dict(X=X, emb=emb.cpu().numpy(), logits=logits.cpu().numpy(), D=Dd.cpu().numpy(),
+                logprob=lp.cpu().numpy(), adv=adv, grad=grad.cpu().numpy())
+
+
+CASES = {
+    "c1": (lambda: workloads.config("c1").graphs[0], 2, 32, 32, True),
+    "ragged_perm_coloc": (lambda: _perm_coloc_graph(), 3, 16, 16, True),
+    "mem_inf": (lambda: workloads.random_dag(300, p_edge=0.1, max_back=30, seed=4), 4, 64, -1, True),
+    "no_superposition": (lambda: workloads.random_dag(200, p_edge=0.15, max_back=20, seed=5), 8, 48, 48, False),
+    "short_memory": (lambda: workloads.random_dag(333, p_edge=0.1, max_back=50, seed=6), 5, 40, 17, True),
+}
+
+
+def _perm_coloc_graph():
+    g = workloads.random_dag(257, p_edge=0.12, max_back=25, seed=2)
+    perm = np.random.default_rng(0).permutation(g.N)
+    inv = np.argsort(perm)
+    g2 = workloads.Graph(name="perm", N=g.N, edges=perm[g.edges].astype(np.int32),
+                         op_type=[g.op_type[i] for i in inv], compute_cost=g.compute_cost[inv],
+                         output_bytes=g.output_bytes[inv], memory_bytes=g.memory_bytes[inv])
+    g2.coloc = np.full(g.N, -1, dtype=np.int32)
+    g2.coloc[[3, 40, 41]] = 0
+    g2.coloc[[10, 200]] = 1
+    return g2
+
+
+@pytest.mark.parametrize("case", sorted(CASES))
+def test_policy_stages(gdp, case):
+    mk, d, S, M, sup = CASES[case]
+    g = mk()
+    th = workloads.init_theta(workloads.F, d, seed=11, mode="random")
+    B = 24
+    r = run_step(gdp, g, d, S, M, sup, B, th)
+    pg = oracle.prepare(g, r["X"])
+    # embed (a1-a4)
+    E = oracle.embed(pg, th, d)
+    ok, err, nbad = close(r["emb"], E)
+    assert ok, ("embed", err, nbad)
+    # place (a5-a10), stage-wise: oracle consumes the GPU embedding
+    z = oracle.place(pg, th, r["emb"], d, S, M, sup)
+    ok, err, nbad = close(r["logits"], z)
+    assert ok, ("place", err, nbad)
+    # sample (a11): shared Philox uniforms, excused only at CDF margins < 1e-5
+    U = Osa.uniforms(g.N, B, 42, 0, 0)
+    D, _, margin = Osa.sample(r["logits"], U, pg.lead)
+    mism = (D != r["D"]) & (margin >= 1e-5)
+    assert not mism.any(), ("sample", np.argwhere(mism)[:5])
+    zl = r["logits"].astype(np.float64)
+    lpv = zl - zl.max(1, keepdims=True)
+    lpv = lpv - np.log(np.exp(lpv).sum(1, keepdims=True))
+    isl = pg.lead == np.arange(g.N)
+    want_lp = (lpv[np.arange(g.N)[None, :], r["D"].astype(np.int64)] * isl[None, :]).sum(1)
+    ok, err, _ = close(r["logprob"], want_lp)
+    assert ok, ("logprob", err)
+    # policy gradient (a14-a15): oracle on the GPU's placements / advantages, chained from theta
+    grad, _ = oracle.policy_grad(pg, th, d, S, M, sup, r["D"], r["adv"], loss_scale=1.0 / B, entropy_coef=0.01)
+    ok, err, nbad = close(r["grad"], grad)
+    assert ok, ("grad", err, nbad)
+
+
+def test_ppo_ratio_branch(gdp):
+    g = workloads.random_dag(150, p_edge=0.15, max_back=20, seed=8)
+    d, S, M = 3, 32, 32
+    th = workloads.init_theta(workloads.F, d, seed=12, mode="random")
+    B = 16
+    r0 = run_step(gdp, g, d, S, M, True, B, th)
+    old = r0["logprob"].astype(np.float64) + np.random.default_rng(1).uniform(-0.5, 0.5, B)
+    r = run_step(gdp, g, d, S, M, True, B, th, old=old.astype(np.float32))
+    pg = oracle.prepare(g, r["X"])
+    grad, _ = oracle.policy_grad(pg, th, d, S, M, True, r["D"], r["adv"],
+                                 old_logprob=old.astype(np.float32).astype(np.float64) +
+                                 (_oracle_logpi(pg, th, d, S, M, r["D"]) - r["logprob"].astype(np.float64)),
+                                 loss_scale=1.0 / B, entropy_coef=0.01)
+    ok, err, nbad = close(r["grad"], grad, rtol=5e-4)
+    assert ok, ("ppo grad", err, nbad)
+
+
+def _oracle_logpi(pg, th, d, S, M, D):
+    z = oracle.place(pg, th, oracle.embed(pg, th, d), d, S, M, True)
+    lp = np.log(Osa.softmax64(z))
+    isl = pg.lead == np.arange(pg.N)
+    return (lp[np.arange(pg.N)[None, :], D.astype(np.int64)] * isl[None, :]).sum(1)
+
+
+def test_advantage_bit_exact(gdp):
+    rng = np.random.default_rng(0)
+    r = -np.sqrt(rng.uniform(0.1, 1.0, 100))
+    r[7] = -10.0
+    rs = torch.zeros(1, dtype=torch.float64, device="cuda")
+    rc = torch.zeros(1, dtype=torch.int64, device="cuda")
+    out = []
+    s, c = 0.0, 0
+    for chunk in (r[:40], r[40:]):
+        adv = torch.empty(len(chunk), dtype=torch.float64, device="cuda")
+        gdp.gdp_advantage(torch.from_numpy(chunk).cuda(), len(chunk), rs, rc, adv)
+        A, s, c = Osa.advantage(chunk, s, c)
+        out.append((adv.cpu().numpy(), A))
+    for a, b in out:
+        assert np.array_equal(a, b)
+    assert rc.item() == 100 and rs.item() == s
+
+
+def test_step_determinism(gdp):
+    g = workloads.config("c1").graphs[0]
+    th = workloads.init_theta(workloads.F, 2, seed=3, mode="random")
+    a = run_step(gdp, g, 2, 32, 32, True, 16, th)
+    b = run_step(gdp, g, 2, 32, 32, True, 16, th)
+    for k in ("emb", "logits", "D", "logprob", "grad"):
+        assert np.array_equal(a[k], b[k]), k
+
+
+@pytest.mark.slow
+def test_full_size_c4_chain(gdp):
+    """BASELINE configs[3] at full size in the bench's launch configuration (B = 8 of the
+    headline 256 for the oracle's sake): embed, place, sampled placements, costs, gradient."""
+    W = workloads.config("c4")
+    g = W.graphs[0]
+    th = workloads.init_theta(workloads.F, W.d, seed=7, mode="default")
+    th[:] += np.random.default_rng(0).uniform(-1e-2, 1e-2, th.size).astype(np.float32)
+    B = 8
+    r = run_step(gdp, g, W.d, W.seg_len, W.mem_len, True, B, th)
+    pg = oracle.prepare(g, r["X"])
+    E = oracle.embed(pg, th, W.d)
+    ok, err, nbad = close(r["emb"], E)
+    assert ok, ("embed", err, nbad)
+    z = oracle.place(pg, th, r["emb"], W.d, W.seg_len, W.mem_len, True)
+    ok, err, nbad = close(r["logits"], z)
+    assert ok, ("place", err, nbad)
+    U = Osa.uniforms(g.N, B, 42, 0, 0)
+    D, _, margin = Osa.sample(r["logits"], U, pg.lead)
+    assert not ((D != r["D"]) & (margin >= 1e-5)).any()
+    t = workloads.topology(g, W.d)
+    assert_cost_equal(g, t, r["D"], cost_gpu(gdp, g, t, r["D"]))
+    grad, _ = oracle.policy_grad(pg, th, W.d, W.seg_len, W.mem_len, True, r["D"], r["adv"], loss_scale=1.0 / B)
+    ok, err, nbad = close(r["grad"], grad, rtol=1e-3)
+    assert ok, ("grad", err, nbad)
