@@ -126,6 +126,9 @@ const char *gdp_last_error(void);
  * (all threads, all devices).  bench.py reads it around the timed region. */
 uint64_t gdp_launch_count(void);
 
+/* Diagnostic: build identification string of this library (never NULL). */
+const char *gdp_build_info(void);
+
 /* Host-only graph check: ids in range, no self or duplicate edges,
  * acyclic.  edges: host E x 2 int32 (producer, consumer).  topo_order (host, N,
  * nullable) receives Kahn's order with ties broken by smallest id.

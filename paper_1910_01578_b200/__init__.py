@@ -24,7 +24,7 @@ STATUS = {0: "GDP_OK", 1: "GDP_ERR_ARG", 2: "GDP_ERR_GRAPH", 3: "GDP_ERR_CYCLE",
 P_COUNT = 90
 REPORT_BYTES = 24
 
-EXPORTS = ["gdp_default_config", "gdp_last_error", "gdp_launch_count", "gdp_graph_validate", "gdp_graph_create", "gdp_graph_destroy",
+EXPORTS = ["gdp_default_config", "gdp_last_error", "gdp_launch_count", "gdp_build_info", "gdp_graph_validate", "gdp_graph_create", "gdp_graph_destroy",
            "gdp_topo_create", "gdp_topo_destroy", "gdp_param_layout", "gdp_workspace_size", "gdp_embed",
            "gdp_place", "gdp_sample", "gdp_cost", "gdp_advantage", "gdp_policy_grad"]
 
@@ -72,6 +72,8 @@ def lib():
             fn.restype = ctypes.c_int
         L.gdp_launch_count.restype = ctypes.c_uint64
         L.gdp_launch_count.argtypes = []
+        L.gdp_build_info.restype = ctypes.c_char_p
+        L.gdp_build_info.argtypes = []
         L.gdp_last_error.restype = ctypes.c_char_p
         L.gdp_last_error.argtypes = []
         _lib = L
@@ -83,6 +85,10 @@ def last_error() -> str:
         return lib().gdp_last_error().decode()
     except Exception:  # pragma: no cover
         return "?"
+
+
+def build_info() -> str:
+    return lib().gdp_build_info().decode()
 
 
 def launch_count() -> int:

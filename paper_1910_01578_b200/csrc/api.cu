@@ -10,6 +10,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "cost2.cuh"
 
 namespace gdp {
 
@@ -152,11 +153,19 @@ bool ws_layout(const gdp_graph_s *g, int d, int B, char *base, WS *w) {
   const size_t Bc = (size_t)std::max(B, 1);
   // everything below depends on B (kept last so the offsets above never move)
   z.wb = reinterpret_cast<double *>(take(Bc * sizeof(double)));
-  z.c_rem = reinterpret_cast<int *>(take(Bc * N * sizeof(int)));
-  z.c_rcons = reinterpret_cast<int *>(take(Bc * N * sizeof(int)));
-  z.c_new = reinterpret_cast<int *>(take(Bc * 2 * N * sizeof(int)));
-  z.c_fifo = reinterpret_cast<int2 *>(take(Bc * N * sizeof(int2)));
-  z.c_chq = reinterpret_cast<int4 *>(take(Bc * E * sizeof(int4)));
+  // cost scratch: one region per placement, large enough for either cost kernel
+  size_t v1 = (2 + 2) * N * sizeof(int) + N * sizeof(int2) + E * sizeof(int4) + N * sizeof(int);
+  size_t v2 = cost2_scratch_per_placement(g->N, g->E, g->nbig);
+  z.c_per_place = (std::max(v1, v2) + 255) & ~(size_t)255;
+  z.c_scratch = reinterpret_cast<unsigned char *>(take(Bc * z.c_per_place));
+  if (z.c_scratch) {
+    // v1 view of the same bytes
+    z.c_rem = reinterpret_cast<int *>(z.c_scratch);
+    z.c_rcons = z.c_rem + Bc * N;
+    z.c_new = z.c_rcons + Bc * N;
+    z.c_fifo = reinterpret_cast<int2 *>(z.c_new + Bc * 2 * N);
+    z.c_chq = reinterpret_cast<int4 *>(z.c_fifo + Bc * N);
+  }
   z.bytes = off;
   (void)d;
   *w = z;
@@ -195,6 +204,8 @@ extern "C" {
 const char *gdp_last_error(void) { return g_err.c_str(); }
 
 uint64_t gdp_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
+
+const char *gdp_build_info(void) { return "libgdp sm_100a built " __DATE__ " " __TIME__; }
 
 gdp_status gdp_default_config(int32_t d, gdp_config *out) {
   if (!out) return fail(GDP_ERR_ARG, "out is NULL");
@@ -326,6 +337,38 @@ gdp_status gdp_graph_create(int32_t N, int32_t F, const float *feat, int64_t E, 
     g->max_indeg = std::max(g->max_indeg, iptr[v + 1] - iptr[v]);
     g->max_outdeg = std::max(g->max_outdeg, optr[v + 1] - optr[v]);
   }
+  // records of the shared-memory cost model
+  std::vector<NRec> nrec(N), erec((size_t)std::max<int64_t>(E, 1));
+  std::vector<IRec> irec((size_t)std::max<int64_t>(E, 1));
+  for (int v = 0; v < N; v++) {
+    NRec &r = nrec[v];
+    r.id = v; r.cost = cost[v]; r.ob = optr[v]; r.oe = optr[v + 1]; r.ib = iptr[v]; r.ie = iptr[v + 1];
+    r.bytes = output_bytes[v];
+  }
+  for (int64_t e = 0; e < E; e++) {
+    erec[(size_t)e] = nrec[oidx[(size_t)e]];
+    irec[(size_t)e].u = iidx[(size_t)e];
+    irec[(size_t)e].pad = 0;
+    irec[(size_t)e].bytes = output_bytes[iidx[(size_t)e]];
+  }
+  std::vector<unsigned> cnt0((N + 3) / 4, 0u);
+  std::vector<int> bigid(N, -1), big_in, big_out;
+  for (int v = 0; v < N; v++) {
+    int din = iptr[v + 1] - iptr[v], dout = optr[v + 1] - optr[v];
+    unsigned nib_in = din, nib_out = dout;
+    if (din >= 15 || dout >= 15) {
+      bigid[v] = (int)big_in.size();
+      big_in.push_back(din);
+      big_out.push_back(dout);
+      if (din >= 15) nib_in = 15;
+      if (dout >= 15) nib_out = 15;
+    }
+    // a big node keeps the sentinel in BOTH nibbles so that both counters use the global path
+    if (bigid[v] >= 0) { nib_in = 15; nib_out = 15; }
+    cnt0[v >> 2] |= (nib_in | (nib_out << 4)) << ((v & 3) * 8);
+  }
+  g->nbig = (int)big_in.size();
+  if (big_in.empty()) { big_in.push_back(0); big_out.push_back(0); }
   auto up = [&](void **dst, const void *src, size_t bytes) -> cudaError_t {
     cudaError_t e = cudaMalloc(dst, bytes ? bytes : 4);
     if (e != cudaSuccess) return e;
@@ -350,6 +393,13 @@ gdp_status gdp_graph_create(int32_t N, int32_t F, const float *feat, int64_t E, 
   UP(mem_bytes, memory_bytes, N * sizeof(long long));
   UP(perm, order.data(), N * sizeof(int));
   UP(leader, leader.data(), N * sizeof(int));
+  UP(nrec, nrec.data(), nrec.size() * sizeof(NRec));
+  UP(erec, erec.data(), erec.size() * sizeof(NRec));
+  UP(irec, irec.data(), irec.size() * sizeof(IRec));
+  UP(cnt0, cnt0.data(), cnt0.size() * sizeof(unsigned));
+  UP(bigid, bigid.data(), N * sizeof(int));
+  UP(big_in, big_in.data(), big_in.size() * sizeof(int));
+  UP(big_out, big_out.data(), big_out.size() * sizeof(int));
 #undef UP
   *out = g;
   return GDP_OK;
@@ -358,7 +408,8 @@ gdp_status gdp_graph_create(int32_t N, int32_t F, const float *feat, int64_t E, 
 gdp_status gdp_graph_destroy(gdp_graph g) {
   if (!g) return GDP_OK;
   void *ptrs[] = {g->X, g->nbr_ptr, g->nbr_idx, g->out_ptr, g->out_idx, g->out_src, g->in_ptr, g->in_idx,
-                  g->cost, g->out_bytes, g->mem_bytes, g->perm, g->leader};
+                  g->cost, g->out_bytes, g->mem_bytes, g->perm, g->leader, g->nrec, g->erec, g->irec,
+                  g->cnt0, g->bigid, g->big_in, g->big_out};
   for (void *p : ptrs)
     if (p) cudaFree(p);
   delete g;

@@ -55,6 +55,11 @@ struct gdp_graph_s {
   long long sum_edge_out_bytes = 0;                 // sum over edges of producer output bytes
   long long n_edges_cross_max = 0;
   int max_indeg = 0, max_outdeg = 0;
+  // shared-memory cost model records (cost2.cuh)
+  void *nrec = nullptr, *erec = nullptr, *irec = nullptr;
+  unsigned *cnt0 = nullptr;
+  int *bigid = nullptr, *big_in = nullptr, *big_out = nullptr;
+  int nbig = 0;
 };
 
 struct gdp_topo_s {
@@ -102,7 +107,9 @@ struct WS {
   // sample
   float *cdf, *logp;
   int *lastpos;
-  // cost scratch
+  // cost scratch: B regions of c_per_place bytes (v2) or the v1 arrays
+  unsigned char *c_scratch;
+  size_t c_per_place;
   int *c_rem, *c_rcons, *c_new;
   int2 *c_fifo;
   int4 *c_chq;

@@ -17,8 +17,10 @@
 // Lanes 0..d-1 own the devices (running op, finish time).  Device time is int32 (the host
 // rejects graphs whose total duration + transfer could reach 2^31 ticks).
 #include <climits>
+#include <cstdlib>
 
 #include "common.cuh"
+#include "cost2.cuh"
 
 namespace gdp {
 namespace {
@@ -400,6 +402,24 @@ __global__ void k_advantage(const double *r, int B, double *sum, long long *cnt,
 
 gdp_status launch_cost(const gdp_graph_s *g, const gdp_topo_s *t, const uint8_t *D, int B, gdp_sim_report *rep,
                        long long *peak, long long *busy, double *reward, const WS &w, cudaStream_t s) {
+  TopoArgs T;
+  T.d = t->d;
+  for (int i = 0; i < 8; i++) { T.cap[i] = t->cap[i]; T.speed[i] = t->speed[i]; }
+  for (int i = 0; i < 64; i++) { T.bpt[i] = t->bpt[i]; T.lat[i] = t->lat[i]; }
+  static const bool force_v1 = getenv("GDP_COST_V1") != nullptr;
+  if (!force_v1) {
+    Cost2Graph C;
+    C.N = g->N; C.E = g->E;
+    C.nrec = static_cast<const NRec *>(g->nrec); C.erec = static_cast<const NRec *>(g->erec);
+    C.irec = static_cast<const IRec *>(g->irec);
+    C.cnt0 = g->cnt0; C.bigid = g->bigid; C.big_in = g->big_in; C.big_out = g->big_out; C.nbig = g->nbig;
+    C.out_idx = g->out_idx; C.out_src = g->out_src; C.in_ptr = g->in_ptr; C.cost = g->cost; C.leader = g->leader;
+    C.out_bytes = g->out_bytes; C.mem_bytes = g->mem_bytes; C.has_coloc = g->has_coloc ? 1 : 0;
+    if (launch_cost2(C, T, D, B, w.c_scratch, w.c_per_place, rep, peak, busy, reward, s)) {
+      GDP_LAUNCH_CHECK("k_cost2");
+      return GDP_OK;
+    }
+  }
   CostGraph G;
   G.N = g->N;
   G.E = g->E;
@@ -408,10 +428,6 @@ gdp_status launch_cost(const gdp_graph_s *g, const gdp_topo_s *t, const uint8_t 
   G.cost = g->cost; G.leader = g->leader;
   G.out_bytes = g->out_bytes; G.mem_bytes = g->mem_bytes;
   G.has_coloc = g->has_coloc ? 1 : 0;
-  TopoArgs T;
-  T.d = t->d;
-  for (int i = 0; i < 8; i++) { T.cap[i] = t->cap[i]; T.speed[i] = t->speed[i]; }
-  for (int i = 0; i < 64; i++) { T.bpt[i] = t->bpt[i]; T.lat[i] = t->lat[i]; }
   note_launch();
   k_cost<<<B, 32, 0, s>>>(G, T, D, B, w.c_rem, w.c_rcons, w.c_fifo, w.c_new, w.c_chq, rep, peak, busy, reward);
   GDP_LAUNCH_CHECK("k_cost");

@@ -1,0 +1,522 @@
+// Cost model, shared-memory kernel (the default; cost.cu's k_cost is the fallback for graphs
+// whose per-placement state does not fit in shared memory).  Same event semantics as the
+// oracle (DESIGN.md §"Cost model"); this is a re-formulation for a GPU warp:
+//
+//  * lane k < d OWNS device k: its running op and finish time (registers), its FIFO of
+//    available ops, and its outgoing channels (k -> t): channel state is only ever touched by
+//    lane k, so enqueue (at lane k's finishes) and dequeue (arrivals) need no atomics and no
+//    warp-wide coordination;
+//  * an op keeps a counter of inputs not yet ARRIVED; it becomes available at the instant the
+//    counter reaches 0 (its ready time), so no per-op ready time and no priority queue exist:
+//    ops made available at one instant are sorted by id and appended to their device FIFO,
+//    which is thus sorted by (ready, id) -- dispatch pops its head (SPEC.md:278 (c));
+//  * per op one byte of counters in smem (low nibble: inputs not yet arrived, high nibble:
+//    consumers not yet finished; degree >= 15 -> global counters), 4-bit device ids in smem;
+//  * FIFOs and channel queues keep their first K entries (full records) in smem; the rest
+//    overflow to global and are pulled back with cp.async as the head advances;
+//  * the successor / producer records an op's finish needs are staged into smem by
+//    cp.async while the op waits at its FIFO head (double-buffered per device).
+// One CTA (one warp) per placement.
+#include <climits>
+#include <cstdlib>
+
+#include "common.cuh"
+#include "cost2.cuh"
+
+namespace gdp {
+namespace {
+
+constexpr int SO = 8;     // staged out-edge records per slot
+constexpr int SI = 8;     // staged in-edge records per slot
+constexpr int KF = 4;     // FIFO entries kept in smem per device
+constexpr int KC = 4;     // channel entries kept in smem per channel
+constexpr int NINC = 32;  // per-device list of ops made available this round (overflow -> global)
+constexpr int INF = INT_MAX;
+
+struct __align__(16) Ent {   // FIFO entry (t = ready) / channel entry (t = arrival, bytes = copy size)
+  NRec r;
+  int t, pad;
+  long long bytes;
+};
+
+struct Smem {
+  NRec st_out[8][2][SO];
+  IRec st_in[8][2][SI];
+  Ent fc[8][KF];
+  Ent cc[8][8][KC];
+  NRec inc[8][NINC];
+  NRec sreq[8];
+  unsigned memlo[8], memhi[8];   // per-device resident bytes as two 32-bit words (native atomics)
+  long long peak[8];
+  int ch_head[8][8], ch_tail[8][8], ch_free[8][8], ch_arr[8][8], ch_off[8][8];
+  int ccnt[64];
+  int inc_n[8], doff[8], sreq_slot[8];
+};
+
+__device__ __forceinline__ void cp16(void *s, const void *g) {
+  unsigned a = (unsigned)__cvta_generic_to_shared(s);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(a), "l"(g) : "memory");
+}
+__device__ __forceinline__ void cp_ent(Ent *s, const Ent *g) {
+  cp16(reinterpret_cast<int4 *>(s), g);
+  cp16(reinterpret_cast<int4 *>(s) + 1, reinterpret_cast<const int4 *>(g) + 1);
+  cp16(reinterpret_cast<int4 *>(s) + 2, reinterpret_cast<const int4 *>(g) + 2);
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_wait0() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_wait1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
+
+__device__ __forceinline__ void copy_rec(NRec *dst, const NRec *src) {
+  const int4 *s = reinterpret_cast<const int4 *>(src);
+  int4 *d = reinterpret_cast<int4 *>(dst);
+  d[0] = s[0];
+  d[1] = s[1];
+}
+__device__ __forceinline__ void store_ent(Ent *dst, const NRec &r, int t, long long bytes) {
+  int4 *d = reinterpret_cast<int4 *>(dst);
+  const int4 *s = reinterpret_cast<const int4 *>(&r);
+  d[0] = s[0];
+  d[1] = s[1];
+  d[2] = make_int4(t, 0, (int)(bytes & 0xffffffffLL), (int)(bytes >> 32));
+}
+__device__ __forceinline__ void load_rec(NRec &r, const NRec *src) {
+  const int4 *s = reinterpret_cast<const int4 *>(src);
+  int4 a = s[0], b = s[1];
+  r.id = a.x; r.cost = a.y; r.ob = a.z; r.oe = a.w; r.ib = b.x; r.ie = b.y;
+  r.bytes = ((long long)(unsigned)b.z) | ((long long)b.w << 32);
+}
+__device__ __forceinline__ long long warp_sum_ll(long long v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+// 64-bit add as two native 32-bit shared atomics: each add carries its own low-word wrap
+__device__ __forceinline__ void add_mem(unsigned *lo, unsigned *hi, int dev, long long v) {
+  const unsigned a = (unsigned)((unsigned long long)v & 0xffffffffull);
+  const unsigned h = (unsigned)((unsigned long long)v >> 32);
+  const unsigned old = atomicAdd(&lo[dev], a);
+  const unsigned hc = h + ((old + a) < old ? 1u : 0u);
+  if (hc) atomicAdd(&hi[dev], hc);
+}
+__device__ __forceinline__ long long read_mem(const unsigned *lo, const unsigned *hi, int dev) {
+  return (long long)(((unsigned long long)hi[dev] << 32) | lo[dev]);
+}
+__device__ __forceinline__ int dev_of(const unsigned *Dn, int v) { return (Dn[v >> 3] >> ((v & 7) * 4)) & 15; }
+
+// decrement the 4-bit counter of v at nibble `hi` (0 = inputs, 1 = consumers); true iff it hits 0
+__device__ __forceinline__ bool dec_counter(unsigned *cnt, int v, int hi, int *bigc, const int *bigid, int nbig) {
+  const int sh = (v & 3) * 8 + hi * 4;
+  if (((cnt[v >> 2] >> sh) & 15u) == 15u) return atomicSub(&bigc[bigid[v] + hi * nbig], 1) == 1;
+  unsigned old = atomicSub(&cnt[v >> 2], 1u << sh);
+  return ((old >> sh) & 15u) == 1u;
+}
+
+__device__ __forceinline__ int xfer_time(long long bytes, int k, int tw, const TopoArgs &T) {
+  const long long bw = T.bpt[k * 8 + tw];
+  long long q;
+  if (bytes < (1LL << 52)) q = (long long)ceil(__ddiv_rn((double)bytes, (double)bw));
+  else q = (bytes + bw - 1) / bw;
+  return (int)q + T.lat[k * 8 + tw];
+}
+
+// an op became available now: append to device dev's incoming list for this round
+__device__ __forceinline__ void push_inc(Smem &S, NRec *ov, int dev, const NRec &r) {
+  const int i = atomicAdd(&S.inc_n[dev], 1);
+  if (i < NINC) copy_rec(&S.inc[dev][i], &r);
+  else copy_rec(ov + S.doff[dev] + i, &r);
+}
+
+__global__ void __launch_bounds__(32) k_cost2(Cost2Graph G, TopoArgs T, const uint8_t *__restrict__ Dall,
+                                              unsigned char *scratch, size_t per_place, gdp_sim_report *rep,
+                                              long long *peak_out, long long *busy_out, double *reward, int dbg) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Smem &S = *reinterpret_cast<Smem *>(smem_raw);
+  const int N = G.N, d = T.d, b = blockIdx.x, lane = threadIdx.x;
+  const unsigned lt = (1u << lane) - 1u;
+  unsigned *cnt = reinterpret_cast<unsigned *>(smem_raw + sizeof(Smem));
+  const int cwords = (N + 3) >> 2;
+  unsigned *Dn = cnt + cwords;
+  const int dwords = (N + 7) >> 3;
+  const uint8_t *D = Dall + (size_t)b * N;
+  unsigned char *base = scratch + (size_t)b * per_place;
+  Ent *fifo = reinterpret_cast<Ent *>(base);
+  Ent *chq = fifo + N;
+  NRec *ov = reinterpret_cast<NRec *>(chq + (G.E > 0 ? G.E : 1));
+  int *bigc = reinterpret_cast<int *>(ov + N);
+
+  // ---------------------------------------------------------------- prologue (warp-wide)
+  for (int i = lane; i < cwords; i += 32) cnt[i] = G.cnt0[i];
+  long long lmem[8], lbusy[8];
+  int lcnt[8], flag = 0;
+#pragma unroll
+  for (int k = 0; k < 8; k++) { lmem[k] = 0; lbusy[k] = 0; lcnt[k] = 0; }
+  for (int p = lane; p < dwords; p += 32) {
+    unsigned packed = 0;
+    for (int j = 0; j < 8; j++) {
+      const int v = 8 * p + j;
+      if (v >= N) break;
+      int k = D[v];
+      if (k >= d) { flag |= 2; k = 0; }
+      packed |= (unsigned)k << (4 * j);
+      const long long mb = G.mem_bytes[v];
+      const long long du = (long long)G.cost[v] * T.speed[k];
+#pragma unroll
+      for (int q = 0; q < 8; q++)
+        if (q == k) { lmem[q] += mb; lbusy[q] += du; lcnt[q] += 1; }
+      if (G.has_coloc && D[G.leader[v]] != D[v]) flag |= 1;
+    }
+    Dn[p] = packed;
+  }
+  for (int j = lane; j < G.nbig; j += 32) { bigc[j] = G.big_in[j]; bigc[G.nbig + j] = G.big_out[j]; }
+  S.ccnt[lane] = 0;
+  S.ccnt[lane + 32] = 0;
+  if (lane < 8) S.inc_n[lane] = 0;
+  flag = __reduce_or_sync(0xffffffffu, flag);
+  long long mymem = 0, mybusy = 0;
+  int mycnt = 0;
+#pragma unroll
+  for (int k = 0; k < 8; k++) {
+    long long a = warp_sum_ll(lmem[k]), c = warp_sum_ll(lbusy[k]);
+    int n = __reduce_add_sync(0xffffffffu, lcnt[k]);
+    if (lane == k) { mymem = a; mybusy = c; mycnt = n; }
+  }
+  gdp_sim_report R;
+  R.makespan = 0; R.cross_bytes = 0; R.valid = 0; R.violation = 0;
+  for (int i = 0; i < 6; i++) R.pad[i] = 0;
+  if (flag & 2) {   // malformed: an entry >= d
+    if (lane == 0) { R.violation = 3; rep[b] = R; reward[b] = -10.0; }
+    if (lane < d) {
+      if (peak_out) peak_out[(size_t)b * d + lane] = 0;
+      if (busy_out) busy_out[(size_t)b * d + lane] = 0;
+    }
+    return;
+  }
+  if (lane < 8) {
+    S.memlo[lane] = (unsigned)((unsigned long long)mymem & 0xffffffffull);
+    S.memhi[lane] = (unsigned)((unsigned long long)mymem >> 32);
+    S.peak[lane] = mymem;
+  }
+  __syncwarp();
+  long long lcross = 0;
+  for (long long e = lane; e < G.E; e += 32) {
+    const int u = G.out_src[e], w = G.out_idx[e];
+    const int su = dev_of(Dn, u), tw = dev_of(Dn, w);
+    if (su != tw) {
+      atomicAdd(&S.ccnt[su * 8 + tw], 1);
+      lcross += G.out_bytes[u];
+    }
+  }
+  const long long cross = warp_sum_ll(lcross);
+  __syncwarp();
+  {  // device regions (FIFO overflow, incoming overflow) from op counts
+    int c = lane < d ? mycnt : 0, inc = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int y = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += y;
+    }
+    if (lane < 8) S.doff[lane] = inc - c;
+  }
+  {  // channel regions, channels 2*lane and 2*lane+1 in (source, target) order
+    const int c0 = S.ccnt[2 * lane], c1 = S.ccnt[2 * lane + 1];
+    const int pair = c0 + c1;
+    int inc = pair;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int y = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += y;
+    }
+    const int c = 2 * lane;
+    S.ch_off[c >> 3][c & 7] = inc - pair;
+    S.ch_off[(c + 1) >> 3][(c + 1) & 7] = inc - pair + c0;
+  }
+  if (lane < 8) {
+#pragma unroll
+    for (int q = 0; q < 8; q++) {
+      S.ch_head[lane][q] = 0; S.ch_tail[lane][q] = 0; S.ch_free[lane][q] = 0; S.ch_arr[lane][q] = INF;
+    }
+  }
+  __syncwarp();
+  // sources are available at t = 0: appended to their FIFO in ascending id
+  int fhead = 0, ftail = 0;   // lane k: FIFO head / tail (relative to the device region)
+  for (int v0 = 0; v0 < N; v0 += 32) {
+    const int v = v0 + lane;
+    const bool src = v < N && G.in_ptr[v + 1] == G.in_ptr[v];
+    if (!__any_sync(0xffffffffu, src)) continue;
+    const int k = src ? dev_of(Dn, v) : 0;
+    int off = 0, cntk = 0;
+    for (int dev = 0; dev < d; dev++) {
+      const unsigned m = __ballot_sync(0xffffffffu, src && k == dev);
+      if (src && k == dev) off = __popc(m & lt);
+      if (lane == dev) cntk = __popc(m);
+    }
+    const int tail_k = __shfl_sync(0xffffffffu, ftail, k & 7);
+    if (src) {
+      NRec r;
+      load_rec(r, G.nrec + v);
+      const int pos = tail_k + off;
+      if (pos < KF) store_ent(&S.fc[k][pos], r, 0, 0);
+      else store_ent(fifo + S.doff[k] + pos, r, 0, 0);
+    }
+    ftail += cntk;
+    __syncwarp();
+  }
+
+  if (dbg == 1) return;
+  // ---------------------------------------------------------------- event loop
+  NRec run;
+  run.id = -1; run.cost = 0; run.ob = run.oe = run.ib = run.ie = 0; run.bytes = 0;
+  int fin = 0, running = 0, mk = 0, dispatched = 0, multi = 0, my_arr = INF;
+  int cur = 0, cur_inst = -2, nxt_id = -1, nxt_inst = -2;
+  int t = 0, n_inst = 0, n_round = 0, n_fin = 0;
+  const bool dl = lane < d;
+  for (int inst = 0;; inst++) {
+    if (inst > 0) {
+      const int cand = dl ? min(running ? fin : INF, my_arr) : INF;
+      t = __reduce_min_sync(0xffffffffu, cand);
+      if (t == INF) break;
+    }
+    {  // records staged at the previous instant may still be in flight
+      const bool need = (dl && running && fin == t && cur_inst == inst - 1) || multi;
+      if (__any_sync(0xffffffffu, need)) cp_wait0(); else cp_wait1();
+    }
+    n_inst++;
+    for (int round = 0;; round++) {
+      n_round++;
+      if (round > 0) cp_wait0();
+      __syncwarp();
+      if (dl) {
+        // (1) arrivals on my outgoing channels (only the first round can have any)
+        if (round == 0) {
+          multi = 0;
+          if (my_arr <= t) {
+            int m = INF;
+            for (int q = 0; q < d; q++) {
+              int a = S.ch_arr[lane][q];
+              if (a <= t) {
+                int head = S.ch_head[lane][q];
+                const int tail = S.ch_tail[lane][q];
+                int popped = 0;
+                while (a <= t) {
+                  if (popped) cp_wait0();
+                  Ent &e = S.cc[lane][q][head % KC];
+                  add_mem(S.memlo, S.memhi, q, e.bytes);
+                  if (dec_counter(cnt, e.r.id, 0, bigc, G.bigid, G.nbig)) push_inc(S, ov, q, e.r);
+                  if (head + KC < tail) cp_ent(&e, chq + S.ch_off[lane][q] + head + KC);
+                  head++;
+                  multi |= popped;
+                  popped = 1;
+                  a = head < tail ? S.cc[lane][q][head % KC].t : INF;
+                }
+                S.ch_head[lane][q] = head;
+                S.ch_arr[lane][q] = a;
+              }
+              m = min(m, a);
+            }
+            my_arr = m;
+          }
+        }
+        // (2) my op finishes now
+        if (running && fin == t) {
+          n_fin++;
+          running = 0;
+          const int k = lane;
+          // frees: copies this op held, producers whose last consumer it was, sink output
+          const int nin = run.ie - run.ib;
+          for (int j = 0; j < nin; j++) {
+            IRec ir;
+            if (j < SI) ir = S.st_in[k][cur][j];
+            else ir = G.irec[run.ib + j];
+            const int du = dev_of(Dn, ir.u);
+            if (du != k) add_mem(S.memlo, S.memhi, k, -ir.bytes);
+            if (dec_counter(cnt, ir.u, 1, bigc, G.bigid, G.nbig)) add_mem(S.memlo, S.memhi, du, -ir.bytes);
+          }
+          if (run.oe == run.ob) add_mem(S.memlo, S.memhi, k, -run.bytes);
+          // out-edges in ascending consumer id: same device -> input arrives now; cross ->
+          // FIFO on channel (k -> tw): arrival = max(t, channel free) + transfer
+          const int nout = run.oe - run.ob;
+          for (int j = 0; j < nout; j++) {
+            NRec wr;
+            if (j < SO) wr = S.st_out[k][cur][j];
+            else load_rec(wr, G.erec + run.ob + j);
+            const int tw = dev_of(Dn, wr.id);
+            if (tw == k) {
+              if (dec_counter(cnt, wr.id, 0, bigc, G.bigid, G.nbig)) push_inc(S, ov, k, wr);
+              continue;
+            }
+            const int arr = max(t, S.ch_free[k][tw]) + xfer_time(run.bytes, k, tw, T);
+            S.ch_free[k][tw] = arr;
+            if (arr == t) {   // zero-time transfer: the copy lands now
+              add_mem(S.memlo, S.memhi, tw, run.bytes);
+              if (dec_counter(cnt, wr.id, 0, bigc, G.bigid, G.nbig)) push_inc(S, ov, tw, wr);
+              continue;
+            }
+            const int head = S.ch_head[k][tw], pos = S.ch_tail[k][tw];
+            if (pos < head + KC) store_ent(&S.cc[k][tw][pos % KC], wr, arr, run.bytes);
+            else store_ent(chq + S.ch_off[k][tw] + pos, wr, arr, run.bytes);
+            if (pos == head) {
+              S.ch_arr[k][tw] = arr;
+              my_arr = min(my_arr, arr);
+            }
+            S.ch_tail[k][tw] = pos + 1;
+          }
+        }
+      }
+      __syncwarp();
+      bool zero = false, req = false;
+      if (dl) {
+        // (3) ops made available now (ready = t) join my FIFO in id order
+        const int n = S.inc_n[lane];
+        if (n > 0) {
+          NRec *L = &S.inc[lane][0];
+          NRec *O = ov + S.doff[lane];
+          for (int i = 1; i < n; i++) {   // insertion sort by id (n is small except after wide fan-outs)
+            NRec key;
+            load_rec(key, i < NINC ? &L[i] : &O[i]);
+            int j = i - 1;
+            while (j >= 0) {
+              NRec *pj = j < NINC ? &L[j] : &O[j];
+              if (pj->id <= key.id) break;
+              copy_rec(j + 1 < NINC ? &L[j + 1] : &O[j + 1], pj);
+              j--;
+            }
+            copy_rec(j + 1 < NINC ? &L[j + 1] : &O[j + 1], &key);
+          }
+          Ent *F = fifo + S.doff[lane];
+          if (round > 0) {
+            // zero-duration corner case: entries appended earlier in this instant share ready
+            // time t and must stay merged by id with the new ones (rare path, done in global)
+            for (int i = fhead; i < min(ftail, fhead + KF); i++) F[i] = S.fc[lane][i % KF];
+            int tail = ftail;
+            for (int i = 0; i < n; i++) store_ent(&F[tail++], i < NINC ? L[i] : O[i], t, 0);
+            int s0 = ftail;
+            while (s0 > fhead && F[s0 - 1].t == t) s0--;
+            for (int i = s0 + 1; i < tail; i++) {
+              Ent key = F[i];
+              int j = i - 1;
+              while (j >= s0 && F[j].r.id > key.r.id) { F[j + 1] = F[j]; j--; }
+              F[j + 1] = key;
+            }
+            for (int i = fhead; i < min(tail, fhead + KF); i++) S.fc[lane][i % KF] = F[i];
+            ftail = tail;
+            nxt_id = -1;
+          } else {
+            for (int i = 0; i < n; i++) {
+              const NRec &r = i < NINC ? L[i] : O[i];
+              if (ftail < fhead + KF) store_ent(&S.fc[lane][ftail % KF], r, t, 0);
+              else store_ent(F + ftail, r, t, 0);
+              ftail++;
+            }
+          }
+          S.inc_n[lane] = 0;
+        }
+        // (4) dispatch my FIFO head if idle
+        if (!running && fhead < ftail) {
+          Ent &e = S.fc[lane][fhead % KF];
+          load_rec(run, &e.r);
+          const int dur = run.cost * T.speed[lane];
+          running = 1;
+          fin = t + dur;
+          mk = max(mk, fin);
+          add_mem(S.memlo, S.memhi, lane, run.bytes);
+          zero = dur == 0;
+          dispatched++;
+          cur ^= 1;
+          if (run.id == nxt_id) {   // its records were staged while it waited
+            cur_inst = nxt_inst;
+          } else {                  // stage now
+            cur_inst = inst;
+            S.sreq[lane] = run;
+            S.sreq_slot[lane] = cur;
+            req = true;
+          }
+          nxt_id = -1;
+          if (fhead + KF < ftail) cp_ent(&e, fifo + S.doff[lane] + fhead + KF);
+          fhead++;
+        }
+        // (5) stage the records of the op now waiting at my FIFO head
+        if (running && nxt_id < 0 && fhead < ftail && !req) {
+          const NRec r = S.fc[lane][fhead % KF].r;
+          S.sreq[lane] = r;
+          S.sreq_slot[lane] = cur ^ 1;
+          nxt_id = r.id;
+          nxt_inst = inst;
+          req = true;
+        }
+      }
+      __syncwarp();
+      unsigned rm = __ballot_sync(0xffffffffu, req);
+      while (rm) {   // warp-cooperative cp.async of the requested records
+        const int k = __ffs(rm) - 1;
+        rm &= rm - 1;
+        const NRec rv = S.sreq[k];
+        const int sl = S.sreq_slot[k];
+        const int no = min(rv.oe - rv.ob, SO), ni = min(rv.ie - rv.ib, SI);
+        if (lane < 2 * no) {
+          cp16(reinterpret_cast<int4 *>(&S.st_out[k][sl][lane >> 1]) + (lane & 1),
+               reinterpret_cast<const int4 *>(G.erec + rv.ob + (lane >> 1)) + (lane & 1));
+        } else if (lane < 2 * no + ni) {
+          cp16(&S.st_in[k][sl][lane - 2 * no], G.irec + rv.ib + (lane - 2 * no));
+        }
+      }
+      cp_commit();
+      // (6) peak after all changes of this round
+      if (dl) S.peak[lane] = max(S.peak[lane], read_mem(S.memlo, S.memhi, lane));
+      if (!__any_sync(0xffffffffu, zero)) break;
+    }
+  }
+  cp_wait0();
+  mk = __reduce_max_sync(0xffffffffu, mk);
+  dispatched = __reduce_add_sync(0xffffffffu, dispatched);
+  __syncwarp();
+  int oom = 0;
+  if (dl) {
+    oom = S.peak[lane] > T.cap[lane];
+    if (peak_out) peak_out[(size_t)b * d + lane] = S.peak[lane];
+    if (busy_out) busy_out[(size_t)b * d + lane] = mybusy;
+  }
+  if (dbg == 2 && busy_out && lane == 0) {   // diagnostics: instants / rounds / my finishes
+    busy_out[(size_t)b * d] = n_inst;
+    if (d > 1) busy_out[(size_t)b * d + 1] = n_round;
+    if (d > 2) busy_out[(size_t)b * d + 2] = n_fin;
+  }
+  oom = __reduce_or_sync(0xffffffffu, oom);
+  if (lane == 0) {
+    R.makespan = mk;
+    R.cross_bytes = cross;
+    R.violation = (flag & 1) ? 1 : (oom ? 2 : 0);
+    if (dispatched != N) R.violation = 3;   // cannot happen for a validated DAG
+    R.valid = R.violation == 0;
+    rep[b] = R;
+    reward[b] = R.valid ? -__dsqrt_rn(__ddiv_rn((double)mk, 1e6)) : -10.0;
+  }
+}
+
+}  // namespace
+
+size_t cost2_smem_bytes(int N) { return sizeof(Smem) + 4 * (size_t)((N + 3) / 4) + 4 * (size_t)((N + 7) / 8); }
+
+size_t cost2_scratch_per_placement(int N, long long E, int nbig) {
+  size_t b = sizeof(Ent) * ((size_t)N + (size_t)(E > 0 ? E : 1)) + sizeof(NRec) * (size_t)N +
+             sizeof(int) * 2 * (size_t)(nbig > 0 ? nbig : 1);
+  return (b + 255) & ~(size_t)255;
+}
+
+bool launch_cost2(const Cost2Graph &G, const TopoArgs &T, const uint8_t *D, int B, unsigned char *scratch,
+                  size_t per_place, gdp_sim_report *rep, long long *peak, long long *busy, double *reward,
+                  cudaStream_t s) {
+  const size_t smem = cost2_smem_bytes(G.N);
+  if (smem > 227 * 1024) return false;
+  static_assert(2 * SO + SI <= 32, "one staging request fits one warp pass");
+  static size_t configured = 0;
+  if (smem > 48 * 1024 && smem > configured) {
+    cudaFuncSetAttribute(k_cost2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    configured = smem;
+  }
+  note_launch();
+  static const int dbg = getenv("GDP_COST_DBG") ? atoi(getenv("GDP_COST_DBG")) : 0;
+  k_cost2<<<B, 32, smem, s>>>(G, T, D, scratch, per_place, rep, peak, busy, reward, dbg);
+  return true;
+}
+
+}  // namespace gdp
