@@ -170,6 +170,7 @@ def main():
     ap.add_argument("--impl", default="gdp", choices=["gdp", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--fp32", action="store_true", help="dense maps in fp32 SIMT instead of tcgen05 bf16")
     args = ap.parse_args()
     W = workloads.config(args.config, batch=args.batch, mem_len=args.mem_len)
     args.batch = W.batch
@@ -195,7 +196,7 @@ def main():
 
     graphs = [(g, workloads.features(g), workloads.topology(g, W.d)) for g in W.graphs]
     ps = gdp.PolicyStep(graphs, W.d, W.seg_len, W.mem_len, W.superposition, W.batch, seed=W.seed,
-                        mode="samples", rank=rank, world=world, device=dev)
+                        mode="samples", rank=rank, world=world, device=dev, tensor_cores=not args.fp32)
     th = workloads.init_theta(workloads.F, W.d, seed=7)
     theta = torch.from_numpy(th).to(dev)
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
@@ -312,7 +313,7 @@ def main():
         rep = st0.reports()
         out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
-               "scaling": "weak", "vs_baseline": None, "dtype": "f32/i32", "data": "synthetic",
+               "scaling": "weak", "vs_baseline": None, "dtype": ("f32" if args.fp32 else "bf16xbf16->f32 (tcgen05 dense maps) / f32") + " policy, i32 cost model", "data": "synthetic",
                "config": config_json(W, argparse.Namespace(batch=W.batch, gpus=world)),
                "clocks": clk.summary(), "gpu_launches": int(launches), "roofline": roof, "e2e": e2e,
                "cpu_baseline": cpu,

@@ -67,6 +67,7 @@ static gdp_status check_config(const gdp_config *c) {
   if (c->num_devices < 1 || c->num_devices > kMaxD) return fail(GDP_ERR_ARG, "num_devices must be in 1..8");
   if (c->seg_len < 1) return fail(GDP_ERR_ARG, "seg_len must be >= 1");
   if (c->mem_len < -1) return fail(GDP_ERR_ARG, "mem_len must be >= -1");
+  if (c->tensor_cores != 0 && c->tensor_cores != 1) return fail(GDP_ERR_ARG, "tensor_cores must be 0 or 1");
   return GDP_OK;
 }
 
@@ -219,6 +220,7 @@ gdp_status gdp_default_config(int32_t d, gdp_config *out) {
   out->seg_len = 128;
   out->mem_len = 128;
   out->superposition = 1;
+  out->tensor_cores = 0;
   return GDP_OK;
 }
 
@@ -488,6 +490,7 @@ gdp_status gdp_embed(gdp_graph g, const gdp_config *c, const float *theta, float
   WS w;
   st = carve_any(g, c->num_devices, 1, ws, ws_bytes, &w);
   if (st != GDP_OK) return st;
+  set_tensor_cores(c->tensor_cores != 0);
   return run_embed(g, theta, node_emb, w, c->num_devices, static_cast<cudaStream_t>(stream));
 }
 
@@ -499,6 +502,7 @@ gdp_status gdp_place(gdp_graph g, const gdp_config *c, const float *theta, const
   WS w;
   st = carve_any(g, c->num_devices, 1, ws, ws_bytes, &w);
   if (st != GDP_OK) return st;
+  set_tensor_cores(c->tensor_cores != 0);
   return run_place(g, c, theta, node_emb, logits, w, static_cast<cudaStream_t>(stream));
 }
 
@@ -565,6 +569,7 @@ gdp_status gdp_policy_grad(gdp_graph g, const gdp_config *c, const float *theta,
   WS w;
   st = carve_any(g, c->num_devices, B, ws, ws_bytes, &w);
   if (st != GDP_OK) return st;
+  set_tensor_cores(false);   // the backward's dense maps stay fp32 (DESIGN.md §7 "tcgen05")
   return run_policy_grad(g, c, theta, logits, placements, B, adv, logprob, old_logprob, clip_eps, entropy_coef,
                          loss_scale, grad, w, static_cast<cudaStream_t>(stream));
 }

@@ -139,6 +139,11 @@ struct GemmArgs {
   int epi;
 };
 void launch_gemm(const GemmArgs &a, cudaStream_t s);
+// tcgen05 path (tc_gemm.cu); launch_gemm routes eligible shapes there when the calling
+// entry point enabled tensor cores (gdp_config.tensor_cores)
+bool tc_eligible(const GemmArgs &a);
+void launch_gemm_tc(const GemmArgs &a, cudaStream_t s);
+void set_tensor_cores(bool on);
 
 // dW_aug[(K + with_bias) x Nout] = [X, 1]^T dY over all M rows, deterministic split-K over rows.
 // Result: out (+)= sum (accumulate flag).  part must hold chunks * (K+1) * Nout floats.

@@ -509,7 +509,7 @@ bool launch_cost2(const Cost2Graph &G, const TopoArgs &T, const uint8_t *D, int 
   if (smem > 227 * 1024) return false;
   static_assert(2 * SO + SI <= 32, "one staging request fits one warp pass");
   static size_t configured = 0;
-  if (smem > 48 * 1024 && smem > configured) {
+  if (smem > 40 * 1024 && smem > configured) {
     cudaFuncSetAttribute(k_cost2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     configured = smem;
   }

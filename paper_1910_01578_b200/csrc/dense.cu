@@ -284,8 +284,15 @@ __global__ void k_fill_rows(float *dst, const float *row, float scale, int N, in
 inline unsigned nblk(size_t n, int t) { return (unsigned)((n + t - 1) / t); }
 }  // namespace
 
+static thread_local bool t_tc = false;
+void set_tensor_cores(bool on) { t_tc = on; }
+
 void launch_gemm(const GemmArgs &a, cudaStream_t s) {
   if (a.M <= 0) return;
+  if (t_tc && tc_eligible(a)) {
+    launch_gemm_tc(a, s);
+    return;
+  }
   dim3 grid((a.M + BM - 1) / BM, (a.Nout + BN - 1) / BN);
   note_launch();
   k_gemm<<<grid, NT, 0, s>>>(a);

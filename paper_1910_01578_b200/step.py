@@ -53,11 +53,11 @@ class PolicyStep:
 
     def __init__(self, graphs: List, d: int, seg_len: int, mem_len: int, superposition: bool, batch: int,
                  seed: int = 42, clip_eps: float = 0.2, entropy_coef: float = 0.01, mode: str = "samples",
-                 rank: int = 0, world: int = 1, device=None):
+                 rank: int = 0, world: int = 1, device=None, tensor_cores: bool = False):
         import torch
         self.torch = torch
         self.device = device if device is not None else torch.device("cuda", torch.cuda.current_device())
-        self.cfg = default_config(d, seg_len, mem_len, superposition)
+        self.cfg = default_config(d, seg_len, mem_len, superposition, tensor_cores)
         self.plan = make_plan(mode, rank, world, batch, len(graphs), entropy_coef,
                               [g[0].N * batch for g in graphs])
         self.seed, self.clip_eps = seed, clip_eps

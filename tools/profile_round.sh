@@ -10,5 +10,5 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --c
     python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e > $OUT/launches_bench.log 2>&1
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:k_cost2 -s 1 -c 1 -o $OUT/prof_cost \
     python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e > $OUT/prof_cost.log 2>&1
-timeout 900 ncu --set full --import-source on --clock-control none -k regex:k_gemm -s 40 -c 3 -o $OUT/prof_gemm \
-    python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e > $OUT/prof_gemm.log 2>&1
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:k_gemm_tc -s 20 -c 3 -o $OUT/prof_gemm_tc \
+    python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e > $OUT/prof_gemm_tc.log 2>&1
