@@ -185,12 +185,13 @@ def main():
     import torch.distributed as dist
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
+    distributed = world > 1 or "RANK" in os.environ     # under torchrun even with one rank
+    if distributed:
         dist.init_process_group("nccl", device_id=dev)
     import __graft_entry__
     if rank == 0:
         __graft_entry__.build()
-    if world > 1:
+    if distributed:
         dist.barrier()
     import paper_1910_01578_b200 as gdp
 
@@ -203,7 +204,7 @@ def main():
 
     def sync():
         torch.cuda.synchronize()
-        if world > 1:
+        if distributed:
             dist.barrier()
             torch.cuda.synchronize()
 
@@ -226,7 +227,7 @@ def main():
             times.append(e0.elapsed_time(e1))
     launches = (gdp.launch_count() - launches0) // args.steps
     total_ms = sum(times)
-    if world > 1:
+    if distributed:
         t = torch.tensor([total_ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
@@ -291,7 +292,7 @@ def main():
             sync()
             et.append(e0.elapsed_time(e1))
         tot = sum(et)
-        if world > 1:
+        if distributed:
             t = torch.tensor([tot], device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             tot = float(t.item())
@@ -322,7 +323,7 @@ def main():
                              "grad": statistics.mean(grad_ms)},
                "valid_frac": float(np.mean(rep["valid"])), "makespan_mean_ticks": float(np.mean(rep["makespan"]))}
         print(json.dumps(out), flush=True)
-    if world > 1:
+    if distributed:
         dist.barrier()
         dist.destroy_process_group()
 

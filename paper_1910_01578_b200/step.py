@@ -69,6 +69,9 @@ class PolicyStep:
         self.grad = torch.zeros(self.n_params, dtype=torch.float32, device=self.device)
         self.step_idx = 0
         self.events: Dict[str, list] = {}
+        # NCCL collectives whenever a process group exists (also with one rank, so that the
+        # multi-GPU code path is exercised on a single GPU)
+        self.collective = torch.distributed.is_available() and torch.distributed.is_initialized()
 
     def _ev(self, name: str, timed: bool):
         if timed:
@@ -93,7 +96,7 @@ class PolicyStep:
             self._ev("cost0", timed)
             gdp_cost(st.g, st.t, st.placements, st.B, st.rep, st.peak, st.busy, st.reward, st.ws)
             self._ev("cost1", timed)
-            if P.mode == "samples" and P.world > 1:
+            if P.mode == "samples" and self.collective:
                 torch.distributed.all_gather_into_tensor(st.reward_all, st.reward)
             else:
                 st.reward_all.copy_(st.reward)
@@ -103,6 +106,6 @@ class PolicyStep:
             gdp_policy_grad(st.g, self.cfg, theta, st.logits, st.placements, st.B, adv, st.logprob, None,
                             self.clip_eps, P.entropy_coef, P.loss_scale, self.grad, st.ws)
             self._ev("grad1", timed)
-        if P.world > 1:
+        if self.collective:
             torch.distributed.all_reduce(self.grad)
         self.step_idx += 1
