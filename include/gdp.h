@@ -66,9 +66,10 @@ typedef struct {
   int32_t seg_len;        /* S >= 1: Transformer-XL segment length */
   int32_t mem_len;        /* M >= 0 cached positions before each segment, or -1 = every earlier segment */
   int32_t superposition;  /* 1: Eq. 4 gates on every placer dense map and the head; 0: gates == 1 */
-  int32_t tensor_cores;   /* 0: every dense map in fp32 (SIMT, the 1e-4 parity mode); 1: the forward dense
-                             maps (gdp_embed, gdp_place) with 16 <= width <= 256 on tcgen05 tensor cores,
-                             bf16 operands, fp32 accumulation; gdp_policy_grad's maps stay fp32 */
+  int32_t tensor_cores;   /* 0: every dense map in fp32 (SIMT, the 1e-4 parity mode); 1: dense maps
+                             Y = X W (forward and the backward dX = dY W^T) with 16 <= width <= 256 and
+                             >= 128 rows on tcgen05 tensor cores, bf16 operands, fp32 accumulation in
+                             TMEM; weight gradients (reductions over nodes) stay fp32 */
 } gdp_config;
 
 /* One cost-model verdict per placement. */

@@ -569,7 +569,7 @@ gdp_status gdp_policy_grad(gdp_graph g, const gdp_config *c, const float *theta,
   WS w;
   st = carve_any(g, c->num_devices, B, ws, ws_bytes, &w);
   if (st != GDP_OK) return st;
-  set_tensor_cores(false);   // the backward's dense maps stay fp32 (DESIGN.md §7 "tcgen05")
+  set_tensor_cores(c->tensor_cores != 0);
   return run_policy_grad(g, c, theta, logits, placements, B, adv, logprob, old_logprob, clip_eps, entropy_coef,
                          loss_scale, grad, w, static_cast<cudaStream_t>(stream));
 }

@@ -44,7 +44,7 @@ __device__ __forceinline__ float epi_apply(int epi, float v) {
   }
 }
 
-__global__ void __launch_bounds__(TT, 1) k_gemm_tc(GemmArgs a, int Kp, int Np, int ncols) {
+__global__ void __launch_bounds__(TT, 2) k_gemm_tc(GemmArgs a, int Kp, int Np, int ncols) {
   extern __shared__ __align__(1024) unsigned char sm[];
   __shared__ __align__(8) uint64_t mbar;
   __shared__ uint32_t tmem_base;
@@ -96,6 +96,9 @@ __global__ void __launch_bounds__(TT, 1) k_gemm_tc(GemmArgs a, int Kp, int Np, i
   const bool vec4 = (a.K % 4 == 0) && (a.K1 % 4 == 0) && (a.ldx1 % 4 == 0) && (a.X2 == nullptr || a.ldx2 % 4 == 0) &&
                     ((reinterpret_cast<uintptr_t>(a.X1) & 15) == 0) &&
                     (a.X2 == nullptr || (reinterpret_cast<uintptr_t>(a.X2) & 15) == 0);
+  const bool vec_out = (a.ldy % 4 == 0) && ((reinterpret_cast<uintptr_t>(a.Y) & 15) == 0) &&
+                       (a.Y2 == nullptr || ((a.ldy2 % 4 == 0) && (reinterpret_cast<uintptr_t>(a.Y2) & 15) == 0)) &&
+                       (a.split % 8 == 0 || a.split >= a.Nout);
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int m0 = tile * TM;
     // X rows -> bf16 canonical (two-operand concat: columns [0, K1) from X1, [K1, K) from X2)
@@ -172,18 +175,38 @@ __global__ void __launch_bounds__(TT, 1) k_gemm_tc(GemmArgs a, int Kp, int Np, i
           : "r"(taddr));
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
       if (m >= a.M) continue;
+      float x[8];
 #pragma unroll
       for (int j = 0; j < 8; j++) {
         const int n = c0 + j;
-        if (n >= a.Nout) break;
-        float x = __uint_as_float(v[j]);
-        if (a.bias) x += a.bias[n];
-        if (a.epi == EPI_MASK) x = a.aux[(size_t)m * a.ldaux + n] > 0.f ? x : 0.f;
-        else x = epi_apply(a.epi, x);
-        if (a.R) x += a.R[(size_t)m * a.ldr + n];
-        float *dst = (n < a.split) ? a.Y + (size_t)m * a.ldy + n : a.Y2 + (size_t)m * a.ldy2 + (n - a.split);
-        if (a.accumulate) x += *dst;
-        *dst = x;
+        float y = __uint_as_float(v[j]);
+        if (n < a.Nout) {
+          if (a.bias) y += a.bias[n];
+          if (a.epi == EPI_MASK) y = a.aux[(size_t)m * a.ldaux + n] > 0.f ? y : 0.f;
+          else y = epi_apply(a.epi, y);
+          if (a.R) y += a.R[(size_t)m * a.ldr + n];
+        }
+        x[j] = y;
+      }
+      if (vec_out && c0 + 8 <= a.Nout && (c0 + 8 <= a.split || c0 >= a.split)) {
+        float *dst = (c0 < a.split) ? a.Y + (size_t)m * a.ldy + c0 : a.Y2 + (size_t)m * a.ldy2 + (c0 - a.split);
+        float4 *d4 = reinterpret_cast<float4 *>(dst);
+        float4 p0 = make_float4(x[0], x[1], x[2], x[3]), p1 = make_float4(x[4], x[5], x[6], x[7]);
+        if (a.accumulate) {
+          const float4 q0 = d4[0], q1 = d4[1];
+          p0.x += q0.x; p0.y += q0.y; p0.z += q0.z; p0.w += q0.w;
+          p1.x += q1.x; p1.y += q1.y; p1.z += q1.z; p1.w += q1.w;
+        }
+        d4[0] = p0;
+        d4[1] = p1;
+      } else {
+#pragma unroll
+        for (int j = 0; j < 8; j++) {
+          const int n = c0 + j;
+          if (n >= a.Nout) break;
+          float *dst = (n < a.split) ? a.Y + (size_t)m * a.ldy + n : a.Y2 + (size_t)m * a.ldy2 + (n - a.split);
+          *dst = a.accumulate ? *dst + x[j] : x[j];
+        }
       }
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -223,7 +246,7 @@ void launch_gemm_tc(const GemmArgs &a, cudaStream_t s) {
     configured = true;
   }
   const int ntiles = (a.M + TM - 1) / TM;
-  const int grid = ntiles < num_sms() ? ntiles : num_sms();
+  const int grid = ntiles < 2 * num_sms() ? ntiles : 2 * num_sms();
   note_launch();
   k_gemm_tc<<<grid, TT, smem, s>>>(a, Kp, Np, ncols);
 }
