@@ -326,3 +326,64 @@ def test_tensor_core_mode(gdp, case):
     cos = float(gg @ grad / (np.linalg.norm(gg) * np.linalg.norm(grad)))
     ratio = float(np.linalg.norm(gg) / np.linalg.norm(grad))
     assert cos > 0.98 and abs(ratio - 1) < 0.15, ("grad", cos, ratio)   # measured: c2 0.990 / 0.906
+
+
+# ------------------------------------------------------------------ cost-kernel overflow paths
+def test_cost_overflow_paths(gdp):
+    """Wide fan-out / fan-in (more ops made available at one instant than the smem incoming
+    list holds, degrees beyond the staged records, channel and FIFO queues longer than their smem
+    windows, degree >= 15 counters) on one, two and eight devices."""
+    rng = np.random.default_rng(17)
+    n_src, n_mid = 3, 300
+    edges = []
+    # 3 sources fan out to 300 middle ops each (out-degree 300), which fan into 40 sinks
+    for s in range(n_src):
+        for m in range(n_mid):
+            edges.append((s, n_src + m))
+    sinks = n_src + n_mid
+    for m in range(n_mid):
+        for k in rng.choice(40, size=3, replace=False):
+            edges.append((n_src + m, sinks + int(k)))
+    N = sinks + 40
+    cost = rng.integers(1, 6, size=N)
+    cost[n_src:sinks] = 2          # many equal finish times -> many ops available per instant
+    g = mkgraph(N, edges, cost, out=rng.integers(0, 4000, size=N), mem=rng.integers(0, 100, size=N))
+    for d in (1, 2, 8):
+        t = mktopo(d, bw=700, lat=1, cap=10 ** 9)
+        D = rng.integers(0, d, size=(8, N)).astype(np.uint8)
+        D[0] = 0
+        assert_cost_equal(g, t, D, cost_gpu(gdp, g, t, D))
+
+
+@pytest.mark.parametrize("d", [1, 2])
+def test_cost_full_size_c4_few_devices(gdp, d):
+    g = workloads.config("c4").graphs[0]
+    t = workloads.topology(g, d)
+    D = np.random.default_rng(d).integers(0, d, size=(3, g.N)).astype(np.uint8)
+    assert_cost_equal(g, t, D, cost_gpu(gdp, g, t, D))
+
+
+def test_cost_v1_fallback_matches(gdp):
+    """The global-memory kernel (used when a graph's state exceeds shared memory) on the same
+    inputs, forced through GDP_COST_V1 in a subprocess."""
+    import subprocess, sys, os, json
+    code = r"""
+import sys, json, numpy as np, torch
+sys.path.insert(0, %r)
+import workloads
+from tests.test_gpu_parity import cost_gpu
+import paper_1910_01578_b200 as gdp
+g = workloads.multibranch(blocks=20, seed=5)
+t = workloads.topology(g, 4)
+D = np.random.default_rng(3).integers(0, 4, size=(16, g.N)).astype(np.uint8)
+r = cost_gpu(gdp, g, t, D)
+print(json.dumps({k: np.asarray(v).tolist() for k, v in r.items()}))
+""" % os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, GDP_COST_V1="1")
+    out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stderr[-2000:]
+    r = {k: np.asarray(v) for k, v in json.loads(out.stdout.strip().splitlines()[-1]).items()}
+    g = workloads.multibranch(blocks=20, seed=5)
+    t = workloads.topology(g, 4)
+    D = np.random.default_rng(3).integers(0, 4, size=(16, g.N)).astype(np.uint8)
+    assert_cost_equal(g, t, D, r)
