@@ -124,6 +124,19 @@ def oracle_placements_per_s(W, B_total: int, n_cost: int, threads: int):
     return B_total / step, dict(t_net_s=t_net, t_cost_per_placement_s=t_cost_per)
 
 
+def oracle_single_thread(W, B_total: int, n_cost: int = 2):
+    """the whole oracle step on one host thread (torch intra-op threads = 1,
+    cost model on the calling thread), bounded to n_cost placements, extrapolated to B_total."""
+    import torch
+    nt = torch.get_num_threads()
+    torch.set_num_threads(1)
+    try:
+        v, info = oracle_placements_per_s(W, B_total, n_cost, 1)
+    finally:
+        torch.set_num_threads(nt)
+    return v, info
+
+
 def run_reference(args, W, rank: int):
     """--impl reference: the oracle timed on the host cores, rank 0 only."""
     if rank != 0:
@@ -304,10 +317,13 @@ def main():
         threads = os.cpu_count() or 1
         n_cost = min(W.batch, 16)
         v, info = oracle_placements_per_s(W, W.batch, n_cost, threads)
+        v1, info1 = oracle_single_thread(W, W.batch)
         cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": "oracle",
                "sample": (f"one full fp64 oracle policy fwd+bwd (N={sum(g.N for g in W.graphs)}) + cost model on "
                           f"{n_cost} of {W.batch} placements over {threads} threads; step extrapolated to "
-                          f"B={W.batch}"), "detail": info}
+                          f"B={W.batch}"), "detail": info,
+               "single_thread": {"value": v1, "unit": UNIT, "cores": 1, "detail": info1,
+                                 "sample": "same, torch intra-op threads = 1, 2 placements costed on 1 thread"}}
 
     if rank == 0:
         st0 = ps.states[0]
