@@ -46,6 +46,8 @@ struct Smem {
   Ent cc[8][8][KC];
   NRec inc[8][NINC];
   NRec sreq[8];
+  NRec run[8];                    // k_cost3: record of the op running on each device
+  int run_slot[8];                // k_cost3: its staging slot
   unsigned memlo[8], memhi[8];   // per-device resident bytes as two 32-bit words (native atomics)
   long long peak[8];
   int ch_head[8][8], ch_tail[8][8], ch_free[8][8], ch_arr[8][8], ch_off[8][8];
@@ -126,28 +128,60 @@ __device__ __forceinline__ void push_inc(Smem &S, NRec *ov, int dev, const NRec 
   else copy_rec(ov + S.doff[dev] + i, &r);
 }
 
-__global__ void __launch_bounds__(32) k_cost2(Cost2Graph G, TopoArgs T, const uint8_t *__restrict__ Dall,
-                                              unsigned char *scratch, size_t per_place, gdp_sim_report *rep,
-                                              long long *peak_out, long long *busy_out, double *reward, int dbg) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  Smem &S = *reinterpret_cast<Smem *>(smem_raw);
-  const int N = G.N, d = T.d, b = blockIdx.x, lane = threadIdx.x;
-  const unsigned lt = (1u << lane) - 1u;
-  unsigned *cnt = reinterpret_cast<unsigned *>(smem_raw + sizeof(Smem));
-  const int cwords = (N + 3) >> 2;
-  unsigned *Dn = cnt + cwords;
-  const int dwords = (N + 7) >> 3;
-  const uint8_t *D = Dall + (size_t)b * N;
-  unsigned char *base = scratch + (size_t)b * per_place;
-  Ent *fifo = reinterpret_cast<Ent *>(base);
-  Ent *chq = fifo + N;
-  NRec *ov = reinterpret_cast<NRec *>(chq + (G.E > 0 ? G.E : 1));
-  int *bigc = reinterpret_cast<int *>(ov + N);
+__device__ __forceinline__ gdp_sim_report empty_report() {
+  gdp_sim_report R;
+  R.makespan = 0; R.cross_bytes = 0; R.valid = 0; R.violation = 0;
+  for (int i = 0; i < 6; i++) R.pad[i] = 0;
+  return R;
+}
 
+// per-placement views of shared and global scratch
+struct Ctx {
+  int N, d, b, lane, cwords, dwords;
+  unsigned lt;
+  unsigned *cnt, *Dn;
+  const uint8_t *D;
+  Ent *fifo, *chq;
+  NRec *ov;
+  int *bigc;
+};
+__device__ __forceinline__ Ctx make_ctx(const Cost2Graph &G, const TopoArgs &T, const uint8_t *Dall,
+                                        unsigned char *scratch, size_t per_place, unsigned char *smem_raw) {
+  Ctx C;
+  C.N = G.N; C.d = T.d; C.b = blockIdx.x; C.lane = threadIdx.x;
+  C.lt = (1u << C.lane) - 1u;
+  C.cnt = reinterpret_cast<unsigned *>(smem_raw + sizeof(Smem));
+  C.cwords = (C.N + 3) >> 2;
+  C.Dn = C.cnt + C.cwords;
+  C.dwords = (C.N + 7) >> 3;
+  C.D = Dall + (size_t)C.b * C.N;
+  unsigned char *base = scratch + (size_t)C.b * per_place;
+  C.fifo = reinterpret_cast<Ent *>(base);
+  C.chq = C.fifo + C.N;
+  C.ov = reinterpret_cast<NRec *>(C.chq + (G.E > 0 ? G.E : 1));
+  C.bigc = reinterpret_cast<int *>(C.ov + C.N);
+  return C;
+}
+
+// Warp-wide prologue shared by both kernels: counters and packed device ids into shared
+// memory, static memory / busy / op counts per device, cross bytes, co-location check,
+// per-device and per-channel overflow regions, sources appended to their FIFO at t = 0.
+// Returns false (outputs written) when the placement holds an entry >= d.
+__device__ __forceinline__ bool prologue(const Cost2Graph &G, const TopoArgs &T, Smem &S, const Ctx &C,
+                                         gdp_sim_report *rep, long long *peak_out, long long *busy_out,
+                                         double *reward, int &flag, long long &mymem, long long &mybusy,
+                                         long long &cross, int &ftail) {
+  const int N = C.N, d = C.d, b = C.b, lane = C.lane, cwords = C.cwords, dwords = C.dwords;
+  const unsigned lt = C.lt;
+  unsigned *cnt = C.cnt, *Dn = C.Dn;
+  const uint8_t *D = C.D;
+  Ent *fifo = C.fifo;
+  int *bigc = C.bigc;
   // ---------------------------------------------------------------- prologue (warp-wide)
   for (int i = lane; i < cwords; i += 32) cnt[i] = G.cnt0[i];
   long long lmem[8], lbusy[8];
-  int lcnt[8], flag = 0;
+  int lcnt[8];
+  flag = 0;
 #pragma unroll
   for (int k = 0; k < 8; k++) { lmem[k] = 0; lbusy[k] = 0; lcnt[k] = 0; }
   for (int p = lane; p < dwords; p += 32) {
@@ -172,7 +206,7 @@ __global__ void __launch_bounds__(32) k_cost2(Cost2Graph G, TopoArgs T, const ui
   S.ccnt[lane + 32] = 0;
   if (lane < 8) S.inc_n[lane] = 0;
   flag = __reduce_or_sync(0xffffffffu, flag);
-  long long mymem = 0, mybusy = 0;
+  mymem = 0; mybusy = 0;
   int mycnt = 0;
 #pragma unroll
   for (int k = 0; k < 8; k++) {
@@ -180,16 +214,18 @@ __global__ void __launch_bounds__(32) k_cost2(Cost2Graph G, TopoArgs T, const ui
     int n = __reduce_add_sync(0xffffffffu, lcnt[k]);
     if (lane == k) { mymem = a; mybusy = c; mycnt = n; }
   }
-  gdp_sim_report R;
-  R.makespan = 0; R.cross_bytes = 0; R.valid = 0; R.violation = 0;
-  for (int i = 0; i < 6; i++) R.pad[i] = 0;
   if (flag & 2) {   // malformed: an entry >= d
-    if (lane == 0) { R.violation = 3; rep[b] = R; reward[b] = -10.0; }
+    if (lane == 0) {
+      gdp_sim_report R = empty_report();
+      R.violation = 3;
+      rep[b] = R;
+      reward[b] = -10.0;
+    }
     if (lane < d) {
       if (peak_out) peak_out[(size_t)b * d + lane] = 0;
       if (busy_out) busy_out[(size_t)b * d + lane] = 0;
     }
-    return;
+    return false;
   }
   if (lane < 8) {
     S.memlo[lane] = (unsigned)((unsigned long long)mymem & 0xffffffffull);
@@ -206,7 +242,7 @@ __global__ void __launch_bounds__(32) k_cost2(Cost2Graph G, TopoArgs T, const ui
       lcross += G.out_bytes[u];
     }
   }
-  const long long cross = warp_sum_ll(lcross);
+  cross = warp_sum_ll(lcross);
   __syncwarp();
   {  // device regions (FIFO overflow, incoming overflow) from op counts
     int c = lane < d ? mycnt : 0, inc = c;
@@ -238,7 +274,7 @@ __global__ void __launch_bounds__(32) k_cost2(Cost2Graph G, TopoArgs T, const ui
   }
   __syncwarp();
   // sources are available at t = 0: appended to their FIFO in ascending id
-  int fhead = 0, ftail = 0;   // lane k: FIFO head / tail (relative to the device region)
+  ftail = 0;   // lane k: FIFO tail (relative to the device region)
   for (int v0 = 0; v0 < N; v0 += 32) {
     const int v = v0 + lane;
     const bool src = v < N && G.in_ptr[v + 1] == G.in_ptr[v];
@@ -262,6 +298,24 @@ __global__ void __launch_bounds__(32) k_cost2(Cost2Graph G, TopoArgs T, const ui
     __syncwarp();
   }
 
+  return true;
+}
+
+__global__ void __launch_bounds__(32) k_cost2(Cost2Graph G, TopoArgs T, const uint8_t *__restrict__ Dall,
+                                              unsigned char *scratch, size_t per_place, gdp_sim_report *rep,
+                                              long long *peak_out, long long *busy_out, double *reward, int dbg) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Smem &S = *reinterpret_cast<Smem *>(smem_raw);
+  const Ctx C = make_ctx(G, T, Dall, scratch, per_place, smem_raw);
+  const int N = C.N, d = C.d, b = C.b, lane = C.lane;
+  unsigned *cnt = C.cnt, *Dn = C.Dn;
+  Ent *fifo = C.fifo, *chq = C.chq;
+  NRec *ov = C.ov;
+  int *bigc = C.bigc;
+  int flag, ftail;
+  long long mymem, mybusy, cross;
+  if (!prologue(G, T, S, C, rep, peak_out, busy_out, reward, flag, mymem, mybusy, cross, ftail)) return;
+  int fhead = 0;
   if (dbg == 1) return;
   // ---------------------------------------------------------------- event loop
   NRec run;
@@ -298,7 +352,7 @@ __global__ void __launch_bounds__(32) k_cost2(Cost2Graph G, TopoArgs T, const ui
                 const int tail = S.ch_tail[lane][q];
                 int popped = 0;
                 while (a <= t) {
-                  if (popped) cp_wait0();
+                  if (popped) { cp_commit(); cp_wait0(); }   // the refill issued by the previous pop
                   Ent &e = S.cc[lane][q][head % KC];
                   add_mem(S.memlo, S.memhi, q, e.bytes);
                   if (dec_counter(cnt, e.r.id, 0, bigc, G.bigid, G.nbig)) push_inc(S, ov, q, e.r);
@@ -482,6 +536,284 @@ __global__ void __launch_bounds__(32) k_cost2(Cost2Graph G, TopoArgs T, const ui
   }
   oom = __reduce_or_sync(0xffffffffu, oom);
   if (lane == 0) {
+    gdp_sim_report R = empty_report();
+    R.makespan = mk;
+    R.cross_bytes = cross;
+    R.violation = (flag & 1) ? 1 : (oom ? 2 : 0);
+    if (dispatched != N) R.violation = 3;   // cannot happen for a validated DAG
+    R.valid = R.violation == 0;
+    rep[b] = R;
+    reward[b] = R.valid ? -__dsqrt_rn(__ddiv_rn((double)mk, 1e6)) : -10.0;
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// k_cost3: same state and event semantics as k_cost2, with the work of one instant spread over
+// the whole warp instead of the owning lane:
+//  * channel (k -> q) is owned by lane (8k + q) / 2, which caches its head arrival in a
+//    register and pops its arrivals (all owners in parallel);
+//  * a finishing op's in-edges and out-edges are handled one per lane; out-edges into the
+//    same channel are ranked with __match_any_sync, so their FIFO arrival times
+//    max(t, free) + (rank + 1) * xfer are computed in parallel (every transfer of one op on
+//    one channel has the same size, so the serial recurrence has this closed form);
+//  * lane q < d still owns device q: FIFO append, dispatch, staging requests, peak.
+__device__ __forceinline__ int pop_channel(Smem &S, const Ctx &C, const Cost2Graph &G, int c, int a, int t) {
+  const int q = c & 7;
+  Ent *ring = &S.cc[0][0][0] + c * KC;
+  int head = (&S.ch_head[0][0])[c];
+  const int tail = (&S.ch_tail[0][0])[c];
+  const int off = (&S.ch_off[0][0])[c];
+  int popped = 0;
+  while (a <= t) {
+    if (popped) { cp_commit(); cp_wait0(); }   // the refill issued by the previous pop
+    Ent &e = ring[head % KC];
+    add_mem(S.memlo, S.memhi, q, e.bytes);
+    if (dec_counter(C.cnt, e.r.id, 0, C.bigc, G.bigid, G.nbig)) push_inc(S, C.ov, q, e.r);
+    if (head + KC < tail) cp_ent(&e, C.chq + off + head + KC);
+    head++;
+    popped = 1;
+    a = head < tail ? ring[head % KC].t : INF;
+  }
+  (&S.ch_head[0][0])[c] = head;
+  (&S.ch_arr[0][0])[c] = a;
+  return a;
+}
+
+__device__ __forceinline__ void finish_op(Smem &S, const Ctx &C, const Cost2Graph &G, const TopoArgs &T,
+                                          int k, int t) {
+  const int lane = C.lane;
+  NRec r;
+  load_rec(r, &S.run[k]);
+  const int sl = S.run_slot[k];
+  const int nin = r.ie - r.ib, nout = r.oe - r.ob;
+  // frees: copies this op held, producers whose last consumer it was, sink output
+  for (int j = lane; j < nin; j += 32) {
+    IRec ir;
+    if (j < SI) ir = S.st_in[k][sl][j];
+    else ir = G.irec[r.ib + j];
+    const int du = dev_of(C.Dn, ir.u);
+    if (du != k) add_mem(S.memlo, S.memhi, k, -ir.bytes);
+    if (dec_counter(C.cnt, ir.u, 1, C.bigc, G.bigid, G.nbig)) add_mem(S.memlo, S.memhi, du, -ir.bytes);
+  }
+  if (nout == 0 && lane == 0) add_mem(S.memlo, S.memhi, k, -r.bytes);
+  int *chf = &S.ch_free[0][0], *cht = &S.ch_tail[0][0], *chh = &S.ch_head[0][0], *cha = &S.ch_arr[0][0];
+  const int *cho = &S.ch_off[0][0];
+  for (int j0 = 0; j0 < nout; j0 += 32) {
+    const int j = j0 + lane;
+    const bool v = j < nout;
+    NRec wr;
+    int tw = -1;
+    if (v) {
+      if (j < SO) wr = S.st_out[k][sl][j];
+      else load_rec(wr, G.erec + r.ob + j);
+      tw = dev_of(C.Dn, wr.id);
+    }
+    const bool cross = v && tw != k;
+    if (v && !cross && dec_counter(C.cnt, wr.id, 0, C.bigc, G.bigid, G.nbig)) push_inc(S, C.ov, k, wr);
+    if (__any_sync(0xffffffffu, cross)) {
+      const unsigned grp = __match_any_sync(0xffffffffu, cross ? tw : -1);
+      if (cross) {
+        const int rank = __popc(grp & C.lt), n = __popc(grp);
+        const int c = k * 8 + tw;
+        const int f = chf[c];
+        const int x = xfer_time(r.bytes, k, tw, T);
+        const int base = max(t, f);
+        const int arr = base + (rank + 1) * x;
+        if (arr == t) {   // zero-time transfers (x = 0, channel free): the copies land now
+          add_mem(S.memlo, S.memhi, tw, r.bytes);
+          if (dec_counter(C.cnt, wr.id, 0, C.bigc, G.bigid, G.nbig)) push_inc(S, C.ov, tw, wr);
+          if (rank == 0) chf[c] = t;
+        } else {
+          const int head = chh[c], tail = cht[c], pos = tail + rank;
+          if (pos < head + KC) store_ent(&S.cc[0][0][0] + c * KC + pos % KC, wr, arr, r.bytes);
+          else store_ent(C.chq + cho[c] + pos, wr, arr, r.bytes);
+          if (rank == 0) {
+            chf[c] = base + n * x;
+            cht[c] = tail + n;
+            if (tail == head) cha[c] = base + x;
+          }
+        }
+      }
+      if (j0 + 32 < nout) __syncwarp();   // channel state of this chunk before the next one
+    }
+  }
+}
+
+__global__ void __launch_bounds__(32) k_cost3(Cost2Graph G, TopoArgs T, const uint8_t *__restrict__ Dall,
+                                              unsigned char *scratch, size_t per_place, gdp_sim_report *rep,
+                                              long long *peak_out, long long *busy_out, double *reward, int dbg) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Smem &S = *reinterpret_cast<Smem *>(smem_raw);
+  const Ctx C = make_ctx(G, T, Dall, scratch, per_place, smem_raw);
+  const int N = C.N, d = C.d, b = C.b, lane = C.lane;
+  Ent *fifo = C.fifo;
+  NRec *ov = C.ov;
+  int flag, ftail;
+  long long mymem, mybusy, cross;
+  if (!prologue(G, T, S, C, rep, peak_out, busy_out, reward, flag, mymem, mybusy, cross, ftail)) return;
+  if (dbg == 1) return;
+  int fhead = 0;
+  const bool dl = lane < d;
+  const int c0 = 2 * lane, c1 = 2 * lane + 1;   // my channels (k = c / 8 -> q = c % 8)
+  int ca0 = INF, ca1 = INF;                       // their head arrivals (channels start empty)
+  int fin = 0, running = 0, mk = 0, dispatched = 0;
+  int cur = 0, cur_inst = -2, nxt_id = -1, nxt_inst = -2;
+  long long pk = mymem;
+  int t = 0, n_inst = 0, n_round = 0;
+  for (int inst = 0;; inst++) {
+    if (inst > 0) {
+      const int cand = min(dl && running ? fin : INF, min(ca0, ca1));
+      t = __reduce_min_sync(0xffffffffu, cand);
+      if (t == INF) break;
+    }
+    {  // records staged at the previous instant may still be in flight
+      const bool need = dl && running && fin == t && cur_inst == inst - 1;
+      if (__any_sync(0xffffffffu, need)) cp_wait0(); else cp_wait1();
+    }
+    n_inst++;
+    for (int round = 0;; round++) {
+      n_round++;
+      if (round > 0) cp_wait0();
+      __syncwarp();
+      // (1) copy arrivals due now, every channel owner in parallel (first round only)
+      if (round == 0) {
+        if (ca0 <= t) ca0 = pop_channel(S, C, G, c0, ca0, t);
+        if (ca1 <= t) ca1 = pop_channel(S, C, G, c1, ca1, t);
+        __syncwarp();
+      }
+      // (2) ops finishing now, each handled by the whole warp
+      const bool fmine = dl && running && fin == t;
+      unsigned fm = __ballot_sync(0xffffffffu, fmine);
+      if (fmine) running = 0;
+      while (fm) {
+        const int k = __ffs(fm) - 1;
+        fm &= fm - 1;
+        finish_op(S, C, G, T, k, t);
+      }
+      __syncwarp();
+      ca0 = (&S.ch_arr[0][0])[c0];
+      ca1 = (&S.ch_arr[0][0])[c1];
+      bool zero = false, req = false;
+      if (dl) {
+        // (3) ops made available now (ready = t) join my FIFO in id order
+        const int n = S.inc_n[lane];
+        if (n > 0) {
+          NRec *L = &S.inc[lane][0];
+          NRec *O = ov + S.doff[lane];
+          for (int i = 1; i < n; i++) {   // insertion sort by id (n is small except after wide fan-outs)
+            NRec key;
+            load_rec(key, i < NINC ? &L[i] : &O[i]);
+            int j = i - 1;
+            while (j >= 0) {
+              NRec *pj = j < NINC ? &L[j] : &O[j];
+              if (pj->id <= key.id) break;
+              copy_rec(j + 1 < NINC ? &L[j + 1] : &O[j + 1], pj);
+              j--;
+            }
+            copy_rec(j + 1 < NINC ? &L[j + 1] : &O[j + 1], &key);
+          }
+          Ent *F = fifo + S.doff[lane];
+          if (round > 0) {
+            // zero-duration corner case: entries appended earlier in this instant share ready
+            // time t and must stay merged by id with the new ones (rare path, done in global)
+            for (int i = fhead; i < min(ftail, fhead + KF); i++) F[i] = S.fc[lane][i % KF];
+            int tail = ftail;
+            for (int i = 0; i < n; i++) store_ent(&F[tail++], i < NINC ? L[i] : O[i], t, 0);
+            int s0 = ftail;
+            while (s0 > fhead && F[s0 - 1].t == t) s0--;
+            for (int i = s0 + 1; i < tail; i++) {
+              Ent key = F[i];
+              int j = i - 1;
+              while (j >= s0 && F[j].r.id > key.r.id) { F[j + 1] = F[j]; j--; }
+              F[j + 1] = key;
+            }
+            for (int i = fhead; i < min(tail, fhead + KF); i++) S.fc[lane][i % KF] = F[i];
+            ftail = tail;
+            nxt_id = -1;
+          } else {
+            for (int i = 0; i < n; i++) {
+              const NRec &r = i < NINC ? L[i] : O[i];
+              if (ftail < fhead + KF) store_ent(&S.fc[lane][ftail % KF], r, t, 0);
+              else store_ent(F + ftail, r, t, 0);
+              ftail++;
+            }
+          }
+          S.inc_n[lane] = 0;
+        }
+        // (4) dispatch my FIFO head if idle
+        if (!running && fhead < ftail) {
+          Ent &e = S.fc[lane][fhead % KF];
+          NRec run;
+          load_rec(run, &e.r);
+          const int dur = run.cost * T.speed[lane];
+          running = 1;
+          fin = t + dur;
+          mk = max(mk, fin);
+          add_mem(S.memlo, S.memhi, lane, run.bytes);
+          zero = dur == 0;
+          dispatched++;
+          cur ^= 1;
+          copy_rec(&S.run[lane], &run);
+          S.run_slot[lane] = cur;
+          if (run.id == nxt_id) {   // its records were staged while it waited
+            cur_inst = nxt_inst;
+          } else {                  // stage now
+            cur_inst = inst;
+            copy_rec(&S.sreq[lane], &run);
+            S.sreq_slot[lane] = cur;
+            req = true;
+          }
+          nxt_id = -1;
+          if (fhead + KF < ftail) cp_ent(&e, fifo + S.doff[lane] + fhead + KF);
+          fhead++;
+        }
+        // (5) stage the records of the op now waiting at my FIFO head
+        if (running && nxt_id < 0 && fhead < ftail && !req) {
+          const NRec r = S.fc[lane][fhead % KF].r;
+          S.sreq[lane] = r;
+          S.sreq_slot[lane] = cur ^ 1;
+          nxt_id = r.id;
+          nxt_inst = inst;
+          req = true;
+        }
+      }
+      __syncwarp();
+      unsigned rm = __ballot_sync(0xffffffffu, req);
+      while (rm) {   // warp-cooperative cp.async of the requested records
+        const int k = __ffs(rm) - 1;
+        rm &= rm - 1;
+        const NRec rv = S.sreq[k];
+        const int sl = S.sreq_slot[k];
+        const int no = min(rv.oe - rv.ob, SO), ni = min(rv.ie - rv.ib, SI);
+        if (lane < 2 * no) {
+          cp16(reinterpret_cast<int4 *>(&S.st_out[k][sl][lane >> 1]) + (lane & 1),
+               reinterpret_cast<const int4 *>(G.erec + rv.ob + (lane >> 1)) + (lane & 1));
+        } else if (lane < 2 * no + ni) {
+          cp16(&S.st_in[k][sl][lane - 2 * no], G.irec + rv.ib + (lane - 2 * no));
+        }
+      }
+      cp_commit();
+      // (6) peak after all changes of this round
+      if (dl) pk = max(pk, read_mem(S.memlo, S.memhi, lane));
+      if (!__any_sync(0xffffffffu, zero)) break;
+    }
+  }
+  cp_wait0();
+  mk = __reduce_max_sync(0xffffffffu, mk);
+  dispatched = __reduce_add_sync(0xffffffffu, dispatched);
+  int oom = 0;
+  if (dl) {
+    oom = pk > T.cap[lane];
+    if (peak_out) peak_out[(size_t)b * d + lane] = pk;
+    if (busy_out) busy_out[(size_t)b * d + lane] = mybusy;
+  }
+  if (dbg == 2 && busy_out && lane == 0) {   // diagnostics: instants / rounds
+    busy_out[(size_t)b * d] = n_inst;
+    if (d > 1) busy_out[(size_t)b * d + 1] = n_round;
+  }
+  oom = __reduce_or_sync(0xffffffffu, oom);
+  if (lane == 0) {
+    gdp_sim_report R = empty_report();
     R.makespan = mk;
     R.cross_bytes = cross;
     R.violation = (flag & 1) ? 1 : (oom ? 2 : 0);
@@ -511,11 +843,14 @@ bool launch_cost2(const Cost2Graph &G, const TopoArgs &T, const uint8_t *D, int 
   static size_t configured = 0;
   if (smem > 40 * 1024 && smem > configured) {
     cudaFuncSetAttribute(k_cost2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_cost3, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     configured = smem;
   }
   note_launch();
   static const int dbg = getenv("GDP_COST_DBG") ? atoi(getenv("GDP_COST_DBG")) : 0;
-  k_cost2<<<B, 32, smem, s>>>(G, T, D, scratch, per_place, rep, peak, busy, reward, dbg);
+  static const bool v2 = getenv("GDP_COST_V2") != nullptr;   // owner-lane kernel (comparison)
+  if (v2) k_cost2<<<B, 32, smem, s>>>(G, T, D, scratch, per_place, rep, peak, busy, reward, dbg);
+  else k_cost3<<<B, 32, smem, s>>>(G, T, D, scratch, per_place, rep, peak, busy, reward, dbg);
   return true;
 }
 
