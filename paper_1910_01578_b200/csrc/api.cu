@@ -157,7 +157,8 @@ bool ws_layout(const gdp_graph_s *g, int d, int B, char *base, WS *w) {
   // cost scratch: one region per placement, large enough for either cost kernel
   size_t v1 = (2 + 2) * N * sizeof(int) + N * sizeof(int2) + E * sizeof(int4) + N * sizeof(int);
   size_t v2 = cost2_scratch_per_placement(g->N, g->E, g->nbig);
-  z.c_per_place = (std::max(v1, v2) + 255) & ~(size_t)255;
+  size_t v4 = cost4_scratch_per_placement(g->N, g->E, g->nbig);
+  z.c_per_place = (std::max(std::max(v1, v2), v4) + 255) & ~(size_t)255;
   z.c_scratch = reinterpret_cast<unsigned char *>(take(Bc * z.c_per_place));
   if (z.c_scratch) {
     // v1 view of the same bytes
@@ -335,7 +336,9 @@ gdp_status gdp_graph_create(int32_t N, int32_t F, const float *feat, int64_t E, 
   for (int i = 0; i < N; i++)
     if (order[i] != i) ident = false;
   g->perm_identity = ident;
+  g->min_cost = N > 0 ? INT_MAX : 0;
   for (int v = 0; v < N; v++) {
+    g->min_cost = std::min(g->min_cost, (int)cost[v]);
     g->max_indeg = std::max(g->max_indeg, iptr[v + 1] - iptr[v]);
     g->max_outdeg = std::max(g->max_outdeg, optr[v + 1] - optr[v]);
   }
@@ -350,7 +353,6 @@ gdp_status gdp_graph_create(int32_t N, int32_t F, const float *feat, int64_t E, 
   for (int64_t e = 0; e < E; e++) {
     erec[(size_t)e] = nrec[oidx[(size_t)e]];
     irec[(size_t)e].u = iidx[(size_t)e];
-    irec[(size_t)e].pad = 0;
     irec[(size_t)e].bytes = output_bytes[iidx[(size_t)e]];
   }
   std::vector<unsigned> cnt0((N + 3) / 4, 0u);
@@ -368,6 +370,14 @@ gdp_status gdp_graph_create(int32_t N, int32_t F, const float *feat, int64_t E, 
     // a big node keeps the sentinel in BOTH nibbles so that both counters use the global path
     if (bigid[v] >= 0) { nib_in = 15; nib_out = 15; }
     cnt0[v >> 2] |= (nib_in | (nib_out << 4)) << ((v & 3) * 8);
+  }
+  // k_cost3 reads the counter kind from the records: NRec.cost bit 31 = op with global
+  // counters, IRec.pad = the producer's global counter index (or -1)
+  for (int v = 0; v < N; v++)
+    if (bigid[v] >= 0) nrec[v].cost |= (int)0x80000000u;
+  for (int64_t e = 0; e < E; e++) {
+    erec[(size_t)e] = nrec[oidx[(size_t)e]];
+    irec[(size_t)e].pad = bigid[iidx[(size_t)e]];
   }
   g->nbig = (int)big_in.size();
   if (big_in.empty()) { big_in.push_back(0); big_out.push_back(0); }

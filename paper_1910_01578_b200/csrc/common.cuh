@@ -55,6 +55,7 @@ struct gdp_graph_s {
   long long sum_edge_out_bytes = 0;                 // sum over edges of producer output bytes
   long long n_edges_cross_max = 0;
   int max_indeg = 0, max_outdeg = 0;
+  int min_cost = 0;   // smallest compute cost (k_cost4 needs every duration >= 1)
   // shared-memory cost model records (cost2.cuh)
   void *nrec = nullptr, *erec = nullptr, *irec = nullptr;
   unsigned *cnt0 = nullptr;
@@ -68,6 +69,7 @@ struct gdp_topo_s {
   int speed[8];
   long long bpt[64];
   int lat[64];
+  double inv_bpt[64];   // 1 / bpt (cost kernels: reciprocal estimate + exact fix-up)
 };
 
 // Topology passed by value to kernels
@@ -77,6 +79,7 @@ struct TopoArgs {
   int speed[8];
   long long bpt[64];
   int lat[64];
+  double inv_bpt[64];   // 1 / bpt (cost kernels: reciprocal estimate + exact fix-up)
 };
 
 namespace gdp {

@@ -405,7 +405,11 @@ gdp_status launch_cost(const gdp_graph_s *g, const gdp_topo_s *t, const uint8_t 
   TopoArgs T;
   T.d = t->d;
   for (int i = 0; i < 8; i++) { T.cap[i] = t->cap[i]; T.speed[i] = t->speed[i]; }
-  for (int i = 0; i < 64; i++) { T.bpt[i] = t->bpt[i]; T.lat[i] = t->lat[i]; }
+  for (int i = 0; i < 64; i++) {
+    T.bpt[i] = t->bpt[i];
+    T.lat[i] = t->lat[i];
+    T.inv_bpt[i] = t->bpt[i] > 0 ? 1.0 / (double)t->bpt[i] : 0.0;
+  }
   static const bool force_v1 = getenv("GDP_COST_V1") != nullptr;
   if (!force_v1) {
     Cost2Graph C;
@@ -415,6 +419,10 @@ gdp_status launch_cost(const gdp_graph_s *g, const gdp_topo_s *t, const uint8_t 
     C.cnt0 = g->cnt0; C.bigid = g->bigid; C.big_in = g->big_in; C.big_out = g->big_out; C.nbig = g->nbig;
     C.out_idx = g->out_idx; C.out_src = g->out_src; C.in_ptr = g->in_ptr; C.cost = g->cost; C.leader = g->leader;
     C.out_bytes = g->out_bytes; C.mem_bytes = g->mem_bytes; C.has_coloc = g->has_coloc ? 1 : 0;
+    if (launch_cost4(C, T, g->min_cost, D, B, w.c_scratch, w.c_per_place, rep, peak, busy, reward, s)) {
+      GDP_LAUNCH_CHECK("k_cost4");
+      return GDP_OK;
+    }
     if (launch_cost2(C, T, D, B, w.c_scratch, w.c_per_place, rep, peak, busy, reward, s)) {
       GDP_LAUNCH_CHECK("k_cost2");
       return GDP_OK;

@@ -22,22 +22,17 @@
 
 #include "common.cuh"
 #include "cost2.cuh"
+#include "cost_util.cuh"
 
 namespace gdp {
 namespace {
+using namespace cu;
 
 constexpr int SO = 8;     // staged out-edge records per slot
 constexpr int SI = 8;     // staged in-edge records per slot
 constexpr int KF = 4;     // FIFO entries kept in smem per device
 constexpr int KC = 4;     // channel entries kept in smem per channel
 constexpr int NINC = 32;  // per-device list of ops made available this round (overflow -> global)
-constexpr int INF = INT_MAX;
-
-struct __align__(16) Ent {   // FIFO entry (t = ready) / channel entry (t = arrival, bytes = copy size)
-  NRec r;
-  int t, pad;
-  long long bytes;
-};
 
 struct Smem {
   NRec st_out[8][2][SO];
@@ -48,6 +43,7 @@ struct Smem {
   NRec sreq[8];
   NRec run[8];                    // k_cost3: record of the op running on each device
   int run_slot[8];                // k_cost3: its staging slot
+  unsigned mw[3][8];              // k_cost3: resident bytes per device, 16 + 16 + 32 bits
   unsigned memlo[8], memhi[8];   // per-device resident bytes as two 32-bit words (native atomics)
   long long peak[8];
   int ch_head[8][8], ch_tail[8][8], ch_free[8][8], ch_arr[8][8], ch_off[8][8];
@@ -55,43 +51,6 @@ struct Smem {
   int inc_n[8], doff[8], sreq_slot[8];
 };
 
-__device__ __forceinline__ void cp16(void *s, const void *g) {
-  unsigned a = (unsigned)__cvta_generic_to_shared(s);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(a), "l"(g) : "memory");
-}
-__device__ __forceinline__ void cp_ent(Ent *s, const Ent *g) {
-  cp16(reinterpret_cast<int4 *>(s), g);
-  cp16(reinterpret_cast<int4 *>(s) + 1, reinterpret_cast<const int4 *>(g) + 1);
-  cp16(reinterpret_cast<int4 *>(s) + 2, reinterpret_cast<const int4 *>(g) + 2);
-}
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-__device__ __forceinline__ void cp_wait0() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
-__device__ __forceinline__ void cp_wait1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
-
-__device__ __forceinline__ void copy_rec(NRec *dst, const NRec *src) {
-  const int4 *s = reinterpret_cast<const int4 *>(src);
-  int4 *d = reinterpret_cast<int4 *>(dst);
-  d[0] = s[0];
-  d[1] = s[1];
-}
-__device__ __forceinline__ void store_ent(Ent *dst, const NRec &r, int t, long long bytes) {
-  int4 *d = reinterpret_cast<int4 *>(dst);
-  const int4 *s = reinterpret_cast<const int4 *>(&r);
-  d[0] = s[0];
-  d[1] = s[1];
-  d[2] = make_int4(t, 0, (int)(bytes & 0xffffffffLL), (int)(bytes >> 32));
-}
-__device__ __forceinline__ void load_rec(NRec &r, const NRec *src) {
-  const int4 *s = reinterpret_cast<const int4 *>(src);
-  int4 a = s[0], b = s[1];
-  r.id = a.x; r.cost = a.y; r.ob = a.z; r.oe = a.w; r.ib = b.x; r.ie = b.y;
-  r.bytes = ((long long)(unsigned)b.z) | ((long long)b.w << 32);
-}
-__device__ __forceinline__ long long warp_sum_ll(long long v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
-}
 // 64-bit add as two native 32-bit shared atomics: each add carries its own low-word wrap
 __device__ __forceinline__ void add_mem(unsigned *lo, unsigned *hi, int dev, long long v) {
   const unsigned a = (unsigned)((unsigned long long)v & 0xffffffffull);
@@ -103,7 +62,6 @@ __device__ __forceinline__ void add_mem(unsigned *lo, unsigned *hi, int dev, lon
 __device__ __forceinline__ long long read_mem(const unsigned *lo, const unsigned *hi, int dev) {
   return (long long)(((unsigned long long)hi[dev] << 32) | lo[dev]);
 }
-__device__ __forceinline__ int dev_of(const unsigned *Dn, int v) { return (Dn[v >> 3] >> ((v & 7) * 4)) & 15; }
 
 // decrement the 4-bit counter of v at nibble `hi` (0 = inputs, 1 = consumers); true iff it hits 0
 __device__ __forceinline__ bool dec_counter(unsigned *cnt, int v, int hi, int *bigc, const int *bigid, int nbig) {
@@ -468,7 +426,7 @@ __global__ void __launch_bounds__(32) k_cost2(Cost2Graph G, TopoArgs T, const ui
         if (!running && fhead < ftail) {
           Ent &e = S.fc[lane][fhead % KF];
           load_rec(run, &e.r);
-          const int dur = run.cost * T.speed[lane];
+          const int dur = (run.cost & 0x7fffffff) * T.speed[lane];
           running = 1;
           fin = t + dur;
           mk = max(mk, fin);
@@ -556,19 +514,67 @@ __global__ void __launch_bounds__(32) k_cost2(Cost2Graph G, TopoArgs T, const ui
 //    same channel are ranked with __match_any_sync, so their FIFO arrival times
 //    max(t, free) + (rank + 1) * xfer are computed in parallel (every transfer of one op on
 //    one channel has the same size, so the serial recurrence has this closed form);
-//  * lane q < d still owns device q: FIFO append, dispatch, staging requests, peak.
-__device__ __forceinline__ int pop_channel(Smem &S, const Ctx &C, const Cost2Graph &G, int c, int a, int t) {
+//  * per-device resident bytes are three 32-bit words (bits 0-15, 16-31, 32-63) updated with
+//    fire-and-forget shared reductions; the owner lane carries and samples them once per round;
+//  * lane q < d still owns device q: FIFO append, dispatch, staging of its records, peak.
+constexpr int MEM_NORM = 1024;   // adds per lane between carries (32 lanes x 1024 x 2^16 < 2^32)
+
+__device__ __forceinline__ void mem_carry_all(Smem &S) {   // atomic-safe carry of every device
+#pragma unroll
+  for (int q = 0; q < 8; q++) {
+    const unsigned o0 = atomicAnd(&S.mw[0][q], 0xffffu);
+    atomicAdd(&S.mw[1][q], o0 >> 16);
+    const unsigned o1 = atomicAnd(&S.mw[1][q], 0xffffu);
+    atomicAdd(&S.mw[2][q], o1 >> 16);
+  }
+}
+__device__ __forceinline__ void add_mem3(Smem &S, int dev, long long v, int &nadd) {
+  atomicAdd(&S.mw[0][dev], (unsigned)(v & 0xffff));
+  atomicAdd(&S.mw[1][dev], (unsigned)((v >> 16) & 0xffff));
+  atomicAdd(&S.mw[2][dev], (unsigned)(int)(v >> 32));
+  if (++nadd >= MEM_NORM) { mem_carry_all(S); nadd = 0; }
+}
+// owner of device q, no concurrent adders: value, normalised in place
+__device__ __forceinline__ long long mem_sample(Smem &S, int q) {
+  const unsigned w0 = S.mw[0][q], w1 = S.mw[1][q], w2 = S.mw[2][q];
+  const long long v = ((long long)(int)w2 << 32) + ((long long)w1 << 16) + (long long)w0;
+  S.mw[0][q] = (unsigned)(v & 0xffff);
+  S.mw[1][q] = (unsigned)((v >> 16) & 0xffff);
+  S.mw[2][q] = (unsigned)(int)(v >> 32);
+  return v;
+}
+// input counter of the op a record describes (cost bit 31 = global counters)
+__device__ __forceinline__ bool dec_in(unsigned *cnt, const NRec &r, int *bigc, const int *bigid) {
+  if (r.cost < 0) return atomicSub(&bigc[bigid[r.id]], 1) == 1;
+  const int sh = (r.id & 3) * 8;
+  return ((atomicSub(&cnt[r.id >> 2], 1u << sh) >> sh) & 15u) == 1u;
+}
+// consumer counter of an in-edge's producer (IRec.pad = its global counter index, or -1)
+__device__ __forceinline__ bool dec_out(unsigned *cnt, const IRec &ir, int *bigc, int nbig) {
+  if (ir.pad >= 0) return atomicSub(&bigc[ir.pad + nbig], 1) == 1;
+  const int sh = (ir.u & 3) * 8 + 4;
+  return ((atomicSub(&cnt[ir.u >> 2], 1u << sh) >> sh) & 15u) == 1u;
+}
+// a device lane stages the out-/in-edge records of op r into its slot sl
+__device__ __forceinline__ void stage_records(Smem &S, const Cost2Graph &G, int k, int sl, const NRec &r) {
+  const int no = min(r.oe - r.ob, SO), ni = min(r.ie - r.ib, SI);
+  const int4 *eo = reinterpret_cast<const int4 *>(G.erec + r.ob);
+  int4 *so = reinterpret_cast<int4 *>(&S.st_out[k][sl][0]);
+  for (int j = 0; j < 2 * no; j++) cp16(so + j, eo + j);
+  for (int j = 0; j < ni; j++) cp16(&S.st_in[k][sl][j], G.irec + r.ib + j);
+}
+
+__device__ __forceinline__ int pop_channel3(Smem &S, const Ctx &C, const Cost2Graph &G, int c, int a, int t,
+                                            int &head, int off, int &nadd) {
   const int q = c & 7;
   Ent *ring = &S.cc[0][0][0] + c * KC;
-  int head = (&S.ch_head[0][0])[c];
   const int tail = (&S.ch_tail[0][0])[c];
-  const int off = (&S.ch_off[0][0])[c];
   int popped = 0;
   while (a <= t) {
     if (popped) { cp_commit(); cp_wait0(); }   // the refill issued by the previous pop
     Ent &e = ring[head % KC];
-    add_mem(S.memlo, S.memhi, q, e.bytes);
-    if (dec_counter(C.cnt, e.r.id, 0, C.bigc, G.bigid, G.nbig)) push_inc(S, C.ov, q, e.r);
+    add_mem3(S, q, e.bytes, nadd);
+    if (dec_in(C.cnt, e.r, C.bigc, G.bigid)) push_inc(S, C.ov, q, e.r);
     if (head + KC < tail) cp_ent(&e, C.chq + off + head + KC);
     head++;
     popped = 1;
@@ -579,8 +585,8 @@ __device__ __forceinline__ int pop_channel(Smem &S, const Ctx &C, const Cost2Gra
   return a;
 }
 
-__device__ __forceinline__ void finish_op(Smem &S, const Ctx &C, const Cost2Graph &G, const TopoArgs &T,
-                                          int k, int t) {
+__device__ __forceinline__ void finish_op3(Smem &S, const Ctx &C, const Cost2Graph &G, const TopoArgs &T,
+                                           int k, int t, int &nadd) {
   const int lane = C.lane;
   NRec r;
   load_rec(r, &S.run[k]);
@@ -592,10 +598,10 @@ __device__ __forceinline__ void finish_op(Smem &S, const Ctx &C, const Cost2Grap
     if (j < SI) ir = S.st_in[k][sl][j];
     else ir = G.irec[r.ib + j];
     const int du = dev_of(C.Dn, ir.u);
-    if (du != k) add_mem(S.memlo, S.memhi, k, -ir.bytes);
-    if (dec_counter(C.cnt, ir.u, 1, C.bigc, G.bigid, G.nbig)) add_mem(S.memlo, S.memhi, du, -ir.bytes);
+    if (du != k) add_mem3(S, k, -ir.bytes, nadd);
+    if (dec_out(C.cnt, ir, C.bigc, G.nbig)) add_mem3(S, du, -ir.bytes, nadd);
   }
-  if (nout == 0 && lane == 0) add_mem(S.memlo, S.memhi, k, -r.bytes);
+  if (nout == 0 && lane == 0) add_mem3(S, k, -r.bytes, nadd);
   int *chf = &S.ch_free[0][0], *cht = &S.ch_tail[0][0], *chh = &S.ch_head[0][0], *cha = &S.ch_arr[0][0];
   const int *cho = &S.ch_off[0][0];
   for (int j0 = 0; j0 < nout; j0 += 32) {
@@ -609,22 +615,23 @@ __device__ __forceinline__ void finish_op(Smem &S, const Ctx &C, const Cost2Grap
       tw = dev_of(C.Dn, wr.id);
     }
     const bool cross = v && tw != k;
-    if (v && !cross && dec_counter(C.cnt, wr.id, 0, C.bigc, G.bigid, G.nbig)) push_inc(S, C.ov, k, wr);
+    if (v && !cross && dec_in(C.cnt, wr, C.bigc, G.bigid)) push_inc(S, C.ov, k, wr);
     if (__any_sync(0xffffffffu, cross)) {
       const unsigned grp = __match_any_sync(0xffffffffu, cross ? tw : -1);
       if (cross) {
         const int rank = __popc(grp & C.lt), n = __popc(grp);
         const int c = k * 8 + tw;
         const int f = chf[c];
-        const int x = xfer_time(r.bytes, k, tw, T);
+        const int x = xfer_time3(r.bytes, c, T);
         const int base = max(t, f);
         const int arr = base + (rank + 1) * x;
         if (arr == t) {   // zero-time transfers (x = 0, channel free): the copies land now
-          add_mem(S.memlo, S.memhi, tw, r.bytes);
-          if (dec_counter(C.cnt, wr.id, 0, C.bigc, G.bigid, G.nbig)) push_inc(S, C.ov, tw, wr);
+          add_mem3(S, tw, r.bytes, nadd);
+          if (dec_in(C.cnt, wr, C.bigc, G.bigid)) push_inc(S, C.ov, tw, wr);
           if (rank == 0) chf[c] = t;
         } else {
           const int head = chh[c], tail = cht[c], pos = tail + rank;
+          __syncwarp(grp);   // every rank has read the channel state before rank 0 moves it
           if (pos < head + KC) store_ent(&S.cc[0][0][0] + c * KC + pos % KC, wr, arr, r.bytes);
           else store_ent(C.chq + cho[c] + pos, wr, arr, r.bytes);
           if (rank == 0) {
@@ -652,35 +659,48 @@ __global__ void __launch_bounds__(32) k_cost3(Cost2Graph G, TopoArgs T, const ui
   long long mymem, mybusy, cross;
   if (!prologue(G, T, S, C, rep, peak_out, busy_out, reward, flag, mymem, mybusy, cross, ftail)) return;
   if (dbg == 1) return;
+  if (lane < 8) {
+    S.mw[0][lane] = (unsigned)(mymem & 0xffff);
+    S.mw[1][lane] = (unsigned)((mymem >> 16) & 0xffff);
+    S.mw[2][lane] = (unsigned)(int)(mymem >> 32);
+  }
+  __syncwarp();
   int fhead = 0;
   const bool dl = lane < d;
   const int c0 = 2 * lane, c1 = 2 * lane + 1;   // my channels (k = c / 8 -> q = c % 8)
   int ca0 = INF, ca1 = INF;                       // their head arrivals (channels start empty)
-  int fin = 0, running = 0, mk = 0, dispatched = 0;
+  int hd0 = 0, hd1 = 0;                           // their heads
+  const int of0 = (&S.ch_off[0][0])[c0], of1 = (&S.ch_off[0][0])[c1];
+  int fin = 0, running = 0, mk = 0, dispatched = 0, nadd = 0;
   int cur = 0, cur_inst = -2, nxt_id = -1, nxt_inst = -2;
   long long pk = mymem;
-  int t = 0, n_inst = 0, n_round = 0;
+  int t = 0, n_inst = 0, n_round = 0, n_need = 0;
+  long long tacc[6] = {0, 0, 0, 0, 0, 0}, tp = clock64();   // dbg == 3: cycles per phase
+#define PH(i) if (dbg == 3) { const long long tn = clock64(); tacc[i] += tn - tp; tp = tn; }
   for (int inst = 0;; inst++) {
     if (inst > 0) {
       const int cand = min(dl && running ? fin : INF, min(ca0, ca1));
       t = __reduce_min_sync(0xffffffffu, cand);
       if (t == INF) break;
     }
+    PH(0)
     {  // records staged at the previous instant may still be in flight
       const bool need = dl && running && fin == t && cur_inst == inst - 1;
-      if (__any_sync(0xffffffffu, need)) cp_wait0(); else cp_wait1();
+      if (__any_sync(0xffffffffu, need)) { cp_wait0(); n_need++; } else cp_wait1();
     }
     n_inst++;
     for (int round = 0;; round++) {
       n_round++;
       if (round > 0) cp_wait0();
       __syncwarp();
+      PH(1)
       // (1) copy arrivals due now, every channel owner in parallel (first round only)
       if (round == 0) {
-        if (ca0 <= t) ca0 = pop_channel(S, C, G, c0, ca0, t);
-        if (ca1 <= t) ca1 = pop_channel(S, C, G, c1, ca1, t);
+        if (ca0 <= t) ca0 = pop_channel3(S, C, G, c0, ca0, t, hd0, of0, nadd);
+        if (ca1 <= t) ca1 = pop_channel3(S, C, G, c1, ca1, t, hd1, of1, nadd);
         __syncwarp();
       }
+      PH(2)
       // (2) ops finishing now, each handled by the whole warp
       const bool fmine = dl && running && fin == t;
       unsigned fm = __ballot_sync(0xffffffffu, fmine);
@@ -688,12 +708,13 @@ __global__ void __launch_bounds__(32) k_cost3(Cost2Graph G, TopoArgs T, const ui
       while (fm) {
         const int k = __ffs(fm) - 1;
         fm &= fm - 1;
-        finish_op(S, C, G, T, k, t);
+        finish_op3(S, C, G, T, k, t, nadd);
       }
       __syncwarp();
+      PH(3)
       ca0 = (&S.ch_arr[0][0])[c0];
       ca1 = (&S.ch_arr[0][0])[c1];
-      bool zero = false, req = false;
+      bool zero = false;
       if (dl) {
         // (3) ops made available now (ready = t) join my FIFO in id order
         const int n = S.inc_n[lane];
@@ -741,15 +762,16 @@ __global__ void __launch_bounds__(32) k_cost3(Cost2Graph G, TopoArgs T, const ui
           S.inc_n[lane] = 0;
         }
         // (4) dispatch my FIFO head if idle
+        bool staged_now = false;
         if (!running && fhead < ftail) {
           Ent &e = S.fc[lane][fhead % KF];
           NRec run;
           load_rec(run, &e.r);
-          const int dur = run.cost * T.speed[lane];
+          const int dur = (run.cost & 0x7fffffff) * T.speed[lane];
           running = 1;
           fin = t + dur;
           mk = max(mk, fin);
-          add_mem(S.memlo, S.memhi, lane, run.bytes);
+          add_mem3(S, lane, run.bytes, nadd);
           zero = dur == 0;
           dispatched++;
           cur ^= 1;
@@ -759,45 +781,32 @@ __global__ void __launch_bounds__(32) k_cost3(Cost2Graph G, TopoArgs T, const ui
             cur_inst = nxt_inst;
           } else {                  // stage now
             cur_inst = inst;
-            copy_rec(&S.sreq[lane], &run);
-            S.sreq_slot[lane] = cur;
-            req = true;
+            stage_records(S, G, lane, cur, run);
+            staged_now = true;
           }
           nxt_id = -1;
           if (fhead + KF < ftail) cp_ent(&e, fifo + S.doff[lane] + fhead + KF);
           fhead++;
         }
         // (5) stage the records of the op now waiting at my FIFO head
-        if (running && nxt_id < 0 && fhead < ftail && !req) {
-          const NRec r = S.fc[lane][fhead % KF].r;
-          S.sreq[lane] = r;
-          S.sreq_slot[lane] = cur ^ 1;
+        if (running && nxt_id < 0 && fhead < ftail && !staged_now) {
+          NRec r;
+          load_rec(r, &S.fc[lane][fhead % KF].r);
+          stage_records(S, G, lane, cur ^ 1, r);
           nxt_id = r.id;
           nxt_inst = inst;
-          req = true;
-        }
-      }
-      __syncwarp();
-      unsigned rm = __ballot_sync(0xffffffffu, req);
-      while (rm) {   // warp-cooperative cp.async of the requested records
-        const int k = __ffs(rm) - 1;
-        rm &= rm - 1;
-        const NRec rv = S.sreq[k];
-        const int sl = S.sreq_slot[k];
-        const int no = min(rv.oe - rv.ob, SO), ni = min(rv.ie - rv.ib, SI);
-        if (lane < 2 * no) {
-          cp16(reinterpret_cast<int4 *>(&S.st_out[k][sl][lane >> 1]) + (lane & 1),
-               reinterpret_cast<const int4 *>(G.erec + rv.ob + (lane >> 1)) + (lane & 1));
-        } else if (lane < 2 * no + ni) {
-          cp16(&S.st_in[k][sl][lane - 2 * no], G.irec + rv.ib + (lane - 2 * no));
         }
       }
       cp_commit();
+      PH(4)
+      __syncwarp();
       // (6) peak after all changes of this round
-      if (dl) pk = max(pk, read_mem(S.memlo, S.memhi, lane));
+      if (dl) pk = max(pk, mem_sample(S, lane));
       if (!__any_sync(0xffffffffu, zero)) break;
     }
+    PH(5)
   }
+#undef PH
   cp_wait0();
   mk = __reduce_max_sync(0xffffffffu, mk);
   dispatched = __reduce_add_sync(0xffffffffu, dispatched);
@@ -810,6 +819,12 @@ __global__ void __launch_bounds__(32) k_cost3(Cost2Graph G, TopoArgs T, const ui
   if (dbg == 2 && busy_out && lane == 0) {   // diagnostics: instants / rounds
     busy_out[(size_t)b * d] = n_inst;
     if (d > 1) busy_out[(size_t)b * d + 1] = n_round;
+  }
+  if (dbg == 3 && busy_out && lane == 0)     // diagnostics: cycles per phase (d >= 6)
+    for (int i = 0; i < 6 && i < d; i++) busy_out[(size_t)b * d + i] = tacc[i];
+  if (dbg == 3 && busy_out && lane == 0 && d >= 8) {
+    busy_out[(size_t)b * d + 6] = n_need;
+    busy_out[(size_t)b * d + 7] = n_inst;
   }
   oom = __reduce_or_sync(0xffffffffu, oom);
   if (lane == 0) {

@@ -31,6 +31,11 @@ struct Cost2Graph {
 
 size_t cost2_smem_bytes(int N);
 size_t cost2_scratch_per_placement(int N, long long E, int nbig);
+size_t cost4_smem_bytes(int N);
+size_t cost4_scratch_per_placement(int N, long long E, int nbig);
+bool launch_cost4(const Cost2Graph &G, const TopoArgs &T, int min_cost, const uint8_t *D, int B,
+                  unsigned char *scratch, size_t per_place, gdp_sim_report *rep, long long *peak, long long *busy,
+                  double *reward, cudaStream_t s);
 bool launch_cost2(const Cost2Graph &G, const TopoArgs &T, const uint8_t *D, int B, unsigned char *scratch,
                   size_t per_place, gdp_sim_report *rep, long long *peak, long long *busy, double *reward,
                   cudaStream_t s);
