@@ -258,7 +258,7 @@ def main():
     # discrete-event loop per placement, bound by dependent ALU/shared-memory latency, so its
     # roofline is the SM issue rate: 148 SMs x 4 schedulers x 1 warp-instruction/clk.  The
     # warp-instructions one launch issues are measured once by ncu for this workload
-    # (profiles/r1_k_cost2_ncu.json, smsp__inst_executed.sum) and divided by the live CUDA-event
+    # (profiles/cost_kernel_ncu.json, smsp__inst_executed.sum) and divided by the live CUDA-event
     # launch time; the algorithmic units (N + E events per placement) are reported
     # beside it as events/s.  DESIGN.md §"Roofline of the cost model".
     pk = peaks()
@@ -267,17 +267,17 @@ def main():
     events_per_launch = sum(g.N + g.E for g in W.graphs) * W.batch / len(W.graphs)
     prof = {}
     try:
-        prof = json.load(open(os.path.join(ROOT, "profiles", "r1_k_cost2_ncu.json")))
+        prof = json.load(open(os.path.join(ROOT, "profiles", "cost_kernel_ncu.json")))
     except Exception:
         pass
     matched = prof.get("workload") == W.name and prof.get("batch") == W.batch
     inst = prof.get("warp_inst_per_launch") if matched else None
     traffic = (prof["dram_bytes_read_per_launch"] + prof["dram_bytes_write_per_launch"]) if matched else None
     achieved = (inst / (cost_avg / 1000.0) / 1e9) if inst else None
-    roof = {"kernel": "k_cost2", "bound": "alu", "achieved": achieved, "peak": peak_ginst, "unit": "Gwarp-inst/s",
+    roof = {"kernel": prof.get("kernel", "cost"), "bound": "alu", "achieved": achieved, "peak": peak_ginst, "unit": "Gwarp-inst/s",
             "frac": (achieved / peak_ginst) if achieved else None, "traffic": traffic,
             "peak_source": "148 SM x 4 issue/clk x sm_max_mhz (MEASURED_PEAKS.json)",
-            "inst_source": "ncu smsp__inst_executed.sum per launch (profiles/r1_k_cost2_ncu.json)" if inst else
+            "inst_source": "ncu smsp__inst_executed.sum per launch (profiles/cost_kernel_ncu.json)" if inst else
                            "no ncu count for this workload",
             "events_per_s": events_per_launch / (cost_avg / 1000.0),
             "launch_ms": cost_avg, "share_of_step": sum(cost_ms) / sum(times)}

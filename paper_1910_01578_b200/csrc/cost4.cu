@@ -41,10 +41,14 @@ struct Smem4 {
   Ent fc[8][KF4];
   Ent cc[64][KC4];                 // consumer-side prefetch ring of channel c = 8k + q
   NRec inc[8][NINC4];
+  NRec run[8];                     // record of the op running on each device
+  int run_slot[8];
   unsigned lb[R4][8][WMAX][3];     // device-warp memory deltas per window set / device / tick
   long long db[R4][8][WMAX];       // producer deaths (memory warp only)
   int cfree[64], ctail[64], cstamp[64];                        // producer side (warp k)
   int pfin[2][8], phead[2][64], pfirst[2][64], ptail[2][64];   // published per window parity
+  int phs[2][64];                  // consumer head at the start of window w (parity w & 1)
+  long long ploc[8];               // PROF: local cycles of each device warp in the window
   int coff[64], ccnt[64];
   int doff[8], ftail0[8], opcnt[8];
   long long stat[8], busyv[8];
@@ -105,6 +109,14 @@ __device__ __forceinline__ bool dec_out4(unsigned *cnt, const IRec &ir, int *big
   const int sh = (ir.u & 3) * 8 + 4;
   return ((atomicSub(&cnt[ir.u >> 2], 1u << sh) >> sh) & 15u) == 1u;
 }
+// the device lane stages the out-/in-edge records of op r into its slot sl
+__device__ __forceinline__ void stage_records4(Smem4 &S, const Cost2Graph &G, int q, int sl, const NRec &r) {
+  const int no = min(r.oe - r.ob, SO4), ni = min(r.ie - r.ib, SI4);
+  const int4 *eo = reinterpret_cast<const int4 *>(G.erec + r.ob);
+  int4 *so = reinterpret_cast<int4 *>(&S.st_out[q][sl][0]);
+  for (int j = 0; j < 2 * no; j++) cp16(so + j, eo + j);
+  for (int j = 0; j < ni; j++) cp16(&S.st_in[q][sl][j], G.irec + r.ib + j);
+}
 __device__ __forceinline__ void put_inc(Smem4 &S, NRec *ovq, int q, int pos, const NRec &r) {
   if (pos < NINC4) copy_rec(&S.inc[q][pos], &r);
   else copy_rec(ovq + pos, &r);
@@ -138,7 +150,7 @@ __global__ void __launch_bounds__(288, 2) k_cost4(Cost2Graph G, TopoArgs T, cons
   for (int i = tid; i < cwords; i += nthr) cnt[i] = G.cnt0[i];
   for (int j = tid; j < G.nbig; j += nthr) { bigc[j] = G.big_in[j]; bigc[G.nbig + j] = G.big_out[j]; }
   for (int v = tid; v < N; v += nthr) dtick[v] = -1;
-  if (tid < 64) { S.ccnt[tid] = 0; S.cstamp[tid] = -1; S.cfree[tid] = 0; S.ctail[tid] = 0; }
+  if (tid < 64) { S.ccnt[tid] = 0; S.cstamp[tid] = -1; S.cfree[tid] = 0; S.ctail[tid] = 0; S.phs[0][tid] = 0; }
   if (tid < 8) { S.stat[tid] = 0; S.busyv[tid] = 0; S.opcnt[tid] = 0; }
   if (tid == 0) {
     S.flag = 0; S.oom = 0; S.cross = 0; S.dq_tail = 0; S.mk = 0; S.disp = 0; S.nwin = 0;
@@ -267,45 +279,48 @@ __global__ void __launch_bounds__(288, 2) k_cost4(Cost2Graph G, TopoArgs T, cons
   if (warp < d) {
     // ---------------------------------------------------------------- device warp q
     const int q = warp;
-    const bool devl = lane == q;                 // FIFO / dispatch / finish bookkeeping
+    const bool devl = lane == q;                 // FIFO / dispatch / staging of device q
     const bool own = lane < d && lane != q;      // consumer of channel (lane -> q)
-    const bool stg = lane >= 8;                  // staging lanes: chunk lane - 8 of 24
     const int cin = 8 * lane + q;
     const int offc = own ? S.coff[cin] : 0;
-    int head = 0, tknown = 0, filled = 0, ha = INF;
+    Ent *ring = &S.cc[own ? cin : 0][0];
+    int head = 0, tknown = 0, filled = 0, ha = INF, hs = 0;
+    unsigned pend = 0;                           // ring slots with a prefetch in flight
     NRec *ovq = ov + S.doff[q];
     Ent *fq_g = fifo + S.doff[q];
     const int spd = T.speed[q];
     int fhead = 0, ftail = S.ftail0[q], running = 0, fin = 0, mk = 0, disp = 0;
-    NRec run;
-    run.id = -1; run.cost = 0; run.ob = run.oe = run.ib = run.ie = 0; run.bytes = 0;
     int cur = 0, cur_li = -2, nxt_id = -1, nxt_li = -2;
-    int li = 0, T0 = 0, w = 0;
-    long long c_local = 0, c_bar = 0, c_post = 0, c_mw = 0, c_a = 0, c_b = 0, tc = clock64();   // dbg == 3
+    int li = 0, T0 = 0, w = 0, memd = -1;
+    long long c_local = 0, c_bar = 0, c_post = 0, c_mw = 0, tc = clock64();   // PROF only
+    long long c_wall = 0, c_maxloc = 0, t_ws = 0, t_prev = clock64();
     long long cl[5] = {0, 0, 0, 0, 0}, tl = 0;
 #define PL(i) if (PROF) { const long long tn = clock64(); cl[i] += tn - tl; tl = tn; }
     for (;; w++) {
       const int set = w % R4;
-      if (w >= R4) {
+      if (w - R4 > memd) {   // the memory warp must have released this window set
         if (lane == 0)
-          while (ld_acq(&S.mem_done) < w - R4) { }
-        __syncwarp();
+          while ((memd = ld_acq(&S.mem_done)) < w - R4) { }
+        memd = __shfl_sync(FULL, memd, 0);
       }
-      if (PROF) { const long long tn = clock64(); c_mw += tn - tc; tc = tn; }
+      if (PROF) { const long long tn = clock64(); c_mw += tn - tc; tc = tn; t_ws = tn; c_wall += tn - t_prev; t_prev = tn; }
       if (q == 0 && lane == 0) S.Tw[set] = T0;
       if (lane < d) S.pfirst[w & 1][8 * q + lane] = INF;
       const int Tend = T0 + Wl;
       for (;;) {
-        // an idle device with a non-empty FIFO dispatches at once (only the sources at t = 0)
-        const int dc = running ? fin : (fhead < ftail ? T0 : INF);
-        const int cand = min(devl ? dc : INF, own ? ha : INF);
+        // key 2 tau (+1 unless my op finishes at tau); an idle device with a non-empty FIFO
+        // dispatches at once (only the sources at t = 0)
+        const unsigned NK = 0xffffffffu;
+        const unsigned dc = running ? 2u * (unsigned)fin : (fhead < ftail ? 2u * (unsigned)T0 + 1u : NK);
+        const unsigned cand = min(devl ? dc : NK, own && ha != INF ? 2u * (unsigned)ha + 1u : NK);
         if (PROF) tl = clock64();
-        const int tau = __reduce_min_sync(FULL, cand);
-        if (tau >= Tend) break;
-        const int fnow = __shfl_sync(FULL, (int)(devl && running && fin == tau), q);
-        const int need = __shfl_sync(FULL, (int)(devl && running && fin == tau && cur_li == li - 1), q);
-        if (stg) { if (need) cp_wait0(); else cp_wait1(); }
-        if (devl) cp_wait1();
+        const unsigned key = __reduce_min_sync(FULL, cand);
+        const int tau = (int)(key >> 1);
+        if (key == NK || tau >= Tend) break;
+        const bool fnow = (key & 1) == 0;
+        if (devl) {   // staged records / FIFO refills: everything older than the last instant
+          if (fnow && cur_li == li - 1) cp_wait0(); else cp_wait1();
+        }
         __syncwarp();
         long long delta = 0;
         int navail = 0;
@@ -315,44 +330,43 @@ __global__ void __launch_bounds__(288, 2) k_cost4(Cost2Graph G, TopoArgs T, cons
           bool av = false;
           NRec ar;
           if (own && ha == tau) {
-            cp_wait_n(filled - 1 - head);
-            Ent &e = S.cc[cin][head % KC4];
-            load_rec(ar, &e.r);
-            delta += e.bytes;
+            int s = head % KC4;
+            if (pend & (1u << s)) { cp_wait0(); pend = 0; }
+            load_rec(ar, &ring[s].r);
+            delta += ring[s].bytes;
             av = dec_in4(cnt, ar, bigc, G.bigid);
             head++;
-            if (filled < tknown) {
-              cp_ent(&S.cc[cin][filled % KC4], chq + offc + filled);
-              cp_commit();
-              filled++;
-            }
             if (head < tknown) {
-              cp_wait_n(filled - 1 - head);
-              ha = S.cc[cin][head % KC4].t;
+              s = head % KC4;
+              if (pend & (1u << s)) { cp_wait0(); pend = 0; }
+              ha = ring[s].t;
             } else {
               ha = INF;
             }
+            if (filled < tknown) {   // keep KC4 entries ahead
+              cp_ent(&ring[filled % KC4], chq + offc + filled);
+              cp_commit();
+              pend |= 1u << (filled % KC4);
+              filled++;
+            }
           }
           const unsigned m = __ballot_sync(FULL, av);
-          if (av) put_inc(S, ovq, q, navail + __popc(m & lt), ar);
-          navail += __popc(m);
+          if (av) put_inc(S, ovq, q, __popc(m & lt), ar);
+          navail = __popc(m);
         }
         PL(1)
         // (2) my op finishes now: its edges one per lane
         if (fnow) {
           if (devl) running = 0;
-          const int rid = __shfl_sync(FULL, run.id, q);
-          const int rob = __shfl_sync(FULL, run.ob, q), roe = __shfl_sync(FULL, run.oe, q);
-          const int rib = __shfl_sync(FULL, run.ib, q), rie = __shfl_sync(FULL, run.ie, q);
-          const long long rbytes = __shfl_sync(FULL, run.bytes, q);
-          const int sl = __shfl_sync(FULL, cur, q);
-          (void)rid;
-          const int nin = rie - rib, nout = roe - rob;
+          NRec r;
+          load_rec(r, &S.run[q]);
+          const int sl = S.run_slot[q];
+          const int nin = r.ie - r.ib, nout = r.oe - r.ob;
           // frees: copies this op held (local), producers whose last consumer it is (queued)
           for (int j = lane; j < nin; j += 32) {
             IRec ir;
             if (j < SI4) ir = S.st_in[q][sl][j];
-            else ir = G.irec[rib + j];
+            else ir = G.irec[r.ib + j];
             if (dev_of(Dn, ir.u) != q) delta -= ir.bytes;
             atomicMax(&dtick[ir.u], tau);
             if (dec_out4(cnt, ir, bigc, G.nbig)) {
@@ -360,7 +374,7 @@ __global__ void __launch_bounds__(288, 2) k_cost4(Cost2Graph G, TopoArgs T, cons
               dq[i] = make_int4(ir.u, 0, (int)(ir.bytes & 0xffffffffLL), (int)(ir.bytes >> 32));
             }
           }
-          if (nout == 0 && lane == 0) delta -= rbytes;
+          if (nout == 0 && lane == 0) delta -= r.bytes;
           for (int j0 = 0; j0 < nout; j0 += 32) {
             const int j = j0 + lane;
             const bool v = j < nout;
@@ -368,7 +382,7 @@ __global__ void __launch_bounds__(288, 2) k_cost4(Cost2Graph G, TopoArgs T, cons
             int tw = -1;
             if (v) {
               if (j < SO4) wr = S.st_out[q][sl][j];
-              else load_rec(wr, G.erec + rob + j);
+              else load_rec(wr, G.erec + r.ob + j);
               tw = dev_of(Dn, wr.id);
             }
             const bool cross = v && tw != q;
@@ -376,17 +390,23 @@ __global__ void __launch_bounds__(288, 2) k_cost4(Cost2Graph G, TopoArgs T, cons
             const unsigned m = __ballot_sync(FULL, avs);
             if (avs) put_inc(S, ovq, q, navail + __popc(m & lt), wr);
             navail += __popc(m);
-            if (__any_sync(FULL, cross)) {
-              const unsigned grp = __match_any_sync(FULL, cross ? tw : -1);
+            const unsigned cm = __ballot_sync(FULL, cross);
+            if (cm) {
+              const unsigned grp = (cm & (cm - 1)) ? __match_any_sync(FULL, cross ? tw : -1) : cm;
               if (cross) {
                 const int rank = __popc(grp & lt), n = __popc(grp);
                 const int c = 8 * q + tw;
                 const int f = S.cfree[c];
-                const int x = xfer_time3(rbytes, c, T);
+                const int x = xfer_time3(r.bytes, c, T);
                 const int bs = max(tau, f);
                 const int tail = S.ctail[c];
+                const int chs = S.phs[w & 1][c];
                 __syncwarp(grp);   // every rank has read the channel state before rank 0 moves it
-                store_ent(chq + S.coff[c] + tail + rank, wr, bs + (rank + 1) * x, rbytes);
+                const int pos = tail + rank, arr = bs + (rank + 1) * x;
+                // the consumer consumed position pos - KC4 before this window: its ring slot is
+                // free, so the entry goes straight there; otherwise to global for a later prefetch
+                if (pos < chs + KC4) store_ent(&S.cc[c][pos % KC4], wr, arr, r.bytes);
+                else store_ent(chq + S.coff[c] + pos, wr, arr, r.bytes);
                 if (rank == 0) {
                   S.cfree[c] = bs + n * x;
                   S.ctail[c] = tail + n;
@@ -397,15 +417,13 @@ __global__ void __launch_bounds__(288, 2) k_cost4(Cost2Graph G, TopoArgs T, cons
             }
           }
         }
-        __syncwarp();
         PL(2)
-        // (3) device lane: ops made available now join the FIFO in id order; dispatch
-        int stage = 0, s_slot = 0;
-        NRec sr;
+        __syncwarp();
+        // (3) device lane: ops made available now join the FIFO in id order; dispatch; stage
         if (devl) {
           const int n = navail;
+          NRec *Li = &S.inc[q][0];
           if (n > 0) {
-            NRec *Li = &S.inc[q][0];
             for (int i = 1; i < n; i++) {   // insertion sort by id (n is small except after wide fan-outs)
               NRec key;
               load_rec(key, i < NINC4 ? &Li[i] : &ovq[i]);
@@ -419,14 +437,16 @@ __global__ void __launch_bounds__(288, 2) k_cost4(Cost2Graph G, TopoArgs T, cons
               copy_rec(j + 1 < NINC4 ? &Li[j + 1] : &ovq[j + 1], &key);
             }
             for (int i = 0; i < n; i++) {
-              const NRec &r = i < NINC4 ? Li[i] : ovq[i];
-              if (ftail < fhead + KF4) store_ent(&S.fc[q][ftail % KF4], r, tau, 0);
-              else store_ent(fq_g + ftail, r, tau, 0);
+              const NRec &rr = i < NINC4 ? Li[i] : ovq[i];
+              if (ftail < fhead + KF4) store_ent(&S.fc[q][ftail % KF4], rr, tau, 0);
+              else store_ent(fq_g + ftail, rr, tau, 0);
               ftail++;
             }
           }
+          bool staged = false;
           if (!running && fhead < ftail) {
             Ent &e = S.fc[q][fhead % KF4];
+            NRec run;
             load_rec(run, &e.r);
             running = 1;
             fin = tau + (run.cost & 0x7fffffff) * spd;
@@ -434,40 +454,29 @@ __global__ void __launch_bounds__(288, 2) k_cost4(Cost2Graph G, TopoArgs T, cons
             delta += run.bytes;
             disp++;
             cur ^= 1;
+            copy_rec(&S.run[q], &run);
+            S.run_slot[q] = cur;
             if (run.id == nxt_id) {   // its records were staged while it waited
               cur_li = nxt_li;
             } else {
               cur_li = li;
-              stage = 1; s_slot = cur; sr = run;
+              stage_records4(S, G, q, cur, run);
+              staged = true;
             }
             nxt_id = -1;
             if (fhead + KF4 < ftail) cp_ent(&e, fq_g + fhead + KF4);
             fhead++;
           }
-          if (!stage && running && nxt_id < 0 && fhead < ftail) {   // stage the op waiting at the head
+          if (!staged && running && nxt_id < 0 && fhead < ftail) {   // stage the op waiting at the head
+            NRec sr;
             load_rec(sr, &S.fc[q][fhead % KF4].r);
-            stage = 1; s_slot = cur ^ 1;
+            stage_records4(S, G, q, cur ^ 1, sr);
             nxt_id = sr.id;
             nxt_li = li;
           }
           cp_commit();
         }
         PL(3)
-        if (__shfl_sync(FULL, stage, q)) {
-          const int sob = __shfl_sync(FULL, sr.ob, q), soe = __shfl_sync(FULL, sr.oe, q);
-          const int sib = __shfl_sync(FULL, sr.ib, q), sie = __shfl_sync(FULL, sr.ie, q);
-          const int ss = __shfl_sync(FULL, s_slot, q);
-          if (stg) {
-            const int ci = lane - 8;
-            const int no = min(soe - sob, SO4), ni = min(sie - sib, SI4);
-            if (ci < 2 * no)
-              cp16(reinterpret_cast<int4 *>(&S.st_out[q][ss][ci >> 1]) + (ci & 1),
-                   reinterpret_cast<const int4 *>(G.erec + sob + (ci >> 1)) + (ci & 1));
-            else if (ci - 2 * no < ni)
-              cp16(&S.st_in[q][ss][ci - 2 * no], G.irec + sib + (ci - 2 * no));
-          }
-        }
-        if (stg) cp_commit();
         // (4) my memory delta at tau
         if (delta != 0) add3(&S.lb[set][q][tau - T0][0], delta);
         li++;
@@ -475,16 +484,23 @@ __global__ void __launch_bounds__(288, 2) k_cost4(Cost2Graph G, TopoArgs T, cons
       }
       // publish the end-of-window state, meet, and find the next window start
       if (devl) S.pfin[w & 1][q] = running ? fin : INF;
-      if (own) S.phead[w & 1][cin] = ha;
+      if (own) {
+        S.phead[w & 1][cin] = ha;
+        S.phs[(w + 1) & 1][cin] = head;
+      }
       if (lane < d) S.ptail[w & 1][8 * q + lane] = S.ctail[8 * q + lane];
-      if (PROF) { const long long tn = clock64(); c_local += tn - tc; tc = tn; }
+      if (PROF) { const long long tn = clock64(); c_local += tn - tc; tc = tn; if (lane == 0) S.ploc[q] = tn - t_ws; }
       bar_devices(32 * d);   // bar.sync orders the window's shared and global writes for all device warps
-      if (PROF) { const long long tn = clock64(); c_bar += tn - tc; tc = tn; }
-      if (q == 0 && lane == 0) {
+      if (PROF) {
+        const long long tn = clock64(); c_bar += tn - tc; tc = tn;
+        long long mx = 0;
+        for (int k = 0; k < d; k++) mx = max(mx, S.ploc[k]);
+        c_maxloc += mx;
+      }
+      if (q == 0 && lane == 31) {   // a lane that rarely has global writes in flight (release fence)
         S.dq_end[set] = S.dq_tail;
         st_rel(&S.win_done, w);
       }
-      if (PROF) { const long long tn = clock64(); c_a += tn - tc; tc = tn; }
       int cand = lane < d ? S.pfin[w & 1][lane] : INF;
 #pragma unroll
       for (int h = 0; h < 2; h++) {
@@ -495,25 +511,24 @@ __global__ void __launch_bounds__(288, 2) k_cost4(Cost2Graph G, TopoArgs T, cons
         }
       }
       const int Tn = __reduce_min_sync(FULL, cand);
-      if (PROF) { const long long tn = clock64(); c_b += tn - tc; tc = tn; }
       if (own) {   // my channel: entries pushed in this window
         const int tn = S.ptail[w & 1][cin];
         if (ha == INF && tn > tknown) ha = S.pfirst[w & 1][cin];
-        tknown = tn;
-        while (filled < tknown && filled < head + KC4) {
-          cp_ent(&S.cc[cin][filled % KC4], chq + offc + filled);
+        const int lim = min(tn, head + KC4);
+        for (; filled < lim; filled++) {
+          if (filled >= tknown && filled < hs + KC4) continue;   // the producer wrote it into the ring
+          cp_ent(&ring[filled % KC4], chq + offc + filled);
           cp_commit();
-          filled++;
+          pend |= 1u << (filled % KC4);
         }
+        tknown = tn;
+        hs = head;
       }
       if (PROF) { const long long tn = clock64(); c_post += tn - tc; tc = tn; }
       if (Tn == INF) break;
       T0 = Tn;
     }
-    if (dbg == 3 && busy_out && lane == 0 && d == 8 && q == 1) {
-      long long *o = busy_out + (size_t)b * d;
-      o[0] = c_local; o[1] = cl[0]; o[2] = cl[1]; o[3] = cl[2]; o[4] = cl[3]; o[5] = cl[4]; o[6] = li; o[7] = w + 1;
-    }
+#undef PL
     cp_wait0();
     if (devl) {
       atomicMax(&S.mk, mk);
@@ -522,6 +537,10 @@ __global__ void __launch_bounds__(288, 2) k_cost4(Cost2Graph G, TopoArgs T, cons
     if (q == 0 && lane == 0) {
       S.nwin = w + 1;
       st_rel(&S.dev_done, 1);
+    }
+    if (PROF && busy_out && lane == 0 && d == 8 && q == 1) {
+      long long *o = busy_out + (size_t)b * d;
+      o[0] = c_wall; o[1] = c_maxloc; o[2] = c_local; o[3] = cl[2]; o[4] = cl[3]; o[5] = c_bar; o[6] = c_post + c_mw; o[7] = li;
     }
   } else {
     // ---------------------------------------------------------------- memory warp
