@@ -225,6 +225,14 @@ gdp_status gdp_cost(gdp_graph g, gdp_topo t, const uint8_t *placements, int32_t 
                     int64_t *peak_mem, int64_t *busy, double *reward, void *ws, size_t ws_bytes,
                     void *stream);
 
+/* Diagnostic: which cost kernel gdp_cost runs for this graph and topology (host only, no
+ * launch): 4 = windowed one-warp-per-device kernel (every duration >= 1 tick and every
+ * cross-device latency >= 1 tick), 3 = warp-cooperative instant-by-instant kernel,
+ * 2 = owner-lane kernel (GDP_COST_V2 set), 1 = global-memory kernel (per-placement state
+ * larger than shared memory, or GDP_COST_V1 set).  All four compute the same integers
+ * (DESIGN.md §"Cost model").  Returns 0 and sets the error for NULL handles. */
+int32_t gdp_cost_kernel(gdp_graph g, gdp_topo t);
+
 /* Advantage ("average reward of all the previous trials as a bias term"):
  * for b = 0..B-1 in order, adv[b] = (count == 0) ? 0 : reward[b] - sum / count, then
  * sum += reward[b], count += 1.  One state per graph.

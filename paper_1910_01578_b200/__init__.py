@@ -24,7 +24,7 @@ STATUS = {0: "GDP_OK", 1: "GDP_ERR_ARG", 2: "GDP_ERR_GRAPH", 3: "GDP_ERR_CYCLE",
 P_COUNT = 90
 REPORT_BYTES = 24
 
-EXPORTS = ["gdp_default_config", "gdp_last_error", "gdp_launch_count", "gdp_build_info", "gdp_graph_validate", "gdp_graph_create", "gdp_graph_destroy",
+EXPORTS = ["gdp_default_config", "gdp_last_error", "gdp_launch_count", "gdp_build_info", "gdp_cost_kernel", "gdp_graph_validate", "gdp_graph_create", "gdp_graph_destroy",
            "gdp_topo_create", "gdp_topo_destroy", "gdp_param_layout", "gdp_workspace_size", "gdp_embed",
            "gdp_place", "gdp_sample", "gdp_cost", "gdp_advantage", "gdp_policy_grad"]
 
@@ -75,6 +75,8 @@ def lib():
         L.gdp_launch_count.argtypes = []
         L.gdp_build_info.restype = ctypes.c_char_p
         L.gdp_build_info.argtypes = []
+        L.gdp_cost_kernel.restype = ctypes.c_int32
+        L.gdp_cost_kernel.argtypes = [P, P]
         L.gdp_last_error.restype = ctypes.c_char_p
         L.gdp_last_error.argtypes = []
         _lib = L
@@ -204,6 +206,15 @@ def gdp_sample(g: Graph, cfg: Config, logits, B: int, seed: int, sample_offset: 
     _check(lib().gdp_sample(g.h, ctypes.byref(cfg), _t_ptr(logits), B, seed, sample_offset, step,
                             _t_ptr(placements), _t_ptr(logprob), _t_ptr(ws), ws.numel(), _stream(stream)),
            "gdp_sample")
+
+
+def cost_kernel(g: Graph, t: Topo) -> int:
+    """Which cost kernel gdp_cost runs for (g, t): 4 windowed, 3 warp-cooperative, 2 owner-lane,
+    1 global-memory (include/gdp.h gdp_cost_kernel)."""
+    k = int(lib().gdp_cost_kernel(g.h, t.h))
+    if k == 0:
+        raise RuntimeError("gdp_cost_kernel: " + last_error())
+    return k
 
 
 def gdp_cost(g: Graph, t: Topo, placements, B: int, rep, peak_mem, busy, reward, ws, stream=None):

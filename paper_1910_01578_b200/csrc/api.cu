@@ -209,6 +209,11 @@ uint64_t gdp_launch_count(void) { return g_launches.load(std::memory_order_relax
 
 const char *gdp_build_info(void) { return "libgdp sm_100a built " __DATE__ " " __TIME__; }
 
+int32_t gdp_cost_kernel(gdp_graph g, gdp_topo t) {
+  if (!g || !t) { set_error("gdp_cost_kernel: NULL handle"); return 0; }
+  return cost_kernel_choice(g, t);
+}
+
 gdp_status gdp_default_config(int32_t d, gdp_config *out) {
   if (!out) return fail(GDP_ERR_ARG, "out is NULL");
   if (d < 1 || d > kMaxD) return fail(GDP_ERR_ARG, "d must be in 1..8");

@@ -188,6 +188,7 @@ void launch_logit_grad(const float *logits, const uint8_t *D, const int *leader,
                        int N, int d, int B, double *wb, float *dlog, cudaStream_t s);
 
 // cost model
+int cost_kernel_choice(const gdp_graph_s *g, const gdp_topo_s *t);
 gdp_status launch_cost(const gdp_graph_s *g, const gdp_topo_s *t, const uint8_t *D, int B,
                        gdp_sim_report *rep, long long *peak, long long *busy, double *reward, const WS &w,
                        cudaStream_t s);

@@ -400,8 +400,7 @@ __global__ void k_advantage(const double *r, int B, double *sum, long long *cnt,
 
 }  // namespace
 
-gdp_status launch_cost(const gdp_graph_s *g, const gdp_topo_s *t, const uint8_t *D, int B, gdp_sim_report *rep,
-                       long long *peak, long long *busy, double *reward, const WS &w, cudaStream_t s) {
+static TopoArgs topo_args(const gdp_topo_s *t) {
   TopoArgs T;
   T.d = t->d;
   for (int i = 0; i < 8; i++) { T.cap[i] = t->cap[i]; T.speed[i] = t->speed[i]; }
@@ -410,6 +409,20 @@ gdp_status launch_cost(const gdp_graph_s *g, const gdp_topo_s *t, const uint8_t 
     T.lat[i] = t->lat[i];
     T.inv_bpt[i] = t->bpt[i] > 0 ? 1.0 / (double)t->bpt[i] : 0.0;
   }
+  return T;
+}
+
+int cost_kernel_choice(const gdp_graph_s *g, const gdp_topo_s *t) {
+  if (getenv("GDP_COST_V1") != nullptr) return 1;
+  const TopoArgs T = topo_args(t);
+  if (cost4_window(T, g->min_cost, g->N) > 0) return 4;
+  if (cost2_smem_bytes(g->N) <= 227 * 1024) return getenv("GDP_COST_V2") != nullptr ? 2 : 3;
+  return 1;
+}
+
+gdp_status launch_cost(const gdp_graph_s *g, const gdp_topo_s *t, const uint8_t *D, int B, gdp_sim_report *rep,
+                       long long *peak, long long *busy, double *reward, const WS &w, cudaStream_t s) {
+  const TopoArgs T = topo_args(t);
   static const bool force_v1 = getenv("GDP_COST_V1") != nullptr;
   if (!force_v1) {
     Cost2Graph C;

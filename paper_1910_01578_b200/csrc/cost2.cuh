@@ -32,6 +32,7 @@ struct Cost2Graph {
 size_t cost2_smem_bytes(int N);
 size_t cost2_scratch_per_placement(int N, long long E, int nbig);
 size_t cost4_smem_bytes(int N);
+int cost4_window(const TopoArgs &T, int min_cost, int N);   // window length, 0 = not eligible
 size_t cost4_scratch_per_placement(int N, long long E, int nbig);
 bool launch_cost4(const Cost2Graph &G, const TopoArgs &T, int min_cost, const uint8_t *D, int B,
                   unsigned char *scratch, size_t per_place, gdp_sim_report *rep, long long *peak, long long *busy,

@@ -126,7 +126,7 @@ template <bool PROF>
 __global__ void __launch_bounds__(288, 2) k_cost4(Cost2Graph G, TopoArgs T, const uint8_t *__restrict__ Dall,
                                                   unsigned char *scratch, size_t per_place, gdp_sim_report *rep,
                                                   long long *peak_out, long long *busy_out, double *reward, int Wl,
-                                                  int dbg) {
+                                                  int dbg, unsigned msleep) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Smem4 &S = *reinterpret_cast<Smem4 *>(smem_raw);
   const int N = G.N, d = T.d, b = blockIdx.x;
@@ -554,7 +554,10 @@ __global__ void __launch_bounds__(288, 2) k_cost4(Cost2Graph G, TopoArgs T, cons
       }
       wd = __shfl_sync(FULL, wd, 0);
       fin_all = __shfl_sync(FULL, fin_all, 0);
-      if (wd > done_w) {
+      if (wd > done_w && dbg == 4) {   // timing experiment: release the sets without memory work
+        if (lane == 0) st_rel(&S.mem_done, wd);
+        done_w = wd;
+      } else if (wd > done_w) {
         // producer deaths queued in windows done_w+1 .. wd
         const int dq_stop = S.dq_end[wd % R4];
         for (int i = dq_start + lane; i < dq_stop; i += 32) {
@@ -588,7 +591,7 @@ __global__ void __launch_bounds__(288, 2) k_cost4(Cost2Graph G, TopoArgs T, cons
       } else if (fin_all && done_w == S.nwin - 1) {
         break;
       } else {
-        __nanosleep(32);
+        __nanosleep(msleep);
       }
     }
     if (lane < d) {
@@ -616,23 +619,30 @@ __global__ void __launch_bounds__(288, 2) k_cost4(Cost2Graph G, TopoArgs T, cons
 size_t cost4_smem_bytes(int N) { return sizeof(Smem4) + 4 * (size_t)((N + 3) / 4) + 4 * (size_t)((N + 7) / 8); }
 size_t cost4_scratch_per_placement(int N, long long E, int nbig) { return scratch4_layout(N, E, nbig).total; }
 
-bool launch_cost4(const Cost2Graph &G, const TopoArgs &T, int min_cost, const uint8_t *D, int B,
-                  unsigned char *scratch, size_t per_place, gdp_sim_report *rep, long long *peak, long long *busy,
-                  double *reward, cudaStream_t s) {
+int cost4_window(const TopoArgs &T, int min_cost, int N) {
   static const bool off = getenv("GDP_COST_V3") != nullptr || getenv("GDP_COST_V2") != nullptr;
-  if (off) return false;
+  if (off) return 0;
   const int d = T.d;
-  if (d < 1 || d > 8 || min_cost < 1) return false;
+  if (d < 1 || d > 8 || min_cost < 1) return 0;   // zero-duration ops need same-instant rounds
   int L = WMAX;
   for (int k = 0; k < d; k++) {
-    if (T.speed[k] < 1) return false;
+    if (T.speed[k] < 1) return 0;
     for (int q = 0; q < d; q++)
       if (k != q) L = L < T.lat[k * 8 + q] ? L : T.lat[k * 8 + q];
   }
+  if (L < 1) return 0;                           // a transfer could land in its own window
+  if (cost4_smem_bytes(N) > 227 * 1024) return 0;
+  return L;
+}
+
+bool launch_cost4(const Cost2Graph &G, const TopoArgs &T, int min_cost, const uint8_t *D, int B,
+                  unsigned char *scratch, size_t per_place, gdp_sim_report *rep, long long *peak, long long *busy,
+                  double *reward, cudaStream_t s) {
+  const int L = cost4_window(T, min_cost, G.N);
   if (L < 1) return false;
   if (per_place < cost4_scratch_per_placement(G.N, G.E, G.nbig)) return false;
+  const int d = T.d;
   const size_t smem = cost4_smem_bytes(G.N);
-  if (smem > 227 * 1024) return false;
   static size_t configured = 0;
   if (smem > 40 * 1024 && smem > configured) {
     cudaFuncSetAttribute(k_cost4<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -642,8 +652,11 @@ bool launch_cost4(const Cost2Graph &G, const TopoArgs &T, int min_cost, const ui
   static_assert(2 * SO4 + SI4 == 24, "24 staging lanes");
   static const int dbg = getenv("GDP_COST_DBG") ? atoi(getenv("GDP_COST_DBG")) : 0;
   note_launch();
-  if (dbg == 3) k_cost4<true><<<B, 32 * (d + 1), smem, s>>>(G, T, D, scratch, per_place, rep, peak, busy, reward, L, dbg);
-  else k_cost4<false><<<B, 32 * (d + 1), smem, s>>>(G, T, D, scratch, per_place, rep, peak, busy, reward, L, dbg);
+  static const unsigned msleep = getenv("GDP_COST_MSLEEP") ? (unsigned)atoi(getenv("GDP_COST_MSLEEP")) : 200u;
+  if (dbg == 3)
+    k_cost4<true><<<B, 32 * (d + 1), smem, s>>>(G, T, D, scratch, per_place, rep, peak, busy, reward, L, dbg, msleep);
+  else
+    k_cost4<false><<<B, 32 * (d + 1), smem, s>>>(G, T, D, scratch, per_place, rep, peak, busy, reward, L, dbg, msleep);
   return true;
 }
 

@@ -23,13 +23,13 @@ def built():
 
 def header_functions():
     txt = open(os.path.join(ROOT, "include", "gdp.h")).read()
-    return sorted(set(re.findall(r"^(?:gdp_status|const char \*|uint64_t)\s*(gdp_\w+)\s*\(", txt, re.M)))
+    return sorted(set(re.findall(r"^(?:gdp_status|const char \*|uint64_t|int32_t)\s*(gdp_\w+)\s*\(", txt, re.M)))
 
 
 def test_exports_every_declared_symbol():
     L = gdp.lib()
     names = header_functions()
-    assert len(names) == 17
+    assert len(names) == 18
     assert sorted(names) == sorted(gdp.EXPORTS)
     for n in names:
         assert hasattr(L, n), n

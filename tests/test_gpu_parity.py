@@ -363,27 +363,98 @@ def test_cost_full_size_c4_few_devices(gdp, d):
     assert_cost_equal(g, t, D, cost_gpu(gdp, g, t, D))
 
 
-def test_cost_v1_fallback_matches(gdp):
-    """The global-memory kernel (used when a graph's state exceeds shared memory) on the same
-    inputs, forced through GDP_COST_V1 in a subprocess."""
-    import subprocess, sys, os, json
-    code = r"""
+FORCED_CASES = r"""
 import sys, json, numpy as np, torch
 sys.path.insert(0, %r)
 import workloads
-from tests.test_gpu_parity import cost_gpu
+from tests.test_gpu_parity import cost_gpu, forced_inputs
 import paper_1910_01578_b200 as gdp
-g = workloads.multibranch(blocks=20, seed=5)
-t = workloads.topology(g, 4)
-D = np.random.default_rng(3).integers(0, 4, size=(16, g.N)).astype(np.uint8)
-r = cost_gpu(gdp, g, t, D)
-print(json.dumps({k: np.asarray(v).tolist() for k, v in r.items()}))
-""" % os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, GDP_COST_V1="1")
-    out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
+out = {}
+for name, (g, t, D) in forced_inputs().items():
+    G, T = gdp.Graph(g, workloads.features(g)), gdp.Topo(t)
+    r = cost_gpu(gdp, g, t, D)
+    r["kernel"] = gdp.cost_kernel(G, T)
+    out[name] = {k: np.asarray(v).tolist() for k, v in r.items()}
+print(json.dumps(out))
+"""
+
+
+def forced_inputs():
+    """A workload graph and a random DAG with zero-duration ops and zero latency."""
+    g1 = workloads.multibranch(blocks=20, seed=5)
+    t1 = workloads.topology(g1, 4)
+    D1 = np.random.default_rng(3).integers(0, 4, size=(16, g1.N)).astype(np.uint8)
+    rng = np.random.default_rng(11)
+    g2 = workloads.random_dag(150, p_edge=0.2, max_back=20, seed=11, cost_max=9)
+    g2.compute_cost[rng.random(150) < 0.2] = 0
+    t2 = mktopo(3, bw=50, lat=0)
+    D2 = rng.integers(0, 3, size=(16, 150)).astype(np.uint8)
+    return {"workload": (g1, t1, D1), "zero_dur": (g2, t2, D2)}
+
+
+@pytest.mark.parametrize("env,kernels", [("GDP_COST_V1", {"workload": 1, "zero_dur": 1}),
+                                         ("GDP_COST_V2", {"workload": 2, "zero_dur": 2}),
+                                         ("GDP_COST_V3", {"workload": 3, "zero_dur": 3}),
+                                         (None, {"workload": 4, "zero_dur": 3})])
+def test_cost_every_kernel_matches(gdp, env, kernels):
+    """Each cost kernel (DESIGN.md §"Cost model": 4 windowed, 3 warp-cooperative, 2 owner-lane,
+    1 global-memory) on the same inputs, selected through its environment switch in a subprocess."""
+    import subprocess, sys, os, json
+    code = FORCED_CASES % os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    e = {k: v for k, v in os.environ.items() if not k.startswith("GDP_COST_")}
+    if env:
+        e[env] = "1"
+    out = subprocess.run([sys.executable, "-c", code], env=e, capture_output=True, text=True, timeout=600)
     assert out.returncode == 0, out.stderr[-2000:]
-    r = {k: np.asarray(v) for k, v in json.loads(out.stdout.strip().splitlines()[-1]).items()}
-    g = workloads.multibranch(blocks=20, seed=5)
-    t = workloads.topology(g, 4)
-    D = np.random.default_rng(3).integers(0, 4, size=(16, g.N)).astype(np.uint8)
-    assert_cost_equal(g, t, D, r)
+    res = json.loads(out.stdout.strip().splitlines()[-1])
+    for name, (g, t, D) in forced_inputs().items():
+        r = {k: np.asarray(v) for k, v in res[name].items()}
+        assert int(r.pop("kernel")) == kernels[name], (name, env)
+        assert_cost_equal(g, t, D, r)
+
+
+def test_cost_kernel_choice(gdp):
+    W = workloads.config("c4")
+    g = W.graphs[0]
+    G = gdp.Graph(g, workloads.features(g))
+    assert gdp.cost_kernel(G, gdp.Topo(workloads.topology(g, 8))) == 4
+    assert gdp.cost_kernel(G, gdp.Topo(workloads.topology(g, 1))) == 4
+    assert gdp.cost_kernel(G, gdp.Topo(workloads.topology(g, 4, lat=0))) == 3
+    gz = mkgraph(3, [(0, 1)], [1, 0, 2])
+    assert gdp.cost_kernel(gdp.Graph(gz, workloads.features(gz)), gdp.Topo(mktopo(2, lat=3))) == 3
+
+
+def topo_general(d, rng, lat_lo, lat_hi, speed_hi=1, cap=None):
+    """Non-uniform latency / bandwidth matrices and per-device speeds."""
+    from workloads import Topology
+    la = rng.integers(lat_lo, lat_hi + 1, size=(d, d)).astype(np.int32)
+    la = np.minimum(la, la.T)                    # the topology is symmetric (SPEC.md)
+    np.fill_diagonal(la, 0)
+    bpt = rng.integers(1, 3000, size=(d, d)).astype(np.int64)
+    bpt = np.minimum(bpt, bpt.T)
+    return Topology(d=d, mem_capacity=np.full(d, cap if cap else 1 << 60, dtype=np.int64),
+                    speed=rng.integers(1, speed_hi + 1, size=d).astype(np.int32),
+                    bytes_per_tick=bpt, latency=la)
+
+
+@pytest.mark.parametrize("case", range(8))
+def test_cost_windowed_kernel(gdp, case):
+    """The windowed kernel's own edge cases: window length 1 (latency 1), capped windows
+    (latency > 8), non-uniform latency / bandwidth, heterogeneous speeds, one device, long
+    channel queues (slow links), dense fan-in (many producer deaths per window), capacity hits."""
+    rng = np.random.default_rng(100 + case)
+    d = [2, 8, 3, 8, 1, 5, 8, 4][case]
+    lat = [(1, 1), (1, 4), (9, 30), (2, 7), (1, 1), (3, 3), (1, 2), (5, 12)][case]
+    n = int(rng.integers(50, 400))
+    g = workloads.random_dag(n, p_edge=float(rng.uniform(0.05, 0.4)), max_back=int(rng.integers(2, 60)),
+                             seed=200 + case, cost_max=int(rng.integers(1, 40)))
+    g.compute_cost = np.maximum(g.compute_cost, 1)
+    if case == 6:
+        g.output_bytes = g.output_bytes * 50 + 5000       # slow transfers: long channel queues
+    t = topo_general(d, rng, *lat, speed_hi=3 if case % 2 else 1,
+                     cap=int(rng.integers(2000, 20000)) if case in (3, 7) else None)
+    G = gdp.Graph(g, workloads.features(g))
+    assert gdp.cost_kernel(G, gdp.Topo(t)) == 4
+    D = rng.integers(0, d, size=(48, n)).astype(np.uint8)
+    D[0] = 0
+    assert_cost_equal(g, t, D, cost_gpu(gdp, g, t, D))
