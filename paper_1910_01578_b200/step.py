@@ -2,7 +2,8 @@
 
 Buffers are torch CUDA tensors; every arithmetic step runs in libgdp.so kernels.
 torch.distributed (NCCL) supplies the exchange steps of the data-parallel path, as laid
-out by sharding.plan:
+out by sharding.plan.  With several graphs, each graph's embed -> place -> sample
+-> cost chain runs on its own CUDA stream; the gradients accumulate on the caller's stream:
   * mode 'samples': an all-gather of the rewards (global trial order for the advantage,
     P:177) and one all-reduce of the flat fp32 gradient;
   * mode 'graphs': one all-reduce of the gradient.
@@ -40,6 +41,7 @@ class _GraphState:
         self.adv_all = torch.empty(B_total, dtype=torch.float64, device=device)
         self.run_sum = torch.zeros(1, dtype=torch.float64, device=device)
         self.run_count = torch.zeros(1, dtype=torch.int64, device=device)
+        self.stream = None          # set when several graphs share the step
 
     def reports(self) -> Dict[str, np.ndarray]:
         r = decode_reports(self.rep.cpu().numpy())
@@ -72,6 +74,11 @@ class PolicyStep:
         # NCCL collectives whenever a process group exists (also with one rank, so that the
         # multi-GPU code path is exercised on a single GPU)
         self.collective = torch.distributed.is_available() and torch.distributed.is_initialized()
+        # several graphs: their independent embed -> place -> sample -> cost chains run on one
+        # stream each (the cost kernel of one graph fills only B of the GPU's CTA slots)
+        if len(self.states) > 1:
+            for st in self.states:
+                st.stream = torch.cuda.Stream(device=self.device)
 
     def _ev(self, name: str, timed: bool):
         if timed:
@@ -84,18 +91,26 @@ class PolicyStep:
         -> [all-reduce]; leaves the summed gradient in self.grad (asynchronous)."""
         torch, P = self.torch, self.plan
         step = self.step_idx
+        main = torch.cuda.current_stream(self.device)
         self.grad.zero_()
         for st in self.states:
-            self._ev("embed0", timed)
-            gdp_embed(st.g, self.cfg, theta, st.node_emb, st.ws)
-            self._ev("place0", timed)
-            gdp_place(st.g, self.cfg, theta, st.node_emb, st.logits, st.ws)
-            self._ev("sample0", timed)
-            gdp_sample(st.g, self.cfg, st.logits, st.B, self.seed, P.sample_offset, step, st.placements,
-                       st.logprob, st.ws)
-            self._ev("cost0", timed)
-            gdp_cost(st.g, st.t, st.placements, st.B, st.rep, st.peak, st.busy, st.reward, st.ws)
-            self._ev("cost1", timed)
+            if st.stream is not None:
+                st.stream.wait_stream(main)
+            with torch.cuda.stream(st.stream if st.stream is not None else main):
+                self._ev("embed0", timed)
+                gdp_embed(st.g, self.cfg, theta, st.node_emb, st.ws)
+                self._ev("place0", timed)
+                gdp_place(st.g, self.cfg, theta, st.node_emb, st.logits, st.ws)
+                self._ev("sample0", timed)
+                gdp_sample(st.g, self.cfg, st.logits, st.B, self.seed, P.sample_offset, step, st.placements,
+                           st.logprob, st.ws)
+                self._ev("cost0", timed)
+                gdp_cost(st.g, st.t, st.placements, st.B, st.rep, st.peak, st.busy, st.reward, st.ws)
+                self._ev("cost1", timed)
+        for st in self.states:
+            if st.stream is not None:
+                main.wait_stream(st.stream)
+        for st in self.states:
             if P.mode == "samples" and self.collective:
                 torch.distributed.all_gather_into_tensor(st.reward_all, st.reward)
             else:

@@ -21,7 +21,8 @@ def run(N, c, d=8, B=256, chain=False):
     t0 = time.perf_counter(); gdp.gdp_cost(G, T, D, B, rep, None, None, rew, ws); torch.cuda.synchronize()
     return 1e3 * (time.perf_counter() - t0)
 
-N = 20000
-for c, chain in ((1000, False), (1, False), (1000, True), (1, True)):
-    ms = run(N, c, chain=chain)
-    print(f"{'chain' if chain else 'iso  '} cost {c:5d}: {ms:7.2f} ms  {ms * 1e3 / N:6.3f} us/op", flush=True)
+if __name__ == "__main__":
+    N = 20000
+    for c, chain in ((1000, False), (1, False), (1000, True), (1, True)):
+        ms = run(N, c, chain=chain)
+        print(f"{'chain' if chain else 'iso  '} cost {c:5d}: {ms:7.2f} ms  {ms * 1e3 / N:6.3f} us/op", flush=True)
