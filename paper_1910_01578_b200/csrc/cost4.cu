@@ -43,6 +43,7 @@ struct Smem4 {
   NRec inc[8][NINC4];
   NRec run[8];                     // record of the op running on each device
   int run_slot[8];
+  unsigned long long smb[8][2];    // mbarrier of each staging slot (bulk copies complete_tx)
   unsigned lb[R4][8][WMAX][3];     // device-warp memory deltas per window set / device / tick
   long long db[R4][8][WMAX];       // producer deaths (memory warp only)
   int cfree[64], ctail[64], cstamp[64];                        // producer side (warp k)
@@ -109,13 +110,35 @@ __device__ __forceinline__ bool dec_out4(unsigned *cnt, const IRec &ir, int *big
   const int sh = (ir.u & 3) * 8 + 4;
   return ((atomicSub(&cnt[ir.u >> 2], 1u << sh) >> sh) & 15u) == 1u;
 }
-// the device lane stages the out-/in-edge records of op r into its slot sl
+__device__ __forceinline__ unsigned smem_u32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_wait(unsigned long long *mbar, unsigned parity) {
+  unsigned done = 0;
+  while (!done)
+    asm volatile("{\n\t.reg .pred P1;\n\tmbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+                 "selp.b32 %0, 1, 0, P1;\n\t}\n"
+                 : "=r"(done)
+                 : "r"(smem_u32(mbar)), "r"(parity)
+                 : "memory");
+}
+// the device lane stages the out-/in-edge records of op r into its slot sl: two bulk copies
+// (contiguous record ranges) completing on the slot's mbarrier
 __device__ __forceinline__ void stage_records4(Smem4 &S, const Cost2Graph &G, int q, int sl, const NRec &r) {
-  const int no = min(r.oe - r.ob, SO4), ni = min(r.ie - r.ib, SI4);
-  const int4 *eo = reinterpret_cast<const int4 *>(G.erec + r.ob);
-  int4 *so = reinterpret_cast<int4 *>(&S.st_out[q][sl][0]);
-  for (int j = 0; j < 2 * no; j++) cp16(so + j, eo + j);
-  for (int j = 0; j < ni; j++) cp16(&S.st_in[q][sl][j], G.irec + r.ib + j);
+  const unsigned no = (unsigned)min(r.oe - r.ob, SO4), ni = (unsigned)min(r.ie - r.ib, SI4);
+  unsigned long long *mb = &S.smb[q][sl];
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // earlier generic reads of the slot
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(mb)),
+               "r"(no * (unsigned)sizeof(NRec) + ni * (unsigned)sizeof(IRec))
+               : "memory");
+  if (no)
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(smem_u32(&S.st_out[q][sl][0])), "l"(G.erec + r.ob), "r"(no * (unsigned)sizeof(NRec)),
+                 "r"(smem_u32(mb))
+                 : "memory");
+  if (ni)
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(smem_u32(&S.st_in[q][sl][0])), "l"(G.irec + r.ib), "r"(ni * (unsigned)sizeof(IRec)),
+                 "r"(smem_u32(mb))
+                 : "memory");
 }
 __device__ __forceinline__ void put_inc(Smem4 &S, NRec *ovq, int q, int pos, const NRec &r) {
   if (pos < NINC4) copy_rec(&S.inc[q][pos], &r);
@@ -126,7 +149,7 @@ template <bool PROF>
 __global__ void __launch_bounds__(288, 2) k_cost4(Cost2Graph G, TopoArgs T, const uint8_t *__restrict__ Dall,
                                                   unsigned char *scratch, size_t per_place, gdp_sim_report *rep,
                                                   long long *peak_out, long long *busy_out, double *reward, int Wl,
-                                                  int dbg, unsigned msleep) {
+                                                  int dbg, unsigned msleep, int dbg_warp) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Smem4 &S = *reinterpret_cast<Smem4 *>(smem_raw);
   const int N = G.N, d = T.d, b = blockIdx.x;
@@ -155,6 +178,10 @@ __global__ void __launch_bounds__(288, 2) k_cost4(Cost2Graph G, TopoArgs T, cons
   if (tid == 0) {
     S.flag = 0; S.oom = 0; S.cross = 0; S.dq_tail = 0; S.mk = 0; S.disp = 0; S.nwin = 0;
     S.win_done = -1; S.mem_done = -1; S.dev_done = 0;
+  }
+  if (tid < 16) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&S.smb[tid >> 1][tid & 1])) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   for (int i = tid; i < R4 * 8 * WMAX * 3; i += nthr) (&S.lb[0][0][0][0])[i] = 0u;
   for (int i = tid; i < R4 * 8 * WMAX; i += nthr) (&S.db[0][0][0])[i] = 0;
@@ -290,7 +317,8 @@ __global__ void __launch_bounds__(288, 2) k_cost4(Cost2Graph G, TopoArgs T, cons
     Ent *fq_g = fifo + S.doff[q];
     const int spd = T.speed[q];
     int fhead = 0, ftail = S.ftail0[q], running = 0, fin = 0, mk = 0, disp = 0;
-    int cur = 0, cur_li = -2, nxt_id = -1, nxt_li = -2;
+    int cur = 0, nxt_id = -1;
+    unsigned nst0 = 0, nst1 = 0;                 // bulk stagings issued per slot (mbarrier phases)
     int li = 0, T0 = 0, w = 0, memd = -1;
     long long c_local = 0, c_bar = 0, c_post = 0, c_mw = 0, tc = clock64();   // PROF only
     long long c_wall = 0, c_maxloc = 0, t_ws = 0, t_prev = clock64();
@@ -318,8 +346,9 @@ __global__ void __launch_bounds__(288, 2) k_cost4(Cost2Graph G, TopoArgs T, cons
         const int tau = (int)(key >> 1);
         if (key == NK || tau >= Tend) break;
         const bool fnow = (key & 1) == 0;
-        if (devl) {   // staged records / FIFO refills: everything older than the last instant
-          if (fnow && cur_li == li - 1) cp_wait0(); else cp_wait1();
+        if (devl) {
+          cp_wait1();   // FIFO refills older than the last instant
+          if (fnow) mbar_wait(&S.smb[q][cur], ((cur ? nst1 : nst0) - 1u) & 1u);   // staged records
         }
         __syncwarp();
         long long delta = 0;
@@ -456,11 +485,9 @@ __global__ void __launch_bounds__(288, 2) k_cost4(Cost2Graph G, TopoArgs T, cons
             cur ^= 1;
             copy_rec(&S.run[q], &run);
             S.run_slot[q] = cur;
-            if (run.id == nxt_id) {   // its records were staged while it waited
-              cur_li = nxt_li;
-            } else {
-              cur_li = li;
+            if (run.id != nxt_id) {   // not staged while it waited: stage now
               stage_records4(S, G, q, cur, run);
+              if (cur) nst1++; else nst0++;
               staged = true;
             }
             nxt_id = -1;
@@ -471,8 +498,8 @@ __global__ void __launch_bounds__(288, 2) k_cost4(Cost2Graph G, TopoArgs T, cons
             NRec sr;
             load_rec(sr, &S.fc[q][fhead % KF4].r);
             stage_records4(S, G, q, cur ^ 1, sr);
+            if (cur) nst0++; else nst1++;
             nxt_id = sr.id;
-            nxt_li = li;
           }
           cp_commit();
         }
@@ -538,7 +565,7 @@ __global__ void __launch_bounds__(288, 2) k_cost4(Cost2Graph G, TopoArgs T, cons
       S.nwin = w + 1;
       st_rel(&S.dev_done, 1);
     }
-    if (PROF && busy_out && lane == 0 && d == 8 && q == 1) {
+    if (PROF && busy_out && lane == 0 && d == 8 && q == (dbg_warp & 7)) {
       long long *o = busy_out + (size_t)b * d;
       o[0] = c_wall; o[1] = c_maxloc; o[2] = c_local; o[3] = cl[2]; o[4] = cl[3]; o[5] = c_bar; o[6] = c_post + c_mw; o[7] = li;
     }
@@ -653,10 +680,13 @@ bool launch_cost4(const Cost2Graph &G, const TopoArgs &T, int min_cost, const ui
   static const int dbg = getenv("GDP_COST_DBG") ? atoi(getenv("GDP_COST_DBG")) : 0;
   note_launch();
   static const unsigned msleep = getenv("GDP_COST_MSLEEP") ? (unsigned)atoi(getenv("GDP_COST_MSLEEP")) : 200u;
+  static const int dbg_warp = getenv("GDP_COST_DBG_WARP") ? atoi(getenv("GDP_COST_DBG_WARP")) : 1;
   if (dbg == 3)
-    k_cost4<true><<<B, 32 * (d + 1), smem, s>>>(G, T, D, scratch, per_place, rep, peak, busy, reward, L, dbg, msleep);
+    k_cost4<true><<<B, 32 * (d + 1), smem, s>>>(G, T, D, scratch, per_place, rep, peak, busy, reward, L, dbg, msleep,
+                                               dbg_warp);
   else
-    k_cost4<false><<<B, 32 * (d + 1), smem, s>>>(G, T, D, scratch, per_place, rep, peak, busy, reward, L, dbg, msleep);
+    k_cost4<false><<<B, 32 * (d + 1), smem, s>>>(G, T, D, scratch, per_place, rep, peak, busy, reward, L, dbg,
+                                                msleep, dbg_warp);
   return true;
 }
 

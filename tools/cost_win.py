@@ -17,8 +17,11 @@ def run(N, c, d=8, B=256, chain=False):
     ws = torch.empty(gdp.workspace_size(G, cfg, B), dtype=torch.uint8, device="cuda")
     D = torch.zeros(B, N, dtype=torch.uint8, device="cuda")
     rep = torch.empty(B, 24, dtype=torch.uint8, device="cuda"); rew = torch.empty(B, dtype=torch.float64, device="cuda")
-    gdp.gdp_cost(G, T, D, B, rep, None, None, rew, ws); torch.cuda.synchronize()
-    t0 = time.perf_counter(); gdp.gdp_cost(G, T, D, B, rep, None, None, rew, ws); torch.cuda.synchronize()
+    busy = torch.empty(B, d, dtype=torch.int64, device="cuda")
+    gdp.gdp_cost(G, T, D, B, rep, None, busy, rew, ws); torch.cuda.synchronize()
+    t0 = time.perf_counter(); gdp.gdp_cost(G, T, D, B, rep, None, busy, rew, ws); torch.cuda.synchronize()
+    if os.environ.get("GDP_COST_DBG") == "3":
+        print("  dbg row0:", busy[0].cpu().numpy().tolist())
     return 1e3 * (time.perf_counter() - t0)
 
 if __name__ == "__main__":
