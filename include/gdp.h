@@ -258,6 +258,33 @@ gdp_status gdp_policy_grad(gdp_graph g, const gdp_config *c, const float *theta,
                            const float *old_logprob, float clip_eps, float entropy_coef, float loss_scale,
                            float *grad, void *ws, size_t ws_bytes, void *stream);
 
+/* ------------------------------------------------------------------ training update */
+
+/* log pi_b of GIVEN placements under the current logits ("pi(D|G)"):
+ * sum over co-location leaders of log softmax(logits_v)[D_b v], fp64 sum in a fixed order.
+ * The PPO epochs need it to form rho = exp(log pi_new - log pi_old).
+ *   logits dev fp32 N x d (in);  placements dev uint8 B x N (in);  logprob dev fp32 B (out)
+ * Uses the sampling scratch of ws.  Errors: GDP_ERR_ARG, GDP_ERR_WORKSPACE, GDP_ERR_CUDA. */
+gdp_status gdp_logprob(gdp_graph g, const gdp_config *c, const float *logits, const uint8_t *placements, int32_t B,
+                       float *logprob, void *ws, size_t ws_bytes, void *stream);
+
+/* Doubles of device scratch gdp_clip_adam needs. */
+#define GDP_ADAM_SCRATCH 1024
+
+/* Global-norm gradient clipping then one bias-corrected Adam step (
+ * DESIGN.md readings R31, R32):
+ *   s = min(1, max_norm / (||grad||_2 + 1e-6));  g = s * grad
+ *   m = beta1 m + (1 - beta1) g;  v = beta2 v + (1 - beta2) g^2
+ *   theta -= lr * (m / (1 - beta1^t)) / (sqrt(v / (1 - beta2^t)) + eps)
+ * ||grad|| is summed in fp64 in a fixed order (deterministic); the update is evaluated in fp64
+ * and stored as fp32.  All arrays are device pointers with 16-byte alignment:
+ *   grad fp32 [n] (in);  theta, m, v fp32 [n] (in/out);  scratch fp64 [GDP_ADAM_SCRATCH];
+ *   norm_out fp64 [1] (out, nullable: the pre-clip norm).  t >= 1 is the step number.
+ * Errors: GDP_ERR_ARG (NULL, n < 1, t < 1, misaligned, beta outside [0, 1)), GDP_ERR_CUDA. */
+gdp_status gdp_clip_adam(const float *grad, int64_t n, double max_norm, double lr, double beta1, double beta2,
+                         double eps, int64_t t, float *theta, float *m, float *v, double *scratch, double *norm_out,
+                         void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -23,9 +23,9 @@ from typing import Dict, Optional
 import numpy as np
 import torch
 
-from . import model, sampling, simulate
+from . import model, sampling, simulate, train
 
-__all__ = ["model", "sampling", "simulate", "Prepared", "prepare", "embed", "place", "logits_and_grad",
+__all__ = ["model", "sampling", "simulate", "train", "Prepared", "prepare", "embed", "place", "logits_and_grad",
            "policy_grad"]
 
 

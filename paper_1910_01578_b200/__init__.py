@@ -24,7 +24,7 @@ STATUS = {0: "GDP_OK", 1: "GDP_ERR_ARG", 2: "GDP_ERR_GRAPH", 3: "GDP_ERR_CYCLE",
 P_COUNT = 90
 REPORT_BYTES = 24
 
-EXPORTS = ["gdp_default_config", "gdp_last_error", "gdp_launch_count", "gdp_build_info", "gdp_cost_kernel", "gdp_graph_validate", "gdp_graph_create", "gdp_graph_destroy",
+EXPORTS = ["gdp_default_config", "gdp_last_error", "gdp_launch_count", "gdp_build_info", "gdp_cost_kernel", "gdp_logprob", "gdp_clip_adam", "gdp_graph_validate", "gdp_graph_create", "gdp_graph_destroy",
            "gdp_topo_create", "gdp_topo_destroy", "gdp_param_layout", "gdp_workspace_size", "gdp_embed",
            "gdp_place", "gdp_sample", "gdp_cost", "gdp_advantage", "gdp_policy_grad"]
 
@@ -49,6 +49,7 @@ def lib():
         if not os.path.exists(LIB_PATH):
             raise RuntimeError(f"libgdp.so not built ({LIB_PATH}); run __graft_entry__.build()")
         L = ctypes.CDLL(LIB_PATH)
+        F64 = ctypes.c_double
         P, I32, I64, U64, F32, SZ = (ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64,
                                      ctypes.c_float, ctypes.c_size_t)
         sig = {
@@ -66,6 +67,8 @@ def lib():
             "gdp_cost": [P, P, P, I32, P, P, P, P, P, SZ, P],
             "gdp_advantage": [P, I32, P, P, P, P],
             "gdp_policy_grad": [P, P, P, P, P, I32, P, P, P, F32, F32, F32, P, P, SZ, P],
+            "gdp_logprob": [P, P, P, P, I32, P, P, SZ, P],
+            "gdp_clip_adam": [P, I64, F64, F64, F64, F64, F64, I64, P, P, P, P, P, P],
         }
         for name, args in sig.items():
             fn = getattr(L, name)
@@ -109,7 +112,12 @@ def _np_ptr(a: Optional[np.ndarray]):
 
 
 def _t_ptr(t):
-    return None if t is None else ctypes.c_void_p(t.data_ptr())
+    """Device pointer of a torch tensor; the C ABI takes dense row-major buffers only."""
+    if t is None:
+        return None
+    if not t.is_contiguous():
+        raise ValueError("libgdp takes contiguous (row-major) tensors; got strides %s" % (tuple(t.stride()),))
+    return ctypes.c_void_p(t.data_ptr())
 
 
 def _stream(stream=None):
@@ -235,6 +243,21 @@ def gdp_policy_grad(g: Graph, cfg: Config, theta, logits, placements, B: int, ad
            "gdp_policy_grad")
 
 
+ADAM_SCRATCH = 1024   # GDP_ADAM_SCRATCH
+
+
+def gdp_logprob(g: Graph, cfg: Config, logits, placements, B: int, logprob, ws, stream=None):
+    _check(lib().gdp_logprob(g.h, ctypes.byref(cfg), _t_ptr(logits), _t_ptr(placements), B, _t_ptr(logprob),
+                             _t_ptr(ws), ws.numel(), _stream(stream)), "gdp_logprob")
+
+
+def gdp_clip_adam(grad, theta, m, v, t: int, lr: float, scratch, norm_out=None, max_norm: float = 1.0,
+                  beta1: float = 0.9, beta2: float = 0.999, eps: float = 1e-8, stream=None):
+    _check(lib().gdp_clip_adam(_t_ptr(grad), grad.numel(), max_norm, lr, beta1, beta2, eps, t, _t_ptr(theta),
+                               _t_ptr(m), _t_ptr(v), _t_ptr(scratch), _t_ptr(norm_out), _stream(stream)),
+           "gdp_clip_adam")
+
+
 def decode_reports(rep_bytes: np.ndarray):
     """gdp_sim_report B x 24 bytes -> dict of arrays (makespan, cross_bytes, valid, violation)."""
     r = np.ascontiguousarray(rep_bytes, dtype=np.uint8).reshape(-1, REPORT_BYTES)
@@ -242,4 +265,4 @@ def decode_reports(rep_bytes: np.ndarray):
                 valid=r[:, 16].copy(), violation=r[:, 17].copy())
 
 
-from .step import PolicyStep  # noqa: E402  (marshalling helper built on the functions above)
+from .step import PolicyStep, PPOTrainer  # noqa: E402  (marshalling helper built on the functions above)

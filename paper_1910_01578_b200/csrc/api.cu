@@ -1,6 +1,7 @@
 // C ABI of libgdp.so (include/gdp.h): validation, graph/topology objects, parameter layout,
 // workspace layout and the hot-path entry points.
 #include <algorithm>
+#include <cmath>
 #include <atomic>
 #include <climits>
 #include <cstring>
@@ -535,6 +536,41 @@ gdp_status gdp_sample(gdp_graph g, const gdp_config *c, const float *logits, int
   launch_sample(logits, g->leader, g->has_coloc, g->N, c->num_devices, B, seed, sample_offset, step, w.cdf,
                 w.logp, w.lastpos, placements, logprob, s);
   GDP_LAUNCH_CHECK("gdp_sample");
+  return GDP_OK;
+}
+
+gdp_status gdp_logprob(gdp_graph g, const gdp_config *c, const float *logits, const uint8_t *placements, int32_t B,
+                       float *logprob, void *ws, size_t ws_bytes, void *stream) {
+  if (!g || !logits || !placements || !logprob) return fail(GDP_ERR_ARG, "NULL argument");
+  gdp_status st = check_config(c);
+  if (st != GDP_OK) return st;
+  if (B < 1) return fail(GDP_ERR_ARG, "B must be >= 1");
+  WS w;
+  st = carve_any(g, c->num_devices, 1, ws, ws_bytes, &w);
+  if (st != GDP_OK) return st;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  launch_node_prep(logits, g->N, c->num_devices, w.cdf, w.logp, w.lastpos, s);
+  launch_logprob(w.logp, g->leader, placements, g->N, c->num_devices, B, logprob, s);
+  GDP_LAUNCH_CHECK("gdp_logprob");
+  return GDP_OK;
+}
+
+gdp_status gdp_clip_adam(const float *grad, int64_t n, double max_norm, double lr, double beta1, double beta2,
+                         double eps, int64_t t, float *theta, float *m, float *v, double *scratch, double *norm_out,
+                         void *stream) {
+  if (!grad || !theta || !m || !v || !scratch) return fail(GDP_ERR_ARG, "NULL argument");
+  if (n < 1 || t < 1) return fail(GDP_ERR_ARG, "n and t must be >= 1");
+  if (!(beta1 >= 0.0 && beta1 < 1.0 && beta2 >= 0.0 && beta2 < 1.0) || !(max_norm > 0.0) || !(eps >= 0.0))
+    return fail(GDP_ERR_ARG, "beta1, beta2 must lie in [0, 1), max_norm > 0, eps >= 0");
+  auto misaligned = [](const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) != 0; };
+  if (misaligned(grad) || misaligned(theta) || misaligned(m) || misaligned(v) || misaligned(scratch))
+    return fail(GDP_ERR_ARG, "grad, theta, m, v and scratch must be 16-byte aligned");
+  static_assert(GDP_ADAM_SCRATCH == kAdamScratch, "scratch size");
+  const double c1 = 1.0 / (1.0 - std::pow(beta1, (double)t));
+  const double c2 = 1.0 / (1.0 - std::pow(beta2, (double)t));
+  launch_clip_adam(grad, n, max_norm, lr, beta1, beta2, eps, c1, c2, theta, m, v, scratch, norm_out,
+                   static_cast<cudaStream_t>(stream));
+  GDP_LAUNCH_CHECK("gdp_clip_adam");
   return GDP_OK;
 }
 

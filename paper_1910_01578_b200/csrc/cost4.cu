@@ -85,12 +85,6 @@ __device__ __forceinline__ void st_rel(int *p, int v) {
 __device__ __forceinline__ void bar_devices(int nthreads) {
   asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
 }
-__device__ __forceinline__ void cp_wait_n(int n) {   // allow the n most recent groups in flight
-  if (n <= 0) asm volatile("cp.async.wait_group 0;\n" ::: "memory");
-  else if (n == 1) asm volatile("cp.async.wait_group 1;\n" ::: "memory");
-  else if (n == 2) asm volatile("cp.async.wait_group 2;\n" ::: "memory");
-  else asm volatile("cp.async.wait_group 3;\n" ::: "memory");
-}
 // 64-bit delta as 16 + 16 + 32-bit fire-and-forget shared reductions (few adds per bucket)
 __device__ __forceinline__ void add3(unsigned *w, long long v) {
   atomicAdd(&w[0], (unsigned)(v & 0xffff));

@@ -171,6 +171,11 @@ void launch_sample(const float *logits, const int *leader, bool has_coloc, int N
   }
 }
 
+void launch_node_prep(const float *logits, int N, int d, float *cdf, float *logp, int *lastpos, cudaStream_t s) {
+  note_launch();
+  k_node_prep<<<(N + 255) / 256, 256, 0, s>>>(logits, N, d, cdf, logp, lastpos);
+}
+
 void launch_logit_grad(const float *logits, const uint8_t *D, const int *leader, const double *adv,
                        const float *logprob, const float *old_logprob, float eps, float beta, float scale,
                        int N, int d, int B, double *wb, float *dlog, cudaStream_t s) {

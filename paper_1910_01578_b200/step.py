@@ -14,8 +14,8 @@ from typing import Dict, List, Optional
 
 import numpy as np
 
-from . import (Config, Graph, Topo, default_config, gdp_advantage, gdp_cost, gdp_embed, gdp_place,
-               gdp_policy_grad, gdp_sample, param_layout, workspace_size, REPORT_BYTES, decode_reports)
+from . import (Config, Graph, Topo, default_config, gdp_advantage, gdp_clip_adam, gdp_cost, gdp_embed, gdp_logprob,
+               gdp_place, gdp_policy_grad, gdp_sample, param_layout, workspace_size, REPORT_BYTES, decode_reports)
 from .sharding import plan as make_plan
 
 
@@ -124,3 +124,74 @@ class PolicyStep:
         if self.collective:
             torch.distributed.all_reduce(self.grad)
         self.step_idx += 1
+
+
+class PPOTrainer:
+    """One GDP-one training update on one graph,
+    marshalling only -- every step runs in libgdp.so kernels:
+      rollouts: embed -> place -> sample R placements -> cost -> advantage (the behaviour
+      log-probs log pi_old are kept);
+      then `epochs` passes over minibatches of the rollouts in order (reading R32): embed ->
+      place at the current theta -> gdp_logprob of the minibatch's placements -> clipped
+      surrogate gradient (loss scale 1 / minibatch) -> gdp_clip_adam (global norm 1.0, Adam).
+    theta (fp32 device tensor) is updated in place; Adam moments live here."""
+
+    def __init__(self, gsrc, feat, topo_src, d: int, seg_len: int = 128, mem_len: int = 128,
+                 superposition: bool = True, rollouts: int = 16, minibatch: int = 8, epochs: int = 4,
+                 lr: float = 3e-4, clip_eps: float = 0.2, entropy_coef: float = 0.01, max_norm: float = 1.0,
+                 seed: int = 42, device=None, tensor_cores: bool = False):
+        import torch
+        from . import ADAM_SCRATCH
+        self.torch = torch
+        self.device = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.cfg = default_config(d, seg_len, mem_len, superposition, tensor_cores)
+        self.R, self.mb, self.epochs = rollouts, minibatch, epochs
+        self.lr, self.clip_eps, self.entropy_coef, self.max_norm, self.seed = lr, clip_eps, entropy_coef, max_norm, seed
+        self.st = _GraphState(gsrc, feat, topo_src, self.cfg, rollouts, rollouts, self.device)
+        self.offsets, self.n_params = param_layout(self.cfg, self.st.F)
+        dev = self.device
+        self.grad = torch.zeros(self.n_params, dtype=torch.float32, device=dev)
+        self.m = torch.zeros(self.n_params, dtype=torch.float32, device=dev)
+        self.v = torch.zeros(self.n_params, dtype=torch.float32, device=dev)
+        self.scratch = torch.zeros(ADAM_SCRATCH, dtype=torch.float64, device=dev)
+        nmb = (rollouts + minibatch - 1) // minibatch
+        self.norms = torch.zeros(epochs * nmb, dtype=torch.float64, device=dev)
+        self.logprob_new = torch.empty(minibatch, dtype=torch.float32, device=dev)
+        self.t = 0
+        self.update_idx = 0
+
+    def rollouts(self, theta):
+        """embed -> place -> sample -> cost -> advantage; returns (placements, adv, old logprob)."""
+        st = self.st
+        gdp_embed(st.g, self.cfg, theta, st.node_emb, st.ws)
+        gdp_place(st.g, self.cfg, theta, st.node_emb, st.logits, st.ws)
+        gdp_sample(st.g, self.cfg, st.logits, self.R, self.seed, 0, self.update_idx, st.placements, st.logprob, st.ws)
+        gdp_cost(st.g, st.t, st.placements, self.R, st.rep, st.peak, st.busy, st.reward, st.ws)
+        gdp_advantage(st.reward, self.R, st.run_sum, st.run_count, st.adv_all)
+        return st.placements, st.adv_all, st.logprob
+
+    def epochs_update(self, theta, placements, adv, old_logprob):
+        """K epochs x minibatches of clipped-surrogate gradient -> clip -> Adam (in place)."""
+        st, R, mb = self.st, placements.shape[0], self.mb
+        k = 0
+        for _ in range(self.epochs):
+            for s0 in range(0, R, mb):
+                nb = min(mb, R - s0)
+                gdp_embed(st.g, self.cfg, theta, st.node_emb, st.ws)
+                gdp_place(st.g, self.cfg, theta, st.node_emb, st.logits, st.ws)
+                Pm = placements[s0:s0 + nb]
+                gdp_logprob(st.g, self.cfg, st.logits, Pm, nb, self.logprob_new, st.ws)
+                self.grad.zero_()
+                gdp_policy_grad(st.g, self.cfg, theta, st.logits, Pm, nb, adv[s0:s0 + nb], self.logprob_new,
+                                old_logprob[s0:s0 + nb], self.clip_eps, self.entropy_coef, 1.0 / nb, self.grad,
+                                st.ws)
+                self.t += 1
+                gdp_clip_adam(self.grad, theta, self.m, self.v, self.t, self.lr, self.scratch, self.norms[k:k + 1],
+                              max_norm=self.max_norm)
+                k += 1
+
+    def update(self, theta):
+        P, A, L = self.rollouts(theta)
+        P, A, L = P.clone(), A[:self.R].clone(), L.clone()
+        self.epochs_update(theta, P, A, L)
+        self.update_idx += 1
