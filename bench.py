@@ -172,6 +172,34 @@ def config_json(W, args):
 
 
 # ----------------------------------------------------------------------------- GPU arm
+def run_train(args, W, gdp, dev):
+    """Informative line for the NEXT-1 training update on the first graph of the config: one
+    update = 16 rollouts (embed, place, sample, cost, advantage) + 4 epochs x 2 minibatches of
+    (embed, place, log pi, clipped-surrogate gradient, clip + Adam).  Not the headline metric."""
+    import torch
+    g = W.graphs[0]
+    tr = gdp.PPOTrainer(g, workloads.features(g), workloads.topology(g, W.d), W.d, W.seg_len, W.mem_len,
+                        W.superposition, seed=W.seed, device=dev, tensor_cores=not args.fp32)
+    theta = torch.from_numpy(workloads.init_theta(workloads.F, W.d, seed=7)).to(dev)
+    for _ in range(args.warmup):
+        tr.update(theta)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    l0 = gdp.launch_count()
+    e0.record()
+    for _ in range(args.steps):
+        tr.update(theta)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    print(json.dumps({"metric": "GDP-one PPO training updates/s (16 rollouts, 4 epochs x 2 minibatches)",
+                      "value": 1000.0 / ms, "unit": "updates/s", "n_gpus": 1, "steps": args.steps,
+                      "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+                      "dtype": "f32" if args.fp32 else "bf16xbf16->f32 dense maps / f32",
+                      "data": "synthetic", "gpu_launches": (gdp.launch_count() - l0) // args.steps,
+                      "config": {"workload": W.name, "graph": g.name, "nodes": g.N, "devices_d": W.d}}))
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -184,6 +212,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--fp32", action="store_true", help="dense maps in fp32 SIMT instead of tcgen05 bf16")
+    ap.add_argument("--train", action="store_true",
+                    help="time the NEXT-1 training update (PPOTrainer.update) instead of the policy step")
     args = ap.parse_args()
     W = workloads.config(args.config, batch=args.batch, mem_len=args.mem_len)
     args.batch = W.batch
@@ -208,6 +238,9 @@ def main():
         dist.barrier()
     import paper_1910_01578_b200 as gdp
 
+    if args.train:
+        run_train(args, W, gdp, dev)
+        return
     graphs = [(g, workloads.features(g), workloads.topology(g, W.d)) for g in W.graphs]
     ps = gdp.PolicyStep(graphs, W.d, W.seg_len, W.mem_len, W.superposition, W.batch, seed=W.seed,
                         mode="samples", rank=rank, world=world, device=dev, tensor_cores=not args.fp32)

@@ -1,2 +1,2 @@
 python -c "import __graft_entry__ as g; g.build()" 
-timeout 900 python -m pytest tests/test_gpu_train.py -x -q -s -k ppo 2>&1 | grep -E "ppo parity|passed|failed|Error" | head
+for c in c1 c2 c4; do timeout 900 python bench.py --train --config $c --steps 3 --warmup 1 2>/dev/null | tail -1; done
