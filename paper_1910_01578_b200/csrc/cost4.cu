@@ -47,7 +47,8 @@ struct Smem4 {
   unsigned lb[R4][8][WMAX][3];     // device-warp memory deltas per window set / device / tick
   long long db[R4][8][WMAX];       // producer deaths (memory warp only)
   int cfree[64], ctail[64], cstamp[64];                        // producer side (warp k)
-  int pfin[2][8], phead[2][64], pfirst[2][64], ptail[2][64];   // published per window parity
+  int pfirst[2][64], ptail[2][64];   // published per window parity: first push's arrival, tail
+  int tn[3];                       // next window start, atomic min over devices' next events and first pushes
   int phs[2][64];                  // consumer head at the start of window w (parity w & 1)
   long long ploc[8];               // PROF: local cycles of each device warp in the window
   int coff[64], ccnt[64];
@@ -172,6 +173,7 @@ __global__ void __launch_bounds__(288, 2) k_cost4(Cost2Graph G, TopoArgs T, cons
   if (tid == 0) {
     S.flag = 0; S.oom = 0; S.cross = 0; S.dq_tail = 0; S.mk = 0; S.disp = 0; S.nwin = 0;
     S.win_done = -1; S.mem_done = -1; S.dev_done = 0;
+    S.tn[0] = INF; S.tn[1] = INF; S.tn[2] = INF;
   }
   if (tid < 16) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&S.smb[tid >> 1][tid & 1])) : "memory");
@@ -326,7 +328,10 @@ __global__ void __launch_bounds__(288, 2) k_cost4(Cost2Graph G, TopoArgs T, cons
         memd = __shfl_sync(FULL, memd, 0);
       }
       if (PROF) { const long long tn = clock64(); c_mw += tn - tc; tc = tn; t_ws = tn; c_wall += tn - t_prev; t_prev = tn; }
-      if (q == 0 && lane == 0) S.Tw[set] = T0;
+      if (q == 0 && lane == 0) {
+        S.Tw[set] = T0;
+        S.tn[(w + 1) % 3] = INF;   // read last after barrier w - 2, written from window w + 1 on
+      }
       if (lane < d) S.pfirst[w & 1][8 * q + lane] = INF;
       const int Tend = T0 + Wl;
       for (;;) {
@@ -338,7 +343,10 @@ __global__ void __launch_bounds__(288, 2) k_cost4(Cost2Graph G, TopoArgs T, cons
         if (PROF) tl = clock64();
         const unsigned key = __reduce_min_sync(FULL, cand);
         const int tau = (int)(key >> 1);
-        if (key == NK || tau >= Tend) break;
+        if (key == NK || tau >= Tend) {   // my next event opens a later window
+          if (lane == 0 && key != NK) atomicMin(&S.tn[w % 3], tau);
+          break;
+        }
         const bool fnow = (key & 1) == 0;
         if (devl) {
           cp_wait1();   // FIFO refills older than the last instant
@@ -433,7 +441,11 @@ __global__ void __launch_bounds__(288, 2) k_cost4(Cost2Graph G, TopoArgs T, cons
                 if (rank == 0) {
                   S.cfree[c] = bs + n * x;
                   S.ctail[c] = tail + n;
-                  if (S.cstamp[c] != w) { S.cstamp[c] = w; S.pfirst[w & 1][c] = bs + x; }
+                  if (S.cstamp[c] != w) {   // first push of this window: the consumer may not know it yet
+        S.cstamp[c] = w;
+        S.pfirst[w & 1][c] = bs + x;
+        atomicMin(&S.tn[w % 3], bs + x);
+      }
                 }
               }
               __syncwarp();
@@ -504,11 +516,7 @@ __global__ void __launch_bounds__(288, 2) k_cost4(Cost2Graph G, TopoArgs T, cons
         PL(4)
       }
       // publish the end-of-window state, meet, and find the next window start
-      if (devl) S.pfin[w & 1][q] = running ? fin : INF;
-      if (own) {
-        S.phead[w & 1][cin] = ha;
-        S.phs[(w + 1) & 1][cin] = head;
-      }
+      if (own) S.phs[(w + 1) & 1][cin] = head;
       if (lane < d) S.ptail[w & 1][8 * q + lane] = S.ctail[8 * q + lane];
       if (PROF) { const long long tn = clock64(); c_local += tn - tc; tc = tn; if (lane == 0) S.ploc[q] = tn - t_ws; }
       bar_devices(32 * d);   // bar.sync orders the window's shared and global writes for all device warps
@@ -522,16 +530,7 @@ __global__ void __launch_bounds__(288, 2) k_cost4(Cost2Graph G, TopoArgs T, cons
         S.dq_end[set] = S.dq_tail;
         st_rel(&S.win_done, w);
       }
-      int cand = lane < d ? S.pfin[w & 1][lane] : INF;
-#pragma unroll
-      for (int h = 0; h < 2; h++) {
-        const int c = 2 * lane + h, k = c >> 3, qq = c & 7;
-        if (k < d && qq < d && k != qq) {
-          const int hv = S.phead[w & 1][c];
-          cand = min(cand, hv != INF ? hv : S.pfirst[w & 1][c]);
-        }
-      }
-      const int Tn = __reduce_min_sync(FULL, cand);
+      const int Tn = S.tn[w % 3];
       if (own) {   // my channel: entries pushed in this window
         const int tn = S.ptail[w & 1][cin];
         if (ha == INF && tn > tknown) ha = S.pfirst[w & 1][cin];

@@ -1,2 +1,4 @@
 python -c "import __graft_entry__ as g; g.build()" 
-for c in c1 c2 c4; do timeout 900 python bench.py --train --config $c --steps 3 --warmup 1 2>/dev/null | tail -1; done
+timeout 300 python tools/run_cost.py --reps 2 2>&1 | tail -4
+python tools/cost_win.py 2>&1 | tail -4
+timeout 900 python -m pytest tests -m gpu -x -q -k "cost" 2>&1 | tail -2
