@@ -442,10 +442,10 @@ __global__ void __launch_bounds__(288, 2) k_cost4(Cost2Graph G, TopoArgs T, cons
                   S.cfree[c] = bs + n * x;
                   S.ctail[c] = tail + n;
                   if (S.cstamp[c] != w) {   // first push of this window: the consumer may not know it yet
-        S.cstamp[c] = w;
-        S.pfirst[w & 1][c] = bs + x;
-        atomicMin(&S.tn[w % 3], bs + x);
-      }
+                    S.cstamp[c] = w;
+                    S.pfirst[w & 1][c] = bs + x;
+                    atomicMin(&S.tn[w % 3], bs + x);
+                  }
                 }
               }
               __syncwarp();
@@ -458,31 +458,44 @@ __global__ void __launch_bounds__(288, 2) k_cost4(Cost2Graph G, TopoArgs T, cons
         if (devl) {
           const int n = navail;
           NRec *Li = &S.inc[q][0];
-          if (n > 0) {
-            for (int i = 1; i < n; i++) {   // insertion sort by id (n is small except after wide fan-outs)
-              NRec key;
-              load_rec(key, i < NINC4 ? &Li[i] : &ovq[i]);
-              int j = i - 1;
-              while (j >= 0) {
-                NRec *pj = j < NINC4 ? &Li[j] : &ovq[j];
-                if (pj->id <= key.id) break;
-                copy_rec(j + 1 < NINC4 ? &Li[j + 1] : &ovq[j + 1], pj);
-                j--;
+          NRec run;
+          bool go = false;
+          if (n == 1 && !running && fhead == ftail) {   // common case: straight to dispatch
+            load_rec(run, Li);
+            ftail++;
+            fhead++;
+            go = true;
+          } else {
+            if (n > 0) {
+              for (int i = 1; i < n; i++) {   // insertion sort by id (n is small except after wide fan-outs)
+                NRec key;
+                load_rec(key, i < NINC4 ? &Li[i] : &ovq[i]);
+                int j = i - 1;
+                while (j >= 0) {
+                  NRec *pj = j < NINC4 ? &Li[j] : &ovq[j];
+                  if (pj->id <= key.id) break;
+                  copy_rec(j + 1 < NINC4 ? &Li[j + 1] : &ovq[j + 1], pj);
+                  j--;
+                }
+                copy_rec(j + 1 < NINC4 ? &Li[j + 1] : &ovq[j + 1], &key);
               }
-              copy_rec(j + 1 < NINC4 ? &Li[j + 1] : &ovq[j + 1], &key);
+              for (int i = 0; i < n; i++) {
+                const NRec &rr = i < NINC4 ? Li[i] : ovq[i];
+                if (ftail < fhead + KF4) store_ent(&S.fc[q][ftail % KF4], rr, tau, 0);
+                else store_ent(fq_g + ftail, rr, tau, 0);
+                ftail++;
+              }
             }
-            for (int i = 0; i < n; i++) {
-              const NRec &rr = i < NINC4 ? Li[i] : ovq[i];
-              if (ftail < fhead + KF4) store_ent(&S.fc[q][ftail % KF4], rr, tau, 0);
-              else store_ent(fq_g + ftail, rr, tau, 0);
-              ftail++;
+            if (!running && fhead < ftail) {
+              Ent &e = S.fc[q][fhead % KF4];
+              load_rec(run, &e.r);
+              if (fhead + KF4 < ftail) cp_ent(&e, fq_g + fhead + KF4);
+              fhead++;
+              go = true;
             }
           }
           bool staged = false;
-          if (!running && fhead < ftail) {
-            Ent &e = S.fc[q][fhead % KF4];
-            NRec run;
-            load_rec(run, &e.r);
+          if (go) {
             running = 1;
             fin = tau + (run.cost & 0x7fffffff) * spd;
             mk = max(mk, fin);
@@ -497,8 +510,6 @@ __global__ void __launch_bounds__(288, 2) k_cost4(Cost2Graph G, TopoArgs T, cons
               staged = true;
             }
             nxt_id = -1;
-            if (fhead + KF4 < ftail) cp_ent(&e, fq_g + fhead + KF4);
-            fhead++;
           }
           if (!staged && running && nxt_id < 0 && fhead < ftail) {   // stage the op waiting at the head
             NRec sr;
