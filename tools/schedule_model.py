@@ -80,3 +80,44 @@ def dyn(optimistic, WM):
     return nw
 for WM in (8, 16):
     print("dynamic windows, cap", WM, ": optimistic", dyn(True, WM), " pessimistic", dyn(False, WM))
+
+# two-phase windows: events at T0 first, then (T0, H) with H = min over devices of the earliest
+# possible new push after phase 1 (running: fin + L; idle: next start + 1 + L, where next start is
+# the true one (optimistic) or T0 + 1 (pessimistic)); cost = sum over windows of the busiest
+# device's local instants (+1 for phase 1)
+def two_phase(optimistic, WM=64):
+    i = nw = 0
+    crit = 0
+    fins = {k: sorted(f for _, f in ops[k]) for k in ops}
+    while i < len(T):
+        t0 = T[i]; nw += 1
+        H = t0 + WM
+        for k in range(W.d):
+            ff = fins[k]; j = bisect.bisect_right(ff, t0)          # first finish after t0
+            ss = starts[k]; js = bisect.bisect_right(ss, t0) - 1
+            running = js >= 0 and ops[k][js][1] > t0
+            if running:
+                e_ = ops[k][js][1] + Lat
+            else:
+                jn = bisect.bisect_right(ss, t0)
+                ns = ss[jn] if jn < len(ss) else 10 ** 12
+                e_ = (ns if optimistic else t0 + 1) + 1 + Lat
+            H = min(H, e_)
+        per_dev = collections.Counter()
+        while i < len(T) and T[i] < H:
+            for (dv, kd) in ev[T[i]]:
+                per_dev[dv] += 1 if kd != "s" else 0
+            i += 1
+        crit += max(per_dev.values()) if per_dev else 0
+    return nw, crit
+print("two-phase windows (optimistic, pessimistic):", two_phase(True), two_phase(False))
+i = nw = crit = 0
+while i < len(T):
+    t0 = T[i]; nw += 1
+    per_dev = collections.Counter()
+    while i < len(T) and T[i] < t0 + Lat:
+        for (dv, kd) in ev[T[i]]:
+            per_dev[dv] += 1 if kd != "s" else 0
+        i += 1
+    crit += max(per_dev.values()) if per_dev else 0
+print("static windows, critical local events:", nw, crit)
