@@ -212,6 +212,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--fp32", action="store_true", help="dense maps in fp32 SIMT instead of tcgen05 bf16")
+    ap.add_argument("--cuda-graph", action="store_true",
+                    help="replay the whole step as one CUDA graph (single process; no per-stage timings)")
     ap.add_argument("--train", action="store_true",
                     help="time the NEXT-1 training update (PPOTrainer.update) instead of the policy step")
     args = ap.parse_args()
@@ -243,7 +245,8 @@ def main():
         return
     graphs = [(g, workloads.features(g), workloads.topology(g, W.d)) for g in W.graphs]
     ps = gdp.PolicyStep(graphs, W.d, W.seg_len, W.mem_len, W.superposition, W.batch, seed=W.seed,
-                        mode="samples", rank=rank, world=world, device=dev, tensor_cores=not args.fp32)
+                        mode="samples", rank=rank, world=world, device=dev, tensor_cores=not args.fp32,
+                        cuda_graph=args.cuda_graph)
     th = workloads.init_theta(workloads.F, W.d, seed=7)
     theta = torch.from_numpy(th).to(dev)
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
@@ -267,7 +270,7 @@ def main():
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record()
-            ps.run(theta, timed=True)
+            ps.run(theta, timed=not ps.cuda_graph)
             e1.record()
             sync()
             times.append(e0.elapsed_time(e1))
@@ -280,40 +283,48 @@ def main():
     placements = W.batch * world * len(W.graphs) * args.steps
     value = placements / (total_ms / 1000.0)
 
-    # dominant kernel: the cost model (one CTA per placement); per-launch time from events
-    cost_ms = [a.elapsed_time(b) for a, b in zip(ps.events["cost0"], ps.events["cost1"])]
-    grad_ms = [a.elapsed_time(b) for a, b in zip(ps.events["grad0"], ps.events["grad1"])]
-    place_ms = [a.elapsed_time(b) for a, b in zip(ps.events["place0"], ps.events["sample0"])]
-    embed_ms = [a.elapsed_time(b) for a, b in zip(ps.events["embed0"], ps.events["place0"])]
-    sample_ms = [a.elapsed_time(b) for a, b in zip(ps.events["sample0"], ps.events["cost0"])]
-    cost_avg = statistics.mean(cost_ms)
-    # The dominant kernel is the cost model (one CTA per placement).  It is a sequential
-    # discrete-event loop per placement, bound by dependent ALU/shared-memory latency, so its
-    # roofline is the SM issue rate: 148 SMs x 4 schedulers x 1 warp-instruction/clk.  The
-    # warp-instructions one launch issues are measured once by ncu for this workload
-    # (profiles/cost_kernel_ncu.json, smsp__inst_executed.sum) and divided by the live CUDA-event
-    # launch time; the algorithmic units (N + E events per placement) are reported
-    # beside it as events/s.  DESIGN.md §"Roofline of the cost model".
-    pk = peaks()
-    sm_mhz = pk.get("sm_max_mhz", 1965.0)
-    peak_ginst = 148 * 4 * sm_mhz * 1e6 / 1e9
-    events_per_launch = sum(g.N + g.E for g in W.graphs) * W.batch / len(W.graphs)
-    prof = {}
-    try:
-        prof = json.load(open(os.path.join(ROOT, "profiles", "cost_kernel_ncu.json")))
-    except Exception:
-        pass
-    matched = prof.get("workload") == W.name and prof.get("batch") == W.batch
-    inst = prof.get("warp_inst_per_launch") if matched else None
-    traffic = (prof["dram_bytes_read_per_launch"] + prof["dram_bytes_write_per_launch"]) if matched else None
-    achieved = (inst / (cost_avg / 1000.0) / 1e9) if inst else None
-    roof = {"kernel": prof.get("kernel", "cost"), "bound": "alu", "achieved": achieved, "peak": peak_ginst, "unit": "Gwarp-inst/s",
-            "frac": (achieved / peak_ginst) if achieved else None, "traffic": traffic,
-            "peak_source": "148 SM x 4 issue/clk x sm_max_mhz (MEASURED_PEAKS.json)",
-            "inst_source": "ncu smsp__inst_executed.sum per launch (profiles/cost_kernel_ncu.json)" if inst else
-                           "no ncu count for this workload",
-            "events_per_s": events_per_launch / (cost_avg / 1000.0),
-            "launch_ms": cost_avg, "share_of_step": sum(cost_ms) / sum(times)}
+    roof = None
+    stage = None
+    if not ps.cuda_graph:
+        # dominant kernel: the cost model (one CTA per placement); per-launch time from events
+        cost_ms = [a.elapsed_time(b) for a, b in zip(ps.events["cost0"], ps.events["cost1"])]
+        grad_ms = [a.elapsed_time(b) for a, b in zip(ps.events["grad0"], ps.events["grad1"])]
+        place_ms = [a.elapsed_time(b) for a, b in zip(ps.events["place0"], ps.events["sample0"])]
+        embed_ms = [a.elapsed_time(b) for a, b in zip(ps.events["embed0"], ps.events["place0"])]
+        sample_ms = [a.elapsed_time(b) for a, b in zip(ps.events["sample0"], ps.events["cost0"])]
+        cost_avg = statistics.mean(cost_ms)
+        # The dominant kernel is the cost model (one CTA per placement).  It is a sequential
+        # discrete-event loop per placement, bound by dependent ALU/shared-memory latency, so its
+        # roofline is the SM issue rate: 148 SMs x 4 schedulers x 1 warp-instruction/clk.  The
+        # warp-instructions one launch issues are measured once by ncu for this workload
+        # (profiles/cost_kernel_ncu.json, smsp__inst_executed.sum) and divided by the live CUDA-event
+        # launch time; the algorithmic units (N + E events per placement) are reported
+        # beside it as events/s.  DESIGN.md §"Roofline of the cost model".
+        pk = peaks()
+        sm_mhz = pk.get("sm_max_mhz", 1965.0)
+        peak_ginst = 148 * 4 * sm_mhz * 1e6 / 1e9
+        events_per_launch = sum(g.N + g.E for g in W.graphs) * W.batch / len(W.graphs)
+        prof = {}
+        try:
+            prof = json.load(open(os.path.join(ROOT, "profiles", "cost_kernel_ncu.json")))
+        except Exception:
+            pass
+        matched = prof.get("workload") == W.name and prof.get("batch") == W.batch
+        inst = prof.get("warp_inst_per_launch") if matched else None
+        traffic = (prof["dram_bytes_read_per_launch"] + prof["dram_bytes_write_per_launch"]) if matched else None
+        achieved = (inst / (cost_avg / 1000.0) / 1e9) if inst else None
+        roof = {"kernel": prof.get("kernel", "cost"), "bound": "alu", "achieved": achieved, "peak": peak_ginst, "unit": "Gwarp-inst/s",
+                "frac": (achieved / peak_ginst) if achieved else None, "traffic": traffic,
+                "peak_source": "148 SM x 4 issue/clk x sm_max_mhz (MEASURED_PEAKS.json)",
+                "inst_source": "ncu smsp__inst_executed.sum per launch (profiles/cost_kernel_ncu.json)" if inst else
+                               "no ncu count for this workload",
+                "events_per_s": events_per_launch / (cost_avg / 1000.0),
+                "launch_ms": cost_avg, "share_of_step": sum(cost_ms) / sum(times)}
+
+        stage = {"embed": statistics.mean(embed_ms), "place": statistics.mean(place_ms),
+                 "sample": statistics.mean(sample_ms), "cost": cost_avg, "grad": statistics.mean(grad_ms)}
+    else:
+        launches = ps.graph_launches     # kernels inside the captured step graph
 
     # e2e through the public API with host buffers: theta H2D, step, grad + rewards D2H
     e2e = None
@@ -321,7 +332,6 @@ def main():
         th_host = torch.from_numpy(th).pin_memory()
         g_host = torch.empty(ps.n_params, dtype=torch.float32).pin_memory()
         r_host = [torch.empty(st.B, dtype=torch.float64).pin_memory() for st in ps.states]
-        theta2 = torch.empty_like(theta)
         et = []
         for _ in range(max(2, args.steps // 2)):
             flush.fill_(1.0)
@@ -329,8 +339,8 @@ def main():
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record()
-            theta2.copy_(th_host, non_blocking=True)
-            ps.run(theta2)
+            theta.copy_(th_host, non_blocking=True)     # same tensor: a captured graph stays valid
+            ps.run(theta)
             g_host.copy_(ps.grad, non_blocking=True)
             for st, rh in zip(ps.states, r_host):
                 rh.copy_(st.reward, non_blocking=True)
@@ -367,9 +377,7 @@ def main():
                "config": config_json(W, argparse.Namespace(batch=W.batch, gpus=world)),
                "clocks": clk.summary(), "gpu_launches": int(launches), "roofline": roof, "e2e": e2e,
                "cpu_baseline": cpu,
-               "stages_ms": {"embed": statistics.mean(embed_ms), "place": statistics.mean(place_ms),
-                             "sample": statistics.mean(sample_ms), "cost": cost_avg,
-                             "grad": statistics.mean(grad_ms)},
+               "stages_ms": stage, "cuda_graph": bool(ps.cuda_graph),
                "valid_frac": float(np.mean(rep["valid"])), "makespan_mean_ticks": float(np.mean(rep["makespan"]))}
         print(json.dumps(out), flush=True)
     if distributed:

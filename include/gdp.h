@@ -209,6 +209,14 @@ gdp_status gdp_sample(gdp_graph g, const gdp_config *c, const float *logits, int
                       uint64_t sample_offset, uint64_t step, uint8_t *placements, float *logprob,
                       void *ws, size_t ws_bytes, void *stream);
 
+/* gdp_sample with the Philox step read from device memory (*step_dev, uint64) when the kernel
+ * runs, so that a captured CUDA graph draws fresh placements on every replay once the caller
+ * advances the counter inside the graph.  Same arguments, results and errors as gdp_sample
+ * (plus GDP_ERR_ARG for step_dev NULL). */
+gdp_status gdp_sample_at(gdp_graph g, const gdp_config *c, const float *logits, int32_t B, uint64_t seed,
+                         uint64_t sample_offset, const uint64_t *step_dev, uint8_t *placements, float *logprob,
+                         void *ws, size_t ws_bytes, void *stream);
+
 /* Step-time cost model (semantics in DESIGN.md §"Cost model"):
  * per placement, list scheduling in integer ticks -- duration = compute_cost x
  * speed[D v]; one transfer per cross-device edge, FIFO on the directed channel

@@ -24,7 +24,7 @@ STATUS = {0: "GDP_OK", 1: "GDP_ERR_ARG", 2: "GDP_ERR_GRAPH", 3: "GDP_ERR_CYCLE",
 P_COUNT = 90
 REPORT_BYTES = 24
 
-EXPORTS = ["gdp_default_config", "gdp_last_error", "gdp_launch_count", "gdp_build_info", "gdp_cost_kernel", "gdp_logprob", "gdp_clip_adam", "gdp_graph_validate", "gdp_graph_create", "gdp_graph_destroy",
+EXPORTS = ["gdp_default_config", "gdp_last_error", "gdp_launch_count", "gdp_build_info", "gdp_cost_kernel", "gdp_logprob", "gdp_clip_adam", "gdp_sample_at", "gdp_graph_validate", "gdp_graph_create", "gdp_graph_destroy",
            "gdp_topo_create", "gdp_topo_destroy", "gdp_param_layout", "gdp_workspace_size", "gdp_embed",
            "gdp_place", "gdp_sample", "gdp_cost", "gdp_advantage", "gdp_policy_grad"]
 
@@ -68,6 +68,7 @@ def lib():
             "gdp_advantage": [P, I32, P, P, P, P],
             "gdp_policy_grad": [P, P, P, P, P, I32, P, P, P, F32, F32, F32, P, P, SZ, P],
             "gdp_logprob": [P, P, P, P, I32, P, P, SZ, P],
+            "gdp_sample_at": [P, P, P, I32, U64, U64, P, P, P, P, SZ, P],
             "gdp_clip_adam": [P, I64, F64, F64, F64, F64, F64, I64, P, P, P, P, P, P],
         }
         for name, args in sig.items():
@@ -214,6 +215,14 @@ def gdp_sample(g: Graph, cfg: Config, logits, B: int, seed: int, sample_offset: 
     _check(lib().gdp_sample(g.h, ctypes.byref(cfg), _t_ptr(logits), B, seed, sample_offset, step,
                             _t_ptr(placements), _t_ptr(logprob), _t_ptr(ws), ws.numel(), _stream(stream)),
            "gdp_sample")
+
+
+def gdp_sample_at(g: Graph, cfg: Config, logits, B: int, seed: int, sample_offset: int, step_dev, placements,
+                  logprob, ws, stream=None):
+    """gdp_sample with the Philox step read from a device uint64 counter (CUDA-graph replays)."""
+    _check(lib().gdp_sample_at(g.h, ctypes.byref(cfg), _t_ptr(logits), B, seed, sample_offset, _t_ptr(step_dev),
+                               _t_ptr(placements), _t_ptr(logprob), _t_ptr(ws), ws.numel(), _stream(stream)),
+           "gdp_sample_at")
 
 
 def cost_kernel(g: Graph, t: Topo) -> int:

@@ -522,9 +522,9 @@ gdp_status gdp_place(gdp_graph g, const gdp_config *c, const float *theta, const
   return run_place(g, c, theta, node_emb, logits, w, static_cast<cudaStream_t>(stream));
 }
 
-gdp_status gdp_sample(gdp_graph g, const gdp_config *c, const float *logits, int32_t B, uint64_t seed,
-                      uint64_t sample_offset, uint64_t step, uint8_t *placements, float *logprob, void *ws,
-                      size_t ws_bytes, void *stream) {
+static gdp_status sample_impl(gdp_graph g, const gdp_config *c, const float *logits, int32_t B, uint64_t seed,
+                              uint64_t sample_offset, uint64_t step, const uint64_t *step_dev, uint8_t *placements,
+                              float *logprob, void *ws, size_t ws_bytes, void *stream) {
   if (!g || !logits || !placements || !logprob) return fail(GDP_ERR_ARG, "NULL argument");
   gdp_status st = check_config(c);
   if (st != GDP_OK) return st;
@@ -533,10 +533,23 @@ gdp_status gdp_sample(gdp_graph g, const gdp_config *c, const float *logits, int
   st = carve_any(g, c->num_devices, 1, ws, ws_bytes, &w);
   if (st != GDP_OK) return st;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  launch_sample(logits, g->leader, g->has_coloc, g->N, c->num_devices, B, seed, sample_offset, step, w.cdf,
+  launch_sample(logits, g->leader, g->has_coloc, g->N, c->num_devices, B, seed, sample_offset, step, step_dev, w.cdf,
                 w.logp, w.lastpos, placements, logprob, s);
   GDP_LAUNCH_CHECK("gdp_sample");
   return GDP_OK;
+}
+
+gdp_status gdp_sample(gdp_graph g, const gdp_config *c, const float *logits, int32_t B, uint64_t seed,
+                      uint64_t sample_offset, uint64_t step, uint8_t *placements, float *logprob, void *ws,
+                      size_t ws_bytes, void *stream) {
+  return sample_impl(g, c, logits, B, seed, sample_offset, step, nullptr, placements, logprob, ws, ws_bytes, stream);
+}
+
+gdp_status gdp_sample_at(gdp_graph g, const gdp_config *c, const float *logits, int32_t B, uint64_t seed,
+                         uint64_t sample_offset, const uint64_t *step_dev, uint8_t *placements, float *logprob,
+                         void *ws, size_t ws_bytes, void *stream) {
+  if (!step_dev) return fail(GDP_ERR_ARG, "NULL step pointer");
+  return sample_impl(g, c, logits, B, seed, sample_offset, 0, step_dev, placements, logprob, ws, ws_bytes, stream);
 }
 
 gdp_status gdp_logprob(gdp_graph g, const gdp_config *c, const float *logits, const uint8_t *placements, int32_t B,

@@ -181,8 +181,8 @@ void launch_fill_rows(float *dst, const float *row, float scale, int N, int C, c
 
 // sampling / loss
 void launch_sample(const float *logits, const int *leader, bool has_coloc, int N, int d, int B, uint64_t seed,
-                   uint64_t offset, uint64_t step, float *cdf, float *logp, int *lastpos, uint8_t *D,
-                   float *logprob, cudaStream_t s);
+                   uint64_t offset, uint64_t step, const uint64_t *step_ptr, float *cdf, float *logp, int *lastpos,
+                   uint8_t *D, float *logprob, cudaStream_t s);
 void launch_node_prep(const float *logits, int N, int d, float *cdf, float *logp, int *lastpos, cudaStream_t s);
 void launch_logit_grad(const float *logits, const uint8_t *D, const int *leader, const double *adv,
                        const float *logprob, const float *old_logprob, float eps, float beta, float scale,

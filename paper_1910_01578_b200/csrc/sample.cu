@@ -49,8 +49,9 @@ __global__ void k_node_prep(const float *logits, int N, int d, float *cdf, float
 constexpr int ST = 256;
 __global__ void __launch_bounds__(ST) k_sample(const float *__restrict__ cdf, const float *__restrict__ logp,
                                                const int *__restrict__ lastpos, const int *__restrict__ leader,
-                                               int N, int d, uint64_t seed, uint64_t offset, uint64_t step,
-                                               uint8_t *D, float *logprob) {
+                                               int N, int d, uint64_t seed, uint64_t offset, uint64_t step_val,
+                                               const uint64_t *step_ptr, uint8_t *D, float *logprob) {
+  const uint64_t step = step_ptr ? *step_ptr : step_val;   // device counter: graph replays advance it
   __shared__ double red[ST / 32];
   const int b = blockIdx.x;
   const uint64_t gidx = offset + (uint64_t)b;
@@ -158,12 +159,12 @@ __global__ void k_logit_grad(const float *__restrict__ logits, const uint8_t *__
 }  // namespace
 
 void launch_sample(const float *logits, const int *leader, bool has_coloc, int N, int d, int B, uint64_t seed,
-                   uint64_t offset, uint64_t step, float *cdf, float *logp, int *lastpos, uint8_t *D,
-                   float *logprob, cudaStream_t s) {
+                   uint64_t offset, uint64_t step, const uint64_t *step_ptr, float *cdf, float *logp, int *lastpos,
+                   uint8_t *D, float *logprob, cudaStream_t s) {
   note_launch();
   k_node_prep<<<(N + 255) / 256, 256, 0, s>>>(logits, N, d, cdf, logp, lastpos);
   note_launch();
-  k_sample<<<B, ST, 0, s>>>(cdf, logp, lastpos, leader, N, d, seed, offset, step, D, logprob);
+  k_sample<<<B, ST, 0, s>>>(cdf, logp, lastpos, leader, N, d, seed, offset, step, step_ptr, D, logprob);
   if (has_coloc) {
     size_t n = (size_t)N * B;
     note_launch();

@@ -15,7 +15,8 @@ from typing import Dict, List, Optional
 import numpy as np
 
 from . import (Config, Graph, Topo, default_config, gdp_advantage, gdp_clip_adam, gdp_cost, gdp_embed, gdp_logprob,
-               gdp_place, gdp_policy_grad, gdp_sample, param_layout, workspace_size, REPORT_BYTES, decode_reports)
+               gdp_place, gdp_policy_grad, gdp_sample, gdp_sample_at, param_layout, workspace_size, REPORT_BYTES,
+               decode_reports)
 from .sharding import plan as make_plan
 
 
@@ -55,7 +56,7 @@ class PolicyStep:
 
     def __init__(self, graphs: List, d: int, seg_len: int, mem_len: int, superposition: bool, batch: int,
                  seed: int = 42, clip_eps: float = 0.2, entropy_coef: float = 0.01, mode: str = "samples",
-                 rank: int = 0, world: int = 1, device=None, tensor_cores: bool = False):
+                 rank: int = 0, world: int = 1, device=None, tensor_cores: bool = False, cuda_graph: bool = False):
         import torch
         self.torch = torch
         self.device = device if device is not None else torch.device("cuda", torch.cuda.current_device())
@@ -79,6 +80,14 @@ class PolicyStep:
         if len(self.states) > 1:
             for st in self.states:
                 st.stream = torch.cuda.Stream(device=self.device)
+                st.gbuf = torch.zeros(self.n_params, dtype=torch.float32, device=self.device)
+        # CUDA graph of one whole step (single process: NCCL calls are not captured); the Philox
+        # step then lives in device memory and the graph advances it on every replay
+        self.cuda_graph = cuda_graph and not self.collective
+        self.step_dev = torch.zeros(1, dtype=torch.int64, device=self.device)
+        self._graph = None
+        self._graph_theta = None
+        self.graph_launches = 0
 
     def _ev(self, name: str, timed: bool):
         if timed:
@@ -89,10 +98,34 @@ class PolicyStep:
     def run(self, theta, timed: bool = False):
         """embed -> place -> sample -> cost -> [all-gather rewards] -> advantage -> grad
         -> [all-reduce]; leaves the summed gradient in self.grad (asynchronous)."""
+        if self.cuda_graph and not timed:
+            torch = self.torch
+            if self._graph is None or self._graph_theta != theta.data_ptr():
+                self._body(theta, False, True)          # this step runs eagerly (one-time setup)
+                torch.cuda.synchronize(self.device)
+                g = torch.cuda.CUDAGraph()
+                from . import launch_count
+                l0 = launch_count()
+                with torch.cuda.graph(g):               # captured, not executed
+                    self._body(theta, False, True)
+                self.graph_launches = launch_count() - l0
+                self.step_idx -= 1                      # undo the capture's host-side bookkeeping
+                self._graph, self._graph_theta = g, theta.data_ptr()
+                return
+            self._graph.replay()
+            self.step_idx += 1
+            return
+        self._body(theta, timed, self.cuda_graph)
+
+    def _body(self, theta, timed: bool, dev_step: bool):
         torch, P = self.torch, self.plan
         step = self.step_idx
         main = torch.cuda.current_stream(self.device)
-        self.grad.zero_()
+        # several graphs in one process: each graph's whole chain, gradient included, runs on its
+        # own stream into its own gradient buffer; the buffers are summed in graph order at the end
+        per_graph = len(self.states) > 1 and not self.collective
+        if not per_graph:
+            self.grad.zero_()
         for st in self.states:
             if st.stream is not None:
                 st.stream.wait_stream(main)
@@ -102,28 +135,47 @@ class PolicyStep:
                 self._ev("place0", timed)
                 gdp_place(st.g, self.cfg, theta, st.node_emb, st.logits, st.ws)
                 self._ev("sample0", timed)
-                gdp_sample(st.g, self.cfg, st.logits, st.B, self.seed, P.sample_offset, step, st.placements,
-                           st.logprob, st.ws)
+                if dev_step:
+                    gdp_sample_at(st.g, self.cfg, st.logits, st.B, self.seed, P.sample_offset, self.step_dev,
+                                  st.placements, st.logprob, st.ws)
+                else:
+                    gdp_sample(st.g, self.cfg, st.logits, st.B, self.seed, P.sample_offset, step, st.placements,
+                               st.logprob, st.ws)
                 self._ev("cost0", timed)
                 gdp_cost(st.g, st.t, st.placements, st.B, st.rep, st.peak, st.busy, st.reward, st.ws)
                 self._ev("cost1", timed)
+                if per_graph:
+                    self._grad_of(st, theta, timed, st.gbuf)
         for st in self.states:
             if st.stream is not None:
                 main.wait_stream(st.stream)
-        for st in self.states:
-            if P.mode == "samples" and self.collective:
-                torch.distributed.all_gather_into_tensor(st.reward_all, st.reward)
-            else:
-                st.reward_all.copy_(st.reward)
-            gdp_advantage(st.reward_all, st.B_total, st.run_sum, st.run_count, st.adv_all)
-            adv = st.adv_all[P.sample_offset:P.sample_offset + st.B]
-            self._ev("grad0", timed)
-            gdp_policy_grad(st.g, self.cfg, theta, st.logits, st.placements, st.B, adv, st.logprob, None,
-                            self.clip_eps, P.entropy_coef, P.loss_scale, self.grad, st.ws)
-            self._ev("grad1", timed)
-        if self.collective:
-            torch.distributed.all_reduce(self.grad)
+        if per_graph:
+            self.grad.copy_(self.states[0].gbuf)
+            for st in self.states[1:]:
+                self.grad.add_(st.gbuf)
+        else:
+            for st in self.states:
+                if P.mode == "samples" and self.collective:
+                    torch.distributed.all_gather_into_tensor(st.reward_all, st.reward)
+                self._grad_of(st, theta, timed, self.grad)
+            if self.collective:
+                torch.distributed.all_reduce(self.grad)
+        if dev_step:
+            self.step_dev += 1
         self.step_idx += 1
+
+    def _grad_of(self, st, theta, timed: bool, grad):
+        P = self.plan
+        if not (P.mode == "samples" and self.collective):
+            st.reward_all.copy_(st.reward)
+        gdp_advantage(st.reward_all, st.B_total, st.run_sum, st.run_count, st.adv_all)
+        adv = st.adv_all[P.sample_offset:P.sample_offset + st.B]
+        if grad is not self.grad:
+            grad.zero_()
+        self._ev("grad0", timed)
+        gdp_policy_grad(st.g, self.cfg, theta, st.logits, st.placements, st.B, adv, st.logprob, None,
+                        self.clip_eps, P.entropy_coef, P.loss_scale, grad, st.ws)
+        self._ev("grad1", timed)
 
 
 class PPOTrainer:

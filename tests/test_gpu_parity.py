@@ -458,3 +458,22 @@ def test_cost_windowed_kernel(gdp, case):
     D = rng.integers(0, d, size=(48, n)).astype(np.uint8)
     D[0] = 0
     assert_cost_equal(g, t, D, cost_gpu(gdp, g, t, D))
+
+
+@pytest.mark.parametrize("cfg", ["c1", "c3"])
+def test_cuda_graph_step_matches_eager(gdp, cfg):
+    """A captured CUDA graph of the whole policy step (Philox step read from device memory,
+    graphs of C3 on their own streams inside the capture) replays bit-identically to eager steps."""
+    W = workloads.config(cfg)
+    graphs = [(g, workloads.features(g), workloads.topology(g, W.d)) for g in W.graphs]
+    theta = torch.from_numpy(workloads.init_theta(workloads.F, W.d, seed=7, mode="random")).cuda()
+    pe = gdp.PolicyStep(graphs, W.d, W.seg_len, W.mem_len, W.superposition, W.batch, seed=W.seed)
+    pgr = gdp.PolicyStep(graphs, W.d, W.seg_len, W.mem_len, W.superposition, W.batch, seed=W.seed, cuda_graph=True)
+    for s in range(3):
+        pe.run(theta)
+        pgr.run(theta)
+        torch.cuda.synchronize()
+        assert torch.equal(pe.grad, pgr.grad), (cfg, s)
+        for a, b in zip(pe.states, pgr.states):
+            assert torch.equal(a.reward, b.reward) and torch.equal(a.placements, b.placements), (cfg, s)
+    assert pgr._graph is not None

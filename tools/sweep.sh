@@ -11,6 +11,8 @@ run c4_b64 --config c4 --batch 64
 run c4_b1024 --config c4 --batch 1024
 run c4_minf --config c4 --mem-len -1
 run c4_fp32 --config c4 --fp32
+run c1_graph --config c1 --cuda-graph
+run c5_graph --config c5 --cuda-graph
 for f in $OUT/*.json; do python - "$f" <<'PY'
 import json, sys
 try:
