@@ -276,6 +276,13 @@ gdp_status gdp_policy_grad(gdp_graph g, const gdp_config *c, const float *theta,
 gdp_status gdp_logprob(gdp_graph g, const gdp_config *c, const float *logits, const uint8_t *placements, int32_t B,
                        float *logprob, void *ws, size_t ws_bytes, void *stream);
 
+/* Greedy decode for zero-shot placement: per node the
+ * argmax of its co-location leader's logits, ties -> lowest device id; optional log pi of it.
+ *   logits dev fp32 N x d (in);  placement dev uint8 N (out);  logprob dev fp32 [1] (out, nullable:
+ *   then ws may be NULL).  Errors: GDP_ERR_ARG, GDP_ERR_WORKSPACE, GDP_ERR_CUDA. */
+gdp_status gdp_greedy(gdp_graph g, const gdp_config *c, const float *logits, uint8_t *placement, float *logprob,
+                      void *ws, size_t ws_bytes, void *stream);
+
 /* Doubles of device scratch gdp_clip_adam needs. */
 #define GDP_ADAM_SCRATCH 1024
 

@@ -94,3 +94,25 @@ def advantage(rewards: np.ndarray, run_sum: float, run_count: int) -> Tuple[np.n
         s += r
         c += 1
     return A, s, c
+
+
+def greedy(logits: np.ndarray, lead: np.ndarray) -> Tuple[np.ndarray, np.ndarray]:
+    """S:527-531 greedy(dist): per-node argmax of the logits, ties -> lowest device id (S:549);
+    non-leaders copy their co-location leader's choice.  Returns (D uint8 [N],
+    margin float64 [N] = logit gap between the best and the runner-up of the deciding node)."""
+    z = np.asarray(logits, dtype=np.float64)
+    N, d = z.shape
+    D = np.zeros(N, dtype=np.int64)
+    margin = np.full(N, np.inf)
+    for v in range(N):
+        best = 0
+        for k in range(1, d):
+            if z[v, k] > z[v, best]:
+                best = k
+        D[v] = best
+        if d > 1:
+            rest = [z[v, k] for k in range(d) if k != best]
+            margin[v] = z[v, best] - max(rest)
+    D = D[lead]
+    margin = margin[lead]
+    return D.astype(np.uint8), margin

@@ -24,7 +24,7 @@ STATUS = {0: "GDP_OK", 1: "GDP_ERR_ARG", 2: "GDP_ERR_GRAPH", 3: "GDP_ERR_CYCLE",
 P_COUNT = 90
 REPORT_BYTES = 24
 
-EXPORTS = ["gdp_default_config", "gdp_last_error", "gdp_launch_count", "gdp_build_info", "gdp_cost_kernel", "gdp_logprob", "gdp_clip_adam", "gdp_sample_at", "gdp_graph_validate", "gdp_graph_create", "gdp_graph_destroy",
+EXPORTS = ["gdp_default_config", "gdp_last_error", "gdp_launch_count", "gdp_build_info", "gdp_cost_kernel", "gdp_logprob", "gdp_clip_adam", "gdp_sample_at", "gdp_greedy", "gdp_graph_validate", "gdp_graph_create", "gdp_graph_destroy",
            "gdp_topo_create", "gdp_topo_destroy", "gdp_param_layout", "gdp_workspace_size", "gdp_embed",
            "gdp_place", "gdp_sample", "gdp_cost", "gdp_advantage", "gdp_policy_grad"]
 
@@ -69,6 +69,7 @@ def lib():
             "gdp_policy_grad": [P, P, P, P, P, I32, P, P, P, F32, F32, F32, P, P, SZ, P],
             "gdp_logprob": [P, P, P, P, I32, P, P, SZ, P],
             "gdp_sample_at": [P, P, P, I32, U64, U64, P, P, P, P, SZ, P],
+            "gdp_greedy": [P, P, P, P, P, P, SZ, P],
             "gdp_clip_adam": [P, I64, F64, F64, F64, F64, F64, I64, P, P, P, P, P, P],
         }
         for name, args in sig.items():
@@ -225,6 +226,11 @@ def gdp_sample_at(g: Graph, cfg: Config, logits, B: int, seed: int, sample_offse
            "gdp_sample_at")
 
 
+def gdp_greedy(g: Graph, cfg: Config, logits, placement, logprob=None, ws=None, stream=None):
+    _check(lib().gdp_greedy(g.h, ctypes.byref(cfg), _t_ptr(logits), _t_ptr(placement), _t_ptr(logprob), _t_ptr(ws),
+                            0 if ws is None else ws.numel(), _stream(stream)), "gdp_greedy")
+
+
 def cost_kernel(g: Graph, t: Topo) -> int:
     """Which cost kernel gdp_cost runs for (g, t): 4 windowed, 3 warp-cooperative, 2 owner-lane,
     1 global-memory (include/gdp.h gdp_cost_kernel)."""
@@ -274,4 +280,4 @@ def decode_reports(rep_bytes: np.ndarray):
                 valid=r[:, 16].copy(), violation=r[:, 17].copy())
 
 
-from .step import PolicyStep, PPOTrainer  # noqa: E402  (marshalling helper built on the functions above)
+from .step import PolicyStep, PPOTrainer, zero_shot, finetune  # noqa: E402  (marshalling helper built on the functions above)

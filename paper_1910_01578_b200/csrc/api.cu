@@ -568,6 +568,24 @@ gdp_status gdp_logprob(gdp_graph g, const gdp_config *c, const float *logits, co
   return GDP_OK;
 }
 
+gdp_status gdp_greedy(gdp_graph g, const gdp_config *c, const float *logits, uint8_t *placement, float *logprob,
+                      void *ws, size_t ws_bytes, void *stream) {
+  if (!g || !logits || !placement) return fail(GDP_ERR_ARG, "NULL argument");
+  gdp_status st = check_config(c);
+  if (st != GDP_OK) return st;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  launch_greedy(logits, g->leader, g->N, c->num_devices, placement, s);
+  if (logprob) {
+    WS w;
+    st = carve_any(g, c->num_devices, 1, ws, ws_bytes, &w);
+    if (st != GDP_OK) return st;
+    launch_node_prep(logits, g->N, c->num_devices, w.cdf, w.logp, w.lastpos, s);
+    launch_logprob(w.logp, g->leader, placement, g->N, c->num_devices, 1, logprob, s);
+  }
+  GDP_LAUNCH_CHECK("gdp_greedy");
+  return GDP_OK;
+}
+
 gdp_status gdp_clip_adam(const float *grad, int64_t n, double max_norm, double lr, double beta1, double beta2,
                          double eps, int64_t t, float *theta, float *m, float *v, double *scratch, double *norm_out,
                          void *stream) {

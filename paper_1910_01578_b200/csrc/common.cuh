@@ -193,6 +193,7 @@ constexpr int kAdamScratch = 1024;   // doubles of caller scratch for gdp_clip_a
 int adam_parts();
 void launch_logprob(const float *logp, const int *leader, const uint8_t *D, int N, int d, int B, float *logprob,
                     cudaStream_t s);
+void launch_greedy(const float *logits, const int *leader, int N, int d, uint8_t *D, cudaStream_t s);
 void launch_clip_adam(const float *g, long long n, double max_norm, double lr, double b1, double b2, double eps,
                       double c1, double c2, float *theta, float *m, float *v, double *scratch, double *norm_out,
                       cudaStream_t s);

@@ -2,6 +2,7 @@
 //  * k_logprob:  one CTA per placement, log pi_b = sum over co-location leaders of
 //                log p_v[D_b v] (R18), fp64 sum in a fixed order
 //                (same per-node log-softmax as k_node_prep);
+//  * k_greedy:   argmax decode for zero-shot placement (NEXT-2);
 //  * k_sumsq:    ||g||^2 in fp64: 2 CTAs per SM, each a contiguous chunk read with 16-byte
 //                loads, fixed-order block reduction -> one partial per CTA (deterministic);
 //  * k_adam:     every CTA sums the partials in the same order, clip factor
@@ -31,6 +32,20 @@ __global__ void __launch_bounds__(LT) k_logprob(const float *__restrict__ logp, 
     for (int i = 0; i < LT / 32; i++) s += red[i];
     logprob[b] = (float)s;
   }
+}
+
+// greedy decode (NEXT-2): per node the argmax of its leader's logits (strict >, so
+// ties go to the lowest device id); non-leaders thereby copy their leader
+__global__ void k_greedy(const float *__restrict__ logits, const int *__restrict__ leader, int N, int d,
+                         uint8_t *D) {
+  const int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= N) return;
+  const float *z = logits + (size_t)leader[v] * d;
+  int best = 0;
+  float bz = z[0];
+  for (int k = 1; k < d; k++)
+    if (z[k] > bz) { bz = z[k]; best = k; }
+  D[v] = (uint8_t)best;
 }
 
 constexpr int AT = 256;
@@ -117,6 +132,11 @@ int sm_count() {
 }  // namespace
 
 int adam_parts() { return 2 * sm_count() < kAdamScratch ? 2 * sm_count() : kAdamScratch; }
+
+void launch_greedy(const float *logits, const int *leader, int N, int d, uint8_t *D, cudaStream_t s) {
+  note_launch();
+  k_greedy<<<(N + 255) / 256, 256, 0, s>>>(logits, leader, N, d, D);
+}
 
 void launch_logprob(const float *logp, const int *leader, const uint8_t *D, int N, int d, int B, float *logprob,
                     cudaStream_t s) {

@@ -15,8 +15,8 @@ from typing import Dict, List, Optional
 import numpy as np
 
 from . import (Config, Graph, Topo, default_config, gdp_advantage, gdp_clip_adam, gdp_cost, gdp_embed, gdp_logprob,
-               gdp_place, gdp_policy_grad, gdp_sample, gdp_sample_at, param_layout, workspace_size, REPORT_BYTES,
-               decode_reports)
+               gdp_greedy, gdp_place, gdp_policy_grad, gdp_sample, gdp_sample_at, param_layout, workspace_size,
+               REPORT_BYTES, decode_reports)
 from .sharding import plan as make_plan
 
 
@@ -247,3 +247,37 @@ class PPOTrainer:
         P, A, L = P.clone(), A[:self.R].clone(), L.clone()
         self.epochs_update(theta, P, A, L)
         self.update_idx += 1
+
+
+def zero_shot(gsrc, feat, topo_src, theta, d: int, seg_len: int = 128, mem_len: int = 128,
+              superposition: bool = True, tensor_cores: bool = False, device=None) -> Dict[str, object]:
+    """Zero-shot placement: embed -> place -> greedy decode ->
+    cost of that one placement, no update.  Returns the placement, its log-probability and the
+    cost-model report (makespan, validity, reward, peaks)."""
+    import torch
+    device = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+    cfg = default_config(d, seg_len, mem_len, superposition, tensor_cores)
+    st = _GraphState(gsrc, feat, topo_src, cfg, 1, 1, device)
+    gdp_embed(st.g, cfg, theta, st.node_emb, st.ws)
+    gdp_place(st.g, cfg, theta, st.node_emb, st.logits, st.ws)
+    gdp_greedy(st.g, cfg, st.logits, st.placements[0], st.logprob, st.ws)
+    gdp_cost(st.g, st.t, st.placements, 1, st.rep, st.peak, st.busy, st.reward, st.ws)
+    r = st.reports()
+    r["placement"] = st.placements[0].cpu().numpy()
+    r["logprob"] = float(st.logprob[0].item())
+    return r
+
+
+def finetune(gsrc, feat, topo_src, theta, d: int, updates: int = 50, **kw) -> Dict[str, object]:
+    """Fine-tune driver ("fewer than 50 steps"): at most
+    `updates` PPO training updates (PPOTrainer) on one target graph from the given theta (updated
+    in place), then the zero-shot placement of the result."""
+    if updates > 50:
+        raise ValueError("fine-tuning runs fewer than 50 updates (P:254)")
+    zs = {k: kw[k] for k in ("seg_len", "mem_len", "superposition", "tensor_cores") if k in kw}
+    tr = PPOTrainer(gsrc, feat, topo_src, d, **kw)
+    for _ in range(updates):
+        tr.update(theta)
+    out = zero_shot(gsrc, feat, topo_src, theta, d, **zs)
+    out["updates"] = updates
+    return out

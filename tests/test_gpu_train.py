@@ -111,3 +111,44 @@ def test_ppo_epochs_match_oracle(gdp):
     mx = np.abs(d_gpu - d_ref).max() / 3e-4
     print("ppo parity: rel L2 %.3e, elementwise frac %.5f, max |diff|/lr %.3e" % (rel, frac, mx))
     assert rel < 1e-3 and frac > 0.99 and mx < 0.25   # measured: 3.0e-4, 0.988 at 1e-3 lr, 0.10
+
+
+@pytest.mark.parametrize("coloc", [False, True])
+def test_greedy_zero_shot_matches_oracle(gdp, coloc):
+    """NEXT-2: greedy decode equals the oracle's argmax wherever the oracle's best-vs-runner-up logit
+    gap exceeds fp32 noise (the decision is taken on each side's own logits); where the placements
+    agree entirely, the zero-shot cost report is bit-exact."""
+    g = workloads.multibranch(blocks=4, seed=2)
+    if coloc:
+        g = workloads.with_colocation(g)
+    d = 4
+    X = workloads.features(g)
+    topo = workloads.topology(g, d)
+    th = workloads.init_theta(X.shape[1], d, seed=5, mode="random").astype(np.float32).astype(np.float64)
+    theta = torch.from_numpy(th.astype(np.float32)).cuda()
+    r = gdp.zero_shot(g, X, topo, theta, d)
+    pg = oracle.prepare(g, X)
+    zo = oracle.place(pg, th, oracle.embed(pg, th, d), d, 128, 128, True)
+    Do, margin = Osa.greedy(zo, pg.lead)
+    sure = margin > 1e-4 * max(1.0, np.abs(zo).max())
+    assert np.array_equal(r["placement"][sure], Do[sure])
+    assert abs(r["logprob"] - Otr.log_prob(zo, r["placement"][None], pg.lead)[0]) <= 1e-4 * abs(r["logprob"])
+    if np.array_equal(r["placement"], Do):
+        o = Osim.simulate_batch(g, topo, Do[None])
+        for k in ("makespan", "valid", "violation", "reward"):
+            assert np.array_equal(np.asarray(r[k]).astype(np.float64), np.asarray(o[k]).astype(np.float64)), k
+
+
+def test_finetune_driver_runs(gdp):
+    """NEXT-2 fine-tune driver: a few PPO updates from a given theta, then the zero-shot placement."""
+    W = workloads.config("c1")
+    g = W.graphs[0]
+    X = workloads.features(g)
+    theta = torch.from_numpy(workloads.init_theta(X.shape[1], W.d, seed=3)).cuda()
+    before = theta.clone()
+    out = gdp.finetune(g, X, workloads.topology(g, W.d), theta, W.d, updates=3, seg_len=W.seg_len,
+                       mem_len=W.mem_len)
+    assert out["updates"] == 3 and out["placement"].shape == (g.N,)
+    assert not torch.equal(before, theta) and torch.isfinite(theta).all()
+    with pytest.raises(ValueError):
+        gdp.finetune(g, X, workloads.topology(g, W.d), theta, W.d, updates=51)

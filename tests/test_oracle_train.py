@@ -72,7 +72,6 @@ def test_ppo_update_improves_bandit_toy():
     """one update on a 2-node / 2-device toy strictly increases the probability of the
     better placement (fixed seed)."""
     g, t = _bandit()
-    W = workloads.config("c1")
     X = workloads.features(g)
     pg = oracle.prepare(g, X)
     d, S, M = 2, 32, 32
@@ -107,3 +106,16 @@ def test_ppo_clipped_sample_has_no_surrogate_gradient():
     g_clip, _ = oracle.policy_grad(pg, th, 2, 32, 32, True, D, np.array([1.0]), lp - math.log(1.4), 0.2, 0.01, 1.0)
     g_ent, _ = oracle.policy_grad(pg, th, 2, 32, 32, True, D, np.array([0.0]), lp, 0.2, 0.01, 1.0)
     assert np.allclose(g_clip, g_ent, rtol=0, atol=1e-15)
+
+
+def test_greedy_pins():
+    # S:533 one-hot logits -> sample == greedy; S:549 ties -> lowest device id; S:530 co-location
+    z = np.array([[0.0, 50.0, 0.0], [80.0, 0.0, 0.0], [0.0, 0.0, 60.0], [1.0, 1.0, 0.5]])
+    lead = np.arange(4)
+    D, m = Osa.greedy(z, lead)
+    U = Osa.uniforms(4, 5, 1, 0, 0)
+    Ds, _, _ = Osa.sample(z, U, lead)
+    assert np.array_equal(D[:3], [1, 0, 2]) and np.all(Ds[:, :3] == D[:3])
+    assert D[3] == 0 and m[3] == 0.0                      # tie between devices 0 and 1
+    D, _ = Osa.greedy(z, np.array([0, 0, 2, 2]))          # nodes 1, 3 follow leaders 0, 2
+    assert np.array_equal(D, [1, 1, 2, 2])
