@@ -120,8 +120,8 @@ def oracle_placements_per_s(W, B_total: int, n_cost: int, threads: int):
         t3 = time.perf_counter()
         t_net += (t1 - t0) + (t3 - t2)
         t_cost_per += (t2 - t1) / n_cost
-    step = t_net + t_cost_per * B_total
-    return B_total / step, dict(t_net_s=t_net, t_cost_per_placement_s=t_cost_per)
+    step = t_net + t_cost_per * B_total          # B_total placements of every graph
+    return B_total * len(W.graphs) / step, dict(t_net_s=t_net, t_cost_per_placement_s=t_cost_per)
 
 
 def oracle_single_thread(W, B_total: int, n_cost: int = 2):
@@ -152,22 +152,25 @@ def run_reference(args, W, rank: int):
     sample = (f"per step: full fp64 oracle policy fwd+bwd (N={sum(g.N for g in W.graphs)}) + cost model on "
               f"{n_cost} of {args.batch} placements over {threads} threads; step time extrapolated to "
               f"B={args.batch}")
+    mode = "graphs" if len(W.graphs) > 2 else "samples"
     out = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-           "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * args.batch / value,
-           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64/i64",
-           "data": "synthetic", "config": config_json(W, args),
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * args.batch * len(W.graphs) / value,
+           "higher_is_better": True, "scaling": "weak" if mode == "samples" else "strong", "vs_baseline": None,
+           "dtype": "f64/i64", "data": "synthetic", "config": config_json(W, args, mode),
            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": sample},
            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
            "detail": info}
     print(json.dumps(out), flush=True)
 
 
-def config_json(W, args):
+def config_json(W, args, mode: str = "samples"):
     g = W.graphs
+    par = (f"dp{args.gpus} (placements sharded)" if mode == "samples" else
+           f"dp{args.gpus} (graphs sharded, LPT on N*B)")
     return {"workload": W.name, "graphs": [x.name for x in g], "nodes": [x.N for x in g],
             "edges": [x.E for x in g], "devices_d": W.d, "seg_len": W.seg_len, "mem_len": W.mem_len,
             "superposition": W.superposition, "batch_per_gpu": args.batch,
-            "global_batch": args.batch * args.gpus, "parallelism": f"dp{args.gpus} (placements sharded)",
+            "global_batch": args.batch * (args.gpus if mode == "samples" else 1), "parallelism": par,
             "l2": "flushed between timed steps (512 MiB write)"}
 
 
@@ -244,8 +247,10 @@ def main():
         run_train(args, W, gdp, dev)
         return
     graphs = [(g, workloads.features(g), workloads.topology(g, W.d)) for g in W.graphs]
+    # C5 (several graphs) is graph-sharded with LPT on N*B; the others split samples
+    mode = "graphs" if len(W.graphs) > 2 else "samples"
     ps = gdp.PolicyStep(graphs, W.d, W.seg_len, W.mem_len, W.superposition, W.batch, seed=W.seed,
-                        mode="samples", rank=rank, world=world, device=dev, tensor_cores=not args.fp32,
+                        mode=mode, rank=rank, world=world, device=dev, tensor_cores=not args.fp32,
                         cuda_graph=args.cuda_graph)
     th = workloads.init_theta(workloads.F, W.d, seed=7)
     theta = torch.from_numpy(th).to(dev)
@@ -280,7 +285,9 @@ def main():
         t = torch.tensor([total_ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
-    placements = W.batch * world * len(W.graphs) * args.steps
+    # placements per step over all ranks: samples mode adds B per rank per graph (weak scaling);
+    # graphs mode splits the fixed set of graphs (strong scaling)
+    placements = W.batch * (world if mode == "samples" else 1) * len(W.graphs) * args.steps
     value = placements / (total_ms / 1000.0)
 
     roof = None
@@ -352,7 +359,8 @@ def main():
             t = torch.tensor([tot], device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             tot = float(t.item())
-        e2e = {"value": W.batch * world * len(W.graphs) * len(et) / (tot / 1000.0), "unit": UNIT,
+        e2e = {"value": W.batch * (world if mode == "samples" else 1) * len(W.graphs) * len(et) / (tot / 1000.0),
+               "unit": UNIT,
                "h2d_bytes_per_step": th.nbytes, "d2h_bytes_per_step": 4 * ps.n_params + 8 * W.batch * len(W.graphs)}
 
     cpu = None
@@ -373,8 +381,9 @@ def main():
         rep = st0.reports()
         out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
-               "scaling": "weak", "vs_baseline": None, "dtype": ("f32" if args.fp32 else "bf16xbf16->f32 (tcgen05 dense maps) / f32") + " policy, i32 cost model", "data": "synthetic",
-               "config": config_json(W, argparse.Namespace(batch=W.batch, gpus=world)),
+               "scaling": "weak" if mode == "samples" else "strong", "vs_baseline": None,
+               "dtype": ("f32" if args.fp32 else "bf16xbf16->f32 (tcgen05 dense maps) / f32") + " policy, i32 cost model", "data": "synthetic",
+               "config": config_json(W, argparse.Namespace(batch=W.batch, gpus=world), mode),
                "clocks": clk.summary(), "gpu_launches": int(launches), "roofline": roof, "e2e": e2e,
                "cpu_baseline": cpu,
                "stages_ms": stage, "cuda_graph": bool(ps.cuda_graph),

@@ -123,7 +123,7 @@ class PolicyStep:
         main = torch.cuda.current_stream(self.device)
         # several graphs in one process: each graph's whole chain, gradient included, runs on its
         # own stream into its own gradient buffer; the buffers are summed in graph order at the end
-        per_graph = len(self.states) > 1 and not self.collective
+        per_graph = len(self.states) > 1 and not (P.mode == "samples" and self.collective)
         if not per_graph:
             self.grad.zero_()
         for st in self.states:
@@ -153,6 +153,8 @@ class PolicyStep:
             self.grad.copy_(self.states[0].gbuf)
             for st in self.states[1:]:
                 self.grad.add_(st.gbuf)
+            if self.collective:
+                torch.distributed.all_reduce(self.grad)
         else:
             for st in self.states:
                 if P.mode == "samples" and self.collective:
