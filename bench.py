@@ -215,12 +215,16 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--fp32", action="store_true", help="dense maps in fp32 SIMT instead of tcgen05 bf16")
+    ap.add_argument("--no-attention", action="store_true", help="NEXT-3 ablation variant (reading R34)")
+    ap.add_argument("--no-superposition", action="store_true", help="NEXT-3 ablation variant (gates == 1)")
     ap.add_argument("--cuda-graph", action="store_true",
                     help="replay the whole step as one CUDA graph (single process; no per-stage timings)")
     ap.add_argument("--train", action="store_true",
                     help="time the NEXT-1 training update (PPOTrainer.update) instead of the policy step")
     args = ap.parse_args()
     W = workloads.config(args.config, batch=args.batch, mem_len=args.mem_len)
+    if args.no_superposition:
+        W.superposition = False
     args.batch = W.batch
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -251,7 +255,7 @@ def main():
     mode = "graphs" if len(W.graphs) > 2 else "samples"
     ps = gdp.PolicyStep(graphs, W.d, W.seg_len, W.mem_len, W.superposition, W.batch, seed=W.seed,
                         mode=mode, rank=rank, world=world, device=dev, tensor_cores=not args.fp32,
-                        cuda_graph=args.cuda_graph)
+                        cuda_graph=args.cuda_graph, no_attention=args.no_attention)
     th = workloads.init_theta(workloads.F, W.d, seed=7)
     theta = torch.from_numpy(th).to(dev)
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)

@@ -70,6 +70,9 @@ typedef struct {
                              Y = X W (forward and the backward dX = dY W^T) with 16 <= width <= 256 and
                              >= 128 rows on tcgen05 tensor cores, bf16 operands, fp32 accumulation in
                              TMEM; weight gradients (reductions over nodes) stay fp32 */
+  int32_t no_attention;   /* ablation: 1 replaces every attention
+                             sublayer (placer and conditioner) by the per-node map
+                             o = ReLU(LN1(x) W_v + b_v) (reading R34); 0: attention */
 } gdp_config;
 
 /* One cost-model verdict per placement. */

@@ -66,11 +66,11 @@ def embed_keep(pg: Prepared, theta, d: int) -> Dict[str, object]:
 
 
 def place(pg: Prepared, theta, E: np.ndarray, d: int, S: int, M: int, superposition: bool = True,
-          keep: Optional[dict] = None) -> np.ndarray:
+          keep: Optional[dict] = None, no_attention: bool = False) -> np.ndarray:
     with torch.no_grad():
         p = model.unflatten(_theta(theta), pg.F, d)
         return model.place(torch.as_tensor(np.asarray(E, dtype=np.float64)), p, pg.order, S, M,
-                           superposition, keep).numpy()
+                           superposition, keep, no_attention=no_attention).numpy()
 
 
 def logit_grad(pg: Prepared, logits: np.ndarray, D, adv, old_logprob, clip_eps, entropy_coef, loss_scale):
@@ -83,14 +83,14 @@ def logit_grad(pg: Prepared, logits: np.ndarray, D, adv, old_logprob, clip_eps, 
 
 def policy_grad(pg: Prepared, theta, d: int, S: int, M: int, superposition: bool, D, adv,
                 old_logprob=None, clip_eps: float = 0.2, entropy_coef: float = 0.01,
-                loss_scale: float = 1.0, mem_srcs: Optional[dict] = None):
+                loss_scale: float = 1.0, mem_srcs: Optional[dict] = None, no_attention: bool = False):
     """Gradient of L (model.policy_loss) w.r.t. the flat theta through place and
     embed (§3.1 "trained jointly ... in an end-to-end fashion").
     Returns (grad float64 [n_params], loss float)."""
     th = _theta(theta).requires_grad_(True)
     p = model.unflatten(th, pg.F, d)
     E = model.embed(pg.X, pg.ptr, pg.idx, p)
-    logits = model.place(E, p, pg.order, S, M, superposition, mem_srcs=mem_srcs)
+    logits = model.place(E, p, pg.order, S, M, superposition, mem_srcs=mem_srcs, no_attention=no_attention)
     L = model.policy_loss(logits, D, adv, pg.lead, old_logprob, clip_eps, entropy_coef, loss_scale)
     (g,) = torch.autograd.grad(L, th)
     return g.numpy(), float(L.detach())

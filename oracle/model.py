@@ -180,7 +180,8 @@ def key_range(i: int, N: int, S: int, M: int) -> Tuple[int, int]:
 
 
 def xl_layer(x: torch.Tensor, p: Dict[str, torch.Tensor], n: str, gam: Optional[Dict[str, torch.Tensor]],
-             S: int, M: int, keep: Optional[dict] = None, mem_src: Optional[torch.Tensor] = None) -> torch.Tensor:
+             S: int, M: int, keep: Optional[dict] = None, mem_src: Optional[torch.Tensor] = None,
+             no_attention: bool = False) -> torch.Tensor:
     """One Transformer-XL layer over the node sequence without positional terms
     (P:144-148).  Segments of S nodes; each attends to itself (bidirectional) and to
     the cached hidden states of up to M earlier positions, which are detached
@@ -188,7 +189,10 @@ def xl_layer(x: torch.Tensor, p: Dict[str, torch.Tensor], n: str, gam: Optional[
     sits on the cached layer input, LN1/K/V parameters still see the memory rows).
     Superposition Eq. 4: every dense map g is applied to c(x0) (.) x.
     `mem_src` (tests only) supplies the cached states from elsewhere -- e.g. frozen at
-    another theta, which is what a finite-difference check of a stop-gradient needs."""
+    another theta, which is what a finite-difference check of a stop-gradient needs.
+    `no_attention` (NEXT-3 ablation, "replaces attention layers with per-node
+    feed-forward of equal width"; reading R34): o = ReLU(LN1(x) W_v + b_v), each node on its
+    own, through the same V and O maps (Q, K unused)."""
     if keep is not None:
         keep.setdefault("inputs", {})[n] = x.detach().clone()
     src = x if mem_src is None else mem_src
@@ -202,7 +206,10 @@ def xl_layer(x: torch.Tensor, p: Dict[str, torch.Tensor], n: str, gam: Optional[
 
     N = x.shape[0]
     outs = []
-    for q0 in range(0, N, S):
+    if no_attention:
+        a = layer_norm(x, p[f"{n}.ln1.g"], p[f"{n}.ln1.b"])
+        outs.append(torch.relu(dense(a, p[f"{n}.Wv"], p[f"{n}.bv"], "v")))
+    for q0 in (range(0, N, S) if not no_attention else []):
         q1 = min(q0 + S, N)
         k0, _ = key_range(q0, N, S, M)
         xk = torch.cat([src[k0:q0].detach(), x[q0:q1]], 0)
@@ -256,11 +263,11 @@ def xl_layer_masked(x: torch.Tensor, p: Dict[str, torch.Tensor], n: str, gam, S:
 
 
 def gates(E_topo: torch.Tensor, p: Dict[str, torch.Tensor], S: int, M: int, keep: Optional[dict] = None,
-          mem_srcs: Optional[dict] = None):
+          mem_srcs: Optional[dict] = None, no_attention: bool = False):
     """Superposition conditioning (readings R14): c = an additional
     transformer layer over the embeddings, averaged over nodes, then per
     gated dense map j: gamma_j = 2 sigmoid(z P_j + q_j) (=1 at P, q = 0)."""
-    C = xl_layer(E_topo, p, "cond", None, S, M, keep, (mem_srcs or {}).get("cond"))
+    C = xl_layer(E_topo, p, "cond", None, S, M, keep, (mem_srcs or {}).get("cond"), no_attention)
     z = C.mean(0)
     gam = [{j: 2 * torch.sigmoid(z @ p[f"gate{l}.{j}.P"] + p[f"gate{l}.{j}.q"]) for j in GATED} for l in range(2)]
     gh = 2 * torch.sigmoid(z @ p["gate.head.P"] + p["gate.head.q"])
@@ -272,7 +279,8 @@ def gates(E_topo: torch.Tensor, p: Dict[str, torch.Tensor], S: int, M: int, keep
 
 
 def place(E: torch.Tensor, p: Dict[str, torch.Tensor], order: Sequence[int], S: int, M: int,
-          superposition: bool = True, keep: Optional[dict] = None, mem_srcs: Optional[dict] = None) -> torch.Tensor:
+          superposition: bool = True, keep: Optional[dict] = None, mem_srcs: Optional[dict] = None,
+          no_attention: bool = False) -> torch.Tensor:
     """§3.2-3.3 placement network: nodes in topological order, 2
     segment-recurrent layers, per-node device logits from the conditioned head with
     no final LN (R15); whole graph placed at once (R13).  Returns logits in
@@ -280,11 +288,11 @@ def place(E: torch.Tensor, p: Dict[str, torch.Tensor], order: Sequence[int], S: 
     perm = torch.as_tensor(list(order), dtype=torch.long)
     x = E[perm]
     if superposition:
-        gam, gh = gates(x, p, S, M, keep, mem_srcs)
+        gam, gh = gates(x, p, S, M, keep, mem_srcs, no_attention)
     else:
         gam, gh = [None, None], None
     for l in range(2):
-        x = xl_layer(x, p, f"xl{l}", gam[l], S, M, keep, (mem_srcs or {}).get(f"xl{l}"))
+        x = xl_layer(x, p, f"xl{l}", gam[l], S, M, keep, (mem_srcs or {}).get(f"xl{l}"), no_attention)
     lt = (x if gh is None else x * gh) @ p["head.W"] + p["head.b"]
     logits = torch.empty_like(lt)
     logits = logits.index_copy(0, perm, lt)

@@ -69,6 +69,7 @@ static gdp_status check_config(const gdp_config *c) {
   if (c->seg_len < 1) return fail(GDP_ERR_ARG, "seg_len must be >= 1");
   if (c->mem_len < -1) return fail(GDP_ERR_ARG, "mem_len must be >= -1");
   if (c->tensor_cores != 0 && c->tensor_cores != 1) return fail(GDP_ERR_ARG, "tensor_cores must be 0 or 1");
+  if (c->no_attention != 0 && c->no_attention != 1) return fail(GDP_ERR_ARG, "no_attention must be 0 or 1");
   return GDP_OK;
 }
 
@@ -228,6 +229,7 @@ gdp_status gdp_default_config(int32_t d, gdp_config *out) {
   out->mem_len = 128;
   out->superposition = 1;
   out->tensor_cores = 0;
+  out->no_attention = 0;
   return GDP_OK;
 }
 
@@ -507,6 +509,7 @@ gdp_status gdp_embed(gdp_graph g, const gdp_config *c, const float *theta, float
   st = carve_any(g, c->num_devices, 1, ws, ws_bytes, &w);
   if (st != GDP_OK) return st;
   set_tensor_cores(c->tensor_cores != 0);
+  set_no_attention(c->no_attention != 0);
   return run_embed(g, theta, node_emb, w, c->num_devices, static_cast<cudaStream_t>(stream));
 }
 
@@ -519,6 +522,7 @@ gdp_status gdp_place(gdp_graph g, const gdp_config *c, const float *theta, const
   st = carve_any(g, c->num_devices, 1, ws, ws_bytes, &w);
   if (st != GDP_OK) return st;
   set_tensor_cores(c->tensor_cores != 0);
+  set_no_attention(c->no_attention != 0);
   return run_place(g, c, theta, node_emb, logits, w, static_cast<cudaStream_t>(stream));
 }
 
@@ -652,6 +656,7 @@ gdp_status gdp_policy_grad(gdp_graph g, const gdp_config *c, const float *theta,
   st = carve_any(g, c->num_devices, B, ws, ws_bytes, &w);
   if (st != GDP_OK) return st;
   set_tensor_cores(c->tensor_cores != 0);
+  set_no_attention(c->no_attention != 0);
   return run_policy_grad(g, c, theta, logits, placements, B, adv, logprob, old_logprob, clip_eps, entropy_coef,
                          loss_scale, grad, w, static_cast<cudaStream_t>(stream));
 }

@@ -147,6 +147,9 @@ void launch_gemm(const GemmArgs &a, cudaStream_t s);
 bool tc_eligible(const GemmArgs &a);
 void launch_gemm_tc(const GemmArgs &a, cudaStream_t s);
 void set_tensor_cores(bool on);
+// ablation variant of the entry point in progress (gdp_config.no_attention)
+void set_no_attention(bool on);
+bool no_attention();
 
 // dW_aug[(K + with_bias) x Nout] = [X, 1]^T dY over all M rows, deterministic split-K over rows.
 // Result: out (+)= sum (accumulate flag).  part must hold chunks * (K+1) * Nout floats.
@@ -168,6 +171,8 @@ void launch_gather_max_bwd(const float *dA, const int *ARG, const float *Z, cons
                            float *dPre, int N, cudaStream_t s);
 
 void launch_attn_fwd(const float *qkv, float *o, float *lse, int N, int S, int M, cudaStream_t s);
+void launch_relu_v(const float *qkv, float *o, int N, cudaStream_t s);
+void launch_relu_v_bwd(const float *qkv, const float *dout, float *dqkv, float *dkvm, int N, cudaStream_t s);
 void launch_attn_bwd(const float *qkv, const float *o, const float *lse, const float *dout, float *dqkv,
                      float *dkvm, float *Dd, int N, int S, int M, cudaStream_t s);
 

@@ -286,6 +286,9 @@ inline unsigned nblk(size_t n, int t) { return (unsigned)((n + t - 1) / t); }
 
 static thread_local bool t_tc = false;
 void set_tensor_cores(bool on) { t_tc = on; }
+static thread_local bool t_noattn = false;
+void set_no_attention(bool on) { t_noattn = on; }
+bool no_attention() { return t_noattn; }
 
 void launch_gemm(const GemmArgs &a, cudaStream_t s) {
   if (a.M <= 0) return;

@@ -278,6 +278,35 @@ void launch_gather_max_bwd(const float *dA, const int *ARG, const float *Z, cons
   k_gather_max_bwd<<<blocks, 256, 0, s>>>(dA, ARG, Z, ptr, idx, dPre, N);
 }
 
+// no_attention ablation (NEXT-3, reading R34): o = ReLU(V) per node; backward dV = dO [V > 0],
+// dQ = dK = 0 and no memory rows
+__global__ void k_relu_v(const float *__restrict__ qkv, float *o, int N) {
+  const size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (size_t)N * 64) return;
+  const size_t i = e / 64, c = e % 64;
+  o[e] = fmaxf(qkv[i * 192 + 128 + c], 0.f);
+}
+__global__ void k_relu_v_bwd(const float *__restrict__ qkv, const float *__restrict__ dout, float *dqkv, float *dkvm,
+                             int N) {
+  const size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (size_t)N * 64) return;
+  const size_t i = e / 64, c = e % 64;
+  dqkv[i * 192 + c] = 0.f;
+  dqkv[i * 192 + 64 + c] = 0.f;
+  dqkv[i * 192 + 128 + c] = qkv[i * 192 + 128 + c] > 0.f ? dout[e] : 0.f;
+  dkvm[i * 128 + c] = 0.f;
+  dkvm[i * 128 + 64 + c] = 0.f;
+}
+
+void launch_relu_v(const float *qkv, float *o, int N, cudaStream_t s) {
+  note_launch();
+  k_relu_v<<<(unsigned)(((size_t)N * 64 + 255) / 256), 256, 0, s>>>(qkv, o, N);
+}
+void launch_relu_v_bwd(const float *qkv, const float *dout, float *dqkv, float *dkvm, int N, cudaStream_t s) {
+  note_launch();
+  k_relu_v_bwd<<<(unsigned)(((size_t)N * 64 + 255) / 256), 256, 0, s>>>(qkv, dout, dqkv, dkvm, N);
+}
+
 void launch_attn_fwd(const float *qkv, float *o, float *lse, int N, int S, int M, cudaStream_t s) {
   int nseg = (N + S - 1) / S;
   note_launch();

@@ -209,7 +209,8 @@ void layer_fwd(const WS &w, const Offs &off, const float *theta, int l, const fl
   GemmArgs g = gemm(N, kH, 192, L.a, kH, L.Wqkv, 192, 1, L.qkv, 192);
   g.bias = L.bqkv;
   launch_gemm(g, s);
-  launch_attn_fwd(L.qkv, L.o, L.lse, N, S, M, s);
+  if (no_attention()) launch_relu_v(L.qkv, L.o, N, s);
+  else launch_attn_fwd(L.qkv, L.o, L.lse, N, S, M, s);
   g = gemm(N, kH, kH, L.o, kH, L.Wo, kH, 1, L.x1, kH);
   g.bias = theta + off[b + BO];
   g.R = x; g.ldr = kH;
@@ -248,7 +249,8 @@ void layer_bwd(const WS &w, const Offs &off, const float *theta, int l, const fl
   launch_gemm(g, s);
   launch_wgrad(N, kH, kH, L.o, kH, kH, nullptr, 0, w.dx1, kH, true, w.part, w.part_floats, L.dWo, false, s);
   // attention backward: dqkv = [dQ | dK_own | dV_own], dkvm = [dK_mem | dV_mem]
-  launch_attn_bwd(L.qkv, L.o, L.lse, w.dout, w.dqkv, w.dkvm, w.dd, N, S, M, s);
+  if (no_attention()) launch_relu_v_bwd(L.qkv, w.dout, w.dqkv, w.dkvm, N, s);
+  else launch_attn_bwd(L.qkv, L.o, L.lse, w.dout, w.dqkv, w.dkvm, w.dd, N, S, M, s);
   // totals for the parameter gradients: dkvt = [dQ | dK_own + dK_mem | dV_own + dV_mem]
   note_launch();
   k_copy_cols<<<nblk((size_t)N * 64, 256), 256, 0, s>>>(w.dqkv, 192, w.dkvt, 192, N, 64);

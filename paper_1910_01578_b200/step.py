@@ -56,11 +56,12 @@ class PolicyStep:
 
     def __init__(self, graphs: List, d: int, seg_len: int, mem_len: int, superposition: bool, batch: int,
                  seed: int = 42, clip_eps: float = 0.2, entropy_coef: float = 0.01, mode: str = "samples",
-                 rank: int = 0, world: int = 1, device=None, tensor_cores: bool = False, cuda_graph: bool = False):
+                 rank: int = 0, world: int = 1, device=None, tensor_cores: bool = False, cuda_graph: bool = False,
+                 no_attention: bool = False):
         import torch
         self.torch = torch
         self.device = device if device is not None else torch.device("cuda", torch.cuda.current_device())
-        self.cfg = default_config(d, seg_len, mem_len, superposition, tensor_cores)
+        self.cfg = default_config(d, seg_len, mem_len, superposition, tensor_cores, no_attention)
         self.plan = make_plan(mode, rank, world, batch, len(graphs), entropy_coef,
                               [g[0].N * batch for g in graphs])
         self.seed, self.clip_eps = seed, clip_eps
@@ -193,12 +194,12 @@ class PPOTrainer:
     def __init__(self, gsrc, feat, topo_src, d: int, seg_len: int = 128, mem_len: int = 128,
                  superposition: bool = True, rollouts: int = 16, minibatch: int = 8, epochs: int = 4,
                  lr: float = 3e-4, clip_eps: float = 0.2, entropy_coef: float = 0.01, max_norm: float = 1.0,
-                 seed: int = 42, device=None, tensor_cores: bool = False):
+                 seed: int = 42, device=None, tensor_cores: bool = False, no_attention: bool = False):
         import torch
         from . import ADAM_SCRATCH
         self.torch = torch
         self.device = device if device is not None else torch.device("cuda", torch.cuda.current_device())
-        self.cfg = default_config(d, seg_len, mem_len, superposition, tensor_cores)
+        self.cfg = default_config(d, seg_len, mem_len, superposition, tensor_cores, no_attention)
         self.R, self.mb, self.epochs = rollouts, minibatch, epochs
         self.lr, self.clip_eps, self.entropy_coef, self.max_norm, self.seed = lr, clip_eps, entropy_coef, max_norm, seed
         self.st = _GraphState(gsrc, feat, topo_src, self.cfg, rollouts, rollouts, self.device)

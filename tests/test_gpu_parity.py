@@ -134,10 +134,11 @@ def test_cost_full_size_c4(gdp):
 
 
 # ------------------------------------------------------------------ policy network stages
-def run_step(gdp, g, W_d, S, M, sup, B, th, seed=42, step=0, old=None, eps=0.2, beta=0.01, scale=None, tc=False):
+def run_step(gdp, g, W_d, S, M, sup, B, th, seed=42, step=0, old=None, eps=0.2, beta=0.01, scale=None, tc=False,
+             na=False):
     X = workloads.features(g)
     G = gdp.Graph(g, X)
-    cfg = gdp.default_config(W_d, S, M, sup, tensor_cores=tc)
+    cfg = gdp.default_config(W_d, S, M, sup, tensor_cores=tc, no_attention=na)
     ws = torch.empty(gdp.workspace_size(G, cfg, B), dtype=torch.uint8, device="cuda")
     theta = torch.from_numpy(th).cuda()
     emb = torch.empty(g.N, 64, device="cuda")
@@ -166,6 +167,9 @@ CASES = {
     "mem_inf": (lambda: workloads.random_dag(300, p_edge=0.1, max_back=30, seed=4), 4, 64, -1, True),
     "no_superposition": (lambda: workloads.random_dag(200, p_edge=0.15, max_back=20, seed=5), 8, 48, 48, False),
     "short_memory": (lambda: workloads.random_dag(333, p_edge=0.1, max_back=50, seed=6), 5, 40, 17, True),
+    # NEXT-3 ablation: attention sublayers replaced by the per-node map (reading R34)
+    "no_attention": (lambda: workloads.random_dag(300, p_edge=0.1, max_back=30, seed=7), 4, 32, 32, True, True),
+    "no_attention_no_sup": (lambda: _perm_coloc_graph(), 3, 16, 16, False, True),
 }
 
 
@@ -184,18 +188,19 @@ def _perm_coloc_graph():
 
 @pytest.mark.parametrize("case", sorted(CASES))
 def test_policy_stages(gdp, case):
-    mk, d, S, M, sup = CASES[case]
+    mk, d, S, M, sup = CASES[case][:5]
+    na = len(CASES[case]) > 5 and CASES[case][5]
     g = mk()
     th = workloads.init_theta(workloads.F, d, seed=11, mode="random")
     B = 24
-    r = run_step(gdp, g, d, S, M, sup, B, th)
+    r = run_step(gdp, g, d, S, M, sup, B, th, na=na)
     pg = oracle.prepare(g, r["X"])
     # embed (a1-a4)
     E = oracle.embed(pg, th, d)
     ok, err, nbad = close(r["emb"], E)
     assert ok, ("embed", err, nbad)
     # place (a5-a10), stage-wise: oracle consumes the GPU embedding
-    z = oracle.place(pg, th, r["emb"], d, S, M, sup)
+    z = oracle.place(pg, th, r["emb"], d, S, M, sup, no_attention=na)
     ok, err, nbad = close(r["logits"], z, floor=LOGIT_FLOOR)
     assert ok, ("place", err, nbad)
     # sample (a11): shared Philox uniforms, excused only at CDF margins < 1e-5
@@ -211,8 +216,9 @@ def test_policy_stages(gdp, case):
     ok, err, _ = close(r["logprob"], want_lp)
     assert ok, ("logprob", err)
     # policy gradient (a14-a15): oracle on the GPU's placements / advantages, chained from theta
-    grad, _ = oracle.policy_grad(pg, th, d, S, M, sup, r["D"], r["adv"], loss_scale=1.0 / B, entropy_coef=0.01)
-    ok, err, nbad = close(r["grad"], grad)
+    grad, _ = oracle.policy_grad(pg, th, d, S, M, sup, r["D"], r["adv"], loss_scale=1.0 / B, entropy_coef=0.01,
+                                 no_attention=na)
+    ok, err, nbad = close(r["grad"], grad, floor=LOGIT_FLOOR)   # sums of N*B terms
     assert ok, ("grad", err, nbad)
 
 
