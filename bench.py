@@ -102,7 +102,8 @@ def oracle_placements_per_s(W, B_total: int, n_cost: int, threads: int):
     from oracle import simulate as Osim
     t_net = 0.0
     t_cost_per = 0.0
-    for g in W.graphs:
+    for i, g in enumerate(W.graphs):
+        dg = W.d_of(i)
         X = workloads.features(g)
         pg = oracle.prepare(g, X)
         th = workloads.init_theta(workloads.F, W.d, seed=7)
@@ -110,13 +111,14 @@ def oracle_placements_per_s(W, B_total: int, n_cost: int, threads: int):
         E = oracle.embed(pg, th, W.d)
         z = oracle.place(pg, th, E, W.d, W.seg_len, W.mem_len, W.superposition)
         U = Osa.uniforms(g.N, n_cost, W.seed, 0, 0)
-        D, _, _ = Osa.sample(z, U, pg.lead)
+        D, _, _ = Osa.sample(z[:, :dg], U, pg.lead)
         t1 = time.perf_counter()
-        topo = workloads.topology(g, W.d)
+        topo = workloads.topology(g, dg)
         r = Osim.simulate_batch(g, topo, D, threads=threads)
         t2 = time.perf_counter()
         A, _, _ = Osa.advantage(r["reward"], 0.0, 0)
-        oracle.policy_grad(pg, th, W.d, W.seg_len, W.mem_len, W.superposition, D, A, loss_scale=1.0 / n_cost)
+        oracle.policy_grad(pg, th, W.d, W.seg_len, W.mem_len, W.superposition, D, A, loss_scale=1.0 / n_cost,
+                           active=dg if dg < W.d else None)
         t3 = time.perf_counter()
         t_net += (t1 - t0) + (t3 - t2)
         t_cost_per += (t2 - t1) / n_cost
@@ -168,7 +170,8 @@ def config_json(W, args, mode: str = "samples"):
     par = (f"dp{args.gpus} (placements sharded)" if mode == "samples" else
            f"dp{args.gpus} (graphs sharded, LPT on N*B)")
     return {"workload": W.name, "graphs": [x.name for x in g], "nodes": [x.N for x in g],
-            "edges": [x.E for x in g], "devices_d": W.d, "seg_len": W.seg_len, "mem_len": W.mem_len,
+            "edges": [x.E for x in g], "devices_d": W.d, "devices_per_graph": W.ds, "seg_len": W.seg_len,
+            "mem_len": W.mem_len,
             "superposition": W.superposition, "batch_per_gpu": args.batch,
             "global_batch": args.batch * (args.gpus if mode == "samples" else 1), "parallelism": par,
             "l2": "flushed between timed steps (512 MiB write)"}
@@ -203,6 +206,30 @@ def run_train(args, W, gdp, dev):
                       "config": {"workload": W.name, "graph": g.name, "nodes": g.N, "devices_d": W.d}}))
 
 
+def run_zero_shot(args, W, gdp, dev):
+    """Informative line for NEXT-2 zero-shot placement of the config's first graph: embed, place,
+    greedy decode and the cost model on that one placement (latency, not the headline)."""
+    import torch
+    g = W.graphs[0]
+    X, topo = workloads.features(g), workloads.topology(g, W.d)
+    theta = torch.from_numpy(workloads.init_theta(workloads.F, W.d, seed=7)).to(dev)
+    for _ in range(args.warmup):
+        r = gdp.zero_shot(g, X, topo, theta, W.d, W.seg_len, W.mem_len, W.superposition, not args.fp32, dev)
+    ts = []
+    for _ in range(args.steps):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        r = gdp.zero_shot(g, X, topo, theta, W.d, W.seg_len, W.mem_len, W.superposition, not args.fp32, dev)
+        ts.append(time.perf_counter() - t0)
+    ms = 1000.0 * statistics.median(ts)
+    print(json.dumps({"metric": "GDP zero-shot placement latency (embed, place, greedy, cost)", "value": ms,
+                      "unit": "ms", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+                      "higher_is_better": False, "data": "synthetic",
+                      "makespan_ticks": int(r["makespan"][0]), "valid": int(r["valid"][0]),
+                      "config": {"workload": W.name, "graph": g.name, "nodes": g.N, "devices_d": W.d},
+                      "note": "wall clock around the public call incl. graph setup and the D2H of the report"}))
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -219,6 +246,8 @@ def main():
     ap.add_argument("--no-superposition", action="store_true", help="NEXT-3 ablation variant (gates == 1)")
     ap.add_argument("--cuda-graph", action="store_true",
                     help="replay the whole step as one CUDA graph (single process; no per-stage timings)")
+    ap.add_argument("--zero-shot", action="store_true",
+                    help="time NEXT-2 zero-shot placement (embed, place, greedy, cost of one placement)")
     ap.add_argument("--train", action="store_true",
                     help="time the NEXT-1 training update (PPOTrainer.update) instead of the policy step")
     args = ap.parse_args()
@@ -250,7 +279,10 @@ def main():
     if args.train:
         run_train(args, W, gdp, dev)
         return
-    graphs = [(g, workloads.features(g), workloads.topology(g, W.d)) for g in W.graphs]
+    if args.zero_shot:
+        run_zero_shot(args, W, gdp, dev)
+        return
+    graphs = [(g, workloads.features(g), workloads.topology(g, W.d_of(i))) for i, g in enumerate(W.graphs)]
     # C5 (several graphs) is graph-sharded with LPT on N*B; the others split samples
     mode = "graphs" if len(W.graphs) > 2 else "samples"
     ps = gdp.PolicyStep(graphs, W.d, W.seg_len, W.mem_len, W.superposition, W.batch, seed=W.seed,

@@ -73,6 +73,9 @@ typedef struct {
   int32_t no_attention;   /* ablation: 1 replaces every attention
                              sublayer (placer and conditioner) by the per-node map
                              o = ReLU(LN1(x) W_v + b_v) (reading R34); 0: attention */
+  int32_t active_devices; /* mixed device counts: the head has num_devices (D_max)
+                             outputs, sampling / log pi / greedy / the loss use the first
+                             active_devices (the rest masked to -inf, zero gradient); 0 = all */
 } gdp_config;
 
 /* One cost-model verdict per placement. */

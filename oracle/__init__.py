@@ -83,14 +83,19 @@ def logit_grad(pg: Prepared, logits: np.ndarray, D, adv, old_logprob, clip_eps, 
 
 def policy_grad(pg: Prepared, theta, d: int, S: int, M: int, superposition: bool, D, adv,
                 old_logprob=None, clip_eps: float = 0.2, entropy_coef: float = 0.01,
-                loss_scale: float = 1.0, mem_srcs: Optional[dict] = None, no_attention: bool = False):
+                loss_scale: float = 1.0, mem_srcs: Optional[dict] = None, no_attention: bool = False,
+                active: Optional[int] = None):
     """Gradient of L (model.policy_loss) w.r.t. the flat theta through place and
     embed (§3.1 "trained jointly ... in an end-to-end fashion").
+    `active` (NEXT-4 mixed device counts): only the first `active` head outputs enter the
+    softmax, the sampled placements and the loss.
     Returns (grad float64 [n_params], loss float)."""
     th = _theta(theta).requires_grad_(True)
     p = model.unflatten(th, pg.F, d)
     E = model.embed(pg.X, pg.ptr, pg.idx, p)
     logits = model.place(E, p, pg.order, S, M, superposition, mem_srcs=mem_srcs, no_attention=no_attention)
+    if active is not None:              # NEXT-4: head padded to d outputs, first `active` devices live;
+        logits = logits[:, :active]     # masking the rest to -inf is the same as dropping them
     L = model.policy_loss(logits, D, adv, pg.lead, old_logprob, clip_eps, entropy_coef, loss_scale)
     (g,) = torch.autograd.grad(L, th)
     return g.numpy(), float(L.detach())

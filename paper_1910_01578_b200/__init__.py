@@ -39,7 +39,8 @@ class Config(ctypes.Structure):
     _fields_ = [("hidden", ctypes.c_int32), ("heads", ctypes.c_int32), ("gnn_layers", ctypes.c_int32),
                 ("xl_layers", ctypes.c_int32), ("ffn", ctypes.c_int32), ("num_devices", ctypes.c_int32),
                 ("seg_len", ctypes.c_int32), ("mem_len", ctypes.c_int32), ("superposition", ctypes.c_int32),
-                ("tensor_cores", ctypes.c_int32), ("no_attention", ctypes.c_int32)]
+                ("tensor_cores", ctypes.c_int32), ("no_attention", ctypes.c_int32),
+                ("active_devices", ctypes.c_int32)]
 
 
 def lib():
@@ -130,12 +131,13 @@ def _stream(stream=None):
 
 # --------------------------------------------------------------------------- setup objects
 def default_config(d: int, seg_len: int = 128, mem_len: int = 128, superposition: bool = True,
-                   tensor_cores: bool = False, no_attention: bool = False) -> Config:
+                   tensor_cores: bool = False, no_attention: bool = False, active_devices: int = 0) -> Config:
     c = Config()
     _check(lib().gdp_default_config(d, ctypes.byref(c)), "gdp_default_config")
     c.seg_len, c.mem_len, c.superposition = seg_len, mem_len, int(bool(superposition))
     c.tensor_cores = int(bool(tensor_cores))
     c.no_attention = int(bool(no_attention))
+    c.active_devices = int(active_devices)
     return c
 
 

@@ -70,8 +70,12 @@ static gdp_status check_config(const gdp_config *c) {
   if (c->mem_len < -1) return fail(GDP_ERR_ARG, "mem_len must be >= -1");
   if (c->tensor_cores != 0 && c->tensor_cores != 1) return fail(GDP_ERR_ARG, "tensor_cores must be 0 or 1");
   if (c->no_attention != 0 && c->no_attention != 1) return fail(GDP_ERR_ARG, "no_attention must be 0 or 1");
+  if (c->active_devices < 0 || c->active_devices > c->num_devices)
+    return fail(GDP_ERR_ARG, "active_devices must be in 0..num_devices");
   return GDP_OK;
 }
+
+int active_devices(const gdp_config *c) { return c->active_devices > 0 ? c->active_devices : c->num_devices; }
 
 // ------------------------------------------------------------------ workspace
 static size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
@@ -230,6 +234,7 @@ gdp_status gdp_default_config(int32_t d, gdp_config *out) {
   out->superposition = 1;
   out->tensor_cores = 0;
   out->no_attention = 0;
+  out->active_devices = 0;
   return GDP_OK;
 }
 
@@ -537,7 +542,8 @@ static gdp_status sample_impl(gdp_graph g, const gdp_config *c, const float *log
   st = carve_any(g, c->num_devices, 1, ws, ws_bytes, &w);
   if (st != GDP_OK) return st;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  launch_sample(logits, g->leader, g->has_coloc, g->N, c->num_devices, B, seed, sample_offset, step, step_dev, w.cdf,
+  launch_sample(logits, c->num_devices, g->leader, g->has_coloc, g->N, active_devices(c), B, seed, sample_offset,
+                step, step_dev, w.cdf,
                 w.logp, w.lastpos, placements, logprob, s);
   GDP_LAUNCH_CHECK("gdp_sample");
   return GDP_OK;
@@ -566,8 +572,8 @@ gdp_status gdp_logprob(gdp_graph g, const gdp_config *c, const float *logits, co
   st = carve_any(g, c->num_devices, 1, ws, ws_bytes, &w);
   if (st != GDP_OK) return st;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  launch_node_prep(logits, g->N, c->num_devices, w.cdf, w.logp, w.lastpos, s);
-  launch_logprob(w.logp, g->leader, placements, g->N, c->num_devices, B, logprob, s);
+  launch_node_prep(logits, c->num_devices, g->N, active_devices(c), w.cdf, w.logp, w.lastpos, s);
+  launch_logprob(w.logp, g->leader, placements, g->N, active_devices(c), B, logprob, s);
   GDP_LAUNCH_CHECK("gdp_logprob");
   return GDP_OK;
 }
@@ -578,13 +584,13 @@ gdp_status gdp_greedy(gdp_graph g, const gdp_config *c, const float *logits, uin
   gdp_status st = check_config(c);
   if (st != GDP_OK) return st;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  launch_greedy(logits, g->leader, g->N, c->num_devices, placement, s);
+  launch_greedy(logits, c->num_devices, g->leader, g->N, active_devices(c), placement, s);
   if (logprob) {
     WS w;
     st = carve_any(g, c->num_devices, 1, ws, ws_bytes, &w);
     if (st != GDP_OK) return st;
-    launch_node_prep(logits, g->N, c->num_devices, w.cdf, w.logp, w.lastpos, s);
-    launch_logprob(w.logp, g->leader, placement, g->N, c->num_devices, 1, logprob, s);
+    launch_node_prep(logits, c->num_devices, g->N, active_devices(c), w.cdf, w.logp, w.lastpos, s);
+    launch_logprob(w.logp, g->leader, placement, g->N, active_devices(c), 1, logprob, s);
   }
   GDP_LAUNCH_CHECK("gdp_greedy");
   return GDP_OK;

@@ -185,11 +185,12 @@ void launch_add(const float *a, int lda, const float *b, int ldb, float *c, int 
 void launch_fill_rows(float *dst, const float *row, float scale, int N, int C, cudaStream_t s);
 
 // sampling / loss
-void launch_sample(const float *logits, const int *leader, bool has_coloc, int N, int d, int B, uint64_t seed,
+void launch_sample(const float *logits, int ld, const int *leader, bool has_coloc, int N, int d, int B, uint64_t seed,
                    uint64_t offset, uint64_t step, const uint64_t *step_ptr, float *cdf, float *logp, int *lastpos,
                    uint8_t *D, float *logprob, cudaStream_t s);
-void launch_node_prep(const float *logits, int N, int d, float *cdf, float *logp, int *lastpos, cudaStream_t s);
-void launch_logit_grad(const float *logits, const uint8_t *D, const int *leader, const double *adv,
+void launch_node_prep(const float *logits, int ld, int N, int d, float *cdf, float *logp, int *lastpos,
+                      cudaStream_t s);
+void launch_logit_grad(const float *logits, int ld, const uint8_t *D, const int *leader, const double *adv,
                        const float *logprob, const float *old_logprob, float eps, float beta, float scale,
                        int N, int d, int B, double *wb, float *dlog, cudaStream_t s);
 
@@ -198,7 +199,9 @@ constexpr int kAdamScratch = 1024;   // doubles of caller scratch for gdp_clip_a
 int adam_parts();
 void launch_logprob(const float *logp, const int *leader, const uint8_t *D, int N, int d, int B, float *logprob,
                     cudaStream_t s);
-void launch_greedy(const float *logits, const int *leader, int N, int d, uint8_t *D, cudaStream_t s);
+void launch_greedy(const float *logits, int ld, const int *leader, int N, int d, uint8_t *D, cudaStream_t s);
+// devices a call samples / scores over: gdp_config.active_devices, or num_devices when 0
+int active_devices(const gdp_config *c);
 void launch_clip_adam(const float *g, long long n, double max_norm, double lr, double b1, double b2, double eps,
                       double c1, double c2, float *theta, float *m, float *v, double *scratch, double *norm_out,
                       cudaStream_t s);

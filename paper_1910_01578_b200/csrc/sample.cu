@@ -23,10 +23,12 @@ __device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint2 k) {
   return c;
 }
 
-__global__ void k_node_prep(const float *logits, int N, int d, float *cdf, float *logp, int *lastpos) {
+// logits rows have stride ld >= d: a head padded to ld devices of which the first d are active
+// (mixed device counts); cdf / logp are stored with stride d
+__global__ void k_node_prep(const float *logits, int ld, int N, int d, float *cdf, float *logp, int *lastpos) {
   int v = blockIdx.x * blockDim.x + threadIdx.x;
   if (v >= N) return;
-  const float *z = logits + (size_t)v * d;
+  const float *z = logits + (size_t)v * ld;
   float mx = z[0];
   for (int k = 1; k < d; k++) mx = fmaxf(mx, z[k]);
   float e[kMaxD], s = 0.f;
@@ -111,7 +113,7 @@ __global__ void k_weights(const double *adv, const float *logprob, const float *
   wb[b] = (rho * A <= cl * A) ? rho * A : 0.0;
 }
 
-__global__ void k_logit_grad(const float *__restrict__ logits, const uint8_t *__restrict__ D,
+__global__ void k_logit_grad(const float *__restrict__ logits, int ld, const uint8_t *__restrict__ D,
                              const int *__restrict__ leader, const double *__restrict__ wb, float beta, float scale,
                              int N, int d, int B, float *dlog) {
   extern __shared__ double swb[];
@@ -119,7 +121,7 @@ __global__ void k_logit_grad(const float *__restrict__ logits, const uint8_t *__
   __syncthreads();
   int v = blockIdx.x * blockDim.x + threadIdx.x;
   if (v >= N) return;
-  const float *z = logits + (size_t)v * d;
+  const float *z = logits + (size_t)v * ld;
   float mx = z[0];
   for (int k = 1; k < d; k++) mx = fmaxf(mx, z[k]);
   float e[kMaxD], s = 0.f;
@@ -152,17 +154,18 @@ __global__ void k_logit_grad(const float *__restrict__ logits, const uint8_t *__
   for (int k = 0; k < d; k++) {
     float g = (float)(-(double)scale * (acc[k] - (double)p[k] * sw));
     g += bn * p[k] * (lp[k] + Hv);
-    dlog[(size_t)v * d + k] = g;
+    dlog[(size_t)v * ld + k] = g;
   }
+  for (int k = d; k < ld; k++) dlog[(size_t)v * ld + k] = 0.f;   // masked head columns
 }
 
 }  // namespace
 
-void launch_sample(const float *logits, const int *leader, bool has_coloc, int N, int d, int B, uint64_t seed,
+void launch_sample(const float *logits, int ld, const int *leader, bool has_coloc, int N, int d, int B, uint64_t seed,
                    uint64_t offset, uint64_t step, const uint64_t *step_ptr, float *cdf, float *logp, int *lastpos,
                    uint8_t *D, float *logprob, cudaStream_t s) {
   note_launch();
-  k_node_prep<<<(N + 255) / 256, 256, 0, s>>>(logits, N, d, cdf, logp, lastpos);
+  k_node_prep<<<(N + 255) / 256, 256, 0, s>>>(logits, ld, N, d, cdf, logp, lastpos);
   note_launch();
   k_sample<<<B, ST, 0, s>>>(cdf, logp, lastpos, leader, N, d, seed, offset, step, step_ptr, D, logprob);
   if (has_coloc) {
@@ -172,12 +175,13 @@ void launch_sample(const float *logits, const int *leader, bool has_coloc, int N
   }
 }
 
-void launch_node_prep(const float *logits, int N, int d, float *cdf, float *logp, int *lastpos, cudaStream_t s) {
+void launch_node_prep(const float *logits, int ld, int N, int d, float *cdf, float *logp, int *lastpos,
+                      cudaStream_t s) {
   note_launch();
-  k_node_prep<<<(N + 255) / 256, 256, 0, s>>>(logits, N, d, cdf, logp, lastpos);
+  k_node_prep<<<(N + 255) / 256, 256, 0, s>>>(logits, ld, N, d, cdf, logp, lastpos);
 }
 
-void launch_logit_grad(const float *logits, const uint8_t *D, const int *leader, const double *adv,
+void launch_logit_grad(const float *logits, int ld, const uint8_t *D, const int *leader, const double *adv,
                        const float *logprob, const float *old_logprob, float eps, float beta, float scale,
                        int N, int d, int B, double *wb, float *dlog, cudaStream_t s) {
   note_launch();
@@ -185,7 +189,7 @@ void launch_logit_grad(const float *logits, const uint8_t *D, const int *leader,
   size_t smem = (size_t)B * sizeof(double);
   if (smem > 48 * 1024) cudaFuncSetAttribute(k_logit_grad, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   note_launch();
-  k_logit_grad<<<(N + 127) / 128, 128, smem, s>>>(logits, D, leader, wb, beta, scale, N, d, B, dlog);
+  k_logit_grad<<<(N + 127) / 128, 128, smem, s>>>(logits, ld, D, leader, wb, beta, scale, N, d, B, dlog);
 }
 
 }  // namespace gdp

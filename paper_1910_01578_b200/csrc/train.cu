@@ -36,11 +36,11 @@ __global__ void __launch_bounds__(LT) k_logprob(const float *__restrict__ logp, 
 
 // greedy decode (NEXT-2): per node the argmax of its leader's logits (strict >, so
 // ties go to the lowest device id); non-leaders thereby copy their leader
-__global__ void k_greedy(const float *__restrict__ logits, const int *__restrict__ leader, int N, int d,
+__global__ void k_greedy(const float *__restrict__ logits, int ld, const int *__restrict__ leader, int N, int d,
                          uint8_t *D) {
   const int v = blockIdx.x * blockDim.x + threadIdx.x;
   if (v >= N) return;
-  const float *z = logits + (size_t)leader[v] * d;
+  const float *z = logits + (size_t)leader[v] * ld;
   int best = 0;
   float bz = z[0];
   for (int k = 1; k < d; k++)
@@ -133,9 +133,9 @@ int sm_count() {
 
 int adam_parts() { return 2 * sm_count() < kAdamScratch ? 2 * sm_count() : kAdamScratch; }
 
-void launch_greedy(const float *logits, const int *leader, int N, int d, uint8_t *D, cudaStream_t s) {
+void launch_greedy(const float *logits, int ld, const int *leader, int N, int d, uint8_t *D, cudaStream_t s) {
   note_launch();
-  k_greedy<<<(N + 255) / 256, 256, 0, s>>>(logits, leader, N, d, D);
+  k_greedy<<<(N + 255) / 256, 256, 0, s>>>(logits, ld, leader, N, d, D);
 }
 
 void launch_logprob(const float *logp, const int *leader, const uint8_t *D, int N, int d, int B, float *logprob,

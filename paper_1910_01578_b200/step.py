@@ -25,6 +25,12 @@ class _GraphState:
         import torch
         self.g = Graph(gsrc, feat)
         self.t = Topo(topo_src)
+        td = int(topo_src.d)
+        if td > cfg.num_devices:
+            raise ValueError("topology has %d devices, the head only %d" % (td, cfg.num_devices))
+        if td < cfg.num_devices:            # NEXT-4: head padded to num_devices, first td live
+            cfg = Config.from_buffer_copy(cfg)
+            cfg.active_devices = td
         self.cfg = cfg
         self.N, self.F = self.g.N, self.g.F
         self.B, self.B_total = B_local, B_total
@@ -35,8 +41,8 @@ class _GraphState:
         self.placements = torch.empty(B_local, self.N, dtype=torch.uint8, device=device)
         self.logprob = torch.empty(B_local, dtype=torch.float32, device=device)
         self.rep = torch.empty(B_local, REPORT_BYTES, dtype=torch.uint8, device=device)
-        self.peak = torch.empty(B_local, d, dtype=torch.int64, device=device)
-        self.busy = torch.empty(B_local, d, dtype=torch.int64, device=device)
+        self.peak = torch.empty(B_local, td, dtype=torch.int64, device=device)
+        self.busy = torch.empty(B_local, td, dtype=torch.int64, device=device)
         self.reward = torch.empty(B_local, dtype=torch.float64, device=device)
         self.reward_all = torch.empty(B_total, dtype=torch.float64, device=device)
         self.adv_all = torch.empty(B_total, dtype=torch.float64, device=device)
@@ -132,15 +138,15 @@ class PolicyStep:
                 st.stream.wait_stream(main)
             with torch.cuda.stream(st.stream if st.stream is not None else main):
                 self._ev("embed0", timed)
-                gdp_embed(st.g, self.cfg, theta, st.node_emb, st.ws)
+                gdp_embed(st.g, st.cfg, theta, st.node_emb, st.ws)
                 self._ev("place0", timed)
-                gdp_place(st.g, self.cfg, theta, st.node_emb, st.logits, st.ws)
+                gdp_place(st.g, st.cfg, theta, st.node_emb, st.logits, st.ws)
                 self._ev("sample0", timed)
                 if dev_step:
-                    gdp_sample_at(st.g, self.cfg, st.logits, st.B, self.seed, P.sample_offset, self.step_dev,
+                    gdp_sample_at(st.g, st.cfg, st.logits, st.B, self.seed, P.sample_offset, self.step_dev,
                                   st.placements, st.logprob, st.ws)
                 else:
-                    gdp_sample(st.g, self.cfg, st.logits, st.B, self.seed, P.sample_offset, step, st.placements,
+                    gdp_sample(st.g, st.cfg, st.logits, st.B, self.seed, P.sample_offset, step, st.placements,
                                st.logprob, st.ws)
                 self._ev("cost0", timed)
                 gdp_cost(st.g, st.t, st.placements, st.B, st.rep, st.peak, st.busy, st.reward, st.ws)
@@ -176,7 +182,7 @@ class PolicyStep:
         if grad is not self.grad:
             grad.zero_()
         self._ev("grad0", timed)
-        gdp_policy_grad(st.g, self.cfg, theta, st.logits, st.placements, st.B, adv, st.logprob, None,
+        gdp_policy_grad(st.g, st.cfg, theta, st.logits, st.placements, st.B, adv, st.logprob, None,
                         self.clip_eps, P.entropy_coef, P.loss_scale, grad, st.ws)
         self._ev("grad1", timed)
 
@@ -218,9 +224,9 @@ class PPOTrainer:
     def rollouts(self, theta):
         """embed -> place -> sample -> cost -> advantage; returns (placements, adv, old logprob)."""
         st = self.st
-        gdp_embed(st.g, self.cfg, theta, st.node_emb, st.ws)
-        gdp_place(st.g, self.cfg, theta, st.node_emb, st.logits, st.ws)
-        gdp_sample(st.g, self.cfg, st.logits, self.R, self.seed, 0, self.update_idx, st.placements, st.logprob, st.ws)
+        gdp_embed(st.g, st.cfg, theta, st.node_emb, st.ws)
+        gdp_place(st.g, st.cfg, theta, st.node_emb, st.logits, st.ws)
+        gdp_sample(st.g, st.cfg, st.logits, self.R, self.seed, 0, self.update_idx, st.placements, st.logprob, st.ws)
         gdp_cost(st.g, st.t, st.placements, self.R, st.rep, st.peak, st.busy, st.reward, st.ws)
         gdp_advantage(st.reward, self.R, st.run_sum, st.run_count, st.adv_all)
         return st.placements, st.adv_all, st.logprob
@@ -232,12 +238,12 @@ class PPOTrainer:
         for _ in range(self.epochs):
             for s0 in range(0, R, mb):
                 nb = min(mb, R - s0)
-                gdp_embed(st.g, self.cfg, theta, st.node_emb, st.ws)
-                gdp_place(st.g, self.cfg, theta, st.node_emb, st.logits, st.ws)
+                gdp_embed(st.g, st.cfg, theta, st.node_emb, st.ws)
+                gdp_place(st.g, st.cfg, theta, st.node_emb, st.logits, st.ws)
                 Pm = placements[s0:s0 + nb]
-                gdp_logprob(st.g, self.cfg, st.logits, Pm, nb, self.logprob_new, st.ws)
+                gdp_logprob(st.g, st.cfg, st.logits, Pm, nb, self.logprob_new, st.ws)
                 self.grad.zero_()
-                gdp_policy_grad(st.g, self.cfg, theta, st.logits, Pm, nb, adv[s0:s0 + nb], self.logprob_new,
+                gdp_policy_grad(st.g, st.cfg, theta, st.logits, Pm, nb, adv[s0:s0 + nb], self.logprob_new,
                                 old_logprob[s0:s0 + nb], self.clip_eps, self.entropy_coef, 1.0 / nb, self.grad,
                                 st.ws)
                 self.t += 1
@@ -261,9 +267,9 @@ def zero_shot(gsrc, feat, topo_src, theta, d: int, seg_len: int = 128, mem_len: 
     device = device if device is not None else torch.device("cuda", torch.cuda.current_device())
     cfg = default_config(d, seg_len, mem_len, superposition, tensor_cores)
     st = _GraphState(gsrc, feat, topo_src, cfg, 1, 1, device)
-    gdp_embed(st.g, cfg, theta, st.node_emb, st.ws)
-    gdp_place(st.g, cfg, theta, st.node_emb, st.logits, st.ws)
-    gdp_greedy(st.g, cfg, st.logits, st.placements[0], st.logprob, st.ws)
+    gdp_embed(st.g, st.cfg, theta, st.node_emb, st.ws)
+    gdp_place(st.g, st.cfg, theta, st.node_emb, st.logits, st.ws)
+    gdp_greedy(st.g, st.cfg, st.logits, st.placements[0], st.logprob, st.ws)
     gdp_cost(st.g, st.t, st.placements, 1, st.rep, st.peak, st.busy, st.reward, st.ws)
     r = st.reports()
     r["placement"] = st.placements[0].cpu().numpy()

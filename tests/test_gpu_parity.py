@@ -135,10 +135,10 @@ def test_cost_full_size_c4(gdp):
 
 # ------------------------------------------------------------------ policy network stages
 def run_step(gdp, g, W_d, S, M, sup, B, th, seed=42, step=0, old=None, eps=0.2, beta=0.01, scale=None, tc=False,
-             na=False):
+             na=False, active=0):
     X = workloads.features(g)
     G = gdp.Graph(g, X)
-    cfg = gdp.default_config(W_d, S, M, sup, tensor_cores=tc, no_attention=na)
+    cfg = gdp.default_config(W_d, S, M, sup, tensor_cores=tc, no_attention=na, active_devices=active)
     ws = torch.empty(gdp.workspace_size(G, cfg, B), dtype=torch.uint8, device="cuda")
     theta = torch.from_numpy(th).cuda()
     emb = torch.empty(g.N, 64, device="cuda")
@@ -170,6 +170,8 @@ CASES = {
     # NEXT-3 ablation: attention sublayers replaced by the per-node map (reading R34)
     "no_attention": (lambda: workloads.random_dag(300, p_edge=0.1, max_back=30, seed=7), 4, 32, 32, True, True),
     "no_attention_no_sup": (lambda: _perm_coloc_graph(), 3, 16, 16, False, True),
+    # NEXT-4: head padded to 8 outputs, 3 devices active (-inf masking)
+    "masked_head": (lambda: _perm_coloc_graph(), 8, 32, 32, True, False, 3),
 }
 
 
@@ -190,10 +192,12 @@ def _perm_coloc_graph():
 def test_policy_stages(gdp, case):
     mk, d, S, M, sup = CASES[case][:5]
     na = len(CASES[case]) > 5 and CASES[case][5]
+    act = CASES[case][6] if len(CASES[case]) > 6 else 0
     g = mk()
     th = workloads.init_theta(workloads.F, d, seed=11, mode="random")
     B = 24
-    r = run_step(gdp, g, d, S, M, sup, B, th, na=na)
+    r = run_step(gdp, g, d, S, M, sup, B, th, na=na, active=act)
+    da = act or d                                   # devices live in sampling and the loss
     pg = oracle.prepare(g, r["X"])
     # embed (a1-a4)
     E = oracle.embed(pg, th, d)
@@ -205,10 +209,11 @@ def test_policy_stages(gdp, case):
     assert ok, ("place", err, nbad)
     # sample (a11): shared Philox uniforms, excused only at CDF margins < 1e-5
     U = Osa.uniforms(g.N, B, 42, 0, 0)
-    D, _, margin = Osa.sample(r["logits"], U, pg.lead)
+    D, _, margin = Osa.sample(r["logits"][:, :da], U, pg.lead)
     mism = (D != r["D"]) & (margin >= 1e-5)
     assert not mism.any(), ("sample", np.argwhere(mism)[:5])
-    zl = r["logits"].astype(np.float64)
+    assert r["D"].max() < da
+    zl = r["logits"][:, :da].astype(np.float64)
     lpv = zl - zl.max(1, keepdims=True)
     lpv = lpv - np.log(np.exp(lpv).sum(1, keepdims=True))
     isl = pg.lead == np.arange(g.N)
@@ -217,7 +222,7 @@ def test_policy_stages(gdp, case):
     assert ok, ("logprob", err)
     # policy gradient (a14-a15): oracle on the GPU's placements / advantages, chained from theta
     grad, _ = oracle.policy_grad(pg, th, d, S, M, sup, r["D"], r["adv"], loss_scale=1.0 / B, entropy_coef=0.01,
-                                 no_attention=na)
+                                 no_attention=na, active=act or None)
     ok, err, nbad = close(r["grad"], grad, floor=LOGIT_FLOOR)   # sums of N*B terms
     assert ok, ("grad", err, nbad)
 
@@ -483,3 +488,24 @@ def test_cuda_graph_step_matches_eager(gdp, cfg):
         for a, b in zip(pe.states, pgr.states):
             assert torch.equal(a.reward, b.reward) and torch.equal(a.placements, b.placements), (cfg, s)
     assert pgr._graph is not None
+
+
+def test_mixed_device_counts_step(gdp):
+    """NEXT-4: one PolicyStep over graphs with 2, 4 and 8 devices (head padded to 8): each graph's
+    placements stay below its own device count and its sampled placements / rewards equal those
+    of a single-graph step with the same masked configuration."""
+    gs = [workloads.random_dag(200, p_edge=0.1, max_back=20, seed=s) for s in (31, 32, 33)]
+    ds = [2, 4, 8]
+    graphs = [(g, workloads.features(g), workloads.topology(g, dg)) for g, dg in zip(gs, ds)]
+    theta = torch.from_numpy(workloads.init_theta(workloads.F, 8, seed=7, mode="random")).cuda()
+    ps = gdp.PolicyStep(graphs, 8, 32, 32, True, 16)
+    ps.run(theta)
+    torch.cuda.synchronize()
+    for st, dg, item in zip(ps.states, ds, graphs):
+        assert int(st.placements.max()) < dg and st.cfg.active_devices == (dg if dg < 8 else 0)
+        one = gdp.PolicyStep([item], 8, 32, 32, True, 16)
+        one.run(theta)
+        torch.cuda.synchronize()
+        assert torch.equal(one.states[0].placements, st.placements)
+        assert torch.equal(one.states[0].reward, st.reward)
+    assert torch.isfinite(ps.grad).all()

@@ -81,3 +81,43 @@ def test_no_attention_finite_differences():
     for i, (name, _) in enumerate(spec):
         if name.endswith((".Wq", ".bq", ".Wk", ".bk")):
             assert np.all(grad[offs[i]:offs[i + 1]] == 0.0), name
+
+
+def _truncate_head(th8, F, d8, d):
+    """theta of a d-device model whose head is the first d columns of a d8-device model's."""
+    s8, s = workloads.param_spec(F, d8), workloads.param_spec(F, d)
+    o8 = np.cumsum([0] + [int(np.prod(x)) for _, x in s8])
+    parts = []
+    for i, (name, shape) in enumerate(s8):
+        blk = th8[o8[i]:o8[i + 1]].reshape(shape)
+        if name == "head.W":
+            blk = blk[:, :d]
+        elif name == "head.b":
+            blk = blk[:d]
+        parts.append(blk.ravel())
+    out = np.concatenate(parts)
+    assert out.size == sum(int(np.prod(x)) for _, x in s)
+    return out
+
+
+def test_masked_head_equals_smaller_head():
+    """NEXT-4: a head padded to 8 outputs with only the first 3 active is the 3-device model whose
+    head is those 3 columns -- same logits, same gradient on every shared parameter, zero gradient
+    on the masked columns."""
+    g, pg, _, D, adv = _small_case(4, N=11, d=3, coloc=False)
+    th8 = workloads.init_theta(37, 8, seed=21, mode="random")
+    th3 = _truncate_head(th8, 37, 8, 3)
+    z8 = oracle.place(pg, th8, oracle.embed(pg, th8, 8), 8, 4, 4, True)
+    z3 = oracle.place(pg, th3, oracle.embed(pg, th3, 3), 3, 4, 4, True)
+    assert np.allclose(z8[:, :3], z3, rtol=0, atol=1e-13)
+    g8, L8 = oracle.policy_grad(pg, th8, 8, 4, 4, True, D, adv, loss_scale=0.5, active=3)
+    g3, L3 = oracle.policy_grad(pg, th3, 3, 4, 4, True, D, adv, loss_scale=0.5)
+    assert abs(L8 - L3) < 1e-12
+    assert np.allclose(_truncate_head(g8, 37, 8, 3), g3, rtol=0, atol=1e-12)
+    s8 = workloads.param_spec(37, 8)
+    o8 = np.cumsum([0] + [int(np.prod(x)) for _, x in s8])
+    for i, (name, shape) in enumerate(s8):
+        if name == "head.W":
+            assert np.all(g8[o8[i]:o8[i + 1]].reshape(shape)[:, 3:] == 0.0)
+        if name == "head.b":
+            assert np.all(g8[o8[i]:o8[i + 1]][3:] == 0.0)

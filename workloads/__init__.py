@@ -495,6 +495,10 @@ class Workload:
     batch: int            # sampled placements per graph per GPU
     superposition: bool = True
     seed: int = 42        # Philox key
+    ds: Optional[List[int]] = None   # per-graph device counts (NEXT-4 mixed batch); None = d for all
+
+    def d_of(self, i: int) -> int:
+        return self.ds[i] if self.ds else self.d
 
 
 def config(name: str, batch: Optional[int] = None, mem_len: Optional[int] = None) -> Workload:
@@ -516,6 +520,10 @@ def config(name: str, batch: Optional[int] = None, mem_len: Optional[int] = None
                    amoeba(seed=s + 2, name=f"amoeba_{i}"),
                    transformer_xl(layers=4, chunks=185, seed=s + 3, name=f"txl4_{i}")]
         w = Workload("c5_mixed8_d4", gs, d=4, seg_len=128, mem_len=128, batch=64)
+    elif name == "c5m":
+        # NEXT-4: the C5 batch with a different device count per graph (head padded to 8)
+        w = config("c5", batch, mem_len)
+        w.name, w.d, w.ds = "c5m_mixed8_d2-8", 8, [2, 4, 8, 4, 8, 2, 4, 8]
     else:
         raise KeyError(name)
     if batch is not None:
