@@ -14,6 +14,7 @@ run c4_fp32 --config c4 --fp32
 run c1_graph --config c1 --cuda-graph
 run c4_noattn --config c4 --no-attention
 run c4_nosup --config c4 --no-superposition
+run c5m --config c5m
 run c5_graph --config c5 --cuda-graph
 timeout 900 python bench.py --train --config c4 --steps 3 --warmup 1 > $OUT/c4_train.line 2>/dev/null
 timeout 900 python bench.py --zero-shot --config c4 --steps 3 --warmup 1 > $OUT/c4_zeroshot.line 2>/dev/null
