@@ -1,3 +1,2 @@
 python -c "import __graft_entry__ as g; g.build()" 
-timeout 1500 python -m pytest tests -m gpu -x -q 2>&1 | tail -3
-timeout 900 python bench.py --config c5m --steps 3 --warmup 2 --no-cpu-baseline 2>/dev/null | tail -1 | head -c 400; echo
+for dbg in 0 5 6; do echo "dbg $dbg"; GDP_COST_DBG=$dbg timeout 300 python tools/run_cost.py --reps 2 2>&1 | grep "cost 256" | tail -1; done

@@ -1,0 +1,759 @@
+// Cost model, windowed multi-warp kernel (the default when its preconditions hold; k_cost3 in
+// cost2.cu otherwise).  Same event semantics as the oracle (SPEC.md:275-284 `simulate`, O11 and
+// the readings R19/R20 in DESIGN.md); this formulation runs the devices of one placement in
+// parallel, one warp per device, in windows of simulated time:
+//
+//  * every cross-device transfer takes at least L = min latency >= 1 tick, so an op finishing
+//    at tick tau in the window [T, T + W) (W <= L) can only affect another device at tick
+//    >= T + W.  Inside a window the devices are therefore independent: warp q processes the
+//    events of device q in time order (arrivals on its incoming channels, its finish,
+//    its dispatch) without hearing from the others; the warps meet at a named barrier at the
+//    end of the window and jump to the next window start (the earliest pending event);
+//  * the schedule never depends on memory, so memory is accounted for off the critical path:
+//    each device warp logs one (tick, delta) entry per local instant (its own copies, frees,
+//    allocations) in tick order; a producer's output dies at the LAST finish tick among its
+//    consumers (each consumer finish does an atomic max on the producer's death tick, the one
+//    that brings the counter to zero queues the producer in the window's death list); two
+//    window boundaries later the producer's device warp reads the settled death ticks
+//    (prefetched), sorts the window's few deaths and appends them to its death log, which is
+//    therefore sorted too; after the simulation each device warp merges its two sorted logs
+//    in parallel (lane chunks + a scan) for its peak.  No warp beyond the d device warps, so
+//    2 CTAs per SM keep 128 registers per thread.
+// Requires: every op duration >= 1 (no zero-duration rounds) and L >= 1 (host checks).
+#include <climits>
+#include <cstdlib>
+
+#include "common.cuh"
+#include "cost2.cuh"
+#include "cost_util.cuh"
+
+namespace gdp {
+namespace {
+using namespace cu;
+
+constexpr int WMAX = 8;    // window length cap (ticks)
+constexpr int DK = 16;     // deaths per window and device staged in shared memory (rest: overflow list)
+constexpr int SO4 = 8;     // staged out-edge records per slot
+constexpr int SI4 = 8;     // staged in-edge records per slot (2 * SO4 + SI4 = 24 staging lanes)
+constexpr int KF4 = 4;     // FIFO entries kept in smem per device
+constexpr int KC4 = 4;     // prefetched channel entries per channel
+constexpr int NINC4 = 8;   // ops made available at one local instant (overflow -> global)
+
+struct Smem4 {
+  NRec st_out[8][2][SO4];
+  IRec st_in[8][2][SI4];
+  Ent fc[8][KF4];
+  Ent cc[64][KC4];                 // consumer-side prefetch ring of channel c = 8k + q
+  NRec inc[8][NINC4];
+  NRec run[8];                     // record of the op running on each device
+  int run_slot[8];
+  unsigned long long smb[8][2];    // mbarrier of each staging slot (bulk copies complete_tx)
+  unsigned acc[8][3];              // memory delta of the current local instant per device (16+16+32 bits)
+  int dn[3][8];                    // deaths per window slot (w % 3) and producer device
+  int dl_u[3][8][DK], dl_t[3][8][DK];
+  long long dl_b[3][8][DK];
+  int ovf_n, ovf_start[3];         // overflow death list (entries beyond DK)
+  int moff[8];                     // memory-log region of each device
+  int cfree[64], ctail[64], cstamp[64];                        // producer side (warp k)
+  int pfirst[2][64], ptail[2][64];   // published per window parity: first push's arrival, tail
+  int tn[3];                       // next window start, atomic min over devices' next events and first pushes
+  int phs[2][64];                  // consumer head at the start of window w (parity w & 1)
+  int coff[64], ccnt[64];
+  int doff[8], ftail0[8], opcnt[8];
+  long long stat[8], busyv[8];
+  int flag, oom, mk, disp, nwin;
+  unsigned long long cross;
+};
+
+struct Scratch4 {   // per-placement global scratch (same prefix as k_cost2 / k_cost3)
+  size_t fifo, chq, ov, bigc, dtick, mlog, dlog, dovf, total;
+};
+struct MemEnt {     // memory-log entry: delta at tick (local log) or -bytes at a death tick
+  int tick, pad;
+  long long delta;
+};
+struct DeathEnt {   // overflow death: producer, its bytes, window slot and device
+  int u, slot_dev;
+  long long bytes;
+};
+__host__ __device__ inline Scratch4 scratch4_layout(int N, long long E, int nbig) {
+  Scratch4 s;
+  s.fifo = 0;
+  s.chq = s.fifo + sizeof(Ent) * (size_t)N;
+  s.ov = s.chq + sizeof(Ent) * (size_t)(E > 0 ? E : 1);
+  s.bigc = s.ov + sizeof(NRec) * (size_t)N;
+  s.dtick = s.bigc + sizeof(int) * 2 * (size_t)(nbig > 0 ? nbig : 1);
+  s.mlog = (s.dtick + sizeof(int) * (size_t)N + 15) & ~(size_t)15;
+  s.dlog = s.mlog + sizeof(MemEnt) * ((size_t)N + (size_t)(E > 0 ? E : 1) + 8);
+  s.dovf = s.dlog + sizeof(MemEnt) * (size_t)N;
+  s.total = (s.dovf + sizeof(DeathEnt) * (size_t)N + 255) & ~(size_t)255;
+  return s;
+}
+
+__device__ __forceinline__ void bar_devices(int nthreads) {
+  asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
+}
+// 64-bit delta as 16 + 16 + 32-bit fire-and-forget shared reductions (few adds per bucket)
+__device__ __forceinline__ void add3(unsigned *w, long long v) {
+  atomicAdd(&w[0], (unsigned)(v & 0xffff));
+  atomicAdd(&w[1], (unsigned)((v >> 16) & 0xffff));
+  atomicAdd(&w[2], (unsigned)(int)(v >> 32));
+}
+__device__ __forceinline__ long long read3(const unsigned *w) {
+  return ((long long)(int)w[2] << 32) + ((long long)w[1] << 16) + (long long)w[0];
+}
+__device__ __forceinline__ bool dec_in4(unsigned *cnt, const NRec &r, int *bigc, const int *bigid) {
+  if (r.cost < 0) return atomicSub(&bigc[bigid[r.id]], 1) == 1;
+  const int sh = (r.id & 3) * 8;
+  return ((atomicSub(&cnt[r.id >> 2], 1u << sh) >> sh) & 15u) == 1u;
+}
+__device__ __forceinline__ bool dec_out4(unsigned *cnt, const IRec &ir, int *bigc, int nbig) {
+  if (ir.pad >= 0) return atomicSub(&bigc[ir.pad + nbig], 1) == 1;
+  const int sh = (ir.u & 3) * 8 + 4;
+  return ((atomicSub(&cnt[ir.u >> 2], 1u << sh) >> sh) & 15u) == 1u;
+}
+__device__ __forceinline__ unsigned smem_u32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_wait(unsigned long long *mbar, unsigned parity) {
+  unsigned done = 0;
+  while (!done)
+    asm volatile("{\n\t.reg .pred P1;\n\tmbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+                 "selp.b32 %0, 1, 0, P1;\n\t}\n"
+                 : "=r"(done)
+                 : "r"(smem_u32(mbar)), "r"(parity)
+                 : "memory");
+}
+// the device lane stages the out-/in-edge records of op r into its slot sl: two bulk copies
+// (contiguous record ranges) completing on the slot's mbarrier
+__device__ __forceinline__ void stage_records4(Smem4 &S, const Cost2Graph &G, int q, int sl, const NRec &r) {
+  const unsigned no = (unsigned)min(r.oe - r.ob, SO4), ni = (unsigned)min(r.ie - r.ib, SI4);
+  unsigned long long *mb = &S.smb[q][sl];
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // earlier generic reads of the slot
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(mb)),
+               "r"(no * (unsigned)sizeof(NRec) + ni * (unsigned)sizeof(IRec))
+               : "memory");
+  if (no)
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(smem_u32(&S.st_out[q][sl][0])), "l"(G.erec + r.ob), "r"(no * (unsigned)sizeof(NRec)),
+                 "r"(smem_u32(mb))
+                 : "memory");
+  if (ni)
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(smem_u32(&S.st_in[q][sl][0])), "l"(G.irec + r.ib), "r"(ni * (unsigned)sizeof(IRec)),
+                 "r"(smem_u32(mb))
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async4(void *s, const void *g) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(smem_u32(s)), "l"(g) : "memory");
+}
+
+// File the deaths of one window for device q into its death log, sorted by tick (deaths of a
+// window have ticks inside that window, so the log stays sorted across windows).  Fast path:
+// at most DK deaths, ticks already prefetched into S.dl_t, one lane per death, rank by
+// (tick, producer).  Rare path: lane 0 gathers the shared ones and the window's overflow
+// entries of device q, reads their settled ticks and insertion-sorts them into the log.
+__device__ __forceinline__ int file_deaths(Smem4 &S, MemEnt *dlq, int dln, const int *dtick, const DeathEnt *dovf,
+                                        int slot, int q, int n, int ovf_lo, int ovf_hi, int lane) {
+  const unsigned FULL = 0xffffffffu;
+  if (n <= DK) {
+    int t = INT_MAX, u = INT_MAX;
+    long long by = 0;
+    if (lane < n) { t = S.dl_t[slot][q][lane]; u = S.dl_u[slot][q][lane]; by = S.dl_b[slot][q][lane]; }
+    int rank = 0;
+    for (int j = 0; j < n; j++) {
+      const int tj = __shfl_sync(FULL, t, j), uj = __shfl_sync(FULL, u, j);
+      if (tj < t || (tj == t && uj < u)) rank++;
+    }
+    if (lane < n) {
+      MemEnt e;
+      e.tick = t; e.pad = 0; e.delta = -by;
+      dlq[dln + rank] = e;
+    }
+    return dln + n;
+  }
+  if (lane == 0) {
+    int k = 0;
+    auto insert = [&](int t, long long by) {
+      int i = k++;
+      while (i > 0 && dlq[dln + i - 1].tick > t) { dlq[dln + i] = dlq[dln + i - 1]; i--; }
+      MemEnt e;
+      e.tick = t; e.pad = 0; e.delta = -by;
+      dlq[dln + i] = e;
+    };
+    for (int i = 0; i < DK; i++) insert(S.dl_t[slot][q][i], S.dl_b[slot][q][i]);
+    for (int e = ovf_lo; e < ovf_hi; e++) {
+      const DeathEnt de = dovf[e];
+      if (de.slot_dev == slot * 8 + q) insert(__ldcg(dtick + de.u), de.bytes);
+    }
+  }
+  return dln + n;
+}
+
+// Peak of one device: static bytes + the running sum over its memory log merged with its
+// death log (both sorted by tick), sampled after every local instant (deaths only free, so the
+// maximum is reached right after some logged instant).  Lane c merges a contiguous chunk of the
+// memory log with the deaths before the next chunk; a scan over lanes joins the chunks.
+__device__ __forceinline__ long long merge_peak(const MemEnt *mlq, int mn, const MemEnt *dlq, int dln,
+                                             long long stat, int lane) {
+  const unsigned FULL = 0xffffffffu;
+  const int per = (mn + 31) / 32;
+  const int s0 = min(mn, lane * per), s1 = min(mn, s0 + per);
+  const int tstart = s0 < mn ? mlq[s0].tick : INT_MAX;
+  int jlo = 0;
+  if (lane > 0) {   // first death with tick >= tstart
+    int lo = 0, hi = dln;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (dlq[mid].tick < tstart) lo = mid + 1; else hi = mid;
+    }
+    jlo = lo;
+  }
+  int jhi = __shfl_down_sync(FULL, jlo, 1);
+  if (lane == 31) jhi = dln;
+  long long msum = 0, dsum = 0, best = LLONG_MIN;
+  int j = jlo;
+  for (int i = s0; i < s1; i++) {
+    const MemEnt e = mlq[i];
+    msum += e.delta;
+    while (j < jhi && dlq[j].tick <= e.tick) { dsum += dlq[j].delta; j++; }
+    best = max(best, msum + dsum);
+  }
+  for (; j < jhi; j++) dsum += dlq[j].delta;
+  const long long tot = msum + dsum;
+  long long off = tot;   // inclusive scan of chunk totals
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const long long y = __shfl_up_sync(FULL, off, o);
+    if (lane >= o) off += y;
+  }
+  off -= tot;
+  long long v = best == LLONG_MIN ? LLONG_MIN : off + best;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(FULL, v, o));
+  return stat + (v > 0 ? v : 0);
+}
+
+__device__ __forceinline__ void put_inc(Smem4 &S, NRec *ovq, int q, int pos, const NRec &r) {
+  if (pos < NINC4) copy_rec(&S.inc[q][pos], &r);
+  else copy_rec(ovq + pos, &r);
+}
+
+__global__ void __launch_bounds__(256, 2) k_cost4(Cost2Graph G, TopoArgs T, const uint8_t *__restrict__ Dall,
+                                                  unsigned char *scratch, size_t per_place, gdp_sim_report *rep,
+                                                  long long *peak_out, long long *busy_out, double *reward, int Wl,
+                                                  int dbg) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Smem4 &S = *reinterpret_cast<Smem4 *>(smem_raw);
+  const int N = G.N, d = T.d, b = blockIdx.x;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, nthr = blockDim.x;
+  const unsigned FULL = 0xffffffffu, lt = (1u << lane) - 1u;
+  unsigned *cnt = reinterpret_cast<unsigned *>(smem_raw + sizeof(Smem4));
+  const int cwords = (N + 3) >> 2;
+  unsigned *Dn = cnt + cwords;
+  const int dwords = (N + 7) >> 3;
+  const uint8_t *D = Dall + (size_t)b * N;
+  const Scratch4 L4 = scratch4_layout(N, G.E, G.nbig);
+  unsigned char *base = scratch + (size_t)b * per_place;
+  Ent *fifo = reinterpret_cast<Ent *>(base + L4.fifo);
+  Ent *chq = reinterpret_cast<Ent *>(base + L4.chq);
+  NRec *ov = reinterpret_cast<NRec *>(base + L4.ov);
+  int *bigc = reinterpret_cast<int *>(base + L4.bigc);
+  int *dtick = reinterpret_cast<int *>(base + L4.dtick);
+  MemEnt *mlog = reinterpret_cast<MemEnt *>(base + L4.mlog);
+  MemEnt *dlog = reinterpret_cast<MemEnt *>(base + L4.dlog);
+  DeathEnt *dovf = reinterpret_cast<DeathEnt *>(base + L4.dovf);
+
+  // ------------------------------------------------------------ prologue (whole block)
+  for (int i = tid; i < cwords; i += nthr) cnt[i] = G.cnt0[i];
+  for (int j = tid; j < G.nbig; j += nthr) { bigc[j] = G.big_in[j]; bigc[G.nbig + j] = G.big_out[j]; }
+  for (int v = tid; v < N; v += nthr) dtick[v] = -1;
+  if (tid < 64) { S.ccnt[tid] = 0; S.cstamp[tid] = -1; S.cfree[tid] = 0; S.ctail[tid] = 0; S.phs[0][tid] = 0; }
+  if (tid < 8) { S.stat[tid] = 0; S.busyv[tid] = 0; S.opcnt[tid] = 0; }
+  if (tid == 0) {
+    S.flag = 0; S.oom = 0; S.cross = 0; S.mk = 0; S.disp = 0; S.nwin = 0;
+    S.tn[0] = INF; S.tn[1] = INF; S.tn[2] = INF;
+    S.ovf_n = 0; S.ovf_start[0] = 0;
+  }
+  if (tid < 24) (&S.dn[0][0])[tid] = 0;
+  if (tid < 24) (&S.acc[0][0])[tid] = 0u;
+  if (tid < 16) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&S.smb[tid >> 1][tid & 1])) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  {
+    long long lmem[8], lbusy[8];
+    int lcnt[8], flag = 0;
+#pragma unroll
+    for (int k = 0; k < 8; k++) { lmem[k] = 0; lbusy[k] = 0; lcnt[k] = 0; }
+    for (int p = tid; p < dwords; p += nthr) {
+      unsigned packed = 0;
+      for (int j = 0; j < 8; j++) {
+        const int v = 8 * p + j;
+        if (v >= N) break;
+        int k = D[v];
+        if (k >= d) { flag |= 2; k = 0; }
+        packed |= (unsigned)k << (4 * j);
+        const long long mb = G.mem_bytes[v];
+        const long long du = (long long)G.cost[v] * T.speed[k];
+#pragma unroll
+        for (int q = 0; q < 8; q++)
+          if (q == k) { lmem[q] += mb; lbusy[q] += du; lcnt[q] += 1; }
+        if (G.has_coloc && D[G.leader[v]] != D[v]) flag |= 1;
+      }
+      Dn[p] = packed;
+    }
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+      const long long a = warp_sum_ll(lmem[k]), c = warp_sum_ll(lbusy[k]);
+      const int n = __reduce_add_sync(FULL, lcnt[k]);
+      if (lane == 0 && n) {
+        atomicAdd(reinterpret_cast<unsigned long long *>(&S.stat[k]), (unsigned long long)a);
+        atomicAdd(reinterpret_cast<unsigned long long *>(&S.busyv[k]), (unsigned long long)c);
+        atomicAdd(&S.opcnt[k], n);
+      }
+    }
+    flag = __reduce_or_sync(FULL, flag);
+    if (lane == 0 && flag) atomicOr(&S.flag, flag);
+  }
+  __syncthreads();
+  if (S.flag & 2) {   // malformed: an entry >= d
+    if (tid == 0) {
+      gdp_sim_report R;
+      R.makespan = 0; R.cross_bytes = 0; R.valid = 0; R.violation = 3;
+      for (int i = 0; i < 6; i++) R.pad[i] = 0;
+      rep[b] = R;
+      reward[b] = -10.0;
+    }
+    if (tid < d) {
+      if (peak_out) peak_out[(size_t)b * d + tid] = 0;
+      if (busy_out) busy_out[(size_t)b * d + tid] = 0;
+    }
+    return;
+  }
+  {
+    long long lcross = 0;
+    for (long long e = tid; e < G.E; e += nthr) {
+      const int u = G.out_src[e], w = G.out_idx[e];
+      const int su = dev_of(Dn, u), tw = dev_of(Dn, w);
+      if (su != tw) {
+        atomicAdd(&S.ccnt[su * 8 + tw], 1);
+        lcross += G.out_bytes[u];
+      }
+    }
+    lcross = warp_sum_ll(lcross);
+    if (lane == 0 && lcross) atomicAdd(&S.cross, (unsigned long long)lcross);
+  }
+  __syncthreads();
+  if (warp == 0) {
+    {  // device regions (FIFO overflow, incoming overflow) from op counts
+      const int c = lane < d ? S.opcnt[lane] : 0;
+      int inc = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(FULL, inc, o);
+        if (lane >= o) inc += y;
+      }
+      if (lane < 8) S.doff[lane] = inc - c;
+    }
+    {  // channel regions, channels 2*lane and 2*lane+1
+      const int c0 = S.ccnt[2 * lane], c1 = S.ccnt[2 * lane + 1];
+      const int pair = c0 + c1;
+      int inc = pair;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(FULL, inc, o);
+        if (lane >= o) inc += y;
+      }
+      S.coff[2 * lane] = inc - pair;
+      S.coff[2 * lane + 1] = inc - pair + c0;
+    }
+    __syncwarp();
+    // sources are available at t = 0: appended to their FIFO in ascending id
+    int ftail = 0;   // lane k: tail of device k
+    for (int v0 = 0; v0 < N; v0 += 32) {
+      const int v = v0 + lane;
+      const bool src = v < N && G.in_ptr[v + 1] == G.in_ptr[v];
+      if (!__any_sync(FULL, src)) continue;
+      const int k = src ? dev_of(Dn, v) : 0;
+      int off = 0, cntk = 0;
+      for (int dev = 0; dev < d; dev++) {
+        const unsigned m = __ballot_sync(FULL, src && k == dev);
+        if (src && k == dev) off = __popc(m & lt);
+        if (lane == dev) cntk = __popc(m);
+      }
+      const int tail_k = __shfl_sync(FULL, ftail, k & 7);
+      if (src) {
+        NRec r;
+        load_rec(r, G.nrec + v);
+        const int pos = tail_k + off;
+        if (pos < KF4) store_ent(&S.fc[k][pos], r, 0, 0);
+        else store_ent(fifo + S.doff[k] + pos, r, 0, 0);
+      }
+      ftail += cntk;
+      __syncwarp();
+    }
+    if (lane < 8) S.ftail0[lane] = ftail;
+    {  // memory-log regions: one entry per local instant (finish, arrival or the t = 0 dispatch)
+      int cap = 0;
+      if (lane < d) {
+        cap = S.opcnt[lane] + 1;
+        for (int k = 0; k < d; k++) cap += S.ccnt[k * 8 + lane];
+      }
+      int inc = cap;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(FULL, inc, o);
+        if (lane >= o) inc += y;
+      }
+      if (lane < 8) S.moff[lane] = inc - cap;
+    }
+  }
+  __syncthreads();
+  if (dbg == 1) return;
+
+  // ------------------------------------------------------------------ device warp q (d warps)
+  const int q = warp;
+  const bool devl = lane == q;                 // FIFO / dispatch / staging / memory log of device q
+  const bool own = lane < d && lane != q;      // consumer of channel (lane -> q)
+  const bool dth = lane >= 8 && lane < 8 + DK; // death-tick prefetch lanes
+  const int cin = 8 * lane + q;
+  const int offc = own ? S.coff[cin] : 0;
+  Ent *ring = &S.cc[own ? cin : 0][0];
+  int head = 0, tknown = 0, filled = 0, ha = INF, hs = 0;
+  unsigned pend = 0;                           // ring slots with a prefetch in flight
+  NRec *ovq = ov + S.doff[q];
+  Ent *fq_g = fifo + S.doff[q];
+  MemEnt *mlq = mlog + S.moff[q];
+  MemEnt *dlq = dlog + S.doff[q];
+  const int spd = T.speed[q];
+  int fhead = 0, ftail = S.ftail0[q], running = 0, fin = 0, mk = 0, disp = 0, mn = 0;
+  int cur = 0, nxt_id = -1, dln = 0;
+  unsigned nst0 = 0, nst1 = 0;                 // bulk stagings issued per slot (mbarrier phases)
+  int T0 = 0, w = 0;
+  for (;; w++) {
+    const int w3 = w % 3;
+    if (q == 0 && lane == 0) S.tn[(w + 1) % 3] = INF;   // read last after barrier w - 2
+    if (lane < d) S.pfirst[w & 1][8 * q + lane] = INF;
+    const int Tend = T0 + Wl;
+    for (;;) {
+      // key 2 tau (+1 unless my op finishes at tau); an idle device with a non-empty FIFO
+      // dispatches at once (only the sources at t = 0)
+      const unsigned NK = 0xffffffffu;
+      const unsigned dc = running ? 2u * (unsigned)fin : (fhead < ftail ? 2u * (unsigned)T0 + 1u : NK);
+      const unsigned cand = min(devl ? dc : NK, own && ha != INF ? 2u * (unsigned)ha + 1u : NK);
+      const unsigned key = __reduce_min_sync(FULL, cand);
+      const int tau = (int)(key >> 1);
+      if (key == NK || tau >= Tend) {   // my next event opens a later window
+        if (lane == 0 && key != NK) atomicMin(&S.tn[w3], tau);
+        break;
+      }
+      const bool fnow = (key & 1) == 0;
+      if (devl) {
+        cp_wait1();   // FIFO refills older than the last instant
+        if (fnow) mbar_wait(&S.smb[q][cur], ((cur ? nst1 : nst0) - 1u) & 1u);   // staged records
+      }
+      __syncwarp();
+      long long delta = 0;
+      int navail = 0;
+      // (1) the copy arriving now on my incoming channel (at most one per channel per tick)
+      {
+        bool av = false;
+        NRec ar;
+        if (own && ha == tau) {
+          int s = head % KC4;
+          if (pend & (1u << s)) { cp_wait0(); pend = 0; }
+          load_rec(ar, &ring[s].r);
+          delta += ring[s].bytes;
+          av = dec_in4(cnt, ar, bigc, G.bigid);
+          head++;
+          if (head < tknown) {
+            s = head % KC4;
+            if (pend & (1u << s)) { cp_wait0(); pend = 0; }
+            ha = ring[s].t;
+          } else {
+            ha = INF;
+          }
+          if (filled < tknown) {   // keep KC4 entries ahead
+            cp_ent(&ring[filled % KC4], chq + offc + filled);
+            cp_commit();
+            pend |= 1u << (filled % KC4);
+            filled++;
+          }
+        }
+        const unsigned m = __ballot_sync(FULL, av);
+        if (av) put_inc(S, ovq, q, __popc(m & lt), ar);
+        navail = __popc(m);
+      }
+      // (2) my op finishes now: its edges one per lane
+      if (fnow) {
+        if (devl) running = 0;
+        NRec r;
+        load_rec(r, &S.run[q]);
+        const int sl = S.run_slot[q];
+        const int nin = r.ie - r.ib, nout = r.oe - r.ob;
+        // frees: copies this op held (local); producers whose last consumer it is are queued for
+        // their device warp with the death tick settled later
+        for (int j = lane; j < nin; j += 32) {
+          IRec ir;
+          if (j < SI4) ir = S.st_in[q][sl][j];
+          else ir = G.irec[r.ib + j];
+          const int du = dev_of(Dn, ir.u);
+          if (du != q) delta -= ir.bytes;
+          atomicMax(&dtick[ir.u], tau);
+          if (dec_out4(cnt, ir, bigc, G.nbig)) {
+            const int i = atomicAdd(&S.dn[w3][du], 1);
+            if (i < DK) {
+              S.dl_u[w3][du][i] = ir.u;
+              S.dl_b[w3][du][i] = ir.bytes;
+            } else {
+              const int k = atomicAdd(&S.ovf_n, 1);
+              DeathEnt e;
+              e.u = ir.u; e.slot_dev = w3 * 8 + du; e.bytes = ir.bytes;
+              dovf[k] = e;
+            }
+          }
+        }
+        if (nout == 0 && lane == 0) delta -= r.bytes;
+        for (int j0 = 0; j0 < nout; j0 += 32) {
+          const int j = j0 + lane;
+          const bool v = j < nout;
+          NRec wr;
+          int tw = -1;
+          if (v) {
+            if (j < SO4) wr = S.st_out[q][sl][j];
+            else load_rec(wr, G.erec + r.ob + j);
+            tw = dev_of(Dn, wr.id);
+          }
+          const bool cross = v && tw != q;
+          const bool avs = v && !cross && dec_in4(cnt, wr, bigc, G.bigid);
+          const unsigned m = __ballot_sync(FULL, avs);
+          if (avs) put_inc(S, ovq, q, navail + __popc(m & lt), wr);
+          navail += __popc(m);
+          const unsigned cm = __ballot_sync(FULL, cross);
+          if (cm) {
+            const unsigned grp = (cm & (cm - 1)) ? __match_any_sync(FULL, cross ? tw : -1) : cm;
+            if (cross) {
+              const int rank = __popc(grp & lt), n = __popc(grp);
+              const int c = 8 * q + tw;
+              const int f = S.cfree[c];
+              const int x = xfer_time3(r.bytes, c, T);
+              const int bs = max(tau, f);
+              const int tail = S.ctail[c];
+              const int chs = S.phs[w & 1][c];
+              __syncwarp(grp);   // every rank has read the channel state before rank 0 moves it
+              const int pos = tail + rank, arr = bs + (rank + 1) * x;
+              // the consumer consumed position pos - KC4 before this window: its ring slot is
+              // free, so the entry goes straight there; otherwise to global for a later prefetch
+              if (pos < chs + KC4) store_ent(&S.cc[c][pos % KC4], wr, arr, r.bytes);
+              else store_ent(chq + S.coff[c] + pos, wr, arr, r.bytes);
+              if (rank == 0) {
+                S.cfree[c] = bs + n * x;
+                S.ctail[c] = tail + n;
+                if (S.cstamp[c] != w) {   // first push of this window: the consumer may not know it yet
+                  S.cstamp[c] = w;
+                  S.pfirst[w & 1][c] = bs + x;
+                  atomicMin(&S.tn[w3], bs + x);
+                }
+              }
+            }
+            __syncwarp();
+          }
+        }
+      }
+      if (delta != 0) add3(&S.acc[q][0], delta);
+      __syncwarp();
+      // (3) device lane: ops made available now join the FIFO in id order; dispatch; stage;
+      // one memory-log entry for the instant
+      if (devl) {
+        const int n = navail;
+        NRec *Li = &S.inc[q][0];
+        NRec run;
+        bool go = false;
+        if (n == 1 && !running && fhead == ftail) {   // common case: straight to dispatch
+          load_rec(run, Li);
+          ftail++;
+          fhead++;
+          go = true;
+        } else {
+          if (n > 0) {
+            for (int i = 1; i < n; i++) {   // insertion sort by id (n is small except after wide fan-outs)
+              NRec key;
+              load_rec(key, i < NINC4 ? &Li[i] : &ovq[i]);
+              int j = i - 1;
+              while (j >= 0) {
+                NRec *pj = j < NINC4 ? &Li[j] : &ovq[j];
+                if (pj->id <= key.id) break;
+                copy_rec(j + 1 < NINC4 ? &Li[j + 1] : &ovq[j + 1], pj);
+                j--;
+              }
+              copy_rec(j + 1 < NINC4 ? &Li[j + 1] : &ovq[j + 1], &key);
+            }
+            for (int i = 0; i < n; i++) {
+              const NRec &rr = i < NINC4 ? Li[i] : ovq[i];
+              if (ftail < fhead + KF4) store_ent(&S.fc[q][ftail % KF4], rr, tau, 0);
+              else store_ent(fq_g + ftail, rr, tau, 0);
+              ftail++;
+            }
+          }
+          if (!running && fhead < ftail) {
+            Ent &e = S.fc[q][fhead % KF4];
+            load_rec(run, &e.r);
+            if (fhead + KF4 < ftail) cp_ent(&e, fq_g + fhead + KF4);
+            fhead++;
+            go = true;
+          }
+        }
+        long long total = 0;
+        if (dbg != 6) {
+          total = read3(&S.acc[q][0]);
+          S.acc[q][0] = 0u; S.acc[q][1] = 0u; S.acc[q][2] = 0u;
+        }
+        bool staged = false;
+        if (go) {
+          running = 1;
+          fin = tau + (run.cost & 0x7fffffff) * spd;
+          mk = max(mk, fin);
+          total += run.bytes;
+          disp++;
+          cur ^= 1;
+          copy_rec(&S.run[q], &run);
+          S.run_slot[q] = cur;
+          if (run.id != nxt_id) {   // not staged while it waited: stage now
+            stage_records4(S, G, q, cur, run);
+            if (cur) nst1++; else nst0++;
+            staged = true;
+          }
+          nxt_id = -1;
+        }
+        if (!staged && running && nxt_id < 0 && fhead < ftail) {   // stage the op waiting at the head
+          NRec sr;
+          load_rec(sr, &S.fc[q][fhead % KF4].r);
+          stage_records4(S, G, q, cur ^ 1, sr);
+          if (cur) nst0++; else nst1++;
+          nxt_id = sr.id;
+        }
+        cp_commit();
+        if (total != 0 && dbg != 6) {
+          MemEnt me;
+          me.tick = tau; me.pad = 0; me.delta = total;
+          mlq[mn++] = me;
+        }
+      }
+    }
+    // publish the end-of-window state, meet, and find the next window start
+    if (own) S.phs[(w + 1) & 1][cin] = head;
+    if (lane < d) S.ptail[w & 1][8 * q + lane] = S.ctail[8 * q + lane];
+    bar_devices(32 * d);   // bar.sync orders the window's shared and global writes for all device warps
+    const int Tn = S.tn[w3];
+    if (q == 0 && lane == 0) S.ovf_start[(w + 1) % 3] = S.ovf_n;
+    if (own) {   // my channel: entries pushed in this window
+      const int tn = S.ptail[w & 1][cin];
+      if (ha == INF && tn > tknown) ha = S.pfirst[w & 1][cin];
+      const int lim = min(tn, head + KC4);
+      for (; filled < lim; filled++) {
+        if (filled >= tknown && filled < hs + KC4) continue;   // the producer wrote it into the ring
+        cp_ent(&ring[filled % KC4], chq + offc + filled);
+        cp_commit();
+        pend |= 1u << (filled % KC4);
+      }
+      tknown = tn;
+      hs = head;
+    }
+    // deaths of my device: prefetch the settled ticks of this window's, file the previous one's
+    {
+      const int n0 = S.dn[w3][q];
+      if (dth && lane - 8 < min(n0, DK))
+        cp_async4(&S.dl_t[w3][q][lane - 8], dtick + S.dl_u[w3][q][lane - 8]);
+      if (dth) cp_commit();
+      if (w > 0) {
+        const int wp = (w + 2) % 3;   // (w - 1) % 3
+        const int n1 = S.dn[wp][q];
+        if (n1 > 0) {
+          if (dth) cp_wait1();
+          __syncwarp();
+          dln = file_deaths(S, dlq, dln, dtick, dovf, wp, q, n1, S.ovf_start[wp], S.ovf_start[w3], lane);
+          __syncwarp();
+          if (lane == 0) S.dn[wp][q] = 0;
+        }
+      }
+    }
+    if (Tn == INF) break;
+    T0 = Tn;
+  }
+  {  // the last window's deaths
+    const int w3 = w % 3, n0 = S.dn[w3][q];
+    cp_wait0();
+    __syncwarp();
+    if (n0 > 0) dln = file_deaths(S, dlq, dln, dtick, dovf, w3, q, n0, S.ovf_start[w3], S.ovf_n, lane);
+  }
+  if (devl) {
+    atomicMax(&S.mk, mk);
+    atomicAdd(&S.disp, disp);
+  }
+  // ------------------------------------------------------------------ peak memory of device q
+  {
+    __syncwarp();   // the device lane's memory log and every lane's death-log entries
+    mn = __shfl_sync(FULL, mn, q);
+    const long long pk = dbg == 5 ? 0 : merge_peak(mlq, mn, dlq, dln, S.stat[q], lane);
+    if (lane == 0) {
+      if (pk > T.cap[q]) atomicOr(&S.oom, 1);
+      if (peak_out) peak_out[(size_t)b * d + q] = pk;
+      if (busy_out) busy_out[(size_t)b * d + q] = S.busyv[q];
+    }
+  }
+  if (dbg == 2 && busy_out && q == 0 && lane == 0) busy_out[(size_t)b * d] = w + 1;
+  __syncthreads();
+  if (tid == 0) {
+    gdp_sim_report R;
+    R.makespan = S.mk; R.cross_bytes = (long long)S.cross; R.valid = 0; R.violation = 0;
+    for (int i = 0; i < 6; i++) R.pad[i] = 0;
+    R.violation = (S.flag & 1) ? 1 : (S.oom ? 2 : 0);
+    if (S.disp != N) R.violation = 3;   // cannot happen for a validated DAG
+    R.valid = R.violation == 0;
+    rep[b] = R;
+    reward[b] = R.valid ? -__dsqrt_rn(__ddiv_rn((double)S.mk, 1e6)) : -10.0;
+  }
+}
+
+}  // namespace
+
+size_t cost4_smem_bytes(int N) { return sizeof(Smem4) + 4 * (size_t)((N + 3) / 4) + 4 * (size_t)((N + 7) / 8); }
+size_t cost4_scratch_per_placement(int N, long long E, int nbig) { return scratch4_layout(N, E, nbig).total; }
+
+int cost4_window(const TopoArgs &T, int min_cost, int N) {
+  static const bool off = getenv("GDP_COST_V3") != nullptr || getenv("GDP_COST_V2") != nullptr;
+  if (off) return 0;
+  const int d = T.d;
+  if (d < 1 || d > 8 || min_cost < 1) return 0;   // zero-duration ops need same-instant rounds
+  int L = WMAX;
+  for (int k = 0; k < d; k++) {
+    if (T.speed[k] < 1) return 0;
+    for (int q = 0; q < d; q++)
+      if (k != q) L = L < T.lat[k * 8 + q] ? L : T.lat[k * 8 + q];
+  }
+  if (L < 1) return 0;                           // a transfer could land in its own window
+  if (cost4_smem_bytes(N) > 227 * 1024) return 0;
+  return L;
+}
+
+bool launch_cost4(const Cost2Graph &G, const TopoArgs &T, int min_cost, const uint8_t *D, int B,
+                  unsigned char *scratch, size_t per_place, gdp_sim_report *rep, long long *peak, long long *busy,
+                  double *reward, cudaStream_t s) {
+  const int L = cost4_window(T, min_cost, G.N);
+  if (L < 1) return false;
+  if (per_place < cost4_scratch_per_placement(G.N, G.E, G.nbig)) return false;
+  const int d = T.d;
+  const size_t smem = cost4_smem_bytes(G.N);
+  static size_t configured = 0;
+  if (smem > 40 * 1024 && smem > configured) {
+    cudaFuncSetAttribute(k_cost4, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    configured = smem;
+  }
+  static_assert(2 * SO4 + SI4 == 24, "24 staging lanes");
+  static const int dbg = getenv("GDP_COST_DBG") ? atoi(getenv("GDP_COST_DBG")) : 0;
+  note_launch();
+  k_cost4<<<B, 32 * d, smem, s>>>(G, T, D, scratch, per_place, rep, peak, busy, reward, L, dbg);
+  return true;
+}
+
+}  // namespace gdp
