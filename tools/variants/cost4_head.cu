@@ -50,6 +50,7 @@ struct Smem4 {
   int pfirst[2][64], ptail[2][64];   // published per window parity: first push's arrival, tail
   int tn[3];                       // next window start, atomic min over devices' next events and first pushes
   int phs[2][64];                  // consumer head at the start of window w (parity w & 1)
+  long long ploc[8];               // PROF: local cycles of each device warp in the window
   int coff[64], ccnt[64];
   int doff[8], ftail0[8], opcnt[8];
   long long stat[8], busyv[8];
@@ -139,10 +140,11 @@ __device__ __forceinline__ void put_inc(Smem4 &S, NRec *ovq, int q, int pos, con
   else copy_rec(ovq + pos, &r);
 }
 
+template <bool PROF>
 __global__ void __launch_bounds__(288, 2) k_cost4(Cost2Graph G, TopoArgs T, const uint8_t *__restrict__ Dall,
                                                   unsigned char *scratch, size_t per_place, gdp_sim_report *rep,
                                                   long long *peak_out, long long *busy_out, double *reward, int Wl,
-                                                  int dbg) {
+                                                  int dbg, unsigned msleep, int dbg_warp) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Smem4 &S = *reinterpret_cast<Smem4 *>(smem_raw);
   const int N = G.N, d = T.d, b = blockIdx.x;
@@ -314,6 +316,10 @@ __global__ void __launch_bounds__(288, 2) k_cost4(Cost2Graph G, TopoArgs T, cons
     int cur = 0, nxt_id = -1;
     unsigned nst0 = 0, nst1 = 0;                 // bulk stagings issued per slot (mbarrier phases)
     int li = 0, T0 = 0, w = 0, memd = -1;
+    long long c_local = 0, c_bar = 0, c_post = 0, c_mw = 0, tc = clock64();   // PROF only
+    long long c_wall = 0, c_maxloc = 0, t_ws = 0, t_prev = clock64();
+    long long cl[5] = {0, 0, 0, 0, 0}, tl = 0;
+#define PL(i) if (PROF) { const long long tn = clock64(); cl[i] += tn - tl; tl = tn; }
     for (;; w++) {
       const int set = w % R4;
       if (w - R4 > memd) {   // the memory warp must have released this window set
@@ -321,6 +327,7 @@ __global__ void __launch_bounds__(288, 2) k_cost4(Cost2Graph G, TopoArgs T, cons
           while ((memd = ld_acq(&S.mem_done)) < w - R4) { }
         memd = __shfl_sync(FULL, memd, 0);
       }
+      if (PROF) { const long long tn = clock64(); c_mw += tn - tc; tc = tn; t_ws = tn; c_wall += tn - t_prev; t_prev = tn; }
       if (q == 0 && lane == 0) {
         S.Tw[set] = T0;
         S.tn[(w + 1) % 3] = INF;   // read last after barrier w - 2, written from window w + 1 on
@@ -333,6 +340,7 @@ __global__ void __launch_bounds__(288, 2) k_cost4(Cost2Graph G, TopoArgs T, cons
         const unsigned NK = 0xffffffffu;
         const unsigned dc = running ? 2u * (unsigned)fin : (fhead < ftail ? 2u * (unsigned)T0 + 1u : NK);
         const unsigned cand = min(devl ? dc : NK, own && ha != INF ? 2u * (unsigned)ha + 1u : NK);
+        if (PROF) tl = clock64();
         const unsigned key = __reduce_min_sync(FULL, cand);
         const int tau = (int)(key >> 1);
         if (key == NK || tau >= Tend) {   // my next event opens a later window
@@ -347,6 +355,7 @@ __global__ void __launch_bounds__(288, 2) k_cost4(Cost2Graph G, TopoArgs T, cons
         __syncwarp();
         long long delta = 0;
         int navail = 0;
+        PL(0)
         // (1) the copy arriving now on my incoming channel (at most one per channel per tick)
         {
           bool av = false;
@@ -376,6 +385,7 @@ __global__ void __launch_bounds__(288, 2) k_cost4(Cost2Graph G, TopoArgs T, cons
           if (av) put_inc(S, ovq, q, __popc(m & lt), ar);
           navail = __popc(m);
         }
+        PL(1)
         // (2) my op finishes now: its edges one per lane
         if (fnow) {
           if (devl) running = 0;
@@ -442,6 +452,7 @@ __global__ void __launch_bounds__(288, 2) k_cost4(Cost2Graph G, TopoArgs T, cons
             }
           }
         }
+        PL(2)
         __syncwarp();
         // (3) device lane: ops made available now join the FIFO in id order; dispatch; stage
         if (devl) {
@@ -509,14 +520,23 @@ __global__ void __launch_bounds__(288, 2) k_cost4(Cost2Graph G, TopoArgs T, cons
           }
           cp_commit();
         }
+        PL(3)
         // (4) my memory delta at tau
         if (delta != 0) add3(&S.lb[set][q][tau - T0][0], delta);
         li++;
+        PL(4)
       }
       // publish the end-of-window state, meet, and find the next window start
       if (own) S.phs[(w + 1) & 1][cin] = head;
       if (lane < d) S.ptail[w & 1][8 * q + lane] = S.ctail[8 * q + lane];
+      if (PROF) { const long long tn = clock64(); c_local += tn - tc; tc = tn; if (lane == 0) S.ploc[q] = tn - t_ws; }
       bar_devices(32 * d);   // bar.sync orders the window's shared and global writes for all device warps
+      if (PROF) {
+        const long long tn = clock64(); c_bar += tn - tc; tc = tn;
+        long long mx = 0;
+        for (int k = 0; k < d; k++) mx = max(mx, S.ploc[k]);
+        c_maxloc += mx;
+      }
       if (q == 0 && lane == 31) {   // a lane that rarely has global writes in flight (release fence)
         S.dq_end[set] = S.dq_tail;
         st_rel(&S.win_done, w);
@@ -535,9 +555,11 @@ __global__ void __launch_bounds__(288, 2) k_cost4(Cost2Graph G, TopoArgs T, cons
         tknown = tn;
         hs = head;
       }
+      if (PROF) { const long long tn = clock64(); c_post += tn - tc; tc = tn; }
       if (Tn == INF) break;
       T0 = Tn;
     }
+#undef PL
     cp_wait0();
     if (devl) {
       atomicMax(&S.mk, mk);
@@ -546,6 +568,10 @@ __global__ void __launch_bounds__(288, 2) k_cost4(Cost2Graph G, TopoArgs T, cons
     if (q == 0 && lane == 0) {
       S.nwin = w + 1;
       st_rel(&S.dev_done, 1);
+    }
+    if (PROF && busy_out && lane == 0 && d == 8 && q == (dbg_warp & 7)) {
+      long long *o = busy_out + (size_t)b * d;
+      o[0] = c_wall; o[1] = c_maxloc; o[2] = c_local; o[3] = cl[2]; o[4] = cl[3]; o[5] = c_bar; o[6] = c_post + c_mw; o[7] = li;
     }
   } else {
     // ---------------------------------------------------------------- memory warp
@@ -559,7 +585,10 @@ __global__ void __launch_bounds__(288, 2) k_cost4(Cost2Graph G, TopoArgs T, cons
       }
       wd = __shfl_sync(FULL, wd, 0);
       fin_all = __shfl_sync(FULL, fin_all, 0);
-      if (wd > done_w) {
+      if (wd > done_w && dbg == 4) {   // timing experiment: release the sets without memory work
+        if (lane == 0) st_rel(&S.mem_done, wd);
+        done_w = wd;
+      } else if (wd > done_w) {
         // producer deaths queued in windows done_w+1 .. wd
         const int dq_stop = S.dq_end[wd % R4];
         for (int i = dq_start + lane; i < dq_stop; i += 32) {
@@ -593,13 +622,13 @@ __global__ void __launch_bounds__(288, 2) k_cost4(Cost2Graph G, TopoArgs T, cons
       } else if (fin_all && done_w == S.nwin - 1) {
         break;
       } else {
-        __nanosleep(200);
+        __nanosleep(msleep);
       }
     }
     if (lane < d) {
       if (pk > T.cap[lane]) atomicOr(&S.oom, 1);
       if (peak_out) peak_out[(size_t)b * d + lane] = pk;
-      if (busy_out) busy_out[(size_t)b * d + lane] = S.busyv[lane];
+      if (busy_out && !PROF) busy_out[(size_t)b * d + lane] = S.busyv[lane];
     }
     if (dbg == 2 && busy_out && lane == 0) busy_out[(size_t)b * d] = S.nwin;
   }
@@ -647,13 +676,21 @@ bool launch_cost4(const Cost2Graph &G, const TopoArgs &T, int min_cost, const ui
   const size_t smem = cost4_smem_bytes(G.N);
   static size_t configured = 0;
   if (smem > 40 * 1024 && smem > configured) {
-    cudaFuncSetAttribute(k_cost4, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_cost4<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_cost4<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     configured = smem;
   }
   static_assert(2 * SO4 + SI4 == 24, "24 staging lanes");
   static const int dbg = getenv("GDP_COST_DBG") ? atoi(getenv("GDP_COST_DBG")) : 0;
   note_launch();
-  k_cost4<<<B, 32 * (d + 1), smem, s>>>(G, T, D, scratch, per_place, rep, peak, busy, reward, L, dbg);
+  static const unsigned msleep = getenv("GDP_COST_MSLEEP") ? (unsigned)atoi(getenv("GDP_COST_MSLEEP")) : 200u;
+  static const int dbg_warp = getenv("GDP_COST_DBG_WARP") ? atoi(getenv("GDP_COST_DBG_WARP")) : 1;
+  if (dbg == 3)
+    k_cost4<true><<<B, 32 * (d + 1), smem, s>>>(G, T, D, scratch, per_place, rep, peak, busy, reward, L, dbg, msleep,
+                                               dbg_warp);
+  else
+    k_cost4<false><<<B, 32 * (d + 1), smem, s>>>(G, T, D, scratch, per_place, rep, peak, busy, reward, L, dbg,
+                                                msleep, dbg_warp);
   return true;
 }
 
