@@ -40,6 +40,48 @@ def peaks():
         return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "sm_max_mhz": 1965.0, "_fallback": True}
 
 
+def kernel_profile(ps, theta, gdp, dev):
+    """Per-kernel live timing of one untimed step (gdp_profile_*): the stream is gated by a spin
+    kernel while the step is enqueued, so consecutive launch events are back to back and each
+    gap is one kernel's duration.  Achieved rates use the algorithmic bytes / flops the library
+    states per launch against MEASURED_PEAKS.json: HBM GB/s for the gathers,
+    element-wise and sampling kernels, bf16 tensor TFLOP/s for k_gemm_tc (its maps are
+    HBM-bound by arithmetic intensity, so both fractions are given)."""
+    import torch
+    pk = peaks()
+    hbm, tc = pk.get("hbm_gbs", 6650.0), pk.get("bf16_tflops", 1590.0)
+    torch.cuda.synchronize()
+    gdp.profile_enable(True)
+    try:
+        torch.cuda._sleep(int(0.3 * pk.get("sm_max_mhz", 1965.0) * 1e6))   # ~0.3 s gate
+        ps.run(theta)
+        main = torch.cuda.current_stream(dev)
+        gdp.profile_mark(main.cuda_stream)
+        for st in ps.states:
+            if st.stream is not None:
+                gdp.profile_mark(st.stream.cuda_stream)
+        torch.cuda.synchronize()
+        rec = gdp.profile_read()
+    finally:
+        gdp.profile_enable(False)
+    step_ms = sum(r["ms"] for r in rec.values())
+    out = {}
+    for name, r in sorted(rec.items(), key=lambda kv: -kv[1]["ms"]):
+        e = {"launches": r["launches"], "ms": round(r["ms"], 4), "share": round(r["ms"] / step_ms, 4)}
+        sec = r["ms"] / 1e3
+        if r["bytes"] > 0 and sec > 0:
+            gbs = r["bytes"] / sec / 1e9
+            e.update({"bytes": r["bytes"], "gbs": round(gbs, 1), "hbm_frac": round(gbs / hbm, 4)})
+        if r["flops"] > 0 and sec > 0:
+            tfs = r["flops"] / sec / 1e12
+            e.update({"flops": r["flops"], "tflops": round(tfs, 3)})
+            if name == "k_gemm_tc":
+                e["tensor_frac"] = round(tfs / tc, 5)
+        out[name] = e
+    return {"method": "gdp_profile_* events, one untimed step, stream gated by a 0.3 s spin kernel",
+            "hbm_peak_gbs": hbm, "bf16_peak_tflops": tc, "sum_ms": round(step_ms, 3), "per_kernel": out}
+
+
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
@@ -241,6 +283,7 @@ def main():
     ap.add_argument("--impl", default="gdp", choices=["gdp", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-kernels", action="store_true", help="skip the per-kernel timing pass")
     ap.add_argument("--fp32", action="store_true", help="dense maps in fp32 SIMT instead of tcgen05 bf16")
     ap.add_argument("--no-attention", action="store_true", help="NEXT-3 ablation variant (reading R34)")
     ap.add_argument("--no-superposition", action="store_true", help="NEXT-3 ablation variant (gates == 1)")
@@ -399,6 +442,10 @@ def main():
                "unit": UNIT,
                "h2d_bytes_per_step": th.nbytes, "d2h_bytes_per_step": 4 * ps.n_params + 8 * W.batch * len(W.graphs)}
 
+    kernels = None
+    if not ps.cuda_graph and not args.no_kernels:
+        kernels = kernel_profile(ps, theta, gdp, dev)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
@@ -421,7 +468,7 @@ def main():
                "dtype": ("f32" if args.fp32 else "bf16xbf16->f32 (tcgen05 dense maps) / f32") + " policy, i32 cost model", "data": "synthetic",
                "config": config_json(W, argparse.Namespace(batch=W.batch, gpus=world), mode),
                "clocks": clk.summary(), "gpu_launches": int(launches), "roofline": roof, "e2e": e2e,
-               "cpu_baseline": cpu,
+               "cpu_baseline": cpu, "kernels": kernels,
                "stages_ms": stage, "cuda_graph": bool(ps.cuda_graph),
                "valid_frac": float(np.mean(rep["valid"])), "makespan_mean_ticks": float(np.mean(rep["makespan"]))}
         print(json.dumps(out), flush=True)

@@ -136,6 +136,24 @@ const char *gdp_last_error(void);
  * (all threads, all devices).  bench.py reads it around the timed region. */
 uint64_t gdp_launch_count(void);
 
+/* Diagnostic: per-kernel timing for the roofline report (bench.py "kernels"; north_star's
+ * "evidenced by" list).  gdp_profile_enable(1) clears earlier records and makes every kernel
+ * launch of the library record a CUDA event on its stream just before the launch, tagged with
+ * the kernel's name and its algorithmic bytes and flops (0 where not stated);
+ * gdp_profile_enable(0) stops recording and keeps the records.  gdp_profile_mark(stream)
+ * records a closing event on stream (a void* cudaStream_t).  A launch's time is the gap to the
+ * next event on the same stream: exact when the GPU is kept busy (bench.py gates the stream
+ * with a spin kernel before enqueuing the step), an upper bound otherwise.
+ * gdp_profile_read synchronises the events and writes, for up to max_names distinct kernels in
+ * first-launch order, the name (static string owned by the library), the number of timed
+ * launches, the summed ms, bytes and flops; it returns the number written, or -1 (see
+ * gdp_last_error).  Not for use inside CUDA graph capture.  Errors: GDP_ERR_ARG from
+ * gdp_profile_mark when profiling is off. */
+gdp_status gdp_profile_enable(int32_t on);
+gdp_status gdp_profile_mark(void *stream);
+int32_t gdp_profile_read(int32_t max_names, const char **names, int32_t *launches, double *ms, double *bytes,
+                         double *flops);
+
 /* Diagnostic: build identification string of this library (never NULL). */
 const char *gdp_build_info(void);
 

@@ -10,7 +10,7 @@ from __future__ import annotations
 
 import ctypes
 import os
-from typing import Optional, Sequence
+from typing import Dict, Optional, Sequence
 
 import numpy as np
 
@@ -26,7 +26,8 @@ REPORT_BYTES = 24
 
 EXPORTS = ["gdp_default_config", "gdp_last_error", "gdp_launch_count", "gdp_build_info", "gdp_cost_kernel", "gdp_logprob", "gdp_clip_adam", "gdp_sample_at", "gdp_greedy", "gdp_graph_validate", "gdp_graph_create", "gdp_graph_destroy",
            "gdp_topo_create", "gdp_topo_destroy", "gdp_param_layout", "gdp_workspace_size", "gdp_embed",
-           "gdp_place", "gdp_sample", "gdp_cost", "gdp_advantage", "gdp_policy_grad"]
+           "gdp_place", "gdp_sample", "gdp_cost", "gdp_advantage", "gdp_policy_grad", "gdp_profile_enable",
+           "gdp_profile_mark", "gdp_profile_read"]
 
 
 class GdpError(RuntimeError):
@@ -72,6 +73,8 @@ def lib():
             "gdp_sample_at": [P, P, P, I32, U64, U64, P, P, P, P, SZ, P],
             "gdp_greedy": [P, P, P, P, P, P, SZ, P],
             "gdp_clip_adam": [P, I64, F64, F64, F64, F64, F64, I64, P, P, P, P, P, P],
+            "gdp_profile_enable": [I32],
+            "gdp_profile_mark": [P],
         }
         for name, args in sig.items():
             fn = getattr(L, name)
@@ -85,6 +88,8 @@ def lib():
         L.gdp_cost_kernel.argtypes = [P, P]
         L.gdp_last_error.restype = ctypes.c_char_p
         L.gdp_last_error.argtypes = []
+        L.gdp_profile_read.restype = ctypes.c_int32
+        L.gdp_profile_read.argtypes = [I32, P, P, P, P, P]
         _lib = L
     return _lib
 
@@ -103,6 +108,28 @@ def build_info() -> str:
 def launch_count() -> int:
     """Kernels launched by libgdp.so so far in this process."""
     return int(lib().gdp_launch_count())
+
+
+def profile_enable(on: bool):
+    """Per-launch timing on (clears earlier records) or off (gdp_profile_enable)."""
+    _check(lib().gdp_profile_enable(1 if on else 0), "gdp_profile_enable")
+
+
+def profile_mark(stream: int = 0):
+    """Closing event on a raw cudaStream_t handle (gdp_profile_mark)."""
+    _check(lib().gdp_profile_mark(ctypes.c_void_p(stream)), "gdp_profile_mark")
+
+
+def profile_read(max_names: int = 64) -> Dict[str, Dict[str, float]]:
+    """{kernel: {launches, ms, bytes, flops}} of the launches recorded since profile_enable(True)."""
+    names = (ctypes.c_char_p * max_names)()
+    cnt = (ctypes.c_int32 * max_names)()
+    ms, by, fl = (ctypes.c_double * max_names)(), (ctypes.c_double * max_names)(), (ctypes.c_double * max_names)()
+    n = lib().gdp_profile_read(max_names, names, cnt, ms, by, fl)
+    if n < 0:
+        raise GdpError(1, "gdp_profile_read")
+    return {names[i].decode(): {"launches": int(cnt[i]), "ms": ms[i], "bytes": by[i], "flops": fl[i]}
+            for i in range(n)}
 
 
 def _check(st: int, where: str):

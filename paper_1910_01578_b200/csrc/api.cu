@@ -6,6 +6,7 @@
 #include <climits>
 #include <cstring>
 #include <functional>
+#include <mutex>
 #include <queue>
 #include <string>
 #include <vector>
@@ -18,7 +19,36 @@ namespace gdp {
 static thread_local std::string g_err = "ok";
 static std::atomic<unsigned long long> g_launches{0};
 
-void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+// per-launch timing (gdp_profile_*): an event before every launch; a launch's time is the gap
+// to the next event recorded on the same stream (exact when the host runs ahead of the GPU)
+struct ProfRec {
+  const char *name;   // nullptr: closing mark
+  cudaStream_t s;
+  cudaEvent_t ev;
+  double bytes, flops;
+};
+static std::mutex g_prof_mu;
+static std::atomic<int> g_prof_on{0};
+static std::vector<ProfRec> g_prof;
+static std::vector<cudaEvent_t> g_prof_pool;
+
+static void prof_record(const char *name, cudaStream_t s, double bytes, double flops) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  cudaEvent_t e;
+  if (g_prof_pool.empty()) {
+    if (cudaEventCreate(&e) != cudaSuccess) return;
+  } else {
+    e = g_prof_pool.back();
+    g_prof_pool.pop_back();
+  }
+  cudaEventRecord(e, s);
+  g_prof.push_back({name, s, e, bytes, flops});
+}
+
+void note_launch(const char *name, cudaStream_t s, double bytes, double flops) {
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  if (g_prof_on.load(std::memory_order_relaxed)) prof_record(name, s, bytes, flops);
+}
 
 void set_error(const std::string &msg) { g_err = msg; }
 
@@ -212,6 +242,55 @@ extern "C" {
 const char *gdp_last_error(void) { return g_err.c_str(); }
 
 uint64_t gdp_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
+
+gdp_status gdp_profile_enable(int32_t on) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  if (on) {
+    for (auto &r : g_prof) g_prof_pool.push_back(r.ev);
+    g_prof.clear();
+  }
+  g_prof_on.store(on ? 1 : 0);
+  return GDP_OK;
+}
+
+gdp_status gdp_profile_mark(void *stream) {
+  if (!g_prof_on.load()) return fail(GDP_ERR_ARG, "profiling is not enabled");
+  prof_record(nullptr, static_cast<cudaStream_t>(stream), 0.0, 0.0);
+  return GDP_OK;
+}
+
+int32_t gdp_profile_read(int32_t max_names, const char **names, int32_t *launches, double *ms, double *bytes,
+                         double *flops) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  if (max_names < 0 || (max_names > 0 && (!names || !launches || !ms || !bytes || !flops))) {
+    set_error("gdp_profile_read: bad arguments");
+    return -1;
+  }
+  for (auto &r : g_prof)
+    if (cudaEventSynchronize(r.ev) != cudaSuccess) {
+      set_error("gdp_profile_read: event synchronisation failed");
+      return -1;
+    }
+  int n = 0;
+  for (size_t i = 0; i < g_prof.size(); i++) {
+    const ProfRec &r = g_prof[i];
+    if (!r.name) continue;
+    size_t j = i + 1;
+    while (j < g_prof.size() && g_prof[j].s != r.s) j++;
+    if (j == g_prof.size()) continue;   // no later event on its stream: untimed
+    float t = 0.f;
+    if (cudaEventElapsedTime(&t, r.ev, g_prof[j].ev) != cudaSuccess) continue;
+    int k = 0;
+    while (k < n && std::strcmp(names[k], r.name) != 0) k++;
+    if (k == n) {
+      if (n == max_names) continue;
+      names[n] = r.name; launches[n] = 0; ms[n] = 0.0; bytes[n] = 0.0; flops[n] = 0.0;
+      n++;
+    }
+    launches[k] += 1; ms[k] += t; bytes[k] += r.bytes; flops[k] += r.flops;
+  }
+  return n;
+}
 
 const char *gdp_build_info(void) { return "libgdp sm_100a built " __DATE__ " " __TIME__; }
 

@@ -18,7 +18,9 @@ constexpr int kMaxD = 8;
 constexpr float kLnEps = 1e-5f;
 
 void set_error(const std::string &msg);
-void note_launch();   // counts kernel launches (gdp_launch_count)
+// counts kernel launches (gdp_launch_count); while gdp_profile_enable(1) is on it also records
+// a CUDA event on s tagged with the kernel name and its algorithmic bytes / flops (0 = not stated)
+void note_launch(const char *name, cudaStream_t s, double bytes = 0.0, double flops = 0.0);
 gdp_status cuda_status(cudaError_t e, const char *what);
 
 #define GDP_CUDA_CHECK(expr)                                      \
@@ -142,6 +144,12 @@ struct GemmArgs {
   int epi;
 };
 void launch_gemm(const GemmArgs &a, cudaStream_t s);
+// algorithmic bytes of one GEMM launch: X, W, Y (+ residual, mask, accumulated Y), fp32
+inline double gemm_bytes(const GemmArgs &a) {
+  const double my = (double)a.M * a.Nout;
+  return 4.0 * ((double)a.M * a.K + (double)a.K * a.Nout + my + (a.R ? my : 0.0) + (a.aux ? my : 0.0) +
+                (a.accumulate ? my : 0.0));
+}
 // tcgen05 path (tc_gemm.cu); launch_gemm routes eligible shapes there when the calling
 // entry point enabled tensor cores (gdp_config.tensor_cores)
 bool tc_eligible(const GemmArgs &a);
@@ -166,9 +174,11 @@ void launch_layernorm_bwd(const float *x, const float *mu, const float *rs, cons
                           int N, cudaStream_t s);
 void launch_colsum(const float *x, int N, int C, float scale, float *out, float *part, cudaStream_t s);
 
-void launch_gather_max(const float *Z, const int *ptr, const int *idx, float *A, int *ARG, int N, cudaStream_t s);
+// nnz = ptr[N] (symmetric neighbour entries), used only for the algorithmic byte count
+void launch_gather_max(const float *Z, const int *ptr, const int *idx, float *A, int *ARG, int N, long long nnz,
+                       cudaStream_t s);
 void launch_gather_max_bwd(const float *dA, const int *ARG, const float *Z, const int *ptr, const int *idx,
-                           float *dPre, int N, cudaStream_t s);
+                           float *dPre, int N, long long nnz, cudaStream_t s);
 
 void launch_attn_fwd(const float *qkv, float *o, float *lse, int N, int S, int M, cudaStream_t s);
 void launch_relu_v(const float *qkv, float *o, int N, cudaStream_t s);

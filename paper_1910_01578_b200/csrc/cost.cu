@@ -449,14 +449,14 @@ gdp_status launch_cost(const gdp_graph_s *g, const gdp_topo_s *t, const uint8_t 
   G.cost = g->cost; G.leader = g->leader;
   G.out_bytes = g->out_bytes; G.mem_bytes = g->mem_bytes;
   G.has_coloc = g->has_coloc ? 1 : 0;
-  note_launch();
+  note_launch("k_cost", s);
   k_cost<<<B, 32, 0, s>>>(G, T, D, B, w.c_rem, w.c_rcons, w.c_fifo, w.c_new, w.c_chq, rep, peak, busy, reward);
   GDP_LAUNCH_CHECK("k_cost");
   return GDP_OK;
 }
 
 void launch_advantage(const double *r, int B, double *sum, long long *cnt, double *adv, cudaStream_t s) {
-  note_launch();
+  note_launch("k_advantage", s);
   k_advantage<<<1, 32, 0, s>>>(r, B, sum, cnt, adv);
 }
 

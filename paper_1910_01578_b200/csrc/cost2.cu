@@ -861,7 +861,7 @@ bool launch_cost2(const Cost2Graph &G, const TopoArgs &T, const uint8_t *D, int 
     cudaFuncSetAttribute(k_cost3, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     configured = smem;
   }
-  note_launch();
+  note_launch("k_cost2", s);
   static const int dbg = getenv("GDP_COST_DBG") ? atoi(getenv("GDP_COST_DBG")) : 0;
   static const bool v2 = getenv("GDP_COST_V2") != nullptr;   // owner-lane kernel (comparison)
   if (v2) k_cost2<<<B, 32, smem, s>>>(G, T, D, scratch, per_place, rep, peak, busy, reward, dbg);

@@ -652,7 +652,7 @@ bool launch_cost4(const Cost2Graph &G, const TopoArgs &T, int min_cost, const ui
   }
   static_assert(2 * SO4 + SI4 == 24, "24 staging lanes");
   static const int dbg = getenv("GDP_COST_DBG") ? atoi(getenv("GDP_COST_DBG")) : 0;
-  note_launch();
+  note_launch("k_cost4", s);
   k_cost4<<<B, 32 * (d + 1), smem, s>>>(G, T, D, scratch, per_place, rep, peak, busy, reward, L, dbg);
   return true;
 }

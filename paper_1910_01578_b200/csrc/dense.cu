@@ -297,7 +297,7 @@ void launch_gemm(const GemmArgs &a, cudaStream_t s) {
     return;
   }
   dim3 grid((a.M + BM - 1) / BM, (a.Nout + BN - 1) / BN);
-  note_launch();
+  note_launch("k_gemm", s, gemm_bytes(a), 2.0 * a.M * a.K * a.Nout);
   k_gemm<<<grid, NT, 0, s>>>(a);
 }
 
@@ -309,16 +309,16 @@ void launch_wgrad(int M, int K, int Nout, const float *X1, int ldx1, int K1, con
   if (chunks < 1) chunks = 1;
   (void)part_floats;
   dim3 grid((Kaug + BM - 1) / BM, (Nout + BN - 1) / BN, chunks);
-  note_launch();
+  note_launch("k_wgrad", s, 4.0 * M * (K + Nout) + 4.0 * chunks * Kaug * Nout, 2.0 * M * Kaug * Nout);
   k_wgrad<<<grid, NT, 0, s>>>(M, K, Kaug, Nout, X1, ldx1, K1, X2, ldx2, dY, ldy, part);
   int count = Kaug * Nout;
-  note_launch();
+  note_launch("k_reduce_chunks", s);
   k_reduce_chunks<<<nblk(count, 256), 256, 0, s>>>(part, chunks, count, out, accumulate ? 1 : 0);
 }
 
 void launch_layernorm(const float *x, const float *g, const float *b, float *y, float *mu, float *rs, int N,
                       cudaStream_t s) {
-  note_launch();
+  note_launch("k_layernorm", s);
   k_layernorm<<<nblk((size_t)N * 32, 256), 256, 0, s>>>(x, g, b, y, mu, rs, N);
 }
 
@@ -326,40 +326,40 @@ void launch_layernorm_bwd(const float *x, const float *mu, const float *rs, cons
                           const float *da_extra, float *dx, bool dx_accumulate, float *dgb, float *part,
                           int N, cudaStream_t s) {
   int chunks = (N + LN_ROWS - 1) / LN_ROWS;
-  note_launch();
+  note_launch("k_layernorm_bwd", s);
   k_layernorm_bwd<<<chunks, 256, 0, s>>>(x, mu, rs, g, da, da_extra, dx, dx_accumulate ? 1 : 0, part, N);
-  note_launch();
+  note_launch("k_reduce_chunks", s);
   k_reduce_chunks<<<1, 128, 0, s>>>(part, chunks, 128, dgb, 1);
 }
 
 void launch_colsum(const float *x, int N, int C, float scale, float *out, float *part, cudaStream_t s) {
   int chunks = (N + LN_ROWS - 1) / LN_ROWS;
-  note_launch();
+  note_launch("k_colsum_part", s);
   k_colsum_part<<<chunks, 256, 0, s>>>(x, N, C, part);
-  note_launch();
+  note_launch("k_reduce_scaled", s);
   k_reduce_scaled<<<nblk(C, 256), 256, 0, s>>>(part, chunks, C, scale, out);
 }
 
 void launch_rows_gather(const float *src, const int *perm, float *dst, int N, int C, cudaStream_t s) {
-  note_launch();
+  note_launch("k_rows_gather", s);
   k_rows_gather<<<nblk((size_t)N * C, 256), 256, 0, s>>>(src, perm, dst, N, C);
 }
 void launch_rows_scatter(const float *src, const int *perm, float *dst, int N, int C, bool accumulate,
                          cudaStream_t s) {
-  note_launch();
+  note_launch("k_rows_scatter", s);
   k_rows_scatter<<<nblk((size_t)N * C, 256), 256, 0, s>>>(src, perm, dst, N, C, accumulate ? 1 : 0);
 }
 void launch_tanh_grad(const float *dHn, const float *Hn, float *dP, int n, cudaStream_t s) {
-  note_launch();
+  note_launch("k_tanh_grad", s);
   k_tanh_grad<<<nblk(n, 256), 256, 0, s>>>(dHn, Hn, dP, (size_t)n);
 }
 void launch_add(const float *a, int lda, const float *b, int ldb, float *c, int ldc, int rows, int cols,
                 cudaStream_t s) {
-  note_launch();
+  note_launch("k_add", s);
   k_add<<<nblk((size_t)rows * cols, 256), 256, 0, s>>>(a, lda, b, ldb, c, ldc, rows, cols);
 }
 void launch_fill_rows(float *dst, const float *row, float scale, int N, int C, cudaStream_t s) {
-  note_launch();
+  note_launch("k_fill_rows", s);
   k_fill_rows<<<nblk((size_t)N * C, 256), 256, 0, s>>>(dst, row, scale, N, C);
 }
 

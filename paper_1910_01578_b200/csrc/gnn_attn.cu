@@ -11,6 +11,7 @@
 //                       keys [max(0, tau S - M), min((tau+1) S, N)) with an online softmax;
 //                       the backward splits dK/dV into the own-segment part (flows into x)
 //                       and the memory part (stop-gradient: parameters only).
+#include <algorithm>
 #include "common.cuh"
 
 namespace gdp {
@@ -265,16 +266,19 @@ __global__ void __launch_bounds__(AQ) k_attn_bwd_dkv(const float *__restrict__ q
 
 }  // namespace
 
-void launch_gather_max(const float *Z, const int *ptr, const int *idx, float *A, int *ARG, int N, cudaStream_t s) {
+// algorithmic (unique) bytes: CSR (N + 1 + nnz) x 4, Z read once N x 64 x 4, A and ARG written
+void launch_gather_max(const float *Z, const int *ptr, const int *idx, float *A, int *ARG, int N, long long nnz,
+                       cudaStream_t s) {
   unsigned blocks = (unsigned)(((size_t)N * 32 + 255) / 256);
-  note_launch();
+  note_launch("k_gather_max", s, 4.0 * ((double)N + 1 + (double)nnz) + 3.0 * 4 * 64 * (double)N);
   k_gather_max<<<blocks, 256, 0, s>>>(Z, ptr, idx, A, ARG, N);
 }
 
 void launch_gather_max_bwd(const float *dA, const int *ARG, const float *Z, const int *ptr, const int *idx,
-                           float *dPre, int N, cudaStream_t s) {
+                           float *dPre, int N, long long nnz, cudaStream_t s) {
   unsigned blocks = (unsigned)(((size_t)N * 32 + 255) / 256);
-  note_launch();
+  // CSR, dA and ARG of every neighbour read once per node (unique), dPre written
+  note_launch("k_gather_max_bwd", s, 4.0 * ((double)N + 1 + (double)nnz) + 3.0 * 4 * 64 * (double)N);
   k_gather_max_bwd<<<blocks, 256, 0, s>>>(dA, ARG, Z, ptr, idx, dPre, N);
 }
 
@@ -299,28 +303,39 @@ __global__ void k_relu_v_bwd(const float *__restrict__ qkv, const float *__restr
 }
 
 void launch_relu_v(const float *qkv, float *o, int N, cudaStream_t s) {
-  note_launch();
+  note_launch("k_relu_v", s);
   k_relu_v<<<(unsigned)(((size_t)N * 64 + 255) / 256), 256, 0, s>>>(qkv, o, N);
 }
 void launch_relu_v_bwd(const float *qkv, const float *dout, float *dqkv, float *dkvm, int N, cudaStream_t s) {
-  note_launch();
+  note_launch("k_relu_v_bwd", s);
   k_relu_v_bwd<<<(unsigned)(((size_t)N * 64 + 255) / 256), 256, 0, s>>>(qkv, dout, dqkv, dkvm, N);
+}
+
+// 4 x 64 flops per (query, key) pair over the key sets K(i) (QK^T and PV), i.e. the forward
+static double attn_flops(int N, int S, int M) {
+  double pairs = 0.0;
+  for (long long t0 = 0; t0 < N; t0 += S) {
+    const long long q = std::min<long long>(S, N - t0);
+    const long long lo = M < 0 ? 0 : std::max<long long>(0, t0 - M);
+    pairs += (double)q * (double)(t0 + q - lo);
+  }
+  return 4.0 * 64 * pairs;
 }
 
 void launch_attn_fwd(const float *qkv, float *o, float *lse, int N, int S, int M, cudaStream_t s) {
   int nseg = (N + S - 1) / S;
-  note_launch();
+  note_launch("k_attn_fwd", s, 4.0 * (double)N * (192 + 64 + kHeads), attn_flops(N, S, M));
   k_attn_fwd<<<dim3(nseg, kHeads), AQ, 0, s>>>(qkv, o, lse, N, S, M);
 }
 
 void launch_attn_bwd(const float *qkv, const float *o, const float *lse, const float *dout, float *dqkv,
                      float *dkvm, float *Dd, int N, int S, int M, cudaStream_t s) {
   int nseg = (N + S - 1) / S;
-  note_launch();
+  note_launch("k_attn_bwd_prep", s);
   k_attn_bwd_prep<<<(N * kHeads + 255) / 256, 256, 0, s>>>(o, dout, Dd, N);
-  note_launch();
+  note_launch("k_attn_bwd_dq", s, 4.0 * (double)N * (192 + 64 + 64 + 2 * kHeads), attn_flops(N, S, M));
   k_attn_bwd_dq<<<dim3(nseg, kHeads), AQ, 0, s>>>(qkv, lse, dout, Dd, dqkv, N, S, M);
-  note_launch();
+  note_launch("k_attn_bwd_dkv", s, 4.0 * (double)N * (192 + 64 + 128 + 2 * kHeads), 1.5 * attn_flops(N, S, M));
   k_attn_bwd_dkv<<<dim3(nseg, kHeads), AQ, 0, s>>>(qkv, lse, dout, Dd, dqkv, dkvm, N, S, M, nseg);
 }
 

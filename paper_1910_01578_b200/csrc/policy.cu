@@ -196,7 +196,7 @@ void fold_layer(const WS &w, const Offs &off, const float *theta, int l, const f
   a.go = g ? g[3] : nullptr; a.g1 = g ? g[4] : nullptr; a.g2 = g ? g[5] : nullptr;
   a.Wqkv = L.Wqkv; a.bqkv = L.bqkv; a.Wo = L.Wo; a.W1 = L.W1; a.W2 = L.W2;
   const int n = 64 * 192 + 192 + 64 * 64 + 64 * 256 + 256 * 64;
-  note_launch();
+  note_launch("k_fold_layer", s);
   k_fold_layer<<<nblk(n, 256), 256, 0, s>>>(a);
 }
 
@@ -252,7 +252,7 @@ void layer_bwd(const WS &w, const Offs &off, const float *theta, int l, const fl
   if (no_attention()) launch_relu_v_bwd(L.qkv, w.dout, w.dqkv, w.dkvm, N, s);
   else launch_attn_bwd(L.qkv, L.o, L.lse, w.dout, w.dqkv, w.dkvm, w.dd, N, S, M, s);
   // totals for the parameter gradients: dkvt = [dQ | dK_own + dK_mem | dV_own + dV_mem]
-  note_launch();
+  note_launch("k_copy_cols", s);
   k_copy_cols<<<nblk((size_t)N * 64, 256), 256, 0, s>>>(w.dqkv, 192, w.dkvt, 192, N, 64);
   launch_add(w.dqkv + 64, 192, w.dkvm, 128, w.dkvt + 64, 192, N, 128, s);
   launch_wgrad(N, kH, 192, L.a, kH, kH, nullptr, 0, w.dkvt, 192, true, w.part, w.part_floats, L.dWqkv, false, s);
@@ -287,7 +287,7 @@ void add_layer_rows(RowTable &T, const WS &w, const Offs &off, int l, const floa
 void run_rows(const RowTable &T, const float *theta, float *grad, cudaStream_t s) {
   if (T.count == 0) return;
   dim3 grid(nblk(257, 128), T.count);
-  note_launch();
+  note_launch("k_gate_bwd_rows", s);
   k_gate_bwd_rows<<<grid, 128, 0, s>>>(theta, T, grad);
 }
 
@@ -310,7 +310,7 @@ gdp_status run_embed(const gdp_graph_s *g, const float *theta, float *node_emb, 
     a.bias = theta + off[pW + 1];
     a.epi = EPI_SIGMOID;
     launch_gemm(a, s);
-    launch_gather_max(w.Z[l], g->nbr_ptr, g->nbr_idx, w.A[l], w.ARG[l], N, s);
+    launch_gather_max(w.Z[l], g->nbr_ptr, g->nbr_idx, w.A[l], w.ARG[l], N, g->E_sym, s);
     // H' = tanh([H | A] W_f + b_f) (Eq. 3)
     float *out = (l == kGNN - 1) ? w.H[3] : w.H[l + 1];
     a = gemm(N, 2 * kH, kH, w.H[l], kH, theta + off[pW + 2], kH, 1, out, kH);
@@ -342,14 +342,14 @@ gdp_status run_place(const gdp_graph_s *g, const gdp_config *c, const float *the
     fold_layer(w, off, theta, 0, nullptr, s);
     layer_fwd(w, off, theta, 0, w.Etopo, N, S, M, s);
     launch_colsum(w.L[0].y, N, kH, 1.0f / (float)N, w.z, w.part, s);
-    note_launch();
+    note_launch("k_gates", s);
     k_gates<<<1, 256, 0, s>>>(theta, w.z, GT, w.gam);
     for (int j = 0; j < 6; j++) { g0[j] = gam_of(w, GT, 0, j); g1[j] = gam_of(w, GT, 1, j); }
     gh = w.gam + GT.m[12].goff;
   }
   fold_layer(w, off, theta, 1, sup ? g0 : nullptr, s);
   fold_layer(w, off, theta, 2, sup ? g1 : nullptr, s);
-  note_launch();
+  note_launch("k_fold_head", s);
   k_fold_head<<<nblk(kH * d, 256), 256, 0, s>>>(theta, (int)off[GDP_P_HEAD_W], d, gh, w.Wh);
   layer_fwd(w, off, theta, 1, w.Etopo, N, S, M, s);
   layer_fwd(w, off, theta, 2, w.L[1].y, N, S, M, s);
@@ -402,9 +402,9 @@ gdp_status run_policy_grad(const gdp_graph_s *g, const gdp_config *c, const floa
   run_rows(RT, theta, grad, s);
   if (sup) {
     dim3 gp(nblk((kH + 1) * kFFN, 256), kGateCount);
-    note_launch();
+    note_launch("k_gate_bwd_P", s);
     k_gate_bwd_P<<<gp, 256, 0, s>>>(w.z, w.dgam, GT, grad);
-    note_launch();
+    note_launch("k_gate_bwd_z", s);
     k_gate_bwd_z<<<1, 64, 0, s>>>(theta, w.dgam, GT, 1.0f / (float)N, w.dz);
     // conditioner: z = mean_v C_v -> dC_v = dz / N for every node
     launch_fill_rows(w.dy, w.dz, 1.0f, N, kH, s);
@@ -433,7 +433,7 @@ gdp_status run_policy_grad(const gdp_graph_s *g, const gdp_config *c, const floa
     a = gemm(N, kH, 2 * kH, w.dP, kH, theta + off[pW + 2], 1, kH, dH, kH);   // [dH | dA] = dP Wf^T
     a.split = kH; a.Y2 = w.dAg; a.ldy2 = kH;
     launch_gemm(a, s);
-    launch_gather_max_bwd(w.dAg, w.ARG[l], w.Z[l], g->nbr_ptr, g->nbr_idx, w.dP, N, s);   // dP := dpre
+    launch_gather_max_bwd(w.dAg, w.ARG[l], w.Z[l], g->nbr_ptr, g->nbr_idx, w.dP, N, g->E_sym, s);   // dP := dpre
     launch_wgrad(N, kH, kH, w.H[l], kH, kH, nullptr, 0, w.dP, kH, true, w.part, w.part_floats, grad + off[pW],
                  true, s);
     a = gemm(N, kH, kH, w.dP, kH, theta + off[pW], 1, kH, dH, kH);             // dH += dpre W^T

@@ -164,31 +164,31 @@ __global__ void k_logit_grad(const float *__restrict__ logits, int ld, const uin
 void launch_sample(const float *logits, int ld, const int *leader, bool has_coloc, int N, int d, int B, uint64_t seed,
                    uint64_t offset, uint64_t step, const uint64_t *step_ptr, float *cdf, float *logp, int *lastpos,
                    uint8_t *D, float *logprob, cudaStream_t s) {
-  note_launch();
+  note_launch("k_node_prep", s);
   k_node_prep<<<(N + 255) / 256, 256, 0, s>>>(logits, ld, N, d, cdf, logp, lastpos);
-  note_launch();
+  note_launch("k_sample", s, (double)B * N + 4.0 * (double)N * (2 * d + 1));
   k_sample<<<B, ST, 0, s>>>(cdf, logp, lastpos, leader, N, d, seed, offset, step, step_ptr, D, logprob);
   if (has_coloc) {
     size_t n = (size_t)N * B;
-    note_launch();
+    note_launch("k_colocate", s);
     k_colocate<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(leader, N, B, D);
   }
 }
 
 void launch_node_prep(const float *logits, int ld, int N, int d, float *cdf, float *logp, int *lastpos,
                       cudaStream_t s) {
-  note_launch();
+  note_launch("k_node_prep", s);
   k_node_prep<<<(N + 255) / 256, 256, 0, s>>>(logits, ld, N, d, cdf, logp, lastpos);
 }
 
 void launch_logit_grad(const float *logits, int ld, const uint8_t *D, const int *leader, const double *adv,
                        const float *logprob, const float *old_logprob, float eps, float beta, float scale,
                        int N, int d, int B, double *wb, float *dlog, cudaStream_t s) {
-  note_launch();
+  note_launch("k_weights", s);
   k_weights<<<(B + 255) / 256, 256, 0, s>>>(adv, logprob, old_logprob, eps, B, wb);
   size_t smem = (size_t)B * sizeof(double);
   if (smem > 48 * 1024) cudaFuncSetAttribute(k_logit_grad, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  note_launch();
+  note_launch("k_logit_grad", s, (double)B * N + 4.0 * 2 * (double)N * d);
   k_logit_grad<<<(N + 127) / 128, 128, smem, s>>>(logits, ld, D, leader, wb, beta, scale, N, d, B, dlog);
 }
 

@@ -247,7 +247,7 @@ void launch_gemm_tc(const GemmArgs &a, cudaStream_t s) {
   }
   const int ntiles = (a.M + TM - 1) / TM;
   const int grid = ntiles < 2 * num_sms() ? ntiles : 2 * num_sms();
-  note_launch();
+  note_launch("k_gemm_tc", s, gemm_bytes(a), 2.0 * a.M * a.K * a.Nout);
   k_gemm_tc<<<grid, TT, smem, s>>>(a, Kp, Np, ncols);
 }
 

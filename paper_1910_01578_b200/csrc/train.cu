@@ -134,13 +134,13 @@ int sm_count() {
 int adam_parts() { return 2 * sm_count() < kAdamScratch ? 2 * sm_count() : kAdamScratch; }
 
 void launch_greedy(const float *logits, int ld, const int *leader, int N, int d, uint8_t *D, cudaStream_t s) {
-  note_launch();
+  note_launch("k_greedy", s);
   k_greedy<<<(N + 255) / 256, 256, 0, s>>>(logits, ld, leader, N, d, D);
 }
 
 void launch_logprob(const float *logp, const int *leader, const uint8_t *D, int N, int d, int B, float *logprob,
                     cudaStream_t s) {
-  note_launch();
+  note_launch("k_logprob", s);
   k_logprob<<<B, LT, 0, s>>>(logp, leader, D, N, d, logprob);
 }
 
@@ -148,9 +148,9 @@ void launch_clip_adam(const float *g, long long n, double max_norm, double lr, d
                       double c1, double c2, float *theta, float *m, float *v, double *scratch, double *norm_out,
                       cudaStream_t s) {
   const int parts = adam_parts();
-  note_launch();
+  note_launch("k_sumsq", s);
   k_sumsq<<<parts, AT, 0, s>>>(g, n, scratch);
-  note_launch();
+  note_launch("k_adam", s);
   k_adam<<<parts, AT, 0, s>>>(g, n, scratch, parts, max_norm, lr, b1, b2, eps, c1, c2, theta, m, v, norm_out);
 }
 

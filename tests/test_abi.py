@@ -29,10 +29,22 @@ def header_functions():
 def test_exports_every_declared_symbol():
     L = gdp.lib()
     names = header_functions()
-    assert len(names) == 22
+    assert len(names) == 25
     assert sorted(names) == sorted(gdp.EXPORTS)
     for n in names:
         assert hasattr(L, n), n
+
+
+def test_profile_host_logic():
+    """gdp_profile_*: mark is refused while off; with no launch recorded the read is empty."""
+    with pytest.raises(gdp.GdpError):
+        gdp.profile_mark(0)
+    gdp.profile_enable(True)
+    try:
+        assert gdp.profile_read() == {}
+    finally:
+        gdp.profile_enable(False)
+    assert gdp.lib().gdp_profile_read(-1, None, None, None, None, None) == -1
 
 
 def test_param_layout_matches_oracle_and_header():
