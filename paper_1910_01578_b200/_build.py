@@ -25,7 +25,8 @@ def stale() -> bool:
 def build(force: bool = False) -> str:
     if force or stale():
         cu = [f for f in sources() if f.endswith(".cu")]
-        cmd = [NVCC] + FLAGS + ["-o", SO] + cu
+        extra = os.environ.get("GDP_NVCC_EXTRA", "").split()   # experiment macros (tools/variants)
+        cmd = [NVCC] + FLAGS + extra + ["-o", SO] + cu
         subprocess.check_call(cmd)
     return SO
 

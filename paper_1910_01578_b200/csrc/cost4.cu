@@ -27,8 +27,14 @@ namespace gdp {
 namespace {
 using namespace cu;
 
+#ifndef COST4_SLEEP_NS
+#define COST4_SLEEP_NS 200   // memory warp back-off when no window is pending
+#endif
 constexpr int WMAX = 8;    // window length cap (ticks) = buckets per window
-constexpr int R4 = 4;      // windows the memory warp may lag behind
+#ifndef COST4_R4
+#define COST4_R4 8
+#endif
+constexpr int R4 = COST4_R4;   // windows the memory warp may lag behind
 constexpr int SO4 = 8;     // staged out-edge records per slot
 constexpr int SI4 = 8;     // staged in-edge records per slot (2 * SO4 + SI4 = 24 staging lanes)
 constexpr int KF4 = 4;     // FIFO entries kept in smem per device
@@ -593,7 +599,7 @@ __global__ void __launch_bounds__(288, 2) k_cost4(Cost2Graph G, TopoArgs T, cons
       } else if (fin_all && done_w == S.nwin - 1) {
         break;
       } else {
-        __nanosleep(200);
+        if (COST4_SLEEP_NS > 0) __nanosleep(COST4_SLEEP_NS);
       }
     }
     if (lane < d) {

@@ -3,6 +3,8 @@
 //              Transformer-XL projections of §3.2 (M = N nodes, K, Nout <= 257).
 //  * k_wgrad:  dW = X^T dY split over row chunks, summed in fixed chunk order.
 //  * LayerNorm forward/backward (pre-LN), column sums (mean over nodes).
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace gdp {
@@ -88,17 +90,21 @@ __global__ void __launch_bounds__(NT) k_gemm(GemmArgs a) {
 }
 
 // ---- wgrad: partial[chunk][k][n] = sum_{rows in chunk} Xaug[r][k] dY[r][n]
-constexpr int WROWS = 256;   // rows per chunk
+// The grid covers the K real input columns; the bias row (Xaug's column K of ones) is the
+// column sum of dY, accumulated by the ty == 0 threads of the blockIdx.x == 0 blocks, so it
+// costs no extra 64-wide K tile.  Rows per chunk (rpc, a multiple of BK) are chosen on the
+// host so that the grid holds about 4 blocks per SM; fixed per shape, hence deterministic.
 __global__ void __launch_bounds__(NT) k_wgrad(int M, int K, int Kaug, int Nout, const float *X1, int ldx1,
                                               int K1, const float *X2, int ldx2, const float *dY, int ldy,
-                                              float *part) {
+                                              float *part, int rpc) {
   __shared__ float Xs[BK][BM + 4];
   __shared__ float Ys[BK][BN + 4];
   const int tid = threadIdx.x;
   const int k0 = blockIdx.x * BM, n0 = blockIdx.y * BN, chunk = blockIdx.z;
-  const int r0 = chunk * WROWS, r1 = min(M, r0 + WROWS);
+  const int r0 = chunk * rpc, r1 = min(M, r0 + rpc);
   const int ty = tid / 16, tx = tid % 16;
-  float acc[4][4];
+  const bool bias_rows = Kaug > K && blockIdx.x == 0 && ty == 0;
+  float acc[4][4], bacc[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
   for (int i = 0; i < 4; i++)
 #pragma unroll
@@ -110,10 +116,7 @@ __global__ void __launch_bounds__(NT) k_wgrad(int M, int K, int Kaug, int Nout, 
       int rr = e / BM, kk = e % BM;
       int r = rb + rr, k = k0 + kk;
       float v = 0.f;
-      if (r < r1 && k < Kaug) {
-        if (k == K) v = 1.f;
-        else v = (k < K1) ? X1[(size_t)r * ldx1 + k] : X2[(size_t)r * ldx2 + (k - K1)];
-      }
+      if (r < r1 && k < K) v = (k < K1) ? X1[(size_t)r * ldx1 + k] : X2[(size_t)r * ldx2 + (k - K1)];
       Xs[rr][kk] = v;
     }
 #pragma unroll
@@ -135,6 +138,10 @@ __global__ void __launch_bounds__(NT) k_wgrad(int M, int K, int Kaug, int Nout, 
       for (int i = 0; i < 4; i++)
 #pragma unroll
         for (int j = 0; j < 4; j++) acc[i][j] = fmaf(xv[i], yv[j], acc[i][j]);
+      if (bias_rows) {
+#pragma unroll
+        for (int j = 0; j < 4; j++) bacc[j] += yv[j];
+      }
     }
     __syncthreads();
   }
@@ -142,11 +149,18 @@ __global__ void __launch_bounds__(NT) k_wgrad(int M, int K, int Kaug, int Nout, 
 #pragma unroll
   for (int i = 0; i < 4; i++) {
     int k = k0 + ty * 4 + i;
-    if (k >= Kaug) continue;
+    if (k >= K) continue;
 #pragma unroll
     for (int j = 0; j < 4; j++) {
       int n = n0 + tx * 4 + j;
       if (n < Nout) P[(size_t)k * Nout + n] = acc[i][j];
+    }
+  }
+  if (bias_rows) {
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+      int n = n0 + tx * 4 + j;
+      if (n < Nout) P[(size_t)K * Nout + n] = bacc[j];
     }
   }
 }
@@ -290,6 +304,17 @@ static thread_local bool t_noattn = false;
 void set_no_attention(bool on) { t_noattn = on; }
 bool no_attention() { return t_noattn; }
 
+static int num_sms_dense() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
 void launch_gemm(const GemmArgs &a, cudaStream_t s) {
   if (a.M <= 0) return;
   if (t_tc && tc_eligible(a)) {
@@ -304,13 +329,17 @@ void launch_gemm(const GemmArgs &a, cudaStream_t s) {
 void launch_wgrad(int M, int K, int Nout, const float *X1, int ldx1, int K1, const float *X2, int ldx2,
                   const float *dY, int ldy, bool with_bias, float *part, size_t part_floats, float *out,
                   bool accumulate, cudaStream_t s) {
-  int Kaug = K + (with_bias ? 1 : 0);
-  int chunks = (M + WROWS - 1) / WROWS;
-  if (chunks < 1) chunks = 1;
-  (void)part_floats;
-  dim3 grid((Kaug + BM - 1) / BM, (Nout + BN - 1) / BN, chunks);
+  const int Kaug = K + (with_bias ? 1 : 0);
+  const int gx = (K + BM - 1) / BM, gy = (Nout + BN - 1) / BN;
+  // about 4 blocks per SM, within the partial buffer, at least BK rows per chunk
+  long long want = (4LL * num_sms_dense() + gx * gy - 1) / (gx * gy);
+  want = std::min<long long>(want, (long long)(part_floats / ((size_t)Kaug * Nout)));
+  want = std::max<long long>(1, std::min<long long>(want, (M + BK - 1) / BK));
+  const int rpc = (int)(((M + want - 1) / want + BK - 1) / BK * BK);
+  const int chunks = (M + rpc - 1) / rpc;
+  dim3 grid(gx, gy, chunks);
   note_launch("k_wgrad", s, 4.0 * M * (K + Nout) + 4.0 * chunks * Kaug * Nout, 2.0 * M * Kaug * Nout);
-  k_wgrad<<<grid, NT, 0, s>>>(M, K, Kaug, Nout, X1, ldx1, K1, X2, ldx2, dY, ldy, part);
+  k_wgrad<<<grid, NT, 0, s>>>(M, K, Kaug, Nout, X1, ldx1, K1, X2, ldx2, dY, ldy, part, rpc);
   int count = Kaug * Nout;
   note_launch("k_reduce_chunks", s);
   k_reduce_chunks<<<nblk(count, 256), 256, 0, s>>>(part, chunks, count, out, accumulate ? 1 : 0);

@@ -17,47 +17,75 @@
 namespace gdp {
 namespace {
 
+// neighbour ids are fetched 32 at a time (one coalesced load, shuffled out) and the rows of
+// GU neighbours are requested before any is compared, so the dependent-load chain per warp is
+// ceil(deg / GU) row latencies instead of deg; comparisons stay in ascending-id order
+constexpr int GU = 4;
+
 __global__ void k_gather_max(const float *__restrict__ Z, const int *__restrict__ ptr,
                              const int *__restrict__ idx, float *A, int *ARG, int N) {
-  int v = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  const int v = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (v >= N) return;
-  int b = ptr[v], e = ptr[v + 1];
-  float m0 = 0.f, m1 = 0.f;
+  const int b = ptr[v], e = ptr[v + 1];
+  const float2 *Z2 = reinterpret_cast<const float2 *>(Z);   // lane owns channels 2 lane, 2 lane + 1
+  float2 m = make_float2(0.f, 0.f);
   int a0 = -1, a1 = -1;
-  if (b < e) {
-    int u = idx[b];
-    m0 = Z[(size_t)u * kH + lane];
-    m1 = Z[(size_t)u * kH + lane + 32];
-    a0 = a1 = u;
-    for (int j = b + 1; j < e; j++) {
-      u = idx[j];
-      float z0 = Z[(size_t)u * kH + lane], z1 = Z[(size_t)u * kH + lane + 32];
-      if (z0 > m0) { m0 = z0; a0 = u; }
-      if (z1 > m1) { m1 = z1; a1 = u; }
+  for (int j0 = b; j0 < e; j0 += 32) {
+    const int n = min(32, e - j0);
+    const int mine = lane < n ? __ldg(idx + j0 + lane) : 0;
+    for (int k0 = 0; k0 < n; k0 += GU) {
+      int u[GU];
+      float2 z[GU];
+#pragma unroll
+      for (int t = 0; t < GU; t++) {
+        u[t] = __shfl_sync(0xffffffffu, mine, (k0 + t) & 31);
+        if (k0 + t < n) z[t] = __ldg(Z2 + (size_t)u[t] * (kH / 2) + lane);
+      }
+#pragma unroll
+      for (int t = 0; t < GU; t++) {
+        if (k0 + t >= n) break;
+        if (a0 < 0 || z[t].x > m.x) { m.x = z[t].x; a0 = u[t]; }   // strict '>': first maximiser wins
+        if (a1 < 0 || z[t].y > m.y) { m.y = z[t].y; a1 = u[t]; }
+      }
     }
   }
-  A[(size_t)v * kH + lane] = m0;
-  A[(size_t)v * kH + lane + 32] = m1;
-  ARG[(size_t)v * kH + lane] = a0;
-  ARG[(size_t)v * kH + lane + 32] = a1;
+  reinterpret_cast<float2 *>(A)[(size_t)v * (kH / 2) + lane] = m;
+  reinterpret_cast<int2 *>(ARG)[(size_t)v * (kH / 2) + lane] = make_int2(a0, a1);
 }
 
 __global__ void k_gather_max_bwd(const float *__restrict__ dA, const int *__restrict__ ARG,
                                  const float *__restrict__ Z, const int *__restrict__ ptr,
                                  const int *__restrict__ idx, float *dPre, int N) {
-  int u = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  const int u = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (u >= N) return;
+  const int b = ptr[u], e = ptr[u + 1];
+  const float2 *dA2 = reinterpret_cast<const float2 *>(dA);
+  const int2 *ARG2 = reinterpret_cast<const int2 *>(ARG);
   float s0 = 0.f, s1 = 0.f;
-  for (int j = ptr[u]; j < ptr[u + 1]; j++) {
-    int v = idx[j];
-    size_t o = (size_t)v * kH;
-    if (ARG[o + lane] == u) s0 += dA[o + lane];
-    if (ARG[o + lane + 32] == u) s1 += dA[o + lane + 32];
+  for (int j0 = b; j0 < e; j0 += 32) {
+    const int n = min(32, e - j0);
+    const int mine = lane < n ? __ldg(idx + j0 + lane) : 0;
+    for (int k0 = 0; k0 < n; k0 += GU) {
+      int2 ag[GU];
+      float2 g[GU];
+#pragma unroll
+      for (int t = 0; t < GU; t++) {
+        const int v = __shfl_sync(0xffffffffu, mine, (k0 + t) & 31);
+        if (k0 + t < n) {
+          ag[t] = __ldg(ARG2 + (size_t)v * (kH / 2) + lane);
+          g[t] = __ldg(dA2 + (size_t)v * (kH / 2) + lane);
+        }
+      }
+#pragma unroll
+      for (int t = 0; t < GU; t++) {   // ascending neighbour order, as the oracle sums
+        if (k0 + t >= n) break;
+        if (ag[t].x == u) s0 += g[t].x;
+        if (ag[t].y == u) s1 += g[t].y;
+      }
+    }
   }
-  size_t o = (size_t)u * kH;
-  float z0 = Z[o + lane], z1 = Z[o + lane + 32];
-  dPre[o + lane] = s0 * z0 * (1.f - z0);
-  dPre[o + lane + 32] = s1 * z1 * (1.f - z1);
+  const float2 z = reinterpret_cast<const float2 *>(Z)[(size_t)u * (kH / 2) + lane];
+  reinterpret_cast<float2 *>(dPre)[(size_t)u * (kH / 2) + lane] = make_float2(s0 * z.x * (1.f - z.x), s1 * z.y * (1.f - z.y));
 }
 
 constexpr int AQ = 128;  // queries (or keys) per thread block pass
