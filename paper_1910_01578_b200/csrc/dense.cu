@@ -93,7 +93,7 @@ __global__ void __launch_bounds__(NT) k_gemm(GemmArgs a) {
 // The grid covers the K real input columns; the bias row (Xaug's column K of ones) is the
 // column sum of dY, accumulated by the ty == 0 threads of the blockIdx.x == 0 blocks, so it
 // costs no extra 64-wide K tile.  Rows per chunk (rpc, a multiple of BK) are chosen on the
-// host so that the grid holds about 4 blocks per SM; fixed per shape, hence deterministic.
+// host so that the grid holds about 2 blocks per SM; fixed per shape, hence deterministic.
 __global__ void __launch_bounds__(NT) k_wgrad(int M, int K, int Kaug, int Nout, const float *X1, int ldx1,
                                               int K1, const float *X2, int ldx2, const float *dY, int ldy,
                                               float *part, int rpc) {
@@ -331,8 +331,8 @@ void launch_wgrad(int M, int K, int Nout, const float *X1, int ldx1, int K1, con
                   bool accumulate, cudaStream_t s) {
   const int Kaug = K + (with_bias ? 1 : 0);
   const int gx = (K + BM - 1) / BM, gy = (Nout + BN - 1) / BN;
-  // about 4 blocks per SM, within the partial buffer, at least BK rows per chunk
-  long long want = (4LL * num_sms_dense() + gx * gy - 1) / (gx * gy);
+  // about 2 blocks per SM, within the partial buffer, at least BK rows per chunk
+  long long want = (2LL * num_sms_dense() + gx * gy - 1) / (gx * gy);
   want = std::min<long long>(want, (long long)(part_floats / ((size_t)Kaug * Nout)));
   want = std::max<long long>(1, std::min<long long>(want, (M + BK - 1) / BK));
   const int rpc = (int)(((M + want - 1) / want + BK - 1) / BK * BK);

@@ -17,10 +17,27 @@
 namespace gdp {
 namespace {
 
-// neighbour ids are fetched 32 at a time (one coalesced load, shuffled out) and the rows of
-// GU neighbours are requested before any is compared, so the dependent-load chain per warp is
-// ceil(deg / GU) row latencies instead of deg; comparisons stay in ascending-id order
-constexpr int GU = 4;
+// neighbour ids are fetched 32 at a time (one coalesced load, shuffled out) and the rows of up
+// to G neighbours are requested before any is compared, so the dependent-load chain of a node
+// of degree deg is about deg / 16 row latencies (the heavy-tailed nodes of the GNMT graphs, deg
+// up to 361, set the kernel's duration); comparisons stay in ascending-id order
+template <int G>
+__device__ __forceinline__ void gmax_batch(const float2 *Z2, int mine, int k0, int n, int lane, float2 &m, int &a0,
+                                           int &a1) {
+  int u[G];
+  float2 z[G];
+#pragma unroll
+  for (int t = 0; t < G; t++) {
+    u[t] = __shfl_sync(0xffffffffu, mine, (k0 + t) & 31);
+    if (k0 + t < n) z[t] = __ldg(Z2 + (size_t)u[t] * (kH / 2) + lane);
+  }
+#pragma unroll
+  for (int t = 0; t < G; t++) {
+    if (k0 + t >= n) break;
+    if (a0 < 0 || z[t].x > m.x) { m.x = z[t].x; a0 = u[t]; }   // strict '>': first maximiser wins
+    if (a1 < 0 || z[t].y > m.y) { m.y = z[t].y; a1 = u[t]; }
+  }
+}
 
 __global__ void k_gather_max(const float *__restrict__ Z, const int *__restrict__ ptr,
                              const int *__restrict__ idx, float *A, int *ARG, int N) {
@@ -33,24 +50,33 @@ __global__ void k_gather_max(const float *__restrict__ Z, const int *__restrict_
   for (int j0 = b; j0 < e; j0 += 32) {
     const int n = min(32, e - j0);
     const int mine = lane < n ? __ldg(idx + j0 + lane) : 0;
-    for (int k0 = 0; k0 < n; k0 += GU) {
-      int u[GU];
-      float2 z[GU];
-#pragma unroll
-      for (int t = 0; t < GU; t++) {
-        u[t] = __shfl_sync(0xffffffffu, mine, (k0 + t) & 31);
-        if (k0 + t < n) z[t] = __ldg(Z2 + (size_t)u[t] * (kH / 2) + lane);
-      }
-#pragma unroll
-      for (int t = 0; t < GU; t++) {
-        if (k0 + t >= n) break;
-        if (a0 < 0 || z[t].x > m.x) { m.x = z[t].x; a0 = u[t]; }   // strict '>': first maximiser wins
-        if (a1 < 0 || z[t].y > m.y) { m.y = z[t].y; a1 = u[t]; }
-      }
-    }
+    int k0 = 0;
+    for (; k0 + 16 <= n; k0 += 16) gmax_batch<16>(Z2, mine, k0, n, lane, m, a0, a1);
+    for (; k0 < n; k0 += 4) gmax_batch<4>(Z2, mine, k0, n, lane, m, a0, a1);
   }
   reinterpret_cast<float2 *>(A)[(size_t)v * (kH / 2) + lane] = m;
   reinterpret_cast<int2 *>(ARG)[(size_t)v * (kH / 2) + lane] = make_int2(a0, a1);
+}
+
+template <int G>
+__device__ __forceinline__ void gmax_bwd_batch(const float2 *dA2, const int2 *ARG2, int mine, int k0, int n, int lane,
+                                               int u, float &s0, float &s1) {
+  int2 ag[G];
+  float2 g[G];
+#pragma unroll
+  for (int t = 0; t < G; t++) {
+    const int v = __shfl_sync(0xffffffffu, mine, (k0 + t) & 31);
+    if (k0 + t < n) {
+      ag[t] = __ldg(ARG2 + (size_t)v * (kH / 2) + lane);
+      g[t] = __ldg(dA2 + (size_t)v * (kH / 2) + lane);
+    }
+  }
+#pragma unroll
+  for (int t = 0; t < G; t++) {   // ascending neighbour order, as the oracle sums
+    if (k0 + t >= n) break;
+    if (ag[t].x == u) s0 += g[t].x;
+    if (ag[t].y == u) s1 += g[t].y;
+  }
 }
 
 __global__ void k_gather_max_bwd(const float *__restrict__ dA, const int *__restrict__ ARG,
@@ -65,24 +91,9 @@ __global__ void k_gather_max_bwd(const float *__restrict__ dA, const int *__rest
   for (int j0 = b; j0 < e; j0 += 32) {
     const int n = min(32, e - j0);
     const int mine = lane < n ? __ldg(idx + j0 + lane) : 0;
-    for (int k0 = 0; k0 < n; k0 += GU) {
-      int2 ag[GU];
-      float2 g[GU];
-#pragma unroll
-      for (int t = 0; t < GU; t++) {
-        const int v = __shfl_sync(0xffffffffu, mine, (k0 + t) & 31);
-        if (k0 + t < n) {
-          ag[t] = __ldg(ARG2 + (size_t)v * (kH / 2) + lane);
-          g[t] = __ldg(dA2 + (size_t)v * (kH / 2) + lane);
-        }
-      }
-#pragma unroll
-      for (int t = 0; t < GU; t++) {   // ascending neighbour order, as the oracle sums
-        if (k0 + t >= n) break;
-        if (ag[t].x == u) s0 += g[t].x;
-        if (ag[t].y == u) s1 += g[t].y;
-      }
-    }
+    int k0 = 0;
+    for (; k0 + 16 <= n; k0 += 16) gmax_bwd_batch<16>(dA2, ARG2, mine, k0, n, lane, u, s0, s1);
+    for (; k0 < n; k0 += 4) gmax_bwd_batch<4>(dA2, ARG2, mine, k0, n, lane, u, s0, s1);
   }
   const float2 z = reinterpret_cast<const float2 *>(Z)[(size_t)u * (kH / 2) + lane];
   reinterpret_cast<float2 *>(dPre)[(size_t)u * (kH / 2) + lane] = make_float2(s0 * z.x * (1.f - z.x), s1 * z.y * (1.f - z.y));
@@ -91,6 +102,17 @@ __global__ void k_gather_max_bwd(const float *__restrict__ dA, const int *__rest
 constexpr int AQ = 128;  // queries (or keys) per thread block pass
 constexpr int AK = 64;   // keys (or queries) per shared-memory tile
 constexpr float kScale = 0.25f;   // 1 / sqrt(16)
+
+// a 16-float tile row into registers with four 16-byte shared loads (the rows are broadcast to
+// the whole warp, so one LDS.128 replaces four scalar LDS: the kernels were LDS-issue bound)
+__device__ __forceinline__ void row16(const float *r, float *x) {
+  const float4 *r4 = reinterpret_cast<const float4 *>(r);
+#pragma unroll
+  for (int t = 0; t < 4; t++) {
+    const float4 v = r4[t];
+    x[4 * t] = v.x; x[4 * t + 1] = v.y; x[4 * t + 2] = v.z; x[4 * t + 3] = v.w;
+  }
+}
 
 __device__ __forceinline__ void key_range(int tau, int N, int S, int M, int *lo, int *hi) {
   long long q0 = (long long)tau * S;
@@ -101,7 +123,7 @@ __device__ __forceinline__ void key_range(int tau, int N, int S, int M, int *lo,
 // qkv: N x 192 [Q | K | V], head h uses columns h*16 .. h*16+15 of each block.
 __global__ void __launch_bounds__(AQ) k_attn_fwd(const float *__restrict__ qkv, float *o, float *lse, int N,
                                                  int S, int M) {
-  __shared__ float Ks[AK][kDH + 1], Vs[AK][kDH + 1];
+  __shared__ __align__(16) float Ks[AK][kDH], Vs[AK][kDH];
   const int tau = blockIdx.x, hd = blockIdx.y;
   int lo, hi;
   key_range(tau, N, S, M, &lo, &hi);
@@ -127,9 +149,12 @@ __global__ void __launch_bounds__(AQ) k_attn_fwd(const float *__restrict__ qkv, 
       __syncthreads();
       const int nk = min(AK, hi - kb);
       for (int j = 0; j < nk; j++) {
+        float kr[kDH], vr[kDH];
+        row16(Ks[j], kr);
+        row16(Vs[j], vr);
         float s = 0.f;
 #pragma unroll
-        for (int c = 0; c < kDH; c++) s = fmaf(q[c], Ks[j][c], s);
+        for (int c = 0; c < kDH; c++) s = fmaf(q[c], kr[c], s);
         s *= kScale;
         if (s > mx) {
           float f = expf(mx - s);
@@ -141,7 +166,7 @@ __global__ void __launch_bounds__(AQ) k_attn_fwd(const float *__restrict__ qkv, 
         float p = expf(s - mx);
         l += p;
 #pragma unroll
-        for (int c = 0; c < kDH; c++) acc[c] = fmaf(p, Vs[j][c], acc[c]);
+        for (int c = 0; c < kDH; c++) acc[c] = fmaf(p, vr[c], acc[c]);
       }
     }
     if (valid) {
@@ -167,7 +192,7 @@ __global__ void k_attn_bwd_prep(const float *o, const float *dout, float *Dd, in
 __global__ void __launch_bounds__(AQ) k_attn_bwd_dq(const float *__restrict__ qkv, const float *__restrict__ lse,
                                                     const float *__restrict__ dout, const float *__restrict__ Dd,
                                                     float *dqkv, int N, int S, int M) {
-  __shared__ float Ks[AK][kDH + 1], Vs[AK][kDH + 1];
+  __shared__ __align__(16) float Ks[AK][kDH], Vs[AK][kDH];
   const int tau = blockIdx.x, hd = blockIdx.y;
   int lo, hi;
   key_range(tau, N, S, M, &lo, &hi);
@@ -195,16 +220,19 @@ __global__ void __launch_bounds__(AQ) k_attn_bwd_dq(const float *__restrict__ qk
       __syncthreads();
       const int nk = min(AK, hi - kb);
       for (int j = 0; j < nk; j++) {
+        float kr[kDH], vr[kDH];
+        row16(Ks[j], kr);
+        row16(Vs[j], vr);
         float s = 0.f, dp = 0.f;
 #pragma unroll
         for (int c = 0; c < kDH; c++) {
-          s = fmaf(q[c], Ks[j][c], s);
-          dp = fmaf(dob[c], Vs[j][c], dp);
+          s = fmaf(q[c], kr[c], s);
+          dp = fmaf(dob[c], vr[c], dp);
         }
         float p = expf(s * kScale - L);
         float ds = p * (dp - D) * kScale;
 #pragma unroll
-        for (int c = 0; c < kDH; c++) dq[c] = fmaf(ds, Ks[j][c], dq[c]);
+        for (int c = 0; c < kDH; c++) dq[c] = fmaf(ds, kr[c], dq[c]);
       }
     }
     if (valid) {
@@ -214,22 +242,25 @@ __global__ void __launch_bounds__(AQ) k_attn_bwd_dq(const float *__restrict__ qk
   }
 }
 
-__device__ __forceinline__ void dkv_accum(int ni, const float (*Qs)[kDH + 1], const float (*dOs)[kDH + 1],
+__device__ __forceinline__ void dkv_accum(int ni, const float (*Qs)[kDH], const float (*dOs)[kDH],
                                           const float *Ls, const float *Ds, const float *k, const float *v,
                                           float *DK, float *DV) {
   for (int r = 0; r < ni; r++) {
+    float qr[kDH], gr[kDH];
+    row16(Qs[r], qr);
+    row16(dOs[r], gr);
     float s = 0.f, dp = 0.f;
 #pragma unroll
     for (int c = 0; c < kDH; c++) {
-      s = fmaf(Qs[r][c], k[c], s);
-      dp = fmaf(dOs[r][c], v[c], dp);
+      s = fmaf(qr[c], k[c], s);
+      dp = fmaf(gr[c], v[c], dp);
     }
     float p = expf(s * kScale - Ls[r]);
     float ds = p * (dp - Ds[r]) * kScale;
 #pragma unroll
     for (int c = 0; c < kDH; c++) {
-      DV[c] = fmaf(p, dOs[r][c], DV[c]);
-      DK[c] = fmaf(ds, Qs[r][c], DK[c]);
+      DV[c] = fmaf(p, gr[c], DV[c]);
+      DK[c] = fmaf(ds, qr[c], DK[c]);
     }
   }
 }
@@ -240,7 +271,8 @@ __device__ __forceinline__ void dkv_accum(int ni, const float (*Qs)[kDH + 1], co
 __global__ void __launch_bounds__(AQ) k_attn_bwd_dkv(const float *__restrict__ qkv, const float *__restrict__ lse,
                                                      const float *__restrict__ dout, const float *__restrict__ Dd,
                                                      float *dqkv, float *dkvm, int N, int S, int M, int nseg) {
-  __shared__ float Qs[AK][kDH + 1], dOs[AK][kDH + 1], Ls[AK], Ds[AK];
+  __shared__ __align__(16) float Qs[AK][kDH], dOs[AK][kDH];
+  __shared__ float Ls[AK], Ds[AK];
   const int sig = blockIdx.x, hd = blockIdx.y;
   const int j0 = sig * S, j1 = min(N, j0 + S);
   int tau_hi = nseg - 1;

@@ -63,7 +63,9 @@ __global__ void __launch_bounds__(TT, 2) k_gemm_tc(GemmArgs a, int Kp, int Np, i
   }
   // W -> bf16 canonical [n][k]: element (n, k) = W[k * ldw_k + n * ldw_n]; consecutive threads
   // walk the contiguous dimension of W
+  // (unrolled: the loads of several elements are in flight at once; W is L2-resident)
   if (a.ldw_n == 1) {
+#pragma unroll 8
     for (int e = tid; e < (Kp / 2) * Np; e += TT) {
       const int kk = e / Np, n = e % Np, k = 2 * kk;
       float w0 = 0.f, w1 = 0.f;
@@ -74,6 +76,7 @@ __global__ void __launch_bounds__(TT, 2) k_gemm_tc(GemmArgs a, int Kp, int Np, i
       *reinterpret_cast<__nv_bfloat162 *>(sB + canon_off(n, k, Kp)) = __floats2bfloat162_rn(w0, w1);
     }
   } else {
+#pragma unroll 8
     for (int e = tid; e < Np * (Kp / 2); e += TT) {
       const int n = e / (Kp / 2), k = (e % (Kp / 2)) * 2;
       float w0 = 0.f, w1 = 0.f;
