@@ -487,6 +487,13 @@ gdp_status gdp_graph_create(int32_t N, int32_t F, const float *feat, int64_t E, 
   UP(X, feat, (size_t)N * F * sizeof(float));
   UP(nbr_ptr, nptr.data(), (N + 1) * sizeof(int));
   UP(nbr_idx, nidx.data(), nidx.size() * sizeof(int));
+  {
+    std::vector<int> heavy;
+    for (int v = 0; v < N; v++)
+      if (nptr[v + 1] - nptr[v] > kHeavyDeg) heavy.push_back(v);
+    g->n_heavy = (int)heavy.size();
+    UP(heavy, heavy.data(), heavy.size() * sizeof(int));
+  }
   UP(out_ptr, optr.data(), (N + 1) * sizeof(int));
   UP(out_idx, oidx.data(), oidx.size() * sizeof(int));
   UP(out_src, osrc.data(), osrc.size() * sizeof(int));
@@ -511,7 +518,7 @@ gdp_status gdp_graph_create(int32_t N, int32_t F, const float *feat, int64_t E, 
 
 gdp_status gdp_graph_destroy(gdp_graph g) {
   if (!g) return GDP_OK;
-  void *ptrs[] = {g->X, g->nbr_ptr, g->nbr_idx, g->out_ptr, g->out_idx, g->out_src, g->in_ptr, g->in_idx,
+  void *ptrs[] = {g->X, g->nbr_ptr, g->nbr_idx, g->heavy, g->out_ptr, g->out_idx, g->out_src, g->in_ptr, g->in_idx,
                   g->cost, g->out_bytes, g->mem_bytes, g->perm, g->leader, g->nrec, g->erec, g->irec,
                   g->cnt0, g->bigid, g->big_in, g->big_out};
   for (void *p : ptrs)

@@ -45,6 +45,8 @@ struct gdp_graph_s {
   // device arrays (caller node ids)
   float *X = nullptr;                               // N x F
   int *nbr_ptr = nullptr, *nbr_idx = nullptr;       // symmetric neighbour CSR (N+1, E_sym)
+  int *heavy = nullptr;                             // nodes with more than kHeavyDeg neighbours, ascending
+  int n_heavy = 0;
   int *out_ptr = nullptr, *out_idx = nullptr, *out_src = nullptr;  // out CSR, consumers ascending
   int *in_ptr = nullptr, *in_idx = nullptr;         // in CSR, producers ascending
   int *cost = nullptr;                              // int32 compute cost
@@ -174,11 +176,13 @@ void launch_layernorm_bwd(const float *x, const float *mu, const float *rs, cons
                           int N, cudaStream_t s);
 void launch_colsum(const float *x, int N, int C, float scale, float *out, float *part, cudaStream_t s);
 
-// nnz = ptr[N] (symmetric neighbour entries), used only for the algorithmic byte count
-void launch_gather_max(const float *Z, const int *ptr, const int *idx, float *A, int *ARG, int N, long long nnz,
-                       cudaStream_t s);
+// nnz = ptr[N] (symmetric neighbour entries), used only for the algorithmic byte count;
+// heavy (n_heavy) = the nodes with more than kHeavyDeg neighbours, one CTA each
+constexpr int kHeavyDeg = 64;
+void launch_gather_max(const float *Z, const int *ptr, const int *idx, const int *heavy, int n_heavy, float *A,
+                       int *ARG, int N, long long nnz, cudaStream_t s);
 void launch_gather_max_bwd(const float *dA, const int *ARG, const float *Z, const int *ptr, const int *idx,
-                           float *dPre, int N, long long nnz, cudaStream_t s);
+                           const int *heavy, int n_heavy, float *dPre, int N, long long nnz, cudaStream_t s);
 
 void launch_attn_fwd(const float *qkv, float *o, float *lse, int N, int S, int M, cudaStream_t s);
 void launch_relu_v(const float *qkv, float *o, int N, cudaStream_t s);

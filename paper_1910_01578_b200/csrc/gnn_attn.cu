@@ -17,83 +17,132 @@
 namespace gdp {
 namespace {
 
-// neighbour ids are fetched 32 at a time (one coalesced load, shuffled out) and the rows of up
-// to G neighbours are requested before any is compared, so the dependent-load chain of a node
-// of degree deg is about deg / 16 row latencies (the heavy-tailed nodes of the GNMT graphs, deg
-// up to 361, set the kernel's duration); comparisons stay in ascending-id order
-template <int G>
-__device__ __forceinline__ void gmax_batch(const float2 *Z2, int mine, int k0, int n, int lane, float2 &m, int &a0,
-                                           int &a1) {
-  int u[G];
-  float2 z[G];
-#pragma unroll
-  for (int t = 0; t < G; t++) {
-    u[t] = __shfl_sync(0xffffffffu, mine, (k0 + t) & 31);
-    if (k0 + t < n) z[t] = __ldg(Z2 + (size_t)u[t] * (kH / 2) + lane);
-  }
-#pragma unroll
-  for (int t = 0; t < G; t++) {
-    if (k0 + t >= n) break;
-    if (a0 < 0 || z[t].x > m.x) { m.x = z[t].x; a0 = u[t]; }   // strict '>': first maximiser wins
-    if (a1 < 0 || z[t].y > m.y) { m.y = z[t].y; a1 = u[t]; }
-  }
-}
+// Neighbour ids are fetched 32 at a time (one coalesced load, shuffled out) and the rows of GU
+// neighbours are requested before any is compared (comparisons stay in ascending-id order).
+// Nodes with more than kHeavyDeg neighbours (the heavy tail of the GNMT graphs: attention
+// memories read by every decoder step, degree up to 361) would set the kernel's duration with
+// one warp each; they get one CTA each instead (blocks after the warp-per-node range): its 8
+// warps scan 8 contiguous, ascending ranges of the neighbour list and the partial results are
+// combined in range order, so the first maximiser still wins (and backward sums stay in a
+// fixed order).
+constexpr int GU = 4;
+constexpr int GW = 8;   // warps per CTA
 
-__global__ void k_gather_max(const float *__restrict__ Z, const int *__restrict__ ptr,
-                             const int *__restrict__ idx, float *A, int *ARG, int N) {
-  const int v = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  if (v >= N) return;
-  const int b = ptr[v], e = ptr[v + 1];
-  const float2 *Z2 = reinterpret_cast<const float2 *>(Z);   // lane owns channels 2 lane, 2 lane + 1
-  float2 m = make_float2(0.f, 0.f);
-  int a0 = -1, a1 = -1;
+__device__ __forceinline__ void gmax_range(const float2 *Z2, const int *__restrict__ idx, int b, int e, int lane,
+                                           float2 &m, int &a0, int &a1) {
   for (int j0 = b; j0 < e; j0 += 32) {
     const int n = min(32, e - j0);
     const int mine = lane < n ? __ldg(idx + j0 + lane) : 0;
-    int k0 = 0;
-    for (; k0 + 16 <= n; k0 += 16) gmax_batch<16>(Z2, mine, k0, n, lane, m, a0, a1);
-    for (; k0 < n; k0 += 4) gmax_batch<4>(Z2, mine, k0, n, lane, m, a0, a1);
+    for (int k0 = 0; k0 < n; k0 += GU) {
+      int u[GU];
+      float2 z[GU];
+#pragma unroll
+      for (int t = 0; t < GU; t++) {
+        u[t] = __shfl_sync(0xffffffffu, mine, (k0 + t) & 31);
+        if (k0 + t < n) z[t] = __ldg(Z2 + (size_t)u[t] * (kH / 2) + lane);
+      }
+#pragma unroll
+      for (int t = 0; t < GU; t++) {
+        if (k0 + t >= n) break;
+        if (a0 < 0 || z[t].x > m.x) { m.x = z[t].x; a0 = u[t]; }   // strict '>': first maximiser wins
+        if (a1 < 0 || z[t].y > m.y) { m.y = z[t].y; a1 = u[t]; }
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(32 * GW) k_gather_max(const float *__restrict__ Z, const int *__restrict__ ptr,
+                                                        const int *__restrict__ idx, const int *__restrict__ heavy,
+                                                        int nb_main, float *A, int *ARG, int N) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const float2 *Z2 = reinterpret_cast<const float2 *>(Z);   // lane owns channels 2 lane, 2 lane + 1
+  float2 m = make_float2(0.f, 0.f);
+  int a0 = -1, a1 = -1;
+  if ((int)blockIdx.x < nb_main) {   // warp per node
+    const int v = blockIdx.x * GW + warp;
+    if (v >= N) return;
+    const int b = ptr[v], e = ptr[v + 1];
+    if (e - b > kHeavyDeg) return;
+    gmax_range(Z2, idx, b, e, lane, m, a0, a1);
+    reinterpret_cast<float2 *>(A)[(size_t)v * (kH / 2) + lane] = m;
+    reinterpret_cast<int2 *>(ARG)[(size_t)v * (kH / 2) + lane] = make_int2(a0, a1);
+    return;
+  }
+  __shared__ float2 sm[GW][32];
+  __shared__ int2 sa[GW][32];
+  const int v = heavy[blockIdx.x - nb_main];
+  const int b = ptr[v], e = ptr[v + 1], len = (e - b + GW - 1) / GW;
+  const int rb = b + warp * len, re = min(e, rb + len);
+  if (rb < re) gmax_range(Z2, idx, rb, re, lane, m, a0, a1);
+  sm[warp][lane] = m;
+  sa[warp][lane] = make_int2(a0, a1);
+  __syncthreads();
+  if (warp != 0) return;
+  for (int w = 1; w < GW; w++) {   // ascending ranges: a later range wins only if strictly greater
+    const float2 mw = sm[w][lane];
+    const int2 aw = sa[w][lane];
+    if (aw.x >= 0 && (a0 < 0 || mw.x > m.x)) { m.x = mw.x; a0 = aw.x; }
+    if (aw.y >= 0 && (a1 < 0 || mw.y > m.y)) { m.y = mw.y; a1 = aw.y; }
   }
   reinterpret_cast<float2 *>(A)[(size_t)v * (kH / 2) + lane] = m;
   reinterpret_cast<int2 *>(ARG)[(size_t)v * (kH / 2) + lane] = make_int2(a0, a1);
 }
 
-template <int G>
-__device__ __forceinline__ void gmax_bwd_batch(const float2 *dA2, const int2 *ARG2, int mine, int k0, int n, int lane,
-                                               int u, float &s0, float &s1) {
-  int2 ag[G];
-  float2 g[G];
-#pragma unroll
-  for (int t = 0; t < G; t++) {
-    const int v = __shfl_sync(0xffffffffu, mine, (k0 + t) & 31);
-    if (k0 + t < n) {
-      ag[t] = __ldg(ARG2 + (size_t)v * (kH / 2) + lane);
-      g[t] = __ldg(dA2 + (size_t)v * (kH / 2) + lane);
-    }
-  }
-#pragma unroll
-  for (int t = 0; t < G; t++) {   // ascending neighbour order, as the oracle sums
-    if (k0 + t >= n) break;
-    if (ag[t].x == u) s0 += g[t].x;
-    if (ag[t].y == u) s1 += g[t].y;
-  }
-}
-
-__global__ void k_gather_max_bwd(const float *__restrict__ dA, const int *__restrict__ ARG,
-                                 const float *__restrict__ Z, const int *__restrict__ ptr,
-                                 const int *__restrict__ idx, float *dPre, int N) {
-  const int u = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  if (u >= N) return;
-  const int b = ptr[u], e = ptr[u + 1];
-  const float2 *dA2 = reinterpret_cast<const float2 *>(dA);
-  const int2 *ARG2 = reinterpret_cast<const int2 *>(ARG);
-  float s0 = 0.f, s1 = 0.f;
+__device__ __forceinline__ void gmax_bwd_range(const float2 *dA2, const int2 *ARG2, const int *__restrict__ idx, int b,
+                                               int e, int lane, int u, float &s0, float &s1) {
   for (int j0 = b; j0 < e; j0 += 32) {
     const int n = min(32, e - j0);
     const int mine = lane < n ? __ldg(idx + j0 + lane) : 0;
-    int k0 = 0;
-    for (; k0 + 16 <= n; k0 += 16) gmax_bwd_batch<16>(dA2, ARG2, mine, k0, n, lane, u, s0, s1);
-    for (; k0 < n; k0 += 4) gmax_bwd_batch<4>(dA2, ARG2, mine, k0, n, lane, u, s0, s1);
+    for (int k0 = 0; k0 < n; k0 += GU) {
+      int2 ag[GU];
+      float2 g[GU];
+#pragma unroll
+      for (int t = 0; t < GU; t++) {
+        const int v = __shfl_sync(0xffffffffu, mine, (k0 + t) & 31);
+        if (k0 + t < n) {
+          ag[t] = __ldg(ARG2 + (size_t)v * (kH / 2) + lane);
+          g[t] = __ldg(dA2 + (size_t)v * (kH / 2) + lane);
+        }
+      }
+#pragma unroll
+      for (int t = 0; t < GU; t++) {   // ascending neighbour order, as the oracle sums
+        if (k0 + t >= n) break;
+        if (ag[t].x == u) s0 += g[t].x;
+        if (ag[t].y == u) s1 += g[t].y;
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(32 * GW) k_gather_max_bwd(const float *__restrict__ dA, const int *__restrict__ ARG,
+                                                            const float *__restrict__ Z, const int *__restrict__ ptr,
+                                                            const int *__restrict__ idx, const int *__restrict__ heavy,
+                                                            int nb_main, float *dPre, int N) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const float2 *dA2 = reinterpret_cast<const float2 *>(dA);
+  const int2 *ARG2 = reinterpret_cast<const int2 *>(ARG);
+  float s0 = 0.f, s1 = 0.f;
+  int u;
+  if ((int)blockIdx.x < nb_main) {
+    u = blockIdx.x * GW + warp;
+    if (u >= N) return;
+    const int b = ptr[u], e = ptr[u + 1];
+    if (e - b > kHeavyDeg) return;
+    gmax_bwd_range(dA2, ARG2, idx, b, e, lane, u, s0, s1);
+  } else {
+    __shared__ float2 ss[GW][32];
+    u = heavy[blockIdx.x - nb_main];
+    const int b = ptr[u], e = ptr[u + 1], len = (e - b + GW - 1) / GW;
+    const int rb = b + warp * len, re = min(e, rb + len);
+    if (rb < re) gmax_bwd_range(dA2, ARG2, idx, rb, re, lane, u, s0, s1);
+    ss[warp][lane] = make_float2(s0, s1);
+    __syncthreads();
+    if (warp != 0) return;
+    s0 = 0.f; s1 = 0.f;
+    for (int w = 0; w < GW; w++) {   // fixed (range) order
+      s0 += ss[w][lane].x;
+      s1 += ss[w][lane].y;
+    }
   }
   const float2 z = reinterpret_cast<const float2 *>(Z)[(size_t)u * (kH / 2) + lane];
   reinterpret_cast<float2 *>(dPre)[(size_t)u * (kH / 2) + lane] = make_float2(s0 * z.x * (1.f - z.x), s1 * z.y * (1.f - z.y));
@@ -327,19 +376,21 @@ __global__ void __launch_bounds__(AQ) k_attn_bwd_dkv(const float *__restrict__ q
 }  // namespace
 
 // algorithmic (unique) bytes: CSR (N + 1 + nnz) x 4, Z read once N x 64 x 4, A and ARG written
-void launch_gather_max(const float *Z, const int *ptr, const int *idx, float *A, int *ARG, int N, long long nnz,
-                       cudaStream_t s) {
-  unsigned blocks = (unsigned)(((size_t)N * 32 + 255) / 256);
+void launch_gather_max(const float *Z, const int *ptr, const int *idx, const int *heavy, int n_heavy, float *A,
+                       int *ARG, int N, long long nnz, cudaStream_t s) {
+  const int nb_main = (N + GW - 1) / GW;
+  const unsigned blocks = (unsigned)(nb_main + n_heavy);
   note_launch("k_gather_max", s, 4.0 * ((double)N + 1 + (double)nnz) + 3.0 * 4 * 64 * (double)N);
-  k_gather_max<<<blocks, 256, 0, s>>>(Z, ptr, idx, A, ARG, N);
+  k_gather_max<<<blocks, 32 * GW, 0, s>>>(Z, ptr, idx, heavy, nb_main, A, ARG, N);
 }
 
 void launch_gather_max_bwd(const float *dA, const int *ARG, const float *Z, const int *ptr, const int *idx,
-                           float *dPre, int N, long long nnz, cudaStream_t s) {
-  unsigned blocks = (unsigned)(((size_t)N * 32 + 255) / 256);
+                           const int *heavy, int n_heavy, float *dPre, int N, long long nnz, cudaStream_t s) {
+  const int nb_main = (N + GW - 1) / GW;
+  const unsigned blocks = (unsigned)(nb_main + n_heavy);
   // CSR, dA and ARG of every neighbour read once per node (unique), dPre written
   note_launch("k_gather_max_bwd", s, 4.0 * ((double)N + 1 + (double)nnz) + 3.0 * 4 * 64 * (double)N);
-  k_gather_max_bwd<<<blocks, 256, 0, s>>>(dA, ARG, Z, ptr, idx, dPre, N);
+  k_gather_max_bwd<<<blocks, 32 * GW, 0, s>>>(dA, ARG, Z, ptr, idx, heavy, nb_main, dPre, N);
 }
 
 // no_attention ablation (NEXT-3, reading R34): o = ReLU(V) per node; backward dV = dO [V > 0],

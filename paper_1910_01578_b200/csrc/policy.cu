@@ -310,7 +310,7 @@ gdp_status run_embed(const gdp_graph_s *g, const float *theta, float *node_emb, 
     a.bias = theta + off[pW + 1];
     a.epi = EPI_SIGMOID;
     launch_gemm(a, s);
-    launch_gather_max(w.Z[l], g->nbr_ptr, g->nbr_idx, w.A[l], w.ARG[l], N, g->E_sym, s);
+    launch_gather_max(w.Z[l], g->nbr_ptr, g->nbr_idx, g->heavy, g->n_heavy, w.A[l], w.ARG[l], N, g->E_sym, s);
     // H' = tanh([H | A] W_f + b_f) (Eq. 3)
     float *out = (l == kGNN - 1) ? w.H[3] : w.H[l + 1];
     a = gemm(N, 2 * kH, kH, w.H[l], kH, theta + off[pW + 2], kH, 1, out, kH);
@@ -433,7 +433,7 @@ gdp_status run_policy_grad(const gdp_graph_s *g, const gdp_config *c, const floa
     a = gemm(N, kH, 2 * kH, w.dP, kH, theta + off[pW + 2], 1, kH, dH, kH);   // [dH | dA] = dP Wf^T
     a.split = kH; a.Y2 = w.dAg; a.ldy2 = kH;
     launch_gemm(a, s);
-    launch_gather_max_bwd(w.dAg, w.ARG[l], w.Z[l], g->nbr_ptr, g->nbr_idx, w.dP, N, g->E_sym, s);   // dP := dpre
+    launch_gather_max_bwd(w.dAg, w.ARG[l], w.Z[l], g->nbr_ptr, g->nbr_idx, g->heavy, g->n_heavy, w.dP, N, g->E_sym, s);   // dP := dpre
     launch_wgrad(N, kH, kH, w.H[l], kH, kH, nullptr, 0, w.dP, kH, true, w.part, w.part_floats, grad + off[pW],
                  true, s);
     a = gemm(N, kH, kH, w.dP, kH, theta + off[pW], 1, kH, dH, kH);             // dH += dpre W^T

@@ -172,7 +172,18 @@ CASES = {
     "no_attention_no_sup": (lambda: _perm_coloc_graph(), 3, 16, 16, False, True),
     # NEXT-4: head padded to 8 outputs, 3 devices active (-inf masking)
     "masked_head": (lambda: _perm_coloc_graph(), 8, 32, 32, True, False, 3),
+    # two hubs above kHeavyDeg = 64 neighbours (one CTA per heavy node in the gathers)
+    "heavy_hubs": (lambda: _hub_graph(), 4, 64, 64, True),
 }
+
+
+def _hub_graph():
+    g = workloads.random_dag(300, p_edge=0.05, max_back=20, seed=8)
+    extra = [(0, v) for v in range(1, 151)] + [(u, 299) for u in range(140, 299)]
+    have = set(map(tuple, g.edges.tolist()))
+    e = np.array(g.edges.tolist() + [x for x in extra if x not in have], dtype=np.int32)
+    return workloads.Graph(name="hubs", N=g.N, edges=e, op_type=g.op_type, compute_cost=g.compute_cost,
+                           output_bytes=g.output_bytes, memory_bytes=g.memory_bytes)
 
 
 def _perm_coloc_graph():
