@@ -421,7 +421,11 @@ gdp_status gdp_graph_create(int32_t N, int32_t F, const float *feat, int64_t E, 
   std::vector<int> cost(N);
   long long sum_cost = 0, sum_edge_out = 0;
   for (int v = 0; v < N; v++) { cost[v] = (int)compute_cost[v]; sum_cost += compute_cost[v]; }
-  for (auto &p : es) sum_edge_out += output_bytes[p.first];
+  g->min_edge_bytes = LLONG_MAX;
+  for (auto &p : es) {
+    sum_edge_out += output_bytes[p.first];
+    g->min_edge_bytes = std::min<long long>(g->min_edge_bytes, output_bytes[p.first]);
+  }
   g->sum_cost = sum_cost;
   g->sum_edge_out_bytes = sum_edge_out;
   bool ident = true;

@@ -60,6 +60,7 @@ struct gdp_graph_s {
   long long n_edges_cross_max = 0;
   int max_indeg = 0, max_outdeg = 0;
   int min_cost = 0;   // smallest compute cost (k_cost4 needs every duration >= 1)
+  long long min_edge_bytes = 0;   // smallest producer output over edges (k_cost4 window); LLONG_MAX: no edges
   // shared-memory cost model records (cost2.cuh)
   void *nrec = nullptr, *erec = nullptr, *irec = nullptr;
   unsigned *cnt0 = nullptr;

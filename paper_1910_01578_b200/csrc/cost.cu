@@ -415,7 +415,7 @@ static TopoArgs topo_args(const gdp_topo_s *t) {
 int cost_kernel_choice(const gdp_graph_s *g, const gdp_topo_s *t) {
   if (getenv("GDP_COST_V1") != nullptr) return 1;
   const TopoArgs T = topo_args(t);
-  if (cost4_window(T, g->min_cost, g->N) > 0) return 4;
+  if (cost4_window(T, g->min_cost, g->N, g->min_edge_bytes) > 0) return 4;
   if (cost2_smem_bytes(g->N) <= 227 * 1024) return getenv("GDP_COST_V2") != nullptr ? 2 : 3;
   return 1;
 }
@@ -432,7 +432,7 @@ gdp_status launch_cost(const gdp_graph_s *g, const gdp_topo_s *t, const uint8_t 
     C.cnt0 = g->cnt0; C.bigid = g->bigid; C.big_in = g->big_in; C.big_out = g->big_out; C.nbig = g->nbig;
     C.out_idx = g->out_idx; C.out_src = g->out_src; C.in_ptr = g->in_ptr; C.cost = g->cost; C.leader = g->leader;
     C.out_bytes = g->out_bytes; C.mem_bytes = g->mem_bytes; C.has_coloc = g->has_coloc ? 1 : 0;
-    if (launch_cost4(C, T, g->min_cost, D, B, w.c_scratch, w.c_per_place, rep, peak, busy, reward, s)) {
+    if (launch_cost4(C, T, g->min_cost, g->min_edge_bytes, D, B, w.c_scratch, w.c_per_place, rep, peak, busy, reward, s)) {
       GDP_LAUNCH_CHECK("k_cost4");
       return GDP_OK;
     }

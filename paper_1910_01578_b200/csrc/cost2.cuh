@@ -32,9 +32,9 @@ struct Cost2Graph {
 size_t cost2_smem_bytes(int N);
 size_t cost2_scratch_per_placement(int N, long long E, int nbig);
 size_t cost4_smem_bytes(int N);
-int cost4_window(const TopoArgs &T, int min_cost, int N);   // window length, 0 = not eligible
+int cost4_window(const TopoArgs &T, int min_cost, int N, long long min_edge_bytes);   // window length, 0 = not eligible
 size_t cost4_scratch_per_placement(int N, long long E, int nbig);
-bool launch_cost4(const Cost2Graph &G, const TopoArgs &T, int min_cost, const uint8_t *D, int B,
+bool launch_cost4(const Cost2Graph &G, const TopoArgs &T, int min_cost, long long min_edge_bytes, const uint8_t *D, int B,
                   unsigned char *scratch, size_t per_place, gdp_sim_report *rep, long long *peak, long long *busy,
                   double *reward, cudaStream_t s);
 bool launch_cost2(const Cost2Graph &G, const TopoArgs &T, const uint8_t *D, int B, unsigned char *scratch,

@@ -30,7 +30,13 @@ using namespace cu;
 #ifndef COST4_SLEEP_NS
 #define COST4_SLEEP_NS 200   // memory warp back-off when no window is pending
 #endif
-constexpr int WMAX = 8;    // window length cap (ticks) = buckets per window
+#ifndef COST4_WMAX
+#define COST4_WMAX 8
+#endif
+#ifndef COST4_DYN
+#define COST4_DYN 0   // window end from the devices' running finishes (else T + Wl)
+#endif
+constexpr int WMAX = COST4_WMAX;   // window length cap (ticks) = buckets per window
 #ifndef COST4_R4
 #define COST4_R4 8
 #endif
@@ -55,11 +61,12 @@ struct Smem4 {
   int cfree[64], ctail[64], cstamp[64];                        // producer side (warp k)
   int pfirst[2][64], ptail[2][64];   // published per window parity: first push's arrival, tail
   int tn[3];                       // next window start, atomic min over devices' next events and first pushes
+  int hf[3], hidle[3];             // next window's horizon: min running finish, any device idle
   int phs[2][64];                  // consumer head at the start of window w (parity w & 1)
   int coff[64], ccnt[64];
   int doff[8], ftail0[8], opcnt[8];
   long long stat[8], busyv[8];
-  int Tw[R4], dq_end[R4];
+  int Tw[R4], Tl[R4], dq_end[R4];
   int dq_tail, flag, oom, mk, disp, nwin;
   int win_done, mem_done, dev_done;
   unsigned long long cross;
@@ -145,7 +152,15 @@ __device__ __forceinline__ void put_inc(Smem4 &S, NRec *ovq, int q, int pos, con
   else copy_rec(ovq + pos, &r);
 }
 
-__global__ void __launch_bounds__(288, 2) k_cost4(Cost2Graph G, TopoArgs T, const uint8_t *__restrict__ Dall,
+#ifndef COST4_MAXNREG
+#define COST4_MAXNREG 0
+#endif
+#if COST4_MAXNREG
+#define COST4_BOUNDS __maxnreg__(COST4_MAXNREG)
+#else
+#define COST4_BOUNDS __launch_bounds__(288, 2)
+#endif
+__global__ void COST4_BOUNDS k_cost4(Cost2Graph G, TopoArgs T, const uint8_t *__restrict__ Dall,
                                                   unsigned char *scratch, size_t per_place, gdp_sim_report *rep,
                                                   long long *peak_out, long long *busy_out, double *reward, int Wl,
                                                   int dbg) {
@@ -178,6 +193,8 @@ __global__ void __launch_bounds__(288, 2) k_cost4(Cost2Graph G, TopoArgs T, cons
     S.flag = 0; S.oom = 0; S.cross = 0; S.dq_tail = 0; S.mk = 0; S.disp = 0; S.nwin = 0;
     S.win_done = -1; S.mem_done = -1; S.dev_done = 0;
     S.tn[0] = INF; S.tn[1] = INF; S.tn[2] = INF;
+    S.hf[0] = INF; S.hf[1] = INF; S.hf[2] = INF;
+    S.hidle[0] = 0; S.hidle[1] = 0; S.hidle[2] = 0;
   }
   if (tid < 16) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&S.smb[tid >> 1][tid & 1])) : "memory");
@@ -319,7 +336,8 @@ __global__ void __launch_bounds__(288, 2) k_cost4(Cost2Graph G, TopoArgs T, cons
     int fhead = 0, ftail = S.ftail0[q], running = 0, fin = 0, mk = 0, disp = 0;
     int cur = 0, nxt_id = -1;
     unsigned nst0 = 0, nst1 = 0;                 // bulk stagings issued per slot (mbarrier phases)
-    int li = 0, T0 = 0, w = 0, memd = -1;
+    // window 0: every device idle at t = 0, so nothing it sends lands before 1 + Wl
+    int li = 0, T0 = 0, Tend = COST4_DYN ? min(1 + Wl, WMAX) : Wl, w = 0, memd = -1;
     for (;; w++) {
       const int set = w % R4;
       if (w - R4 > memd) {   // the memory warp must have released this window set
@@ -329,10 +347,12 @@ __global__ void __launch_bounds__(288, 2) k_cost4(Cost2Graph G, TopoArgs T, cons
       }
       if (q == 0 && lane == 0) {
         S.Tw[set] = T0;
+        S.Tl[set] = Tend - T0;
         S.tn[(w + 1) % 3] = INF;   // read last after barrier w - 2, written from window w + 1 on
+        S.hf[(w + 1) % 3] = INF;
+        S.hidle[(w + 1) % 3] = 0;
       }
       if (lane < d) S.pfirst[w & 1][8 * q + lane] = INF;
-      const int Tend = T0 + Wl;
       for (;;) {
         // key 2 tau (+1 unless my op finishes at tau); an idle device with a non-empty FIFO
         // dispatches at once (only the sources at t = 0)
@@ -522,6 +542,10 @@ __global__ void __launch_bounds__(288, 2) k_cost4(Cost2Graph G, TopoArgs T, cons
       // publish the end-of-window state, meet, and find the next window start
       if (own) S.phs[(w + 1) & 1][cin] = head;
       if (lane < d) S.ptail[w & 1][8 * q + lane] = S.ctail[8 * q + lane];
+      if (COST4_DYN && devl) {   // my earliest possible send from the next window on: my running op's finish, else T + 1
+        if (running) atomicMin(&S.hf[w % 3], fin);
+        else S.hidle[w % 3] = 1;
+      }
       bar_devices(32 * d);   // bar.sync orders the window's shared and global writes for all device warps
       if (q == 0 && lane == 31) {   // a lane that rarely has global writes in flight (release fence)
         S.dq_end[set] = S.dq_tail;
@@ -542,6 +566,13 @@ __global__ void __launch_bounds__(288, 2) k_cost4(Cost2Graph G, TopoArgs T, cons
         hs = head;
       }
       if (Tn == INF) break;
+      // lookahead: a transfer takes >= Wl ticks, so nothing sent in [Tn, Tend) lands before Tend
+      {
+        const int hf = S.hf[w % 3];
+        int H = hf == INF ? INF : hf + Wl;
+        if (S.hidle[w % 3]) H = min(H, Tn + 1 + Wl);
+        Tend = COST4_DYN ? min(Tn + WMAX, H) : Tn + Wl;
+      }
       T0 = Tn;
     }
     cp_wait0();
@@ -575,7 +606,7 @@ __global__ void __launch_bounds__(288, 2) k_cost4(Cost2Graph G, TopoArgs T, cons
           const int tk = __ldcg(dtick + u);
           const int du = dev_of(Dn, u);
           int ww = done_w + 1;
-          while (ww < wd && tk >= S.Tw[ww % R4] + Wl) ww++;
+          while (ww < wd && tk >= S.Tw[ww % R4] + S.Tl[ww % R4]) ww++;
           atomicAdd(reinterpret_cast<unsigned long long *>(&S.db[ww % R4][du][tk - S.Tw[ww % R4]]),
                     (unsigned long long)(-bytes));
         }
@@ -584,7 +615,8 @@ __global__ void __launch_bounds__(288, 2) k_cost4(Cost2Graph G, TopoArgs T, cons
         for (int ww = done_w + 1; ww <= wd; ww++) {   // tick-ordered sweep of each window
           const int s = ww % R4;
           if (lane < d) {
-            for (int o = 0; o < Wl; o++) {
+            const int len = S.Tl[s];
+            for (int o = 0; o < len; o++) {
               unsigned *wv = &S.lb[s][lane][o][0];
               mem += read3(wv) + S.db[s][lane][o];
               pk = max(pk, mem);
@@ -627,7 +659,12 @@ __global__ void __launch_bounds__(288, 2) k_cost4(Cost2Graph G, TopoArgs T, cons
 size_t cost4_smem_bytes(int N) { return sizeof(Smem4) + 4 * (size_t)((N + 3) / 4) + 4 * (size_t)((N + 7) / 8); }
 size_t cost4_scratch_per_placement(int N, long long E, int nbig) { return scratch4_layout(N, E, nbig).total; }
 
-int cost4_window(const TopoArgs &T, int min_cost, int N) {
+// Wl = the shortest possible transfer: min over device pairs of latency + ceil(smallest edge's
+// bytes / bandwidth), capped at WMAX
+#ifndef COST4_XMIN
+#define COST4_XMIN 1
+#endif
+int cost4_window(const TopoArgs &T, int min_cost, int N, long long min_edge_bytes) {
   static const bool off = getenv("GDP_COST_V3") != nullptr || getenv("GDP_COST_V2") != nullptr;
   if (off) return 0;
   const int d = T.d;
@@ -636,17 +673,21 @@ int cost4_window(const TopoArgs &T, int min_cost, int N) {
   for (int k = 0; k < d; k++) {
     if (T.speed[k] < 1) return 0;
     for (int q = 0; q < d; q++)
-      if (k != q) L = L < T.lat[k * 8 + q] ? L : T.lat[k * 8 + q];
+      if (k != q) {
+        long long x = T.lat[k * 8 + q];
+        if (COST4_XMIN && min_edge_bytes > 0 && T.bpt[k * 8 + q] > 0) x += (min_edge_bytes - 1) / T.bpt[k * 8 + q] + 1;
+        L = L < x ? L : (int)x;
+      }
   }
   if (L < 1) return 0;                           // a transfer could land in its own window
   if (cost4_smem_bytes(N) > 227 * 1024) return 0;
   return L;
 }
 
-bool launch_cost4(const Cost2Graph &G, const TopoArgs &T, int min_cost, const uint8_t *D, int B,
+bool launch_cost4(const Cost2Graph &G, const TopoArgs &T, int min_cost, long long min_edge_bytes, const uint8_t *D, int B,
                   unsigned char *scratch, size_t per_place, gdp_sim_report *rep, long long *peak, long long *busy,
                   double *reward, cudaStream_t s) {
-  const int L = cost4_window(T, min_cost, G.N);
+  const int L = cost4_window(T, min_cost, G.N, min_edge_bytes);
   if (L < 1) return false;
   if (per_place < cost4_scratch_per_placement(G.N, G.E, G.nbig)) return false;
   const int d = T.d;

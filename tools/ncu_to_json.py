@@ -27,5 +27,15 @@ res["dram_bytes_read_per_launch"] = to_bytes("dram__bytes_read.sum")
 res["dram_bytes_write_per_launch"] = to_bytes("dram__bytes_write.sum")
 dur_unit = units.get("gpu__time_duration.sum", "msecond")
 res["ncu_duration_ms"] = f("gpu__time_duration.sum") * {"msecond": 1, "usecond": 1e-3, "nsecond": 1e-6, "second": 1e3}.get(dur_unit, 1)
+# warp-state breakdown: cycles a warp spends per issued instruction, by stall reason
+st = {}
+for k in h:
+    if k.startswith("smsp__average_warps_issue_stalled_") and k.endswith("_per_issue_active.ratio"):
+        x = f(k)
+        if x >= 0.05:
+            st[k[len("smsp__average_warps_issue_stalled_"):-len("_per_issue_active.ratio")]] = round(x, 3)
+if st:
+    res["stall_cycles_per_issued_inst"] = dict(sorted(st.items(), key=lambda kv: -kv[1]))
+    res["warp_latency_per_inst"] = round(f("smsp__average_warp_latency_per_inst_issued.ratio"), 3)
 json.dump(res, open(out, "w"), indent=2)
 print(json.dumps(res, indent=2))

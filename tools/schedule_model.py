@@ -30,13 +30,13 @@ for a_, w_ in zip(arr.tolist(), w[cross].tolist()):
     ev[int(a_)][(int(dev[w_]), "a")] += 1
 T = sorted(ev)
 print("N", g.N, "makespan", int(r["makespan"][0]), "distinct event ticks", len(T))
-Lat = 5
+Lat = int(os.environ.get("LAT", "5"))
 i = nw = 0
 while i < len(T):
     t0 = T[i]; nw += 1
     while i < len(T) and T[i] < t0 + Lat:
         i += 1
-print("static windows (L = 5):", nw)
+print("static windows (L = %d):" % Lat, nw)
 per = collections.defaultdict(set)
 for t_, cn in ev.items():
     for (dv, kd), c in cn.items():
