@@ -1,10 +1,12 @@
+// EXPERIMENT (not built): the memory warp takes over a finish's in-edges (frees, producer consumer
+// counts, death ticks) from the device warps.  Bit-exact (GPU parity green) but 166.6 vs 99.5 ms
+// at C4 B = 256: the memory warp falls behind and throttles the device warps.
 // Cost model, windowed multi-warp kernel (the default when its preconditions hold; k_cost3 in
 // cost2.cu otherwise).  Same event semantics as the oracle (SPEC.md:275-284 `simulate`, O11 and
 // the readings R19/R20 in DESIGN.md); this formulation runs the devices of one placement in
 // parallel, one warp per device, in windows of simulated time:
 //
-//  * every cross-device transfer takes at least L ticks (L = min over device pairs of latency +
-//    ceil(smallest edge's bytes / bandwidth), >= 1, capped at WMAX), so an op finishing
+//  * every cross-device transfer takes at least L = min latency >= 1 tick, so an op finishing
 //    at tick tau in the window [T, T + W) (W <= L) can only affect another device at tick
 //    >= T + W.  Inside a window the devices are therefore independent: warp q processes the
 //    events of device q in time order (arrivals on its incoming channels, its finish,
@@ -34,11 +36,17 @@ using namespace cu;
 #ifndef COST4_WMAX
 #define COST4_WMAX 8
 #endif
+#ifndef COST4_DYN
+#define COST4_DYN 0   // window end from the devices' running finishes (else T + Wl)
+#endif
 constexpr int WMAX = COST4_WMAX;   // window length cap (ticks) = buckets per window
 #ifndef COST4_R4
 #define COST4_R4 8
 #endif
 constexpr int R4 = COST4_R4;   // windows the memory warp may lag behind
+#ifndef COST4_DEFER
+#define COST4_DEFER 1   // a finish's in-edges (frees, consumer counts of producers) handled by the memory warp
+#endif
 constexpr int SO4 = 8;     // staged out-edge records per slot
 constexpr int SI4 = 8;     // staged in-edge records per slot (2 * SO4 + SI4 = 24 staging lanes)
 constexpr int KF4 = 4;     // FIFO entries kept in smem per device
@@ -47,7 +55,12 @@ constexpr int NINC4 = 8;   // ops made available at one local instant (overflow 
 
 struct Smem4 {
   NRec st_out[8][2][SO4];
+#if COST4_DEFER
+  int4 fl[R4][8][WMAX];            // finish per window set / device: in-CSR range, tick, op if a sink else -1
+  int nfl[R4][8];
+#else
   IRec st_in[8][2][SI4];
+#endif
   Ent fc[8][KF4];
   Ent cc[64][KC4];                 // consumer-side prefetch ring of channel c = 8k + q
   NRec inc[8][NINC4];
@@ -59,11 +72,12 @@ struct Smem4 {
   int cfree[64], ctail[64], cstamp[64];                        // producer side (warp k)
   int pfirst[2][64], ptail[2][64];   // published per window parity: first push's arrival, tail
   int tn[3];                       // next window start, atomic min over devices' next events and first pushes
+  int hf[3], hidle[3];             // next window's horizon: min running finish, any device idle
   int phs[2][64];                  // consumer head at the start of window w (parity w & 1)
   int coff[64], ccnt[64];
   int doff[8], ftail0[8], opcnt[8];
   long long stat[8], busyv[8];
-  int Tw[R4], dq_end[R4];
+  int Tw[R4], Tl[R4], dq_end[R4];
   int dq_tail, flag, oom, mk, disp, nwin;
   int win_done, mem_done, dev_done;
   unsigned long long cross;
@@ -127,7 +141,12 @@ __device__ __forceinline__ void mbar_wait(unsigned long long *mbar, unsigned par
 // the device lane stages the out-/in-edge records of op r into its slot sl: two bulk copies
 // (contiguous record ranges) completing on the slot's mbarrier
 __device__ __forceinline__ void stage_records4(Smem4 &S, const Cost2Graph &G, int q, int sl, const NRec &r) {
-  const unsigned no = (unsigned)min(r.oe - r.ob, SO4), ni = (unsigned)min(r.ie - r.ib, SI4);
+  const unsigned no = (unsigned)min(r.oe - r.ob, SO4);
+#if COST4_DEFER
+  const unsigned ni = 0;
+#else
+  const unsigned ni = (unsigned)min(r.ie - r.ib, SI4);
+#endif
   unsigned long long *mb = &S.smb[q][sl];
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // earlier generic reads of the slot
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(mb)),
@@ -138,20 +157,28 @@ __device__ __forceinline__ void stage_records4(Smem4 &S, const Cost2Graph &G, in
                  ::"r"(smem_u32(&S.st_out[q][sl][0])), "l"(G.erec + r.ob), "r"(no * (unsigned)sizeof(NRec)),
                  "r"(smem_u32(mb))
                  : "memory");
+#if !COST4_DEFER
   if (ni)
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
                  ::"r"(smem_u32(&S.st_in[q][sl][0])), "l"(G.irec + r.ib), "r"(ni * (unsigned)sizeof(IRec)),
                  "r"(smem_u32(mb))
                  : "memory");
+#endif
 }
 __device__ __forceinline__ void put_inc(Smem4 &S, NRec *ovq, int q, int pos, const NRec &r) {
   if (pos < NINC4) copy_rec(&S.inc[q][pos], &r);
   else copy_rec(ovq + pos, &r);
 }
 
-// 2 CTAs per SM cap the registers at 96; more registers (one CTA per SM) run a placement ~8 %
-// faster but need two waves for B = 256 (A/B: 99.5 ms vs 182.5 ms at 112 registers)
-__global__ void __launch_bounds__(288, 2) k_cost4(Cost2Graph G, TopoArgs T, const uint8_t *__restrict__ Dall,
+#ifndef COST4_MAXNREG
+#define COST4_MAXNREG 0
+#endif
+#if COST4_MAXNREG
+#define COST4_BOUNDS __maxnreg__(COST4_MAXNREG)
+#else
+#define COST4_BOUNDS __launch_bounds__(288, 2)
+#endif
+__global__ void COST4_BOUNDS k_cost4(Cost2Graph G, TopoArgs T, const uint8_t *__restrict__ Dall,
                                                   unsigned char *scratch, size_t per_place, gdp_sim_report *rep,
                                                   long long *peak_out, long long *busy_out, double *reward, int Wl,
                                                   int dbg) {
@@ -173,6 +200,7 @@ __global__ void __launch_bounds__(288, 2) k_cost4(Cost2Graph G, TopoArgs T, cons
   int *bigc = reinterpret_cast<int *>(base + L4.bigc);
   int *dtick = reinterpret_cast<int *>(base + L4.dtick);
   int4 *dq = reinterpret_cast<int4 *>(base + L4.dq);
+  (void)dq;
 
   // ------------------------------------------------------------ prologue (whole block)
   for (int i = tid; i < cwords; i += nthr) cnt[i] = G.cnt0[i];
@@ -184,6 +212,8 @@ __global__ void __launch_bounds__(288, 2) k_cost4(Cost2Graph G, TopoArgs T, cons
     S.flag = 0; S.oom = 0; S.cross = 0; S.dq_tail = 0; S.mk = 0; S.disp = 0; S.nwin = 0;
     S.win_done = -1; S.mem_done = -1; S.dev_done = 0;
     S.tn[0] = INF; S.tn[1] = INF; S.tn[2] = INF;
+    S.hf[0] = INF; S.hf[1] = INF; S.hf[2] = INF;
+    S.hidle[0] = 0; S.hidle[1] = 0; S.hidle[2] = 0;
   }
   if (tid < 16) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&S.smb[tid >> 1][tid & 1])) : "memory");
@@ -325,9 +355,11 @@ __global__ void __launch_bounds__(288, 2) k_cost4(Cost2Graph G, TopoArgs T, cons
     int fhead = 0, ftail = S.ftail0[q], running = 0, fin = 0, mk = 0, disp = 0;
     int cur = 0, nxt_id = -1;
     unsigned nst0 = 0, nst1 = 0;                 // bulk stagings issued per slot (mbarrier phases)
-    int li = 0, T0 = 0, w = 0, memd = -1;
+    // window 0: every device idle at t = 0, so nothing it sends lands before 1 + Wl
+    int li = 0, T0 = 0, Tend = COST4_DYN ? min(1 + Wl, WMAX) : Wl, w = 0, memd = -1;
     for (;; w++) {
       const int set = w % R4;
+      int nf = 0;   // finishes of this window (warp-uniform)
       if (w - R4 > memd) {   // the memory warp must have released this window set
         if (lane == 0)
           while ((memd = ld_acq(&S.mem_done)) < w - R4) { }
@@ -335,11 +367,12 @@ __global__ void __launch_bounds__(288, 2) k_cost4(Cost2Graph G, TopoArgs T, cons
       }
       if (q == 0 && lane == 0) {
         S.Tw[set] = T0;
+        S.Tl[set] = Tend - T0;
         S.tn[(w + 1) % 3] = INF;   // read last after barrier w - 2, written from window w + 1 on
+        S.hf[(w + 1) % 3] = INF;
+        S.hidle[(w + 1) % 3] = 0;
       }
-      // (pfirst[w & 1][c] needs no reset: it is read after window w only if channel c was pushed
-      // to in window w, and the first of those pushes wrote it)
-      const int Tend = T0 + Wl;
+      if (lane < d) S.pfirst[w & 1][8 * q + lane] = INF;
       for (;;) {
         // key 2 tau (+1 unless my op finishes at tau); an idle device with a non-empty FIFO
         // dispatches at once (only the sources at t = 0)
@@ -396,6 +429,12 @@ __global__ void __launch_bounds__(288, 2) k_cost4(Cost2Graph G, TopoArgs T, cons
           load_rec(r, &S.run[q]);
           const int sl = S.run_slot[q];
           const int nin = r.ie - r.ib, nout = r.oe - r.ob;
+#if COST4_DEFER
+          // the memory warp frees what this op held and counts down its producers' consumers
+          if (lane == 0) S.fl[set][q][nf] = make_int4(r.ib, r.ie, tau, nout == 0 ? r.id : -1);
+          nf++;
+          (void)sl; (void)nin;
+#else
           // frees: copies this op held (local), producers whose last consumer it is (queued)
           for (int j = lane; j < nin; j += 32) {
             IRec ir;
@@ -409,6 +448,7 @@ __global__ void __launch_bounds__(288, 2) k_cost4(Cost2Graph G, TopoArgs T, cons
             }
           }
           if (nout == 0 && lane == 0) delta -= r.bytes;
+#endif
           for (int j0 = 0; j0 < nout; j0 += 32) {
             const int j = j0 + lane;
             const bool v = j < nout;
@@ -529,6 +569,13 @@ __global__ void __launch_bounds__(288, 2) k_cost4(Cost2Graph G, TopoArgs T, cons
       // publish the end-of-window state, meet, and find the next window start
       if (own) S.phs[(w + 1) & 1][cin] = head;
       if (lane < d) S.ptail[w & 1][8 * q + lane] = S.ctail[8 * q + lane];
+#if COST4_DEFER
+      if (lane == 0) S.nfl[set][q] = nf;
+#endif
+      if (COST4_DYN && devl) {   // my earliest possible send from the next window on: my running op's finish, else T + 1
+        if (running) atomicMin(&S.hf[w % 3], fin);
+        else S.hidle[w % 3] = 1;
+      }
       bar_devices(32 * d);   // bar.sync orders the window's shared and global writes for all device warps
       if (q == 0 && lane == 31) {   // a lane that rarely has global writes in flight (release fence)
         S.dq_end[set] = S.dq_tail;
@@ -549,6 +596,13 @@ __global__ void __launch_bounds__(288, 2) k_cost4(Cost2Graph G, TopoArgs T, cons
         hs = head;
       }
       if (Tn == INF) break;
+      // lookahead: a transfer takes >= Wl ticks, so nothing sent in [Tn, Tend) lands before Tend
+      {
+        const int hf = S.hf[w % 3];
+        int H = hf == INF ? INF : hf + Wl;
+        if (S.hidle[w % 3]) H = min(H, Tn + 1 + Wl);
+        Tend = COST4_DYN ? min(Tn + WMAX, H) : Tn + Wl;
+      }
       T0 = Tn;
     }
     cp_wait0();
@@ -563,7 +617,10 @@ __global__ void __launch_bounds__(288, 2) k_cost4(Cost2Graph G, TopoArgs T, cons
   } else {
     // ---------------------------------------------------------------- memory warp
     long long mem = lane < d ? S.stat[lane] : 0, pk = mem;
-    int done_w = -1, dq_start = 0;
+    int done_w = -1;
+#if !COST4_DEFER
+    int dq_start = 0;
+#endif
     for (;;) {
       int wd = 0, fin_all = 0;
       if (lane == 0) {
@@ -573,6 +630,53 @@ __global__ void __launch_bounds__(288, 2) k_cost4(Cost2Graph G, TopoArgs T, cons
       wd = __shfl_sync(FULL, wd, 0);
       fin_all = __shfl_sync(FULL, fin_all, 0);
       if (wd > done_w) {
+#if COST4_DEFER
+        // finishes of windows done_w+1 .. wd, one lane per (window, device) list, 32 / 8 windows a pass:
+        // (A) the copies the op held die at its finish (-bytes on its device), a sink's output dies
+        // at its finish, and every producer's death tick is raised to this finish; (B) after the
+        // warp barrier, the producer's consumer count goes down, and the lane that brings it to 0
+        // files the death at the (now final) max tick into the window holding it
+        for (int wb = done_w + 1; wb <= wd; wb += 4) {
+          const int ww = wb + (lane >> 3), k = lane & 7;
+          const bool act = ww <= wd && k < d;
+          const int s = ww % R4;
+          const int n = act ? S.nfl[s][k] : 0;
+          const int Tws = act ? S.Tw[s] : 0;
+          for (int e = 0; e < n; e++) {
+            const int4 f = S.fl[s][k][e];
+            long long fr = f.w >= 0 ? G.out_bytes[f.w] : 0;   // a sink's output dies at its finish
+            for (int j0 = f.x; j0 < f.y; j0 += 4) {   // four independent record loads in flight
+              IRec ir4[4];
+#pragma unroll
+              for (int i = 0; i < 4; i++)
+                if (j0 + i < f.y) ir4[i] = G.irec[j0 + i];
+#pragma unroll
+              for (int i = 0; i < 4; i++)
+                if (j0 + i < f.y) {
+                  if (dev_of(Dn, ir4[i].u) != k) fr += ir4[i].bytes;
+                  atomicMax(&dtick[ir4[i].u], f.z);
+                }
+            }
+            if (fr) atomicAdd(reinterpret_cast<unsigned long long *>(&S.db[s][k][f.z - Tws]), (unsigned long long)(-fr));
+          }
+          __syncwarp();
+          for (int e = 0; e < n; e++) {
+            const int4 f = S.fl[s][k][e];
+            for (int j = f.x; j < f.y; j++) {
+              const IRec ir = G.irec[j];
+              if (dec_out4(cnt, ir, bigc, G.nbig)) {
+                const int tk = __ldcg(dtick + ir.u);
+                const int du = dev_of(Dn, ir.u);
+                int wv = done_w + 1;
+                while (wv < wd && tk >= S.Tw[wv % R4] + S.Tl[wv % R4]) wv++;
+                atomicAdd(reinterpret_cast<unsigned long long *>(&S.db[wv % R4][du][tk - S.Tw[wv % R4]]),
+                          (unsigned long long)(-ir.bytes));
+              }
+            }
+          }
+          __syncwarp();
+        }
+#else
         // producer deaths queued in windows done_w+1 .. wd
         const int dq_stop = S.dq_end[wd % R4];
         for (int i = dq_start + lane; i < dq_stop; i += 32) {
@@ -582,16 +686,18 @@ __global__ void __launch_bounds__(288, 2) k_cost4(Cost2Graph G, TopoArgs T, cons
           const int tk = __ldcg(dtick + u);
           const int du = dev_of(Dn, u);
           int ww = done_w + 1;
-          while (ww < wd && tk >= S.Tw[ww % R4] + Wl) ww++;
+          while (ww < wd && tk >= S.Tw[ww % R4] + S.Tl[ww % R4]) ww++;
           atomicAdd(reinterpret_cast<unsigned long long *>(&S.db[ww % R4][du][tk - S.Tw[ww % R4]]),
                     (unsigned long long)(-bytes));
         }
         dq_start = dq_stop;
         __syncwarp();
+#endif
         for (int ww = done_w + 1; ww <= wd; ww++) {   // tick-ordered sweep of each window
           const int s = ww % R4;
           if (lane < d) {
-            for (int o = 0; o < Wl; o++) {
+            const int len = S.Tl[s];
+            for (int o = 0; o < len; o++) {
               unsigned *wv = &S.lb[s][lane][o][0];
               mem += read3(wv) + S.db[s][lane][o];
               pk = max(pk, mem);
@@ -636,6 +742,9 @@ size_t cost4_scratch_per_placement(int N, long long E, int nbig) { return scratc
 
 // Wl = the shortest possible transfer: min over device pairs of latency + ceil(smallest edge's
 // bytes / bandwidth), capped at WMAX
+#ifndef COST4_XMIN
+#define COST4_XMIN 1
+#endif
 int cost4_window(const TopoArgs &T, int min_cost, int N, long long min_edge_bytes) {
   static const bool off = getenv("GDP_COST_V3") != nullptr || getenv("GDP_COST_V2") != nullptr;
   if (off) return 0;
@@ -647,7 +756,7 @@ int cost4_window(const TopoArgs &T, int min_cost, int N, long long min_edge_byte
     for (int q = 0; q < d; q++)
       if (k != q) {
         long long x = T.lat[k * 8 + q];
-        if (min_edge_bytes > 0 && T.bpt[k * 8 + q] > 0) x += (min_edge_bytes - 1) / T.bpt[k * 8 + q] + 1;
+        if (COST4_XMIN && min_edge_bytes > 0 && T.bpt[k * 8 + q] > 0) x += (min_edge_bytes - 1) / T.bpt[k * 8 + q] + 1;
         L = L < x ? L : (int)x;
       }
   }
