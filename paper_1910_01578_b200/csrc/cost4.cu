@@ -67,6 +67,9 @@ struct Smem4 {
   int dq_tail, flag, oom, mk, disp, nwin;
   int win_done, mem_done, dev_done;
   unsigned long long cross;
+#ifdef COST4_PROF
+  unsigned prof[8][10];
+#endif
 };
 
 struct Scratch4 {   // per-placement global scratch (same prefix as k_cost2 / k_cost3)
@@ -84,6 +87,19 @@ __host__ __device__ inline Scratch4 scratch4_layout(int N, long long E, int nbig
   return s;
 }
 
+#ifdef COST4_PROF   // per-phase cycle totals of each device warp (lane 0), printed by block 0
+#define PROF_MARK(k)                                           \
+  do {                                                         \
+    __syncwarp();                                              \
+    const unsigned now_ = (unsigned)clock();                   \
+    if (lane == 0) S.prof[q][k] += now_ - plast;               \
+    plast = now_;                                              \
+  } while (0)
+#else
+#define PROF_MARK(k) \
+  do {               \
+  } while (0)
+#endif
 __device__ __forceinline__ int ld_acq(const int *p) {
   int v;
   asm volatile("ld.acquire.cta.shared::cta.b32 %0, [%1];" : "=r"(v) : "r"((unsigned)__cvta_generic_to_shared(p)) : "memory");
@@ -326,6 +342,10 @@ __global__ void __launch_bounds__(288, 2) k_cost4(Cost2Graph G, TopoArgs T, cons
     int cur = 0, nxt_id = -1;
     unsigned nst0 = 0, nst1 = 0;                 // bulk stagings issued per slot (mbarrier phases)
     int li = 0, T0 = 0, w = 0, memd = -1;
+#ifdef COST4_PROF
+    if (lane < 10) S.prof[q][lane] = 0;
+    unsigned plast = (unsigned)clock(), ninst = 0;
+#endif
     for (;; w++) {
       const int set = w % R4;
       if (w - R4 > memd) {   // the memory warp must have released this window set
@@ -340,6 +360,7 @@ __global__ void __launch_bounds__(288, 2) k_cost4(Cost2Graph G, TopoArgs T, cons
       // (pfirst[w & 1][c] needs no reset: it is read after window w only if channel c was pushed
       // to in window w, and the first of those pushes wrote it)
       const int Tend = T0 + Wl;
+      PROF_MARK(0);
       for (;;) {
         // key 2 tau (+1 unless my op finishes at tau); an idle device with a non-empty FIFO
         // dispatches at once (only the sources at t = 0)
@@ -350,14 +371,20 @@ __global__ void __launch_bounds__(288, 2) k_cost4(Cost2Graph G, TopoArgs T, cons
         const int tau = (int)(key >> 1);
         if (key == NK || tau >= Tend) {   // my next event opens a later window
           if (lane == 0 && key != NK) atomicMin(&S.tn[w % 3], tau);
+          PROF_MARK(1);
           break;
         }
+        PROF_MARK(1);
+#ifdef COST4_PROF
+        ninst++;
+#endif
         const bool fnow = (key & 1) == 0;
         if (devl) {
           cp_wait1();   // FIFO refills older than the last instant
           if (fnow) mbar_wait(&S.smb[q][cur], ((cur ? nst1 : nst0) - 1u) & 1u);   // staged records
         }
         __syncwarp();
+        PROF_MARK(2);
         long long delta = 0;
         int navail = 0;
         // (1) the copy arriving now on my incoming channel (at most one per channel per tick)
@@ -389,6 +416,7 @@ __global__ void __launch_bounds__(288, 2) k_cost4(Cost2Graph G, TopoArgs T, cons
           if (av) put_inc(S, ovq, q, __popc(m & lt), ar);
           navail = __popc(m);
         }
+        PROF_MARK(3);
         // (2) my op finishes now: its edges one per lane
         if (fnow) {
           if (devl) running = 0;
@@ -409,6 +437,7 @@ __global__ void __launch_bounds__(288, 2) k_cost4(Cost2Graph G, TopoArgs T, cons
             }
           }
           if (nout == 0 && lane == 0) delta -= r.bytes;
+          PROF_MARK(4);
           for (int j0 = 0; j0 < nout; j0 += 32) {
             const int j = j0 + lane;
             const bool v = j < nout;
@@ -456,6 +485,7 @@ __global__ void __launch_bounds__(288, 2) k_cost4(Cost2Graph G, TopoArgs T, cons
           }
         }
         __syncwarp();
+        PROF_MARK(5);
         // (3) device lane: ops made available now join the FIFO in id order; dispatch; stage
         if (devl) {
           const int n = navail;
@@ -524,16 +554,19 @@ __global__ void __launch_bounds__(288, 2) k_cost4(Cost2Graph G, TopoArgs T, cons
         }
         // (4) my memory delta at tau
         if (delta != 0) add3(&S.lb[set][q][tau - T0][0], delta);
+        PROF_MARK(6);
         li++;
       }
       // publish the end-of-window state, meet, and find the next window start
       if (own) S.phs[(w + 1) & 1][cin] = head;
       if (lane < d) S.ptail[w & 1][8 * q + lane] = S.ctail[8 * q + lane];
+      PROF_MARK(7);
       bar_devices(32 * d);   // bar.sync orders the window's shared and global writes for all device warps
       if (q == 0 && lane == 31) {   // a lane that rarely has global writes in flight (release fence)
         S.dq_end[set] = S.dq_tail;
         st_rel(&S.win_done, w);
       }
+      PROF_MARK(8);
       const int Tn = S.tn[w % 3];
       if (own) {   // my channel: entries pushed in this window
         const int tn = S.ptail[w & 1][cin];
@@ -552,6 +585,12 @@ __global__ void __launch_bounds__(288, 2) k_cost4(Cost2Graph G, TopoArgs T, cons
       T0 = Tn;
     }
     cp_wait0();
+#ifdef COST4_PROF
+    if (b == 0 && lane == 0)
+      printf("PROF q=%d win=%d inst=%u pre=%u key=%u wait=%u arr=%u finin=%u finout=%u disp=%u post=%u bar=%u\n", q,
+             w + 1, ninst, S.prof[q][0], S.prof[q][1], S.prof[q][2], S.prof[q][3], S.prof[q][4], S.prof[q][5],
+             S.prof[q][6], S.prof[q][7], S.prof[q][8]);
+#endif
     if (devl) {
       atomicMax(&S.mk, mk);
       atomicAdd(&S.disp, disp);

@@ -1,7 +1,7 @@
 // tcgen05 tensor-core path for the tall-skinny dense maps of the policy network (bf16
 // operands, fp32 accumulation in TMEM): Y = epi(X W + b) (+R), the same contract as k_gemm.
 //
-// One persistent CTA (4 warps) per SM-slot.  The weight operand W (K x Nout, <= 256 x 256) is
+// Persistent CTAs (8 warps), up to 4 per SM as shared memory and TMEM allow.  The weight operand W (K x Nout, <= 256 x 256) is
 // converted to bf16 once per CTA into shared memory in the UMMA canonical K-major layout
 // (SWIZZLE_NONE: 8-row x 16-byte core matrices, LBO = next core matrix along K, SBO = next
 // 8-row group).  For every 128-row tile of X: the 4 warps convert the fp32 rows to bf16 into
@@ -44,7 +44,7 @@ __device__ __forceinline__ float epi_apply(int epi, float v) {
   }
 }
 
-__global__ void __launch_bounds__(TT, 2) k_gemm_tc(GemmArgs a, int Kp, int Np, int ncols) {
+__global__ void __launch_bounds__(TT, 4) k_gemm_tc(GemmArgs a, int Kp, int Np, int ncols) {
   extern __shared__ __align__(1024) unsigned char sm[];
   __shared__ __align__(8) uint64_t mbar;
   __shared__ uint32_t tmem_base;
@@ -102,13 +102,15 @@ __global__ void __launch_bounds__(TT, 2) k_gemm_tc(GemmArgs a, int Kp, int Np, i
   const bool vec_out = (a.ldy % 4 == 0) && ((reinterpret_cast<uintptr_t>(a.Y) & 15) == 0) &&
                        (a.Y2 == nullptr || ((a.ldy2 % 4 == 0) && (reinterpret_cast<uintptr_t>(a.Y2) & 15) == 0)) &&
                        (a.split % 8 == 0 || a.split >= a.Nout);
+  const bool vec_epi = (a.aux == nullptr || ((a.ldaux % 4 == 0) && (reinterpret_cast<uintptr_t>(a.aux) & 15) == 0)) &&
+                       (a.R == nullptr || ((a.ldr % 4 == 0) && (reinterpret_cast<uintptr_t>(a.R) & 15) == 0));
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int m0 = tile * TM;
     // X rows -> bf16 canonical (two-operand concat: columns [0, K1) from X1, [K1, K) from X2)
     if (vec4) {
       // 16-byte loads, 4 columns per item, unrolled for memory-level parallelism
       const int q = Kp / 4;
-#pragma unroll 4
+#pragma unroll 8
       for (int e = tid; e < TM * q; e += TT) {
         const int r = e / q, k = (e % q) * 4;
         const int m = m0 + r;
@@ -179,17 +181,40 @@ __global__ void __launch_bounds__(TT, 2) k_gemm_tc(GemmArgs a, int Kp, int Np, i
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
       if (m >= a.M) continue;
       float x[8];
-#pragma unroll
-      for (int j = 0; j < 8; j++) {
-        const int n = c0 + j;
-        float y = __uint_as_float(v[j]);
-        if (n < a.Nout) {
-          if (a.bias) y += a.bias[n];
-          if (a.epi == EPI_MASK) y = a.aux[(size_t)m * a.ldaux + n] > 0.f ? y : 0.f;
-          else y = epi_apply(a.epi, y);
-          if (a.R) y += a.R[(size_t)m * a.ldr + n];
+      if (vec_epi && c0 + 8 <= a.Nout) {   // full 8-column chunk: 16-byte loads of mask and residual
+        float mk[8], rr[8];
+        if (a.epi == EPI_MASK) {
+          const float4 *p = reinterpret_cast<const float4 *>(a.aux + (size_t)m * a.ldaux + c0);
+          const float4 u0 = p[0], u1 = p[1];
+          mk[0] = u0.x; mk[1] = u0.y; mk[2] = u0.z; mk[3] = u0.w; mk[4] = u1.x; mk[5] = u1.y; mk[6] = u1.z; mk[7] = u1.w;
         }
-        x[j] = y;
+        if (a.R) {
+          const float4 *p = reinterpret_cast<const float4 *>(a.R + (size_t)m * a.ldr + c0);
+          const float4 u0 = p[0], u1 = p[1];
+          rr[0] = u0.x; rr[1] = u0.y; rr[2] = u0.z; rr[3] = u0.w; rr[4] = u1.x; rr[5] = u1.y; rr[6] = u1.z; rr[7] = u1.w;
+        }
+#pragma unroll
+        for (int j = 0; j < 8; j++) {
+          float y = __uint_as_float(v[j]);
+          if (a.bias) y += a.bias[c0 + j];
+          if (a.epi == EPI_MASK) y = mk[j] > 0.f ? y : 0.f;
+          else y = epi_apply(a.epi, y);
+          if (a.R) y += rr[j];
+          x[j] = y;
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < 8; j++) {
+          const int n = c0 + j;
+          float y = __uint_as_float(v[j]);
+          if (n < a.Nout) {
+            if (a.bias) y += a.bias[n];
+            if (a.epi == EPI_MASK) y = a.aux[(size_t)m * a.ldaux + n] > 0.f ? y : 0.f;
+            else y = epi_apply(a.epi, y);
+            if (a.R) y += a.R[(size_t)m * a.ldr + n];
+          }
+          x[j] = y;
+        }
       }
       if (vec_out && c0 + 8 <= a.Nout && (c0 + 8 <= a.split || c0 >= a.split)) {
         float *dst = (c0 < a.split) ? a.Y + (size_t)m * a.ldy + c0 : a.Y2 + (size_t)m * a.ldy2 + (c0 - a.split);
@@ -248,8 +273,14 @@ void launch_gemm_tc(const GemmArgs &a, cudaStream_t s) {
     cudaFuncSetAttribute(k_gemm_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     configured = true;
   }
+  // as many resident CTAs per SM as shared memory (and TMEM columns: 512 per SM) allow, up to 4,
+  // so that more 128-row tiles have their loads in flight at once
   const int ntiles = (a.M + TM - 1) / TM;
-  const int grid = ntiles < 2 * num_sms() ? ntiles : 2 * num_sms();
+  int per_sm = (int)((227 * 1024) / (smem + 2048));
+  per_sm = per_sm < 512 / ncols ? per_sm : 512 / ncols;
+  per_sm = per_sm < 4 ? (per_sm < 1 ? 1 : per_sm) : 4;
+  const int slots = per_sm * num_sms();
+  const int grid = ntiles < slots ? ntiles : slots;
   note_launch("k_gemm_tc", s, gemm_bytes(a), 2.0 * a.M * a.K * a.Nout);
   k_gemm_tc<<<grid, TT, smem, s>>>(a, Kp, Np, ncols);
 }

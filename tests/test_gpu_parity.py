@@ -482,6 +482,37 @@ def test_cost_windowed_kernel(gdp, case):
     assert_cost_equal(g, t, D, cost_gpu(gdp, g, t, D))
 
 
+@pytest.mark.parametrize("case", range(3))
+def test_cost_window_from_bytes(gdp, case):
+    """The window is the shortest possible transfer, latency + ceil(smallest edge bytes /
+    bandwidth): (0) every transfer takes exactly that long (each lands on a window boundary),
+    (1) a zero-byte edge brings the window back to the latency alone, (2) bytes alone make the
+    window (latency 1, transfers of 3-7 ticks)."""
+    from workloads import Topology
+    rng = np.random.default_rng(300 + case)
+    d = [4, 8, 3][case]
+    n = int(rng.integers(150, 400))
+    g = workloads.random_dag(n, p_edge=0.15, max_back=30, seed=400 + case, cost_max=12)
+    g.compute_cost = np.maximum(g.compute_cost, 1)
+    bpt = 1000
+    if case == 0:
+        g.output_bytes = np.full(n, 3 * bpt, dtype=np.int64)          # every transfer 3 + 2 ticks
+    elif case == 1:
+        g.output_bytes = g.output_bytes.copy()
+        g.output_bytes[int(g.edges[0, 0])] = 0
+    else:
+        g.output_bytes = rng.integers(2 * bpt + 1, 7 * bpt, size=n).astype(np.int64)
+    la = np.full((d, d), [2, 3, 1][case], dtype=np.int32)
+    np.fill_diagonal(la, 0)
+    bp = np.full((d, d), bpt, dtype=np.int64)
+    t = Topology(d=d, mem_capacity=np.full(d, 1 << 60, dtype=np.int64), speed=np.ones(d, dtype=np.int32),
+                 bytes_per_tick=bp, latency=la)
+    G = gdp.Graph(g, workloads.features(g))
+    assert gdp.cost_kernel(G, gdp.Topo(t)) == 4
+    D = rng.integers(0, d, size=(48, n)).astype(np.uint8)
+    assert_cost_equal(g, t, D, cost_gpu(gdp, g, t, D))
+
+
 @pytest.mark.parametrize("cfg", ["c1", "c3"])
 def test_cuda_graph_step_matches_eager(gdp, cfg):
     """A captured CUDA graph of the whole policy step (Philox step read from device memory,
