@@ -94,11 +94,12 @@ __global__ void __launch_bounds__(NT) k_gemm(GemmArgs a) {
 // column sum of dY, accumulated by the ty == 0 threads of the blockIdx.x == 0 blocks, so it
 // costs no extra 64-wide K tile.  Rows per chunk (rpc, a multiple of BK) are chosen on the
 // host so that the grid holds about 2 blocks per SM; fixed per shape, hence deterministic.
-__global__ void __launch_bounds__(NT) k_wgrad(int M, int K, int Kaug, int Nout, const float *X1, int ldx1,
-                                              int K1, const float *X2, int ldx2, const float *dY, int ldy,
-                                              float *part, int rpc) {
-  __shared__ float Xs[BK][BM + 4];
-  __shared__ float Ys[BK][BN + 4];
+constexpr int WK = 32;   // rows of X / dY per k_wgrad stage
+__global__ void __launch_bounds__(NT, 3) k_wgrad(int M, int K, int Kaug, int Nout, const float *X1, int ldx1,
+                                                 int K1, const float *X2, int ldx2, const float *dY, int ldy,
+                                                 float *part, int rpc) {
+  __shared__ float Xs[WK][BM + 4];
+  __shared__ float Ys[WK][BN + 4];
   const int tid = threadIdx.x;
   const int k0 = blockIdx.x * BM, n0 = blockIdx.y * BN, chunk = blockIdx.z;
   const int r0 = chunk * rpc, r1 = min(M, r0 + rpc);
@@ -109,38 +110,49 @@ __global__ void __launch_bounds__(NT) k_wgrad(int M, int K, int Kaug, int Nout, 
   for (int i = 0; i < 4; i++)
 #pragma unroll
     for (int j = 0; j < 4; j++) acc[i][j] = 0.f;
-  for (int rb = r0; rb < r1; rb += BK) {
+  // the next stage's X and dY values are loaded into registers while this stage is multiplied
+  constexpr int PX = (BM * WK) / NT, PY = (BN * WK) / NT;
+  float xr[PX], yr[PY];
+  auto fetch = [&](int rb) {
 #pragma unroll
-    for (int i = 0; i < (BM * BK) / NT; i++) {
-      int e = tid + i * NT;
-      int rr = e / BM, kk = e % BM;
-      int r = rb + rr, k = k0 + kk;
-      float v = 0.f;
-      if (r < r1 && k < K) v = (k < K1) ? X1[(size_t)r * ldx1 + k] : X2[(size_t)r * ldx2 + (k - K1)];
-      Xs[rr][kk] = v;
+    for (int i = 0; i < PX; i++) {
+      const int e = tid + i * NT, rr = e / BM, kk = e % BM;
+      const int r = rb + rr, k = k0 + kk;
+      xr[i] = (r < r1 && k < K) ? ((k < K1) ? X1[(size_t)r * ldx1 + k] : X2[(size_t)r * ldx2 + (k - K1)]) : 0.f;
     }
 #pragma unroll
-    for (int i = 0; i < (BN * BK) / NT; i++) {
-      int e = tid + i * NT;
-      int rr = e / BN, c = e % BN;
-      int r = rb + rr, n = n0 + c;
-      Ys[rr][c] = (r < r1 && n < Nout) ? dY[(size_t)r * ldy + n] : 0.f;
+    for (int i = 0; i < PY; i++) {
+      const int e = tid + i * NT, rr = e / BN, c = e % BN;
+      const int r = rb + rr, n = n0 + c;
+      yr[i] = (r < r1 && n < Nout) ? dY[(size_t)r * ldy + n] : 0.f;
+    }
+  };
+  if (r0 < r1) fetch(r0);
+  for (int rb = r0; rb < r1; rb += WK) {
+#pragma unroll
+    for (int i = 0; i < PX; i++) {
+      const int e = tid + i * NT;
+      Xs[e / BM][e % BM] = xr[i];
+    }
+#pragma unroll
+    for (int i = 0; i < PY; i++) {
+      const int e = tid + i * NT;
+      Ys[e / BN][e % BN] = yr[i];
     }
     __syncthreads();
+    if (rb + WK < r1) fetch(rb + WK);
 #pragma unroll
-    for (int rr = 0; rr < BK; rr++) {
-      float xv[4], yv[4];
-#pragma unroll
-      for (int i = 0; i < 4; i++) xv[i] = Xs[rr][ty * 4 + i];
-#pragma unroll
-      for (int j = 0; j < 4; j++) yv[j] = Ys[rr][tx * 4 + j];
+    for (int rr = 0; rr < WK; rr++) {
+      const float4 xv = *reinterpret_cast<const float4 *>(&Xs[rr][ty * 4]);
+      const float4 yv = *reinterpret_cast<const float4 *>(&Ys[rr][tx * 4]);
+      const float xa[4] = {xv.x, xv.y, xv.z, xv.w}, ya[4] = {yv.x, yv.y, yv.z, yv.w};
 #pragma unroll
       for (int i = 0; i < 4; i++)
 #pragma unroll
-        for (int j = 0; j < 4; j++) acc[i][j] = fmaf(xv[i], yv[j], acc[i][j]);
+        for (int j = 0; j < 4; j++) acc[i][j] = fmaf(xa[i], ya[j], acc[i][j]);
       if (bias_rows) {
 #pragma unroll
-        for (int j = 0; j < 4; j++) bacc[j] += yv[j];
+        for (int j = 0; j < 4; j++) bacc[j] += ya[j];
       }
     }
     __syncthreads();
@@ -331,11 +343,11 @@ void launch_wgrad(int M, int K, int Nout, const float *X1, int ldx1, int K1, con
                   bool accumulate, cudaStream_t s) {
   const int Kaug = K + (with_bias ? 1 : 0);
   const int gx = (K + BM - 1) / BM, gy = (Nout + BN - 1) / BN;
-  // about 2 blocks per SM, within the partial buffer, at least BK rows per chunk
-  long long want = (2LL * num_sms_dense() + gx * gy - 1) / (gx * gy);
+  // about 3 blocks per SM (the launch bound), within the partial buffer, at least WK rows per chunk
+  long long want = (3LL * num_sms_dense() + gx * gy - 1) / (gx * gy);
   want = std::min<long long>(want, (long long)(part_floats / ((size_t)Kaug * Nout)));
-  want = std::max<long long>(1, std::min<long long>(want, (M + BK - 1) / BK));
-  const int rpc = (int)(((M + want - 1) / want + BK - 1) / BK * BK);
+  want = std::max<long long>(1, std::min<long long>(want, (M + WK - 1) / WK));
+  const int rpc = (int)(((M + want - 1) / want + WK - 1) / WK * WK);
   const int chunks = (M + rpc - 1) / rpc;
   dim3 grid(gx, gy, chunks);
   note_launch("k_wgrad", s, 4.0 * M * (K + Nout) + 4.0 * chunks * Kaug * Nout, 2.0 * M * Kaug * Nout);
