@@ -562,15 +562,20 @@ __global__ void __launch_bounds__(288, 2) k_cost4(Cost2Graph G, TopoArgs T, cons
       if (lane < d) S.ptail[w & 1][8 * q + lane] = S.ctail[8 * q + lane];
       PROF_MARK(7);
       bar_devices(32 * d);   // bar.sync orders the window's shared and global writes for all device warps
+      PROF_MARK(8);
+      // the next window start and my channel's state first (independent loads in flight together;
+      // pfirst is meaningful only if the channel was pushed to in window w), then the memory-warp
+      // release (its memory clobber would otherwise order these loads behind it)
+      const int Tn = S.tn[w % 3];
+      const int tn_c = own ? S.ptail[w & 1][cin] : 0;
+      const int pf_c = own ? S.pfirst[w & 1][cin] : INF;
       if (q == 0 && lane == 31) {   // a lane that rarely has global writes in flight (release fence)
         S.dq_end[set] = S.dq_tail;
         st_rel(&S.win_done, w);
       }
-      PROF_MARK(8);
-      const int Tn = S.tn[w % 3];
       if (own) {   // my channel: entries pushed in this window
-        const int tn = S.ptail[w & 1][cin];
-        if (ha == INF && tn > tknown) ha = S.pfirst[w & 1][cin];
+        const int tn = tn_c;
+        if (ha == INF && tn > tknown) ha = pf_c;
         const int lim = min(tn, head + KC4);
         for (; filled < lim; filled++) {
           if (filled >= tknown && filled < hs + KC4) continue;   // the producer wrote it into the ring
