@@ -34,9 +34,6 @@ using namespace cu;
 #ifndef COST4_WMAX
 #define COST4_WMAX 8
 #endif
-#ifndef COST4_PT
-#define COST4_PT 1
-#endif
 constexpr int WMAX = COST4_WMAX;   // window length cap (ticks) = buckets per window
 #ifndef COST4_R4
 #define COST4_R4 8
@@ -61,9 +58,6 @@ struct Smem4 {
   long long db[R4][8][WMAX];       // producer deaths (memory warp only)
   int cfree[64], ctail[64], cstamp[64];                        // producer side (warp k)
   int pfirst[2][64], ptail[2][64];   // published per window parity: first push's arrival, tail
-#if COST4_PT
-  int pst[2][64];                  // per window parity: the window that last pushed to the channel
-#endif
   int tn[3];                       // next window start, atomic min over devices' next events and first pushes
   int phs[2][64];                  // consumer head at the start of window w (parity w & 1)
   int coff[64], ccnt[64];
@@ -201,9 +195,6 @@ __global__ void __launch_bounds__(288, 2) k_cost4(Cost2Graph G, TopoArgs T, cons
   for (int j = tid; j < G.nbig; j += nthr) { bigc[j] = G.big_in[j]; bigc[G.nbig + j] = G.big_out[j]; }
   for (int v = tid; v < N; v += nthr) dtick[v] = -1;
   if (tid < 64) { S.ccnt[tid] = 0; S.cstamp[tid] = -1; S.cfree[tid] = 0; S.ctail[tid] = 0; S.phs[0][tid] = 0; }
-#if COST4_PT
-  if (tid < 128) (&S.pst[0][0])[tid] = -1;
-#endif
   if (tid < 8) { S.stat[tid] = 0; S.busyv[tid] = 0; S.opcnt[tid] = 0; }
   if (tid == 0) {
     S.flag = 0; S.oom = 0; S.cross = 0; S.dq_tail = 0; S.mk = 0; S.disp = 0; S.nwin = 0;
@@ -482,14 +473,8 @@ __global__ void __launch_bounds__(288, 2) k_cost4(Cost2Graph G, TopoArgs T, cons
                 if (rank == 0) {
                   S.cfree[c] = bs + n * x;
                   S.ctail[c] = tail + n;
-#if COST4_PT
-                  S.ptail[w & 1][c] = tail + n;   // published as it moves (the consumer reads it after the barrier)
-                  if (S.pst[w & 1][c] != w) {   // first push of this window: the consumer may not know it yet
-                    S.pst[w & 1][c] = w;
-#else
                   if (S.cstamp[c] != w) {   // first push of this window: the consumer may not know it yet
                     S.cstamp[c] = w;
-#endif
                     S.pfirst[w & 1][c] = bs + x;
                     atomicMin(&S.tn[w % 3], bs + x);
                   }
@@ -574,9 +559,7 @@ __global__ void __launch_bounds__(288, 2) k_cost4(Cost2Graph G, TopoArgs T, cons
       }
       // publish the end-of-window state, meet, and find the next window start
       if (own) S.phs[(w + 1) & 1][cin] = head;
-#if !COST4_PT
       if (lane < d) S.ptail[w & 1][8 * q + lane] = S.ctail[8 * q + lane];
-#endif
       PROF_MARK(7);
       bar_devices(32 * d);   // bar.sync orders the window's shared and global writes for all device warps
       PROF_MARK(8);
@@ -584,14 +567,7 @@ __global__ void __launch_bounds__(288, 2) k_cost4(Cost2Graph G, TopoArgs T, cons
       // pfirst is meaningful only if the channel was pushed to in window w), then the memory-warp
       // release (its memory clobber would otherwise order these loads behind it)
       const int Tn = S.tn[w % 3];
-#if COST4_PT
-      // the channel's tail moved in window w only if it was pushed to then (parity slot w & 1 is
-      // rewritten no earlier than window w + 2)
-      const int ps_c = own ? S.pst[w & 1][cin] : -1, pt_c = own ? S.ptail[w & 1][cin] : 0;
-      const int tn_c = ps_c == w ? pt_c : tknown;
-#else
       const int tn_c = own ? S.ptail[w & 1][cin] : 0;
-#endif
       const int pf_c = own ? S.pfirst[w & 1][cin] : INF;
       if (q == 0 && lane == 31) {   // a lane that rarely has global writes in flight (release fence)
         S.dq_end[set] = S.dq_tail;
