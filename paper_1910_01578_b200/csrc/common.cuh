@@ -158,6 +158,9 @@ inline double gemm_bytes(const GemmArgs &a) {
 bool tc_eligible(const GemmArgs &a);
 void launch_gemm_tc(const GemmArgs &a, cudaStream_t s);
 void set_tensor_cores(bool on);
+bool tensor_cores_on();
+bool attn_fwd_tc_eligible(int S, int M);
+void launch_attn_fwd_tc(const float *qkv, float *o, float *lse, int N, int S, int M, cudaStream_t s);
 // ablation variant of the entry point in progress (gdp_config.no_attention)
 void set_no_attention(bool on);
 bool no_attention();

@@ -312,6 +312,7 @@ inline unsigned nblk(size_t n, int t) { return (unsigned)((n + t - 1) / t); }
 
 static thread_local bool t_tc = false;
 void set_tensor_cores(bool on) { t_tc = on; }
+bool tensor_cores_on() { return t_tc; }
 static thread_local bool t_noattn = false;
 void set_no_attention(bool on) { t_noattn = on; }
 bool no_attention() { return t_noattn; }

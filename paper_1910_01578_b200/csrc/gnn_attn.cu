@@ -435,6 +435,11 @@ static double attn_flops(int N, int S, int M) {
 
 void launch_attn_fwd(const float *qkv, float *o, float *lse, int N, int S, int M, cudaStream_t s) {
   int nseg = (N + S - 1) / S;
+  if (tensor_cores_on() && attn_fwd_tc_eligible(S, M)) {   // tensor-core mode: tcgen05 tiles (attn_tc.cu)
+    note_launch("k_attn_fwd_tc", s, 4.0 * (double)N * (192 + 64 + kHeads), attn_flops(N, S, M));
+    launch_attn_fwd_tc(qkv, o, lse, N, S, M, s);
+    return;
+  }
   note_launch("k_attn_fwd", s, 4.0 * (double)N * (192 + 64 + kHeads), attn_flops(N, S, M));
   k_attn_fwd<<<dim3(nseg, kHeads), AQ, 0, s>>>(qkv, o, lse, N, S, M);
 }

@@ -321,13 +321,17 @@ TC_RTOL = 2e-2
 TC_FLOOR = 1.0   # bf16 operands: errors scale with the largest magnitudes, so compare norm-wise
 
 
-@pytest.mark.parametrize("case", ["c2", "mem_inf_big"])
+@pytest.mark.parametrize("case", ["c2", "mem_inf_big", "seg_ragged"])
 def test_tensor_core_mode(gdp, case):
-    """Dense maps on tcgen05 (bf16 operands, fp32 accumulation): every stage within the
-    bf16 tolerance of BASELINE north_star (rtol 2e-2)."""
+    """Dense maps and (when a segment's keys fit one 256-key tile) the attention forward on
+    tcgen05 (bf16 operands, fp32 accumulation): every stage within the bf16 tolerance of
+    BASELINE north_star (rtol 2e-2).  seg_ragged: S = 96, M = 160 (keys 96..256, a ragged last
+    segment) on the tensor-core attention tile; mem_inf_big: M = inf on the SIMT attention."""
     if case == "c2":
         W = workloads.config("c2")
         g, d, S, M = W.graphs[0], W.d, W.seg_len, W.mem_len
+    elif case == "seg_ragged":
+        g, d, S, M = workloads.random_dag(1000, p_edge=0.05, max_back=60, seed=21), 4, 96, 160
     else:
         g, d, S, M = workloads.random_dag(700, p_edge=0.05, max_back=60, seed=9), 8, 100, -1
     th = workloads.init_theta(workloads.F, d, seed=13, mode="random")
