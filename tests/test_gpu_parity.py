@@ -321,17 +321,20 @@ TC_RTOL = 2e-2
 TC_FLOOR = 1.0   # bf16 operands: errors scale with the largest magnitudes, so compare norm-wise
 
 
-@pytest.mark.parametrize("case", ["c2", "mem_inf_big", "seg_ragged"])
+@pytest.mark.parametrize("case", ["c2", "mem_inf_big", "seg_ragged", "short_mem"])
 def test_tensor_core_mode(gdp, case):
     """Dense maps and (when a segment's keys fit one 256-key tile) the attention forward on
     tcgen05 (bf16 operands, fp32 accumulation): every stage within the bf16 tolerance of
     BASELINE north_star (rtol 2e-2).  seg_ragged: S = 96, M = 160 (keys 96..256, a ragged last
-    segment) on the tensor-core attention tile; mem_inf_big: M = inf on the SIMT attention."""
+    segment) on the tensor-core forward tile (its backward, M > S, on SIMT); short_mem: S = 100,
+    M = 60 on both tensor-core tiles; mem_inf_big: M = inf on the SIMT attention."""
     if case == "c2":
         W = workloads.config("c2")
         g, d, S, M = W.graphs[0], W.d, W.seg_len, W.mem_len
     elif case == "seg_ragged":
         g, d, S, M = workloads.random_dag(1000, p_edge=0.05, max_back=60, seed=21), 4, 96, 160
+    elif case == "short_mem":
+        g, d, S, M = workloads.random_dag(1000, p_edge=0.05, max_back=60, seed=22), 4, 100, 60
     else:
         g, d, S, M = workloads.random_dag(700, p_edge=0.05, max_back=60, seed=9), 8, 100, -1
     th = workloads.init_theta(workloads.F, d, seed=13, mode="random")
@@ -352,6 +355,29 @@ def test_tensor_core_mode(gdp, case):
     cos = float(gg @ grad / (np.linalg.norm(gg) * np.linalg.norm(grad)))
     ratio = float(np.linalg.norm(gg) / np.linalg.norm(grad))
     assert cos > 0.98 and abs(ratio - 1) < 0.15, ("grad", cos, ratio)   # measured: c2 0.990 / 0.906
+
+
+@pytest.mark.parametrize("case", ["c1", "seg", "short_mem", "ragged"])
+def test_tensor_core_attention_matches_simt(gdp, case, monkeypatch):
+    """The tcgen05 attention tiles (forward k_attn_fwd_tc, backward k_attn_bwd_tc) against the
+    SIMT kernels inside the same tensor-core-mode step (GDP_ATTN_SIMT=1 switches them off):
+    logits within the bf16 tolerance, the gradient along the same direction (bf16 P and dS)."""
+    g, d, S, M = {"c1": (workloads.config("c1").graphs[0], 2, 32, 32),
+                  "seg": (workloads.random_dag(900, p_edge=0.05, max_back=60, seed=31), 4, 128, 128),
+                  "short_mem": (workloads.random_dag(1000, p_edge=0.05, max_back=60, seed=32), 8, 100, 60),
+                  "ragged": (workloads.random_dag(517, p_edge=0.08, max_back=40, seed=33), 4, 64, 64)}[case]
+    th = workloads.init_theta(workloads.F, d, seed=13, mode="random")
+    B = 16
+    monkeypatch.setenv("GDP_ATTN_SIMT", "1")
+    ref = run_step(gdp, g, d, S, M, True, B, th, tc=True)
+    monkeypatch.setenv("GDP_ATTN_SIMT", "0")
+    r = run_step(gdp, g, d, S, M, True, B, th, tc=True)
+    ok, err, nbad = close(r["logits"], ref["logits"], rtol=TC_RTOL, floor=TC_FLOOR)
+    assert ok, ("logits", err, nbad)
+    assert (r["D"] == ref["D"]).mean() > 0.99          # placements sampled from both logits
+    a, b = r["grad"].astype(np.float64), ref["grad"].astype(np.float64)
+    cos = float(a @ b / (np.linalg.norm(a) * np.linalg.norm(b)))
+    assert cos > 0.99 and abs(np.linalg.norm(a) / np.linalg.norm(b) - 1) < 0.05, ("grad", cos)
 
 
 # ------------------------------------------------------------------ cost-kernel overflow paths

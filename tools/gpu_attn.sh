@@ -1,5 +1,5 @@
 python -c "import __graft_entry__ as g; g.build()" > /dev/null 2>&1
-timeout 900 python -m pytest tests/test_gpu_parity.py -m gpu -q -x -k "tensor_core_mode" 2>&1 | tail -15
+timeout 900 python -m pytest tests/test_gpu_parity.py -m gpu -q -x -k "tensor_core" 2>&1 | tail -15
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
 timeout 600 python bench.py --no-cpu-baseline --no-e2e --steps 5 > gpurun_out/bench_pol.json 2>/dev/null
 python - <<'PY'
