@@ -1,6 +1,6 @@
-// tcgen05 tensor-core forward of the segment attention (a7) for the
-// tensor-core mode (bf16 operands, fp32 accumulation in TMEM), used when a query segment's whole
-// key range fits one 256-key tile (S <= 128 and M <= 256 - S: the headline M = S = 128).
+// tcgen05 tensor-core tiles of the segment attention (a7) for the
+// tensor-core mode (bf16 operands, fp32 accumulation in TMEM), segments of S <= 128 queries.
+// Forward: any memory length (M = inf included), online softmax over 256-key blocks.
 //
 // One CTA (4 warps, thread = query row) per (segment tau, head h):
 //   1. Q (128 x 16), K (keys x 16) and V^T (16 x keys) -> bf16 in shared memory, UMMA canonical
@@ -9,7 +9,9 @@
 //   3. each warp drains its 32 TMEM lanes (`tcgen05.ld.32x32b.x16`): row max of S / 4, then
 //      p = exp(S / 4 - max), the row sum in fp32, and P as bf16 back to shared memory;
 //   4. 16 MMAs (K = 16 keys each) give P V in TMEM columns 0..15 (S is consumed by then);
-//   5. O = (P V) / sum and LSE = max + log(sum), the same outputs as k_attn_fwd.
+//   5. O = (P V) / sum and LSE = max + log(sum), the same outputs as k_attn_fwd;
+//   with more than 256 keys (M > 256 - S) steps 2-4 repeat per 256-key block with the running
+//   max / sum / output rescaled (flash-attention style; O accumulates in fp32 registers).
 // Memory rows are stop-gradient only for the backward, which stays on k_attn_bwd_* (SIMT).
 #include <cuda_bf16.h>
 
@@ -71,10 +73,10 @@ __global__ void __launch_bounds__(TQ, 2) k_attn_fwd_tc(const float *__restrict__
   unsigned char *sV = sK + TKEY * 16 * 2;        // V^T: 16 x 256
   unsigned char *sP = sV + 16 * TKEY * 2;        // 128 x 256
   const int tid = threadIdx.x, warp = tid >> 5;
-  const int tau = blockIdx.x, hd = blockIdx.y;
+  const int nseg = gridDim.x;
+  const int tau = nseg - 1 - blockIdx.x, hd = blockIdx.y;   // longest key ranges first
   const int q0 = tau * S, q1 = min(N, q0 + S);
   const int lo = M < 0 ? 0 : max(0, q0 - M), hi = q1;
-  const int nk = hi - lo, Np = (nk + 15) & ~15;
 
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(&tmem_base)), "r"(256));
@@ -84,7 +86,7 @@ __global__ void __launch_bounds__(TQ, 2) k_attn_fwd_tc(const float *__restrict__
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&mbar)));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  // Q row tid, K / V rows tid and tid + 128 (16-byte loads; zero rows past the ranges)
+  // Q row tid (16-byte loads; zero rows past the segment)
   {
     const int i = q0 + tid;
     float4 a[4] = {};
@@ -98,104 +100,124 @@ __global__ void __launch_bounds__(TQ, 2) k_attn_fwd_tc(const float *__restrict__
     *reinterpret_cast<uint4 *>(sQ + coff(tid, 0, 16)) = lo8;
     *reinterpret_cast<uint4 *>(sQ + coff(tid, 8, 16)) = hi8;
   }
+  const uint32_t trow_off = (uint32_t)(warp * 32) << 16;
+  float mx = -INFINITY, sum = 0.f, acc[16];
 #pragma unroll
-  for (int h2 = 0; h2 < 2; h2++) {
-    const int j = tid + h2 * TQ, r = lo + j;
-    float4 kk[4] = {}, vv[4] = {};
-    if (j < nk) {
-      const float4 *pk = reinterpret_cast<const float4 *>(qkv + (size_t)r * 192 + 64 + hd * 16);
-      const float4 *pv = reinterpret_cast<const float4 *>(qkv + (size_t)r * 192 + 128 + hd * 16);
+  for (int c = 0; c < 16; c++) acc[c] = 0.f;
+  uint32_t phase = 0;
+  // online softmax over 256-key blocks (one block when M <= 256 - S, the headline)
+  for (int kb = lo; kb < hi; kb += TKEY) {
+    const int nk = min(TKEY, hi - kb), Np = (nk + 15) & ~15;
 #pragma unroll
-      for (int t = 0; t < 4; t++) { kk[t] = pk[t]; vv[t] = pv[t]; }
+    for (int h2 = 0; h2 < 2; h2++) {   // K / V rows tid and tid + 128 of this block
+      const int j = tid + h2 * TQ, r = kb + j;
+      float4 kk[4] = {}, vv[4] = {};
+      if (j < nk) {
+        const float4 *pk = reinterpret_cast<const float4 *>(qkv + (size_t)r * 192 + 64 + hd * 16);
+        const float4 *pv = reinterpret_cast<const float4 *>(qkv + (size_t)r * 192 + 128 + hd * 16);
+#pragma unroll
+        for (int t = 0; t < 4; t++) { kk[t] = pk[t]; vv[t] = pv[t]; }
+      }
+      *reinterpret_cast<uint4 *>(sK + coff(j, 0, 16)) =
+          make_uint4(pack2(kk[0].x, kk[0].y), pack2(kk[0].z, kk[0].w), pack2(kk[1].x, kk[1].y), pack2(kk[1].z, kk[1].w));
+      *reinterpret_cast<uint4 *>(sK + coff(j, 8, 16)) =
+          make_uint4(pack2(kk[2].x, kk[2].y), pack2(kk[2].z, kk[2].w), pack2(kk[3].x, kk[3].y), pack2(kk[3].z, kk[3].w));
+      const float vf[16] = {vv[0].x, vv[0].y, vv[0].z, vv[0].w, vv[1].x, vv[1].y, vv[1].z, vv[1].w,
+                            vv[2].x, vv[2].y, vv[2].z, vv[2].w, vv[3].x, vv[3].y, vv[3].z, vv[3].w};
+#pragma unroll
+      for (int c = 0; c < 16; c++)   // V^T: row = head dim c, column = key j
+        *reinterpret_cast<__nv_bfloat16 *>(sV + coff(c, j, TKEY)) = __float2bfloat16_rn(vf[c]);
     }
-    *reinterpret_cast<uint4 *>(sK + coff(j, 0, 16)) =
-        make_uint4(pack2(kk[0].x, kk[0].y), pack2(kk[0].z, kk[0].w), pack2(kk[1].x, kk[1].y), pack2(kk[1].z, kk[1].w));
-    *reinterpret_cast<uint4 *>(sK + coff(j, 8, 16)) =
-        make_uint4(pack2(kk[2].x, kk[2].y), pack2(kk[2].z, kk[2].w), pack2(kk[3].x, kk[3].y), pack2(kk[3].z, kk[3].w));
-    const float vf[16] = {vv[0].x, vv[0].y, vv[0].z, vv[0].w, vv[1].x, vv[1].y, vv[1].z, vv[1].w,
-                          vv[2].x, vv[2].y, vv[2].z, vv[2].w, vv[3].x, vv[3].y, vv[3].z, vv[3].w};
-#pragma unroll
-    for (int c = 0; c < 16; c++)   // V^T: row = head dim c, column = key j
-      *reinterpret_cast<__nv_bfloat16 *>(sV + coff(c, j, TKEY)) = __float2bfloat16_rn(vf[c]);
-  }
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  const uint32_t tmem = tmem_base;
-  // S = Q K^T: M = 128, N = Np, K = 16
-  if (tid == 0) {
-    const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(Np >> 3) << 17) | ((uint32_t)(TQ >> 4) << 24);
-    const uint64_t ad = desc(su32(sQ), 128, 256), bd = desc(su32(sK), 128, 256);
-    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-                 "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem),
-                 "l"(ad), "l"(bd), "r"(idesc), "r"(0u));
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(&mbar))
-                 : "memory");
-  }
-  mbar_wait_parity(&mbar, 0);
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  // softmax of row tid over the nk valid columns (TMEM lanes 32 * warp .. belong to this warp)
-  const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
-  float mx = -INFINITY;
-  for (int c0 = 0; c0 < Np; c0 += 16) {
-    float x[16];
-    tmem_ld16(trow + c0, x);
-#pragma unroll
-    for (int j = 0; j < 16; j++)
-      if (c0 + j < nk) mx = fmaxf(mx, x[j] * kScaleTc);
-  }
-  float sum = 0.f;
-  for (int c0 = 0; c0 < TKEY; c0 += 16) {
-    float x[16];
-    if (c0 < Np) tmem_ld16(trow + c0, x);
-    float p[16];
-#pragma unroll
-    for (int j = 0; j < 16; j++) {
-      p[j] = (c0 + j < nk) ? __expf(x[j] * kScaleTc - mx) : 0.f;
-      sum += p[j];
-    }
-    *reinterpret_cast<uint4 *>(sP + coff(tid, c0, TKEY)) =
-        make_uint4(pack2(p[0], p[1]), pack2(p[2], p[3]), pack2(p[4], p[5]), pack2(p[6], p[7]));
-    *reinterpret_cast<uint4 *>(sP + coff(tid, c0 + 8, TKEY)) =
-        make_uint4(pack2(p[8], p[9]), pack2(p[10], p[11]), pack2(p[12], p[13]), pack2(p[14], p[15]));
-  }
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();   // every row's S has been read and P written
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  // O = P V: M = 128, N = 16, K = 256 keys (16 steps), into TMEM columns 0..15
-  if (tid == 0) {
-    const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(16 >> 3) << 17) | ((uint32_t)(TQ >> 4) << 24);
-    const uint32_t sbo = (TKEY >> 3) * 128;
-    for (int ks = 0; ks < TKEY / 16; ks++) {
-      const uint64_t ad = desc(su32(sP) + ks * 256, 128, sbo), bd = desc(su32(sV) + ks * 256, 128, sbo);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();   // (also: the previous block's P V has been drained by every warp)
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = tmem_base;
+    const uint32_t trow = tmem + trow_off;
+    // S = Q K^T: M = 128, N = Np, K = 16
+    if (tid == 0) {
+      const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(Np >> 3) << 17) | ((uint32_t)(TQ >> 4) << 24);
+      const uint64_t ad = desc(su32(sQ), 128, 256), bd = desc(su32(sK), 128, 256);
       asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
                    "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem),
-                   "l"(ad), "l"(bd), "r"(idesc), "r"(ks > 0 ? 1u : 0u));
+                   "l"(ad), "l"(bd), "r"(idesc), "r"(0u));
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(&mbar))
+                   : "memory");
     }
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(&mbar))
-                 : "memory");
+    mbar_wait_parity(&mbar, phase);
+    phase ^= 1u;
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    // row max of this block, rescale of the running sum and output, P = exp(S / 4 - max)
+    float bm = -INFINITY;
+    for (int c0 = 0; c0 < Np; c0 += 16) {
+      float x[16];
+      tmem_ld16(trow + c0, x);
+#pragma unroll
+      for (int j = 0; j < 16; j++)
+        if (c0 + j < nk) bm = fmaxf(bm, x[j] * kScaleTc);
+    }
+    const float nm = fmaxf(mx, bm);
+    const float alpha = __expf(mx - nm);   // 0 on the first block (mx = -inf)
+    sum *= alpha;
+#pragma unroll
+    for (int c = 0; c < 16; c++) acc[c] *= alpha;
+    mx = nm;
+    for (int c0 = 0; c0 < TKEY; c0 += 16) {
+      float x[16];
+      if (c0 < Np) tmem_ld16(trow + c0, x);
+      float p[16];
+#pragma unroll
+      for (int j = 0; j < 16; j++) {
+        p[j] = (c0 + j < nk) ? __expf(x[j] * kScaleTc - mx) : 0.f;
+        sum += p[j];
+      }
+      *reinterpret_cast<uint4 *>(sP + coff(tid, c0, TKEY)) =
+          make_uint4(pack2(p[0], p[1]), pack2(p[2], p[3]), pack2(p[4], p[5]), pack2(p[6], p[7]));
+      *reinterpret_cast<uint4 *>(sP + coff(tid, c0 + 8, TKEY)) =
+          make_uint4(pack2(p[8], p[9]), pack2(p[10], p[11]), pack2(p[12], p[13]), pack2(p[14], p[15]));
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();   // every row's S has been read and P written
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    // P V: M = 128, N = 16, K = 256 keys (16 steps), into TMEM columns 0..15
+    if (tid == 0) {
+      const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(16 >> 3) << 17) | ((uint32_t)(TQ >> 4) << 24);
+      const uint32_t sbo = (TKEY >> 3) * 128;
+      for (int ks = 0; ks < Np / 16; ks++) {
+        const uint64_t ad = desc(su32(sP) + ks * 256, 128, sbo), bd = desc(su32(sV) + ks * 256, 128, sbo);
+        asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                     "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem),
+                     "l"(ad), "l"(bd), "r"(idesc), "r"(ks > 0 ? 1u : 0u));
+      }
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(&mbar))
+                   : "memory");
+    }
+    mbar_wait_parity(&mbar, phase);
+    phase ^= 1u;
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    {
+      float x[16];
+      tmem_ld16(trow, x);
+#pragma unroll
+      for (int c = 0; c < 16; c++) acc[c] += x[c];
+    }
   }
-  mbar_wait_parity(&mbar, 1);
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   {
-    float x[16];
-    tmem_ld16(trow, x);
     const int i = q0 + tid;
     if (i < q1) {
       const float inv = 1.f / sum;
       float4 *dst = reinterpret_cast<float4 *>(o + (size_t)i * kH + hd * 16);
 #pragma unroll
-      for (int t = 0; t < 4; t++) dst[t] = make_float4(x[4 * t] * inv, x[4 * t + 1] * inv, x[4 * t + 2] * inv, x[4 * t + 3] * inv);
+      for (int t = 0; t < 4; t++)
+        dst[t] = make_float4(acc[4 * t] * inv, acc[4 * t + 1] * inv, acc[4 * t + 2] * inv, acc[4 * t + 3] * inv);
       lse[(size_t)i * kHeads + hd] = mx + logf(sum);
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
-  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256));
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(256));
 }
-
 
 // Backward of the same tile (M <= S, so every key has at most one memory contribution, from the
 // next segment): one CTA per (segment tau, head h), thread = query row.
@@ -413,7 +435,7 @@ __global__ void __launch_bounds__(TQ, 1) k_attn_bwd_tc(const float *__restrict__
 
 }  // namespace
 
-bool attn_fwd_tc_eligible(int S, int M) { return S >= 1 && S <= TQ && M >= 0 && (long long)M + S <= TKEY; }
+bool attn_fwd_tc_eligible(int S, int M) { return S >= 1 && S <= TQ && M >= -1; }
 bool attn_bwd_tc_eligible(int S, int M) { return S >= 1 && S <= TQ && M >= 0 && M <= S; }
 
 void launch_attn_bwd_tc(const float *qkv, const float *o, const float *lse, const float *dout, float *dqkv,

@@ -357,15 +357,19 @@ def test_tensor_core_mode(gdp, case):
     assert cos > 0.98 and abs(ratio - 1) < 0.15, ("grad", cos, ratio)   # measured: c2 0.990 / 0.906
 
 
-@pytest.mark.parametrize("case", ["c1", "seg", "short_mem", "ragged"])
+@pytest.mark.parametrize("case", ["c1", "seg", "short_mem", "ragged", "mem_inf", "long_mem"])
 def test_tensor_core_attention_matches_simt(gdp, case, monkeypatch):
     """The tcgen05 attention tiles (forward k_attn_fwd_tc, backward k_attn_bwd_tc) against the
     SIMT kernels inside the same tensor-core-mode step (GDP_ATTN_SIMT=1 switches them off):
-    logits within the bf16 tolerance, the gradient along the same direction (bf16 P and dS)."""
+    logits within the bf16 tolerance, the gradient along the same direction (bf16 P and dS).
+    mem_inf / long_mem: more than 256 keys per segment (several key blocks in the forward; the
+    backward of M > S stays on SIMT)."""
     g, d, S, M = {"c1": (workloads.config("c1").graphs[0], 2, 32, 32),
                   "seg": (workloads.random_dag(900, p_edge=0.05, max_back=60, seed=31), 4, 128, 128),
                   "short_mem": (workloads.random_dag(1000, p_edge=0.05, max_back=60, seed=32), 8, 100, 60),
-                  "ragged": (workloads.random_dag(517, p_edge=0.08, max_back=40, seed=33), 4, 64, 64)}[case]
+                  "ragged": (workloads.random_dag(517, p_edge=0.08, max_back=40, seed=33), 4, 64, 64),
+                  "mem_inf": (workloads.random_dag(1100, p_edge=0.05, max_back=60, seed=34), 4, 128, -1),
+                  "long_mem": (workloads.random_dag(900, p_edge=0.05, max_back=60, seed=35), 4, 80, 300)}[case]
     th = workloads.init_theta(workloads.F, d, seed=13, mode="random")
     B = 16
     monkeypatch.setenv("GDP_ATTN_SIMT", "1")
