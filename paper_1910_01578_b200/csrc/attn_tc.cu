@@ -433,10 +433,340 @@ __global__ void __launch_bounds__(TQ, 1) k_attn_bwd_tc(const float *__restrict__
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
 }
 
+// ---------------------------------------------------------------- backward, M > S (M = inf too)
+// A key of segment sigma then receives memory contributions from several later query segments,
+// so the backward splits into a query-major dQ pass and a key-major dK / dV pass (as the SIMT
+// k_attn_bwd_dq / _dkv), each on tcgen05 with 128 x 128 (query x key) tiles:
+//   k_attn_bwd_dq_tc  (segment tau, head h), thread = query row, per 128-key block:
+//     S = Q K^T and dP = dO V^T into TMEM columns [0, 128) / [128, 256); p = exp(S/4 - LSE),
+//     dS = p (dP - D) / 4 as bf16 to shared memory; dQ_block = dS K (M = 128, N = 16,
+//     K = keys) into TMEM columns [0, 16), summed over blocks in fp32 registers.
+//   k_attn_bwd_dkv_tc (segment sigma, head h), thread = key row, per query segment tau >= sigma
+//     whose key range reaches the block: S^T = K Q^T and dP^T = V dO^T (M = 128 keys, N = queries),
+//     P^T and dS^T as bf16, dK_tau = dS^T Q and dV_tau = P^T dO (M = 128 keys, N = 16, K = queries)
+//     into TMEM columns [0, 32).  tau == sigma is the own contribution (dqkv[:, 64:192]); the
+//     later segments' are summed in fp32 registers into the memory rows dkvm[:, 0:128]
+//     (stop-gradient for x), zeros where no later segment reaches the key.  Every output row is
+//     written exactly once, no atomics.
+__device__ __forceinline__ void st_row16(unsigned char *tile, int r, const float *f) {   // K-major row, Kp = 16
+  *reinterpret_cast<uint4 *>(tile + coff(r, 0, 16)) =
+      make_uint4(pack2(f[0], f[1]), pack2(f[2], f[3]), pack2(f[4], f[5]), pack2(f[6], f[7]));
+  *reinterpret_cast<uint4 *>(tile + coff(r, 8, 16)) =
+      make_uint4(pack2(f[8], f[9]), pack2(f[10], f[11]), pack2(f[12], f[13]), pack2(f[14], f[15]));
+}
+__device__ __forceinline__ void st_col16(unsigned char *tile, int r, const float *f) {   // transposed, Kp = 128
+#pragma unroll
+  for (int c = 0; c < 16; c++) *reinterpret_cast<__nv_bfloat16 *>(tile + coff(c, r, TQ)) = __float2bfloat16_rn(f[c]);
+}
+__device__ __forceinline__ void ld16(const float *p, float *f) {
+#pragma unroll
+  for (int t = 0; t < 4; t++) {
+    const float4 a = reinterpret_cast<const float4 *>(p)[t];
+    f[4 * t] = a.x; f[4 * t + 1] = a.y; f[4 * t + 2] = a.z; f[4 * t + 3] = a.w;
+  }
+}
+__device__ __forceinline__ void mma_f16(uint32_t tmem, uint64_t ad, uint64_t bd, uint32_t idesc, uint32_t accum) {
+  asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+               "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem),
+               "l"(ad), "l"(bd), "r"(idesc), "r"(accum));
+}
+__device__ __forceinline__ void mma_commit(uint64_t *mb) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(mb))
+               : "memory");
+}
+__device__ __forceinline__ void sync_for_mma() {   // generic-proxy smem writes / TMEM reads -> MMA
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t idesc_f16(int n) {   // bf16 x bf16 -> fp32, M = 128, K-major A and B
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(TQ >> 4) << 24);
+}
+constexpr uint32_t kSbo128 = (TQ >> 3) * 128;   // next 8-row group of a K-major tile with 128 columns
+
+__global__ void __launch_bounds__(TQ, 2) k_attn_bwd_dq_tc(const float *__restrict__ qkv, const float *__restrict__ o,
+                                                         const float *__restrict__ lse,
+                                                         const float *__restrict__ dout, float *dqkv, int N, int S,
+                                                         int M) {
+  extern __shared__ __align__(1024) unsigned char sm[];
+  __shared__ __align__(8) uint64_t mbar;
+  __shared__ uint32_t tmem_base;
+  unsigned char *sQ = sm;                 // 128 x 16 (A of S)
+  unsigned char *sdO = sQ + TQ * 32;      // 128 x 16 (A of dP)
+  unsigned char *sK = sdO + TQ * 32;      // 128 keys x 16 (B of S)
+  unsigned char *sV = sK + TQ * 32;       // 128 keys x 16 (B of dP)
+  unsigned char *sKt = sV + TQ * 32;      // 16 x 128 keys (B of dQ)
+  unsigned char *sdS = sKt + TQ * 32;     // 128 queries x 128 keys (A of dQ)
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const int tau = gridDim.x - 1 - blockIdx.x, hd = blockIdx.y;   // longest key ranges first
+  const int q0 = tau * S, q1 = min(N, q0 + S);
+  const int lo = M < 0 ? 0 : max(0, q0 - M), hi = q1;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(&tmem_base)), "r"(256));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::);
+  }
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&mbar)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  const int i = q0 + tid;
+  const bool qv = i < q1;
+  float L = 0.f, D = 0.f;
+  {
+    float qf[16] = {}, gf[16] = {}, of[16] = {};
+    if (qv) {
+      ld16(qkv + (size_t)i * 192 + hd * 16, qf);
+      ld16(dout + (size_t)i * kH + hd * 16, gf);
+      ld16(o + (size_t)i * kH + hd * 16, of);
+      L = lse[(size_t)i * kHeads + hd];
+#pragma unroll
+      for (int c = 0; c < 16; c++) D = fmaf(gf[c], of[c], D);
+    }
+    st_row16(sQ, tid, qf);
+    st_row16(sdO, tid, gf);
+  }
+  const uint32_t trow_off = (uint32_t)(warp * 32) << 16;
+  float acc[16];
+#pragma unroll
+  for (int c = 0; c < 16; c++) acc[c] = 0.f;
+  uint32_t phase = 0;
+  for (int kb = lo; kb < hi; kb += TQ) {
+    const int nk = min(TQ, hi - kb), Np = (nk + 15) & ~15;
+    {
+      float kf[16] = {}, vf[16] = {};
+      if (tid < nk) {
+        ld16(qkv + (size_t)(kb + tid) * 192 + 64 + hd * 16, kf);
+        ld16(qkv + (size_t)(kb + tid) * 192 + 128 + hd * 16, vf);
+      }
+      st_row16(sK, tid, kf);
+      st_row16(sV, tid, vf);
+      st_col16(sKt, tid, kf);
+    }
+    sync_for_mma();   // (also: the previous block's dQ has been drained by every warp)
+    const uint32_t tmem = tmem_base, trow = tmem + trow_off;
+    if (tid == 0) {
+      mma_f16(tmem, desc(su32(sQ), 128, 256), desc(su32(sK), 128, 256), idesc_f16(Np), 0u);
+      mma_f16(tmem + 128u, desc(su32(sdO), 128, 256), desc(su32(sV), 128, 256), idesc_f16(Np), 0u);
+      mma_commit(&mbar);
+    }
+    mbar_wait_parity(&mbar, phase);
+    phase ^= 1u;
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    for (int c0 = 0; c0 < TQ; c0 += 16) {
+      float sx[16], dpx[16], ds[16];
+      if (c0 < Np) {
+        tmem_ld16(trow + c0, sx);
+        tmem_ld16(trow + 128 + c0, dpx);
+      }
+#pragma unroll
+      for (int jj = 0; jj < 16; jj++) {
+        const bool kv = qv && c0 + jj < nk;
+        const float p = kv ? __expf(sx[jj] * kScaleTc - L) : 0.f;
+        ds[jj] = kv ? p * (dpx[jj] - D) * kScaleTc : 0.f;
+      }
+      *reinterpret_cast<uint4 *>(sdS + coff(tid, c0, TQ)) =
+          make_uint4(pack2(ds[0], ds[1]), pack2(ds[2], ds[3]), pack2(ds[4], ds[5]), pack2(ds[6], ds[7]));
+      *reinterpret_cast<uint4 *>(sdS + coff(tid, c0 + 8, TQ)) =
+          make_uint4(pack2(ds[8], ds[9]), pack2(ds[10], ds[11]), pack2(ds[12], ds[13]), pack2(ds[14], ds[15]));
+    }
+    sync_for_mma();   // every row's S / dP read, dS written
+    if (tid == 0) {   // dQ_block = dS K: M = 128, N = 16, K = Np keys
+      for (int ks = 0; ks < Np / 16; ks++)
+        mma_f16(tmem, desc(su32(sdS) + ks * 256, 128, kSbo128), desc(su32(sKt) + ks * 256, 128, kSbo128),
+                idesc_f16(16), ks > 0 ? 1u : 0u);
+      mma_commit(&mbar);
+    }
+    mbar_wait_parity(&mbar, phase);
+    phase ^= 1u;
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    {
+      float x[16];
+      tmem_ld16(trow, x);
+#pragma unroll
+      for (int c = 0; c < 16; c++) acc[c] += x[c];
+    }
+  }
+  if (qv) {
+    float4 *dst = reinterpret_cast<float4 *>(dqkv + (size_t)i * 192 + hd * 16);
+#pragma unroll
+    for (int t = 0; t < 4; t++) dst[t] = make_float4(acc[4 * t], acc[4 * t + 1], acc[4 * t + 2], acc[4 * t + 3]);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(256));
+}
+
+__global__ void __launch_bounds__(TQ, 2) k_attn_bwd_dkv_tc(const float *__restrict__ qkv, const float *__restrict__ o,
+                                                          const float *__restrict__ lse,
+                                                          const float *__restrict__ dout, float *dqkv, float *dkvm,
+                                                          int N, int S, int M, int nseg) {
+  extern __shared__ __align__(1024) unsigned char sm[];
+  __shared__ __align__(8) uint64_t mbar;
+  __shared__ uint32_t tmem_base;
+  __shared__ float sL[TQ], sD[TQ];
+  unsigned char *sK = sm;                 // 128 keys x 16 (A of S^T)
+  unsigned char *sV = sK + TQ * 32;       // 128 keys x 16 (A of dP^T)
+  unsigned char *sQ = sV + TQ * 32;       // 128 queries x 16 (B of S^T)
+  unsigned char *sdO = sQ + TQ * 32;      // 128 queries x 16 (B of dP^T)
+  unsigned char *sQt = sdO + TQ * 32;     // 16 x 128 queries (B of dK)
+  unsigned char *sdOt = sQt + TQ * 32;    // 16 x 128 queries (B of dV)
+  unsigned char *sPt = sdOt + TQ * 32;    // 128 keys x 128 queries (A of dV)
+  unsigned char *sdSt = sPt + TQ * TQ * 2;   // 128 keys x 128 queries (A of dK)
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const int sig = blockIdx.x, hd = blockIdx.y;   // sigma = 0 has the most query segments: first
+  const int k0 = sig * S, k1 = min(N, k0 + S), nk = k1 - k0;
+  const int tau_hi = M < 0 ? nseg - 1 : min(nseg - 1, (int)(((long long)k1 - 1 + M) / S));
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(&tmem_base)), "r"(256));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::);
+  }
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&mbar)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  const int j = k0 + tid;
+  const bool kvalid = tid < nk;
+  {
+    float kf[16] = {}, vf[16] = {};
+    if (kvalid) {
+      ld16(qkv + (size_t)j * 192 + 64 + hd * 16, kf);
+      ld16(qkv + (size_t)j * 192 + 128 + hd * 16, vf);
+    }
+    st_row16(sK, tid, kf);
+    st_row16(sV, tid, vf);
+  }
+  const uint32_t trow_off = (uint32_t)(warp * 32) << 16;
+  float dkm[16], dvm[16];
+#pragma unroll
+  for (int c = 0; c < 16; c++) dkm[c] = dvm[c] = 0.f;
+  uint32_t phase = 0;
+  for (int tau = sig; tau <= tau_hi; tau++) {
+    const int q0 = tau * S, q1 = min(N, q0 + S), nq = q1 - q0, Nqp = (nq + 15) & ~15;
+    const int lo = M < 0 ? 0 : max(0, q0 - M);
+    const bool inr = kvalid && j >= lo;
+    {
+      const int i = q0 + tid;
+      float qf[16] = {}, gf[16] = {}, of[16] = {};
+      float L = 0.f, D = 0.f;
+      if (tid < nq) {
+        ld16(qkv + (size_t)i * 192 + hd * 16, qf);
+        ld16(dout + (size_t)i * kH + hd * 16, gf);
+        ld16(o + (size_t)i * kH + hd * 16, of);
+        L = lse[(size_t)i * kHeads + hd];
+#pragma unroll
+        for (int c = 0; c < 16; c++) D = fmaf(gf[c], of[c], D);
+      }
+      st_row16(sQ, tid, qf);
+      st_row16(sdO, tid, gf);
+      st_col16(sQt, tid, qf);
+      st_col16(sdOt, tid, gf);
+      sL[tid] = L;
+      sD[tid] = D;
+    }
+    sync_for_mma();   // (also: the previous segment's dK / dV have been drained by every warp)
+    const uint32_t tmem = tmem_base, trow = tmem + trow_off;
+    if (tid == 0) {   // S^T = K Q^T -> cols [0, Nqp); dP^T = V dO^T -> cols [128, 128 + Nqp)
+      mma_f16(tmem, desc(su32(sK), 128, 256), desc(su32(sQ), 128, 256), idesc_f16(Nqp), 0u);
+      mma_f16(tmem + 128u, desc(su32(sV), 128, 256), desc(su32(sdO), 128, 256), idesc_f16(Nqp), 0u);
+      mma_commit(&mbar);
+    }
+    mbar_wait_parity(&mbar, phase);
+    phase ^= 1u;
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    for (int c0 = 0; c0 < Nqp; c0 += 16) {
+      float sx[16], dpx[16], p[16], ds[16];
+      tmem_ld16(trow + c0, sx);
+      tmem_ld16(trow + 128 + c0, dpx);
+#pragma unroll
+      for (int qq = 0; qq < 16; qq++) {
+        const int q = c0 + qq;
+        const bool v = inr && q < nq;
+        p[qq] = v ? __expf(sx[qq] * kScaleTc - sL[q]) : 0.f;
+        ds[qq] = v ? p[qq] * (dpx[qq] - sD[q]) * kScaleTc : 0.f;
+      }
+      *reinterpret_cast<uint4 *>(sPt + coff(tid, c0, TQ)) =
+          make_uint4(pack2(p[0], p[1]), pack2(p[2], p[3]), pack2(p[4], p[5]), pack2(p[6], p[7]));
+      *reinterpret_cast<uint4 *>(sPt + coff(tid, c0 + 8, TQ)) =
+          make_uint4(pack2(p[8], p[9]), pack2(p[10], p[11]), pack2(p[12], p[13]), pack2(p[14], p[15]));
+      *reinterpret_cast<uint4 *>(sdSt + coff(tid, c0, TQ)) =
+          make_uint4(pack2(ds[0], ds[1]), pack2(ds[2], ds[3]), pack2(ds[4], ds[5]), pack2(ds[6], ds[7]));
+      *reinterpret_cast<uint4 *>(sdSt + coff(tid, c0 + 8, TQ)) =
+          make_uint4(pack2(ds[8], ds[9]), pack2(ds[10], ds[11]), pack2(ds[12], ds[13]), pack2(ds[14], ds[15]));
+    }
+    sync_for_mma();   // S^T / dP^T consumed, P^T and dS^T written
+    if (tid == 0) {   // dK = dS^T Q -> cols [0, 16); dV = P^T dO -> cols [16, 32); K = Nqp queries
+      for (int ks = 0; ks < Nqp / 16; ks++) {
+        mma_f16(tmem, desc(su32(sdSt) + ks * 256, 128, kSbo128), desc(su32(sQt) + ks * 256, 128, kSbo128),
+                idesc_f16(16), ks > 0 ? 1u : 0u);
+        mma_f16(tmem + 16u, desc(su32(sPt) + ks * 256, 128, kSbo128), desc(su32(sdOt) + ks * 256, 128, kSbo128),
+                idesc_f16(16), ks > 0 ? 1u : 0u);
+      }
+      mma_commit(&mbar);
+    }
+    mbar_wait_parity(&mbar, phase);
+    phase ^= 1u;
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    float dk[16], dv[16];
+    tmem_ld16(trow, dk);
+    tmem_ld16(trow + 16u, dv);
+    if (tau == sig) {
+      if (kvalid) {
+#pragma unroll
+        for (int t = 0; t < 4; t++) {
+          reinterpret_cast<float4 *>(dqkv + (size_t)j * 192 + 64 + hd * 16)[t] =
+              make_float4(dk[4 * t], dk[4 * t + 1], dk[4 * t + 2], dk[4 * t + 3]);
+          reinterpret_cast<float4 *>(dqkv + (size_t)j * 192 + 128 + hd * 16)[t] =
+              make_float4(dv[4 * t], dv[4 * t + 1], dv[4 * t + 2], dv[4 * t + 3]);
+        }
+      }
+    } else {
+#pragma unroll
+      for (int c = 0; c < 16; c++) { dkm[c] += dk[c]; dvm[c] += dv[c]; }
+    }
+  }
+  if (kvalid) {
+#pragma unroll
+    for (int t = 0; t < 4; t++) {
+      reinterpret_cast<float4 *>(dkvm + (size_t)j * 128 + hd * 16)[t] =
+          make_float4(dkm[4 * t], dkm[4 * t + 1], dkm[4 * t + 2], dkm[4 * t + 3]);
+      reinterpret_cast<float4 *>(dkvm + (size_t)j * 128 + 64 + hd * 16)[t] =
+          make_float4(dvm[4 * t], dvm[4 * t + 1], dvm[4 * t + 2], dvm[4 * t + 3]);
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(256));
+}
+
 }  // namespace
 
 bool attn_fwd_tc_eligible(int S, int M) { return S >= 1 && S <= TQ && M >= -1; }
 bool attn_bwd_tc_eligible(int S, int M) { return S >= 1 && S <= TQ && M >= 0 && M <= S; }
+bool attn_bwd_tc_long_eligible(int S, int M) { return S >= 1 && S <= TQ && (M == -1 || M > S); }
+
+static const size_t kSmemDq = (size_t)5 * TQ * 32 + (size_t)TQ * TQ * 2;         // 52 KB
+static const size_t kSmemDkv = (size_t)6 * TQ * 32 + (size_t)2 * TQ * TQ * 2;    // 88 KB
+void launch_attn_bwd_dq_tc(const float *qkv, const float *o, const float *lse, const float *dout, float *dqkv, int N,
+                           int S, int M, cudaStream_t s) {
+  const int nseg = (N + S - 1) / S;
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(k_attn_bwd_dq_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemDq);
+    configured = true;
+  }
+  k_attn_bwd_dq_tc<<<dim3(nseg, kHeads), TQ, kSmemDq, s>>>(qkv, o, lse, dout, dqkv, N, S, M);
+}
+void launch_attn_bwd_dkv_tc(const float *qkv, const float *o, const float *lse, const float *dout, float *dqkv,
+                            float *dkvm, int N, int S, int M, cudaStream_t s) {
+  const int nseg = (N + S - 1) / S;
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(k_attn_bwd_dkv_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemDkv);
+    configured = true;
+  }
+  k_attn_bwd_dkv_tc<<<dim3(nseg, kHeads), TQ, kSmemDkv, s>>>(qkv, o, lse, dout, dqkv, dkvm, N, S, M, nseg);
+}
 
 void launch_attn_bwd_tc(const float *qkv, const float *o, const float *lse, const float *dout, float *dqkv,
                         float *dkvm, int N, int S, int M, cudaStream_t s) {

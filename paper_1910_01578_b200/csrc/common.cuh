@@ -164,6 +164,11 @@ void launch_attn_fwd_tc(const float *qkv, float *o, float *lse, int N, int S, in
 bool attn_bwd_tc_eligible(int S, int M);
 void launch_attn_bwd_tc(const float *qkv, const float *o, const float *lse, const float *dout, float *dqkv,
                         float *dkvm, int N, int S, int M, cudaStream_t s);
+bool attn_bwd_tc_long_eligible(int S, int M);   // M > S or M = inf: query-major dQ + key-major dK / dV
+void launch_attn_bwd_dq_tc(const float *qkv, const float *o, const float *lse, const float *dout, float *dqkv, int N,
+                           int S, int M, cudaStream_t s);
+void launch_attn_bwd_dkv_tc(const float *qkv, const float *o, const float *lse, const float *dout, float *dqkv,
+                            float *dkvm, int N, int S, int M, cudaStream_t s);
 // ablation variant of the entry point in progress (gdp_config.no_attention)
 void set_no_attention(bool on);
 bool no_attention();

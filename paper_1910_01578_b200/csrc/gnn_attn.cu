@@ -461,6 +461,13 @@ void launch_attn_bwd(const float *qkv, const float *o, const float *lse, const f
     launch_attn_bwd_tc(qkv, o, lse, dout, dqkv, dkvm, N, S, M, s);
     return;
   }
+  if (tensor_cores_on() && attn_bwd_tc_long_eligible(S, M) && !attn_simt_forced()) {   // M > S (attn_tc.cu)
+    note_launch("k_attn_bwd_dq_tc", s, 4.0 * (double)N * (192 + 64 + 64 + kHeads + 64), attn_flops(N, S, M));
+    launch_attn_bwd_dq_tc(qkv, o, lse, dout, dqkv, N, S, M, s);
+    note_launch("k_attn_bwd_dkv_tc", s, 4.0 * (double)N * (192 + 64 + 64 + kHeads + 128 + 128), 1.5 * attn_flops(N, S, M));
+    launch_attn_bwd_dkv_tc(qkv, o, lse, dout, dqkv, dkvm, N, S, M, s);
+    return;
+  }
   note_launch("k_attn_bwd_prep", s);
   k_attn_bwd_prep<<<(N * kHeads + 255) / 256, 256, 0, s>>>(o, dout, Dd, N);
   note_launch("k_attn_bwd_dq", s, 4.0 * (double)N * (192 + 64 + 64 + 2 * kHeads), attn_flops(N, S, M));

@@ -327,7 +327,7 @@ def test_tensor_core_mode(gdp, case):
     tcgen05 (bf16 operands, fp32 accumulation): every stage within the bf16 tolerance of
     BASELINE north_star (rtol 2e-2).  seg_ragged: S = 96, M = 160 (keys 96..256, a ragged last
     segment) on the tensor-core forward tile (its backward, M > S, on SIMT); short_mem: S = 100,
-    M = 60 on both tensor-core tiles; mem_inf_big: M = inf on the SIMT attention."""
+    M = 60 on both tensor-core tiles; mem_inf_big: M = inf (forward with several key blocks, backward k_attn_bwd_dq_tc + _dkv_tc)."""
     if case == "c2":
         W = workloads.config("c2")
         g, d, S, M = W.graphs[0], W.d, W.seg_len, W.mem_len
@@ -363,7 +363,7 @@ def test_tensor_core_attention_matches_simt(gdp, case, monkeypatch):
     SIMT kernels inside the same tensor-core-mode step (GDP_ATTN_SIMT=1 switches them off):
     logits within the bf16 tolerance, the gradient along the same direction (bf16 P and dS).
     mem_inf / long_mem: more than 256 keys per segment (several key blocks in the forward; the
-    backward of M > S stays on SIMT)."""
+    backward of M > S on k_attn_bwd_dq_tc + k_attn_bwd_dkv_tc)."""
     g, d, S, M = {"c1": (workloads.config("c1").graphs[0], 2, 32, 32),
                   "seg": (workloads.random_dag(900, p_edge=0.05, max_back=60, seed=31), 4, 128, 128),
                   "short_mem": (workloads.random_dag(1000, p_edge=0.05, max_back=60, seed=32), 8, 100, 60),
