@@ -292,7 +292,7 @@ def test_step_determinism(gdp):
 @pytest.mark.slow
 def test_full_size_c4_chain(gdp):
     """BASELINE configs[3] at full size in the bench's launch configuration (B = 8 of the
-    headline 256 for the oracle's sake): embed, place, sampled placements, costs, gradient."""
+    headline 296 for the oracle's sake): embed, place, sampled placements, costs, gradient."""
     W = workloads.config("c4")
     g = W.graphs[0]
     th = workloads.init_theta(workloads.F, W.d, seed=7, mode="default")
