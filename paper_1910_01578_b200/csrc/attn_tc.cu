@@ -62,6 +62,45 @@ __device__ __forceinline__ uint32_t pack2(float a, float b) {
   __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
   return *reinterpret_cast<uint32_t *>(&h);
 }
+// TMEM loads issued back to back with one wait: tmem_ld16_nw, then tmem_wait_ld, then
+// reg_fence16 on each destination (an empty volatile asm that the compiler cannot hoist above
+// the wait, so no use of the registers is scheduled before the data has landed).
+__device__ __forceinline__ void tmem_ld16_nw(uint32_t taddr, uint32_t *v) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
+        "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void reg_fence16(uint32_t *v) {
+  asm volatile(""
+               : "+r"(v[0]), "+r"(v[1]), "+r"(v[2]), "+r"(v[3]), "+r"(v[4]), "+r"(v[5]), "+r"(v[6]), "+r"(v[7]),
+                 "+r"(v[8]), "+r"(v[9]), "+r"(v[10]), "+r"(v[11]), "+r"(v[12]), "+r"(v[13]), "+r"(v[14]), "+r"(v[15]));
+}
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// K / V rows j and j + 128 of one key block (fp32, 16 floats each) into registers
+__device__ __forceinline__ void ld_kv(const float *__restrict__ qkv, int kb, int nk, int j0, int hd, float4 (&kk)[2][4],
+                                      float4 (&vv)[2][4]) {
+#pragma unroll
+  for (int h2 = 0; h2 < 2; h2++) {
+    const int j = j0 + h2 * TQ;
+#pragma unroll
+    for (int t = 0; t < 4; t++) kk[h2][t] = vv[h2][t] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (j < nk) {
+      const float4 *pk = reinterpret_cast<const float4 *>(qkv + (size_t)(kb + j) * 192 + 64 + hd * 16);
+      const float4 *pv = reinterpret_cast<const float4 *>(qkv + (size_t)(kb + j) * 192 + 128 + hd * 16);
+#pragma unroll
+      for (int t = 0; t < 4; t++) { kk[h2][t] = __ldg(pk + t); vv[h2][t] = __ldg(pv + t); }
+    }
+  }
+}
 
 __global__ void __launch_bounds__(TQ, 2) k_attn_fwd_tc(const float *__restrict__ qkv, float *o, float *lse, int N,
                                                       int S, int M) {
@@ -77,6 +116,8 @@ __global__ void __launch_bounds__(TQ, 2) k_attn_fwd_tc(const float *__restrict__
   const int tau = nseg - 1 - blockIdx.x, hd = blockIdx.y;   // longest key ranges first
   const int q0 = tau * S, q1 = min(N, q0 + S);
   const int lo = M < 0 ? 0 : max(0, q0 - M), hi = q1;
+  // scores in log2 units: s2 = S_ij / 4 * log2(e), p = 2^(s2 - m2)
+  const float kC = kScaleTc * 1.4426950408889634f;
 
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(&tmem_base)), "r"(256));
@@ -101,33 +142,32 @@ __global__ void __launch_bounds__(TQ, 2) k_attn_fwd_tc(const float *__restrict__
     *reinterpret_cast<uint4 *>(sQ + coff(tid, 8, 16)) = hi8;
   }
   const uint32_t trow_off = (uint32_t)(warp * 32) << 16;
-  float mx = -INFINITY, sum = 0.f, acc[16];
+  float m2 = -INFINITY, sum = 0.f, acc[16];
 #pragma unroll
   for (int c = 0; c < 16; c++) acc[c] = 0.f;
   uint32_t phase = 0;
+  float4 kk[2][4], vv[2][4];   // the next key block's rows, loaded one block ahead
+  ld_kv(qkv, lo, min(TKEY, hi - lo), tid, hd, kk, vv);
   // online softmax over 256-key blocks (one block when M <= 256 - S, the headline)
   for (int kb = lo; kb < hi; kb += TKEY) {
     const int nk = min(TKEY, hi - kb), Np = (nk + 15) & ~15;
 #pragma unroll
-    for (int h2 = 0; h2 < 2; h2++) {   // K / V rows tid and tid + 128 of this block
-      const int j = tid + h2 * TQ, r = kb + j;
-      float4 kk[4] = {}, vv[4] = {};
-      if (j < nk) {
-        const float4 *pk = reinterpret_cast<const float4 *>(qkv + (size_t)r * 192 + 64 + hd * 16);
-        const float4 *pv = reinterpret_cast<const float4 *>(qkv + (size_t)r * 192 + 128 + hd * 16);
-#pragma unroll
-        for (int t = 0; t < 4; t++) { kk[t] = pk[t]; vv[t] = pv[t]; }
-      }
+    for (int h2 = 0; h2 < 2; h2++) {   // K / V rows tid and tid + 128 of this block -> bf16 tiles
+      const int j = tid + h2 * TQ;
       *reinterpret_cast<uint4 *>(sK + coff(j, 0, 16)) =
-          make_uint4(pack2(kk[0].x, kk[0].y), pack2(kk[0].z, kk[0].w), pack2(kk[1].x, kk[1].y), pack2(kk[1].z, kk[1].w));
+          make_uint4(pack2(kk[h2][0].x, kk[h2][0].y), pack2(kk[h2][0].z, kk[h2][0].w), pack2(kk[h2][1].x, kk[h2][1].y),
+                     pack2(kk[h2][1].z, kk[h2][1].w));
       *reinterpret_cast<uint4 *>(sK + coff(j, 8, 16)) =
-          make_uint4(pack2(kk[2].x, kk[2].y), pack2(kk[2].z, kk[2].w), pack2(kk[3].x, kk[3].y), pack2(kk[3].z, kk[3].w));
-      const float vf[16] = {vv[0].x, vv[0].y, vv[0].z, vv[0].w, vv[1].x, vv[1].y, vv[1].z, vv[1].w,
-                            vv[2].x, vv[2].y, vv[2].z, vv[2].w, vv[3].x, vv[3].y, vv[3].z, vv[3].w};
+          make_uint4(pack2(kk[h2][2].x, kk[h2][2].y), pack2(kk[h2][2].z, kk[h2][2].w), pack2(kk[h2][3].x, kk[h2][3].y),
+                     pack2(kk[h2][3].z, kk[h2][3].w));
+      const float vf[16] = {vv[h2][0].x, vv[h2][0].y, vv[h2][0].z, vv[h2][0].w, vv[h2][1].x, vv[h2][1].y,
+                            vv[h2][1].z, vv[h2][1].w, vv[h2][2].x, vv[h2][2].y, vv[h2][2].z, vv[h2][2].w,
+                            vv[h2][3].x, vv[h2][3].y, vv[h2][3].z, vv[h2][3].w};
 #pragma unroll
       for (int c = 0; c < 16; c++)   // V^T: row = head dim c, column = key j
         *reinterpret_cast<__nv_bfloat16 *>(sV + coff(c, j, TKEY)) = __float2bfloat16_rn(vf[c]);
     }
+    if (kb + TKEY < hi) ld_kv(qkv, kb + TKEY, min(TKEY, hi - kb - TKEY), tid, hd, kk, vv);   // in flight meanwhile
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();   // (also: the previous block's P V has been drained by every warp)
@@ -147,34 +187,75 @@ __global__ void __launch_bounds__(TQ, 2) k_attn_fwd_tc(const float *__restrict__
     mbar_wait_parity(&mbar, phase);
     phase ^= 1u;
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    // row max of this block, rescale of the running sum and output, P = exp(S / 4 - max)
+    // row max of this block (64 columns per TMEM wait), then the rescale of the running sum / output
     float bm = -INFINITY;
-    for (int c0 = 0; c0 < Np; c0 += 16) {
-      float x[16];
-      tmem_ld16(trow + c0, x);
+    if (nk == TKEY) {
+#pragma unroll 1
+      for (int c0 = 0; c0 < TKEY; c0 += 64) {
+        uint32_t x[4][16];
 #pragma unroll
-      for (int j = 0; j < 16; j++)
-        if (c0 + j < nk) bm = fmaxf(bm, x[j] * kScaleTc);
+        for (int u = 0; u < 4; u++) tmem_ld16_nw(trow + c0 + 16 * u, x[u]);
+        tmem_wait_ld();
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+          reg_fence16(x[u]);
+#pragma unroll
+          for (int jj = 0; jj < 16; jj++) bm = fmaxf(bm, __uint_as_float(x[u][jj]));
+        }
+      }
+    } else {
+      for (int c0 = 0; c0 < Np; c0 += 16) {
+        float x[16];
+        tmem_ld16(trow + c0, x);
+#pragma unroll
+        for (int jj = 0; jj < 16; jj++)
+          if (c0 + jj < nk) bm = fmaxf(bm, x[jj]);
+      }
     }
-    const float nm = fmaxf(mx, bm);
-    const float alpha = __expf(mx - nm);   // 0 on the first block (mx = -inf)
+    const float nm2 = fmaxf(m2, bm * kC);   // kC > 0: the max commutes with the scale
+    const float alpha = ex2(m2 - nm2);       // 0 on the first block (m2 = -inf)
     sum *= alpha;
 #pragma unroll
     for (int c = 0; c < 16; c++) acc[c] *= alpha;
-    mx = nm;
-    for (int c0 = 0; c0 < TKEY; c0 += 16) {
-      float x[16];
-      if (c0 < Np) tmem_ld16(trow + c0, x);
-      float p[16];
+    m2 = nm2;
+    // P = 2^(s2 - m2) as bf16 into shared memory, 32 columns per TMEM wait
+    if (nk == TKEY) {
+#pragma unroll 1
+      for (int c0 = 0; c0 < TKEY; c0 += 32) {
+        uint32_t x[2][16];
+        tmem_ld16_nw(trow + c0, x[0]);
+        tmem_ld16_nw(trow + c0 + 16, x[1]);
+        tmem_wait_ld();
 #pragma unroll
-      for (int j = 0; j < 16; j++) {
-        p[j] = (c0 + j < nk) ? __expf(x[j] * kScaleTc - mx) : 0.f;
-        sum += p[j];
+        for (int u = 0; u < 2; u++) {
+          reg_fence16(x[u]);
+          float p[16];
+#pragma unroll
+          for (int jj = 0; jj < 16; jj++) {
+            p[jj] = ex2(fmaf(__uint_as_float(x[u][jj]), kC, -m2));
+            sum += p[jj];
+          }
+          *reinterpret_cast<uint4 *>(sP + coff(tid, c0 + 16 * u, TKEY)) =
+              make_uint4(pack2(p[0], p[1]), pack2(p[2], p[3]), pack2(p[4], p[5]), pack2(p[6], p[7]));
+          *reinterpret_cast<uint4 *>(sP + coff(tid, c0 + 16 * u + 8, TKEY)) =
+              make_uint4(pack2(p[8], p[9]), pack2(p[10], p[11]), pack2(p[12], p[13]), pack2(p[14], p[15]));
+        }
       }
-      *reinterpret_cast<uint4 *>(sP + coff(tid, c0, TKEY)) =
-          make_uint4(pack2(p[0], p[1]), pack2(p[2], p[3]), pack2(p[4], p[5]), pack2(p[6], p[7]));
-      *reinterpret_cast<uint4 *>(sP + coff(tid, c0 + 8, TKEY)) =
-          make_uint4(pack2(p[8], p[9]), pack2(p[10], p[11]), pack2(p[12], p[13]), pack2(p[14], p[15]));
+    } else {
+      for (int c0 = 0; c0 < TKEY; c0 += 16) {
+        float x[16];
+        if (c0 < Np) tmem_ld16(trow + c0, x);
+        float p[16];
+#pragma unroll
+        for (int jj = 0; jj < 16; jj++) {
+          p[jj] = (c0 + jj < nk) ? ex2(fmaf(x[jj], kC, -m2)) : 0.f;
+          sum += p[jj];
+        }
+        *reinterpret_cast<uint4 *>(sP + coff(tid, c0, TKEY)) =
+            make_uint4(pack2(p[0], p[1]), pack2(p[2], p[3]), pack2(p[4], p[5]), pack2(p[6], p[7]));
+        *reinterpret_cast<uint4 *>(sP + coff(tid, c0 + 8, TKEY)) =
+            make_uint4(pack2(p[8], p[9]), pack2(p[10], p[11]), pack2(p[12], p[13]), pack2(p[14], p[15]));
+      }
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -211,7 +292,7 @@ __global__ void __launch_bounds__(TQ, 2) k_attn_fwd_tc(const float *__restrict__
 #pragma unroll
       for (int t = 0; t < 4; t++)
         dst[t] = make_float4(acc[4 * t] * inv, acc[4 * t + 1] * inv, acc[4 * t + 2] * inv, acc[4 * t + 3] * inv);
-      lse[(size_t)i * kHeads + hd] = mx + logf(sum);
+      lse[(size_t)i * kHeads + hd] = m2 * 0.6931471805599453f + logf(sum);
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -512,14 +593,16 @@ __global__ void __launch_bounds__(TQ, 2) k_attn_bwd_dq_tc(const float *__restric
   }
   const int i = q0 + tid;
   const bool qv = i < q1;
-  float L = 0.f, D = 0.f;
+  // L2 = LSE in log2 units (+inf on padding rows, so p = 2^(s2 - L2) = 0 there without a branch)
+  const float kC = kScaleTc * 1.4426950408889634f;
+  float L2 = INFINITY, D = 0.f;
   {
     float qf[16] = {}, gf[16] = {}, of[16] = {};
     if (qv) {
       ld16(qkv + (size_t)i * 192 + hd * 16, qf);
       ld16(dout + (size_t)i * kH + hd * 16, gf);
       ld16(o + (size_t)i * kH + hd * 16, of);
-      L = lse[(size_t)i * kHeads + hd];
+      L2 = lse[(size_t)i * kHeads + hd] * 1.4426950408889634f;
 #pragma unroll
       for (int c = 0; c < 16; c++) D = fmaf(gf[c], of[c], D);
     }
@@ -531,18 +614,22 @@ __global__ void __launch_bounds__(TQ, 2) k_attn_bwd_dq_tc(const float *__restric
 #pragma unroll
   for (int c = 0; c < 16; c++) acc[c] = 0.f;
   uint32_t phase = 0;
+  float kf[16], vf[16];   // the next key block's rows, loaded one block ahead
+  auto ld_kv_row = [&](int kb) {
+#pragma unroll
+    for (int c = 0; c < 16; c++) kf[c] = vf[c] = 0.f;
+    if (kb + tid < hi) {
+      ld16(qkv + (size_t)(kb + tid) * 192 + 64 + hd * 16, kf);
+      ld16(qkv + (size_t)(kb + tid) * 192 + 128 + hd * 16, vf);
+    }
+  };
+  ld_kv_row(lo);
   for (int kb = lo; kb < hi; kb += TQ) {
     const int nk = min(TQ, hi - kb), Np = (nk + 15) & ~15;
-    {
-      float kf[16] = {}, vf[16] = {};
-      if (tid < nk) {
-        ld16(qkv + (size_t)(kb + tid) * 192 + 64 + hd * 16, kf);
-        ld16(qkv + (size_t)(kb + tid) * 192 + 128 + hd * 16, vf);
-      }
-      st_row16(sK, tid, kf);
-      st_row16(sV, tid, vf);
-      st_col16(sKt, tid, kf);
-    }
+    st_row16(sK, tid, kf);
+    st_row16(sV, tid, vf);
+    st_col16(sKt, tid, kf);
+    if (kb + TQ < hi) ld_kv_row(kb + TQ);   // in flight during this block
     sync_for_mma();   // (also: the previous block's dQ has been drained by every warp)
     const uint32_t tmem = tmem_base, trow = tmem + trow_off;
     if (tid == 0) {
@@ -553,17 +640,20 @@ __global__ void __launch_bounds__(TQ, 2) k_attn_bwd_dq_tc(const float *__restric
     mbar_wait_parity(&mbar, phase);
     phase ^= 1u;
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    for (int c0 = 0; c0 < TQ; c0 += 16) {
-      float sx[16], dpx[16], ds[16];
-      if (c0 < Np) {
-        tmem_ld16(trow + c0, sx);
-        tmem_ld16(trow + 128 + c0, dpx);
-      }
+    const bool full = nk == TQ;
+    for (int c0 = 0; c0 < Np; c0 += 16) {
+      uint32_t sx[16], dpx[16];
+      float ds[16];
+      tmem_ld16_nw(trow + c0, sx);
+      tmem_ld16_nw(trow + 128 + c0, dpx);
+      tmem_wait_ld();
+      reg_fence16(sx);
+      reg_fence16(dpx);
 #pragma unroll
       for (int jj = 0; jj < 16; jj++) {
-        const bool kv = qv && c0 + jj < nk;
-        const float p = kv ? __expf(sx[jj] * kScaleTc - L) : 0.f;
-        ds[jj] = kv ? p * (dpx[jj] - D) * kScaleTc : 0.f;
+        const float p = ex2(fmaf(__uint_as_float(sx[jj]), kC, -L2));
+        const float d = p * (__uint_as_float(dpx[jj]) - D) * kScaleTc;
+        ds[jj] = (full || c0 + jj < nk) ? d : 0.f;
       }
       *reinterpret_cast<uint4 *>(sdS + coff(tid, c0, TQ)) =
           make_uint4(pack2(ds[0], ds[1]), pack2(ds[2], ds[3]), pack2(ds[4], ds[5]), pack2(ds[6], ds[7]));
@@ -604,7 +694,7 @@ __global__ void __launch_bounds__(TQ, 2) k_attn_bwd_dkv_tc(const float *__restri
   extern __shared__ __align__(1024) unsigned char sm[];
   __shared__ __align__(8) uint64_t mbar;
   __shared__ uint32_t tmem_base;
-  __shared__ float sL[TQ], sD[TQ];
+  __shared__ __align__(16) float sL[TQ], sD[TQ];
   unsigned char *sK = sm;                 // 128 keys x 16 (A of S^T)
   unsigned char *sV = sK + TQ * 32;       // 128 keys x 16 (A of dP^T)
   unsigned char *sQ = sV + TQ * 32;       // 128 queries x 16 (B of S^T)
@@ -641,29 +731,38 @@ __global__ void __launch_bounds__(TQ, 2) k_attn_bwd_dkv_tc(const float *__restri
 #pragma unroll
   for (int c = 0; c < 16; c++) dkm[c] = dvm[c] = 0.f;
   uint32_t phase = 0;
+  // the next query segment's rows (Q, dO, O, LSE) are loaded one segment ahead
+  float qf[16], gf[16], of[16], Lr = 0.f;
+  auto ld_q_rows = [&](int tau) {
+    const int i = tau * S + tid;
+#pragma unroll
+    for (int c = 0; c < 16; c++) qf[c] = gf[c] = of[c] = 0.f;
+    Lr = INFINITY;
+    if (i < min(N, tau * S + S)) {
+      ld16(qkv + (size_t)i * 192 + hd * 16, qf);
+      ld16(dout + (size_t)i * kH + hd * 16, gf);
+      ld16(o + (size_t)i * kH + hd * 16, of);
+      Lr = lse[(size_t)i * kHeads + hd] * 1.4426950408889634f;
+    }
+  };
+  const float kC = kScaleTc * 1.4426950408889634f;
+  ld_q_rows(sig);
   for (int tau = sig; tau <= tau_hi; tau++) {
     const int q0 = tau * S, q1 = min(N, q0 + S), nq = q1 - q0, Nqp = (nq + 15) & ~15;
     const int lo = M < 0 ? 0 : max(0, q0 - M);
     const bool inr = kvalid && j >= lo;
     {
-      const int i = q0 + tid;
-      float qf[16] = {}, gf[16] = {}, of[16] = {};
-      float L = 0.f, D = 0.f;
-      if (tid < nq) {
-        ld16(qkv + (size_t)i * 192 + hd * 16, qf);
-        ld16(dout + (size_t)i * kH + hd * 16, gf);
-        ld16(o + (size_t)i * kH + hd * 16, of);
-        L = lse[(size_t)i * kHeads + hd];
+      float D = 0.f;
 #pragma unroll
-        for (int c = 0; c < 16; c++) D = fmaf(gf[c], of[c], D);
-      }
+      for (int c = 0; c < 16; c++) D = fmaf(gf[c], of[c], D);
       st_row16(sQ, tid, qf);
       st_row16(sdO, tid, gf);
       st_col16(sQt, tid, qf);
       st_col16(sdOt, tid, gf);
-      sL[tid] = L;
+      sL[tid] = Lr;   // LSE in log2 units, +inf past the segment (p = 0 there)
       sD[tid] = D;
     }
+    if (tau < tau_hi) ld_q_rows(tau + 1);   // in flight during this segment
     sync_for_mma();   // (also: the previous segment's dK / dV have been drained by every warp)
     const uint32_t tmem = tmem_base, trow = tmem + trow_off;
     if (tid == 0) {   // S^T = K Q^T -> cols [0, Nqp); dP^T = V dO^T -> cols [128, 128 + Nqp)
@@ -675,15 +774,25 @@ __global__ void __launch_bounds__(TQ, 2) k_attn_bwd_dkv_tc(const float *__restri
     phase ^= 1u;
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     for (int c0 = 0; c0 < Nqp; c0 += 16) {
-      float sx[16], dpx[16], p[16], ds[16];
-      tmem_ld16(trow + c0, sx);
-      tmem_ld16(trow + 128 + c0, dpx);
+      uint32_t sx[16], dpx[16];
+      float p[16], ds[16];
+      tmem_ld16_nw(trow + c0, sx);
+      tmem_ld16_nw(trow + 128 + c0, dpx);
+      tmem_wait_ld();
+      reg_fence16(sx);
+      reg_fence16(dpx);
 #pragma unroll
-      for (int qq = 0; qq < 16; qq++) {
-        const int q = c0 + qq;
-        const bool v = inr && q < nq;
-        p[qq] = v ? __expf(sx[qq] * kScaleTc - sL[q]) : 0.f;
-        ds[qq] = v ? p[qq] * (dpx[qq] - sD[q]) * kScaleTc : 0.f;
+      for (int q4 = 0; q4 < 16; q4 += 4) {
+        const float4 l4 = *reinterpret_cast<const float4 *>(sL + c0 + q4);
+        const float4 d4 = *reinterpret_cast<const float4 *>(sD + c0 + q4);
+        const float lq[4] = {l4.x, l4.y, l4.z, l4.w}, dq[4] = {d4.x, d4.y, d4.z, d4.w};
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+          const int qq = q4 + u;
+          const float pv = ex2(fmaf(__uint_as_float(sx[qq]), kC, -lq[u]));   // 0 past the segment (L = +inf)
+          p[qq] = inr ? pv : 0.f;
+          ds[qq] = p[qq] * (__uint_as_float(dpx[qq]) - dq[u]) * kScaleTc;
+        }
       }
       *reinterpret_cast<uint4 *>(sPt + coff(tid, c0, TQ)) =
           make_uint4(pack2(p[0], p[1]), pack2(p[2], p[3]), pack2(p[4], p[5]), pack2(p[6], p[7]));
