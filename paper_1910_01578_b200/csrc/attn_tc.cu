@@ -79,6 +79,11 @@ __device__ __forceinline__ void reg_fence16(uint32_t *v) {
                : "+r"(v[0]), "+r"(v[1]), "+r"(v[2]), "+r"(v[3]), "+r"(v[4]), "+r"(v[5]), "+r"(v[6]), "+r"(v[7]),
                  "+r"(v[8]), "+r"(v[9]), "+r"(v[10]), "+r"(v[11]), "+r"(v[12]), "+r"(v[13]), "+r"(v[14]), "+r"(v[15]));
 }
+__device__ __forceinline__ float fmax3(float a, float b, float c) {   // sm_100 three-input max
+  float y;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(y) : "f"(a), "f"(b), "f"(c));
+  return y;
+}
 __device__ __forceinline__ float ex2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -200,7 +205,7 @@ __global__ void __launch_bounds__(TQ, 2) k_attn_fwd_tc(const float *__restrict__
         for (int u = 0; u < 4; u++) {
           reg_fence16(x[u]);
 #pragma unroll
-          for (int jj = 0; jj < 16; jj++) bm = fmaxf(bm, __uint_as_float(x[u][jj]));
+          for (int jj = 0; jj < 16; jj += 2) bm = fmax3(bm, __uint_as_float(x[u][jj]), __uint_as_float(x[u][jj + 1]));
         }
       }
     } else {
@@ -609,6 +614,8 @@ __global__ void __launch_bounds__(TQ, 2) k_attn_bwd_dq_tc(const float *__restric
     st_row16(sQ, tid, qf);
     st_row16(sdO, tid, gf);
   }
+  static_assert(kScaleTc == 0.25f, "the dS scale is folded into the exponent as 2^-2");
+  const float L2q = L2 + 2.f;
   const uint32_t trow_off = (uint32_t)(warp * 32) << 16;
   float acc[16];
 #pragma unroll
@@ -649,11 +656,17 @@ __global__ void __launch_bounds__(TQ, 2) k_attn_bwd_dq_tc(const float *__restric
       tmem_wait_ld();
       reg_fence16(sx);
       reg_fence16(dpx);
+      // dS = p (dP - D) / 4 with the 1/4 folded into the exponent: p / 4 = 2^(s2 - L2 - 2)
+      if (full) {
 #pragma unroll
-      for (int jj = 0; jj < 16; jj++) {
-        const float p = ex2(fmaf(__uint_as_float(sx[jj]), kC, -L2));
-        const float d = p * (__uint_as_float(dpx[jj]) - D) * kScaleTc;
-        ds[jj] = (full || c0 + jj < nk) ? d : 0.f;
+        for (int jj = 0; jj < 16; jj++)
+          ds[jj] = ex2(fmaf(__uint_as_float(sx[jj]), kC, -L2q)) * (__uint_as_float(dpx[jj]) - D);
+      } else {
+#pragma unroll
+        for (int jj = 0; jj < 16; jj++) {
+          const float d = ex2(fmaf(__uint_as_float(sx[jj]), kC, -L2q)) * (__uint_as_float(dpx[jj]) - D);
+          ds[jj] = c0 + jj < nk ? d : 0.f;
+        }
       }
       *reinterpret_cast<uint4 *>(sdS + coff(tid, c0, TQ)) =
           make_uint4(pack2(ds[0], ds[1]), pack2(ds[2], ds[3]), pack2(ds[4], ds[5]), pack2(ds[6], ds[7]));
@@ -742,7 +755,7 @@ __global__ void __launch_bounds__(TQ, 2) k_attn_bwd_dkv_tc(const float *__restri
       ld16(qkv + (size_t)i * 192 + hd * 16, qf);
       ld16(dout + (size_t)i * kH + hd * 16, gf);
       ld16(o + (size_t)i * kH + hd * 16, of);
-      Lr = lse[(size_t)i * kHeads + hd] * 1.4426950408889634f;
+      Lr = lse[(size_t)i * kHeads + hd];   // scaled to log2 units at its use, so the load stays in flight
     }
   };
   const float kC = kScaleTc * 1.4426950408889634f;
@@ -759,7 +772,7 @@ __global__ void __launch_bounds__(TQ, 2) k_attn_bwd_dkv_tc(const float *__restri
       st_row16(sdO, tid, gf);
       st_col16(sQt, tid, qf);
       st_col16(sdOt, tid, gf);
-      sL[tid] = Lr;   // LSE in log2 units, +inf past the segment (p = 0 there)
+      sL[tid] = Lr * 1.4426950408889634f;   // LSE in log2 units, +inf past the segment (p = 0 there)
       sD[tid] = D;
     }
     if (tau < tau_hi) ld_q_rows(tau + 1);   // in flight during this segment
