@@ -1,18 +1,20 @@
 // tcgen05 tensor-core tiles of the segment attention (a7) for the
 // tensor-core mode (bf16 operands, fp32 accumulation in TMEM), segments of S <= 128 queries.
-// Forward: any memory length (M = inf included), online softmax over 256-key blocks.
+// Forward: any memory length (M = inf included), online softmax over 128-key blocks.
 //
-// One CTA (4 warps, thread = query row) per (segment tau, head h):
+// One CTA (4 warps, thread = query row) per (segment tau, head h), 4 CTAs per SM:
 //   1. Q (128 x 16), K (keys x 16) and V^T (16 x keys) -> bf16 in shared memory, UMMA canonical
-//      K-major SWIZZLE_NONE layout (as in tc_gemm.cu);
-//   2. one `tcgen05.mma.kind::f16` M = 128, N = keys (<= 256), K = 16 gives S = Q K^T in TMEM;
-//   3. each warp drains its 32 TMEM lanes (`tcgen05.ld.32x32b.x16`): row max of S / 4, then
-//      p = exp(S / 4 - max), the row sum in fp32, and P as bf16 back to shared memory;
-//   4. 16 MMAs (K = 16 keys each) give P V in TMEM columns 0..15 (S is consumed by then);
+//      K-major SWIZZLE_NONE layout (as in tc_gemm.cu); the next block's K/V rows are loaded into
+//      registers one block ahead;
+//   2. one `tcgen05.mma.kind::f16` M = 128, N = keys (<= 128), K = 16 gives S = Q K^T in TMEM;
+//   3. each warp drains its 32 TMEM lanes (`tcgen05.ld.32x32b.x16`, several under one wait):
+//      row max of S, then p = 2^(S log2(e) / 4 - m2), the row sum in fp32, and P as bf16 back
+//      to shared memory;
+//   4. 8 MMAs (K = 16 keys each) give P V in TMEM columns 0..15 (S is consumed by then);
 //   5. O = (P V) / sum and LSE = max + log(sum), the same outputs as k_attn_fwd;
-//   with more than 256 keys (M > 256 - S) steps 2-4 repeat per 256-key block with the running
-//   max / sum / output rescaled (flash-attention style; O accumulates in fp32 registers).
-// Memory rows are stop-gradient only for the backward, which stays on k_attn_bwd_* (SIMT).
+//   with more than 128 keys steps 2-4 repeat per 128-key block with the running max / sum /
+//   output rescaled (flash-attention style; O accumulates in fp32 registers).
+// Backward: k_attn_bwd_tc (M <= S), k_attn_bwd_dq_tc + k_attn_bwd_dkv_tc (M > S, M = inf).
 #include <cuda_bf16.h>
 
 #include "common.cuh"
@@ -90,11 +92,15 @@ __device__ __forceinline__ float ex2(float x) {
   return y;
 }
 
-// K / V rows j and j + 128 of one key block (fp32, 16 floats each) into registers
-__device__ __forceinline__ void ld_kv(const float *__restrict__ qkv, int kb, int nk, int j0, int hd, float4 (&kk)[2][4],
-                                      float4 (&vv)[2][4]) {
+// Forward key block: 128 keys, so S needs 128 TMEM columns and the tiles 45 KB of shared memory:
+// 4 CTAs (16 warps) per SM instead of 2 with 256-key blocks.
+constexpr int TKF = 128;
+constexpr int KR = TKF / TQ;   // key rows staged per thread
+// K / V rows j (+ 128 ...) of one key block (fp32, 16 floats each) into registers
+__device__ __forceinline__ void ld_kv(const float *__restrict__ qkv, int kb, int nk, int j0, int hd, float4 (&kk)[KR][4],
+                                      float4 (&vv)[KR][4]) {
 #pragma unroll
-  for (int h2 = 0; h2 < 2; h2++) {
+  for (int h2 = 0; h2 < KR; h2++) {
     const int j = j0 + h2 * TQ;
 #pragma unroll
     for (int t = 0; t < 4; t++) kk[h2][t] = vv[h2][t] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -107,15 +113,15 @@ __device__ __forceinline__ void ld_kv(const float *__restrict__ qkv, int kb, int
   }
 }
 
-__global__ void __launch_bounds__(TQ, 2) k_attn_fwd_tc(const float *__restrict__ qkv, float *o, float *lse, int N,
+__global__ void __launch_bounds__(TQ, 4) k_attn_fwd_tc(const float *__restrict__ qkv, float *o, float *lse, int N,
                                                       int S, int M) {
   extern __shared__ __align__(1024) unsigned char sm[];
   __shared__ __align__(8) uint64_t mbar;
   __shared__ uint32_t tmem_base;
   unsigned char *sQ = sm;                        // 128 x 16 bf16
   unsigned char *sK = sm + TQ * 16 * 2;          // 256 x 16
-  unsigned char *sV = sK + TKEY * 16 * 2;        // V^T: 16 x 256
-  unsigned char *sP = sV + 16 * TKEY * 2;        // 128 x 256
+  unsigned char *sV = sK + TKF * 16 * 2;        // V^T: 16 x 128
+  unsigned char *sP = sV + 16 * TKF * 2;        // 128 x 128
   const int tid = threadIdx.x, warp = tid >> 5;
   const int nseg = gridDim.x;
   const int tau = nseg - 1 - blockIdx.x, hd = blockIdx.y;   // longest key ranges first
@@ -125,7 +131,7 @@ __global__ void __launch_bounds__(TQ, 2) k_attn_fwd_tc(const float *__restrict__
   const float kC = kScaleTc * 1.4426950408889634f;
 
   if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(&tmem_base)), "r"(256));
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(&tmem_base)), "r"((uint32_t)TKF));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::);
   }
   if (tid == 0) {
@@ -151,13 +157,13 @@ __global__ void __launch_bounds__(TQ, 2) k_attn_fwd_tc(const float *__restrict__
 #pragma unroll
   for (int c = 0; c < 16; c++) acc[c] = 0.f;
   uint32_t phase = 0;
-  float4 kk[2][4], vv[2][4];   // the next key block's rows, loaded one block ahead
-  ld_kv(qkv, lo, min(TKEY, hi - lo), tid, hd, kk, vv);
-  // online softmax over 256-key blocks (one block when M <= 256 - S, the headline)
-  for (int kb = lo; kb < hi; kb += TKEY) {
-    const int nk = min(TKEY, hi - kb), Np = (nk + 15) & ~15;
+  float4 kk[KR][4], vv[KR][4];   // the next key block's rows, loaded one block ahead
+  ld_kv(qkv, lo, min(TKF, hi - lo), tid, hd, kk, vv);
+  // online softmax over 128-key blocks
+  for (int kb = lo; kb < hi; kb += TKF) {
+    const int nk = min(TKF, hi - kb), Np = (nk + 15) & ~15;
 #pragma unroll
-    for (int h2 = 0; h2 < 2; h2++) {   // K / V rows tid and tid + 128 of this block -> bf16 tiles
+    for (int h2 = 0; h2 < KR; h2++) {   // K / V rows tid and tid + 128 of this block -> bf16 tiles
       const int j = tid + h2 * TQ;
       *reinterpret_cast<uint4 *>(sK + coff(j, 0, 16)) =
           make_uint4(pack2(kk[h2][0].x, kk[h2][0].y), pack2(kk[h2][0].z, kk[h2][0].w), pack2(kk[h2][1].x, kk[h2][1].y),
@@ -170,9 +176,9 @@ __global__ void __launch_bounds__(TQ, 2) k_attn_fwd_tc(const float *__restrict__
                             vv[h2][3].x, vv[h2][3].y, vv[h2][3].z, vv[h2][3].w};
 #pragma unroll
       for (int c = 0; c < 16; c++)   // V^T: row = head dim c, column = key j
-        *reinterpret_cast<__nv_bfloat16 *>(sV + coff(c, j, TKEY)) = __float2bfloat16_rn(vf[c]);
+        *reinterpret_cast<__nv_bfloat16 *>(sV + coff(c, j, TKF)) = __float2bfloat16_rn(vf[c]);
     }
-    if (kb + TKEY < hi) ld_kv(qkv, kb + TKEY, min(TKEY, hi - kb - TKEY), tid, hd, kk, vv);   // in flight meanwhile
+    if (kb + TKF < hi) ld_kv(qkv, kb + TKF, min(TKF, hi - kb - TKF), tid, hd, kk, vv);   // in flight meanwhile
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();   // (also: the previous block's P V has been drained by every warp)
@@ -194,9 +200,9 @@ __global__ void __launch_bounds__(TQ, 2) k_attn_fwd_tc(const float *__restrict__
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     // row max of this block (64 columns per TMEM wait), then the rescale of the running sum / output
     float bm = -INFINITY;
-    if (nk == TKEY) {
+    if (nk == TKF) {
 #pragma unroll 1
-      for (int c0 = 0; c0 < TKEY; c0 += 64) {
+      for (int c0 = 0; c0 < TKF; c0 += 64) {
         uint32_t x[4][16];
 #pragma unroll
         for (int u = 0; u < 4; u++) tmem_ld16_nw(trow + c0 + 16 * u, x[u]);
@@ -224,9 +230,9 @@ __global__ void __launch_bounds__(TQ, 2) k_attn_fwd_tc(const float *__restrict__
     for (int c = 0; c < 16; c++) acc[c] *= alpha;
     m2 = nm2;
     // P = 2^(s2 - m2) as bf16 into shared memory, 32 columns per TMEM wait
-    if (nk == TKEY) {
+    if (nk == TKF) {
 #pragma unroll 1
-      for (int c0 = 0; c0 < TKEY; c0 += 32) {
+      for (int c0 = 0; c0 < TKF; c0 += 32) {
         uint32_t x[2][16];
         tmem_ld16_nw(trow + c0, x[0]);
         tmem_ld16_nw(trow + c0 + 16, x[1]);
@@ -240,14 +246,14 @@ __global__ void __launch_bounds__(TQ, 2) k_attn_fwd_tc(const float *__restrict__
             p[jj] = ex2(fmaf(__uint_as_float(x[u][jj]), kC, -m2));
             sum += p[jj];
           }
-          *reinterpret_cast<uint4 *>(sP + coff(tid, c0 + 16 * u, TKEY)) =
+          *reinterpret_cast<uint4 *>(sP + coff(tid, c0 + 16 * u, TKF)) =
               make_uint4(pack2(p[0], p[1]), pack2(p[2], p[3]), pack2(p[4], p[5]), pack2(p[6], p[7]));
-          *reinterpret_cast<uint4 *>(sP + coff(tid, c0 + 16 * u + 8, TKEY)) =
+          *reinterpret_cast<uint4 *>(sP + coff(tid, c0 + 16 * u + 8, TKF)) =
               make_uint4(pack2(p[8], p[9]), pack2(p[10], p[11]), pack2(p[12], p[13]), pack2(p[14], p[15]));
         }
       }
     } else {
-      for (int c0 = 0; c0 < TKEY; c0 += 16) {
+      for (int c0 = 0; c0 < TKF; c0 += 16) {
         float x[16];
         if (c0 < Np) tmem_ld16(trow + c0, x);
         float p[16];
@@ -256,9 +262,9 @@ __global__ void __launch_bounds__(TQ, 2) k_attn_fwd_tc(const float *__restrict__
           p[jj] = (c0 + jj < nk) ? ex2(fmaf(x[jj], kC, -m2)) : 0.f;
           sum += p[jj];
         }
-        *reinterpret_cast<uint4 *>(sP + coff(tid, c0, TKEY)) =
+        *reinterpret_cast<uint4 *>(sP + coff(tid, c0, TKF)) =
             make_uint4(pack2(p[0], p[1]), pack2(p[2], p[3]), pack2(p[4], p[5]), pack2(p[6], p[7]));
-        *reinterpret_cast<uint4 *>(sP + coff(tid, c0 + 8, TKEY)) =
+        *reinterpret_cast<uint4 *>(sP + coff(tid, c0 + 8, TKF)) =
             make_uint4(pack2(p[8], p[9]), pack2(p[10], p[11]), pack2(p[12], p[13]), pack2(p[14], p[15]));
       }
     }
@@ -269,7 +275,7 @@ __global__ void __launch_bounds__(TQ, 2) k_attn_fwd_tc(const float *__restrict__
     // P V: M = 128, N = 16, K = 256 keys (16 steps), into TMEM columns 0..15
     if (tid == 0) {
       const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(16 >> 3) << 17) | ((uint32_t)(TQ >> 4) << 24);
-      const uint32_t sbo = (TKEY >> 3) * 128;
+      const uint32_t sbo = (TKF >> 3) * 128;
       for (int ks = 0; ks < Np / 16; ks++) {
         const uint64_t ad = desc(su32(sP) + ks * 256, 128, sbo), bd = desc(su32(sV) + ks * 256, 128, sbo);
         asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
@@ -302,7 +308,7 @@ __global__ void __launch_bounds__(TQ, 2) k_attn_fwd_tc(const float *__restrict__
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
-  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(256));
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"((uint32_t)TKF));
 }
 
 // Backward of the same tile (M <= S, so every key has at most one memory contribution, from the
@@ -904,7 +910,7 @@ void launch_attn_bwd_tc(const float *qkv, const float *o, const float *lse, cons
 
 void launch_attn_fwd_tc(const float *qkv, float *o, float *lse, int N, int S, int M, cudaStream_t s) {
   const int nseg = (N + S - 1) / S;
-  const size_t smem = (size_t)(TQ * 16 + TKEY * 16 + 16 * TKEY + TQ * TKEY) * 2;   // 86 KB
+  const size_t smem = (size_t)(TQ * 16 + TKF * 16 + 16 * TKF + TQ * TKF) * 2;   // 45 KB
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(k_attn_fwd_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
