@@ -577,7 +577,10 @@ __device__ __forceinline__ uint32_t idesc_f16(int n) {   // bf16 x bf16 -> fp32,
 }
 constexpr uint32_t kSbo128 = (TQ >> 3) * 128;   // next 8-row group of a K-major tile with 128 columns
 
-__global__ void __launch_bounds__(TQ, 2) k_attn_bwd_dq_tc(const float *__restrict__ qkv, const float *__restrict__ o,
+// dQ key block: 64 keys, so S and dP take 128 TMEM columns together: 4 CTAs per SM.  The shared
+// tiles keep their 128-key layouts (Kp = 128); only the first 64 rows / K columns are used.
+constexpr int TKQ = 64;
+__global__ void __launch_bounds__(TQ, 4) k_attn_bwd_dq_tc(const float *__restrict__ qkv, const float *__restrict__ o,
                                                          const float *__restrict__ lse,
                                                          const float *__restrict__ dout, float *dqkv, int N, int S,
                                                          int M) {
@@ -595,7 +598,7 @@ __global__ void __launch_bounds__(TQ, 2) k_attn_bwd_dq_tc(const float *__restric
   const int q0 = tau * S, q1 = min(N, q0 + S);
   const int lo = M < 0 ? 0 : max(0, q0 - M), hi = q1;
   if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(&tmem_base)), "r"(256));
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(&tmem_base)), "r"((uint32_t)(2 * TKQ)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::);
   }
   if (tid == 0) {
@@ -631,34 +634,36 @@ __global__ void __launch_bounds__(TQ, 2) k_attn_bwd_dq_tc(const float *__restric
   auto ld_kv_row = [&](int kb) {
 #pragma unroll
     for (int c = 0; c < 16; c++) kf[c] = vf[c] = 0.f;
-    if (kb + tid < hi) {
+    if (tid < TKQ && kb + tid < hi) {
       ld16(qkv + (size_t)(kb + tid) * 192 + 64 + hd * 16, kf);
       ld16(qkv + (size_t)(kb + tid) * 192 + 128 + hd * 16, vf);
     }
   };
   ld_kv_row(lo);
-  for (int kb = lo; kb < hi; kb += TQ) {
-    const int nk = min(TQ, hi - kb), Np = (nk + 15) & ~15;
-    st_row16(sK, tid, kf);
-    st_row16(sV, tid, vf);
-    st_col16(sKt, tid, kf);
-    if (kb + TQ < hi) ld_kv_row(kb + TQ);   // in flight during this block
+  for (int kb = lo; kb < hi; kb += TKQ) {
+    const int nk = min(TKQ, hi - kb), Np = (nk + 15) & ~15;
+    if (tid < TKQ) {
+      st_row16(sK, tid, kf);
+      st_row16(sV, tid, vf);
+      st_col16(sKt, tid, kf);
+    }
+    if (kb + TKQ < hi) ld_kv_row(kb + TKQ);   // in flight during this block
     sync_for_mma();   // (also: the previous block's dQ has been drained by every warp)
     const uint32_t tmem = tmem_base, trow = tmem + trow_off;
     if (tid == 0) {
       mma_f16(tmem, desc(su32(sQ), 128, 256), desc(su32(sK), 128, 256), idesc_f16(Np), 0u);
-      mma_f16(tmem + 128u, desc(su32(sdO), 128, 256), desc(su32(sV), 128, 256), idesc_f16(Np), 0u);
+      mma_f16(tmem + (uint32_t)TKQ, desc(su32(sdO), 128, 256), desc(su32(sV), 128, 256), idesc_f16(Np), 0u);
       mma_commit(&mbar);
     }
     mbar_wait_parity(&mbar, phase);
     phase ^= 1u;
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    const bool full = nk == TQ;
+    const bool full = nk == TKQ;
     for (int c0 = 0; c0 < Np; c0 += 16) {
       uint32_t sx[16], dpx[16];
       float ds[16];
       tmem_ld16_nw(trow + c0, sx);
-      tmem_ld16_nw(trow + 128 + c0, dpx);
+      tmem_ld16_nw(trow + TKQ + c0, dpx);
       tmem_wait_ld();
       reg_fence16(sx);
       reg_fence16(dpx);
@@ -703,7 +708,7 @@ __global__ void __launch_bounds__(TQ, 2) k_attn_bwd_dq_tc(const float *__restric
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
-  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(256));
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"((uint32_t)(2 * TKQ)));
 }
 
 __global__ void __launch_bounds__(TQ, 2) k_attn_bwd_dkv_tc(const float *__restrict__ qkv, const float *__restrict__ o,
