@@ -711,7 +711,13 @@ __global__ void __launch_bounds__(TQ, 4) k_attn_bwd_dq_tc(const float *__restric
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"((uint32_t)(2 * TKQ)));
 }
 
-__global__ void __launch_bounds__(TQ, 2) k_attn_bwd_dkv_tc(const float *__restrict__ qkv, const float *__restrict__ o,
+// dK / dV query chunk: 64 queries, so S^T and dP^T take 128 TMEM columns together and P^T / dS^T
+// 16 KB each (56 KB of shared memory): 3 CTAs per SM instead of 2.  A query segment is staged
+// whole (Q, dO and their transposes) and processed as up to two chunks; the chunks' dK / dV are
+// summed in fp32 registers.
+constexpr int TQC = 64;
+constexpr uint32_t kSbo64 = (TQC >> 3) * 128;   // next 8-row group of a K-major tile with 64 columns
+__global__ void __launch_bounds__(TQ, 3) k_attn_bwd_dkv_tc(const float *__restrict__ qkv, const float *__restrict__ o,
                                                           const float *__restrict__ lse,
                                                           const float *__restrict__ dout, float *dqkv, float *dkvm,
                                                           int N, int S, int M, int nseg) {
@@ -721,18 +727,18 @@ __global__ void __launch_bounds__(TQ, 2) k_attn_bwd_dkv_tc(const float *__restri
   __shared__ __align__(16) float sL[TQ], sD[TQ];
   unsigned char *sK = sm;                 // 128 keys x 16 (A of S^T)
   unsigned char *sV = sK + TQ * 32;       // 128 keys x 16 (A of dP^T)
-  unsigned char *sQ = sV + TQ * 32;       // 128 queries x 16 (B of S^T)
+  unsigned char *sQ = sV + TQ * 32;       // 128 queries x 16 (B of S^T; chunk c from row 64c)
   unsigned char *sdO = sQ + TQ * 32;      // 128 queries x 16 (B of dP^T)
-  unsigned char *sQt = sdO + TQ * 32;     // 16 x 128 queries (B of dK)
+  unsigned char *sQt = sdO + TQ * 32;     // 16 x 128 queries (B of dK; chunk c from column 64c)
   unsigned char *sdOt = sQt + TQ * 32;    // 16 x 128 queries (B of dV)
-  unsigned char *sPt = sdOt + TQ * 32;    // 128 keys x 128 queries (A of dV)
-  unsigned char *sdSt = sPt + TQ * TQ * 2;   // 128 keys x 128 queries (A of dK)
+  unsigned char *sPt = sdOt + TQ * 32;    // 128 keys x 64 queries (A of dV)
+  unsigned char *sdSt = sPt + TQ * TQC * 2;   // 128 keys x 64 queries (A of dK)
   const int tid = threadIdx.x, warp = tid >> 5;
   const int sig = blockIdx.x, hd = blockIdx.y;   // sigma = 0 has the most query segments: first
   const int k0 = sig * S, k1 = min(N, k0 + S), nk = k1 - k0;
   const int tau_hi = M < 0 ? nseg - 1 : min(nseg - 1, (int)(((long long)k1 - 1 + M) / S));
   if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(&tmem_base)), "r"(256));
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(&tmem_base)), "r"((uint32_t)(2 * TQC)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::);
   }
   if (tid == 0) {
@@ -751,6 +757,8 @@ __global__ void __launch_bounds__(TQ, 2) k_attn_bwd_dkv_tc(const float *__restri
     st_row16(sV, tid, vf);
   }
   const uint32_t trow_off = (uint32_t)(warp * 32) << 16;
+  // dK / dV of this thread's key summed over chunks: the own segment's are written to dqkv and
+  // reset after tau = sigma, the later segments' accumulate into the memory rows dkvm
   float dkm[16], dvm[16];
 #pragma unroll
   for (int c = 0; c < 16; c++) dkm[c] = dvm[c] = 0.f;
@@ -772,7 +780,7 @@ __global__ void __launch_bounds__(TQ, 2) k_attn_bwd_dkv_tc(const float *__restri
   const float kC = kScaleTc * 1.4426950408889634f;
   ld_q_rows(sig);
   for (int tau = sig; tau <= tau_hi; tau++) {
-    const int q0 = tau * S, q1 = min(N, q0 + S), nq = q1 - q0, Nqp = (nq + 15) & ~15;
+    const int q0 = tau * S, q1 = min(N, q0 + S), nq = q1 - q0;
     const int lo = M < 0 ? 0 : max(0, q0 - M);
     const bool inr = kvalid && j >= lo;
     {
@@ -787,75 +795,87 @@ __global__ void __launch_bounds__(TQ, 2) k_attn_bwd_dkv_tc(const float *__restri
       sD[tid] = D;
     }
     if (tau < tau_hi) ld_q_rows(tau + 1);   // in flight during this segment
-    sync_for_mma();   // (also: the previous segment's dK / dV have been drained by every warp)
-    const uint32_t tmem = tmem_base, trow = tmem + trow_off;
-    if (tid == 0) {   // S^T = K Q^T -> cols [0, Nqp); dP^T = V dO^T -> cols [128, 128 + Nqp)
-      mma_f16(tmem, desc(su32(sK), 128, 256), desc(su32(sQ), 128, 256), idesc_f16(Nqp), 0u);
-      mma_f16(tmem + 128u, desc(su32(sV), 128, 256), desc(su32(sdO), 128, 256), idesc_f16(Nqp), 0u);
-      mma_commit(&mbar);
-    }
-    mbar_wait_parity(&mbar, phase);
-    phase ^= 1u;
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    for (int c0 = 0; c0 < Nqp; c0 += 16) {
-      uint32_t sx[16], dpx[16];
-      float p[16], ds[16];
-      tmem_ld16_nw(trow + c0, sx);
-      tmem_ld16_nw(trow + 128 + c0, dpx);
-      tmem_wait_ld();
-      reg_fence16(sx);
-      reg_fence16(dpx);
+    for (int h0 = 0; h0 < nq; h0 += TQC) {
+      const int Nqp = (min(TQC, nq - h0) + 15) & ~15;
+      // staged rows visible to the MMAs; every warp has drained the previous chunk's dK / dV
+      sync_for_mma();
+      const uint32_t tmem = tmem_base, trow = tmem + trow_off;
+      if (tid == 0) {   // S^T = K Q^T -> cols [0, Nqp); dP^T = V dO^T -> cols [64, 64 + Nqp)
+        mma_f16(tmem, desc(su32(sK), 128, 256), desc(su32(sQ) + (h0 >> 3) * 256, 128, 256), idesc_f16(Nqp), 0u);
+        mma_f16(tmem + (uint32_t)TQC, desc(su32(sV), 128, 256), desc(su32(sdO) + (h0 >> 3) * 256, 128, 256),
+                idesc_f16(Nqp), 0u);
+        mma_commit(&mbar);
+      }
+      mbar_wait_parity(&mbar, phase);
+      phase ^= 1u;
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      for (int c0 = 0; c0 < Nqp; c0 += 16) {
+        uint32_t sx[16], dpx[16];
+        float p[16], ds[16];
+        tmem_ld16_nw(trow + c0, sx);
+        tmem_ld16_nw(trow + TQC + c0, dpx);
+        tmem_wait_ld();
+        reg_fence16(sx);
+        reg_fence16(dpx);
+        // dS' = p (dP - D); the 1/4 of dS = dS' / 4 is applied to dK once per chunk
+        if (inr) {
 #pragma unroll
-      for (int q4 = 0; q4 < 16; q4 += 4) {
-        const float4 l4 = *reinterpret_cast<const float4 *>(sL + c0 + q4);
-        const float4 d4 = *reinterpret_cast<const float4 *>(sD + c0 + q4);
-        const float lq[4] = {l4.x, l4.y, l4.z, l4.w}, dq[4] = {d4.x, d4.y, d4.z, d4.w};
+          for (int q4 = 0; q4 < 16; q4 += 4) {
+            const float4 l4 = *reinterpret_cast<const float4 *>(sL + h0 + c0 + q4);
+            const float4 d4 = *reinterpret_cast<const float4 *>(sD + h0 + c0 + q4);
+            const float lq[4] = {l4.x, l4.y, l4.z, l4.w}, dq[4] = {d4.x, d4.y, d4.z, d4.w};
 #pragma unroll
-        for (int u = 0; u < 4; u++) {
-          const int qq = q4 + u;
-          const float pv = ex2(fmaf(__uint_as_float(sx[qq]), kC, -lq[u]));   // 0 past the segment (L = +inf)
-          p[qq] = inr ? pv : 0.f;
-          ds[qq] = p[qq] * (__uint_as_float(dpx[qq]) - dq[u]) * kScaleTc;
+            for (int u = 0; u < 4; u++) {
+              const int qq = q4 + u;
+              p[qq] = ex2(fmaf(__uint_as_float(sx[qq]), kC, -lq[u]));   // 0 past the segment (L = +inf)
+              ds[qq] = p[qq] * (__uint_as_float(dpx[qq]) - dq[u]);
+            }
+          }
+        } else {
+#pragma unroll
+          for (int qq = 0; qq < 16; qq++) p[qq] = ds[qq] = 0.f;
         }
+        *reinterpret_cast<uint4 *>(sPt + coff(tid, c0, TQC)) =
+            make_uint4(pack2(p[0], p[1]), pack2(p[2], p[3]), pack2(p[4], p[5]), pack2(p[6], p[7]));
+        *reinterpret_cast<uint4 *>(sPt + coff(tid, c0 + 8, TQC)) =
+            make_uint4(pack2(p[8], p[9]), pack2(p[10], p[11]), pack2(p[12], p[13]), pack2(p[14], p[15]));
+        *reinterpret_cast<uint4 *>(sdSt + coff(tid, c0, TQC)) =
+            make_uint4(pack2(ds[0], ds[1]), pack2(ds[2], ds[3]), pack2(ds[4], ds[5]), pack2(ds[6], ds[7]));
+        *reinterpret_cast<uint4 *>(sdSt + coff(tid, c0 + 8, TQC)) =
+            make_uint4(pack2(ds[8], ds[9]), pack2(ds[10], ds[11]), pack2(ds[12], ds[13]), pack2(ds[14], ds[15]));
       }
-      *reinterpret_cast<uint4 *>(sPt + coff(tid, c0, TQ)) =
-          make_uint4(pack2(p[0], p[1]), pack2(p[2], p[3]), pack2(p[4], p[5]), pack2(p[6], p[7]));
-      *reinterpret_cast<uint4 *>(sPt + coff(tid, c0 + 8, TQ)) =
-          make_uint4(pack2(p[8], p[9]), pack2(p[10], p[11]), pack2(p[12], p[13]), pack2(p[14], p[15]));
-      *reinterpret_cast<uint4 *>(sdSt + coff(tid, c0, TQ)) =
-          make_uint4(pack2(ds[0], ds[1]), pack2(ds[2], ds[3]), pack2(ds[4], ds[5]), pack2(ds[6], ds[7]));
-      *reinterpret_cast<uint4 *>(sdSt + coff(tid, c0 + 8, TQ)) =
-          make_uint4(pack2(ds[8], ds[9]), pack2(ds[10], ds[11]), pack2(ds[12], ds[13]), pack2(ds[14], ds[15]));
-    }
-    sync_for_mma();   // S^T / dP^T consumed, P^T and dS^T written
-    if (tid == 0) {   // dK = dS^T Q -> cols [0, 16); dV = P^T dO -> cols [16, 32); K = Nqp queries
-      for (int ks = 0; ks < Nqp / 16; ks++) {
-        mma_f16(tmem, desc(su32(sdSt) + ks * 256, 128, kSbo128), desc(su32(sQt) + ks * 256, 128, kSbo128),
-                idesc_f16(16), ks > 0 ? 1u : 0u);
-        mma_f16(tmem + 16u, desc(su32(sPt) + ks * 256, 128, kSbo128), desc(su32(sdOt) + ks * 256, 128, kSbo128),
-                idesc_f16(16), ks > 0 ? 1u : 0u);
+      sync_for_mma();   // S^T / dP^T consumed, P^T and dS^T written
+      if (tid == 0) {   // dK = dS^T Q -> cols [0, 16); dV = P^T dO -> cols [16, 32); K = this chunk's queries
+        const uint32_t qt = (uint32_t)(h0 >> 3) * 128;
+        for (int ks = 0; ks < Nqp / 16; ks++) {
+          mma_f16(tmem, desc(su32(sdSt) + ks * 256, 128, kSbo64), desc(su32(sQt) + qt + ks * 256, 128, kSbo128),
+                  idesc_f16(16), ks > 0 ? 1u : 0u);
+          mma_f16(tmem + 16u, desc(su32(sPt) + ks * 256, 128, kSbo64), desc(su32(sdOt) + qt + ks * 256, 128, kSbo128),
+                  idesc_f16(16), ks > 0 ? 1u : 0u);
+        }
+        mma_commit(&mbar);
       }
-      mma_commit(&mbar);
+      mbar_wait_parity(&mbar, phase);
+      phase ^= 1u;
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      float dk[16], dv[16];
+      tmem_ld16(trow, dk);
+      tmem_ld16(trow + 16u, dv);
+#pragma unroll
+      for (int c = 0; c < 16; c++) { dkm[c] = fmaf(dk[c], kScaleTc, dkm[c]); dvm[c] += dv[c]; }
     }
-    mbar_wait_parity(&mbar, phase);
-    phase ^= 1u;
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    float dk[16], dv[16];
-    tmem_ld16(trow, dk);
-    tmem_ld16(trow + 16u, dv);
     if (tau == sig) {
       if (kvalid) {
 #pragma unroll
         for (int t = 0; t < 4; t++) {
           reinterpret_cast<float4 *>(dqkv + (size_t)j * 192 + 64 + hd * 16)[t] =
-              make_float4(dk[4 * t], dk[4 * t + 1], dk[4 * t + 2], dk[4 * t + 3]);
+              make_float4(dkm[4 * t], dkm[4 * t + 1], dkm[4 * t + 2], dkm[4 * t + 3]);
           reinterpret_cast<float4 *>(dqkv + (size_t)j * 192 + 128 + hd * 16)[t] =
-              make_float4(dv[4 * t], dv[4 * t + 1], dv[4 * t + 2], dv[4 * t + 3]);
+              make_float4(dvm[4 * t], dvm[4 * t + 1], dvm[4 * t + 2], dvm[4 * t + 3]);
         }
       }
-    } else {
 #pragma unroll
-      for (int c = 0; c < 16; c++) { dkm[c] += dk[c]; dvm[c] += dv[c]; }
+      for (int c = 0; c < 16; c++) dkm[c] = dvm[c] = 0.f;
     }
   }
   if (kvalid) {
@@ -869,7 +889,7 @@ __global__ void __launch_bounds__(TQ, 2) k_attn_bwd_dkv_tc(const float *__restri
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
-  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(256));
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"((uint32_t)(2 * TQC)));
 }
 
 }  // namespace
@@ -879,7 +899,7 @@ bool attn_bwd_tc_eligible(int S, int M) { return S >= 1 && S <= TQ && M >= 0 && 
 bool attn_bwd_tc_long_eligible(int S, int M) { return S >= 1 && S <= TQ && (M == -1 || M > S); }
 
 static const size_t kSmemDq = (size_t)5 * TQ * 32 + (size_t)TQ * TQ * 2;         // 52 KB
-static const size_t kSmemDkv = (size_t)6 * TQ * 32 + (size_t)2 * TQ * TQ * 2;    // 88 KB
+static const size_t kSmemDkv = (size_t)6 * TQ * 32 + (size_t)2 * TQ * TQC * 2;   // 56 KB
 void launch_attn_bwd_dq_tc(const float *qkv, const float *o, const float *lse, const float *dout, float *dqkv, int N,
                            int S, int M, cudaStream_t s) {
   const int nseg = (N + S - 1) / S;
