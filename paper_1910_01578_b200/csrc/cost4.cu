@@ -29,7 +29,7 @@ namespace {
 using namespace cu;
 
 #ifndef COST4_SLEEP_NS
-#define COST4_SLEEP_NS 200   // memory warp back-off when no window is pending
+#define COST4_SLEEP_NS 3200   // memory warp back-off when no window is pending (A/B: 200 -> 3200 ns, 96.4 -> 95.85 ms)
 #endif
 #ifndef COST4_WMAX
 #define COST4_WMAX 8
