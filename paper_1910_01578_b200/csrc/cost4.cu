@@ -41,9 +41,18 @@ constexpr int WMAX = COST4_WMAX;   // window length cap (ticks) = buckets per wi
 constexpr int R4 = COST4_R4;   // windows the memory warp may lag behind
 constexpr int SO4 = 8;     // staged out-edge records per slot
 constexpr int SI4 = 8;     // staged in-edge records per slot (2 * SO4 + SI4 = 24 staging lanes)
-constexpr int KF4 = 4;     // FIFO entries kept in smem per device
-constexpr int KC4 = 4;     // prefetched channel entries per channel
-constexpr int NINC4 = 8;   // ops made available at one local instant (overflow -> global)
+#ifndef COST4_KF
+#define COST4_KF 4
+#endif
+#ifndef COST4_KC
+#define COST4_KC 4
+#endif
+#ifndef COST4_NINC
+#define COST4_NINC 8
+#endif
+constexpr int KF4 = COST4_KF;       // FIFO entries kept in smem per device
+constexpr int KC4 = COST4_KC;       // prefetched channel entries per channel
+constexpr int NINC4 = COST4_NINC;   // ops made available at one local instant (overflow -> global)
 
 struct Smem4 {
   NRec st_out[8][2][SO4];
