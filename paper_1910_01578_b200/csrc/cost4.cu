@@ -176,7 +176,10 @@ __device__ __forceinline__ void put_inc(Smem4 &S, NRec *ovq, int q, int pos, con
 
 // 2 CTAs per SM cap the registers at 96; more registers (one CTA per SM) run a placement ~8 %
 // faster but need two waves for B = 256 (A/B: 99.5 ms vs 182.5 ms at 112 registers)
-__global__ void __launch_bounds__(288, 2) k_cost4(Cost2Graph G, TopoArgs T, const uint8_t *__restrict__ Dall,
+#ifndef COST4_MINB
+#define COST4_MINB 2   // resident CTAs per SM the register allocation is sized for
+#endif
+__global__ void __launch_bounds__(288, COST4_MINB) k_cost4(Cost2Graph G, TopoArgs T, const uint8_t *__restrict__ Dall,
                                                   unsigned char *scratch, size_t per_place, gdp_sim_report *rep,
                                                   long long *peak_out, long long *busy_out, double *reward, int Wl,
                                                   int dbg) {
