@@ -176,10 +176,11 @@ __device__ __forceinline__ void put_inc(Smem4 &S, NRec *ovq, int q, int pos, con
 
 // 2 CTAs per SM cap the registers at 96; more registers (one CTA per SM) run a placement ~8 %
 // faster but need two waves for B = 256 (A/B: 99.5 ms vs 182.5 ms at 112 registers)
-#ifndef COST4_MINB
-#define COST4_MINB 2   // resident CTAs per SM the register allocation is sized for
-#endif
-__global__ void __launch_bounds__(288, COST4_MINB) k_cost4(Cost2Graph G, TopoArgs T, const uint8_t *__restrict__ Dall,
+// MINB = resident CTAs per SM the register allocation is sized for: 2 (96 registers) or 3 (72
+// registers, a few spills; chosen when shared memory admits a third CTA and the batch is larger
+// than one wave of two per SM — profiles/r1_ab_s6/cost4_sleep.md)
+template <int MINB>
+__global__ void __launch_bounds__(288, MINB) k_cost4(Cost2Graph G, TopoArgs T, const uint8_t *__restrict__ Dall,
                                                   unsigned char *scratch, size_t per_place, gdp_sim_report *rep,
                                                   long long *peak_out, long long *busy_out, double *reward, int Wl,
                                                   int dbg) {
@@ -718,17 +719,37 @@ bool launch_cost4(const Cost2Graph &G, const TopoArgs &T, int min_cost, long lon
   const int L = cost4_window(T, min_cost, G.N, min_edge_bytes);
   if (L < 1) return false;
   if (per_place < cost4_scratch_per_placement(G.N, G.E, G.nbig)) return false;
-  const int d = T.d;
+  const int d = T.d, nthr = 32 * (d + 1);
   const size_t smem = cost4_smem_bytes(G.N);
-  static size_t configured = 0;
-  if (smem > 40 * 1024 && smem > configured) {
-    cudaFuncSetAttribute(k_cost4, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    configured = smem;
+  static size_t configured2 = 0, configured3 = 0;
+  if (smem > 40 * 1024 && smem > configured2) {
+    cudaFuncSetAttribute(k_cost4<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    configured2 = smem;
+  }
+  if (smem > 40 * 1024 && smem > configured3) {
+    cudaFuncSetAttribute(k_cost4<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    configured3 = smem;
   }
   static_assert(2 * SO4 + SI4 == 24, "24 staging lanes");
   static const int dbg = getenv("GDP_COST_DBG") ? atoi(getenv("GDP_COST_DBG")) : 0;
+  // GDP_COST4_MINB = 2 | 3 forces a variant (A/B); otherwise the 72-register one runs when it
+  // keeps more CTAs resident per SM and the batch does not fit one wave of the 96-register one
+  static const int force = getenv("GDP_COST4_MINB") ? atoi(getenv("GDP_COST4_MINB")) : 0;
+  static int nsm = 0;
+  if (!nsm) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  }
+  int occ2 = 0, occ3 = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, k_cost4<2>, nthr, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ3, k_cost4<3>, nthr, smem);
+  const bool use3 = force ? force == 3 : (occ3 > occ2 && (long long)B > (long long)occ2 * nsm);
   note_launch("k_cost4", s);
-  k_cost4<<<B, 32 * (d + 1), smem, s>>>(G, T, D, scratch, per_place, rep, peak, busy, reward, L, dbg);
+  if (use3)
+    k_cost4<3><<<B, nthr, smem, s>>>(G, T, D, scratch, per_place, rep, peak, busy, reward, L, dbg);
+  else
+    k_cost4<2><<<B, nthr, smem, s>>>(G, T, D, scratch, per_place, rep, peak, busy, reward, L, dbg);
   return true;
 }
 

@@ -122,6 +122,20 @@ def test_cost_workloads(gdp, cfg):
         assert_cost_equal(g, t, D, cost_gpu(gdp, g, t, D))
 
 
+def test_cost_three_ctas_per_sm(gdp):
+    """C3 (N ~ 20 k: shared memory admits three k_cost4 CTAs per SM) with B = 444 > one wave of
+    two per SM on 148 SMs: the launch takes the 72-register k_cost4<3> (DESIGN.md, cost kernel);
+    bit-exact against the oracle like every other cost kernel."""
+    W = workloads.config("c3")
+    g = W.graphs[0]
+    t = workloads.topology(g, W.d)
+    rng = np.random.default_rng(21)
+    D = rng.integers(0, W.d, size=(444, g.N)).astype(np.uint8)
+    D[3] = 0
+    D[7] = (np.arange(g.N) * W.d // g.N).astype(np.uint8)
+    assert_cost_equal(g, t, D, cost_gpu(gdp, g, t, D))
+
+
 def test_cost_full_size_c4(gdp):
     W = workloads.config("c4")
     g = W.graphs[0]
