@@ -123,8 +123,9 @@ __global__ void __launch_bounds__(TQ, 4) k_attn_fwd_tc(const float *__restrict__
   unsigned char *sV = sK + TKF * 16 * 2;        // V^T: 16 x 128
   unsigned char *sP = sV + 16 * TKF * 2;        // 128 x 128
   const int tid = threadIdx.x, warp = tid >> 5;
-  const int nseg = gridDim.x;
-  const int tau = nseg - 1 - blockIdx.x, hd = blockIdx.y;   // longest key ranges first
+  const int nseg = gridDim.y;
+  // blockIdx.x = head (fastest in dispatch order), so the four heads' longest key ranges go first
+  const int tau = nseg - 1 - blockIdx.y, hd = blockIdx.x;
   const int q0 = tau * S, q1 = min(N, q0 + S);
   const int lo = M < 0 ? 0 : max(0, q0 - M), hi = q1;
   // scores in log2 units: s2 = S_ij / 4 * log2(e), p = 2^(s2 - m2)
@@ -594,7 +595,8 @@ __global__ void __launch_bounds__(TQ, 4) k_attn_bwd_dq_tc(const float *__restric
   unsigned char *sKt = sV + TQ * 32;      // 16 x 128 keys (B of dQ)
   unsigned char *sdS = sKt + TQ * 32;     // 128 queries x 128 keys (A of dQ)
   const int tid = threadIdx.x, warp = tid >> 5;
-  const int tau = gridDim.x - 1 - blockIdx.x, hd = blockIdx.y;   // longest key ranges first
+  // blockIdx.x = head (fastest in dispatch order), so the four heads' longest key ranges go first
+  const int tau = gridDim.y - 1 - blockIdx.y, hd = blockIdx.x;
   const int q0 = tau * S, q1 = min(N, q0 + S);
   const int lo = M < 0 ? 0 : max(0, q0 - M), hi = q1;
   if (warp == 0) {
@@ -734,7 +736,8 @@ __global__ void __launch_bounds__(TQ, 3) k_attn_bwd_dkv_tc(const float *__restri
   unsigned char *sPt = sdOt + TQ * 32;    // 128 keys x 64 queries (A of dV)
   unsigned char *sdSt = sPt + TQ * TQC * 2;   // 128 keys x 64 queries (A of dK)
   const int tid = threadIdx.x, warp = tid >> 5;
-  const int sig = blockIdx.x, hd = blockIdx.y;   // sigma = 0 has the most query segments: first
+  // sigma = 0 has the most query segments; blockIdx.x = head, so every head's heaviest CTAs go first
+  const int sig = blockIdx.y, hd = blockIdx.x;
   const int k0 = sig * S, k1 = min(N, k0 + S), nk = k1 - k0;
   const int tau_hi = M < 0 ? nseg - 1 : min(nseg - 1, (int)(((long long)k1 - 1 + M) / S));
   if (warp == 0) {
@@ -908,7 +911,7 @@ void launch_attn_bwd_dq_tc(const float *qkv, const float *o, const float *lse, c
     cudaFuncSetAttribute(k_attn_bwd_dq_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemDq);
     configured = true;
   }
-  k_attn_bwd_dq_tc<<<dim3(nseg, kHeads), TQ, kSmemDq, s>>>(qkv, o, lse, dout, dqkv, N, S, M);
+  k_attn_bwd_dq_tc<<<dim3(kHeads, nseg), TQ, kSmemDq, s>>>(qkv, o, lse, dout, dqkv, N, S, M);
 }
 void launch_attn_bwd_dkv_tc(const float *qkv, const float *o, const float *lse, const float *dout, float *dqkv,
                             float *dkvm, int N, int S, int M, cudaStream_t s) {
@@ -918,7 +921,7 @@ void launch_attn_bwd_dkv_tc(const float *qkv, const float *o, const float *lse, 
     cudaFuncSetAttribute(k_attn_bwd_dkv_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemDkv);
     configured = true;
   }
-  k_attn_bwd_dkv_tc<<<dim3(nseg, kHeads), TQ, kSmemDkv, s>>>(qkv, o, lse, dout, dqkv, dkvm, N, S, M, nseg);
+  k_attn_bwd_dkv_tc<<<dim3(kHeads, nseg), TQ, kSmemDkv, s>>>(qkv, o, lse, dout, dqkv, dkvm, N, S, M, nseg);
 }
 
 void launch_attn_bwd_tc(const float *qkv, const float *o, const float *lse, const float *dout, float *dqkv,
@@ -941,7 +944,7 @@ void launch_attn_fwd_tc(const float *qkv, float *o, float *lse, int N, int S, in
     cudaFuncSetAttribute(k_attn_fwd_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     configured = true;
   }
-  k_attn_fwd_tc<<<dim3(nseg, kHeads), TQ, smem, s>>>(qkv, o, lse, N, S, M);
+  k_attn_fwd_tc<<<dim3(kHeads, nseg), TQ, smem, s>>>(qkv, o, lse, N, S, M);
 }
 
 }  // namespace gdp
