@@ -69,7 +69,10 @@ typedef struct {
   int32_t tensor_cores;   /* 0: every dense map in fp32 (SIMT, the 1e-4 parity mode); 1: dense maps
                              Y = X W (forward and the backward dX = dY W^T) with 16 <= width <= 256 and
                              >= 128 rows on tcgen05 tensor cores, bf16 operands, fp32 accumulation in
-                             TMEM; weight gradients (reductions over nodes) stay fp32 */
+                             TMEM, and the segment attention on tcgen05 tiles; weight gradients
+                             (reductions over nodes) stay fp32.  2 (diagnostic): as 1 but with the
+                             SIMT attention kernels, so that tests compare the attention tiles inside
+                             one tensor-core step */
   int32_t no_attention;   /* ablation: 1 replaces every attention
                              sublayer (placer and conditioner) by the per-node map
                              o = ReLU(LN1(x) W_v + b_v) (reading R34); 0: attention */
@@ -258,12 +261,33 @@ gdp_status gdp_cost(gdp_graph g, gdp_topo t, const uint8_t *placements, int32_t 
                     void *stream);
 
 /* Diagnostic: which cost kernel gdp_cost runs for this graph and topology (host only, no
- * launch): 4 = windowed one-warp-per-device kernel (every duration >= 1 tick and every
- * cross-device latency >= 1 tick), 3 = warp-cooperative instant-by-instant kernel,
- * 2 = owner-lane kernel (GDP_COST_V2 set), 1 = global-memory kernel (per-placement state
- * larger than shared memory, or GDP_COST_V1 set).  All four compute the same integers
- * (DESIGN.md §"Cost model").  Returns 0 and sets the error for NULL handles. */
+ * launch): 5 = simulation-warp + memory-warp kernel (every duration >= 1 tick and every
+ * transfer >= 1 tick), 3 = warp-cooperative instant-by-instant kernel (zero-duration ops or
+ * zero-tick transfers: same-instant rounds), 1 = global-memory kernel (per-placement state
+ * larger than shared memory).  All three compute the same integers (DESIGN.md §7 "Cost
+ * model").  Returns 0 and sets the error for NULL handles. */
 int32_t gdp_cost_kernel(gdp_graph g, gdp_topo t);
+
+/* Diagnostic (tests): device pointer to an intermediate that the last gdp_embed / gdp_place on
+ * this workspace saved in `ws` (no copy, no launch; valid until the next call on ws):
+ *   what 0: max-pool argmax of GNN layer `layer` (0..2), int32 N x 64, caller node order, the
+ *           lowest-id neighbour attaining the max per channel (Eq. 2), -1 if none;
+ *   what 1: FFN hidden activation m = ReLU(LN2(x1) W1' + b1) of Transformer-XL layer `layer`
+ *           (0 conditioner, 1, 2 placement layers), fp32 N x 256, Kahn (topological) row order;
+ *   what 2: the per-node map o = ReLU(LN1(x) Wv' + bv) of layer `layer` in the no_attention
+ *           ablation (else the attention output), fp32 N x 64, Kahn row order.
+ * The parity tests use them to adopt the GPU's decision at max-pool near-ties and ReLU inputs
+ * near zero ("tie import").  Errors: GDP_ERR_ARG, GDP_ERR_WORKSPACE. */
+gdp_status gdp_debug_tensor(gdp_graph g, const gdp_config *c, void *ws, size_t ws_bytes, int32_t what,
+                            int32_t layer, void **out);
+
+/* Diagnostic / test entry: gdp_cost on an explicitly chosen kernel (5, 3 or 1; 0 = the
+ * automatic choice gdp_cost makes).  GDP_ERR_ARG if that kernel does not apply to (g, t)
+ * (e.g. 5 with a zero-duration op).  Used by the tests to hold every kernel to the oracle on
+ * the same inputs; otherwise identical to gdp_cost. */
+gdp_status gdp_cost_with_kernel(gdp_graph g, gdp_topo t, const uint8_t *placements, int32_t B,
+                                gdp_sim_report *rep, int64_t *peak_mem, int64_t *busy, double *reward,
+                                void *ws, size_t ws_bytes, int32_t kernel, void *stream);
 
 /* Advantage ("average reward of all the previous trials as a bias term"):
  * for b = 0..B-1 in order, adv[b] = (count == 0) ? 0 : reward[b] - sum / count, then

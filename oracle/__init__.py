@@ -26,7 +26,9 @@ import torch
 from . import model, sampling, simulate, train
 
 __all__ = ["model", "sampling", "simulate", "train", "Prepared", "prepare", "embed", "place", "logits_and_grad",
-           "policy_grad"]
+           "policy_grad", "Numerics"]
+
+Numerics = model.Numerics
 
 
 class Prepared:
@@ -50,10 +52,10 @@ def _theta(theta) -> torch.Tensor:
     return torch.as_tensor(np.asarray(theta, dtype=np.float64)).clone()
 
 
-def embed(pg: Prepared, theta, d: int) -> np.ndarray:
+def embed(pg: Prepared, theta, d: int, num: Optional[model.Numerics] = None) -> np.ndarray:
     with torch.no_grad():
         p = model.unflatten(_theta(theta), pg.F, d)
-        return model.embed(pg.X, pg.ptr, pg.idx, p).numpy()
+        return model.embed(pg.X, pg.ptr, pg.idx, p, num=num or model.EXACT).numpy()
 
 
 def embed_keep(pg: Prepared, theta, d: int) -> Dict[str, object]:
@@ -66,11 +68,11 @@ def embed_keep(pg: Prepared, theta, d: int) -> Dict[str, object]:
 
 
 def place(pg: Prepared, theta, E: np.ndarray, d: int, S: int, M: int, superposition: bool = True,
-          keep: Optional[dict] = None, no_attention: bool = False) -> np.ndarray:
+          keep: Optional[dict] = None, no_attention: bool = False, num: Optional[model.Numerics] = None) -> np.ndarray:
     with torch.no_grad():
         p = model.unflatten(_theta(theta), pg.F, d)
         return model.place(torch.as_tensor(np.asarray(E, dtype=np.float64)), p, pg.order, S, M,
-                           superposition, keep, no_attention=no_attention).numpy()
+                           superposition, keep, no_attention=no_attention, num=num or model.EXACT).numpy()
 
 
 def logit_grad(pg: Prepared, logits: np.ndarray, D, adv, old_logprob, clip_eps, entropy_coef, loss_scale):
@@ -84,7 +86,7 @@ def logit_grad(pg: Prepared, logits: np.ndarray, D, adv, old_logprob, clip_eps, 
 def policy_grad(pg: Prepared, theta, d: int, S: int, M: int, superposition: bool, D, adv,
                 old_logprob=None, clip_eps: float = 0.2, entropy_coef: float = 0.01,
                 loss_scale: float = 1.0, mem_srcs: Optional[dict] = None, no_attention: bool = False,
-                active: Optional[int] = None):
+                active: Optional[int] = None, num: Optional[model.Numerics] = None):
     """Gradient of L (model.policy_loss) w.r.t. the flat theta through place and
     embed (§3.1 "trained jointly ... in an end-to-end fashion").
     `active` (NEXT-4 mixed device counts): only the first `active` head outputs enter the
@@ -92,8 +94,9 @@ def policy_grad(pg: Prepared, theta, d: int, S: int, M: int, superposition: bool
     Returns (grad float64 [n_params], loss float)."""
     th = _theta(theta).requires_grad_(True)
     p = model.unflatten(th, pg.F, d)
-    E = model.embed(pg.X, pg.ptr, pg.idx, p)
-    logits = model.place(E, p, pg.order, S, M, superposition, mem_srcs=mem_srcs, no_attention=no_attention)
+    num = num or model.EXACT
+    E = model.embed(pg.X, pg.ptr, pg.idx, p, num=num)
+    logits = model.place(E, p, pg.order, S, M, superposition, mem_srcs=mem_srcs, no_attention=no_attention, num=num)
     if active is not None:              # NEXT-4: head padded to d outputs, first `active` devices live;
         logits = logits[:, :active]     # masking the rest to -inf is the same as dropping them
     L = model.policy_loss(logits, D, adv, pg.lead, old_logprob, clip_eps, entropy_coef, loss_scale)

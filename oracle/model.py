@@ -56,6 +56,124 @@ def unflatten(theta: torch.Tensor, F: int, d: int) -> Dict[str, torch.Tensor]:
     return p
 
 
+# --------------------------------------------------------------------------- numerics
+class Numerics:
+    """How the oracle evaluates the network (SURVEY §8(c) parity metric).
+
+    * exact (the default): float64 everywhere -- the definition of the method;
+    * bf16 = True: the tensor-core mode of the GPU path as include/gdp.h defines it
+      (gdp_config.tensor_cores = 1): every dense map Y = X W whose shape the tensor cores take
+      (16 <= width <= 256, K <= 256, >= 128 rows), and its backward dX = dY W^T under the same
+      shape rule, multiplies X and W rounded to bfloat16 (round to nearest even) and
+      accumulates exactly; the segment attention multiplies bf16 Q, K, V and softmax numerators
+      P (and bf16 dO, dS, P in its backward); everything else (LayerNorm, activations, softmax,
+      reductions, weight gradients, the head's forward of width d < 16) stays exact.  With the
+      GPU's rounding points reproduced, what remains between the two is accumulation order.
+    * tie import (`ties`): where the oracle's own decision is within `tie_tol` of a kink -- a
+      max-pool channel whose top-2 margin is below tie_tol * max(1, |top|), a ReLU input within
+      tie_tol of zero -- it adopts the GPU's recorded decision instead (either side of a kink is
+      a correct subgradient; the gradient must then route the same way to be comparable).
+      `ties` = {"argmax": [3 x (N, 64) int], "relu": {layer name: bool mask (Kahn order)},
+      "relu_v": {...}}; `imported` counts the adopted decisions."""
+
+    def __init__(self, bf16: bool = False, ties: Optional[dict] = None, tie_tol: float = 1e-5,
+                 attn_tc: bool = True):
+        self.bf16 = bf16
+        self.attn_tc = attn_tc
+        self.ties = ties or {}
+        self.tie_tol = tie_tol
+        self.imported = {"argmax": 0, "relu": 0}
+
+
+EXACT = Numerics()
+
+
+def bf(x: torch.Tensor) -> torch.Tensor:
+    """Round to bfloat16 (nearest even, through float32 as the GPU holds the value) and back."""
+    return x.to(torch.float32).to(torch.bfloat16).to(x.dtype)
+
+
+def tc_shape(M: int, K: int, Nout: int) -> bool:
+    """The tensor cores take Y (M x Nout) = X (M x K) W: 16 <= Nout <= 256, 1 <= K <= 256, M >= 128."""
+    return 16 <= Nout <= 256 and 1 <= K <= 256 and M >= 128
+
+
+class _DenseBF16(torch.autograd.Function):
+    """y = bf(x) bf(W) + b when the forward shape is a tensor-core shape (fwd_tc); backward
+    dx = bf(dy) bf(W)^T when that shape is one (bwd_tc); dW = x^T dy, db = sum dy exact."""
+
+    @staticmethod
+    def forward(ctx, x, W, b, fwd_tc, bwd_tc):
+        ctx.save_for_backward(x, W)
+        ctx.bwd_tc = bwd_tc
+        y = (bf(x) @ bf(W)) if fwd_tc else (x @ W)
+        return y + b
+
+    @staticmethod
+    def backward(ctx, dy):
+        x, W = ctx.saved_tensors
+        dx = (bf(dy) @ bf(W).T) if ctx.bwd_tc else (dy @ W.T)
+        return dx, x.T @ dy, dy.sum(0), None, None
+
+
+def dense_map(x: torch.Tensor, W: torch.Tensor, b: torch.Tensor, rows: int, num: Numerics) -> torch.Tensor:
+    """x W + b (Eq. 2-3, S:490 dense maps).  `rows` = the rows of the GPU's GEMM for this
+    map (all N nodes), which decides the tensor-core shape rule in bf16 mode."""
+    if not num.bf16:
+        return x @ W + b
+    K, Nout = W.shape
+    return _DenseBF16.apply(x, W, b, tc_shape(rows, K, Nout), tc_shape(rows, Nout, K))
+
+
+class _AttnBF16(torch.autograd.Function):
+    """One segment's attention in the tensor-core mode: scores from bf16 Q, K; O = (bf16 P~ @
+    bf16 V) / sum P~ with P~ = exp(s - max) (softmax numerators); backward with bf16 dO, V for
+    dP, bf16 dS, Q for dK, bf16 P, dO for dV, and dS (bf16 when M > S or M = inf, the MMA
+    kernels) times bf16 K for dQ."""
+
+    @staticmethod
+    def forward(ctx, Q, K, V, dq_bf16):
+        outs, probs = [], []
+        for hd in range(HEADS):
+            sl = slice(hd * DH, (hd + 1) * DH)
+            s = bf(Q[:, sl]) @ bf(K[:, sl]).T / math.sqrt(DH)
+            pt = torch.exp(s - s.max(1, keepdim=True).values)
+            outs.append((bf(pt) @ bf(V[:, sl])) / pt.sum(1, keepdim=True))
+            probs.append(pt / pt.sum(1, keepdim=True))
+        O = torch.cat(outs, 1)
+        ctx.save_for_backward(Q, K, V, O, *probs)
+        ctx.dq_bf16 = dq_bf16
+        return O
+
+    @staticmethod
+    def backward(ctx, dO):
+        Q, K, V, O = ctx.saved_tensors[:4]
+        probs = ctx.saved_tensors[4:]
+        dQ, dK, dV = torch.zeros_like(Q), torch.zeros_like(K), torch.zeros_like(V)
+        for hd in range(HEADS):
+            sl = slice(hd * DH, (hd + 1) * DH)
+            P = probs[hd]
+            Dr = (dO[:, sl] * O[:, sl]).sum(1, keepdim=True)
+            dP = bf(dO[:, sl]) @ bf(V[:, sl]).T
+            dS = P * (dP - Dr) / math.sqrt(DH)
+            dQ[:, sl] = (bf(dS) if ctx.dq_bf16 else dS) @ bf(K[:, sl])
+            dK[:, sl] = bf(dS).T @ bf(Q[:, sl])
+            dV[:, sl] = bf(P).T @ bf(dO[:, sl])
+        return dQ, dK, dV, None
+
+
+def relu_map(pre: torch.Tensor, num: Numerics, gpu_active: Optional[torch.Tensor]) -> torch.Tensor:
+    """ReLU (R12 FFN nonlinearity; R34 ablation map); with tie import, inputs within tie_tol of
+    zero take the GPU's active / inactive decision."""
+    if gpu_active is None:
+        return torch.relu(pre)
+    own = pre.detach() > 0
+    near = pre.detach().abs() < num.tie_tol
+    use = torch.where(near, torch.as_tensor(gpu_active, dtype=torch.bool), own)
+    num.imported["relu"] += int((near & (use != own)).sum())
+    return pre * use.to(pre.dtype)
+
+
 # --------------------------------------------------------------------------- graph plumbing
 def topo_order(N: int, edges: np.ndarray) -> List[int]:
     """Kahn's algorithm, ties broken by ascending node id."""
@@ -108,10 +226,13 @@ def leaders(N: int, coloc: Optional[np.ndarray]) -> np.ndarray:
 
 
 # --------------------------------------------------------------------------- GNN (§3.1)
-def gather_max(Z: torch.Tensor, ptr: np.ndarray, idx: np.ndarray) -> Tuple[torch.Tensor, torch.Tensor]:
+def gather_max(Z: torch.Tensor, ptr: np.ndarray, idx: np.ndarray, num: Numerics = EXACT,
+               gpu_arg: Optional[torch.Tensor] = None) -> Tuple[torch.Tensor, torch.Tensor]:
     """Eq. 2 max over u in N(v) (P:126-134), per channel; empty N(v) -> 0 (S:429);
     argmax = the lowest-id u attaining the max (S:75 first index on ties).  The value
-    is returned as a gather of Z at the argmax so the gradient routes there only."""
+    is returned as a gather of Z at the argmax so the gradient routes there only.
+    Tie import (Numerics): where the top-2 margin is below tie_tol * max(1, |top|) the GPU's
+    argmax `gpu_arg` is adopted."""
     N, h = Z.shape
     deg = np.diff(ptr)
     rows = torch.from_numpy(np.repeat(np.arange(N), deg))
@@ -124,6 +245,15 @@ def gather_max(Z: torch.Tensor, ptr: np.ndarray, idx: np.ndarray) -> Tuple[torch
     arg = torch.full((N, h), N, dtype=torch.long).scatter_reduce(0, rows[:, None].expand(-1, h), cand, "amin")
     empty = torch.from_numpy(deg == 0)
     arg[empty] = -1
+    if gpu_arg is not None:
+        not_top = cols[:, None] != arg[rows]
+        top2 = torch.full((N, h), -math.inf, dtype=Z.dtype).scatter_reduce(
+            0, rows[:, None].expand(-1, h), torch.where(not_top, vals, torch.full_like(vals, -math.inf)), "amax")
+        near = (amax - top2) < num.tie_tol * torch.clamp(amax.abs(), min=1.0)
+        ga = torch.as_tensor(np.asarray(gpu_arg), dtype=torch.long)
+        take = near & (ga != arg) & (ga >= 0) & ~empty[:, None]
+        num.imported["argmax"] += int(take.sum())
+        arg = torch.where(take, ga, arg)
     A = torch.gather(Z, 0, arg.clamp(min=0)) * (~empty)[:, None].to(Z.dtype)
     return A, arg
 
@@ -147,19 +277,21 @@ def gather_max_loop(Z: torch.Tensor, nbrs: Sequence[Sequence[int]]) -> Tuple[tor
 
 
 def embed(X: torch.Tensor, ptr: np.ndarray, idx: np.ndarray, p: Dict[str, torch.Tensor],
-          keep: Optional[dict] = None, layers: int = L_GNN) -> torch.Tensor:
+          keep: Optional[dict] = None, layers: int = L_GNN, num: Numerics = EXACT) -> torch.Tensor:
     """§3.1: input projection to h (affine, reading R3), then L rounds of
     Eq. 2 aggregation h_N(v) = max_u sigma(W h_u + b) and Eq. 3 combine
     h_v' = tanh(concat(h_v, h_N(v)) W_f + b_f) (activation tanh)."""
-    Hh = X @ p["gnn.in.W"] + p["gnn.in.b"]
+    N = X.shape[0]
+    Hh = dense_map(X, p["gnn.in.W"], p["gnn.in.b"], N, num)
+    gargs = num.ties.get("argmax")
     for l in range(layers):
-        Z = torch.sigmoid(Hh @ p[f"gnn.{l}.W"] + p[f"gnn.{l}.b"])
-        A, arg = gather_max(Z, ptr, idx)
+        Z = torch.sigmoid(dense_map(Hh, p[f"gnn.{l}.W"], p[f"gnn.{l}.b"], N, num))
+        A, arg = gather_max(Z, ptr, idx, num, None if gargs is None else gargs[l])
         if keep is not None:
             keep.setdefault("Z", []).append(Z)
             keep.setdefault("A", []).append(A)
             keep.setdefault("argmax", []).append(arg)
-        Hh = torch.tanh(torch.cat([Hh, A], 1) @ p[f"gnn.{l}.Wf"] + p[f"gnn.{l}.bf"])
+        Hh = torch.tanh(dense_map(torch.cat([Hh, A], 1), p[f"gnn.{l}.Wf"], p[f"gnn.{l}.bf"], N, num))
     return Hh
 
 
@@ -179,9 +311,21 @@ def key_range(i: int, N: int, S: int, M: int) -> Tuple[int, int]:
     return lo, min((tau + 1) * S, N)
 
 
+def attention_heads(Q: torch.Tensor, K: torch.Tensor, V: torch.Tensor) -> torch.Tensor:
+    """Multi-head scaled dot-product attention of one segment's queries over its key range
+    (Transformer-XL attention without positional terms, R8): per head of DH = 16
+    dims, p = softmax(Q K^T / sqrt(16)) over the keys, output p V; heads concatenated."""
+    heads = []
+    for hd in range(HEADS):
+        sl = slice(hd * DH, (hd + 1) * DH)
+        s = Q[:, sl] @ K[:, sl].T / math.sqrt(DH)
+        heads.append(torch.softmax(s, dim=1) @ V[:, sl])
+    return torch.cat(heads, 1)
+
+
 def xl_layer(x: torch.Tensor, p: Dict[str, torch.Tensor], n: str, gam: Optional[Dict[str, torch.Tensor]],
              S: int, M: int, keep: Optional[dict] = None, mem_src: Optional[torch.Tensor] = None,
-             no_attention: bool = False) -> torch.Tensor:
+             no_attention: bool = False, num: Numerics = EXACT) -> torch.Tensor:
     """One Transformer-XL layer over the node sequence without positional terms
     (P:144-148).  Segments of S nodes; each attends to itself (bidirectional) and to
     the cached hidden states of up to M earlier positions, which are detached
@@ -200,15 +344,21 @@ def xl_layer(x: torch.Tensor, p: Dict[str, torch.Tensor], n: str, gam: Optional[
     def g(j):
         return None if gam is None else gam[j]
 
+    N = x.shape[0]
+
     def dense(inp, W, b, j):
         gj = g(j)
-        return (inp if gj is None else inp * gj) @ W + b
+        if not num.bf16:
+            return (inp if gj is None else inp * gj) @ W + b
+        # the GPU folds the gate into the weight (W' = diag(gamma) W, the same product) and
+        # rounds W' for the tensor cores
+        return dense_map(inp, W if gj is None else gj[:, None] * W, b, N, num)
 
-    N = x.shape[0]
+    relu_ties = num.ties.get("relu", {})
     outs = []
     if no_attention:
         a = layer_norm(x, p[f"{n}.ln1.g"], p[f"{n}.ln1.b"])
-        outs.append(torch.relu(dense(a, p[f"{n}.Wv"], p[f"{n}.bv"], "v")))
+        outs.append(relu_map(dense(a, p[f"{n}.Wv"], p[f"{n}.bv"], "v"), num, num.ties.get("relu_v", {}).get(n)))
     for q0 in (range(0, N, S) if not no_attention else []):
         q1 = min(q0 + S, N)
         k0, _ = key_range(q0, N, S, M)
@@ -218,16 +368,14 @@ def xl_layer(x: torch.Tensor, p: Dict[str, torch.Tensor], n: str, gam: Optional[
         Q = dense(aq, p[f"{n}.Wq"], p[f"{n}.bq"], "q")
         K = dense(ak, p[f"{n}.Wk"], p[f"{n}.bk"], "k")
         V = dense(ak, p[f"{n}.Wv"], p[f"{n}.bv"], "v")
-        heads = []
-        for hd in range(HEADS):
-            sl = slice(hd * DH, (hd + 1) * DH)
-            s = Q[:, sl] @ K[:, sl].T / math.sqrt(DH)
-            heads.append(torch.softmax(s, dim=1) @ V[:, sl])
-        outs.append(torch.cat(heads, 1))
+        if num.bf16 and num.attn_tc and S <= 128:      # the tcgen05 attention tiles take S <= 128
+            outs.append(_AttnBF16.apply(Q, K, V, M < 0 or M > S))
+        else:
+            outs.append(attention_heads(Q, K, V))
     o = torch.cat(outs, 0)
     x1 = x + dense(o, p[f"{n}.Wo"], p[f"{n}.bo"], "o")
     c = layer_norm(x1, p[f"{n}.ln2.g"], p[f"{n}.ln2.b"])
-    m = torch.relu(dense(c, p[f"{n}.W1"], p[f"{n}.b1"], "f1"))
+    m = relu_map(dense(c, p[f"{n}.W1"], p[f"{n}.b1"], "f1"), num, relu_ties.get(n))
     y = x1 + dense(m, p[f"{n}.W2"], p[f"{n}.b2"], "f2")
     if keep is not None:
         keep.setdefault(n, {}).update(o=o, x1=x1, y=y)
@@ -263,11 +411,11 @@ def xl_layer_masked(x: torch.Tensor, p: Dict[str, torch.Tensor], n: str, gam, S:
 
 
 def gates(E_topo: torch.Tensor, p: Dict[str, torch.Tensor], S: int, M: int, keep: Optional[dict] = None,
-          mem_srcs: Optional[dict] = None, no_attention: bool = False):
+          mem_srcs: Optional[dict] = None, no_attention: bool = False, num: Numerics = EXACT):
     """Superposition conditioning (readings R14): c = an additional
     transformer layer over the embeddings, averaged over nodes, then per
     gated dense map j: gamma_j = 2 sigmoid(z P_j + q_j) (=1 at P, q = 0)."""
-    C = xl_layer(E_topo, p, "cond", None, S, M, keep, (mem_srcs or {}).get("cond"), no_attention)
+    C = xl_layer(E_topo, p, "cond", None, S, M, keep, (mem_srcs or {}).get("cond"), no_attention, num)
     z = C.mean(0)
     gam = [{j: 2 * torch.sigmoid(z @ p[f"gate{l}.{j}.P"] + p[f"gate{l}.{j}.q"]) for j in GATED} for l in range(2)]
     gh = 2 * torch.sigmoid(z @ p["gate.head.P"] + p["gate.head.q"])
@@ -280,7 +428,7 @@ def gates(E_topo: torch.Tensor, p: Dict[str, torch.Tensor], S: int, M: int, keep
 
 def place(E: torch.Tensor, p: Dict[str, torch.Tensor], order: Sequence[int], S: int, M: int,
           superposition: bool = True, keep: Optional[dict] = None, mem_srcs: Optional[dict] = None,
-          no_attention: bool = False) -> torch.Tensor:
+          no_attention: bool = False, num: Numerics = EXACT) -> torch.Tensor:
     """§3.2-3.3 placement network: nodes in topological order, 2
     segment-recurrent layers, per-node device logits from the conditioned head with
     no final LN (R15); whole graph placed at once (R13).  Returns logits in
@@ -288,12 +436,15 @@ def place(E: torch.Tensor, p: Dict[str, torch.Tensor], order: Sequence[int], S: 
     perm = torch.as_tensor(list(order), dtype=torch.long)
     x = E[perm]
     if superposition:
-        gam, gh = gates(x, p, S, M, keep, mem_srcs, no_attention)
+        gam, gh = gates(x, p, S, M, keep, mem_srcs, no_attention, num)
     else:
         gam, gh = [None, None], None
     for l in range(2):
-        x = xl_layer(x, p, f"xl{l}", gam[l], S, M, keep, (mem_srcs or {}).get(f"xl{l}"), no_attention)
-    lt = (x if gh is None else x * gh) @ p["head.W"] + p["head.b"]
+        x = xl_layer(x, p, f"xl{l}", gam[l], S, M, keep, (mem_srcs or {}).get(f"xl{l}"), no_attention, num)
+    if num.bf16:   # the head's forward (width d < 16) is exact; its backward dX is a tensor-core shape
+        lt = dense_map(x, p["head.W"] if gh is None else gh[:, None] * p["head.W"], p["head.b"], x.shape[0], num)
+    else:
+        lt = (x if gh is None else x * gh) @ p["head.W"] + p["head.b"]
     logits = torch.empty_like(lt)
     logits = logits.index_copy(0, perm, lt)
     return logits

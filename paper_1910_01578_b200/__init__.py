@@ -26,7 +26,7 @@ REPORT_BYTES = 24
 
 EXPORTS = ["gdp_default_config", "gdp_last_error", "gdp_launch_count", "gdp_build_info", "gdp_cost_kernel", "gdp_logprob", "gdp_clip_adam", "gdp_sample_at", "gdp_greedy", "gdp_graph_validate", "gdp_graph_create", "gdp_graph_destroy",
            "gdp_topo_create", "gdp_topo_destroy", "gdp_param_layout", "gdp_workspace_size", "gdp_embed",
-           "gdp_place", "gdp_sample", "gdp_cost", "gdp_advantage", "gdp_policy_grad", "gdp_profile_enable",
+           "gdp_place", "gdp_sample", "gdp_cost", "gdp_cost_with_kernel", "gdp_debug_tensor", "gdp_advantage", "gdp_policy_grad", "gdp_profile_enable",
            "gdp_profile_mark", "gdp_profile_read"]
 
 
@@ -67,6 +67,8 @@ def lib():
             "gdp_place": [P, P, P, P, P, P, SZ, P],
             "gdp_sample": [P, P, P, I32, U64, U64, U64, P, P, P, SZ, P],
             "gdp_cost": [P, P, P, I32, P, P, P, P, P, SZ, P],
+            "gdp_cost_with_kernel": [P, P, P, I32, P, P, P, P, P, SZ, I32, P],
+            "gdp_debug_tensor": [P, P, P, SZ, I32, I32, ctypes.POINTER(ctypes.c_void_p)],
             "gdp_advantage": [P, I32, P, P, P, P],
             "gdp_policy_grad": [P, P, P, P, P, I32, P, P, P, F32, F32, F32, P, P, SZ, P],
             "gdp_logprob": [P, P, P, P, I32, P, P, SZ, P],
@@ -162,7 +164,7 @@ def default_config(d: int, seg_len: int = 128, mem_len: int = 128, superposition
     c = Config()
     _check(lib().gdp_default_config(d, ctypes.byref(c)), "gdp_default_config")
     c.seg_len, c.mem_len, c.superposition = seg_len, mem_len, int(bool(superposition))
-    c.tensor_cores = int(bool(tensor_cores))
+    c.tensor_cores = int(tensor_cores) if not isinstance(tensor_cores, bool) else int(tensor_cores)
     c.no_attention = int(bool(no_attention))
     c.active_devices = int(active_devices)
     return c
@@ -262,7 +264,7 @@ def gdp_greedy(g: Graph, cfg: Config, logits, placement, logprob=None, ws=None, 
 
 
 def cost_kernel(g: Graph, t: Topo) -> int:
-    """Which cost kernel gdp_cost runs for (g, t): 4 windowed, 3 warp-cooperative, 2 owner-lane,
+    """Which cost kernel gdp_cost runs for (g, t): 5 simulation + memory warps, 3 warp-cooperative,
     1 global-memory (include/gdp.h gdp_cost_kernel)."""
     k = int(lib().gdp_cost_kernel(g.h, t.h))
     if k == 0:
@@ -270,9 +272,32 @@ def cost_kernel(g: Graph, t: Topo) -> int:
     return k
 
 
-def gdp_cost(g: Graph, t: Topo, placements, B: int, rep, peak_mem, busy, reward, ws, stream=None):
+def gdp_cost(g: Graph, t: Topo, placements, B: int, rep, peak_mem, busy, reward, ws, stream=None, kernel: int = 0):
+    """kernel = 0: the automatic choice; 5 / 3 / 1 forces a kernel (gdp_cost_with_kernel, tests)."""
+    if kernel:
+        _check(lib().gdp_cost_with_kernel(g.h, t.h, _t_ptr(placements), B, _t_ptr(rep), _t_ptr(peak_mem),
+                                          _t_ptr(busy), _t_ptr(reward), _t_ptr(ws), ws.numel(), kernel,
+                                          _stream(stream)), "gdp_cost_with_kernel")
+        return
     _check(lib().gdp_cost(g.h, t.h, _t_ptr(placements), B, _t_ptr(rep), _t_ptr(peak_mem), _t_ptr(busy),
                           _t_ptr(reward), _t_ptr(ws), ws.numel(), _stream(stream)), "gdp_cost")
+
+
+def debug_tensor(g: Graph, cfg: Config, ws, what: int, layer: int):
+    """gdp_debug_tensor: a torch view (on the workspace's device) of a saved intermediate:
+    what 0 max-pool argmax of GNN layer (int32 N x 64), 1 FFN hidden m of XL layer (fp32 N x 256,
+    Kahn order), 2 the no-attention map o (fp32 N x 64, Kahn order)."""
+    import torch
+    ptr = ctypes.c_void_p()
+    _check(lib().gdp_debug_tensor(g.h, ctypes.byref(cfg), _t_ptr(ws), ws.numel(), what, layer, ctypes.byref(ptr)),
+           "gdp_debug_tensor")
+    n = g.N * (64 if what in (0, 2) else 256)
+    esz = 4
+    base = ws.data_ptr()
+    off = ptr.value - base
+    assert 0 <= off and off + n * esz <= ws.numel(), "debug tensor outside the workspace"
+    t = ws[off:off + n * esz].view(torch.int32 if what == 0 else torch.float32)
+    return t.view(g.N, -1)
 
 
 def gdp_advantage(reward, B: int, run_sum, run_count, adv, stream=None):

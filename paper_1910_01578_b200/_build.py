@@ -14,8 +14,23 @@ def sources():
     return sorted(glob.glob(os.path.join(HERE, "csrc", "*.cu"))) + sorted(glob.glob(os.path.join(HERE, "csrc", "*.cuh")))
 
 
+FLAGS_FILE = SO + ".flags"
+
+
+def _extra():
+    return os.environ.get("GDP_NVCC_EXTRA", "").split()   # experiment macros (e.g. -DCOST5_PROF)
+
+
 def stale() -> bool:
     if not os.path.exists(SO):
+        return True
+    # the flags the library was built with are stored next to it: a build with other
+    # experiment macros is never reused silently
+    try:
+        with open(FLAGS_FILE) as f:
+            if f.read().split() != _extra():
+                return True
+    except OSError:
         return True
     t = os.path.getmtime(SO)
     hdr = os.path.join(os.path.dirname(HERE), "include", "gdp.h")
@@ -25,9 +40,11 @@ def stale() -> bool:
 def build(force: bool = False) -> str:
     if force or stale():
         cu = [f for f in sources() if f.endswith(".cu")]
-        extra = os.environ.get("GDP_NVCC_EXTRA", "").split()   # experiment macros (tools/variants)
+        extra = _extra()
         cmd = [NVCC] + FLAGS + extra + ["-o", SO] + cu
         subprocess.check_call(cmd)
+        with open(FLAGS_FILE, "w") as f:
+            f.write(" ".join(extra))
     return SO
 
 

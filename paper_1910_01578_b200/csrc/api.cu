@@ -98,7 +98,7 @@ static gdp_status check_config(const gdp_config *c) {
   if (c->num_devices < 1 || c->num_devices > kMaxD) return fail(GDP_ERR_ARG, "num_devices must be in 1..8");
   if (c->seg_len < 1) return fail(GDP_ERR_ARG, "seg_len must be >= 1");
   if (c->mem_len < -1) return fail(GDP_ERR_ARG, "mem_len must be >= -1");
-  if (c->tensor_cores != 0 && c->tensor_cores != 1) return fail(GDP_ERR_ARG, "tensor_cores must be 0 or 1");
+  if (c->tensor_cores < 0 || c->tensor_cores > 2) return fail(GDP_ERR_ARG, "tensor_cores must be 0, 1 or 2");
   if (c->no_attention != 0 && c->no_attention != 1) return fail(GDP_ERR_ARG, "no_attention must be 0 or 1");
   if (c->active_devices < 0 || c->active_devices > c->num_devices)
     return fail(GDP_ERR_ARG, "active_devices must be in 0..num_devices");
@@ -193,8 +193,8 @@ bool ws_layout(const gdp_graph_s *g, int d, int B, char *base, WS *w) {
   // cost scratch: one region per placement, large enough for either cost kernel
   size_t v1 = (2 + 2) * N * sizeof(int) + N * sizeof(int2) + E * sizeof(int4) + N * sizeof(int);
   size_t v2 = cost2_scratch_per_placement(g->N, g->E, g->nbig);
-  size_t v4 = cost4_scratch_per_placement(g->N, g->E, g->nbig);
-  z.c_per_place = (std::max(std::max(v1, v2), v4) + 255) & ~(size_t)255;
+  size_t v5 = cost5_scratch_per_placement(g->N, g->E, g->ngbig5);
+  z.c_per_place = (std::max(std::max(v1, v2), v5) + 255) & ~(size_t)255;
   z.c_scratch = reinterpret_cast<unsigned char *>(take(Bc * z.c_per_place));
   if (z.c_scratch) {
     // v1 view of the same bytes
@@ -296,7 +296,7 @@ const char *gdp_build_info(void) { return "libgdp sm_100a built " __DATE__ " " _
 
 int32_t gdp_cost_kernel(gdp_graph g, gdp_topo t) {
   if (!g || !t) { set_error("gdp_cost_kernel: NULL handle"); return 0; }
-  return cost_kernel_choice(g, t);
+  return cost_kernel_choice(g, t, 0);
 }
 
 gdp_status gdp_default_config(int32_t d, gdp_config *out) {
@@ -515,6 +515,21 @@ gdp_status gdp_graph_create(int32_t N, int32_t F, const float *feat, int64_t E, 
   UP(bigid, bigid.data(), N * sizeof(int));
   UP(big_in, big_in.data(), big_in.size() * sizeof(int));
   UP(big_out, big_out.data(), big_out.size() * sizeof(int));
+  {
+    Cost5Host h5;
+    cost5_build(N, E, optr.data(), oidx.data(), iptr.data(), cost.data(), reinterpret_cast<const long long *>(output_bytes),
+                &h5);
+    g->c5_ok = h5.ok;
+    g->nsrc5 = (int)h5.srcs.size();
+    g->nbigb5 = (int)h5.bigb.size();
+    g->ngbig5 = (int)h5.gbig.size();
+    UP(rec5, h5.rec.data(), h5.rec.size() * sizeof(Rec5));
+    UP(erec5, h5.erec.data(), h5.erec.size() * sizeof(Rec5));
+    UP(srcs5, h5.srcs.data(), h5.srcs.size() * sizeof(int));
+    UP(gbig5, h5.gbig.data(), h5.gbig.size() * sizeof(int));
+    UP(outdeg5, h5.outdeg.data(), h5.outdeg.size() * sizeof(int));
+    UP(bigb5, h5.bigb.data(), h5.bigb.size() * sizeof(unsigned));
+  }
 #undef UP
   *out = g;
   return GDP_OK;
@@ -524,7 +539,8 @@ gdp_status gdp_graph_destroy(gdp_graph g) {
   if (!g) return GDP_OK;
   void *ptrs[] = {g->X, g->nbr_ptr, g->nbr_idx, g->heavy, g->out_ptr, g->out_idx, g->out_src, g->in_ptr, g->in_idx,
                   g->cost, g->out_bytes, g->mem_bytes, g->perm, g->leader, g->nrec, g->erec, g->irec,
-                  g->cnt0, g->bigid, g->big_in, g->big_out};
+                  g->cnt0, g->bigid, g->big_in, g->big_out, g->rec5, g->erec5, g->srcs5, g->gbig5, g->outdeg5,
+                  g->bigb5};
   for (void *p : ptrs)
     if (p) cudaFree(p);
   delete g;
@@ -595,6 +611,20 @@ static gdp_status carve_any(const gdp_graph_s *g, int d, int Bneed, void *ws, si
   return carve(g, d, Bneed, ws, ws_bytes, w);
 }
 
+gdp_status gdp_debug_tensor(gdp_graph g, const gdp_config *c, void *ws, size_t ws_bytes, int32_t what,
+                            int32_t layer, void **out) {
+  if (!g || !out) return fail(GDP_ERR_ARG, "NULL argument");
+  gdp_status st = check_config(c);
+  if (st != GDP_OK) return st;
+  WS w;
+  st = carve_any(g, c->num_devices, 1, ws, ws_bytes, &w);
+  if (st != GDP_OK) return st;
+  if (what == 0 && layer >= 0 && layer < kGNN) { *out = w.ARG[layer]; return GDP_OK; }
+  if (what == 1 && layer >= 0 && layer < 3) { *out = w.L[layer].m; return GDP_OK; }
+  if (what == 2 && layer >= 0 && layer < 3) { *out = w.L[layer].o; return GDP_OK; }
+  return fail(GDP_ERR_ARG, "gdp_debug_tensor: unknown (what, layer)");
+}
+
 gdp_status gdp_embed(gdp_graph g, const gdp_config *c, const float *theta, float *node_emb, void *ws,
                      size_t ws_bytes, void *stream) {
   if (!g || !theta || !node_emb) return fail(GDP_ERR_ARG, "NULL argument");
@@ -603,7 +633,7 @@ gdp_status gdp_embed(gdp_graph g, const gdp_config *c, const float *theta, float
   WS w;
   st = carve_any(g, c->num_devices, 1, ws, ws_bytes, &w);
   if (st != GDP_OK) return st;
-  set_tensor_cores(c->tensor_cores != 0);
+  set_tensor_cores(c->tensor_cores);
   set_no_attention(c->no_attention != 0);
   return run_embed(g, theta, node_emb, w, c->num_devices, static_cast<cudaStream_t>(stream));
 }
@@ -616,7 +646,7 @@ gdp_status gdp_place(gdp_graph g, const gdp_config *c, const float *theta, const
   WS w;
   st = carve_any(g, c->num_devices, 1, ws, ws_bytes, &w);
   if (st != GDP_OK) return st;
-  set_tensor_cores(c->tensor_cores != 0);
+  set_tensor_cores(c->tensor_cores);
   set_no_attention(c->no_attention != 0);
   return run_place(g, c, theta, node_emb, logits, w, static_cast<cudaStream_t>(stream));
 }
@@ -707,6 +737,12 @@ gdp_status gdp_clip_adam(const float *grad, int64_t n, double max_norm, double l
 
 gdp_status gdp_cost(gdp_graph g, gdp_topo t, const uint8_t *placements, int32_t B, gdp_sim_report *rep,
                     int64_t *peak_mem, int64_t *busy, double *reward, void *ws, size_t ws_bytes, void *stream) {
+  return gdp_cost_with_kernel(g, t, placements, B, rep, peak_mem, busy, reward, ws, ws_bytes, 0, stream);
+}
+
+gdp_status gdp_cost_with_kernel(gdp_graph g, gdp_topo t, const uint8_t *placements, int32_t B, gdp_sim_report *rep,
+                                int64_t *peak_mem, int64_t *busy, double *reward, void *ws, size_t ws_bytes,
+                                int32_t kernel, void *stream) {
   if (!g || !t || !placements || !rep || !reward) return fail(GDP_ERR_ARG, "NULL argument");
   if (B < 1) return fail(GDP_ERR_ARG, "B must be >= 1");
   // int32 device time: the schedule never exceeds sum(durations) + sum(transfers)
@@ -725,8 +761,11 @@ gdp_status gdp_cost(gdp_graph g, gdp_topo t, const uint8_t *placements, int32_t 
   WS w;
   gdp_status st = carve_any(g, t->d, B, ws, ws_bytes, &w);
   if (st != GDP_OK) return st;
+  if (kernel != 0 && kernel != 1 && kernel != 3 && kernel != 5) return fail(GDP_ERR_ARG, "kernel must be 0, 1, 3 or 5");
+  if (kernel != 0 && cost_kernel_choice(g, t, kernel) != kernel)
+    return fail(GDP_ERR_ARG, "the requested cost kernel does not apply to this graph and topology");
   return launch_cost(g, t, placements, B, rep, reinterpret_cast<long long *>(peak_mem),
-                     reinterpret_cast<long long *>(busy), reward, w, static_cast<cudaStream_t>(stream));
+                     reinterpret_cast<long long *>(busy), reward, w, kernel, static_cast<cudaStream_t>(stream));
 }
 
 gdp_status gdp_advantage(const double *reward, int32_t B, double *run_sum, int64_t *run_count, double *adv,
@@ -751,7 +790,7 @@ gdp_status gdp_policy_grad(gdp_graph g, const gdp_config *c, const float *theta,
   WS w;
   st = carve_any(g, c->num_devices, B, ws, ws_bytes, &w);
   if (st != GDP_OK) return st;
-  set_tensor_cores(c->tensor_cores != 0);
+  set_tensor_cores(c->tensor_cores);
   set_no_attention(c->no_attention != 0);
   return run_policy_grad(g, c, theta, logits, placements, B, adv, logprob, old_logprob, clip_eps, entropy_coef,
                          loss_scale, grad, w, static_cast<cudaStream_t>(stream));

@@ -59,13 +59,19 @@ struct gdp_graph_s {
   long long sum_edge_out_bytes = 0;                 // sum over edges of producer output bytes
   long long n_edges_cross_max = 0;
   int max_indeg = 0, max_outdeg = 0;
-  int min_cost = 0;   // smallest compute cost (k_cost4 needs every duration >= 1)
-  long long min_edge_bytes = 0;   // smallest producer output over edges (k_cost4 window); LLONG_MAX: no edges
+  int min_cost = 0;   // smallest compute cost (k_cost5 needs every duration >= 1)
+  long long min_edge_bytes = 0;   // smallest producer output over edges (k_cost5: shortest transfer); LLONG_MAX: no edges
   // shared-memory cost model records (cost2.cuh)
   void *nrec = nullptr, *erec = nullptr, *irec = nullptr;
   unsigned *cnt0 = nullptr;
   int *bigid = nullptr, *big_in = nullptr, *big_out = nullptr;
   int nbig = 0;
+  // k_cost5 records (cost5.cu)
+  bool c5_ok = false;
+  void *rec5 = nullptr, *erec5 = nullptr;
+  int *srcs5 = nullptr, *gbig5 = nullptr, *outdeg5 = nullptr;
+  unsigned *bigb5 = nullptr;
+  int nsrc5 = 0, nbigb5 = 0, ngbig5 = 0;
 };
 
 struct gdp_topo_s {
@@ -157,8 +163,11 @@ inline double gemm_bytes(const GemmArgs &a) {
 // entry point enabled tensor cores (gdp_config.tensor_cores)
 bool tc_eligible(const GemmArgs &a);
 void launch_gemm_tc(const GemmArgs &a, cudaStream_t s);
-void set_tensor_cores(bool on);
+// gdp_config.tensor_cores: 0 SIMT fp32, 1 tcgen05 dense maps + attention, 2 tcgen05 dense maps with
+// the SIMT attention (diagnostic: compares the attention tiles inside one tensor-core step)
+void set_tensor_cores(int mode);
 bool tensor_cores_on();
+bool tensor_core_attention_on();
 bool attn_fwd_tc_eligible(int S, int M);
 void launch_attn_fwd_tc(const float *qkv, float *o, float *lse, int N, int S, int M, cudaStream_t s);
 bool attn_bwd_tc_eligible(int S, int M);
@@ -233,10 +242,12 @@ void launch_clip_adam(const float *g, long long n, double max_norm, double lr, d
                       cudaStream_t s);
 
 // cost model
-int cost_kernel_choice(const gdp_graph_s *g, const gdp_topo_s *t);
+// kernel gdp_cost runs (5, 3 or 1); `force` != 0 asks whether that kernel applies (it is
+// returned if so, else the automatic choice)
+int cost_kernel_choice(const gdp_graph_s *g, const gdp_topo_s *t, int force);
 gdp_status launch_cost(const gdp_graph_s *g, const gdp_topo_s *t, const uint8_t *D, int B,
                        gdp_sim_report *rep, long long *peak, long long *busy, double *reward, const WS &w,
-                       cudaStream_t s);
+                       int force, cudaStream_t s);
 void launch_advantage(const double *r, int B, double *sum, long long *cnt, double *adv, cudaStream_t s);
 
 }  // namespace gdp

@@ -412,19 +412,41 @@ static TopoArgs topo_args(const gdp_topo_s *t) {
   return T;
 }
 
-int cost_kernel_choice(const gdp_graph_s *g, const gdp_topo_s *t) {
-  if (getenv("GDP_COST_V1") != nullptr) return 1;
+static Cost5Graph cost5_graph(const gdp_graph_s *g) {
+  Cost5Graph C;
+  C.N = g->N; C.E = g->E; C.ok = g->c5_ok ? 1 : 0;
+  C.rec = static_cast<const Rec5 *>(g->rec5); C.erec = static_cast<const Rec5 *>(g->erec5);
+  C.irec = static_cast<const IRec *>(g->irec);
+  C.out_idx = g->out_idx; C.out_src = g->out_src; C.cost = g->cost; C.leader = g->leader;
+  C.srcs = g->srcs5; C.outdeg = g->outdeg5; C.gbig0 = g->gbig5; C.bigb0 = g->bigb5;
+  C.out_bytes = g->out_bytes; C.mem_bytes = g->mem_bytes;
+  C.nsrc = g->nsrc5; C.nbigb = g->nbigb5; C.ngbig = g->ngbig5; C.has_coloc = g->has_coloc ? 1 : 0;
+  return C;
+}
+
+// 5: k_cost5 (cost5.cu) whenever every duration and every transfer takes >= 1 tick and its
+// state fits in shared memory; 3: k_cost3 (cost2.cu, zero-duration ops / zero-tick transfers);
+// 1: k_cost below (per-placement state larger than shared memory)
+int cost_kernel_choice(const gdp_graph_s *g, const gdp_topo_s *t, int force) {
   const TopoArgs T = topo_args(t);
-  if (cost4_window(T, g->min_cost, g->N, g->min_edge_bytes) > 0) return 4;
-  if (cost2_smem_bytes(g->N) <= 227 * 1024) return getenv("GDP_COST_V2") != nullptr ? 2 : 3;
-  return 1;
+  const bool ok5 = cost5_eligible(T, cost5_graph(g), g->min_cost, g->min_edge_bytes);
+  const bool ok3 = cost2_smem_bytes(g->N) <= 227 * 1024;
+  if (force == 5 && ok5) return 5;
+  if (force == 3 && ok3) return 3;
+  if (force == 1) return 1;
+  return ok5 ? 5 : (ok3 ? 3 : 1);
 }
 
 gdp_status launch_cost(const gdp_graph_s *g, const gdp_topo_s *t, const uint8_t *D, int B, gdp_sim_report *rep,
-                       long long *peak, long long *busy, double *reward, const WS &w, cudaStream_t s) {
+                       long long *peak, long long *busy, double *reward, const WS &w, int force, cudaStream_t s) {
   const TopoArgs T = topo_args(t);
-  static const bool force_v1 = getenv("GDP_COST_V1") != nullptr;
-  if (!force_v1) {
+  const int k = cost_kernel_choice(g, t, force);
+  if (k == 5 && launch_cost5(cost5_graph(g), T, g->min_cost, g->min_edge_bytes, D, B, w.c_scratch, w.c_per_place, rep,
+                             peak, busy, reward, s)) {
+    GDP_LAUNCH_CHECK("k_cost5");
+    return GDP_OK;
+  }
+  if (k == 3) {
     Cost2Graph C;
     C.N = g->N; C.E = g->E;
     C.nrec = static_cast<const NRec *>(g->nrec); C.erec = static_cast<const NRec *>(g->erec);
@@ -432,12 +454,8 @@ gdp_status launch_cost(const gdp_graph_s *g, const gdp_topo_s *t, const uint8_t 
     C.cnt0 = g->cnt0; C.bigid = g->bigid; C.big_in = g->big_in; C.big_out = g->big_out; C.nbig = g->nbig;
     C.out_idx = g->out_idx; C.out_src = g->out_src; C.in_ptr = g->in_ptr; C.cost = g->cost; C.leader = g->leader;
     C.out_bytes = g->out_bytes; C.mem_bytes = g->mem_bytes; C.has_coloc = g->has_coloc ? 1 : 0;
-    if (launch_cost4(C, T, g->min_cost, g->min_edge_bytes, D, B, w.c_scratch, w.c_per_place, rep, peak, busy, reward, s)) {
-      GDP_LAUNCH_CHECK("k_cost4");
-      return GDP_OK;
-    }
     if (launch_cost2(C, T, D, B, w.c_scratch, w.c_per_place, rep, peak, busy, reward, s)) {
-      GDP_LAUNCH_CHECK("k_cost2");
+      GDP_LAUNCH_CHECK("k_cost3");
       return GDP_OK;
     }
   }

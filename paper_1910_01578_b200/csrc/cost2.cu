@@ -1,6 +1,7 @@
-// Cost model, shared-memory kernel (the default; cost.cu's k_cost is the fallback for graphs
-// whose per-placement state does not fit in shared memory).  Same event semantics as the
-// oracle (DESIGN.md §"Cost model"); this is a re-formulation for a GPU warp:
+// Cost model, k_cost3: the warp-cooperative instant-by-instant kernel that gdp_cost runs when
+// k_cost5 (cost5.cu) does not apply -- zero-duration ops or zero-tick transfers, which need
+// same-instant rounds (cost.cu's k_cost takes graphs whose state does not fit in shared
+// memory).  Same event semantics as the oracle (DESIGN.md §7 "Cost model"):
 //
 //  * lane k < d OWNS device k: its running op and finish time (registers), its FIFO of
 //    available ops, and its outgoing channels (k -> t): channel state is only ever touched by
@@ -259,255 +260,8 @@ __device__ __forceinline__ bool prologue(const Cost2Graph &G, const TopoArgs &T,
   return true;
 }
 
-__global__ void __launch_bounds__(32) k_cost2(Cost2Graph G, TopoArgs T, const uint8_t *__restrict__ Dall,
-                                              unsigned char *scratch, size_t per_place, gdp_sim_report *rep,
-                                              long long *peak_out, long long *busy_out, double *reward, int dbg) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  Smem &S = *reinterpret_cast<Smem *>(smem_raw);
-  const Ctx C = make_ctx(G, T, Dall, scratch, per_place, smem_raw);
-  const int N = C.N, d = C.d, b = C.b, lane = C.lane;
-  unsigned *cnt = C.cnt, *Dn = C.Dn;
-  Ent *fifo = C.fifo, *chq = C.chq;
-  NRec *ov = C.ov;
-  int *bigc = C.bigc;
-  int flag, ftail;
-  long long mymem, mybusy, cross;
-  if (!prologue(G, T, S, C, rep, peak_out, busy_out, reward, flag, mymem, mybusy, cross, ftail)) return;
-  int fhead = 0;
-  if (dbg == 1) return;
-  // ---------------------------------------------------------------- event loop
-  NRec run;
-  run.id = -1; run.cost = 0; run.ob = run.oe = run.ib = run.ie = 0; run.bytes = 0;
-  int fin = 0, running = 0, mk = 0, dispatched = 0, multi = 0, my_arr = INF;
-  int cur = 0, cur_inst = -2, nxt_id = -1, nxt_inst = -2;
-  int t = 0, n_inst = 0, n_round = 0, n_fin = 0;
-  const bool dl = lane < d;
-  for (int inst = 0;; inst++) {
-    if (inst > 0) {
-      const int cand = dl ? min(running ? fin : INF, my_arr) : INF;
-      t = __reduce_min_sync(0xffffffffu, cand);
-      if (t == INF) break;
-    }
-    {  // records staged at the previous instant may still be in flight
-      const bool need = (dl && running && fin == t && cur_inst == inst - 1) || multi;
-      if (__any_sync(0xffffffffu, need)) cp_wait0(); else cp_wait1();
-    }
-    n_inst++;
-    for (int round = 0;; round++) {
-      n_round++;
-      if (round > 0) cp_wait0();
-      __syncwarp();
-      if (dl) {
-        // (1) arrivals on my outgoing channels (only the first round can have any)
-        if (round == 0) {
-          multi = 0;
-          if (my_arr <= t) {
-            int m = INF;
-            for (int q = 0; q < d; q++) {
-              int a = S.ch_arr[lane][q];
-              if (a <= t) {
-                int head = S.ch_head[lane][q];
-                const int tail = S.ch_tail[lane][q];
-                int popped = 0;
-                while (a <= t) {
-                  if (popped) { cp_commit(); cp_wait0(); }   // the refill issued by the previous pop
-                  Ent &e = S.cc[lane][q][head % KC];
-                  add_mem(S.memlo, S.memhi, q, e.bytes);
-                  if (dec_counter(cnt, e.r.id, 0, bigc, G.bigid, G.nbig)) push_inc(S, ov, q, e.r);
-                  if (head + KC < tail) cp_ent(&e, chq + S.ch_off[lane][q] + head + KC);
-                  head++;
-                  multi |= popped;
-                  popped = 1;
-                  a = head < tail ? S.cc[lane][q][head % KC].t : INF;
-                }
-                S.ch_head[lane][q] = head;
-                S.ch_arr[lane][q] = a;
-              }
-              m = min(m, a);
-            }
-            my_arr = m;
-          }
-        }
-        // (2) my op finishes now
-        if (running && fin == t) {
-          n_fin++;
-          running = 0;
-          const int k = lane;
-          // frees: copies this op held, producers whose last consumer it was, sink output
-          const int nin = run.ie - run.ib;
-          for (int j = 0; j < nin; j++) {
-            IRec ir;
-            if (j < SI) ir = S.st_in[k][cur][j];
-            else ir = G.irec[run.ib + j];
-            const int du = dev_of(Dn, ir.u);
-            if (du != k) add_mem(S.memlo, S.memhi, k, -ir.bytes);
-            if (dec_counter(cnt, ir.u, 1, bigc, G.bigid, G.nbig)) add_mem(S.memlo, S.memhi, du, -ir.bytes);
-          }
-          if (run.oe == run.ob) add_mem(S.memlo, S.memhi, k, -run.bytes);
-          // out-edges in ascending consumer id: same device -> input arrives now; cross ->
-          // FIFO on channel (k -> tw): arrival = max(t, channel free) + transfer
-          const int nout = run.oe - run.ob;
-          for (int j = 0; j < nout; j++) {
-            NRec wr;
-            if (j < SO) wr = S.st_out[k][cur][j];
-            else load_rec(wr, G.erec + run.ob + j);
-            const int tw = dev_of(Dn, wr.id);
-            if (tw == k) {
-              if (dec_counter(cnt, wr.id, 0, bigc, G.bigid, G.nbig)) push_inc(S, ov, k, wr);
-              continue;
-            }
-            const int arr = max(t, S.ch_free[k][tw]) + xfer_time(run.bytes, k, tw, T);
-            S.ch_free[k][tw] = arr;
-            if (arr == t) {   // zero-time transfer: the copy lands now
-              add_mem(S.memlo, S.memhi, tw, run.bytes);
-              if (dec_counter(cnt, wr.id, 0, bigc, G.bigid, G.nbig)) push_inc(S, ov, tw, wr);
-              continue;
-            }
-            const int head = S.ch_head[k][tw], pos = S.ch_tail[k][tw];
-            if (pos < head + KC) store_ent(&S.cc[k][tw][pos % KC], wr, arr, run.bytes);
-            else store_ent(chq + S.ch_off[k][tw] + pos, wr, arr, run.bytes);
-            if (pos == head) {
-              S.ch_arr[k][tw] = arr;
-              my_arr = min(my_arr, arr);
-            }
-            S.ch_tail[k][tw] = pos + 1;
-          }
-        }
-      }
-      __syncwarp();
-      bool zero = false, req = false;
-      if (dl) {
-        // (3) ops made available now (ready = t) join my FIFO in id order
-        const int n = S.inc_n[lane];
-        if (n > 0) {
-          NRec *L = &S.inc[lane][0];
-          NRec *O = ov + S.doff[lane];
-          for (int i = 1; i < n; i++) {   // insertion sort by id (n is small except after wide fan-outs)
-            NRec key;
-            load_rec(key, i < NINC ? &L[i] : &O[i]);
-            int j = i - 1;
-            while (j >= 0) {
-              NRec *pj = j < NINC ? &L[j] : &O[j];
-              if (pj->id <= key.id) break;
-              copy_rec(j + 1 < NINC ? &L[j + 1] : &O[j + 1], pj);
-              j--;
-            }
-            copy_rec(j + 1 < NINC ? &L[j + 1] : &O[j + 1], &key);
-          }
-          Ent *F = fifo + S.doff[lane];
-          if (round > 0) {
-            // zero-duration corner case: entries appended earlier in this instant share ready
-            // time t and must stay merged by id with the new ones (rare path, done in global)
-            for (int i = fhead; i < min(ftail, fhead + KF); i++) F[i] = S.fc[lane][i % KF];
-            int tail = ftail;
-            for (int i = 0; i < n; i++) store_ent(&F[tail++], i < NINC ? L[i] : O[i], t, 0);
-            int s0 = ftail;
-            while (s0 > fhead && F[s0 - 1].t == t) s0--;
-            for (int i = s0 + 1; i < tail; i++) {
-              Ent key = F[i];
-              int j = i - 1;
-              while (j >= s0 && F[j].r.id > key.r.id) { F[j + 1] = F[j]; j--; }
-              F[j + 1] = key;
-            }
-            for (int i = fhead; i < min(tail, fhead + KF); i++) S.fc[lane][i % KF] = F[i];
-            ftail = tail;
-            nxt_id = -1;
-          } else {
-            for (int i = 0; i < n; i++) {
-              const NRec &r = i < NINC ? L[i] : O[i];
-              if (ftail < fhead + KF) store_ent(&S.fc[lane][ftail % KF], r, t, 0);
-              else store_ent(F + ftail, r, t, 0);
-              ftail++;
-            }
-          }
-          S.inc_n[lane] = 0;
-        }
-        // (4) dispatch my FIFO head if idle
-        if (!running && fhead < ftail) {
-          Ent &e = S.fc[lane][fhead % KF];
-          load_rec(run, &e.r);
-          const int dur = (run.cost & 0x7fffffff) * T.speed[lane];
-          running = 1;
-          fin = t + dur;
-          mk = max(mk, fin);
-          add_mem(S.memlo, S.memhi, lane, run.bytes);
-          zero = dur == 0;
-          dispatched++;
-          cur ^= 1;
-          if (run.id == nxt_id) {   // its records were staged while it waited
-            cur_inst = nxt_inst;
-          } else {                  // stage now
-            cur_inst = inst;
-            S.sreq[lane] = run;
-            S.sreq_slot[lane] = cur;
-            req = true;
-          }
-          nxt_id = -1;
-          if (fhead + KF < ftail) cp_ent(&e, fifo + S.doff[lane] + fhead + KF);
-          fhead++;
-        }
-        // (5) stage the records of the op now waiting at my FIFO head
-        if (running && nxt_id < 0 && fhead < ftail && !req) {
-          const NRec r = S.fc[lane][fhead % KF].r;
-          S.sreq[lane] = r;
-          S.sreq_slot[lane] = cur ^ 1;
-          nxt_id = r.id;
-          nxt_inst = inst;
-          req = true;
-        }
-      }
-      __syncwarp();
-      unsigned rm = __ballot_sync(0xffffffffu, req);
-      while (rm) {   // warp-cooperative cp.async of the requested records
-        const int k = __ffs(rm) - 1;
-        rm &= rm - 1;
-        const NRec rv = S.sreq[k];
-        const int sl = S.sreq_slot[k];
-        const int no = min(rv.oe - rv.ob, SO), ni = min(rv.ie - rv.ib, SI);
-        if (lane < 2 * no) {
-          cp16(reinterpret_cast<int4 *>(&S.st_out[k][sl][lane >> 1]) + (lane & 1),
-               reinterpret_cast<const int4 *>(G.erec + rv.ob + (lane >> 1)) + (lane & 1));
-        } else if (lane < 2 * no + ni) {
-          cp16(&S.st_in[k][sl][lane - 2 * no], G.irec + rv.ib + (lane - 2 * no));
-        }
-      }
-      cp_commit();
-      // (6) peak after all changes of this round
-      if (dl) S.peak[lane] = max(S.peak[lane], read_mem(S.memlo, S.memhi, lane));
-      if (!__any_sync(0xffffffffu, zero)) break;
-    }
-  }
-  cp_wait0();
-  mk = __reduce_max_sync(0xffffffffu, mk);
-  dispatched = __reduce_add_sync(0xffffffffu, dispatched);
-  __syncwarp();
-  int oom = 0;
-  if (dl) {
-    oom = S.peak[lane] > T.cap[lane];
-    if (peak_out) peak_out[(size_t)b * d + lane] = S.peak[lane];
-    if (busy_out) busy_out[(size_t)b * d + lane] = mybusy;
-  }
-  if (dbg == 2 && busy_out && lane == 0) {   // diagnostics: instants / rounds / my finishes
-    busy_out[(size_t)b * d] = n_inst;
-    if (d > 1) busy_out[(size_t)b * d + 1] = n_round;
-    if (d > 2) busy_out[(size_t)b * d + 2] = n_fin;
-  }
-  oom = __reduce_or_sync(0xffffffffu, oom);
-  if (lane == 0) {
-    gdp_sim_report R = empty_report();
-    R.makespan = mk;
-    R.cross_bytes = cross;
-    R.violation = (flag & 1) ? 1 : (oom ? 2 : 0);
-    if (dispatched != N) R.violation = 3;   // cannot happen for a validated DAG
-    R.valid = R.violation == 0;
-    rep[b] = R;
-    reward[b] = R.valid ? -__dsqrt_rn(__ddiv_rn((double)mk, 1e6)) : -10.0;
-  }
-}
-
 // ------------------------------------------------------------------------------------------
-// k_cost3: same state and event semantics as k_cost2, with the work of one instant spread over
-// the whole warp instead of the owning lane:
+// k_cost3: the work of one instant spread over the whole warp:
 //  * channel (k -> q) is owned by lane (8k + q) / 2, which caches its head arrival in a
 //    register and pops its arrivals (all owners in parallel);
 //  * a finishing op's in-edges and out-edges are handled one per lane; out-edges into the
@@ -857,15 +611,11 @@ bool launch_cost2(const Cost2Graph &G, const TopoArgs &T, const uint8_t *D, int 
   static_assert(2 * SO + SI <= 32, "one staging request fits one warp pass");
   static size_t configured = 0;
   if (smem > 40 * 1024 && smem > configured) {
-    cudaFuncSetAttribute(k_cost2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaFuncSetAttribute(k_cost3, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     configured = smem;
   }
-  note_launch("k_cost2", s);
-  static const int dbg = getenv("GDP_COST_DBG") ? atoi(getenv("GDP_COST_DBG")) : 0;
-  static const bool v2 = getenv("GDP_COST_V2") != nullptr;   // owner-lane kernel (comparison)
-  if (v2) k_cost2<<<B, 32, smem, s>>>(G, T, D, scratch, per_place, rep, peak, busy, reward, dbg);
-  else k_cost3<<<B, 32, smem, s>>>(G, T, D, scratch, per_place, rep, peak, busy, reward, dbg);
+  note_launch("k_cost3", s);
+  k_cost3<<<B, 32, smem, s>>>(G, T, D, scratch, per_place, rep, peak, busy, reward, 0);
   return true;
 }
 

@@ -1,5 +1,7 @@
-// Records and launcher of the shared-memory cost model (cost2.cu).
+// Records and launchers of the shared-memory cost kernels (k_cost5 in cost5.cu, k_cost3 in cost2.cu).
 #pragma once
+#include <vector>
+
 #include "common.cuh"
 
 namespace gdp {
@@ -29,14 +31,42 @@ struct Cost2Graph {
   int has_coloc;
 };
 
+// ---- k_cost5 (cost5.cu): graph-static records of the simulation warp
+struct __align__(16) Rec5 {   // one op, 32 bytes
+  int id, cost, ob, ib;       // id, compute cost, first out-edge slot, first in-edge slot
+  int nn;                     // out-degree | in-degree << 16
+  int cinfo;                  // input counter: kind (bits 0-1: 0 = at most one input, 1 = two inputs
+                              // (flag bit), 2 = byte counter, 3 = global counter) | index << 2
+  long long bytes;            // output bytes
+};
+struct Cost5Host {            // host images built at graph creation (cost5_build)
+  bool ok = false;
+  std::vector<Rec5> rec, erec;  // erec[e] = rec[out_idx[e]] (out-CSR order)
+  std::vector<int> srcs, gbig, outdeg;
+  std::vector<unsigned> bigb;   // byte counters (in-degree 3..254), 4 per word, 16-byte padded
+};
+struct Cost5Graph {
+  int N;
+  long long E;
+  int ok;
+  const Rec5 *rec, *erec;
+  const IRec *irec;
+  const int *out_idx, *out_src, *cost, *leader, *srcs, *outdeg, *gbig0;
+  const unsigned *bigb0;
+  const long long *out_bytes, *mem_bytes;
+  int nsrc, nbigb, ngbig, has_coloc;
+};
+gdp_status cost5_build(int N, long long E, const int *optr, const int *oidx, const int *iptr, const int *cost,
+                       const long long *out_bytes, Cost5Host *h);
+size_t cost5_smem_bytes(int N, int nbigb);
+size_t cost5_scratch_per_placement(int N, long long E, int ngbig);
+bool cost5_eligible(const TopoArgs &T, const Cost5Graph &G, int min_cost, long long min_edge_bytes);
+bool launch_cost5(const Cost5Graph &G, const TopoArgs &T, int min_cost, long long min_edge_bytes, const uint8_t *D,
+                  int B, unsigned char *scratch, size_t per_place, gdp_sim_report *rep, long long *peak,
+                  long long *busy, double *reward, cudaStream_t s);
+
 size_t cost2_smem_bytes(int N);
 size_t cost2_scratch_per_placement(int N, long long E, int nbig);
-size_t cost4_smem_bytes(int N);
-int cost4_window(const TopoArgs &T, int min_cost, int N, long long min_edge_bytes);   // window length, 0 = not eligible
-size_t cost4_scratch_per_placement(int N, long long E, int nbig);
-bool launch_cost4(const Cost2Graph &G, const TopoArgs &T, int min_cost, long long min_edge_bytes, const uint8_t *D, int B,
-                  unsigned char *scratch, size_t per_place, gdp_sim_report *rep, long long *peak, long long *busy,
-                  double *reward, cudaStream_t s);
 bool launch_cost2(const Cost2Graph &G, const TopoArgs &T, const uint8_t *D, int B, unsigned char *scratch,
                   size_t per_place, gdp_sim_report *rep, long long *peak, long long *busy, double *reward,
                   cudaStream_t s);

@@ -1,0 +1,762 @@
+// Cost model (a12), the default kernel: one SIMULATION warp and one MEMORY warp per placement.
+//
+// Same event semantics as the oracle (SPEC.md:275-284 `simulate`, SURVEY O11 with the readings
+// R19/R20 in DESIGN.md §2), in the arrival-event formulation: an op keeps a count of inputs not
+// yet ARRIVED and becomes available at the instant the count reaches zero (= its ready time), so
+// device FIFOs are appended in time order and stay sorted by (ready, id) without a priority
+// queue; the events of an instant are the copy arrivals due now (one per directed channel at
+// most, because every transfer takes >= 1 tick) and the finishes due now (ascending op id).
+//
+//  * Simulation warp (the critical path).  Lane q < d owns device q: its running op (record in
+//    registers), its FIFO and the staging slots of its out-edge records.  Lane L owns the
+//    directed channels 2L and 2L+1 (c = 8 * src + dst): the head arrival time of each in a
+//    register.  An instant is: t = min over the lanes' candidates (one REDUX), arrivals popped by
+//    their owners in parallel, each finishing op's out-edges one per lane (same device -> input
+//    arrived now; other device -> FIFO push on the directed channel, ranked with match_any so
+//    that max(t, free) + (rank + 1) * xfer is computed in parallel), the ops made available now
+//    appended to their device FIFO in id order, idle devices dispatch their FIFO head.  Nothing
+//    of the memory accounting is on this path: the warp only appends 8-byte items (instant,
+//    kind, device, index) to a ring in shared memory.
+//  * Memory warp (off the critical path, lagging).  Consumes the item ring 32 items at a time:
+//    allocations (an op's output from its start, a copy from its arrival), the frees of a finish
+//    (the copies the op held; producers whose LAST consumer this is -- a per-placement counter in
+//    global memory, one atomic per producer and batch; the op's own output if it is a sink), and
+//    samples each device's resident bytes whenever the instant changes (= after every change of
+//    an instant, the oracle's step (4)).
+//  * Per-op state in shared memory is 4 bits: the device (3 bits) and, for ops with exactly two
+//    inputs, an "one input arrived" flag toggled with atomicXor; ops with one input need no
+//    counter, ops with 3..254 inputs a byte counter, more a global counter.  Device ids, static
+//    memory, busy time, channel sizes and the co-location check come from k_cost5_pre (one CTA
+//    per placement, fully parallel) so that the simulation starts at once.
+// Requires (host-checked): every duration >= 1 and every transfer >= 1 tick (no same-instant
+// rounds), N and E < 2^25, degrees < 2^16.  Otherwise gdp_cost runs k_cost3 / k_cost (cost2.cu,
+// cost.cu).
+#include <algorithm>
+#include <climits>
+#include <vector>
+
+#include "common.cuh"
+#include "cost2.cuh"
+#include "cost_util.cuh"
+
+namespace gdp {
+namespace {
+using namespace cu;
+
+constexpr int KC5 = 4;      // channel entries kept in shared memory per channel (power of 2)
+constexpr int KF5 = 4;      // FIFO entries kept in shared memory per device (power of 2)
+constexpr int SO5 = 8;      // staged out-edge records per slot
+constexpr int NINC5 = 4;    // ops made available at one instant kept in shared memory per device
+constexpr int RI5 = 256;    // memory item ring (power of 2)
+
+#ifdef COST5_PROF   // per-phase cycle totals of the simulation warp (lane 0), printed by block 0
+#define P5(i)                                              \
+  do {                                                     \
+    const long long now_ = clock64();                      \
+    prof[i] += now_ - plast;                               \
+    plast = now_;                                          \
+  } while (0)
+#define P5C(i) (prof[i]++)
+#else
+#define P5(i) \
+  do {        \
+  } while (0)
+#define P5C(i) \
+  do {         \
+  } while (0)
+#endif
+
+enum { IT_ALLOC_OP = 0, IT_ALLOC_COPY = 1, IT_INEDGE = 2, IT_SINK = 3, IT_END = 4 };
+
+struct __align__(16) Ent5 {   // channel entry: consumer record, arrival, producer
+  Rec5 r;
+  int arr, u, pad0, pad1;
+};
+
+struct Pre5 {   // per-placement results of k_cost5_pre
+  long long stat[8], busy[8];
+  long long cross;
+  int opcnt[8];
+  int chcnt[64];
+  int flag;      // bit 0 co-location violation, bit 1 malformed (an entry >= d)
+  int pad[3];
+};
+
+struct Smem5 {
+  Ent5 cc[64][KC5];                 // channel rings, c = 8 * src + dst
+  Rec5 stage[8][2][SO5];            // out-edge records of the running / next op of each device
+  Rec5 fc[8][KF5];                  // FIFO rings
+  Rec5 inc[8][NINC5];               // ops made available at this instant
+  unsigned long long items[RI5];    // memory items: t | code << 32
+  Rec5 drun[8];                     // record of the op running on each device
+  int cfree[64], ctail[64], chead[64], coff[64];
+  int ca[64];                       // arrival time of each channel's head entry (INF: empty)
+  int dfin[8];                      // finish of each device's running op (INF: idle)
+  int fh[8], ft[8], cur[8], nxt[8]; // FIFO head / tail, staging slot of the running op, op staged in the other
+  int inc_n[8], doff[8];
+  int mhead;                        // items consumed by the memory warp
+  int mk, disp, oom;
+};
+
+struct Scratch5 {
+  size_t pre, nib, outcnt, gbig, fifo, ov, chq, total;
+};
+__host__ __device__ inline Scratch5 scratch5_layout(int N, long long E, int ngbig) {
+  auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
+  Scratch5 s;
+  s.pre = 0;
+  s.nib = al(sizeof(Pre5));
+  s.outcnt = s.nib + al(4 * (size_t)((N + 31) / 32) * 4);
+  s.gbig = s.outcnt + al(4 * (size_t)N);
+  s.fifo = s.gbig + al(4 * (size_t)(ngbig > 0 ? ngbig : 1));
+  s.ov = s.fifo + al(sizeof(Rec5) * (size_t)N);
+  s.chq = s.ov + al(sizeof(Rec5) * (size_t)N);
+  s.total = s.chq + al(sizeof(Ent5) * (size_t)(E > 0 ? E : 1));
+  return s;
+}
+// nibble words in shared memory: ceil(N / 8) rounded up to whole 16-byte vectors
+__host__ __device__ inline int nib_words(int N) { return ((N + 31) / 32) * 4; }
+
+__device__ __forceinline__ void load_rec5(Rec5 &r, const Rec5 *src) {
+  const int4 *s = reinterpret_cast<const int4 *>(src);
+  const int4 a = s[0], b = s[1];
+  r.id = a.x; r.cost = a.y; r.ob = a.z; r.ib = a.w; r.nn = b.x; r.cinfo = b.y;
+  r.bytes = ((long long)(unsigned)b.z) | ((long long)b.w << 32);
+}
+__device__ __forceinline__ void store_rec5(Rec5 *dst, const Rec5 &r) {
+  int4 *d = reinterpret_cast<int4 *>(dst);
+  d[0] = make_int4(r.id, r.cost, r.ob, r.ib);
+  d[1] = make_int4(r.nn, r.cinfo, (int)(r.bytes & 0xffffffffLL), (int)(r.bytes >> 32));
+}
+__device__ __forceinline__ void store_ent5(Ent5 *dst, const Rec5 &r, int arr, int u) {
+  store_rec5(&dst->r, r);
+  reinterpret_cast<int4 *>(dst)[2] = make_int4(arr, u, 0, 0);
+}
+__device__ __forceinline__ void cp_rec5(Rec5 *s, const Rec5 *g) {
+  cp16(reinterpret_cast<int4 *>(s), g);
+  cp16(reinterpret_cast<int4 *>(s) + 1, reinterpret_cast<const int4 *>(g) + 1);
+}
+// shared-memory words addressed by their 32-bit shared-window address (computed once per kernel)
+__device__ __forceinline__ unsigned lds_u32(unsigned a) {
+  unsigned v;
+  asm("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));   // device bits never change: no ordering needed
+  return v;
+}
+__device__ __forceinline__ unsigned atoms_xor(unsigned a, unsigned x) {
+  unsigned v;
+  asm volatile("atom.shared.xor.b32 %0, [%1], %2;" : "=r"(v) : "r"(a), "r"(x) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned atoms_add(unsigned a, unsigned x) {
+  unsigned v;
+  asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(v) : "r"(a), "r"(x) : "memory");
+  return v;
+}
+__device__ __forceinline__ int nib_dev(unsigned nib_s, int v) { return (lds_u32(nib_s + 4u * (unsigned)(v >> 3)) >> ((v & 7) * 4)) & 7; }
+
+// the input of op r arrived now: true iff it was the last one (the op becomes available now)
+__device__ __forceinline__ bool arrive5(unsigned nib_s, unsigned bigb_s, int *gbig, const Rec5 &r) {
+  const int kind = r.cinfo & 3;
+  if (kind == 0) return true;
+  if (kind == 1) {
+    const unsigned bit = 8u << ((r.id & 7) * 4);
+    return (atoms_xor(nib_s + 4u * (unsigned)(r.id >> 3), bit) & bit) != 0u;
+  }
+  const int ix = r.cinfo >> 2;
+  if (kind == 2) {
+    const int sh = (ix & 3) * 8;
+    return ((atoms_add(bigb_s + 4u * (unsigned)(ix >> 2), 0u - (1u << sh)) >> sh) & 255u) == 1u;
+  }
+  return atomicSub(&gbig[ix], 1) == 1;
+}
+
+__device__ __forceinline__ unsigned long long item5(int t, int kind, int dev, int idx, unsigned pos) {
+  const unsigned code = ((pos / RI5) & 1u) | ((unsigned)kind << 1) | ((unsigned)dev << 4) | ((unsigned)idx << 7);
+  return (unsigned long long)(unsigned)t | ((unsigned long long)code << 32);
+}
+
+// ------------------------------------------------------------------------ pre-pass
+// One CTA per placement: device nibbles, static memory / busy time / op count per device,
+// co-location and malformed flags, cross bytes and per-channel transfer counts (the sizes of the
+// global overflow regions), consumer counters of the memory warp, global input counters.
+__global__ void __launch_bounds__(512) k_cost5_pre(Cost5Graph G, TopoArgs T, const uint8_t *__restrict__ Dall,
+                                                   unsigned char *scratch, size_t per_place) {
+  __shared__ unsigned long long s_stat[8], s_busy[8], s_cross;
+  __shared__ int s_cnt[8], s_ch[64], s_flag;
+  const int N = G.N, d = T.d, b = blockIdx.x, tid = threadIdx.x, lane = tid & 31;
+  const unsigned FULL = 0xffffffffu;
+  const uint8_t *D = Dall + (size_t)b * N;
+  const Scratch5 L = scratch5_layout(N, G.E, G.ngbig);
+  unsigned char *base = scratch + (size_t)b * per_place;
+  Pre5 *pre = reinterpret_cast<Pre5 *>(base + L.pre);
+  unsigned *nib = reinterpret_cast<unsigned *>(base + L.nib);
+  int *outcnt = reinterpret_cast<int *>(base + L.outcnt);
+  int *gbig = reinterpret_cast<int *>(base + L.gbig);
+  if (tid < 8) { s_stat[tid] = 0; s_busy[tid] = 0; s_cnt[tid] = 0; }
+  if (tid < 64) s_ch[tid] = 0;
+  if (tid == 0) { s_cross = 0; s_flag = 0; }
+  __syncthreads();
+  {
+    long long lm[8], lb[8];
+    int lc[8], flag = 0;
+#pragma unroll
+    for (int k = 0; k < 8; k++) { lm[k] = 0; lb[k] = 0; lc[k] = 0; }
+    const int nw = nib_words(N);
+    for (int p = tid; p < nw; p += blockDim.x) {
+      unsigned packed = 0;
+#pragma unroll
+      for (int j = 0; j < 8; j++) {
+        const int v = 8 * p + j;
+        if (v < N) {
+          int k = D[v];
+          if (k >= d) { flag |= 2; k = 0; }
+          packed |= (unsigned)k << (4 * j);
+          const long long mb = G.mem_bytes[v];
+          const long long du = (long long)G.cost[v] * T.speed[k];
+#pragma unroll
+          for (int q = 0; q < 8; q++)
+            if (q == k) { lm[q] += mb; lb[q] += du; lc[q] += 1; }
+          if (G.has_coloc && D[G.leader[v]] != D[v]) flag |= 1;
+        }
+      }
+      nib[p] = packed;
+    }
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+      const long long a = warp_sum_ll(lm[k]), c = warp_sum_ll(lb[k]);
+      const int n = __reduce_add_sync(FULL, lc[k]);
+      if (lane == 0 && n) {
+        atomicAdd(&s_stat[k], (unsigned long long)a);
+        atomicAdd(&s_busy[k], (unsigned long long)c);
+        atomicAdd(&s_cnt[k], n);
+      }
+    }
+    flag = __reduce_or_sync(FULL, flag);
+    if (lane == 0 && flag) atomicOr(&s_flag, flag);
+  }
+  {
+    long long lcross = 0;
+    for (long long e = tid; e < G.E; e += blockDim.x) {
+      const int u = G.out_src[e], w = G.out_idx[e];
+      const int su = D[u], tw = D[w];
+      if (su != tw && su < d && tw < d) {
+        atomicAdd(&s_ch[su * 8 + tw], 1);
+        lcross += G.out_bytes[u];
+      }
+    }
+    lcross = warp_sum_ll(lcross);
+    if (lane == 0 && lcross) atomicAdd(&s_cross, (unsigned long long)lcross);
+  }
+  for (int v = tid; v < N; v += blockDim.x) outcnt[v] = G.outdeg[v];
+  for (int i = tid; i < G.ngbig; i += blockDim.x) gbig[i] = G.gbig0[i];
+  __syncthreads();
+  if (tid < 8) {
+    pre->stat[tid] = (long long)s_stat[tid];
+    pre->busy[tid] = (long long)s_busy[tid];
+    pre->opcnt[tid] = s_cnt[tid];
+  }
+  if (tid < 64) pre->chcnt[tid] = s_ch[tid];
+  if (tid == 0) { pre->cross = (long long)s_cross; pre->flag = s_flag; }
+}
+
+// ------------------------------------------------------------------------ main kernel
+__global__ void __launch_bounds__(64) k_cost5(Cost5Graph G, TopoArgs T, unsigned char *scratch, size_t per_place,
+                                              gdp_sim_report *rep, long long *peak_out, long long *busy_out,
+                                              double *reward) {
+  __shared__ Smem5 S;                                       // fixed state (static: direct addressing)
+  extern __shared__ __align__(16) unsigned char smem_raw[];   // per-op nibbles + byte counters
+  const int N = G.N, d = T.d, b = blockIdx.x;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const unsigned FULL = 0xffffffffu, lt = (1u << lane) - 1u;
+  const int nw = nib_words(N);
+  unsigned *nib = reinterpret_cast<unsigned *>(smem_raw);
+  unsigned *bigb = nib + nw;
+  const unsigned nib_s = (unsigned)__cvta_generic_to_shared(nib), bigb_s = nib_s + 4u * (unsigned)nw;
+  const Scratch5 L = scratch5_layout(N, G.E, G.ngbig);
+  unsigned char *base = scratch + (size_t)b * per_place;
+  const Pre5 *pre = reinterpret_cast<const Pre5 *>(base + L.pre);
+  int *outcnt = reinterpret_cast<int *>(base + L.outcnt);
+  int *gbig = reinterpret_cast<int *>(base + L.gbig);
+  Rec5 *fifo_g = reinterpret_cast<Rec5 *>(base + L.fifo);
+  Rec5 *ov_g = reinterpret_cast<Rec5 *>(base + L.ov);
+  Ent5 *chq_g = reinterpret_cast<Ent5 *>(base + L.chq);
+
+  // ------------------------------------------------------------ prologue (both warps)
+  {
+    const uint4 *src = reinterpret_cast<const uint4 *>(base + L.nib);
+    for (int i = tid; i < nw / 4; i += 64) reinterpret_cast<uint4 *>(nib)[i] = src[i];
+    for (int i = tid; i < G.nbigb; i += 64) bigb[i] = G.bigb0[i];
+    for (int i = tid; i < RI5; i += 64) S.items[i] = 1ull << 32;   // lap parity 1: empty for lap 0
+    S.cfree[tid] = 0; S.ctail[tid] = 0; S.chead[tid] = 0;
+    if (tid < 8) S.inc_n[tid] = 0;
+    if (tid == 0) { S.mhead = 0; S.mk = 0; S.disp = 0; S.oom = 0; }
+    if (tid == 32) {
+      int o = 0;
+      for (int k = 0; k < 8; k++) { S.doff[k] = o; o += pre->opcnt[k]; }
+      o = 0;
+      for (int c = 0; c < 64; c++) { S.coff[c] = o; o += pre->chcnt[c]; }
+    }
+  }
+  const int pflag = pre->flag;
+  __syncthreads();
+  if (pflag & 2) {   // malformed: an entry >= d
+    if (tid == 0) {
+      gdp_sim_report R;
+      R.makespan = 0; R.cross_bytes = 0; R.valid = 0; R.violation = 3;
+      for (int i = 0; i < 6; i++) R.pad[i] = 0;
+      rep[b] = R;
+      reward[b] = -10.0;
+    }
+    if (tid < d) {
+      if (peak_out) peak_out[(size_t)b * d + tid] = 0;
+      if (busy_out) busy_out[(size_t)b * d + tid] = 0;
+    }
+    return;
+  }
+
+  if (warp == 0) {
+    // ============================================================ simulation warp
+    // Warp-uniform serial event processing: every lane executes the same code on the same
+    // values (so a lane reads back its own stores of the shared state and no lane diverges);
+    // lane parallelism only where it pays -- the next-event minimum (one REDUX over the 64
+    // channel heads and 8 running finishes), the out-edges of a finish, the in-edge items and
+    // the staging copies (those sections end with __syncwarp).
+    int mk = 0, disp = 0, t = 0;
+    unsigned spend = 0;                 // this lane's staging copies in flight (bit 2k + slot)
+    unsigned itail = 0, mcache = 0;     // items appended; memory-warp head as last read
+    unsigned incm = 0;                  // devices with ops made available at this instant
+#ifdef COST5_PROF
+    long long prof[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0}, plast = clock64();
+#endif
+    auto ensure = [&](unsigned n) {
+      while (itail + n - mcache > (unsigned)RI5) {
+        P5C(8);
+        mcache = (unsigned)*reinterpret_cast<volatile int *>(&S.mhead);
+        if (itail + n - mcache > (unsigned)RI5) __nanosleep(64);
+      }
+    };
+    auto item = [&](int kind, int dev, int idx) {   // uniform: every lane stores the same item
+      ensure(1);
+      S.items[itail & (RI5 - 1)] = item5(t, kind, dev, idx, itail);
+      itail++;
+    };
+    // synchronous copy of one record / channel entry from global (rare overflow paths)
+    auto ld_rec_g = [&](Rec5 &r, const Rec5 *g) { load_rec5(r, g); };
+    auto to_inc = [&](int q, const Rec5 &r) {       // uniform
+      const int n = S.inc_n[q];
+      if (n < NINC5) store_rec5(&S.inc[q][n], r);
+      else store_rec5(ov_g + S.doff[q] + n, r);
+      S.inc_n[q] = n + 1;
+      incm |= 1u << q;
+    };
+    // uniform input arrival (no other lane touches the counters concurrently)
+    auto arrive_u = [&](const Rec5 &r) -> bool {
+      const int kind = r.cinfo & 3;
+      if (kind == 0) return true;
+      if (kind == 1) {
+        const unsigned bit = 8u << ((r.id & 7) * 4), w = nib[r.id >> 3];
+        nib[r.id >> 3] = w ^ bit;
+        return (w & bit) != 0u;
+      }
+      const int ix = r.cinfo >> 2;
+      if (kind == 2) {
+        const int sh = (ix & 3) * 8;
+        const unsigned w = bigb[ix >> 2];
+        bigb[ix >> 2] = w - (1u << sh);
+        return ((w >> sh) & 255u) == 1u;
+      }
+      const int o = gbig[ix];
+      gbig[ix] = o - 1;
+      return o == 1;
+    };
+    auto stage = [&](int k, int sl, const Rec5 &r) {   // lane j copies out-edge record j
+      const int no = min(r.nn & 0xffff, SO5);
+      if (lane < no) {
+        cp_rec5(&S.stage[k][sl][lane], G.erec + r.ob + lane);
+        spend |= 1u << (2 * k + sl);
+      }
+      cp_commit();
+    };
+
+    if (lane < 64 - 32) { S.ca[lane] = INF; S.ca[lane + 32] = INF; }
+    if (lane < 8) { S.dfin[lane] = INF; S.cur[lane] = 0; S.nxt[lane] = -1; S.fh[lane] = 0; S.ft[lane] = 0; }
+    __syncwarp();
+    // sources are available at t = 0: appended to their FIFO in ascending id (uniform)
+    for (int i = 0; i < G.nsrc; i++) {
+      const int v = G.srcs[i], q = nib_dev(nib_s, v);
+      Rec5 r;
+      load_rec5(r, G.rec + v);
+      const int f = S.ft[q];
+      if (f < KF5) store_rec5(&S.fc[q][f], r);
+      else store_rec5(fifo_g + S.doff[q] + f, r);
+      S.ft[q] = f + 1;
+    }
+    unsigned att = (1u << d) - 1u;   // devices to dispatch at t = 0
+    for (bool first = true;; first = false) {
+      if (!first) {
+        // ---------------------------------------------------------- next instant
+        const int ca0 = S.ca[2 * lane], ca1 = S.ca[2 * lane + 1], df = lane < 8 ? S.dfin[lane] : INF;
+        t = (int)__reduce_min_sync(FULL, (unsigned)min(min(ca0, ca1), df));
+        if (t == INF) break;
+        const unsigned e0 = __ballot_sync(FULL, ca0 == t), e1 = __ballot_sync(FULL, ca1 == t);
+        unsigned ef = __ballot_sync(FULL, df == t);
+        P5C(9);
+        P5(0);
+        // ---------------------------------------------------------- (1) copies arriving now
+        for (unsigned m0 = e0, m1 = e1; m0 | m1;) {
+          int c;
+          if (m0) { c = 2 * (__ffs(m0) - 1); m0 &= m0 - 1; }
+          else { c = 2 * (__ffs(m1) - 1) + 1; m1 &= m1 - 1; }
+          const int h = S.chead[c], tail = S.ctail[c], s = h & (KC5 - 1);
+          Rec5 r;
+          load_rec5(r, &S.cc[c][s].r);
+          const int u = S.cc[c][s].u;
+          S.chead[c] = h + 1;
+          if (h + KC5 < tail) {   // the slot takes position h + KC5 from the global overflow (rare)
+            const int4 *g = reinterpret_cast<const int4 *>(chq_g + S.coff[c] + h + KC5);
+            int4 *sm = reinterpret_cast<int4 *>(&S.cc[c][s]);
+            const int4 x0 = g[0], x1 = g[1], x2 = g[2];
+            sm[0] = x0; sm[1] = x1; sm[2] = x2;
+          }
+          S.ca[c] = h + 1 < tail ? S.cc[c][(h + 1) & (KC5 - 1)].arr : INF;
+          item(IT_ALLOC_COPY, c & 7, u);
+          if (arrive_u(r)) to_inc(c & 7, r);
+        }
+        P5(1);
+        // ---------------------------------------------------------- (2) ops finishing now, ascending id
+        att = ef;
+        if (ef) P5C(10);
+        while (ef) {
+          int k = __ffs(ef) - 1;
+          if (ef & (ef - 1)) {
+            int best = S.drun[k].id;
+            for (unsigned m = ef & (ef - 1); m; m &= m - 1) {
+              const int k2 = __ffs(m) - 1, id2 = S.drun[k2].id;
+              if (id2 < best) { best = id2; k = k2; }
+            }
+          }
+          ef &= ~(1u << k);
+          Rec5 r;
+          load_rec5(r, &S.drun[k]);
+          const int sl = S.cur[k];
+          S.dfin[k] = INF;
+          const int nout = r.nn & 0xffff, nin = (int)((unsigned)r.nn >> 16);
+          for (int j0 = 0; j0 < nin; j0 += 32) {   // frees of this finish -> memory warp, one item per lane
+            const int n = min(32, nin - j0);
+            ensure((unsigned)n);
+            if (lane < n) S.items[(itail + lane) & (RI5 - 1)] = item5(t, IT_INEDGE, k, r.ib + j0 + lane, itail + lane);
+            itail += n;
+          }
+          if (nout == 0) item(IT_SINK, k, r.id);
+          for (int j0 = 0; j0 < nout; j0 += 32) {   // out-edges, one per lane
+            const int j = j0 + lane;
+            const bool valid = j < nout;
+            Rec5 wr;
+            int tw = k;
+            if (valid) {
+              if (j < SO5) {
+                if (spend & (1u << (2 * k + sl))) { cp_wait0(); spend = 0; }
+                load_rec5(wr, &S.stage[k][sl][j]);
+              } else {
+                load_rec5(wr, G.erec + r.ob + j);
+              }
+              tw = nib_dev(nib_s, wr.id);
+            }
+            const bool same = valid && tw == k, cross = valid && tw != k;
+            const bool av = same && arrive5(nib_s, bigb_s, gbig, wr);
+            const unsigned am = __ballot_sync(FULL, av);
+            const unsigned cm = __ballot_sync(FULL, cross);
+            if (am) {   // ops made available now on device k, in lane (= id) order
+              const int n0 = S.inc_n[k];
+              if (av) {
+                const int pos = n0 + __popc(am & lt);
+                if (pos < NINC5) store_rec5(&S.inc[k][pos], wr);
+                else store_rec5(ov_g + S.doff[k] + pos, wr);
+              }
+              __syncwarp();
+              S.inc_n[k] = n0 + __popc(am);
+              incm |= 1u << k;
+            }
+            if (cm) {   // FIFO pushes on the directed channels k -> tw, ranked within each channel
+              const unsigned grp = (cm & (cm - 1)) ? __match_any_sync(FULL, cross ? tw : -1) : cm;
+              if (cross) {
+                const int rank = __popc(grp & lt), n = __popc(grp);
+                const int c = 8 * k + tw;
+                const int f = S.cfree[c], tail = S.ctail[c], hd = S.chead[c];
+                const int x = xfer_time3(r.bytes, c, T);
+                const int bt = max(t, f);
+                const int pos = tail + rank, arr = bt + (rank + 1) * x;
+                if (pos < hd + KC5) store_ent5(&S.cc[c][pos & (KC5 - 1)], wr, arr, r.id);
+                else store_ent5(chq_g + S.coff[c] + pos, wr, arr, r.id);
+                if (rank == 0) {
+                  S.cfree[c] = bt + n * x;
+                  S.ctail[c] = tail + n;
+                  if (tail == hd) S.ca[c] = bt + x;   // the channel was empty: a new head
+                }
+              }
+            }
+            __syncwarp();
+          }
+        }
+        P5(2);
+      }
+      // ---------------------------------------------------------- (3) FIFO append + dispatch
+      for (att |= incm, incm = 0; att; att &= att - 1) {
+        const int k = __ffs(att) - 1;
+        const int n = S.inc_n[k];
+        bool running = S.dfin[k] != INF, go = false;
+        int fh = S.fh[k], ft = S.ft[k];
+        Rec5 run;
+        if (n > 0) {
+          S.inc_n[k] = 0;
+          Rec5 *Li = &S.inc[k][0];
+          Rec5 *Lo = ov_g + S.doff[k];
+          if (n == 1 && !running && fh == ft) {   // common case: straight to dispatch
+            load_rec5(run, Li);
+            go = true;
+          } else {
+            for (int i = 1; i < n; i++) {   // insertion sort by id (n is small except after wide fan-outs)
+              Rec5 key;
+              load_rec5(key, i < NINC5 ? &Li[i] : &Lo[i]);
+              int j = i - 1;
+              while (j >= 0) {
+                Rec5 pj;
+                load_rec5(pj, j < NINC5 ? &Li[j] : &Lo[j]);
+                if (pj.id <= key.id) break;
+                store_rec5(j + 1 < NINC5 ? &Li[j + 1] : &Lo[j + 1], pj);
+                j--;
+              }
+              store_rec5(j + 1 < NINC5 ? &Li[j + 1] : &Lo[j + 1], key);
+            }
+            for (int i = 0; i < n; i++, ft++) {
+              Rec5 x;
+              load_rec5(x, i < NINC5 ? &Li[i] : &Lo[i]);
+              if (ft < fh + KF5) store_rec5(&S.fc[k][ft & (KF5 - 1)], x);
+              else store_rec5(fifo_g + S.doff[k] + ft, x);
+            }
+            S.ft[k] = ft;
+          }
+        }
+        if (!go && !running && fh < ft) {   // pop the FIFO head
+          const int s = fh & (KF5 - 1);
+          load_rec5(run, &S.fc[k][s]);
+          if (fh + KF5 < ft) {   // the slot takes position fh + KF5 from the global overflow (rare)
+            Rec5 x;
+            ld_rec_g(x, fifo_g + S.doff[k] + fh + KF5);
+            store_rec5(&S.fc[k][s], x);
+          }
+          S.fh[k] = ++fh;
+          go = true;
+        }
+        int cur = S.cur[k];
+        if (go) {
+          const int fin = t + run.cost * T.speed[k];
+          S.dfin[k] = fin;
+          store_rec5(&S.drun[k], run);
+          mk = max(mk, fin);
+          disp++;
+          item(IT_ALLOC_OP, k, run.id);
+          cur ^= 1;   // the slot the head was staged into, or the one it is staged into now
+          S.cur[k] = cur;
+          const int staged = S.nxt[k];
+          S.nxt[k] = -1;
+          if (run.id != staged && (run.nn & 0xffff)) stage(k, cur, run);
+          running = true;
+        }
+        if (running && fh < ft && S.nxt[k] < 0) {   // stage the op now waiting at the head
+          Rec5 hr;
+          load_rec5(hr, &S.fc[k][fh & (KF5 - 1)]);
+          S.nxt[k] = hr.id;
+          if (hr.nn & 0xffff) stage(k, cur ^ 1, hr);
+        }
+      }
+      __syncwarp();
+      P5(3);
+    }
+#ifdef COST5_PROF
+    if (b == 0 && lane == 0)
+      printf("C5PROF inst=%lld fin_inst=%lld ensure_waits=%lld next=%lld arr=%lld fin=%lld disp=%lld\n", prof[9],
+             prof[10], prof[8], prof[0], prof[1], prof[2], prof[3]);
+#endif
+    // ---------------------------------------------------------- end of the simulation
+    item(IT_END, 0, 0);
+    cp_wait0();
+    if (lane == 0) { S.mk = mk; S.disp = disp; }
+  } else {
+    // ============================================================ memory warp
+    const bool dl = lane < d;
+    long long mem = dl ? pre->stat[lane] : 0, pk = mem;
+    int last_t = -1;
+    unsigned mh = 0;
+    int nwait = 0;
+    bool done = false;
+    auto kind_end = [](unsigned long long x) { return ((unsigned)(x >> 33) & 7u) == (unsigned)IT_END; };
+#ifdef COST5_PROF
+    long long nidle = 0, nbatch = 0, nitems = 0, m0 = clock64();
+#endif
+    while (!done) {
+      const unsigned pos = mh + lane;
+      const unsigned long long it = *reinterpret_cast<volatile unsigned long long *>(&S.items[pos & (RI5 - 1)]);
+      const unsigned code = (unsigned)(it >> 32);
+      const bool valid = (code & 1u) == ((pos / RI5) & 1u);
+      const unsigned vm = __ballot_sync(FULL, valid);
+      const int n = vm == FULL ? 32 : __ffs(~vm) - 1;
+      if (n < 32 && !__any_sync(FULL, valid && kind_end(it))) {
+        // wait for a full batch unless the simulation has ended: few, large batches leave the
+        // issue slots to the simulation warps
+        if (n == 0 || ++nwait < 4) {
+#ifdef COST5_PROF
+          nidle++;
+#endif
+          __nanosleep(1000);
+          continue;
+        }
+      }
+      nwait = 0;
+#ifdef COST5_PROF
+      nbatch++;
+      nitems += n;
+#endif
+      const bool mine = lane < n;
+      const int ti = (int)(unsigned)(it & 0xffffffffull);
+      const int kind = (int)((code >> 1) & 7u), dev = (int)((code >> 4) & 7u), idx = (int)(code >> 7);
+      int dA = -1, dB = -1, u = -1;
+      long long xA = 0, xB = 0, bu = 0;
+      int du = 0;
+      if (mine) {
+        if (kind == IT_ALLOC_OP || kind == IT_ALLOC_COPY) { dA = dev; xA = G.out_bytes[idx]; }
+        else if (kind == IT_SINK) { dA = dev; xA = -G.out_bytes[idx]; }
+        else if (kind == IT_INEDGE) {
+          const IRec ir = G.irec[idx];
+          u = ir.u;
+          bu = ir.bytes;
+          du = nib_dev(nib_s, u);
+          if (du != dev) { dA = dev; xA = -bu; }   // the copy this op held
+        } else {
+          done = true;
+        }
+      }
+      done = __any_sync(FULL, done);
+      {  // producers whose last consumer finishes: one counter update per producer and batch
+        const unsigned grp = __match_any_sync(FULL, u);
+        const int leader = __ffs(grp) - 1, last = 31 - __clz(grp), cnt = __popc(grp);
+        int old = 0;
+        if (u >= 0 && lane == leader) old = atomicSub(&outcnt[u], cnt);
+        old = __shfl_sync(FULL, old, leader);
+        if (u >= 0 && lane == last && old == cnt) { dB = du; xB = -bu; }
+      }
+      // apply in item order; sample the peak whenever the instant changes
+      for (int i = 0; i < n; i++) {
+        const int tI = __shfl_sync(FULL, ti, i);
+        const int aD = __shfl_sync(FULL, dA, i), bD = __shfl_sync(FULL, dB, i);
+        const long long aX = __shfl_sync(FULL, xA, i), bX = __shfl_sync(FULL, xB, i);
+        if (tI != last_t) { pk = max(pk, mem); last_t = tI; }
+        if (aD == lane) mem += aX;
+        if (bD == lane) mem += bX;
+      }
+      mh += n;
+      __syncwarp();
+      if (lane == 0) {
+        asm volatile("st.release.cta.shared::cta.b32 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(&S.mhead)),
+                     "r"(mh)
+                     : "memory");
+      }
+    }
+    pk = max(pk, mem);
+#ifdef COST5_PROF
+    if (b == 0 && lane == 0)
+      printf("C5MEM batches=%lld items=%lld idle_polls=%lld cycles=%lld\n", nbatch, nitems, nidle, clock64() - m0);
+#endif
+    if (dl) {
+      if (pk > T.cap[lane]) atomicOr(&S.oom, 1);
+      if (peak_out) peak_out[(size_t)b * d + lane] = pk;
+      if (busy_out) busy_out[(size_t)b * d + lane] = pre->busy[lane];
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    gdp_sim_report R;
+    R.makespan = S.mk; R.cross_bytes = pre->cross;
+    for (int i = 0; i < 6; i++) R.pad[i] = 0;
+    R.violation = (pflag & 1) ? 1 : (S.oom ? 2 : 0);
+    if (S.disp != N) R.violation = 3;   // cannot happen for a validated DAG
+    R.valid = R.violation == 0;
+    rep[b] = R;
+    reward[b] = R.valid ? -__dsqrt_rn(__ddiv_rn((double)S.mk, 1e6)) : -10.0;
+  }
+}
+
+}  // namespace
+
+size_t cost5_smem_bytes(int N, int nbigb) { return 4 * (size_t)nib_words(N) + 4 * (size_t)nbigb; }   // dynamic part
+size_t cost5_scratch_per_placement(int N, long long E, int ngbig) { return scratch5_layout(N, E, ngbig).total; }
+
+// every transfer takes >= 1 tick and every duration >= 1 (no same-instant rounds)
+bool cost5_eligible(const TopoArgs &T, const Cost5Graph &G, int min_cost, long long min_edge_bytes) {
+  const int d = T.d;
+  if (!G.ok || d < 1 || d > 8 || min_cost < 1) return false;
+  for (int k = 0; k < d; k++) {
+    if (T.speed[k] < 1) return false;
+    for (int q = 0; q < d; q++)
+      if (k != q) {
+        long long x = T.lat[k * 8 + q];
+        if (min_edge_bytes > 0 && min_edge_bytes != LLONG_MAX && T.bpt[k * 8 + q] > 0)
+          x += (min_edge_bytes - 1) / T.bpt[k * 8 + q] + 1;
+        if (x < 1) return false;
+      }
+  }
+  return sizeof(Smem5) + cost5_smem_bytes(G.N, G.nbigb) <= 227 * 1024;
+}
+
+bool launch_cost5(const Cost5Graph &G, const TopoArgs &T, int min_cost, long long min_edge_bytes, const uint8_t *D,
+                  int B, unsigned char *scratch, size_t per_place, gdp_sim_report *rep, long long *peak,
+                  long long *busy, double *reward, cudaStream_t s) {
+  if (!cost5_eligible(T, G, min_cost, min_edge_bytes)) return false;
+  if (per_place < cost5_scratch_per_placement(G.N, G.E, G.ngbig)) return false;
+  const size_t smem = cost5_smem_bytes(G.N, G.nbigb);
+  static size_t configured = 0;
+  if (smem + sizeof(Smem5) > 48 * 1024 && smem > configured) {
+    cudaFuncSetAttribute(k_cost5, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    configured = smem;
+  }
+  note_launch("k_cost5_pre", s);
+  k_cost5_pre<<<B, 512, 0, s>>>(G, T, D, scratch, per_place);
+  note_launch("k_cost5", s);
+  k_cost5<<<B, 64, smem, s>>>(G, T, scratch, per_place, rep, peak, busy, reward);
+  return true;
+}
+
+// ------------------------------------------------------------------------ graph records (host)
+gdp_status cost5_build(int N, long long E, const int *optr, const int *oidx, const int *iptr, const int *cost,
+                       const long long *out_bytes, Cost5Host *h) {
+  h->ok = N < (1 << 25) && E < (1LL << 25);
+  h->rec.assign(N, Rec5{});
+  h->erec.assign((size_t)std::max<long long>(E, 1), Rec5{});
+  h->srcs.clear();
+  h->bigb.clear();
+  h->gbig.clear();
+  h->outdeg.assign(N, 0);
+  int nb = 0;
+  std::vector<unsigned char> bytes;
+  for (int v = 0; v < N; v++) {
+    const int din = iptr[v + 1] - iptr[v], dout = optr[v + 1] - optr[v];
+    if (din >= 65536 || dout >= 65536) h->ok = false;
+    Rec5 &r = h->rec[v];
+    r.id = v; r.cost = cost[v]; r.ob = optr[v]; r.ib = iptr[v];
+    r.nn = (dout & 0xffff) | ((din & 0xffff) << 16);
+    r.bytes = out_bytes[v];
+    if (din <= 1) r.cinfo = 0;
+    else if (din == 2) r.cinfo = 1;
+    else if (din < 255) { r.cinfo = 2 | (nb << 2); bytes.push_back((unsigned char)din); nb++; }
+    else { r.cinfo = 3 | ((int)h->gbig.size() << 2); h->gbig.push_back(din); }
+    if (din == 0) h->srcs.push_back(v);
+    h->outdeg[v] = dout;
+  }
+  for (long long e = 0; e < E; e++) h->erec[(size_t)e] = h->rec[oidx[e]];
+  while (bytes.size() % 16) bytes.push_back(0);
+  h->bigb.assign(bytes.size() / 4, 0u);
+  for (size_t i = 0; i < bytes.size(); i++) h->bigb[i / 4] |= (unsigned)bytes[i] << (8 * (i % 4));
+  return GDP_OK;
+}
+
+}  // namespace gdp

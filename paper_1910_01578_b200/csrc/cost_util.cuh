@@ -1,4 +1,4 @@
-// Device helpers shared by the shared-memory cost kernels (cost2.cu, cost4.cu).
+// Device helpers shared by the shared-memory cost kernels (cost2.cu, cost5.cu).
 #pragma once
 #include <climits>
 

@@ -310,9 +310,10 @@ __global__ void k_fill_rows(float *dst, const float *row, float scale, int N, in
 inline unsigned nblk(size_t n, int t) { return (unsigned)((n + t - 1) / t); }
 }  // namespace
 
-static thread_local bool t_tc = false;
-void set_tensor_cores(bool on) { t_tc = on; }
+static thread_local bool t_tc = false, t_tc_attn = false;
+void set_tensor_cores(int mode) { t_tc = mode != 0; t_tc_attn = mode == 1; }
 bool tensor_cores_on() { return t_tc; }
+bool tensor_core_attention_on() { return t_tc_attn; }
 static thread_local bool t_noattn = false;
 void set_no_attention(bool on) { t_noattn = on; }
 bool no_attention() { return t_noattn; }

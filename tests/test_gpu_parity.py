@@ -42,7 +42,7 @@ def gdp():
     return m
 
 
-def cost_gpu(gdp, g, t, D):
+def cost_gpu(gdp, g, t, D, kernel=0):
     G = gdp.Graph(g, workloads.features(g))
     T = gdp.Topo(t)
     B = D.shape[0]
@@ -53,7 +53,7 @@ def cost_gpu(gdp, g, t, D):
     peak = torch.empty(B, t.d, dtype=torch.int64, device="cuda")
     busy = torch.empty(B, t.d, dtype=torch.int64, device="cuda")
     rew = torch.empty(B, dtype=torch.float64, device="cuda")
-    gdp.gdp_cost(G, T, Dd, B, rep, peak, busy, rew, ws)
+    gdp.gdp_cost(G, T, Dd, B, rep, peak, busy, rew, ws, kernel=kernel)
     torch.cuda.synchronize()
     r = gdp.decode_reports(rep.cpu().numpy())
     r.update(peak=peak.cpu().numpy(), busy=busy.cpu().numpy(), reward=rew.cpu().numpy())
@@ -122,17 +122,18 @@ def test_cost_workloads(gdp, cfg):
         assert_cost_equal(g, t, D, cost_gpu(gdp, g, t, D))
 
 
-def test_cost_three_ctas_per_sm(gdp):
-    """C3 (N ~ 20 k: shared memory admits three k_cost4 CTAs per SM) with B = 444 > one wave of
-    two per SM on 148 SMs: the launch takes the 72-register k_cost4<3> (DESIGN.md, cost kernel);
-    bit-exact against the oracle like every other cost kernel."""
+def test_cost_full_wave_c3(gdp):
+    """C3 (N ~ 20 k) with B = 888: several k_cost5 CTAs per SM and more than one wave on 148
+    SMs; bit-exact against the oracle like every other cost kernel."""
     W = workloads.config("c3")
     g = W.graphs[0]
     t = workloads.topology(g, W.d)
     rng = np.random.default_rng(21)
-    D = rng.integers(0, W.d, size=(444, g.N)).astype(np.uint8)
+    D = rng.integers(0, W.d, size=(888, g.N)).astype(np.uint8)
     D[3] = 0
     D[7] = (np.arange(g.N) * W.d // g.N).astype(np.uint8)
+    G = gdp.Graph(g, workloads.features(g))
+    assert gdp.cost_kernel(G, gdp.Topo(t)) == 5
     assert_cost_equal(g, t, D, cost_gpu(gdp, g, t, D))
 
 
@@ -373,9 +374,9 @@ def test_tensor_core_mode(gdp, case):
 
 @pytest.mark.parametrize("case", ["c1", "seg", "short_mem", "ragged", "mem_inf", "long_mem", "one_chunk_inf",
                                   "ragged_chunk"])
-def test_tensor_core_attention_matches_simt(gdp, case, monkeypatch):
+def test_tensor_core_attention_matches_simt(gdp, case):
     """The tcgen05 attention tiles (forward k_attn_fwd_tc, backward k_attn_bwd_tc) against the
-    SIMT kernels inside the same tensor-core-mode step (GDP_ATTN_SIMT=1 switches them off):
+    SIMT kernels inside the same tensor-core-mode step (gdp_config.tensor_cores = 2):
     logits within the bf16 tolerance; the gradient along the same direction as the SIMT one when
     both runs sampled the same placements, and as the oracle's for the tile run's placements.
     mem_inf / long_mem: more than 256 keys per segment (several key blocks in the forward; the
@@ -392,9 +393,7 @@ def test_tensor_core_attention_matches_simt(gdp, case, monkeypatch):
                   "ragged_chunk": (workloads.random_dag(1030, p_edge=0.05, max_back=60, seed=37), 4, 112, 200)}[case]
     th = workloads.init_theta(workloads.F, d, seed=13, mode="random")
     B = 16
-    monkeypatch.setenv("GDP_ATTN_SIMT", "1")
-    ref = run_step(gdp, g, d, S, M, True, B, th, tc=True)
-    monkeypatch.setenv("GDP_ATTN_SIMT", "0")
+    ref = run_step(gdp, g, d, S, M, True, B, th, tc=2)   # tensor_cores = 2: SIMT attention
     r = run_step(gdp, g, d, S, M, True, B, th, tc=True)
     ok, err, nbad = close(r["logits"], ref["logits"], rtol=TC_RTOL, floor=TC_FLOOR)
     assert ok, ("logits", err, nbad)
@@ -449,22 +448,6 @@ def test_cost_full_size_c4_few_devices(gdp, d):
     assert_cost_equal(g, t, D, cost_gpu(gdp, g, t, D))
 
 
-FORCED_CASES = r"""
-import sys, json, numpy as np, torch
-sys.path.insert(0, %r)
-import workloads
-from tests.test_gpu_parity import cost_gpu, forced_inputs
-import paper_1910_01578_b200 as gdp
-out = {}
-for name, (g, t, D) in forced_inputs().items():
-    G, T = gdp.Graph(g, workloads.features(g)), gdp.Topo(t)
-    r = cost_gpu(gdp, g, t, D)
-    r["kernel"] = gdp.cost_kernel(G, T)
-    out[name] = {k: np.asarray(v).tolist() for k, v in r.items()}
-print(json.dumps(out))
-"""
-
-
 def forced_inputs():
     """A workload graph and a random DAG with zero-duration ops and zero latency."""
     g1 = workloads.multibranch(blocks=20, seed=5)
@@ -478,33 +461,28 @@ def forced_inputs():
     return {"workload": (g1, t1, D1), "zero_dur": (g2, t2, D2)}
 
 
-@pytest.mark.parametrize("env,kernels", [("GDP_COST_V1", {"workload": 1, "zero_dur": 1}),
-                                         ("GDP_COST_V2", {"workload": 2, "zero_dur": 2}),
-                                         ("GDP_COST_V3", {"workload": 3, "zero_dur": 3}),
-                                         (None, {"workload": 4, "zero_dur": 3})])
-def test_cost_every_kernel_matches(gdp, env, kernels):
-    """Each cost kernel (DESIGN.md §"Cost model": 4 windowed, 3 warp-cooperative, 2 owner-lane,
-    1 global-memory) on the same inputs, selected through its environment switch in a subprocess."""
-    import subprocess, sys, os, json
-    code = FORCED_CASES % os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    e = {k: v for k, v in os.environ.items() if not k.startswith("GDP_COST_")}
-    if env:
-        e[env] = "1"
-    out = subprocess.run([sys.executable, "-c", code], env=e, capture_output=True, text=True, timeout=600)
-    assert out.returncode == 0, out.stderr[-2000:]
-    res = json.loads(out.stdout.strip().splitlines()[-1])
+@pytest.mark.parametrize("kernel,applies", [(1, {"workload": True, "zero_dur": True}),
+                                            (3, {"workload": True, "zero_dur": True}),
+                                            (5, {"workload": True, "zero_dur": False}),
+                                            (0, {"workload": True, "zero_dur": True})])
+def test_cost_every_kernel_matches(gdp, kernel, applies):
+    """Each cost kernel (5 simulation + memory warps, 3 warp-cooperative,
+    1 global-memory; 0 = the automatic choice) on the same inputs through gdp_cost_with_kernel;
+    a kernel that does not apply (5 with zero-duration ops) is refused with GDP_ERR_ARG."""
     for name, (g, t, D) in forced_inputs().items():
-        r = {k: np.asarray(v) for k, v in res[name].items()}
-        assert int(r.pop("kernel")) == kernels[name], (name, env)
-        assert_cost_equal(g, t, D, r)
+        if not applies[name]:
+            with pytest.raises(gdp.GdpError):
+                cost_gpu(gdp, g, t, D, kernel=kernel)
+            continue
+        assert_cost_equal(g, t, D, cost_gpu(gdp, g, t, D, kernel=kernel))
 
 
 def test_cost_kernel_choice(gdp):
     W = workloads.config("c4")
     g = W.graphs[0]
     G = gdp.Graph(g, workloads.features(g))
-    assert gdp.cost_kernel(G, gdp.Topo(workloads.topology(g, 8))) == 4
-    assert gdp.cost_kernel(G, gdp.Topo(workloads.topology(g, 1))) == 4
+    assert gdp.cost_kernel(G, gdp.Topo(workloads.topology(g, 8))) == 5
+    assert gdp.cost_kernel(G, gdp.Topo(workloads.topology(g, 1))) == 5
     assert gdp.cost_kernel(G, gdp.Topo(workloads.topology(g, 4, lat=0))) == 3
     gz = mkgraph(3, [(0, 1)], [1, 0, 2])
     assert gdp.cost_kernel(gdp.Graph(gz, workloads.features(gz)), gdp.Topo(mktopo(2, lat=3))) == 3
@@ -524,10 +502,10 @@ def topo_general(d, rng, lat_lo, lat_hi, speed_hi=1, cap=None):
 
 
 @pytest.mark.parametrize("case", range(8))
-def test_cost_windowed_kernel(gdp, case):
-    """The windowed kernel's own edge cases: window length 1 (latency 1), capped windows
-    (latency > 8), non-uniform latency / bandwidth, heterogeneous speeds, one device, long
-    channel queues (slow links), dense fan-in (many producer deaths per window), capacity hits."""
+def test_cost_kernel5_edge_cases(gdp, case):
+    """k_cost5's edge cases: one-tick transfers (latency 1), long latencies, non-uniform latency /
+    bandwidth, heterogeneous speeds, one device, long channel queues (slow links: entries beyond
+    the shared-memory ring), dense fan-in (many producer deaths per memory batch), capacity hits."""
     rng = np.random.default_rng(100 + case)
     d = [2, 8, 3, 8, 1, 5, 8, 4][case]
     lat = [(1, 1), (1, 4), (9, 30), (2, 7), (1, 1), (3, 3), (1, 2), (5, 12)][case]
@@ -540,18 +518,17 @@ def test_cost_windowed_kernel(gdp, case):
     t = topo_general(d, rng, *lat, speed_hi=3 if case % 2 else 1,
                      cap=int(rng.integers(2000, 20000)) if case in (3, 7) else None)
     G = gdp.Graph(g, workloads.features(g))
-    assert gdp.cost_kernel(G, gdp.Topo(t)) == 4
+    assert gdp.cost_kernel(G, gdp.Topo(t)) == 5
     D = rng.integers(0, d, size=(48, n)).astype(np.uint8)
     D[0] = 0
     assert_cost_equal(g, t, D, cost_gpu(gdp, g, t, D))
 
 
 @pytest.mark.parametrize("case", range(3))
-def test_cost_window_from_bytes(gdp, case):
-    """The window is the shortest possible transfer, latency + ceil(smallest edge bytes /
-    bandwidth): (0) every transfer takes exactly that long (each lands on a window boundary),
-    (1) a zero-byte edge brings the window back to the latency alone, (2) bytes alone make the
-    window (latency 1, transfers of 3-7 ticks)."""
+def test_cost_transfer_lengths(gdp, case):
+    """Transfer lengths latency + ceil(bytes / bandwidth): (0) every transfer exactly the same
+    length (arrivals on many channels at the same instants), (1) a zero-byte edge (a transfer of
+    the latency alone), (2) bytes alone make the length (latency 1, transfers of 3-7 ticks)."""
     from workloads import Topology
     rng = np.random.default_rng(300 + case)
     d = [4, 8, 3][case]
@@ -572,7 +549,7 @@ def test_cost_window_from_bytes(gdp, case):
     t = Topology(d=d, mem_capacity=np.full(d, 1 << 60, dtype=np.int64), speed=np.ones(d, dtype=np.int32),
                  bytes_per_tick=bp, latency=la)
     G = gdp.Graph(g, workloads.features(g))
-    assert gdp.cost_kernel(G, gdp.Topo(t)) == 4
+    assert gdp.cost_kernel(G, gdp.Topo(t)) == 5
     D = rng.integers(0, d, size=(48, n)).astype(np.uint8)
     assert_cost_equal(g, t, D, cost_gpu(gdp, g, t, D))
 

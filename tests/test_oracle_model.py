@@ -383,3 +383,70 @@ def test_p19_no_gradient_into_cached_states():
     y2 = Mo.xl_layer(x.detach(), p2, "xl0", None, S, S)
     (gk,) = torch.autograd.grad(y2[S:2 * S].sum(), p2["xl0.Wk"])
     assert gk.abs().max() > 0
+
+
+# ------------------------------------------------------------------ round-2 pins
+def test_attention_scale_two_key_hand_example():
+    """P:144-148 scaled dot-product attention with head dim 16: one query, two keys.
+    Head 0: q . k1 = 2 * 4 = 8, q . k2 = 0, so the scaled scores are 8 / sqrt(16) = 2 and 0 and
+    the weights e^2 / (e^2 + 1) = 0.8807970779778823, 1 / (e^2 + 1) = 0.11920292202211755
+    (a 1/16 scale would give 0.6225, no scale 0.99966).  Head 1: zero scores -> uniform weights,
+    the output is the mean of the two values in that head (3 + (-1)) / 2 = 1."""
+    Q = torch.zeros(1, 64, dtype=DT)
+    K = torch.zeros(2, 64, dtype=DT)
+    V = torch.zeros(2, 64, dtype=DT)
+    Q[0, 0] = 2.0
+    K[0, 0] = 4.0
+    V[0, 0] = 1.0                      # head 0 value of key 1
+    V[1, 1] = 1.0                      # head 0 value of key 2 (another dim)
+    V[0, 20] = 3.0                     # head 1 values
+    V[1, 20] = -1.0
+    o = Mo.attention_heads(Q, K, V)
+    assert o.shape == (1, 64)
+    assert abs(float(o[0, 0]) - 0.8807970779778823) < 1e-15
+    assert abs(float(o[0, 1]) - 0.11920292202211755) < 1e-15
+    assert abs(float(o[0, 20]) - 1.0) < 1e-15
+    assert float(o.abs().sum()) == pytest.approx(0.8807970779778823 + 0.11920292202211755 + 1.0, abs=1e-14)
+
+
+def test_ffn_sublayer_closed_form():
+    """The XL layer's gated FFN sublayer (R12: pre-LN, ReLU FFN of width 4h) in closed
+    form.  With the attention output map zeroed (Wo = 0, bo = 0) the layer is
+    y = x + ReLU(LN2(x) W1 + b1) W2 + b2.  LN2 with gain 0 and bias beta returns beta for every
+    row, so with W1 = [I | 0], b1 = 0 the hidden row is ReLU(beta) = (0.5, 0, 1.5, 0, ...)
+    (beta = (0.5, -1, 1.5, -2, 0, ...)), and with W2 = 2 [I; 0], b2 = (0, 0, 0, 0.25, 0, ...)
+    y = x + (1.0, 0, 3.0, 0.25, 0, ...) exactly, whatever x is (a missing LN2 would make it
+    depend on x, a ReLU after W2 or a missing residual would change the values)."""
+    F, d = 8, 2
+    p = {k: v.clone() for k, v in rand_params(F, d, 3)[0].items()}
+    n = "xl0"
+    p[f"{n}.Wo"].zero_()
+    p[f"{n}.bo"].zero_()
+    p[f"{n}.ln2.g"].zero_()
+    beta = torch.zeros(64, dtype=DT)
+    beta[:4] = torch.tensor([0.5, -1.0, 1.5, -2.0], dtype=DT)
+    p[f"{n}.ln2.b"].copy_(beta)
+    p[f"{n}.W1"].zero_()
+    p[f"{n}.W1"][:, :64] = torch.eye(64, dtype=DT)
+    p[f"{n}.b1"].zero_()
+    p[f"{n}.W2"].zero_()
+    p[f"{n}.W2"][:64, :] = 2 * torch.eye(64, dtype=DT)
+    p[f"{n}.b2"].zero_()
+    p[f"{n}.b2"][3] = 0.25
+    x = torch.from_numpy(np.random.default_rng(0).normal(size=(7, 64)))
+    y = Mo.xl_layer(x, p, n, None, 4, 4)
+    want = torch.zeros(64, dtype=DT)
+    want[:4] = torch.tensor([1.0, 0.0, 3.0, 0.25], dtype=DT)
+    assert torch.equal(y - x, want.expand(7, 64)) or float((y - x - want).abs().max()) < 1e-15
+
+
+def test_kahn_order_with_id_ties():
+    """S:185-193 Kahn's order, ties broken by ascending id.  S:191's diamond A->B, A->C, B->D,
+    C->D gives [A, B, C, D]; and on ids that are not topological (edges 3->0, 2->0, 1->2): the
+    ready set starts {1, 3}, 1 goes first (smallest id) and makes 2 ready, then 2 (< 3), then 3,
+    which finally readies 0: [1, 2, 3, 0]."""
+    assert Mo.topo_order(4, np.array([[0, 1], [0, 2], [1, 3], [2, 3]])) == [0, 1, 2, 3]
+    assert Mo.topo_order(4, np.array([[3, 0], [2, 0], [1, 2]])) == [1, 2, 3, 0]
+    # no edges: ascending ids; two disjoint chains interleave by id
+    assert Mo.topo_order(3, np.zeros((0, 2), dtype=np.int64)) == [0, 1, 2]
+    assert Mo.topo_order(4, np.array([[2, 0], [3, 1]])) == [2, 0, 3, 1]

@@ -222,3 +222,19 @@ def test_reward_closed_forms():
     assert abs(S.reward(234_000, True) + 0.48373546489791297) < 1e-15
     xs = [S.reward(m, True) for m in range(0, 3_000_000, 7919)]
     assert all(a > b for a, b in zip(xs, xs[1:]))                 # S:650 strictly decreasing
+
+
+def test_critical_path_bound_spec_examples():
+    """longest path by compute_cost x min speed, ignoring transfers.  S:292 chain with
+    costs {1, 2, 3} -> 6; S:293 diamond with unit costs -> 3 (A, then B or C, then D); with
+    speeds (2, 3) the minimum speed 2 doubles it: chain -> 12; a wide fan-out of unit ops below a
+    cost-5 root -> 6 whatever the width."""
+    chain = graph(3, [(0, 1), (1, 2)], [1, 2, 3])
+    assert S.critical_path_bound(chain, topo(2)) == 6
+    diamond = graph(4, [(0, 1), (0, 2), (1, 3), (2, 3)], [1, 1, 1, 1])
+    assert S.critical_path_bound(diamond, topo(2)) == 3
+    t = topo(2)
+    t.speed = np.array([2, 3], dtype=np.int32)
+    assert S.critical_path_bound(chain, t) == 12
+    fan = graph(6, [(0, v) for v in range(1, 6)], [5, 1, 1, 1, 1, 1])
+    assert S.critical_path_bound(fan, topo(3)) == 6
