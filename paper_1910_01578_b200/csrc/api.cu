@@ -520,12 +520,12 @@ gdp_status gdp_graph_create(int32_t N, int32_t F, const float *feat, int64_t E, 
     cost5_build(N, E, optr.data(), oidx.data(), iptr.data(), cost.data(), reinterpret_cast<const long long *>(output_bytes),
                 &h5);
     g->c5_ok = h5.ok;
-    g->nsrc5 = (int)h5.srcs.size();
+    g->nsrc5 = (int)h5.srcq.size();
     g->nbigb5 = (int)h5.bigb.size();
     g->ngbig5 = (int)h5.gbig.size();
-    UP(rec5, h5.rec.data(), h5.rec.size() * sizeof(Rec5));
-    UP(erec5, h5.erec.data(), h5.erec.size() * sizeof(Rec5));
-    UP(srcs5, h5.srcs.data(), h5.srcs.size() * sizeof(int));
+    g->nflagw5 = h5.nflagw;
+    UP(slots5, h5.slots.data(), h5.slots.size() * sizeof(Slot5));
+    UP(srcq5, h5.srcq.data(), h5.srcq.size() * sizeof(Q5));
     UP(gbig5, h5.gbig.data(), h5.gbig.size() * sizeof(int));
     UP(outdeg5, h5.outdeg.data(), h5.outdeg.size() * sizeof(int));
     UP(bigb5, h5.bigb.data(), h5.bigb.size() * sizeof(unsigned));
@@ -539,7 +539,7 @@ gdp_status gdp_graph_destroy(gdp_graph g) {
   if (!g) return GDP_OK;
   void *ptrs[] = {g->X, g->nbr_ptr, g->nbr_idx, g->heavy, g->out_ptr, g->out_idx, g->out_src, g->in_ptr, g->in_idx,
                   g->cost, g->out_bytes, g->mem_bytes, g->perm, g->leader, g->nrec, g->erec, g->irec,
-                  g->cnt0, g->bigid, g->big_in, g->big_out, g->rec5, g->erec5, g->srcs5, g->gbig5, g->outdeg5,
+                  g->cnt0, g->bigid, g->big_in, g->big_out, g->slots5, g->srcq5, g->gbig5, g->outdeg5,
                   g->bigb5};
   for (void *p : ptrs)
     if (p) cudaFree(p);

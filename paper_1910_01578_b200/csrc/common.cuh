@@ -68,10 +68,10 @@ struct gdp_graph_s {
   int nbig = 0;
   // k_cost5 records (cost5.cu)
   bool c5_ok = false;
-  void *rec5 = nullptr, *erec5 = nullptr;
-  int *srcs5 = nullptr, *gbig5 = nullptr, *outdeg5 = nullptr;
+  void *slots5 = nullptr, *srcq5 = nullptr;
+  int *gbig5 = nullptr, *outdeg5 = nullptr;
   unsigned *bigb5 = nullptr;
-  int nsrc5 = 0, nbigb5 = 0, ngbig5 = 0;
+  int nsrc5 = 0, nbigb5 = 0, ngbig5 = 0, nflagw5 = 0;
 };
 
 struct gdp_topo_s {

@@ -415,12 +415,13 @@ static TopoArgs topo_args(const gdp_topo_s *t) {
 static Cost5Graph cost5_graph(const gdp_graph_s *g) {
   Cost5Graph C;
   C.N = g->N; C.E = g->E; C.ok = g->c5_ok ? 1 : 0;
-  C.rec = static_cast<const Rec5 *>(g->rec5); C.erec = static_cast<const Rec5 *>(g->erec5);
+  C.slots = static_cast<const Slot5 *>(g->slots5); C.srcq = static_cast<const Q5 *>(g->srcq5);
   C.irec = static_cast<const IRec *>(g->irec);
   C.out_idx = g->out_idx; C.out_src = g->out_src; C.cost = g->cost; C.leader = g->leader;
-  C.srcs = g->srcs5; C.outdeg = g->outdeg5; C.gbig0 = g->gbig5; C.bigb0 = g->bigb5;
+  C.outdeg = g->outdeg5; C.gbig0 = g->gbig5; C.bigb0 = g->bigb5;
   C.out_bytes = g->out_bytes; C.mem_bytes = g->mem_bytes;
-  C.nsrc = g->nsrc5; C.nbigb = g->nbigb5; C.ngbig = g->ngbig5; C.has_coloc = g->has_coloc ? 1 : 0;
+  C.nsrc = g->nsrc5; C.nbigb = g->nbigb5; C.ngbig = g->ngbig5; C.nflagw = g->nflagw5;
+  C.has_coloc = g->has_coloc ? 1 : 0;
   return C;
 }
 

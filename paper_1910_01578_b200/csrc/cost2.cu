@@ -52,34 +52,6 @@ struct Smem {
   int inc_n[8], doff[8], sreq_slot[8];
 };
 
-// 64-bit add as two native 32-bit shared atomics: each add carries its own low-word wrap
-__device__ __forceinline__ void add_mem(unsigned *lo, unsigned *hi, int dev, long long v) {
-  const unsigned a = (unsigned)((unsigned long long)v & 0xffffffffull);
-  const unsigned h = (unsigned)((unsigned long long)v >> 32);
-  const unsigned old = atomicAdd(&lo[dev], a);
-  const unsigned hc = h + ((old + a) < old ? 1u : 0u);
-  if (hc) atomicAdd(&hi[dev], hc);
-}
-__device__ __forceinline__ long long read_mem(const unsigned *lo, const unsigned *hi, int dev) {
-  return (long long)(((unsigned long long)hi[dev] << 32) | lo[dev]);
-}
-
-// decrement the 4-bit counter of v at nibble `hi` (0 = inputs, 1 = consumers); true iff it hits 0
-__device__ __forceinline__ bool dec_counter(unsigned *cnt, int v, int hi, int *bigc, const int *bigid, int nbig) {
-  const int sh = (v & 3) * 8 + hi * 4;
-  if (((cnt[v >> 2] >> sh) & 15u) == 15u) return atomicSub(&bigc[bigid[v] + hi * nbig], 1) == 1;
-  unsigned old = atomicSub(&cnt[v >> 2], 1u << sh);
-  return ((old >> sh) & 15u) == 1u;
-}
-
-__device__ __forceinline__ int xfer_time(long long bytes, int k, int tw, const TopoArgs &T) {
-  const long long bw = T.bpt[k * 8 + tw];
-  long long q;
-  if (bytes < (1LL << 52)) q = (long long)ceil(__ddiv_rn((double)bytes, (double)bw));
-  else q = (bytes + bw - 1) / bw;
-  return (int)q + T.lat[k * 8 + tw];
-}
-
 // an op became available now: append to device dev's incoming list for this round
 __device__ __forceinline__ void push_inc(Smem &S, NRec *ov, int dev, const NRec &r) {
   const int i = atomicAdd(&S.inc_n[dev], 1);

@@ -32,33 +32,40 @@ struct Cost2Graph {
 };
 
 // ---- k_cost5 (cost5.cu): graph-static records of the simulation warp
-struct __align__(16) Rec5 {   // one op, 32 bytes
-  int id, cost, ob, ib;       // id, compute cost, first out-edge slot, first in-edge slot
-  int nn;                     // out-degree | in-degree << 16
+struct __align__(16) Q5 {     // an op in a queue (channel ring, FIFO, available list), 32 bytes
+  int id, cost, ob, nn;       // id, compute cost, first out-edge slot, out-degree | in-degree << 16
   int cinfo;                  // input counter: kind (bits 0-1: 0 = at most one input, 1 = two inputs
                               // (flag bit), 2 = byte counter, 3 = global counter) | index << 2
-  long long bytes;            // output bytes
+  int ib;                     // first in-edge slot
+  int arr, u;                 // channel entries: arrival tick and producer id
+};
+struct __align__(16) Slot5 {  // out-edge slot e = (v -> w), out-CSR order, 32 bytes
+  int w, cost, ob, nn, cinfo, ib;   // the consumer's queue fields
+  long long bytes;                  // the producer's output bytes (the copy on this edge)
 };
 struct Cost5Host {            // host images built at graph creation (cost5_build)
   bool ok = false;
-  std::vector<Rec5> rec, erec;  // erec[e] = rec[out_idx[e]] (out-CSR order)
-  std::vector<int> srcs, gbig, outdeg;
-  std::vector<unsigned> bigb;   // byte counters (in-degree 3..254), 4 per word, 16-byte padded
+  std::vector<Slot5> slots;
+  std::vector<Q5> srcq;        // the sources, ascending id
+  std::vector<int> gbig, outdeg;
+  std::vector<unsigned> bigb;  // byte counters (in-degree 3..254), 4 per word, 16-byte padded
+  int nflagw = 0;              // words of the two-input flag bitmap
 };
 struct Cost5Graph {
   int N;
   long long E;
   int ok;
-  const Rec5 *rec, *erec;
+  const Slot5 *slots;
+  const Q5 *srcq;
   const IRec *irec;
-  const int *out_idx, *out_src, *cost, *leader, *srcs, *outdeg, *gbig0;
+  const int *out_idx, *out_src, *cost, *leader, *outdeg, *gbig0;
   const unsigned *bigb0;
   const long long *out_bytes, *mem_bytes;
-  int nsrc, nbigb, ngbig, has_coloc;
+  int nsrc, nbigb, ngbig, nflagw, has_coloc;
 };
 gdp_status cost5_build(int N, long long E, const int *optr, const int *oidx, const int *iptr, const int *cost,
                        const long long *out_bytes, Cost5Host *h);
-size_t cost5_smem_bytes(int N, int nbigb);
+size_t cost5_smem_bytes(int nflagw, int nbigb);
 size_t cost5_scratch_per_placement(int N, long long E, int ngbig);
 bool cost5_eligible(const TopoArgs &T, const Cost5Graph &G, int min_cost, long long min_edge_bytes);
 bool launch_cost5(const Cost5Graph &G, const TopoArgs &T, int min_cost, long long min_edge_bytes, const uint8_t *D,

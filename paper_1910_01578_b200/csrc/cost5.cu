@@ -23,11 +23,14 @@
 //    global memory, one atomic per producer and batch; the op's own output if it is a sink), and
 //    samples each device's resident bytes whenever the instant changes (= after every change of
 //    an instant, the oracle's step (4)).
-//  * Per-op state in shared memory is 4 bits: the device (3 bits) and, for ops with exactly two
-//    inputs, an "one input arrived" flag toggled with atomicXor; ops with one input need no
-//    counter, ops with 3..254 inputs a byte counter, more a global counter.  Device ids, static
-//    memory, busy time, channel sizes and the co-location check come from k_cost5_pre (one CTA
-//    per placement, fully parallel) so that the simulation starts at once.
+//  * Per-op state in shared memory is only the input counters: ops with one input need none,
+//    ops with exactly two inputs one "first input arrived" bit (a compact bitmap), ops with
+//    3..254 inputs a byte counter, more a global counter (C4: 9.7 KB).  Device ids are not in
+//    shared memory: a finishing op's consumers' devices come with its staged out-edge records
+//    (a per-placement byte per out-edge slot that k_cost5_pre writes), the memory warp reads the
+//    placement row from L2.  Static memory, busy time, channel sizes and the co-location check
+//    also come from k_cost5_pre (one CTA per placement, fully parallel).  With ~27 KB of shared
+//    memory per placement, eight CTAs (placements) share an SM at C4.
 // Requires (host-checked): every duration >= 1 and every transfer >= 1 tick (no same-instant
 // rounds), N and E < 2^25, degrees < 2^16.  Otherwise gdp_cost runs k_cost3 / k_cost (cost2.cu,
 // cost.cu).
@@ -46,8 +49,8 @@ using namespace cu;
 constexpr int KC5 = 4;      // channel entries kept in shared memory per channel (power of 2)
 constexpr int KF5 = 4;      // FIFO entries kept in shared memory per device (power of 2)
 constexpr int SO5 = 8;      // staged out-edge records per slot
-constexpr int NINC5 = 4;    // ops made available at one instant kept in shared memory per device
-constexpr int RI5 = 256;    // memory item ring (power of 2)
+constexpr int NINC5 = 2;    // ops made available at one instant kept in shared memory per device
+constexpr int RI5 = 128;    // memory item ring (power of 2)
 
 #ifdef COST5_PROF   // per-phase cycle totals of the simulation warp (lane 0), printed by block 0
 #define P5(i)                                              \
@@ -68,10 +71,6 @@ constexpr int RI5 = 256;    // memory item ring (power of 2)
 
 enum { IT_ALLOC_OP = 0, IT_ALLOC_COPY = 1, IT_INEDGE = 2, IT_SINK = 3, IT_END = 4 };
 
-struct __align__(16) Ent5 {   // channel entry: consumer record, arrival, producer
-  Rec5 r;
-  int arr, u, pad0, pad1;
-};
 
 struct Pre5 {   // per-placement results of k_cost5_pre
   long long stat[8], busy[8];
@@ -83,12 +82,13 @@ struct Pre5 {   // per-placement results of k_cost5_pre
 };
 
 struct Smem5 {
-  Ent5 cc[64][KC5];                 // channel rings, c = 8 * src + dst
-  Rec5 stage[8][2][SO5];            // out-edge records of the running / next op of each device
-  Rec5 fc[8][KF5];                  // FIFO rings
-  Rec5 inc[8][NINC5];               // ops made available at this instant
+  Q5 cc[64][KC5];                   // channel rings (arr, u set), c = 8 * src + dst
+  Slot5 stage[8][2][SO5];           // out-edge slots of the running / next op of each device
+  unsigned sdev[8][2][SO5];         // the 4 bytes of the placement's slot-device array holding each slot's
+  Q5 fc[8][KF5];                    // FIFO rings
+  Q5 inc[8][NINC5];                 // ops made available at this instant
   unsigned long long items[RI5];    // memory items: t | code << 32
-  Rec5 drun[8];                     // record of the op running on each device
+  Q5 drun[8];                       // the op running on each device
   int cfree[64], ctail[64], chead[64], coff[64];
   int ca[64];                       // arrival time of each channel's head entry (INF: empty)
   int dfin[8];                      // finish of each device's running op (INF: idle)
@@ -99,49 +99,53 @@ struct Smem5 {
 };
 
 struct Scratch5 {
-  size_t pre, nib, outcnt, gbig, fifo, ov, chq, total;
+  size_t pre, sdev, outcnt, gbig, fifo, ov, chq, total;
 };
 __host__ __device__ inline Scratch5 scratch5_layout(int N, long long E, int ngbig) {
   auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
   Scratch5 s;
   s.pre = 0;
-  s.nib = al(sizeof(Pre5));
-  s.outcnt = s.nib + al(4 * (size_t)((N + 31) / 32) * 4);
+  s.sdev = al(sizeof(Pre5));
+  s.outcnt = s.sdev + al((size_t)(E > 0 ? E : 1) + 16);
   s.gbig = s.outcnt + al(4 * (size_t)N);
   s.fifo = s.gbig + al(4 * (size_t)(ngbig > 0 ? ngbig : 1));
-  s.ov = s.fifo + al(sizeof(Rec5) * (size_t)N);
-  s.chq = s.ov + al(sizeof(Rec5) * (size_t)N);
-  s.total = s.chq + al(sizeof(Ent5) * (size_t)(E > 0 ? E : 1));
+  s.ov = s.fifo + al(sizeof(Q5) * (size_t)N);
+  s.chq = s.ov + al(sizeof(Q5) * (size_t)N);
+  s.total = s.chq + al(sizeof(Q5) * (size_t)(E > 0 ? E : 1));
   return s;
 }
-// nibble words in shared memory: ceil(N / 8) rounded up to whole 16-byte vectors
-__host__ __device__ inline int nib_words(int N) { return ((N + 31) / 32) * 4; }
 
-__device__ __forceinline__ void load_rec5(Rec5 &r, const Rec5 *src) {
+__device__ __forceinline__ void load_q5(Q5 &r, const Q5 *src) {
   const int4 *s = reinterpret_cast<const int4 *>(src);
   const int4 a = s[0], b = s[1];
-  r.id = a.x; r.cost = a.y; r.ob = a.z; r.ib = a.w; r.nn = b.x; r.cinfo = b.y;
-  r.bytes = ((long long)(unsigned)b.z) | ((long long)b.w << 32);
+  r.id = a.x; r.cost = a.y; r.ob = a.z; r.nn = a.w; r.cinfo = b.x; r.ib = b.y; r.arr = b.z; r.u = b.w;
 }
-__device__ __forceinline__ void store_rec5(Rec5 *dst, const Rec5 &r) {
+__device__ __forceinline__ void store_q5(Q5 *dst, const Q5 &r) {
   int4 *d = reinterpret_cast<int4 *>(dst);
-  d[0] = make_int4(r.id, r.cost, r.ob, r.ib);
-  d[1] = make_int4(r.nn, r.cinfo, (int)(r.bytes & 0xffffffffLL), (int)(r.bytes >> 32));
+  d[0] = make_int4(r.id, r.cost, r.ob, r.nn);
+  d[1] = make_int4(r.cinfo, r.ib, r.arr, r.u);
 }
-__device__ __forceinline__ void store_ent5(Ent5 *dst, const Rec5 &r, int arr, int u) {
-  store_rec5(&dst->r, r);
-  reinterpret_cast<int4 *>(dst)[2] = make_int4(arr, u, 0, 0);
+// the queue fields of an out-edge slot's consumer (+ arrival and producer for a channel entry)
+__device__ __forceinline__ Q5 q_of_slot(const Slot5 &e, int arr, int u) {
+  Q5 r;
+  r.id = e.w; r.cost = e.cost; r.ob = e.ob; r.nn = e.nn; r.cinfo = e.cinfo; r.ib = e.ib; r.arr = arr; r.u = u;
+  return r;
 }
-__device__ __forceinline__ void cp_rec5(Rec5 *s, const Rec5 *g) {
+__device__ __forceinline__ void load_slot5(Slot5 &e, const Slot5 *src) {
+  const int4 *s = reinterpret_cast<const int4 *>(src);
+  const int4 a = s[0], b = s[1];
+  e.w = a.x; e.cost = a.y; e.ob = a.z; e.nn = a.w; e.cinfo = b.x; e.ib = b.y;
+  e.bytes = ((long long)(unsigned)b.z) | ((long long)b.w << 32);
+}
+__device__ __forceinline__ void cp_32(void *s, const void *g) {
   cp16(reinterpret_cast<int4 *>(s), g);
   cp16(reinterpret_cast<int4 *>(s) + 1, reinterpret_cast<const int4 *>(g) + 1);
 }
-// shared-memory words addressed by their 32-bit shared-window address (computed once per kernel)
-__device__ __forceinline__ unsigned lds_u32(unsigned a) {
-  unsigned v;
-  asm("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));   // device bits never change: no ordering needed
-  return v;
+__device__ __forceinline__ void cp_4(void *s, const void *g) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"((unsigned)__cvta_generic_to_shared(s)), "l"(g)
+               : "memory");
 }
+// shared-memory words addressed by their 32-bit shared-window address (computed once per kernel)
 __device__ __forceinline__ unsigned atoms_xor(unsigned a, unsigned x) {
   unsigned v;
   asm volatile("atom.shared.xor.b32 %0, [%1], %2;" : "=r"(v) : "r"(a), "r"(x) : "memory");
@@ -152,17 +156,15 @@ __device__ __forceinline__ unsigned atoms_add(unsigned a, unsigned x) {
   asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(v) : "r"(a), "r"(x) : "memory");
   return v;
 }
-__device__ __forceinline__ int nib_dev(unsigned nib_s, int v) { return (lds_u32(nib_s + 4u * (unsigned)(v >> 3)) >> ((v & 7) * 4)) & 7; }
-
-// the input of op r arrived now: true iff it was the last one (the op becomes available now)
-__device__ __forceinline__ bool arrive5(unsigned nib_s, unsigned bigb_s, int *gbig, const Rec5 &r) {
-  const int kind = r.cinfo & 3;
+// an input of op (cinfo) arrived now: true iff it was the last one (the op becomes available now)
+__device__ __forceinline__ bool arrive5(unsigned flag_s, unsigned bigb_s, int *gbig, int cinfo) {
+  const int kind = cinfo & 3;
   if (kind == 0) return true;
+  const int ix = cinfo >> 2;
   if (kind == 1) {
-    const unsigned bit = 8u << ((r.id & 7) * 4);
-    return (atoms_xor(nib_s + 4u * (unsigned)(r.id >> 3), bit) & bit) != 0u;
+    const unsigned bit = 1u << (ix & 31);
+    return (atoms_xor(flag_s + 4u * (unsigned)(ix >> 5), bit) & bit) != 0u;
   }
-  const int ix = r.cinfo >> 2;
   if (kind == 2) {
     const int sh = (ix & 3) * 8;
     return ((atoms_add(bigb_s + 4u * (unsigned)(ix >> 2), 0u - (1u << sh)) >> sh) & 255u) == 1u;
@@ -176,9 +178,10 @@ __device__ __forceinline__ unsigned long long item5(int t, int kind, int dev, in
 }
 
 // ------------------------------------------------------------------------ pre-pass
-// One CTA per placement: device nibbles, static memory / busy time / op count per device,
-// co-location and malformed flags, cross bytes and per-channel transfer counts (the sizes of the
-// global overflow regions), consumer counters of the memory warp, global input counters.
+// One CTA per placement: static memory / busy time / op count per device, co-location and
+// malformed flags, the device of every out-edge slot's consumer (one byte per slot, out-CSR
+// order), cross bytes and per-channel transfer counts (the sizes of the global overflow
+// regions), consumer counters of the memory warp, global input counters.
 __global__ void __launch_bounds__(512) k_cost5_pre(Cost5Graph G, TopoArgs T, const uint8_t *__restrict__ Dall,
                                                    unsigned char *scratch, size_t per_place) {
   __shared__ unsigned long long s_stat[8], s_busy[8], s_cross;
@@ -189,7 +192,7 @@ __global__ void __launch_bounds__(512) k_cost5_pre(Cost5Graph G, TopoArgs T, con
   const Scratch5 L = scratch5_layout(N, G.E, G.ngbig);
   unsigned char *base = scratch + (size_t)b * per_place;
   Pre5 *pre = reinterpret_cast<Pre5 *>(base + L.pre);
-  unsigned *nib = reinterpret_cast<unsigned *>(base + L.nib);
+  uint8_t *sdev = base + L.sdev;
   int *outcnt = reinterpret_cast<int *>(base + L.outcnt);
   int *gbig = reinterpret_cast<int *>(base + L.gbig);
   if (tid < 8) { s_stat[tid] = 0; s_busy[tid] = 0; s_cnt[tid] = 0; }
@@ -201,25 +204,15 @@ __global__ void __launch_bounds__(512) k_cost5_pre(Cost5Graph G, TopoArgs T, con
     int lc[8], flag = 0;
 #pragma unroll
     for (int k = 0; k < 8; k++) { lm[k] = 0; lb[k] = 0; lc[k] = 0; }
-    const int nw = nib_words(N);
-    for (int p = tid; p < nw; p += blockDim.x) {
-      unsigned packed = 0;
+    for (int v = tid; v < N; v += blockDim.x) {
+      int k = D[v];
+      if (k >= d) { flag |= 2; k = 0; }
+      const long long mb = G.mem_bytes[v];
+      const long long du = (long long)G.cost[v] * T.speed[k];
 #pragma unroll
-      for (int j = 0; j < 8; j++) {
-        const int v = 8 * p + j;
-        if (v < N) {
-          int k = D[v];
-          if (k >= d) { flag |= 2; k = 0; }
-          packed |= (unsigned)k << (4 * j);
-          const long long mb = G.mem_bytes[v];
-          const long long du = (long long)G.cost[v] * T.speed[k];
-#pragma unroll
-          for (int q = 0; q < 8; q++)
-            if (q == k) { lm[q] += mb; lb[q] += du; lc[q] += 1; }
-          if (G.has_coloc && D[G.leader[v]] != D[v]) flag |= 1;
-        }
-      }
-      nib[p] = packed;
+      for (int q = 0; q < 8; q++)
+        if (q == k) { lm[q] += mb; lb[q] += du; lc[q] += 1; }
+      if (G.has_coloc && D[G.leader[v]] != D[v]) flag |= 1;
     }
 #pragma unroll
     for (int k = 0; k < 8; k++) {
@@ -239,6 +232,7 @@ __global__ void __launch_bounds__(512) k_cost5_pre(Cost5Graph G, TopoArgs T, con
     for (long long e = tid; e < G.E; e += blockDim.x) {
       const int u = G.out_src[e], w = G.out_idx[e];
       const int su = D[u], tw = D[w];
+      sdev[e] = (uint8_t)tw;
       if (su != tw && su < d && tw < d) {
         atomicAdd(&s_ch[su * 8 + tw], 1);
         lcross += G.out_bytes[u];
@@ -260,31 +254,31 @@ __global__ void __launch_bounds__(512) k_cost5_pre(Cost5Graph G, TopoArgs T, con
 }
 
 // ------------------------------------------------------------------------ main kernel
-__global__ void __launch_bounds__(64) k_cost5(Cost5Graph G, TopoArgs T, unsigned char *scratch, size_t per_place,
-                                              gdp_sim_report *rep, long long *peak_out, long long *busy_out,
-                                              double *reward) {
+__global__ void __launch_bounds__(64) k_cost5(Cost5Graph G, TopoArgs T, const uint8_t *__restrict__ Dall,
+                                              unsigned char *scratch, size_t per_place, gdp_sim_report *rep,
+                                              long long *peak_out, long long *busy_out, double *reward) {
   __shared__ Smem5 S;                                       // fixed state (static: direct addressing)
-  extern __shared__ __align__(16) unsigned char smem_raw[];   // per-op nibbles + byte counters
+  extern __shared__ __align__(16) unsigned char smem_raw[];   // input counters: flag bits, byte counters
   const int N = G.N, d = T.d, b = blockIdx.x;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const unsigned FULL = 0xffffffffu, lt = (1u << lane) - 1u;
-  const int nw = nib_words(N);
-  unsigned *nib = reinterpret_cast<unsigned *>(smem_raw);
-  unsigned *bigb = nib + nw;
-  const unsigned nib_s = (unsigned)__cvta_generic_to_shared(nib), bigb_s = nib_s + 4u * (unsigned)nw;
+  unsigned *flags = reinterpret_cast<unsigned *>(smem_raw);
+  unsigned *bigb = flags + G.nflagw;
+  const unsigned flag_s = (unsigned)__cvta_generic_to_shared(flags), bigb_s = flag_s + 4u * (unsigned)G.nflagw;
+  const uint8_t *D = Dall + (size_t)b * N;
   const Scratch5 L = scratch5_layout(N, G.E, G.ngbig);
   unsigned char *base = scratch + (size_t)b * per_place;
   const Pre5 *pre = reinterpret_cast<const Pre5 *>(base + L.pre);
+  const uint8_t *sdev_g = base + L.sdev;
   int *outcnt = reinterpret_cast<int *>(base + L.outcnt);
   int *gbig = reinterpret_cast<int *>(base + L.gbig);
-  Rec5 *fifo_g = reinterpret_cast<Rec5 *>(base + L.fifo);
-  Rec5 *ov_g = reinterpret_cast<Rec5 *>(base + L.ov);
-  Ent5 *chq_g = reinterpret_cast<Ent5 *>(base + L.chq);
+  Q5 *fifo_g = reinterpret_cast<Q5 *>(base + L.fifo);
+  Q5 *ov_g = reinterpret_cast<Q5 *>(base + L.ov);
+  Q5 *chq_g = reinterpret_cast<Q5 *>(base + L.chq);
 
   // ------------------------------------------------------------ prologue (both warps)
   {
-    const uint4 *src = reinterpret_cast<const uint4 *>(base + L.nib);
-    for (int i = tid; i < nw / 4; i += 64) reinterpret_cast<uint4 *>(nib)[i] = src[i];
+    for (int i = tid; i < G.nflagw; i += 64) flags[i] = 0u;
     for (int i = tid; i < G.nbigb; i += 64) bigb[i] = G.bigb0[i];
     for (int i = tid; i < RI5; i += 64) S.items[i] = 1ull << 32;   // lap parity 1: empty for lap 0
     S.cfree[tid] = 0; S.ctail[tid] = 0; S.chead[tid] = 0;
@@ -340,25 +334,23 @@ __global__ void __launch_bounds__(64) k_cost5(Cost5Graph G, TopoArgs T, unsigned
       S.items[itail & (RI5 - 1)] = item5(t, kind, dev, idx, itail);
       itail++;
     };
-    // synchronous copy of one record / channel entry from global (rare overflow paths)
-    auto ld_rec_g = [&](Rec5 &r, const Rec5 *g) { load_rec5(r, g); };
-    auto to_inc = [&](int q, const Rec5 &r) {       // uniform
+    auto to_inc = [&](int q, const Q5 &r) {       // uniform
       const int n = S.inc_n[q];
-      if (n < NINC5) store_rec5(&S.inc[q][n], r);
-      else store_rec5(ov_g + S.doff[q] + n, r);
+      if (n < NINC5) store_q5(&S.inc[q][n], r);
+      else store_q5(ov_g + S.doff[q] + n, r);
       S.inc_n[q] = n + 1;
       incm |= 1u << q;
     };
     // uniform input arrival (no other lane touches the counters concurrently)
-    auto arrive_u = [&](const Rec5 &r) -> bool {
-      const int kind = r.cinfo & 3;
+    auto arrive_u = [&](int cinfo) -> bool {
+      const int kind = cinfo & 3;
       if (kind == 0) return true;
+      const int ix = cinfo >> 2;
       if (kind == 1) {
-        const unsigned bit = 8u << ((r.id & 7) * 4), w = nib[r.id >> 3];
-        nib[r.id >> 3] = w ^ bit;
+        const unsigned bit = 1u << (ix & 31), w = flags[ix >> 5];
+        flags[ix >> 5] = w ^ bit;
         return (w & bit) != 0u;
       }
-      const int ix = r.cinfo >> 2;
       if (kind == 2) {
         const int sh = (ix & 3) * 8;
         const unsigned w = bigb[ix >> 2];
@@ -369,10 +361,12 @@ __global__ void __launch_bounds__(64) k_cost5(Cost5Graph G, TopoArgs T, unsigned
       gbig[ix] = o - 1;
       return o == 1;
     };
-    auto stage = [&](int k, int sl, const Rec5 &r) {   // lane j copies out-edge record j
+    auto stage = [&](int k, int sl, const Q5 &r) {   // lane j copies out-edge slot j and its device byte
       const int no = min(r.nn & 0xffff, SO5);
       if (lane < no) {
-        cp_rec5(&S.stage[k][sl][lane], G.erec + r.ob + lane);
+        const int e = r.ob + lane;
+        cp_32(&S.stage[k][sl][lane], G.slots + e);
+        cp_4(&S.sdev[k][sl][lane], sdev_g + (e & ~3));
         spend |= 1u << (2 * k + sl);
       }
       cp_commit();
@@ -383,12 +377,12 @@ __global__ void __launch_bounds__(64) k_cost5(Cost5Graph G, TopoArgs T, unsigned
     __syncwarp();
     // sources are available at t = 0: appended to their FIFO in ascending id (uniform)
     for (int i = 0; i < G.nsrc; i++) {
-      const int v = G.srcs[i], q = nib_dev(nib_s, v);
-      Rec5 r;
-      load_rec5(r, G.rec + v);
+      Q5 r;
+      load_q5(r, G.srcq + i);
+      const int q = D[r.id];
       const int f = S.ft[q];
-      if (f < KF5) store_rec5(&S.fc[q][f], r);
-      else store_rec5(fifo_g + S.doff[q] + f, r);
+      if (f < KF5) store_q5(&S.fc[q][f], r);
+      else store_q5(fifo_g + S.doff[q] + f, r);
       S.ft[q] = f + 1;
     }
     unsigned att = (1u << d) - 1u;   // devices to dispatch at t = 0
@@ -408,19 +402,17 @@ __global__ void __launch_bounds__(64) k_cost5(Cost5Graph G, TopoArgs T, unsigned
           if (m0) { c = 2 * (__ffs(m0) - 1); m0 &= m0 - 1; }
           else { c = 2 * (__ffs(m1) - 1) + 1; m1 &= m1 - 1; }
           const int h = S.chead[c], tail = S.ctail[c], s = h & (KC5 - 1);
-          Rec5 r;
-          load_rec5(r, &S.cc[c][s].r);
-          const int u = S.cc[c][s].u;
+          Q5 r;
+          load_q5(r, &S.cc[c][s]);
           S.chead[c] = h + 1;
           if (h + KC5 < tail) {   // the slot takes position h + KC5 from the global overflow (rare)
-            const int4 *g = reinterpret_cast<const int4 *>(chq_g + S.coff[c] + h + KC5);
-            int4 *sm = reinterpret_cast<int4 *>(&S.cc[c][s]);
-            const int4 x0 = g[0], x1 = g[1], x2 = g[2];
-            sm[0] = x0; sm[1] = x1; sm[2] = x2;
+            Q5 x;
+            load_q5(x, chq_g + S.coff[c] + h + KC5);
+            store_q5(&S.cc[c][s], x);
           }
           S.ca[c] = h + 1 < tail ? S.cc[c][(h + 1) & (KC5 - 1)].arr : INF;
-          item(IT_ALLOC_COPY, c & 7, u);
-          if (arrive_u(r)) to_inc(c & 7, r);
+          item(IT_ALLOC_COPY, c & 7, r.u);
+          if (arrive_u(r.cinfo)) to_inc(c & 7, r);
         }
         P5(1);
         // ---------------------------------------------------------- (2) ops finishing now, ascending id
@@ -436,8 +428,8 @@ __global__ void __launch_bounds__(64) k_cost5(Cost5Graph G, TopoArgs T, unsigned
             }
           }
           ef &= ~(1u << k);
-          Rec5 r;
-          load_rec5(r, &S.drun[k]);
+          Q5 r;
+          load_q5(r, &S.drun[k]);
           const int sl = S.cur[k];
           S.dfin[k] = INF;
           const int nout = r.nn & 0xffff, nin = (int)((unsigned)r.nn >> 16);
@@ -451,27 +443,28 @@ __global__ void __launch_bounds__(64) k_cost5(Cost5Graph G, TopoArgs T, unsigned
           for (int j0 = 0; j0 < nout; j0 += 32) {   // out-edges, one per lane
             const int j = j0 + lane;
             const bool valid = j < nout;
-            Rec5 wr;
+            Slot5 e;
             int tw = k;
             if (valid) {
               if (j < SO5) {
                 if (spend & (1u << (2 * k + sl))) { cp_wait0(); spend = 0; }
-                load_rec5(wr, &S.stage[k][sl][j]);
+                load_slot5(e, &S.stage[k][sl][j]);
+                tw = (S.sdev[k][sl][j] >> (8 * ((r.ob + j) & 3))) & 0xff;
               } else {
-                load_rec5(wr, G.erec + r.ob + j);
+                load_slot5(e, G.slots + r.ob + j);
+                tw = sdev_g[r.ob + j];
               }
-              tw = nib_dev(nib_s, wr.id);
             }
             const bool same = valid && tw == k, cross = valid && tw != k;
-            const bool av = same && arrive5(nib_s, bigb_s, gbig, wr);
+            const bool av = same && arrive5(flag_s, bigb_s, gbig, e.cinfo);
             const unsigned am = __ballot_sync(FULL, av);
             const unsigned cm = __ballot_sync(FULL, cross);
             if (am) {   // ops made available now on device k, in lane (= id) order
               const int n0 = S.inc_n[k];
               if (av) {
                 const int pos = n0 + __popc(am & lt);
-                if (pos < NINC5) store_rec5(&S.inc[k][pos], wr);
-                else store_rec5(ov_g + S.doff[k] + pos, wr);
+                if (pos < NINC5) store_q5(&S.inc[k][pos], q_of_slot(e, 0, r.id));
+                else store_q5(ov_g + S.doff[k] + pos, q_of_slot(e, 0, r.id));
               }
               __syncwarp();
               S.inc_n[k] = n0 + __popc(am);
@@ -483,11 +476,12 @@ __global__ void __launch_bounds__(64) k_cost5(Cost5Graph G, TopoArgs T, unsigned
                 const int rank = __popc(grp & lt), n = __popc(grp);
                 const int c = 8 * k + tw;
                 const int f = S.cfree[c], tail = S.ctail[c], hd = S.chead[c];
-                const int x = xfer_time3(r.bytes, c, T);
+                const int x = xfer_time3(e.bytes, c, T);
                 const int bt = max(t, f);
                 const int pos = tail + rank, arr = bt + (rank + 1) * x;
-                if (pos < hd + KC5) store_ent5(&S.cc[c][pos & (KC5 - 1)], wr, arr, r.id);
-                else store_ent5(chq_g + S.coff[c] + pos, wr, arr, r.id);
+                const Q5 q = q_of_slot(e, arr, r.id);
+                if (pos < hd + KC5) store_q5(&S.cc[c][pos & (KC5 - 1)], q);
+                else store_q5(chq_g + S.coff[c] + pos, q);
                 if (rank == 0) {
                   S.cfree[c] = bt + n * x;
                   S.ctail[c] = tail + n;
@@ -506,44 +500,44 @@ __global__ void __launch_bounds__(64) k_cost5(Cost5Graph G, TopoArgs T, unsigned
         const int n = S.inc_n[k];
         bool running = S.dfin[k] != INF, go = false;
         int fh = S.fh[k], ft = S.ft[k];
-        Rec5 run;
+        Q5 run;
         if (n > 0) {
           S.inc_n[k] = 0;
-          Rec5 *Li = &S.inc[k][0];
-          Rec5 *Lo = ov_g + S.doff[k];
+          Q5 *Li = &S.inc[k][0];
+          Q5 *Lo = ov_g + S.doff[k];
           if (n == 1 && !running && fh == ft) {   // common case: straight to dispatch
-            load_rec5(run, Li);
+            load_q5(run, Li);
             go = true;
           } else {
             for (int i = 1; i < n; i++) {   // insertion sort by id (n is small except after wide fan-outs)
-              Rec5 key;
-              load_rec5(key, i < NINC5 ? &Li[i] : &Lo[i]);
+              Q5 key;
+              load_q5(key, i < NINC5 ? &Li[i] : &Lo[i]);
               int j = i - 1;
               while (j >= 0) {
-                Rec5 pj;
-                load_rec5(pj, j < NINC5 ? &Li[j] : &Lo[j]);
+                Q5 pj;
+                load_q5(pj, j < NINC5 ? &Li[j] : &Lo[j]);
                 if (pj.id <= key.id) break;
-                store_rec5(j + 1 < NINC5 ? &Li[j + 1] : &Lo[j + 1], pj);
+                store_q5(j + 1 < NINC5 ? &Li[j + 1] : &Lo[j + 1], pj);
                 j--;
               }
-              store_rec5(j + 1 < NINC5 ? &Li[j + 1] : &Lo[j + 1], key);
+              store_q5(j + 1 < NINC5 ? &Li[j + 1] : &Lo[j + 1], key);
             }
             for (int i = 0; i < n; i++, ft++) {
-              Rec5 x;
-              load_rec5(x, i < NINC5 ? &Li[i] : &Lo[i]);
-              if (ft < fh + KF5) store_rec5(&S.fc[k][ft & (KF5 - 1)], x);
-              else store_rec5(fifo_g + S.doff[k] + ft, x);
+              Q5 x;
+              load_q5(x, i < NINC5 ? &Li[i] : &Lo[i]);
+              if (ft < fh + KF5) store_q5(&S.fc[k][ft & (KF5 - 1)], x);
+              else store_q5(fifo_g + S.doff[k] + ft, x);
             }
             S.ft[k] = ft;
           }
         }
         if (!go && !running && fh < ft) {   // pop the FIFO head
           const int s = fh & (KF5 - 1);
-          load_rec5(run, &S.fc[k][s]);
+          load_q5(run, &S.fc[k][s]);
           if (fh + KF5 < ft) {   // the slot takes position fh + KF5 from the global overflow (rare)
-            Rec5 x;
-            ld_rec_g(x, fifo_g + S.doff[k] + fh + KF5);
-            store_rec5(&S.fc[k][s], x);
+            Q5 x;
+            load_q5(x, fifo_g + S.doff[k] + fh + KF5);
+            store_q5(&S.fc[k][s], x);
           }
           S.fh[k] = ++fh;
           go = true;
@@ -552,7 +546,7 @@ __global__ void __launch_bounds__(64) k_cost5(Cost5Graph G, TopoArgs T, unsigned
         if (go) {
           const int fin = t + run.cost * T.speed[k];
           S.dfin[k] = fin;
-          store_rec5(&S.drun[k], run);
+          store_q5(&S.drun[k], run);
           mk = max(mk, fin);
           disp++;
           item(IT_ALLOC_OP, k, run.id);
@@ -564,8 +558,8 @@ __global__ void __launch_bounds__(64) k_cost5(Cost5Graph G, TopoArgs T, unsigned
           running = true;
         }
         if (running && fh < ft && S.nxt[k] < 0) {   // stage the op now waiting at the head
-          Rec5 hr;
-          load_rec5(hr, &S.fc[k][fh & (KF5 - 1)]);
+          Q5 hr;
+          load_q5(hr, &S.fc[k][fh & (KF5 - 1)]);
           S.nxt[k] = hr.id;
           if (hr.nn & 0xffff) stage(k, cur ^ 1, hr);
         }
@@ -630,7 +624,7 @@ __global__ void __launch_bounds__(64) k_cost5(Cost5Graph G, TopoArgs T, unsigned
           const IRec ir = G.irec[idx];
           u = ir.u;
           bu = ir.bytes;
-          du = nib_dev(nib_s, u);
+          du = D[u];
           if (du != dev) { dA = dev; xA = -bu; }   // the copy this op held
         } else {
           done = true;
@@ -688,7 +682,7 @@ __global__ void __launch_bounds__(64) k_cost5(Cost5Graph G, TopoArgs T, unsigned
 
 }  // namespace
 
-size_t cost5_smem_bytes(int N, int nbigb) { return 4 * (size_t)nib_words(N) + 4 * (size_t)nbigb; }   // dynamic part
+size_t cost5_smem_bytes(int nflagw, int nbigb) { return 4 * (size_t)nflagw + 4 * (size_t)nbigb; }   // dynamic part
 size_t cost5_scratch_per_placement(int N, long long E, int ngbig) { return scratch5_layout(N, E, ngbig).total; }
 
 // every transfer takes >= 1 tick and every duration >= 1 (no same-instant rounds)
@@ -705,7 +699,7 @@ bool cost5_eligible(const TopoArgs &T, const Cost5Graph &G, int min_cost, long l
         if (x < 1) return false;
       }
   }
-  return sizeof(Smem5) + cost5_smem_bytes(G.N, G.nbigb) <= 227 * 1024;
+  return sizeof(Smem5) + cost5_smem_bytes(G.nflagw, G.nbigb) <= 227 * 1024;
 }
 
 bool launch_cost5(const Cost5Graph &G, const TopoArgs &T, int min_cost, long long min_edge_bytes, const uint8_t *D,
@@ -713,7 +707,7 @@ bool launch_cost5(const Cost5Graph &G, const TopoArgs &T, int min_cost, long lon
                   long long *busy, double *reward, cudaStream_t s) {
   if (!cost5_eligible(T, G, min_cost, min_edge_bytes)) return false;
   if (per_place < cost5_scratch_per_placement(G.N, G.E, G.ngbig)) return false;
-  const size_t smem = cost5_smem_bytes(G.N, G.nbigb);
+  const size_t smem = cost5_smem_bytes(G.nflagw, G.nbigb);
   static size_t configured = 0;
   if (smem + sizeof(Smem5) > 48 * 1024 && smem > configured) {
     cudaFuncSetAttribute(k_cost5, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -722,7 +716,7 @@ bool launch_cost5(const Cost5Graph &G, const TopoArgs &T, int min_cost, long lon
   note_launch("k_cost5_pre", s);
   k_cost5_pre<<<B, 512, 0, s>>>(G, T, D, scratch, per_place);
   note_launch("k_cost5", s);
-  k_cost5<<<B, 64, smem, s>>>(G, T, scratch, per_place, rep, peak, busy, reward);
+  k_cost5<<<B, 64, smem, s>>>(G, T, D, scratch, per_place, rep, peak, busy, reward);
   return true;
 }
 
@@ -730,29 +724,35 @@ bool launch_cost5(const Cost5Graph &G, const TopoArgs &T, int min_cost, long lon
 gdp_status cost5_build(int N, long long E, const int *optr, const int *oidx, const int *iptr, const int *cost,
                        const long long *out_bytes, Cost5Host *h) {
   h->ok = N < (1 << 25) && E < (1LL << 25);
-  h->rec.assign(N, Rec5{});
-  h->erec.assign((size_t)std::max<long long>(E, 1), Rec5{});
-  h->srcs.clear();
+  h->slots.assign((size_t)std::max<long long>(E, 1), Slot5{});
+  h->srcq.clear();
   h->bigb.clear();
   h->gbig.clear();
   h->outdeg.assign(N, 0);
-  int nb = 0;
+  std::vector<Q5> q(N);
+  int nb = 0, nf = 0;
   std::vector<unsigned char> bytes;
   for (int v = 0; v < N; v++) {
     const int din = iptr[v + 1] - iptr[v], dout = optr[v + 1] - optr[v];
     if (din >= 65536 || dout >= 65536) h->ok = false;
-    Rec5 &r = h->rec[v];
-    r.id = v; r.cost = cost[v]; r.ob = optr[v]; r.ib = iptr[v];
+    Q5 &r = q[v];
+    r.id = v; r.cost = cost[v]; r.ob = optr[v]; r.ib = iptr[v]; r.arr = 0; r.u = 0;
     r.nn = (dout & 0xffff) | ((din & 0xffff) << 16);
-    r.bytes = out_bytes[v];
     if (din <= 1) r.cinfo = 0;
-    else if (din == 2) r.cinfo = 1;
+    else if (din == 2) r.cinfo = 1 | (nf++ << 2);
     else if (din < 255) { r.cinfo = 2 | (nb << 2); bytes.push_back((unsigned char)din); nb++; }
     else { r.cinfo = 3 | ((int)h->gbig.size() << 2); h->gbig.push_back(din); }
-    if (din == 0) h->srcs.push_back(v);
+    if (din == 0) h->srcq.push_back(r);
     h->outdeg[v] = dout;
   }
-  for (long long e = 0; e < E; e++) h->erec[(size_t)e] = h->rec[oidx[e]];
+  for (int v = 0; v < N; v++)
+    for (int e = optr[v]; e < optr[v + 1]; e++) {
+      const Q5 &w = q[oidx[e]];
+      Slot5 &s = h->slots[(size_t)e];
+      s.w = w.id; s.cost = w.cost; s.ob = w.ob; s.nn = w.nn; s.cinfo = w.cinfo; s.ib = w.ib;
+      s.bytes = out_bytes[v];   // the producer's output: the size of the copy on this edge
+    }
+  h->nflagw = (nf + 31) / 32;
   while (bytes.size() % 16) bytes.push_back(0);
   h->bigb.assign(bytes.size() / 4, 0u);
   for (size_t i = 0; i < bytes.size(); i++) h->bigb[i / 4] |= (unsigned)bytes[i] << (8 * (i % 4));

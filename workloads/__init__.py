@@ -511,9 +511,9 @@ def config(name: str, batch: Optional[int] = None, mem_len: Optional[int] = None
         w = Workload("c3_txl20k_wavenet20k_d8", [transformer_xl(seed=1003), wavenet(seed=1004)],
                      d=8, seg_len=128, mem_len=128, batch=64)
     elif name == "c4":
-        # B = 592 = 148 SMs x 4 resident k_cost5 CTAs: one full wave of the cost kernel (one CTA
-        # per placement, 54.5 KB of shared memory each at N = 52 k)
-        w = Workload("c4_gnmt52k_d8", [gnmt(seed=1005)], d=8, seg_len=128, mem_len=128, batch=592)
+        # B = 1184 = 148 SMs x 8 resident k_cost5 CTAs: one full wave of the cost kernel (one CTA
+        # per placement, 27 KB of shared memory each at N = 52 k)
+        w = Workload("c4_gnmt52k_d8", [gnmt(seed=1005)], d=8, seg_len=128, mem_len=128, batch=1184)
     elif name == "c5":
         gs = []
         for i, s in enumerate([1011, 1015]):
