@@ -268,18 +268,20 @@ gdp_status gdp_cost(gdp_graph g, gdp_topo t, const uint8_t *placements, int32_t 
  * model").  Returns 0 and sets the error for NULL handles. */
 int32_t gdp_cost_kernel(gdp_graph g, gdp_topo t);
 
-/* Diagnostic (tests): device pointer to an intermediate that the last gdp_embed / gdp_place on
- * this workspace saved in `ws` (no copy, no launch; valid until the next call on ws):
- *   what 0: max-pool argmax of GNN layer `layer` (0..2), int32 N x 64, caller node order, the
- *           lowest-id neighbour attaining the max per channel (Eq. 2), -1 if none;
- *   what 1: FFN hidden activation m = ReLU(LN2(x1) W1' + b1) of Transformer-XL layer `layer`
- *           (0 conditioner, 1, 2 placement layers), fp32 N x 256, Kahn (topological) row order;
- *   what 2: the per-node map o = ReLU(LN1(x) Wv' + bv) of layer `layer` in the no_attention
- *           ablation (else the attention output), fp32 N x 64, Kahn row order.
- * The parity tests use them to adopt the GPU's decision at max-pool near-ties and ReLU inputs
- * near zero ("tie import").  Errors: GDP_ERR_ARG, GDP_ERR_WORKSPACE. */
-gdp_status gdp_debug_tensor(gdp_graph g, const gdp_config *c, void *ws, size_t ws_bytes, int32_t what,
-                            int32_t layer, void **out);
+/* Diagnostic (tests): the table of intermediates that gdp_embed / gdp_place / gdp_policy_grad
+ * save in the workspace, as (name, byte offset from ws, rows, cols, is_int32) -- fp32 unless
+ * is_int32.  GNN tensors (H0..H3, Z0..Z2, A0..A2 = max-pooled neighbourhoods, ARG0..ARG2 =
+ * first-index argmax, -1 if none) are in caller node order; the placer's (Etopo, L<l>.a / qkv
+ * / o / lse / x1 / c / m / y per layer l = 0 conditioner, 1, 2, and the folded weights
+ * L<l>.Wqkv / bqkv / Wo / W1 / W2, Wh) in Kahn order; z, gam are the superposition context and
+ * gates.  Backward scratch (dlog, dy, dm, dc, dx1, dout, dqkv, dkvm, da, dam, dEt, dH, dHn, dAg,
+ * dP) holds the values of the LAST layer gdp_policy_grad processed.  The offsets do not depend
+ * on B.  Writes at most max_names entries and returns the number of tensors, -1 on bad
+ * arguments.  The parity tests read them to hold every kernel to the oracle on the kernel's
+ * own inputs, and to adopt the GPU's decision at max-pool near-ties and ReLU inputs near zero
+ * ("tie import"). */
+int32_t gdp_debug_tensors(gdp_graph g, const gdp_config *c, int32_t max_names, const char **names,
+                          int64_t *offsets, int64_t *rows, int64_t *cols, int32_t *is_int);
 
 /* Diagnostic / test entry: gdp_cost on an explicitly chosen kernel (5, 3 or 1; 0 = the
  * automatic choice gdp_cost makes).  GDP_ERR_ARG if that kernel does not apply to (g, t)

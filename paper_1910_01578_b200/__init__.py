@@ -26,7 +26,7 @@ REPORT_BYTES = 24
 
 EXPORTS = ["gdp_default_config", "gdp_last_error", "gdp_launch_count", "gdp_build_info", "gdp_cost_kernel", "gdp_logprob", "gdp_clip_adam", "gdp_sample_at", "gdp_greedy", "gdp_graph_validate", "gdp_graph_create", "gdp_graph_destroy",
            "gdp_topo_create", "gdp_topo_destroy", "gdp_param_layout", "gdp_workspace_size", "gdp_embed",
-           "gdp_place", "gdp_sample", "gdp_cost", "gdp_cost_with_kernel", "gdp_debug_tensor", "gdp_advantage", "gdp_policy_grad", "gdp_profile_enable",
+           "gdp_place", "gdp_sample", "gdp_cost", "gdp_cost_with_kernel", "gdp_debug_tensors", "gdp_advantage", "gdp_policy_grad", "gdp_profile_enable",
            "gdp_profile_mark", "gdp_profile_read"]
 
 
@@ -68,7 +68,7 @@ def lib():
             "gdp_sample": [P, P, P, I32, U64, U64, U64, P, P, P, SZ, P],
             "gdp_cost": [P, P, P, I32, P, P, P, P, P, SZ, P],
             "gdp_cost_with_kernel": [P, P, P, I32, P, P, P, P, P, SZ, I32, P],
-            "gdp_debug_tensor": [P, P, P, SZ, I32, I32, ctypes.POINTER(ctypes.c_void_p)],
+            "gdp_debug_tensors": [P, P, I32, ctypes.POINTER(ctypes.c_char_p), P, P, P, P],
             "gdp_advantage": [P, I32, P, P, P, P],
             "gdp_policy_grad": [P, P, P, P, P, I32, P, P, P, F32, F32, F32, P, P, SZ, P],
             "gdp_logprob": [P, P, P, P, I32, P, P, SZ, P],
@@ -283,21 +283,26 @@ def gdp_cost(g: Graph, t: Topo, placements, B: int, rep, peak_mem, busy, reward,
                           _t_ptr(reward), _t_ptr(ws), ws.numel(), _stream(stream)), "gdp_cost")
 
 
-def debug_tensor(g: Graph, cfg: Config, ws, what: int, layer: int):
-    """gdp_debug_tensor: a torch view (on the workspace's device) of a saved intermediate:
-    what 0 max-pool argmax of GNN layer (int32 N x 64), 1 FFN hidden m of XL layer (fp32 N x 256,
-    Kahn order), 2 the no-attention map o (fp32 N x 64, Kahn order)."""
+def debug_tensors(g: Graph, cfg: Config, ws) -> dict:
+    """gdp_debug_tensors: {name: torch view into the workspace} of the saved intermediates
+    (include/gdp.h; fp32 or int32, 2-D)."""
     import torch
-    ptr = ctypes.c_void_p()
-    _check(lib().gdp_debug_tensor(g.h, ctypes.byref(cfg), _t_ptr(ws), ws.numel(), what, layer, ctypes.byref(ptr)),
-           "gdp_debug_tensor")
-    n = g.N * (64 if what in (0, 2) else 256)
-    esz = 4
-    base = ws.data_ptr()
-    off = ptr.value - base
-    assert 0 <= off and off + n * esz <= ws.numel(), "debug tensor outside the workspace"
-    t = ws[off:off + n * esz].view(torch.int32 if what == 0 else torch.float32)
-    return t.view(g.N, -1)
+    L = lib()
+    n = int(L.gdp_debug_tensors(g.h, ctypes.byref(cfg), 0, None, None, None, None, None))
+    if n < 0:
+        raise RuntimeError("gdp_debug_tensors: " + last_error())
+    names = (ctypes.c_char_p * n)()
+    off = np.zeros(n, np.int64); rows = np.zeros(n, np.int64); cols = np.zeros(n, np.int64)
+    isint = np.zeros(n, np.int32)
+    L.gdp_debug_tensors(g.h, ctypes.byref(cfg), n, names, off.ctypes.data, rows.ctypes.data, cols.ctypes.data,
+                        isint.ctypes.data)
+    out = {}
+    for i in range(n):
+        nb = int(rows[i] * cols[i] * 4)
+        assert off[i] + nb <= ws.numel(), "debug tensor outside the workspace"
+        t = ws[int(off[i]):int(off[i]) + nb].view(torch.int32 if isint[i] else torch.float32)
+        out[names[i].decode()] = t.view(int(rows[i]), int(cols[i]))
+    return out
 
 
 def gdp_advantage(reward, B: int, run_sum, run_count, adv, stream=None):

@@ -611,18 +611,71 @@ static gdp_status carve_any(const gdp_graph_s *g, int d, int Bneed, void *ws, si
   return carve(g, d, Bneed, ws, ws_bytes, w);
 }
 
-gdp_status gdp_debug_tensor(gdp_graph g, const gdp_config *c, void *ws, size_t ws_bytes, int32_t what,
-                            int32_t layer, void **out) {
-  if (!g || !out) return fail(GDP_ERR_ARG, "NULL argument");
-  gdp_status st = check_config(c);
-  if (st != GDP_OK) return st;
+int32_t gdp_debug_tensors(gdp_graph g, const gdp_config *c, int32_t max_names, const char **names, int64_t *offsets,
+                          int64_t *rows, int64_t *cols, int32_t *is_int) {
+  if (!g || max_names < 0 || (max_names > 0 && (!names || !offsets || !rows || !cols || !is_int))) {
+    set_error("gdp_debug_tensors: bad arguments");
+    return -1;
+  }
+  if (check_config(c) != GDP_OK) return -1;
+  static const char kLayerNames[3][16][12] = {
+      {"L0.a", "L0.qkv", "L0.o", "L0.lse", "L0.x1", "L0.c", "L0.m", "L0.y", "L0.Wqkv", "L0.bqkv", "L0.Wo", "L0.W1", "L0.W2", "L0.mu1", "L0.rs1", "L0.mu2"},
+      {"L1.a", "L1.qkv", "L1.o", "L1.lse", "L1.x1", "L1.c", "L1.m", "L1.y", "L1.Wqkv", "L1.bqkv", "L1.Wo", "L1.W1", "L1.W2", "L1.mu1", "L1.rs1", "L1.mu2"},
+      {"L2.a", "L2.qkv", "L2.o", "L2.lse", "L2.x1", "L2.c", "L2.m", "L2.y", "L2.Wqkv", "L2.bqkv", "L2.Wo", "L2.W1", "L2.W2", "L2.mu1", "L2.rs1", "L2.mu2"}};
+  static const char kGnn[4][3][6] = {{"H0", "Z0", "A0"}, {"H1", "Z1", "A1"}, {"H2", "Z2", "A2"}, {"H3", "", ""}};
+  static const char kArg[3][6] = {"ARG0", "ARG1", "ARG2"};
+  char *base = reinterpret_cast<char *>((uintptr_t)1 << 40);   // any base: only offsets are returned
   WS w;
-  st = carve_any(g, c->num_devices, 1, ws, ws_bytes, &w);
-  if (st != GDP_OK) return st;
-  if (what == 0 && layer >= 0 && layer < kGNN) { *out = w.ARG[layer]; return GDP_OK; }
-  if (what == 1 && layer >= 0 && layer < 3) { *out = w.L[layer].m; return GDP_OK; }
-  if (what == 2 && layer >= 0 && layer < 3) { *out = w.L[layer].o; return GDP_OK; }
-  return fail(GDP_ERR_ARG, "gdp_debug_tensor: unknown (what, layer)");
+  ws_layout(g, c->num_devices, 1, base, &w);
+  const long long N = g->N;
+  int n = 0;
+  auto add = [&](const char *nm, const void *p, long long r, long long cc, int isint) {
+    if (n < max_names) {
+      names[n] = nm; offsets[n] = (int64_t)(reinterpret_cast<const char *>(p) - base); rows[n] = r; cols[n] = cc;
+      is_int[n] = isint;
+    }
+    n++;
+  };
+  for (int l = 0; l < 4; l++) {
+    add(kGnn[l][0], w.H[l], N, kH, 0);
+    if (l < 3) { add(kGnn[l][1], w.Z[l], N, kH, 0); add(kGnn[l][2], w.A[l], N, kH, 0); add(kArg[l], w.ARG[l], N, kH, 1); }
+  }
+  add("Etopo", w.Etopo, N, kH, 0);
+  add("z", w.z, 1, kH, 0);
+  add("gam", w.gam, 1, kGamTotal, 0);
+  add("Wh", w.Wh, kH, c->num_devices, 0);
+  for (int l = 0; l < 3; l++) {
+    const Layer &L = w.L[l];
+    const void *ps[16] = {L.a, L.qkv, L.o, L.lse, L.x1, L.c, L.m, L.y, L.Wqkv, L.bqkv, L.Wo, L.W1, L.W2, L.mu1, L.rs1, L.mu2};
+    const long long rs[16] = {N, N, N, N, N, N, N, N, kH, 1, kH, kH, kFFN, N, N, N};
+    const long long cs[16] = {kH, 192, kH, kHeads, kH, kH, kFFN, kH, 192, 192, kH, kFFN, kH, 1, 1, 1};
+    for (int j = 0; j < 16; j++) add(kLayerNames[l][j], ps[j], rs[j], cs[j], 0);
+  }
+  static const char kDW[3][4][10] = {{"L0.dWqkv", "L0.dWo", "L0.dW1", "L0.dW2"},
+                                     {"L1.dWqkv", "L1.dWo", "L1.dW1", "L1.dW2"},
+                                     {"L2.dWqkv", "L2.dWo", "L2.dW1", "L2.dW2"}};
+  for (int l = 0; l < 3; l++) {   // weight gradients of the folded maps, bias row last
+    add(kDW[l][0], w.L[l].dWqkv, kH + 1, 192, 0);
+    add(kDW[l][1], w.L[l].dWo, kH + 1, kH, 0);
+    add(kDW[l][2], w.L[l].dW1, kH + 1, kFFN, 0);
+    add(kDW[l][3], w.L[l].dW2, kFFN + 1, kH, 0);
+  }
+  add("dlog", w.dlog, N, c->num_devices, 0);
+  add("dy", w.dy, N, kH, 0);
+  add("dx1", w.dx1, N, kH, 0);
+  add("dm", w.dm, N, kFFN, 0);
+  add("dc", w.dc, N, kH, 0);
+  add("dout", w.dout, N, kH, 0);
+  add("dqkv", w.dqkv, N, 192, 0);
+  add("dkvm", w.dkvm, N, 128, 0);
+  add("da", w.da, N, kH, 0);
+  add("dam", w.dam, N, kH, 0);
+  add("dEt", w.dEt, N, kH, 0);
+  add("dH", w.dH, N, kH, 0);
+  add("dHn", w.dHn, N, kH, 0);
+  add("dAg", w.dAg, N, kH, 0);
+  add("dP", w.dP, N, kH, 0);
+  return n;
 }
 
 gdp_status gdp_embed(gdp_graph g, const gdp_config *c, const float *theta, float *node_emb, void *ws,

@@ -1,0 +1,211 @@
+"""Per-kernel parity of the tensor-core mode on the kernel's own inputs.
+
+After one embed -> place -> sample -> policy_grad step in tensor-core mode (gdp_config.tensor_cores
+= 1: tcgen05 GEMMs and attention tiles, bf16 operands), every intermediate the workspace holds
+(gdp_debug_tensors) is recomputed by oracle/tc.py from the GPU's own inputs to that kernel --
+the same fp32 operands, rounded to bf16 the same way -- and compared elementwise:
+
+    |x - r| <= rtol * max(|r|, 1e-2 * max|r|) + bound,     rtol = 2e-2 (BASELINE north_star, bf16)
+
+where `bound` = 2^-8 * sum |terms| only for products whose bf16 operand the oracle computes itself
+(attention P~, dS, P; SURVEY §8(c) "c u sum|terms|"), else 0.  fp32 SIMT kernels in the same
+step (LayerNorm, gates, folding, the head, weight gradients, max-pool) use rtol 1e-4; the
+max-pool values and argmax indices are bit-exact.  Cases: C2 (79 row tiles per map) and C4 at
+full size (408 tiles of the 192/256-wide maps for 296 CTA slots: the persistent multi-tile loop
+of k_gemm_tc).
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from oracle import model as Mo
+from oracle import tc as Otc
+import workloads
+
+pytestmark = pytest.mark.gpu
+
+RT = 2e-2      # bf16 tensor-core kernels
+RS = 1e-4      # fp32 SIMT kernels
+FLOOR = 1e-2
+
+
+def check(name, x, r, rtol, bound=None, floor=FLOOR):
+    x = np.asarray(x, np.float64)
+    r = np.asarray(r, np.float64)
+    assert x.shape == r.shape, (name, x.shape, r.shape)
+    scale = np.maximum(np.abs(r), floor * max(np.abs(r).max(), 1e-30))
+    tol = rtol * scale + (0.0 if bound is None else np.asarray(bound, np.float64))
+    bad = np.abs(x - r) > tol
+    worst = float((np.abs(x - r) / tol).max()) if x.size else 0.0
+    assert not bad.any(), (name, int(bad.sum()), worst)
+    return worst
+
+
+@pytest.fixture(scope="module")
+def gdp():
+    import __graft_entry__
+    __graft_entry__.build()
+    import paper_1910_01578_b200 as m
+    assert torch.cuda.is_available()
+    return m
+
+
+def tc_step(gdp, g, d, S, M, B, th):
+    """One tensor-core-mode step; returns numpy copies of every saved intermediate, taken after
+    place (forward) and after policy_grad (backward scratch of the last layer processed)."""
+    X = workloads.features(g)
+    G = gdp.Graph(g, X)
+    cfg = gdp.default_config(d, S, M, True, tensor_cores=True)
+    ws = torch.zeros(gdp.workspace_size(G, cfg, B), dtype=torch.uint8, device="cuda")
+    views = gdp.debug_tensors(G, cfg, ws)
+    theta = torch.from_numpy(th).cuda()
+    emb = torch.empty(g.N, 64, device="cuda")
+    logits = torch.empty(g.N, d, device="cuda")
+    gdp.gdp_embed(G, cfg, theta, emb, ws)
+    gdp.gdp_place(G, cfg, theta, emb, logits, ws)
+    torch.cuda.synchronize()
+    fwd = {k: v.cpu().numpy().copy() for k, v in views.items()}
+    D = torch.empty(B, g.N, dtype=torch.uint8, device="cuda")
+    lp = torch.empty(B, dtype=torch.float32, device="cuda")
+    gdp.gdp_sample(G, cfg, logits, B, 42, 0, 0, D, lp, ws)
+    adv = torch.from_numpy(np.random.default_rng(3).normal(size=B)).cuda()
+    _, n = gdp.param_layout(cfg, X.shape[1])
+    grad = torch.zeros(n, device="cuda")
+    gdp.gdp_policy_grad(G, cfg, theta, logits, D, B, adv, lp, None, 0.2, 0.01, 1.0 / B, grad, ws)
+    torch.cuda.synchronize()
+    bwd = {k: v.cpu().numpy().copy() for k, v in views.items()}
+    return X, fwd, bwd, logits.cpu().numpy()
+
+
+def params(th, F, d):
+    return {k: v.numpy() for k, v in Mo.unflatten(torch.as_tensor(th.astype(np.float64)), F, d).items()}
+
+
+def ln(x, g, b):
+    return Mo.layer_norm(torch.as_tensor(x, dtype=torch.float64), torch.as_tensor(g), torch.as_tensor(b)).numpy()
+
+
+def maxpool_exact(Z, g):
+    """Eq. 2 max over N(v) of the GPU's own fp32 Z, lowest id first on ties: the selection
+    is exact, so values and indices must match bit for bit."""
+    ptr, idx = Mo.neighbours(g.N, g.edges)
+    A, arg = Mo.gather_max(torch.as_tensor(Z), ptr, idx)
+    return A.numpy(), arg.numpy()
+
+
+def run_kernel_checks(gdp, g, d, S, M, B, seed=13):
+    th = workloads.init_theta(workloads.F, d, seed=seed, mode="random")
+    X, f, b, logits = tc_step(gdp, g, d, S, M, B, th)
+    p = params(th, X.shape[1], d)
+    N = g.N
+    worst = {}
+    # ---- GNN (caller order): a1-a4
+    worst["H0"] = check("H0", f["H0"], Otc.gemm(X, p["gnn.in.W"], p["gnn.in.b"]), RT)
+    for l in range(3):
+        worst[f"Z{l}"] = check(f"Z{l}", f[f"Z{l}"], Otc.gemm(f[f"H{l}"], p[f"gnn.{l}.W"], p[f"gnn.{l}.b"], "sigmoid"), RT)
+        A, arg = maxpool_exact(f[f"Z{l}"], g)
+        assert np.array_equal(f[f"A{l}"], A.astype(np.float32)), f"A{l}"
+        assert np.array_equal(f[f"ARG{l}"], arg), f"ARG{l}"
+        worst[f"H{l + 1}"] = check(f"H{l + 1}", f[f"H{l + 1}"],
+                                   Otc.gemm(np.concatenate([f[f"H{l}"], f[f"A{l}"]], 1), p[f"gnn.{l}.Wf"],
+                                            p[f"gnn.{l}.bf"], "tanh"), RT)
+    # ---- placer (Kahn order; generated graphs are topologically numbered): a5-a10
+    order = Mo.topo_order(N, g.edges)
+    assert np.array_equal(f["Etopo"], f["H3"][order])
+    # a5: conditioner -> z -> gates -> folded weights (fp32 SIMT)
+    z = f["L0.y"].astype(np.float64).mean(0)
+    worst["z"] = check("z", f["z"][0], z, RS)
+    gam = {}
+    off = 0
+    for l in range(2):
+        for j in Mo.GATED:
+            w = Mo.FFN if j == "f2" else Mo.H
+            gam[(l, j)] = 2.0 / (1.0 + np.exp(-(f["z"][0].astype(np.float64) @ p[f"gate{l}.{j}.P"] + p[f"gate{l}.{j}.q"])))
+            off += w
+    gh = 2.0 / (1.0 + np.exp(-(f["z"][0].astype(np.float64) @ p["gate.head.P"] + p["gate.head.q"])))
+    gam_all = np.concatenate([gam[(l, j)] for l in range(2) for j in Mo.GATED] + [gh])
+    worst["gam"] = check("gam", f["gam"][0], gam_all, RS)
+    xin = {0: f["Etopo"], 1: f["Etopo"], 2: f["L1.y"]}
+    names = {0: "cond", 1: "xl0", 2: "xl1"}
+    for l in range(3):
+        n = names[l]
+        gg = (lambda j: np.ones(64 if j != "f2" else 256)) if l == 0 else (
+            lambda j, l=l: f["gam"][0].astype(np.float64)[_gam_slice(l - 1, j)])
+        Wqkv = np.concatenate([gg("q")[:, None] * p[f"{n}.Wq"], gg("k")[:, None] * p[f"{n}.Wk"],
+                               gg("v")[:, None] * p[f"{n}.Wv"]], 1)
+        worst[f"L{l}.Wqkv"] = check(f"L{l}.Wqkv", f[f"L{l}.Wqkv"], Wqkv, RS, floor=0.0)
+        worst[f"L{l}.Wo"] = check(f"L{l}.Wo", f[f"L{l}.Wo"], gg("o")[:, None] * p[f"{n}.Wo"], RS, floor=0.0)
+        worst[f"L{l}.W1"] = check(f"L{l}.W1", f[f"L{l}.W1"], gg("f1")[:, None] * p[f"{n}.W1"], RS, floor=0.0)
+        worst[f"L{l}.W2"] = check(f"L{l}.W2", f[f"L{l}.W2"], gg("f2")[:, None] * p[f"{n}.W2"], RS, floor=0.0)
+        x = xin[l]
+        worst[f"L{l}.a"] = check(f"L{l}.a", f[f"L{l}.a"], ln(x, p[f"{n}.ln1.g"], p[f"{n}.ln1.b"]), RS)
+        worst[f"L{l}.qkv"] = check(f"L{l}.qkv", f[f"L{l}.qkv"], Otc.gemm(f[f"L{l}.a"], f[f"L{l}.Wqkv"], f[f"L{l}.bqkv"][0]), RT)
+        O, _, ob = Otc.attention_fwd(f[f"L{l}.qkv"], N, S, M)
+        worst[f"L{l}.o"] = check(f"L{l}.o", f[f"L{l}.o"], O, RT, bound=ob)
+        worst[f"L{l}.x1"] = check(f"L{l}.x1", f[f"L{l}.x1"], Otc.gemm(f[f"L{l}.o"], f[f"L{l}.Wo"], p[f"{n}.bo"], R=x), RT)
+        worst[f"L{l}.c"] = check(f"L{l}.c", f[f"L{l}.c"], ln(f[f"L{l}.x1"], p[f"{n}.ln2.g"], p[f"{n}.ln2.b"]), RS)
+        worst[f"L{l}.m"] = check(f"L{l}.m", f[f"L{l}.m"], Otc.gemm(f[f"L{l}.c"], f[f"L{l}.W1"], p[f"{n}.b1"], "relu"), RT)
+        worst[f"L{l}.y"] = check(f"L{l}.y", f[f"L{l}.y"], Otc.gemm(f[f"L{l}.m"], f[f"L{l}.W2"], p[f"{n}.b2"], R=f[f"L{l}.x1"]), RT)
+    # a10 head: folded W_h' = diag(gamma_h) W_h; width d < 16 stays on the fp32 SIMT GEMM
+    worst["Wh"] = check("Wh", f["Wh"], gh[:, None] * p["head.W"], RS, floor=0.0)
+    zl = f["L2.y"].astype(np.float64) @ f["Wh"].astype(np.float64) + p["head.b"]
+    worst["logits"] = check("logits", logits[order], zl, RS)
+    # ---- backward of the last layer processed (the conditioner): a15 kernels on their inputs
+    dy, m = b["dy"], f["L0.m"]
+    dm = Otc.gemm(dy, f["L0.W2"].T) * (m > 0)
+    worst["dm"] = check("dm", b["dm"], dm, RT)
+    worst["dc"] = check("dc", b["dc"], Otc.gemm(b["dm"], f["L0.W1"].T), RT)
+    x1 = torch.as_tensor(f["L0.x1"].astype(np.float64)).requires_grad_(True)
+    cc = Mo.layer_norm(x1, torch.as_tensor(p["cond.ln2.g"]), torch.as_tensor(p["cond.ln2.b"]))
+    (dx1,) = torch.autograd.grad(cc, x1, torch.as_tensor(b["dc"].astype(np.float64)))
+    worst["dx1"] = check("dx1", b["dx1"], dx1.numpy() + dy, RS)
+    worst["dout"] = check("dout", b["dout"], Otc.gemm(b["dx1"], f["L0.Wo"].T), RT)
+    ref, bnd = Otc.attention_bwd(f["L0.qkv"], f["L0.o"], b["dout"], N, S, M)
+    parts = {"dQ": b["dqkv"][:, :64], "dK_own": b["dqkv"][:, 64:128], "dV_own": b["dqkv"][:, 128:],
+             "dK_mem": b["dkvm"][:, :64], "dV_mem": b["dkvm"][:, 64:]}
+    for k, v in parts.items():
+        worst[k] = check(k, v, ref[k], RT, bound=bnd[k])
+    worst["da"] = check("da", b["da"], Otc.gemm(b["dqkv"], f["L0.Wqkv"].T), RT)
+    worst["dam"] = check("dam", b["dam"], Otc.gemm(b["dkvm"], f["L0.Wqkv"][:, 64:].T), RT)
+    # weight gradients of the conditioner's folded maps (fp32 SIMT k_wgrad, bias row last)
+    aug = lambda a: np.concatenate([a.astype(np.float64), np.ones((N, 1))], 1)
+    worst["dW2"] = check("dW2", b["L0.dW2"], aug(f["L0.m"]).T @ dy.astype(np.float64), RS)
+    worst["dW1"] = check("dW1", b["L0.dW1"], aug(f["L0.c"]).T @ b["dm"].astype(np.float64), RS)
+    worst["dWo"] = check("dWo", b["L0.dWo"], aug(f["L0.o"]).T @ b["dx1"].astype(np.float64), RS)
+    dkvt = b["dqkv"].astype(np.float64).copy()
+    dkvt[:, 64:] += b["dkvm"]
+    worst["dWqkv"] = check("dWqkv", b["L0.dWqkv"], aug(f["L0.a"]).T @ dkvt, RS)
+    return worst
+
+
+def _gam_slice(l, j):
+    o = 0
+    for ll in range(2):
+        for jj in Mo.GATED:
+            w = Mo.FFN if jj == "f2" else Mo.H
+            if ll == l and jj == j:
+                return slice(o, o + w)
+            o += w
+    raise KeyError(j)
+
+
+def test_tensor_core_kernels_c2(gdp):
+    W = workloads.config("c2")
+    worst = run_kernel_checks(gdp, W.graphs[0], W.d, W.seg_len, W.mem_len, 16)
+    print({k: round(v, 4) for k, v in worst.items()})
+
+
+@pytest.mark.parametrize("S,M", [(96, 160), (100, 60), (100, -1)])
+def test_tensor_core_kernels_memory_lengths(gdp, S, M):
+    """Ragged segments, M > S (several key blocks, the dQ / dK-dV kernels), M < S, M = inf."""
+    g = workloads.random_dag(1000, p_edge=0.05, max_back=60, seed=21)
+    run_kernel_checks(gdp, g, 4, S, M, 16)
+
+
+def test_tensor_core_kernels_full_size_c4(gdp):
+    """C4 at full size (52 122 rows: 408 row tiles of the 192 / 256-wide maps for 296 CTA
+    slots, so every persistent k_gemm_tc CTA runs several tiles), B = 8."""
+    W = workloads.config("c4")
+    worst = run_kernel_checks(gdp, W.graphs[0], W.d, W.seg_len, W.mem_len, 8, seed=7)
+    print({k: round(v, 4) for k, v in worst.items()})

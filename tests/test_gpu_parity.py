@@ -1,13 +1,18 @@
 """GPU parity: every C-ABI stage against the oracle on the same seeded inputs.
 
-Tolerances (BASELINE.json north_star; DESIGN.md §"Parity"):
+Tolerances (BASELINE.json north_star):
   * integers (placements, makespans, validity, peaks, busy, cross bytes) bit-exact;
     sampled placements excused only where the oracle's CDF margin |u - c_k| < 1e-5;
   * reward / advantage bit-exact (IEEE divide + sqrt, no contraction);
-  * fp32 tensors: |x - r| <= 1e-4 * max(|r|, floor * max|r|) elementwise, floor = 1e-2; for
-    the logits floor = 5e-2: a logit is a 64-term dot product whose fp32 rounding error scales
-    with max|z| (the magnitude of its terms), so logits far below max|z| cannot carry 1e-4
-    of their own size (DESIGN.md §"Parity").
+  * fp32 tensors: |x - r| <= 1e-4 * max(|r|, 1e-2 * max|r|) elementwise (+ for the logits the
+    oracle-computed fp32 accumulation bound 64 * 2^-24 * sum_k |y_k W'_kj| of the head's dot
+    products); the gradient with "tie import": where the oracle's own max-pool top-2 margin or
+    ReLU input is within 1e-5 of the kink it adopts the GPU's recorded decision
+    (gdp_debug_tensors), counted in the assertion message;
+  * bf16 tensor-core mode: every tcgen05 kernel elementwise at rtol 2e-2 on its own inputs
+    (tests/test_gpu_kernels.py); the chained step against the oracle that reproduces the bf16
+    rounding points (oracle.Numerics(bf16=True), tie import at 2^-8) within a relative L2
+    error of 2e-2 for embeddings, logits and gradient.
 """
 import numpy as np
 import pytest
@@ -22,7 +27,39 @@ from tests.helpers import graph as mkgraph, topo as mktopo
 pytestmark = pytest.mark.gpu
 
 RTOL = 1e-4
-LOGIT_FLOOR = 5e-2
+TC_RTOL = 2e-2
+BF16_TIE = 2.0 ** -8   # tie-import margin in bf16 mode: one bf16 unit
+
+
+def close_bound(x, r, bound, rtol=RTOL, floor=1e-2):
+    """close() plus an oracle-computed absolute bound per element."""
+    x = np.asarray(x, dtype=np.float64)
+    r = np.asarray(r, dtype=np.float64)
+    scale = rtol * np.maximum(np.abs(r), floor * max(np.abs(r).max(), 1e-30)) + bound
+    bad = np.abs(x - r) > scale
+    return (not bad.any()), float((np.abs(x - r) / scale).max()), int(bad.sum())
+
+
+def rel_l2(x, r):
+    x = np.asarray(x, dtype=np.float64)
+    r = np.asarray(r, dtype=np.float64)
+    return float(np.linalg.norm(x - r) / max(np.linalg.norm(r), 1e-300))
+
+
+def head_bound(pg, th, d, S, M, sup, emb, na=False):
+    """fp32 accumulation bound of the head's dot products, 64 * 2^-24 * sum_k |y_k W'_kj| + |b_j|,
+    from the oracle's own last-layer output y and folded head weights (Kahn -> caller order)."""
+    keep = {}
+    oracle.place(pg, th, emb, d, S, M, sup, keep, no_attention=na)
+    y = keep["xl1"]["y"].numpy()
+    p = oracle.model.unflatten(torch.as_tensor(np.asarray(th, np.float64)), pg.F, d)
+    W = p["head.W"].numpy()
+    if sup:
+        W = keep["gamma_head"].numpy()[:, None] * W
+    b = np.abs(np.abs(y) @ np.abs(W) + np.abs(p["head.b"].numpy()))
+    out = np.empty_like(b)
+    out[np.asarray(pg.order)] = b
+    return 64 * 2.0 ** -24 * out
 
 
 def close(x, r, rtol=RTOL, floor=1e-2):
@@ -149,6 +186,17 @@ def test_cost_full_size_c4(gdp):
 
 
 # ------------------------------------------------------------------ policy network stages
+def gpu_ties(gdp, G, cfg, ws, na=False):
+    """The GPU's recorded decisions at the kinks (gdp_debug_tensors): max-pool argmax per GNN
+    layer (caller order) and ReLU activity of each XL layer's FFN (and of the no-attention map),
+    Kahn order -- for the oracle's tie import."""
+    v = gdp.debug_tensors(G, cfg, ws)
+    names = ["cond", "xl0", "xl1"]
+    return {"argmax": [v[f"ARG{l}"].cpu().numpy().astype(np.int64) for l in range(3)],
+            "relu": {n: v[f"L{i}.m"].cpu().numpy() > 0 for i, n in enumerate(names)},
+            "relu_v": {n: v[f"L{i}.o"].cpu().numpy() > 0 for i, n in enumerate(names)} if na else {}}
+
+
 def run_step(gdp, g, W_d, S, M, sup, B, th, seed=42, step=0, old=None, eps=0.2, beta=0.01, scale=None, tc=False,
              na=False, active=0):
     X = workloads.features(g)
@@ -173,7 +221,7 @@ def run_step(gdp, g, W_d, S, M, sup, B, th, seed=42, step=0, old=None, eps=0.2, 
                         scale if scale is not None else 1.0 / B, grad, ws)
     torch.cuda.synchronize()
     return dict(X=X, emb=emb.cpu().numpy(), logits=logits.cpu().numpy(), D=Dd.cpu().numpy(),
-                logprob=lp.cpu().numpy(), adv=adv, grad=grad.cpu().numpy())
+                logprob=lp.cpu().numpy(), adv=adv, grad=grad.cpu().numpy(), ties=gpu_ties(gdp, G, cfg, ws, na))
 
 
 CASES = {
@@ -231,7 +279,7 @@ def test_policy_stages(gdp, case):
     assert ok, ("embed", err, nbad)
     # place (a5-a10), stage-wise: oracle consumes the GPU embedding
     z = oracle.place(pg, th, r["emb"], d, S, M, sup, no_attention=na)
-    ok, err, nbad = close(r["logits"], z, floor=LOGIT_FLOOR)
+    ok, err, nbad = close_bound(r["logits"], z, head_bound(pg, th, d, S, M, sup, r["emb"], na))
     assert ok, ("place", err, nbad)
     # sample (a11): shared Philox uniforms, excused only at CDF margins < 1e-5
     U = Osa.uniforms(g.N, B, 42, 0, 0)
@@ -246,11 +294,13 @@ def test_policy_stages(gdp, case):
     want_lp = (lpv[np.arange(g.N)[None, :], r["D"].astype(np.int64)] * isl[None, :]).sum(1)
     ok, err, _ = close(r["logprob"], want_lp)
     assert ok, ("logprob", err)
-    # policy gradient (a14-a15): oracle on the GPU's placements / advantages, chained from theta
+    # policy gradient (a14-a15): oracle on the GPU's placements / advantages, chained from theta,
+    # adopting the GPU's decision at max-pool near-ties / ReLU inputs near zero (tie import)
+    num = oracle.Numerics(ties=r["ties"], tie_tol=1e-5)
     grad, _ = oracle.policy_grad(pg, th, d, S, M, sup, r["D"], r["adv"], loss_scale=1.0 / B, entropy_coef=0.01,
-                                 no_attention=na, active=act or None)
-    ok, err, nbad = close(r["grad"], grad, floor=LOGIT_FLOOR)   # sums of N*B terms
-    assert ok, ("grad", err, nbad)
+                                 no_attention=na, active=act or None, num=num)
+    ok, err, nbad = close(r["grad"], grad)
+    assert ok, ("grad", err, nbad, num.imported)
 
 
 def test_ppo_ratio_branch(gdp):
@@ -262,11 +312,12 @@ def test_ppo_ratio_branch(gdp):
     old = r0["logprob"].astype(np.float64) + np.random.default_rng(1).uniform(-0.5, 0.5, B)
     r = run_step(gdp, g, d, S, M, True, B, th, old=old.astype(np.float32))
     pg = oracle.prepare(g, r["X"])
+    num = oracle.Numerics(ties=r["ties"], tie_tol=1e-5)
     grad, _ = oracle.policy_grad(pg, th, d, S, M, True, r["D"], r["adv"],
                                  old_logprob=old.astype(np.float32).astype(np.float64) +
                                  (_oracle_logpi(pg, th, d, S, M, r["D"]) - r["logprob"].astype(np.float64)),
-                                 loss_scale=1.0 / B, entropy_coef=0.01)
-    ok, err, nbad = close(r["grad"], grad, rtol=5e-4)
+                                 loss_scale=1.0 / B, entropy_coef=0.01, num=num)
+    ok, err, nbad = close(r["grad"], grad)
     assert ok, ("ppo grad", err, nbad)
 
 
@@ -319,30 +370,59 @@ def test_full_size_c4_chain(gdp):
     ok, err, nbad = close(r["emb"], E)
     assert ok, ("embed", err, nbad)
     z = oracle.place(pg, th, r["emb"], W.d, W.seg_len, W.mem_len, True)
-    ok, err, nbad = close(r["logits"], z, floor=LOGIT_FLOOR)
+    ok, err, nbad = close_bound(r["logits"], z, head_bound(pg, th, W.d, W.seg_len, W.mem_len, True, r["emb"]))
     assert ok, ("place", err, nbad)
     U = Osa.uniforms(g.N, B, 42, 0, 0)
     D, _, margin = Osa.sample(r["logits"], U, pg.lead)
     assert not ((D != r["D"]) & (margin >= 1e-5)).any()
     t = workloads.topology(g, W.d)
     assert_cost_equal(g, t, r["D"], cost_gpu(gdp, g, t, r["D"]))
-    grad, _ = oracle.policy_grad(pg, th, W.d, W.seg_len, W.mem_len, True, r["D"], r["adv"], loss_scale=1.0 / B)
-    ok, err, nbad = close(r["grad"], grad, rtol=1e-3)
-    assert ok, ("grad", err, nbad)
+    num = oracle.Numerics(ties=r["ties"], tie_tol=1e-5)
+    grad, _ = oracle.policy_grad(pg, th, W.d, W.seg_len, W.mem_len, True, r["D"], r["adv"], loss_scale=1.0 / B, num=num)
+    ok, err, nbad = close(r["grad"], grad)
+    assert ok, ("grad", err, nbad, num.imported)
+
+
+@pytest.mark.slow
+def test_full_size_c4_chain_tc(gdp):
+    """The headline configuration at full size in tensor-core mode (the bench's launch
+    configuration: tcgen05 maps with the persistent multi-tile loop, tcgen05 attention), B = 8:
+    embeddings, logits and gradient against the bf16-emulating oracle (relative L2 <= 2e-2),
+    placements from the GPU logits and their costs exact (kernel-by-kernel elementwise parity at
+    this size: tests/test_gpu_kernels.py)."""
+    W = workloads.config("c4")
+    g = W.graphs[0]
+    th = workloads.init_theta(workloads.F, W.d, seed=7, mode="default")
+    th[:] += np.random.default_rng(0).uniform(-1e-2, 1e-2, th.size).astype(np.float32)
+    B = 8
+    r = run_step(gdp, g, W.d, W.seg_len, W.mem_len, True, B, th, tc=True)
+    pg = oracle.prepare(g, r["X"])
+    num = oracle.Numerics(bf16=True, ties=r["ties"], tie_tol=BF16_TIE)
+    assert rel_l2(r["emb"], oracle.embed(pg, th, W.d, num)) < TC_RTOL
+    assert rel_l2(r["logits"], oracle.place(pg, th, r["emb"], W.d, W.seg_len, W.mem_len, True, num=num)) < TC_RTOL
+    U = Osa.uniforms(g.N, B, 42, 0, 0)
+    D, _, margin = Osa.sample(r["logits"], U, pg.lead)
+    assert not ((D != r["D"]) & (margin >= 1e-5)).any()
+    t = workloads.topology(g, W.d)
+    assert_cost_equal(g, t, r["D"], cost_gpu(gdp, g, t, r["D"]))
+    numg = oracle.Numerics(bf16=True, ties=r["ties"], tie_tol=BF16_TIE)
+    grad, _ = oracle.policy_grad(pg, th, W.d, W.seg_len, W.mem_len, True, r["D"], r["adv"], loss_scale=1.0 / B,
+                                 num=numg)
+    e = rel_l2(r["grad"], grad)
+    assert e < TC_RTOL, ("grad", e, numg.imported)
 
 
 # ------------------------------------------------------------------ tcgen05 (bf16) mode
-TC_RTOL = 2e-2
-TC_FLOOR = 1.0   # bf16 operands: errors scale with the largest magnitudes, so compare norm-wise
-
-
 @pytest.mark.parametrize("case", ["c2", "mem_inf_big", "seg_ragged", "short_mem"])
 def test_tensor_core_mode(gdp, case):
-    """Dense maps and (when a segment's keys fit one 256-key tile) the attention forward on
-    tcgen05 (bf16 operands, fp32 accumulation): every stage within the bf16 tolerance of
-    BASELINE north_star (rtol 2e-2).  seg_ragged: S = 96, M = 160 (keys 96..256, a ragged last
-    segment) on the tensor-core forward tile (its backward, M > S, on SIMT); short_mem: S = 100,
-    M = 60 on both tensor-core tiles; mem_inf_big: M = inf (forward with several key blocks, backward k_attn_bwd_dq_tc + _dkv_tc)."""
+    """The chained step in tensor-core mode (bf16 operands, fp32 accumulation) against the oracle
+    that reproduces the mode's rounding points (oracle.Numerics(bf16=True)) with tie import at
+    one bf16 unit: embeddings, logits and gradient within a relative L2 error of 2e-2 (BASELINE
+    north_star).  Elementwise, each kernel of this chain is held at 2e-2 on its own inputs in
+    tests/test_gpu_kernels.py; chained, a rounding boundary that the oracle's float64 operand and
+    the GPU's float32 operand fall on different sides of moves one term by a bf16 unit, and
+    such flips compound through the layers.  seg_ragged: S = 96, M = 160 (keys
+    96..256, ragged last segment); short_mem: S = 100, M = 60; mem_inf_big: M = inf."""
     if case == "c2":
         W = workloads.config("c2")
         g, d, S, M = W.graphs[0], W.d, W.seg_len, W.mem_len
@@ -356,29 +436,22 @@ def test_tensor_core_mode(gdp, case):
     B = 16
     r = run_step(gdp, g, d, S, M, True, B, th, tc=True)
     pg = oracle.prepare(g, r["X"])
-    E = oracle.embed(pg, th, d)
-    ok, err, nbad = close(r["emb"], E, rtol=TC_RTOL, floor=TC_FLOOR)
-    assert ok, ("embed", err, nbad)
-    z = oracle.place(pg, th, r["emb"], d, S, M, True)
-    ok, err, nbad = close(r["logits"], z, rtol=TC_RTOL, floor=TC_FLOOR)
-    assert ok, ("place", err, nbad)
-    # The gradient in this mode is the fp32 backward of the bf16-forward network: bf16 rounding
-    # flips ReLU / max-pool kinks near zero, so elementwise 2e-2 is not a property it has; what
-    # it must keep is the direction and size of the update.
-    grad, _ = oracle.policy_grad(pg, th, d, S, M, True, r["D"], r["adv"], loss_scale=1.0 / B, entropy_coef=0.01)
-    gg = r["grad"].astype(np.float64)
-    cos = float(gg @ grad / (np.linalg.norm(gg) * np.linalg.norm(grad)))
-    ratio = float(np.linalg.norm(gg) / np.linalg.norm(grad))
-    assert cos > 0.98 and abs(ratio - 1) < 0.15, ("grad", cos, ratio)   # measured: c2 0.990 / 0.906
+    num = oracle.Numerics(bf16=True, ties=r["ties"], tie_tol=BF16_TIE)
+    e_emb = rel_l2(r["emb"], oracle.embed(pg, th, d, num))
+    e_log = rel_l2(r["logits"], oracle.place(pg, th, r["emb"], d, S, M, True, num=num))
+    numg = oracle.Numerics(bf16=True, ties=r["ties"], tie_tol=BF16_TIE)
+    grad, _ = oracle.policy_grad(pg, th, d, S, M, True, r["D"], r["adv"], loss_scale=1.0 / B, entropy_coef=0.01,
+                                 num=numg)
+    e_g = rel_l2(r["grad"], grad)
+    assert max(e_emb, e_log, e_g) < TC_RTOL, (e_emb, e_log, e_g, numg.imported)
 
 
 @pytest.mark.parametrize("case", ["c1", "seg", "short_mem", "ragged", "mem_inf", "long_mem", "one_chunk_inf",
                                   "ragged_chunk"])
 def test_tensor_core_attention_matches_simt(gdp, case):
-    """The tcgen05 attention tiles (forward k_attn_fwd_tc, backward k_attn_bwd_tc) against the
-    SIMT kernels inside the same tensor-core-mode step (gdp_config.tensor_cores = 2):
-    logits within the bf16 tolerance; the gradient along the same direction as the SIMT one when
-    both runs sampled the same placements, and as the oracle's for the tile run's placements.
+    """The tcgen05 attention tiles (forward k_attn_fwd_tc, backward k_attn_bwd_tc) and the SIMT
+    attention kernels inside a tensor-core-mode step (gdp_config.tensor_cores = 2), each against
+    the bf16-emulating oracle of its own mode (relative L2 <= 2e-2) for logits and gradient.
     mem_inf / long_mem: more than 256 keys per segment (several key blocks in the forward; the
     backward of M > S on k_attn_bwd_dq_tc + k_attn_bwd_dkv_tc).  one_chunk_inf: S = 48 (one
     64-query dK/dV chunk per segment, 48 of its rows used); ragged_chunk: S = 112 (a full chunk and
@@ -393,24 +466,16 @@ def test_tensor_core_attention_matches_simt(gdp, case):
                   "ragged_chunk": (workloads.random_dag(1030, p_edge=0.05, max_back=60, seed=37), 4, 112, 200)}[case]
     th = workloads.init_theta(workloads.F, d, seed=13, mode="random")
     B = 16
-    ref = run_step(gdp, g, d, S, M, True, B, th, tc=2)   # tensor_cores = 2: SIMT attention
-    r = run_step(gdp, g, d, S, M, True, B, th, tc=True)
-    ok, err, nbad = close(r["logits"], ref["logits"], rtol=TC_RTOL, floor=TC_FLOOR)
-    assert ok, ("logits", err, nbad)
-    assert (r["D"] == ref["D"]).mean() > 0.99          # placements sampled from both logits
-    a = r["grad"].astype(np.float64)
-    if (r["D"] == ref["D"]).all():
-        b = ref["grad"].astype(np.float64)
-        cos = float(a @ b / (np.linalg.norm(a) * np.linalg.norm(b)))
-        assert cos > 0.99 and abs(np.linalg.norm(a) / np.linalg.norm(b) - 1) < 0.05, ("grad vs simt", cos)
-    # A placement that differs between the two runs changes its sample's reward and advantage, so
-    # the two gradients are then different quantities; the tile gradient is checked against the
-    # oracle's gradient for the tile run's own placements and advantages.
-    pg = oracle.prepare(g, r["X"])
-    b, _ = oracle.policy_grad(pg, th, d, S, M, True, r["D"], r["adv"], loss_scale=1.0 / B, entropy_coef=0.01)
-    cos = float(a @ b / (np.linalg.norm(a) * np.linalg.norm(b)))
-    ratio = float(np.linalg.norm(a) / np.linalg.norm(b))
-    assert cos > 0.99 and abs(ratio - 1) < 0.05, ("grad vs oracle", cos, ratio)
+    for tc, attn_tc in ((1, True), (2, False)):         # tensor_cores = 2: SIMT attention
+        r = run_step(gdp, g, d, S, M, True, B, th, tc=tc)
+        pg = oracle.prepare(g, r["X"])
+        num = oracle.Numerics(bf16=True, ties=r["ties"], tie_tol=BF16_TIE, attn_tc=attn_tc)
+        e_log = rel_l2(r["logits"], oracle.place(pg, th, r["emb"], d, S, M, True, num=num))
+        numg = oracle.Numerics(bf16=True, ties=r["ties"], tie_tol=BF16_TIE, attn_tc=attn_tc)
+        grad, _ = oracle.policy_grad(pg, th, d, S, M, True, r["D"], r["adv"], loss_scale=1.0 / B,
+                                     entropy_coef=0.01, num=numg)
+        e_g = rel_l2(r["grad"], grad)
+        assert max(e_log, e_g) < TC_RTOL, (tc, e_log, e_g, numg.imported)
 
 
 # ------------------------------------------------------------------ cost-kernel overflow paths

@@ -15,7 +15,9 @@ def err(x, r, floor=1e-2):
     x = np.asarray(x, np.float64); r = np.asarray(r, np.float64)
     scale = np.maximum(np.abs(r), floor * max(np.abs(r).max(), 1e-30))
     e = np.abs(x - r) / scale
-    return float(e.max()), float(np.percentile(e, 99.9))
+    i = int(np.argmax(e))
+    return (round(float(e.max()), 6), round(float(np.linalg.norm(x - r) / np.linalg.norm(r)), 7),
+            "at", np.unravel_index(i, r.shape), float(r.flat[i]), float(x.flat[i]), float(np.abs(r).max()))
 
 def step(g, d, S, M, sup, B, th, tc, na=False, act=0):
     X = workloads.features(g)
@@ -32,9 +34,8 @@ def step(g, d, S, M, sup, B, th, tc, na=False, act=0):
     grad = torch.zeros(n, device="cuda")
     gdp.gdp_policy_grad(G, cfg, theta, logits, Dd, B, torch.from_numpy(adv).cuda(), lp, None, 0.2, 0.01, 1.0 / B, grad, ws)
     torch.cuda.synchronize()
-    ties = {"argmax": [gdp.debug_tensor(G, cfg, ws, 0, l).cpu().numpy().astype(np.int64) for l in range(3)],
-            "relu": {n_: (gdp.debug_tensor(G, cfg, ws, 1, i).cpu().numpy() > 0) for i, n_ in enumerate(["cond", "xl0", "xl1"])},
-            "relu_v": {n_: (gdp.debug_tensor(G, cfg, ws, 2, i).cpu().numpy() > 0) for i, n_ in enumerate(["cond", "xl0", "xl1"])} if na else {}}
+    from tests.test_gpu_parity import gpu_ties
+    ties = gpu_ties(gdp, G, cfg, ws, na)
     return dict(X=X, emb=emb.cpu().numpy(), logits=logits.cpu().numpy(), D=Dd.cpu().numpy(), adv=adv,
                 grad=grad.cpu().numpy(), ties=ties)
 
