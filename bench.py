@@ -256,12 +256,14 @@ def run_zero_shot(args, W, gdp, dev):
     X, topo = workloads.features(g), workloads.topology(g, W.d)
     theta = torch.from_numpy(workloads.init_theta(workloads.F, W.d, seed=7)).to(dev)
     for _ in range(args.warmup):
-        r = gdp.zero_shot(g, X, topo, theta, W.d, W.seg_len, W.mem_len, W.superposition, not args.fp32, dev)
+        r = gdp.zero_shot(g, X, topo, theta, W.d, W.seg_len, W.mem_len, W.superposition, not args.fp32, dev,
+                          no_attention=args.no_attention)
     ts = []
     for _ in range(args.steps):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        r = gdp.zero_shot(g, X, topo, theta, W.d, W.seg_len, W.mem_len, W.superposition, not args.fp32, dev)
+        r = gdp.zero_shot(g, X, topo, theta, W.d, W.seg_len, W.mem_len, W.superposition, not args.fp32, dev,
+                          no_attention=args.no_attention)
         ts.append(time.perf_counter() - t0)
     ms = 1000.0 * statistics.median(ts)
     print(json.dumps({"metric": "GDP zero-shot placement latency (embed, place, greedy, cost)", "value": ms,

@@ -46,7 +46,7 @@ typedef enum {
   GDP_ERR_SHAPE = 4,      /* sizes disagree (e.g. F or d differs from the graph / config) */
   GDP_ERR_CUDA = 5,       /* a CUDA call failed (message in gdp_last_error) */
   GDP_ERR_OVERFLOW = 6,   /* sum of durations + transfers could reach 2^31 ticks (device time is int32) */
-  GDP_ERR_NONFINITE = 7,  /* reserved: non-finite gradient */
+  GDP_ERR_NONFINITE = 7,  /* non-finite gradient (gdp_grad_check; gdp_clip_adam skips such an update) */
   GDP_ERR_WORKSPACE = 8   /* ws_bytes smaller than gdp_workspace_size */
 } gdp_status;
 
@@ -283,6 +283,13 @@ int32_t gdp_cost_kernel(gdp_graph g, gdp_topo t);
 int32_t gdp_debug_tensors(gdp_graph g, const gdp_config *c, int32_t max_names, const char **names,
                           int64_t *offsets, int64_t *rows, int64_t *cols, int32_t *is_int);
 
+/* Finite check of a gradient ("a NaN gradient must raise a training error naming the
+ * parameter"): SYNCHRONOUS on `stream`.  GDP_OK if every entry of grad[0, n_params) is
+ * finite, else GDP_ERR_NONFINITE with gdp_last_error() naming the first offending entry's
+ * parameter tensor (gdp_param_id and its name) and element.  grad dev fp32 n_params (layout of
+ * (c, F)); scratch dev, >= 8 bytes.  Errors: GDP_ERR_ARG, GDP_ERR_NONFINITE, GDP_ERR_CUDA. */
+gdp_status gdp_grad_check(const float *grad, const gdp_config *c, int32_t F, double *scratch, void *stream);
+
 /* Diagnostic / test entry: gdp_cost on an explicitly chosen kernel (5, 3 or 1; 0 = the
  * automatic choice gdp_cost makes).  GDP_ERR_ARG if that kernel does not apply to (g, t)
  * (e.g. 5 with a zero-duration op).  Used by the tests to hold every kernel to the oracle on
@@ -345,6 +352,9 @@ gdp_status gdp_greedy(gdp_graph g, const gdp_config *c, const float *logits, uin
  * and stored as fp32.  All arrays are device pointers with 16-byte alignment:
  *   grad fp32 [n] (in);  theta, m, v fp32 [n] (in/out);  scratch fp64 [GDP_ADAM_SCRATCH];
  *   norm_out fp64 [1] (out, nullable: the pre-clip norm).  t >= 1 is the step number.
+ * A non-finite gradient (NaN or Inf anywhere: ||grad|| is not finite) leaves theta, m and v
+ * unchanged and norm_out reports the non-finite norm; gdp_grad_check then names the offending
+ * parameter.
  * Errors: GDP_ERR_ARG (NULL, n < 1, t < 1, misaligned, beta outside [0, 1)), GDP_ERR_CUDA. */
 gdp_status gdp_clip_adam(const float *grad, int64_t n, double max_norm, double lr, double beta1, double beta2,
                          double eps, int64_t t, float *theta, float *m, float *v, double *scratch, double *norm_out,

@@ -26,7 +26,7 @@ REPORT_BYTES = 24
 
 EXPORTS = ["gdp_default_config", "gdp_last_error", "gdp_launch_count", "gdp_build_info", "gdp_cost_kernel", "gdp_logprob", "gdp_clip_adam", "gdp_sample_at", "gdp_greedy", "gdp_graph_validate", "gdp_graph_create", "gdp_graph_destroy",
            "gdp_topo_create", "gdp_topo_destroy", "gdp_param_layout", "gdp_workspace_size", "gdp_embed",
-           "gdp_place", "gdp_sample", "gdp_cost", "gdp_cost_with_kernel", "gdp_debug_tensors", "gdp_advantage", "gdp_policy_grad", "gdp_profile_enable",
+           "gdp_place", "gdp_sample", "gdp_cost", "gdp_cost_with_kernel", "gdp_debug_tensors", "gdp_grad_check", "gdp_advantage", "gdp_policy_grad", "gdp_profile_enable",
            "gdp_profile_mark", "gdp_profile_read"]
 
 
@@ -69,6 +69,7 @@ def lib():
             "gdp_cost": [P, P, P, I32, P, P, P, P, P, SZ, P],
             "gdp_cost_with_kernel": [P, P, P, I32, P, P, P, P, P, SZ, I32, P],
             "gdp_debug_tensors": [P, P, I32, ctypes.POINTER(ctypes.c_char_p), P, P, P, P],
+            "gdp_grad_check": [P, P, I32, P, P],
             "gdp_advantage": [P, I32, P, P, P, P],
             "gdp_policy_grad": [P, P, P, P, P, I32, P, P, P, F32, F32, F32, P, P, SZ, P],
             "gdp_logprob": [P, P, P, P, I32, P, P, SZ, P],
@@ -303,6 +304,12 @@ def debug_tensors(g: Graph, cfg: Config, ws) -> dict:
         t = ws[int(off[i]):int(off[i]) + nb].view(torch.int32 if isint[i] else torch.float32)
         out[names[i].decode()] = t.view(int(rows[i]), int(cols[i]))
     return out
+
+
+def gdp_grad_check(grad, cfg: Config, F: int, scratch, stream=None):
+    """Synchronous finite check; raises GdpError(GDP_ERR_NONFINITE) naming the parameter."""
+    _check(lib().gdp_grad_check(_t_ptr(grad), ctypes.byref(cfg), F, _t_ptr(scratch), _stream(stream)),
+           "gdp_grad_check")
 
 
 def gdp_advantage(reward, B: int, run_sum, run_count, adv, stream=None):

@@ -62,6 +62,22 @@ static gdp_status fail(gdp_status s, const std::string &msg) {
   return s;
 }
 
+// parameter tensor names in GDP_P_* order (error messages)
+static const char *const kParamNames[GDP_P_COUNT] = {
+    "gnn.in.W", "gnn.in.b", "gnn.0.W", "gnn.0.b", "gnn.0.Wf", "gnn.0.bf", "gnn.1.W", "gnn.1.b", "gnn.1.Wf",
+    "gnn.1.bf", "gnn.2.W", "gnn.2.b", "gnn.2.Wf", "gnn.2.bf",
+    "cond.ln1.g", "cond.ln1.b", "cond.Wq", "cond.bq", "cond.Wk", "cond.bk", "cond.Wv", "cond.bv", "cond.Wo",
+    "cond.bo", "cond.ln2.g", "cond.ln2.b", "cond.W1", "cond.b1", "cond.W2", "cond.b2",
+    "xl0.ln1.g", "xl0.ln1.b", "xl0.Wq", "xl0.bq", "xl0.Wk", "xl0.bk", "xl0.Wv", "xl0.bv", "xl0.Wo", "xl0.bo",
+    "xl0.ln2.g", "xl0.ln2.b", "xl0.W1", "xl0.b1", "xl0.W2", "xl0.b2",
+    "xl1.ln1.g", "xl1.ln1.b", "xl1.Wq", "xl1.bq", "xl1.Wk", "xl1.bk", "xl1.Wv", "xl1.bv", "xl1.Wo", "xl1.bo",
+    "xl1.ln2.g", "xl1.ln2.b", "xl1.W1", "xl1.b1", "xl1.W2", "xl1.b2",
+    "gate0.q.P", "gate0.q.q", "gate0.k.P", "gate0.k.q", "gate0.v.P", "gate0.v.q", "gate0.o.P", "gate0.o.q",
+    "gate0.f1.P", "gate0.f1.q", "gate0.f2.P", "gate0.f2.q",
+    "gate1.q.P", "gate1.q.q", "gate1.k.P", "gate1.k.q", "gate1.v.P", "gate1.v.q", "gate1.o.P", "gate1.o.q",
+    "gate1.f1.P", "gate1.f1.q", "gate1.f2.P", "gate1.f2.q",
+    "gate.head.P", "gate.head.q", "head.W", "head.b"};
+
 // parameter tensor shapes in GDP_P_* order
 static void param_shapes(int F, int d, long long *sz) {
   const long long H = kH, FF = kFFN;
@@ -786,6 +802,25 @@ gdp_status gdp_clip_adam(const float *grad, int64_t n, double max_norm, double l
                    static_cast<cudaStream_t>(stream));
   GDP_LAUNCH_CHECK("gdp_clip_adam");
   return GDP_OK;
+}
+
+gdp_status gdp_grad_check(const float *grad, const gdp_config *c, int32_t F, double *scratch, void *stream) {
+  if (!grad || !scratch) return fail(GDP_ERR_ARG, "NULL argument");
+  gdp_status st = check_config(c);
+  if (st != GDP_OK) return st;
+  if (F < 1) return fail(GDP_ERR_ARG, "F must be >= 1");
+  long long off[GDP_P_COUNT + 1];
+  param_offsets(F, c->num_devices, off);
+  const long long n = off[GDP_P_COUNT];
+  const long long i = first_nonfinite(grad, n, reinterpret_cast<unsigned long long *>(scratch),
+                                      static_cast<cudaStream_t>(stream));
+  if (i < 0) return cuda_status(cudaGetLastError(), "gdp_grad_check");
+  if (i >= n) return GDP_OK;
+  int t = 0;
+  while (t + 1 < GDP_P_COUNT && off[t + 1] <= i) t++;
+  return fail(GDP_ERR_NONFINITE, "non-finite gradient at theta[" + std::to_string(i) + "]: parameter tensor " +
+                                     std::to_string(t) + " (gdp_param_id, " + kParamNames[t] + ") element " +
+                                     std::to_string(i - off[t]));
 }
 
 gdp_status gdp_cost(gdp_graph g, gdp_topo t, const uint8_t *placements, int32_t B, gdp_sim_report *rep,

@@ -237,6 +237,9 @@ void launch_logprob(const float *logp, const int *leader, const uint8_t *D, int 
 void launch_greedy(const float *logits, int ld, const int *leader, int N, int d, uint8_t *D, cudaStream_t s);
 // devices a call samples / scores over: gdp_config.active_devices, or num_devices when 0
 int active_devices(const gdp_config *c);
+// synchronous: index of the first non-finite entry of g[0, n) (n if none, -1 on a CUDA error);
+// scratch = one device uint64
+long long first_nonfinite(const float *g, long long n, unsigned long long *scratch, cudaStream_t s);
 void launch_clip_adam(const float *g, long long n, double max_norm, double lr, double b1, double b2, double eps,
                       double c1, double c2, float *theta, float *m, float *v, double *scratch, double *norm_out,
                       cudaStream_t s);

@@ -94,11 +94,14 @@ __global__ void __launch_bounds__(AT) k_adam(const float *__restrict__ g, long l
     for (int i = 0; i < nparts; i++) s += part[i];   // same order in every CTA
     const double norm = sqrt(s);
     const double f = max_norm / (norm + 1e-6);
-    s_scale = f < 1.0 ? f : 1.0;
+    // a non-finite gradient (NaN, or Inf: Inf * 0 = NaN) leaves theta, m and v untouched; the
+    // norm reports it (gdp_grad_check names the parameter)
+    s_scale = isfinite(norm) ? (f < 1.0 ? f : 1.0) : -1.0;
     if (blockIdx.x == 0 && norm_out) *norm_out = norm;
   }
   __syncthreads();
   const double scale = s_scale;
+  if (scale < 0.0) return;
   const long long n4 = n / 4;
   float4 *t4 = reinterpret_cast<float4 *>(theta), *m4 = reinterpret_cast<float4 *>(m),
          *v4 = reinterpret_cast<float4 *>(v);
@@ -116,6 +119,12 @@ __global__ void __launch_bounds__(AT) k_adam(const float *__restrict__ g, long l
   }
   for (long long i = 4 * n4 + (long long)blockIdx.x * AT + threadIdx.x; i < n; i += (long long)gridDim.x * AT)
     adam1(theta[i], m[i], v[i], g[i], scale, lr, b1, b2, eps, c1, c2);
+}
+
+// index of the first non-finite gradient entry (atomicMin; n if none)
+__global__ void k_first_nonfinite(const float *__restrict__ g, long long n, unsigned long long *first) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    if (!isfinite(g[i])) atomicMin(first, (unsigned long long)i);
 }
 
 int sm_count() {
@@ -142,6 +151,16 @@ void launch_logprob(const float *logp, const int *leader, const uint8_t *D, int 
                     cudaStream_t s) {
   note_launch("k_logprob", s);
   k_logprob<<<B, LT, 0, s>>>(logp, leader, D, N, d, logprob);
+}
+
+long long first_nonfinite(const float *g, long long n, unsigned long long *scratch, cudaStream_t s) {
+  unsigned long long h = (unsigned long long)n;
+  if (cudaMemcpyAsync(scratch, &h, sizeof(h), cudaMemcpyHostToDevice, s) != cudaSuccess) return -1;
+  note_launch("k_first_nonfinite", s);
+  k_first_nonfinite<<<2 * sm_count(), 256, 0, s>>>(g, n, scratch);
+  if (cudaMemcpyAsync(&h, scratch, sizeof(h), cudaMemcpyDeviceToHost, s) != cudaSuccess) return -1;
+  if (cudaStreamSynchronize(s) != cudaSuccess) return -1;
+  return (long long)h;
 }
 
 void launch_clip_adam(const float *g, long long n, double max_norm, double lr, double b1, double b2, double eps,

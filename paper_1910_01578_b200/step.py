@@ -250,6 +250,12 @@ class PPOTrainer:
                 gdp_clip_adam(self.grad, theta, self.m, self.v, self.t, self.lr, self.scratch, self.norms[k:k + 1],
                               max_norm=self.max_norm)
                 k += 1
+        # a non-finite gradient skipped its Adam step (gdp_clip_adam); it is a training error that
+        # names the parameter -- one host read per update, after the epochs
+        if not bool(self.torch.isfinite(self.norms[:k]).all()):
+            from . import gdp_grad_check
+            gdp_grad_check(self.grad, st.cfg, st.F, self.scratch)
+            raise RuntimeError("non-finite gradient norm in the PPO update")
 
     def update(self, theta):
         P, A, L = self.rollouts(theta)
@@ -259,13 +265,14 @@ class PPOTrainer:
 
 
 def zero_shot(gsrc, feat, topo_src, theta, d: int, seg_len: int = 128, mem_len: int = 128,
-              superposition: bool = True, tensor_cores: bool = False, device=None) -> Dict[str, object]:
+              superposition: bool = True, tensor_cores: bool = False, device=None,
+              no_attention: bool = False) -> Dict[str, object]:
     """Zero-shot placement: embed -> place -> greedy decode ->
     cost of that one placement, no update.  Returns the placement, its log-probability and the
     cost-model report (makespan, validity, reward, peaks)."""
     import torch
     device = device if device is not None else torch.device("cuda", torch.cuda.current_device())
-    cfg = default_config(d, seg_len, mem_len, superposition, tensor_cores)
+    cfg = default_config(d, seg_len, mem_len, superposition, tensor_cores, no_attention)
     st = _GraphState(gsrc, feat, topo_src, cfg, 1, 1, device)
     gdp_embed(st.g, st.cfg, theta, st.node_emb, st.ws)
     gdp_place(st.g, st.cfg, theta, st.node_emb, st.logits, st.ws)
@@ -283,7 +290,7 @@ def finetune(gsrc, feat, topo_src, theta, d: int, updates: int = 50, **kw) -> Di
     in place), then the zero-shot placement of the result."""
     if updates > 50:
         raise ValueError("fine-tuning runs fewer than 50 updates (P:254)")
-    zs = {k: kw[k] for k in ("seg_len", "mem_len", "superposition", "tensor_cores") if k in kw}
+    zs = {k: kw[k] for k in ("seg_len", "mem_len", "superposition", "tensor_cores", "no_attention") if k in kw}
     tr = PPOTrainer(gsrc, feat, topo_src, d, **kw)
     for _ in range(updates):
         tr.update(theta)

@@ -152,3 +152,44 @@ def test_finetune_driver_runs(gdp):
     assert not torch.equal(before, theta) and torch.isfinite(theta).all()
     with pytest.raises(ValueError):
         gdp.finetune(g, X, workloads.topology(g, W.d), theta, W.d, updates=51)
+
+
+@pytest.mark.parametrize("bad", [float("nan"), float("inf")])
+def test_nonfinite_gradient_skips_update_and_names_parameter(gdp, bad):
+    """SPEC.md:105 / 613: a NaN (or Inf) gradient must not reach theta, m, v (gdp_clip_adam skips
+    the step and reports the non-finite norm) and must raise a training error naming the
+    parameter (gdp_grad_check -> GDP_ERR_NONFINITE)."""
+    cfg = gdp.default_config(4)
+    offs, n = gdp.param_layout(cfg, workloads.F)
+    rng = np.random.default_rng(5)
+    g = (rng.normal(size=n) * 1e-3).astype(np.float32)
+    XL0_W1 = 14 + 16 + 12            # gdp_param_id GDP_P_XL0_W1 (include/gdp.h order)
+    i = int(offs[XL0_W1]) + 77                                      # xl0.W1, element 77
+    g[i] = bad
+    th = rng.normal(size=n).astype(np.float32)
+    cu = {k: torch.from_numpy(a.copy()).cuda() for k, a in dict(g=g, th=th, m=np.zeros(n, np.float32),
+                                                                  v=np.zeros(n, np.float32)).items()}
+    scratch = torch.zeros(gdp.ADAM_SCRATCH, dtype=torch.float64, device="cuda")
+    norm = torch.zeros(1, dtype=torch.float64, device="cuda")
+    gdp.gdp_clip_adam(cu["g"], cu["th"], cu["m"], cu["v"], 1, 3e-4, scratch, norm, max_norm=1.0)
+    torch.cuda.synchronize()
+    assert not np.isfinite(norm.item())
+    assert np.array_equal(cu["th"].cpu().numpy(), th) and not cu["m"].any() and not cu["v"].any()
+    with pytest.raises(gdp.GdpError) as e:
+        gdp.gdp_grad_check(cu["g"], cfg, workloads.F, scratch)
+    assert e.value.status == 7 and "xl0.W1" in str(e.value) and "element 77" in str(e.value)
+    cu["g"][i] = 0.0
+    gdp.gdp_grad_check(cu["g"], cfg, workloads.F, scratch)        # finite: no error
+
+
+def test_finetune_no_attention_evaluates_the_ablation(gdp):
+    """finetune(no_attention=True) must evaluate its zero-shot placement with the
+    same ablated network it trained (the greedy placement equals zero_shot(no_attention=True))."""
+    W = workloads.config("c1")
+    g = W.graphs[0]
+    X = workloads.features(g)
+    t = workloads.topology(g, W.d)
+    theta = torch.from_numpy(workloads.init_theta(X.shape[1], W.d, seed=4, mode="random")).cuda()
+    out = gdp.finetune(g, X, t, theta, W.d, updates=1, seg_len=W.seg_len, mem_len=W.mem_len, no_attention=True)
+    ref = gdp.zero_shot(g, X, t, theta, W.d, W.seg_len, W.mem_len, no_attention=True)
+    assert np.array_equal(out["placement"], ref["placement"])
