@@ -283,6 +283,32 @@ int32_t gdp_cost_kernel(gdp_graph g, gdp_topo t);
 int32_t gdp_debug_tensors(gdp_graph g, const gdp_config *c, int32_t max_names, const char **names,
                           int64_t *offsets, int64_t *rows, int64_t *cols, int32_t *is_int);
 
+/* Gradient buckets, in the order the backward of gdp_policy_grad completes them (SURVEY §8(e):
+ * the all-reduce of a bucket can start while the rest of the backward runs):
+ *   0: placement layers, gates and head [off(GDP_P_XL0_LN1_G), n_params)
+ *   1: the conditioner layer            [off(GDP_P_COND_LN1_G), off(GDP_P_XL0_LN1_G))
+ *   2: the GNN                          [0, off(GDP_P_COND_LN1_G))
+ * first/last host int64[GDP_GRAD_BUCKETS] (out): element ranges of the flat theta.
+ * Errors: GDP_ERR_ARG. */
+#define GDP_GRAD_BUCKETS 3
+gdp_status gdp_grad_buckets(const gdp_config *c, int32_t F, int64_t *first, int64_t *last);
+
+/* gdp_policy_grad that also records bucket_events[i] (GDP_GRAD_BUCKETS cudaEvent_t passed as
+ * void*, created by the caller) on `stream` as soon as bucket i's gradient entries are final, so
+ * that a caller can launch the bucket's NCCL all-reduce on a side stream waiting on the event
+ * while the backward continues (Eq. 1 average over ranks).  Otherwise identical. */
+gdp_status gdp_policy_grad_bucketed(gdp_graph g, const gdp_config *c, const float *theta, const float *logits,
+                                    const uint8_t *placements, int32_t B, const double *adv, const float *logprob,
+                                    const float *old_logprob, float clip_eps, float entropy_coef, float loss_scale,
+                                    float *grad, void *ws, size_t ws_bytes, void *const *bucket_events,
+                                    void *stream);
+
+/* Sum of per-graph gradients (Eq. 1 sum over graphs): out = grads[0] + grads[1] + ...
+ * in that fixed order (deterministic).  grads host array of n_grads device pointers, each fp32
+ * [len]; out dev fp32 [len] (may alias none of them).  Asynchronous on stream.
+ * Errors: GDP_ERR_ARG, GDP_ERR_CUDA. */
+gdp_status gdp_grad_sum(const float *const *grads, int32_t n_grads, int64_t len, float *out, void *stream);
+
 /* Finite check of a gradient ("a NaN gradient must raise a training error naming the
  * parameter"): SYNCHRONOUS on `stream`.  GDP_OK if every entry of grad[0, n_params) is
  * finite, else GDP_ERR_NONFINITE with gdp_last_error() naming the first offending entry's

@@ -26,7 +26,7 @@ REPORT_BYTES = 24
 
 EXPORTS = ["gdp_default_config", "gdp_last_error", "gdp_launch_count", "gdp_build_info", "gdp_cost_kernel", "gdp_logprob", "gdp_clip_adam", "gdp_sample_at", "gdp_greedy", "gdp_graph_validate", "gdp_graph_create", "gdp_graph_destroy",
            "gdp_topo_create", "gdp_topo_destroy", "gdp_param_layout", "gdp_workspace_size", "gdp_embed",
-           "gdp_place", "gdp_sample", "gdp_cost", "gdp_cost_with_kernel", "gdp_debug_tensors", "gdp_grad_check", "gdp_advantage", "gdp_policy_grad", "gdp_profile_enable",
+           "gdp_place", "gdp_sample", "gdp_cost", "gdp_cost_with_kernel", "gdp_debug_tensors", "gdp_grad_check", "gdp_grad_buckets", "gdp_policy_grad_bucketed", "gdp_grad_sum", "gdp_advantage", "gdp_policy_grad", "gdp_profile_enable",
            "gdp_profile_mark", "gdp_profile_read"]
 
 
@@ -70,6 +70,9 @@ def lib():
             "gdp_cost_with_kernel": [P, P, P, I32, P, P, P, P, P, SZ, I32, P],
             "gdp_debug_tensors": [P, P, I32, ctypes.POINTER(ctypes.c_char_p), P, P, P, P],
             "gdp_grad_check": [P, P, I32, P, P],
+            "gdp_grad_buckets": [P, I32, P, P],
+            "gdp_policy_grad_bucketed": [P, P, P, P, P, I32, P, P, P, F32, F32, F32, P, P, SZ, P, P],
+            "gdp_grad_sum": [P, I32, I64, P, P],
             "gdp_advantage": [P, I32, P, P, P, P],
             "gdp_policy_grad": [P, P, P, P, P, I32, P, P, P, F32, F32, F32, P, P, SZ, P],
             "gdp_logprob": [P, P, P, P, I32, P, P, SZ, P],
@@ -304,6 +307,33 @@ def debug_tensors(g: Graph, cfg: Config, ws) -> dict:
         t = ws[int(off[i]):int(off[i]) + nb].view(torch.int32 if isint[i] else torch.float32)
         out[names[i].decode()] = t.view(int(rows[i]), int(cols[i]))
     return out
+
+
+GRAD_BUCKETS = 3
+
+
+def grad_buckets(cfg: Config, F: int):
+    """[(first, last)] element ranges of the gradient buckets in backward completion order."""
+    a = np.zeros(GRAD_BUCKETS, np.int64)
+    b = np.zeros(GRAD_BUCKETS, np.int64)
+    _check(lib().gdp_grad_buckets(ctypes.byref(cfg), F, _np_ptr(a), _np_ptr(b)), "gdp_grad_buckets")
+    return [(int(x), int(y)) for x, y in zip(a, b)]
+
+
+def gdp_policy_grad_bucketed(g: Graph, cfg: Config, theta, logits, placements, B: int, adv, logprob, old_logprob,
+                             clip_eps: float, entropy_coef: float, loss_scale: float, grad, ws, events, stream=None):
+    """gdp_policy_grad recording torch.cuda.Event `events[i]` when bucket i is final."""
+    arr = (ctypes.c_void_p * GRAD_BUCKETS)(*[e.cuda_event for e in events])
+    _check(lib().gdp_policy_grad_bucketed(g.h, ctypes.byref(cfg), _t_ptr(theta), _t_ptr(logits), _t_ptr(placements),
+                                          B, _t_ptr(adv), _t_ptr(logprob), _t_ptr(old_logprob), clip_eps,
+                                          entropy_coef, loss_scale, _t_ptr(grad), _t_ptr(ws), ws.numel(), arr,
+                                          _stream(stream)), "gdp_policy_grad_bucketed")
+
+
+def gdp_grad_sum(grads, out, stream=None):
+    """out = grads[0] + grads[1] + ... (fixed order) on the device."""
+    arr = (ctypes.c_void_p * len(grads))(*[t.data_ptr() for t in grads])
+    _check(lib().gdp_grad_sum(arr, len(grads), out.numel(), _t_ptr(out), _stream(stream)), "gdp_grad_sum")
 
 
 def gdp_grad_check(grad, cfg: Config, F: int, scratch, stream=None):

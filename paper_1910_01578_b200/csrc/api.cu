@@ -11,12 +11,21 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "common.cuh"
 #include "cost2.cuh"
 
 namespace gdp {
 
 static thread_local std::string g_err = "ok";
+
+// an NVTX range around every hot-path ABI call (visible in nsys / ncu --nvtx; header-only NVTX3,
+// a no-op without an attached tool)
+struct NvtxRange {
+  explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 static std::atomic<unsigned long long> g_launches{0};
 
 // per-launch timing (gdp_profile_*): an event before every launch; a launch's time is the gap
@@ -250,7 +259,8 @@ gdp_status run_place(const gdp_graph_s *g, const gdp_config *c, const float *the
 gdp_status run_policy_grad(const gdp_graph_s *g, const gdp_config *c, const float *theta, const float *logits,
                            const uint8_t *D, int B, const double *adv, const float *logprob,
                            const float *old_logprob, float eps, float beta, float scale, float *grad, const WS &w,
-                           cudaStream_t s);
+                           cudaStream_t s, cudaEvent_t const *bucket_done);
+void launch_grad_sum(const float *const *grads, int n, long long len, float *out, cudaStream_t s);
 }  // namespace gdp
 
 extern "C" {
@@ -696,6 +706,7 @@ int32_t gdp_debug_tensors(gdp_graph g, const gdp_config *c, int32_t max_names, c
 
 gdp_status gdp_embed(gdp_graph g, const gdp_config *c, const float *theta, float *node_emb, void *ws,
                      size_t ws_bytes, void *stream) {
+  NvtxRange nvtx_("gdp_embed");
   if (!g || !theta || !node_emb) return fail(GDP_ERR_ARG, "NULL argument");
   gdp_status st = check_config(c);
   if (st != GDP_OK) return st;
@@ -709,6 +720,7 @@ gdp_status gdp_embed(gdp_graph g, const gdp_config *c, const float *theta, float
 
 gdp_status gdp_place(gdp_graph g, const gdp_config *c, const float *theta, const float *node_emb, float *logits,
                      void *ws, size_t ws_bytes, void *stream) {
+  NvtxRange nvtx_("gdp_place");
   if (!g || !theta || !node_emb || !logits) return fail(GDP_ERR_ARG, "NULL argument");
   gdp_status st = check_config(c);
   if (st != GDP_OK) return st;
@@ -741,18 +753,21 @@ static gdp_status sample_impl(gdp_graph g, const gdp_config *c, const float *log
 gdp_status gdp_sample(gdp_graph g, const gdp_config *c, const float *logits, int32_t B, uint64_t seed,
                       uint64_t sample_offset, uint64_t step, uint8_t *placements, float *logprob, void *ws,
                       size_t ws_bytes, void *stream) {
+  NvtxRange nvtx_("gdp_sample");
   return sample_impl(g, c, logits, B, seed, sample_offset, step, nullptr, placements, logprob, ws, ws_bytes, stream);
 }
 
 gdp_status gdp_sample_at(gdp_graph g, const gdp_config *c, const float *logits, int32_t B, uint64_t seed,
                          uint64_t sample_offset, const uint64_t *step_dev, uint8_t *placements, float *logprob,
                          void *ws, size_t ws_bytes, void *stream) {
+  NvtxRange nvtx_("gdp_sample_at");
   if (!step_dev) return fail(GDP_ERR_ARG, "NULL step pointer");
   return sample_impl(g, c, logits, B, seed, sample_offset, 0, step_dev, placements, logprob, ws, ws_bytes, stream);
 }
 
 gdp_status gdp_logprob(gdp_graph g, const gdp_config *c, const float *logits, const uint8_t *placements, int32_t B,
                        float *logprob, void *ws, size_t ws_bytes, void *stream) {
+  NvtxRange nvtx_("gdp_logprob");
   if (!g || !logits || !placements || !logprob) return fail(GDP_ERR_ARG, "NULL argument");
   gdp_status st = check_config(c);
   if (st != GDP_OK) return st;
@@ -769,6 +784,7 @@ gdp_status gdp_logprob(gdp_graph g, const gdp_config *c, const float *logits, co
 
 gdp_status gdp_greedy(gdp_graph g, const gdp_config *c, const float *logits, uint8_t *placement, float *logprob,
                       void *ws, size_t ws_bytes, void *stream) {
+  NvtxRange nvtx_("gdp_greedy");
   if (!g || !logits || !placement) return fail(GDP_ERR_ARG, "NULL argument");
   gdp_status st = check_config(c);
   if (st != GDP_OK) return st;
@@ -788,6 +804,7 @@ gdp_status gdp_greedy(gdp_graph g, const gdp_config *c, const float *logits, uin
 gdp_status gdp_clip_adam(const float *grad, int64_t n, double max_norm, double lr, double beta1, double beta2,
                          double eps, int64_t t, float *theta, float *m, float *v, double *scratch, double *norm_out,
                          void *stream) {
+  NvtxRange nvtx_("gdp_clip_adam");
   if (!grad || !theta || !m || !v || !scratch) return fail(GDP_ERR_ARG, "NULL argument");
   if (n < 1 || t < 1) return fail(GDP_ERR_ARG, "n and t must be >= 1");
   if (!(beta1 >= 0.0 && beta1 < 1.0 && beta2 >= 0.0 && beta2 < 1.0) || !(max_norm > 0.0) || !(eps >= 0.0))
@@ -831,6 +848,7 @@ gdp_status gdp_cost(gdp_graph g, gdp_topo t, const uint8_t *placements, int32_t 
 gdp_status gdp_cost_with_kernel(gdp_graph g, gdp_topo t, const uint8_t *placements, int32_t B, gdp_sim_report *rep,
                                 int64_t *peak_mem, int64_t *busy, double *reward, void *ws, size_t ws_bytes,
                                 int32_t kernel, void *stream) {
+  NvtxRange nvtx_("gdp_cost_with_kernel");
   if (!g || !t || !placements || !rep || !reward) return fail(GDP_ERR_ARG, "NULL argument");
   if (B < 1) return fail(GDP_ERR_ARG, "B must be >= 1");
   // int32 device time: the schedule never exceeds sum(durations) + sum(transfers)
@@ -870,6 +888,7 @@ gdp_status gdp_policy_grad(gdp_graph g, const gdp_config *c, const float *theta,
                            const uint8_t *placements, int32_t B, const double *adv, const float *logprob,
                            const float *old_logprob, float clip_eps, float entropy_coef, float loss_scale,
                            float *grad, void *ws, size_t ws_bytes, void *stream) {
+  NvtxRange nvtx_("gdp_policy_grad");
   if (!g || !theta || !logits || !placements || !adv || !grad) return fail(GDP_ERR_ARG, "NULL argument");
   if (old_logprob && !logprob) return fail(GDP_ERR_ARG, "logprob is required with old_logprob");
   gdp_status st = check_config(c);
@@ -881,7 +900,53 @@ gdp_status gdp_policy_grad(gdp_graph g, const gdp_config *c, const float *theta,
   set_tensor_cores(c->tensor_cores);
   set_no_attention(c->no_attention != 0);
   return run_policy_grad(g, c, theta, logits, placements, B, adv, logprob, old_logprob, clip_eps, entropy_coef,
-                         loss_scale, grad, w, static_cast<cudaStream_t>(stream));
+                         loss_scale, grad, w, static_cast<cudaStream_t>(stream), nullptr);
+}
+
+gdp_status gdp_policy_grad_bucketed(gdp_graph g, const gdp_config *c, const float *theta, const float *logits,
+                                    const uint8_t *placements, int32_t B, const double *adv, const float *logprob,
+                                    const float *old_logprob, float clip_eps, float entropy_coef, float loss_scale,
+                                    float *grad, void *ws, size_t ws_bytes, void *const *bucket_events,
+                                    void *stream) {
+  NvtxRange nvtx_("gdp_policy_grad_bucketed");
+  if (!g || !theta || !logits || !placements || !adv || !grad || !bucket_events)
+    return fail(GDP_ERR_ARG, "NULL argument");
+  if (old_logprob && !logprob) return fail(GDP_ERR_ARG, "logprob is required with old_logprob");
+  gdp_status st = check_config(c);
+  if (st != GDP_OK) return st;
+  if (B < 1) return fail(GDP_ERR_ARG, "B must be >= 1");
+  WS w;
+  st = carve_any(g, c->num_devices, B, ws, ws_bytes, &w);
+  if (st != GDP_OK) return st;
+  set_tensor_cores(c->tensor_cores);
+  set_no_attention(c->no_attention != 0);
+  cudaEvent_t ev[GDP_GRAD_BUCKETS];
+  for (int i = 0; i < GDP_GRAD_BUCKETS; i++) ev[i] = static_cast<cudaEvent_t>(bucket_events[i]);
+  return run_policy_grad(g, c, theta, logits, placements, B, adv, logprob, old_logprob, clip_eps, entropy_coef,
+                         loss_scale, grad, w, static_cast<cudaStream_t>(stream), ev);
+}
+
+gdp_status gdp_grad_buckets(const gdp_config *c, int32_t F, int64_t *first, int64_t *last) {
+  if (!first || !last) return fail(GDP_ERR_ARG, "NULL argument");
+  gdp_status st = check_config(c);
+  if (st != GDP_OK) return st;
+  if (F < 1) return fail(GDP_ERR_ARG, "F must be >= 1");
+  long long off[GDP_P_COUNT + 1];
+  param_offsets(F, c->num_devices, off);
+  first[0] = off[GDP_P_XL0_LN1_G]; last[0] = off[GDP_P_COUNT];
+  first[1] = off[GDP_P_COND_LN1_G]; last[1] = off[GDP_P_XL0_LN1_G];
+  first[2] = 0; last[2] = off[GDP_P_COND_LN1_G];
+  return GDP_OK;
+}
+
+gdp_status gdp_grad_sum(const float *const *grads, int32_t n_grads, int64_t len, float *out, void *stream) {
+  NvtxRange nvtx_("gdp_grad_sum");
+  if (!grads || !out || n_grads < 1 || len < 1) return fail(GDP_ERR_ARG, "bad argument");
+  for (int i = 0; i < n_grads; i++)
+    if (!grads[i]) return fail(GDP_ERR_ARG, "NULL gradient");
+  launch_grad_sum(grads, n_grads, len, out, static_cast<cudaStream_t>(stream));
+  GDP_LAUNCH_CHECK("gdp_grad_sum");
+  return GDP_OK;
 }
 
 }  // extern "C"

@@ -364,7 +364,13 @@ gdp_status run_place(const gdp_graph_s *g, const gdp_config *c, const float *the
 gdp_status run_policy_grad(const gdp_graph_s *g, const gdp_config *c, const float *theta, const float *logits,
                            const uint8_t *D, int B, const double *adv, const float *logprob,
                            const float *old_logprob, float eps, float beta, float scale, float *grad, const WS &w,
-                           cudaStream_t s) {
+                           cudaStream_t s, cudaEvent_t const *bucket_done) {
+  // bucket_done (nullable): events recorded as the gradient buckets become final, in the order
+  // the backward completes them -- [xl0 .. head] (placement layers, gates, head), the
+  // conditioner, the GNN (gdp_grad_buckets) -- so that their all-reduce can start early
+  auto mark = [&](int i) {
+    if (bucket_done && bucket_done[i]) cudaEventRecord(bucket_done[i], s);
+  };
   Offs off;
   const int d = c->num_devices, N = g->N, S = c->seg_len, M = c->mem_len;
   param_offsets(g->F, d, off.o);
@@ -400,10 +406,12 @@ gdp_status run_policy_grad(const gdp_graph_s *g, const gdp_config *c, const floa
     r.dpre = sup ? w.dgam + GT.m[12].goff : nullptr;
   }
   run_rows(RT, theta, grad, s);
+  if (!sup) { mark(0); mark(1); }   // no conditioner: its gradient stays zero
   if (sup) {
     dim3 gp(nblk((kH + 1) * kFFN, 256), kGateCount);
     note_launch("k_gate_bwd_P", s);
     k_gate_bwd_P<<<gp, 256, 0, s>>>(w.z, w.dgam, GT, grad);
+    mark(0);
     note_launch("k_gate_bwd_z", s);
     k_gate_bwd_z<<<1, 64, 0, s>>>(theta, w.dgam, GT, 1.0f / (float)N, w.dz);
     // conditioner: z = mean_v C_v -> dC_v = dz / N for every node
@@ -413,6 +421,7 @@ gdp_status run_policy_grad(const gdp_graph_s *g, const gdp_config *c, const floa
     RC.count = 0;
     add_layer_rows(RC, w, off, 0, nullptr, nullptr, GT, 0);
     run_rows(RC, theta, grad, s);
+    mark(1);
   }
   // back to caller order
   const float *dE = w.dEt;
@@ -443,6 +452,7 @@ gdp_status run_policy_grad(const gdp_graph_s *g, const gdp_config *c, const floa
   }
   launch_wgrad(N, g->F, kH, g->X, g->F, g->F, nullptr, 0, dHn, kH, true, w.part, w.part_floats,
                grad + off[GDP_P_GNN_IN_W], true, s);
+  mark(2);
   GDP_LAUNCH_CHECK("gdp_policy_grad");
   return GDP_OK;
 }

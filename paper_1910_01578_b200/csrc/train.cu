@@ -163,6 +163,38 @@ long long first_nonfinite(const float *g, long long n, unsigned long long *scrat
   return (long long)h;
 }
 
+// out = sum_i grads[i] in the fixed order i = 0, 1, ... (deterministic), 16-byte vectors
+struct GradPtrs {
+  const float *p[16];
+};
+__global__ void k_grad_sum(GradPtrs P, int n, long long len, int first, float *out) {
+  const long long n4 = len / 4;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (long long)gridDim.x * blockDim.x) {
+    float4 acc = first ? make_float4(0.f, 0.f, 0.f, 0.f) : reinterpret_cast<const float4 *>(out)[i];
+    for (int k = 0; k < n; k++) {
+      const float4 x = reinterpret_cast<const float4 *>(P.p[k])[i];
+      acc.x += x.x; acc.y += x.y; acc.z += x.z; acc.w += x.w;
+    }
+    reinterpret_cast<float4 *>(out)[i] = acc;
+  }
+  for (long long i = 4 * n4 + (long long)blockIdx.x * blockDim.x + threadIdx.x; i < len;
+       i += (long long)gridDim.x * blockDim.x) {
+    float acc = first ? 0.f : out[i];
+    for (int k = 0; k < n; k++) acc += P.p[k][i];
+    out[i] = acc;
+  }
+}
+
+void launch_grad_sum(const float *const *grads, int n, long long len, float *out, cudaStream_t s) {
+  for (int k0 = 0; k0 < n; k0 += 16) {
+    GradPtrs P;
+    const int m = n - k0 < 16 ? n - k0 : 16;
+    for (int k = 0; k < m; k++) P.p[k] = grads[k0 + k];
+    note_launch("k_grad_sum", s, 4.0 * (double)len * (m + 1 + (k0 ? 1 : 0)));
+    k_grad_sum<<<2 * sm_count(), 256, 0, s>>>(P, m, len, k0 == 0, out);
+  }
+}
+
 void launch_clip_adam(const float *g, long long n, double max_norm, double lr, double b1, double b2, double eps,
                       double c1, double c2, float *theta, float *m, float *v, double *scratch, double *norm_out,
                       cudaStream_t s) {

@@ -5,8 +5,11 @@ torch.distributed (NCCL) supplies the exchange steps of the data-parallel path, 
 out by sharding.plan.  With several graphs, each graph's embed -> place -> sample
 -> cost chain runs on its own CUDA stream; the gradients accumulate on the caller's stream:
   * mode 'samples': an all-gather of the rewards (global trial order for the advantage,
-    P:177) and one all-reduce of the flat fp32 gradient;
-  * mode 'graphs': one all-reduce of the gradient.
+    P:177) and the all-reduce of the flat fp32 gradient -- over NCCL in three buckets
+    (gdp_grad_buckets), each launched on a side stream as soon as gdp_policy_grad_bucketed has
+    finished it, overlapping the rest of the backward;
+  * mode 'graphs': the per-graph gradients summed on the device in graph order (gdp_grad_sum),
+    then one all-reduce.
 """
 from __future__ import annotations
 
@@ -15,8 +18,8 @@ from typing import Dict, List, Optional
 import numpy as np
 
 from . import (Config, Graph, Topo, default_config, gdp_advantage, gdp_clip_adam, gdp_cost, gdp_embed, gdp_logprob,
-               gdp_greedy, gdp_place, gdp_policy_grad, gdp_sample, gdp_sample_at, param_layout, workspace_size,
-               REPORT_BYTES, decode_reports)
+               gdp_greedy, gdp_place, gdp_policy_grad, gdp_policy_grad_bucketed, gdp_grad_sum, gdp_sample,
+               gdp_sample_at, grad_buckets, param_layout, workspace_size, GRAD_BUCKETS, REPORT_BYTES, decode_reports)
 from .sharding import plan as make_plan
 
 
@@ -157,23 +160,30 @@ class PolicyStep:
             if st.stream is not None:
                 main.wait_stream(st.stream)
         if per_graph:
-            self.grad.copy_(self.states[0].gbuf)
-            for st in self.states[1:]:
-                self.grad.add_(st.gbuf)
+            gdp_grad_sum([st.gbuf for st in self.states], self.grad)   # Eq. 1 sum over graphs, fixed order
             if self.collective:
                 torch.distributed.all_reduce(self.grad)
         else:
+            # one graph per step over NCCL: the gradient all-reduce runs in buckets, each launched on
+            # a side stream as soon as the backward has finished it (gdp_policy_grad_bucketed)
+            bucketed = (self.collective and len(self.states) == 1 and
+                        torch.distributed.get_backend() == "nccl")
+            works = []
             for st in self.states:
                 if P.mode == "samples" and self.collective:
                     torch.distributed.all_gather_into_tensor(st.reward_all, st.reward)
-                self._grad_of(st, theta, timed, self.grad)
-            if self.collective:
+                works += self._grad_of(st, theta, timed, self.grad, bucketed)
+            if bucketed:
+                for w in works:
+                    w.wait()                      # the current stream waits for the NCCL stream
+                main.wait_stream(self.side)
+            elif self.collective:
                 torch.distributed.all_reduce(self.grad)
         if dev_step:
             self.step_dev += 1
         self.step_idx += 1
 
-    def _grad_of(self, st, theta, timed: bool, grad):
+    def _grad_of(self, st, theta, timed: bool, grad, bucketed: bool = False):
         P = self.plan
         if not (P.mode == "samples" and self.collective):
             st.reward_all.copy_(st.reward)
@@ -182,9 +192,24 @@ class PolicyStep:
         if grad is not self.grad:
             grad.zero_()
         self._ev("grad0", timed)
-        gdp_policy_grad(st.g, st.cfg, theta, st.logits, st.placements, st.B, adv, st.logprob, None,
-                        self.clip_eps, P.entropy_coef, P.loss_scale, grad, st.ws)
+        works = []
+        if bucketed:
+            torch = self.torch
+            if not hasattr(self, "side"):
+                self.side = torch.cuda.Stream(device=self.device)
+                self.bucket_ev = [torch.cuda.Event() for _ in range(GRAD_BUCKETS)]
+                self.buckets = grad_buckets(self.cfg, st.F)
+            gdp_policy_grad_bucketed(st.g, st.cfg, theta, st.logits, st.placements, st.B, adv, st.logprob, None,
+                                     self.clip_eps, P.entropy_coef, P.loss_scale, grad, st.ws, self.bucket_ev)
+            with torch.cuda.stream(self.side):
+                for ev, (a, b) in zip(self.bucket_ev, self.buckets):
+                    self.side.wait_event(ev)
+                    works.append(torch.distributed.all_reduce(grad[a:b], async_op=True))
+        else:
+            gdp_policy_grad(st.g, st.cfg, theta, st.logits, st.placements, st.B, adv, st.logprob, None,
+                            self.clip_eps, P.entropy_coef, P.loss_scale, grad, st.ws)
         self._ev("grad1", timed)
+        return works
 
 
 class PPOTrainer:

@@ -29,7 +29,7 @@ def header_functions():
 def test_exports_every_declared_symbol():
     L = gdp.lib()
     names = header_functions()
-    assert len(names) == 28
+    assert len(names) == 31
     assert sorted(names) == sorted(gdp.EXPORTS)
     for n in names:
         assert hasattr(L, n), n
@@ -135,3 +135,13 @@ def test_product_path_never_imports_the_oracle():
                 txt = open(os.path.join(dirpath, f)).read()
                 for pat in ("import oracle", "from oracle", "liboracle", "oracle/sim", "oracle.simulate"):
                     assert pat not in txt, (f, pat)
+
+
+def test_grad_buckets_partition_theta():
+    """gdp_grad_buckets: the three buckets partition [0, n_params) along parameter-tensor
+    boundaries, in backward completion order (placement layers + gates + head, conditioner, GNN)."""
+    cfg = gdp.default_config(8)
+    off, n = gdp.param_layout(cfg, 37)
+    b = gdp.grad_buckets(cfg, 37)
+    assert b[2][0] == 0 and b[2][1] == b[1][0] and b[1][1] == b[0][0] and b[0][1] == n
+    assert b[1][0] == off[14] and b[0][0] == off[30]      # GDP_P_COND_LN1_G, GDP_P_XL0_LN1_G

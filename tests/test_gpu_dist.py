@@ -35,12 +35,12 @@ def _graphs(cfg):
     return W, [(g, workloads.features(g), workloads.topology(g, W.d)) for g in gs]
 
 
-def _run(mode, rank, world, batch, steps):
+def _run(mode, rank, world, batch, steps, dev=0):
     import paper_1910_01578_b200 as gdp
     W, graphs = _graphs(mode)
-    theta = torch.from_numpy(workloads.init_theta(workloads.F, W.d, seed=7, mode="random")).cuda()
+    theta = torch.from_numpy(workloads.init_theta(workloads.F, W.d, seed=7, mode="random")).cuda(dev)
     ps = gdp.PolicyStep(graphs, W.d, W.seg_len, W.mem_len, True, batch, seed=W.seed, mode=mode, rank=rank,
-                        world=world, device=torch.device("cuda", 0))
+                        world=world, device=torch.device("cuda", dev))
     out = []
     for _ in range(steps):
         ps.run(theta)
@@ -50,20 +50,26 @@ def _run(mode, rank, world, batch, steps):
     return out
 
 
-def _worker(rank, world, port, mode, batch, steps, q):
+def _worker(rank, world, port, mode, batch, steps, q, backend="gloo"):
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
-    torch.cuda.set_device(0)
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    dev = rank if backend == "nccl" else 0          # NCCL: one GPU per rank (bucketed all-reduce)
+    torch.cuda.set_device(dev)
+    dist.init_process_group(backend, rank=rank, world_size=world)
     try:
-        q.put((rank, _run(mode, rank, world, batch, steps)))
+        q.put((rank, _run(mode, rank, world, batch, steps, dev)))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("mode", ["samples", "graphs"])
-def test_two_ranks_match_one(mode):
+@pytest.mark.parametrize("mode,backend", [("samples", "gloo"), ("graphs", "gloo"), ("samples", "nccl"),
+                                          ("graphs", "nccl")])
+def test_two_ranks_match_one(mode, backend):
+    """gloo: two ranks sharing cuda:0.  nccl: two ranks on two GPUs (skipped when fewer are
+    visible) -- the bucketed all-reduce that overlaps the backward (gdp_policy_grad_bucketed)."""
+    if backend == "nccl" and torch.cuda.device_count() < 2:
+        pytest.skip("NCCL with two ranks needs two GPUs")
     from paper_1910_01578_b200 import _build
     _build.build()
     world, batch, steps = 2, 8, 2
@@ -71,7 +77,7 @@ def test_two_ranks_match_one(mode):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, mode, batch, steps, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, mode, batch, steps, q, backend)) for r in range(world)]
     for p in procs:
         p.start()
     res = dict(q.get(timeout=600) for _ in range(world))
@@ -99,3 +105,35 @@ def test_two_ranks_match_one(mode):
             assert sorted(got) == list(range(3))
             for gi in range(3):
                 assert np.array_equal(got[gi][0], single[s][1][gi]) and np.array_equal(got[gi][1], single[s][2][gi])
+
+
+def test_nccl_single_rank_bucketed_matches_plain():
+    """One NCCL rank (the bench's torchrun path at N = 1): the bucketed all-reduce issued from the
+    backward's events gives the same gradient as the plain single-process step, bit for bit."""
+    import torch.distributed as dist
+    import paper_1910_01578_b200 as gdp
+    from paper_1910_01578_b200 import _build
+    _build.build()
+    plain = _run("samples", 0, 1, 8, 2)
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(_free_port())
+    dist.init_process_group("nccl", rank=0, world_size=1)
+    try:
+        buck = _run("samples", 0, 1, 8, 2)
+    finally:
+        dist.destroy_process_group()
+    for s in range(2):
+        assert np.array_equal(plain[s][0], buck[s][0])
+
+
+def test_grad_sum_fixed_order():
+    """gdp_grad_sum: out = g0 + g1 + g2 in that order, bit-exact against the same fp32 sums."""
+    import paper_1910_01578_b200 as gdp
+    rng = np.random.default_rng(0)
+    n = 269_193
+    gs = [rng.normal(size=n).astype(np.float32) for _ in range(3)]
+    out = torch.empty(n, device="cuda")
+    gdp.gdp_grad_sum([torch.from_numpy(g).cuda() for g in gs], out)
+    torch.cuda.synchronize()
+    ref = (gs[0] + gs[1]) + gs[2]
+    assert np.array_equal(out.cpu().numpy(), ref)
