@@ -212,6 +212,7 @@ bool ws_layout(const gdp_graph_s *g, int d, int B, char *base, WS *w) {
   z.cdf = F32(N * kMaxD);
   z.logp = F32(N * kMaxD);
   z.lastpos = reinterpret_cast<int *>(take(N * sizeof(int)));
+  z.lpart = reinterpret_cast<double *>(take((size_t)kLogitChunks * N * kMaxD * sizeof(double)));
   const size_t Bc = (size_t)std::max(B, 1);
   // everything below depends on B (kept last so the offsets above never move)
   z.wb = reinterpret_cast<double *>(take(Bc * sizeof(double)));

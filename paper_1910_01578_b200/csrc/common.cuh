@@ -112,7 +112,7 @@ struct WS {
   float *Etopo, *zsum, *z, *gam, *Wh, *dWh, *logits_topo;
   Layer L[3];  // 0 = conditioner, 1 = xl0, 2 = xl1
   // grad scratch
-  double *wb;
+  double *wb, *lpart;
   float *dlog, *dlog_topo, *dy, *dx1, *dm, *dc, *dout, *dqkv, *dkvm, *dkvt, *da, *dam, *dxa, *dEt, *dE;
   float *dH, *dHn, *dAg, *dP, *dd;
   float *part;           // wgrad / column-sum partials
@@ -225,9 +225,11 @@ void launch_sample(const float *logits, int ld, const int *leader, bool has_colo
                    uint8_t *D, float *logprob, cudaStream_t s);
 void launch_node_prep(const float *logits, int ld, int N, int d, float *cdf, float *logp, int *lastpos,
                       cudaStream_t s);
+// dL/dlogits (a14): part = kLogitChunks x N x kMaxD doubles of scratch (ws.lpart)
+constexpr int kLogitChunks = 16;
 void launch_logit_grad(const float *logits, int ld, const uint8_t *D, const int *leader, const double *adv,
                        const float *logprob, const float *old_logprob, float eps, float beta, float scale,
-                       int N, int d, int B, double *wb, float *dlog, cudaStream_t s);
+                       int N, int d, int B, double *wb, double *part, float *dlog, cudaStream_t s);
 
 // training update (NEXT-1)
 constexpr int kAdamScratch = 1024;   // doubles of caller scratch for gdp_clip_adam (GDP_ADAM_SCRATCH)

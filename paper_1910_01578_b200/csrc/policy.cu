@@ -378,7 +378,7 @@ gdp_status run_policy_grad(const gdp_graph_s *g, const gdp_config *c, const floa
   const GateTable GT = gate_table(off);
   // a14: dL/dlogits (caller order) -> topological order
   launch_logit_grad(logits, d, D, g->leader, adv, logprob, old_logprob, eps, beta, scale, N, active_devices(c), B,
-                    w.wb, w.dlog, s);
+                    w.wb, w.lpart, w.dlog, s);
   const float *dlt = w.dlog;
   if (!g->perm_identity) {
     launch_rows_gather(w.dlog, g->perm, w.dlog_topo, N, d, s);

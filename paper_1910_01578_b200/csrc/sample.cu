@@ -49,10 +49,15 @@ __global__ void k_node_prep(const float *logits, int ld, int N, int d, float *cd
 }
 
 constexpr int ST = 256;
+// One CTA per placement; a thread draws 4 consecutive nodes from one Philox4x32-10 call.  The
+// inverse CDF is the count of CDF entries <= u (the CDF is non-decreasing, so that count is the
+// first k with u < c_k; d (none) -> the last k with p_k > 0); the 4 device bytes leave as one
+// 32-bit store when the placement row is 4-byte aligned.
 __global__ void __launch_bounds__(ST) k_sample(const float *__restrict__ cdf, const float *__restrict__ logp,
                                                const int *__restrict__ lastpos, const int *__restrict__ leader,
-                                               int N, int d, uint64_t seed, uint64_t offset, uint64_t step_val,
-                                               const uint64_t *step_ptr, uint8_t *D, float *logprob) {
+                                               int has_coloc, int N, int d, uint64_t seed, uint64_t offset,
+                                               uint64_t step_val, const uint64_t *step_ptr, uint8_t *D,
+                                               float *logprob) {
   const uint64_t step = step_ptr ? *step_ptr : step_val;   // device counter: graph replays advance it
   __shared__ double red[ST / 32];
   const int b = blockIdx.x;
@@ -61,24 +66,35 @@ __global__ void __launch_bounds__(ST) k_sample(const float *__restrict__ cdf, co
   double acc = 0.0;
   const int nq = (N + 3) >> 2;
   uint8_t *Db = D + (size_t)b * N;
+  const bool aligned = ((N & 3) == 0);
   for (int q = threadIdx.x; q < nq; q += ST) {
-    uint4 w = philox4x32_10(make_uint4((unsigned)q, (unsigned)(gidx & 0xffffffffu), (unsigned)(step & 0xffffffffu),
-                                       (unsigned)(gidx >> 32)),
-                            key);
-    unsigned ws[4] = {w.x, w.y, w.z, w.w};
+    const uint4 w = philox4x32_10(make_uint4((unsigned)q, (unsigned)(gidx & 0xffffffffu),
+                                             (unsigned)(step & 0xffffffffu), (unsigned)(gidx >> 32)),
+                                  key);
+    const unsigned ws[4] = {w.x, w.y, w.z, w.w};
+    unsigned packed = 0;
 #pragma unroll
     for (int j = 0; j < 4; j++) {
-      int v = 4 * q + j;
-      if (v >= N) break;
-      float u = (float)(ws[j] >> 8) * 5.9604644775390625e-08f;  // 2^-24
-      const float *cv = cdf + (size_t)v * d;
-      int k = -1;
-      for (int t = 0; t < d; t++)
-        if (u < cv[t]) { k = t; break; }
-      if (k < 0) k = lastpos[v];
-      Db[v] = (uint8_t)k;
-      if (leader[v] == v) acc += (double)logp[(size_t)v * d + k];
+      const int v = 4 * q + j;
+      if (v < N) {
+        const float u = (float)(ws[j] >> 8) * 5.9604644775390625e-08f;  // 2^-24
+        const float *cv = cdf + (size_t)v * d;
+        int k = 0;
+        if (d == 8) {
+          const float4 c0 = __ldg(reinterpret_cast<const float4 *>(cv)), c1 = __ldg(reinterpret_cast<const float4 *>(cv) + 1);
+          k = (c0.x <= u) + (c0.y <= u) + (c0.z <= u) + (c0.w <= u) + (c1.x <= u) + (c1.y <= u) + (c1.z <= u) +
+              (c1.w <= u);
+        } else {
+          for (int t = 0; t < d; t++) k += (__ldg(cv + t) <= u);
+        }
+        if (k >= d) k = __ldg(lastpos + v);
+        packed |= (unsigned)k << (8 * j);
+        if (!has_coloc || __ldg(leader + v) == v) acc += (double)__ldg(logp + (size_t)v * d + k);
+      }
     }
+    if (aligned) *reinterpret_cast<unsigned *>(Db + 4 * q) = packed;
+    else
+      for (int j = 0; j < 4 && 4 * q + j < N; j++) Db[4 * q + j] = (uint8_t)(packed >> (8 * j));
   }
   // fixed-order block reduction
 #pragma unroll
@@ -91,7 +107,6 @@ __global__ void __launch_bounds__(ST) k_sample(const float *__restrict__ cdf, co
     logprob[b] = (float)s;
   }
 }
-
 __global__ void k_colocate(const int *leader, int N, int B, uint8_t *D) {
   size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= (size_t)N * B) return;
@@ -113,13 +128,60 @@ __global__ void k_weights(const double *adv, const float *logprob, const float *
   wb[b] = (rho * A <= cl * A) ? rho * A : 0.0;
 }
 
-__global__ void k_logit_grad(const float *__restrict__ logits, int ld, const uint8_t *__restrict__ D,
-                             const int *__restrict__ leader, const double *__restrict__ wb, float beta, float scale,
-                             int N, int d, int B, float *dlog) {
-  extern __shared__ double swb[];
-  for (int b = threadIdx.x; b < B; b += blockDim.x) swb[b] = wb[b];
+// a14, part 1: per (node, device) the fp64 sum over one chunk of placements of w_b [D_bv = k];
+// a thread covers 4 consecutive nodes (one 32-bit load of their device bytes per placement when
+// the rows are 4-byte aligned); chunk c of the placements -> part[c][v][k] (fixed order later)
+constexpr int LG_T = 128;
+__global__ void __launch_bounds__(LG_T) k_logit_acc(const uint8_t *__restrict__ D, const double *__restrict__ wb,
+                                                     int N, int d, int B, int b_per, double *part) {
+  const int q = blockIdx.x * LG_T + threadIdx.x;
+  const int v0 = 4 * q;
+  const int c = blockIdx.y, b0 = c * b_per, b1 = min(B, b0 + b_per);
+  double acc[4][kMaxD];
+#pragma unroll
+  for (int j = 0; j < 4; j++)
+#pragma unroll
+    for (int k = 0; k < kMaxD; k++) acc[j][k] = 0.0;
+  if (v0 < N) {
+    const bool aligned = ((N & 3) == 0) && v0 + 3 < N;
+    for (int b = b0; b < b1; b++) {
+      const double w = __ldg(wb + b);
+      unsigned x;
+      if (aligned) x = __ldg(reinterpret_cast<const unsigned *>(D + (size_t)b * N + v0));
+      else {
+        x = 0;
+        for (int j = 0; j < 4 && v0 + j < N; j++) x |= (unsigned)D[(size_t)b * N + v0 + j] << (8 * j);
+      }
+#pragma unroll
+      for (int j = 0; j < 4; j++) {
+        const unsigned k = (x >> (8 * j)) & 0xffu;
+#pragma unroll
+        for (int t = 0; t < kMaxD; t++) acc[j][t] += (t == (int)k) ? w : 0.0;
+      }
+    }
+  }
+  for (int j = 0; j < 4; j++) {
+    const int v = v0 + j;
+    if (v >= N) break;
+#pragma unroll
+    for (int t = 0; t < kMaxD; t++)
+      if (t < d) part[((size_t)c * N + v) * d + t] = acc[j][t];
+  }
+}
+
+// a14, part 2: dL/dz_vk = -s (sum_b w_b [D_bv = k] - p_vk sum_b w_b) [v leader] + (beta/N) p_vk
+// (log p_vk + H_v); the chunk partials summed in chunk order (deterministic)
+__global__ void k_logit_fin(const float *__restrict__ logits, int ld, const int *__restrict__ leader,
+                            const double *__restrict__ wb, const double *__restrict__ part, int nchunks, float beta,
+                            float scale, int N, int d, int B, float *dlog) {
+  __shared__ double s_sw;
+  if (threadIdx.x == 0) {
+    double sw = 0.0;
+    for (int b = 0; b < B; b++) sw += wb[b];
+    s_sw = sw;
+  }
   __syncthreads();
-  int v = blockIdx.x * blockDim.x + threadIdx.x;
+  const int v = blockIdx.x * blockDim.x + threadIdx.x;
   if (v >= N) return;
   const float *z = logits + (size_t)v * ld;
   float mx = z[0];
@@ -129,21 +191,9 @@ __global__ void k_logit_grad(const float *__restrict__ logits, int ld, const uin
     e[k] = expf(z[k] - mx);
     s += e[k];
   }
-  float ls = logf(s);
-  double acc[kMaxD];
-  for (int k = 0; k < kMaxD; k++) acc[k] = 0.0;
-  double sw = 0.0;
+  const float ls = logf(s);
   const bool lead = leader[v] == v;
-  if (lead) {
-    for (int b = 0; b < B; b++) {
-      int k = D[(size_t)b * N + v];
-      double w = swb[b];
-      sw += w;
-#pragma unroll
-      for (int t = 0; t < kMaxD; t++)
-        if (t == k) acc[t] += w;
-    }
-  }
+  const double sw = lead ? s_sw : 0.0;
   float p[kMaxD], lp[kMaxD], Hv = 0.f;
   for (int k = 0; k < d; k++) {
     p[k] = e[k] / s;
@@ -152,7 +202,10 @@ __global__ void k_logit_grad(const float *__restrict__ logits, int ld, const uin
   }
   const float bn = beta / (float)N;
   for (int k = 0; k < d; k++) {
-    float g = (float)(-(double)scale * (acc[k] - (double)p[k] * sw));
+    double acc = 0.0;
+    if (lead)
+      for (int c = 0; c < nchunks; c++) acc += part[((size_t)c * N + v) * d + k];
+    float g = (float)(-(double)scale * (acc - (double)p[k] * sw));
     g += bn * p[k] * (lp[k] + Hv);
     dlog[(size_t)v * ld + k] = g;
   }
@@ -167,7 +220,8 @@ void launch_sample(const float *logits, int ld, const int *leader, bool has_colo
   note_launch("k_node_prep", s);
   k_node_prep<<<(N + 255) / 256, 256, 0, s>>>(logits, ld, N, d, cdf, logp, lastpos);
   note_launch("k_sample", s, (double)B * N + 4.0 * (double)N * (2 * d + 1));
-  k_sample<<<B, ST, 0, s>>>(cdf, logp, lastpos, leader, N, d, seed, offset, step, step_ptr, D, logprob);
+  k_sample<<<B, ST, 0, s>>>(cdf, logp, lastpos, leader, has_coloc ? 1 : 0, N, d, seed, offset, step, step_ptr, D,
+                            logprob);
   if (has_coloc) {
     size_t n = (size_t)N * B;
     note_launch("k_colocate", s);
@@ -183,13 +237,20 @@ void launch_node_prep(const float *logits, int ld, int N, int d, float *cdf, flo
 
 void launch_logit_grad(const float *logits, int ld, const uint8_t *D, const int *leader, const double *adv,
                        const float *logprob, const float *old_logprob, float eps, float beta, float scale,
-                       int N, int d, int B, double *wb, float *dlog, cudaStream_t s) {
+                       int N, int d, int B, double *wb, double *part, float *dlog, cudaStream_t s) {
   note_launch("k_weights", s);
   k_weights<<<(B + 255) / 256, 256, 0, s>>>(adv, logprob, old_logprob, eps, B, wb);
-  size_t smem = (size_t)B * sizeof(double);
-  if (smem > 48 * 1024) cudaFuncSetAttribute(k_logit_grad, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  note_launch("k_logit_grad", s, (double)B * N + 4.0 * 2 * (double)N * d);
-  k_logit_grad<<<(N + 127) / 128, 128, smem, s>>>(logits, ld, D, leader, wb, beta, scale, N, d, B, dlog);
+  // placements split into chunks so that ~4 waves of threads stream the B x N bytes
+  const int nq = (N + 3) / 4, nblk = (nq + LG_T - 1) / LG_T;
+  int nch = (148 * 8 + nblk - 1) / nblk;   // ~8 CTAs of 128 threads per SM
+  nch = nch < 1 ? 1 : (nch > kLogitChunks ? kLogitChunks : nch);
+  if (nch > B) nch = B;
+  const int b_per = (B + nch - 1) / nch;
+  nch = (B + b_per - 1) / b_per;
+  note_launch("k_logit_acc", s, (double)B * N + 8.0 * d * (double)N * nch);
+  k_logit_acc<<<dim3(nblk, nch), LG_T, 0, s>>>(D, wb, N, d, B, b_per, part);
+  note_launch("k_logit_grad", s, 8.0 * d * (double)N * nch + 4.0 * 2 * (double)N * d);
+  k_logit_fin<<<(N + 127) / 128, 128, 0, s>>>(logits, ld, leader, wb, part, nch, beta, scale, N, d, B, dlog);
 }
 
 }  // namespace gdp

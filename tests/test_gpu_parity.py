@@ -185,6 +185,22 @@ def test_cost_full_size_c4(gdp):
     assert_cost_equal(g, t, D, cost_gpu(gdp, g, t, D))
 
 
+def test_cost_full_size_c4_64k(gdp):
+    """PAPER.md:181 "over 60k nodes": the 64 274-op GNMT (BASELINE configs[3] unrolled further)
+    on k_cost5, bit-exact against the oracle -- random, single-device (OOM) and block placements."""
+    W = workloads.config("c4_64k")
+    g = W.graphs[0]
+    assert g.N > 60000
+    t = workloads.topology(g, W.d)
+    G = gdp.Graph(g, workloads.features(g))
+    assert gdp.cost_kernel(G, gdp.Topo(t)) == 5
+    rng = np.random.default_rng(64)
+    D = rng.integers(0, W.d, size=(6, g.N)).astype(np.uint8)
+    D[1] = 0
+    D[2] = (np.arange(g.N) * W.d // g.N).astype(np.uint8)
+    assert_cost_equal(g, t, D, cost_gpu(gdp, g, t, D))
+
+
 # ------------------------------------------------------------------ policy network stages
 def gpu_ties(gdp, G, cfg, ws, na=False):
     """The GPU's recorded decisions at the kinks (gdp_debug_tensors): max-pool argmax per GNN

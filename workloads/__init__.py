@@ -514,6 +514,10 @@ def config(name: str, batch: Optional[int] = None, mem_len: Optional[int] = None
         # B = 1184 = 148 SMs x 8 resident k_cost5 CTAs: one full wave of the cost kernel (one CTA
         # per placement, 27 KB of shared memory each at N = 52 k)
         w = Workload("c4_gnmt52k_d8", [gnmt(seed=1005)], d=8, seg_len=128, mem_len=128, batch=1184)
+    elif name == "c4_64k":
+        # PAPER.md:181 "over 60k nodes": the same GNMT shape unrolled over 148 steps (64 274 ops);
+        # 30.4 KB of cost-kernel shared memory per placement -> 7 CTAs per SM, B = 1036 = one wave
+        w = Workload("c4_gnmt64k_d8", [gnmt(steps=148, seed=1005)], d=8, seg_len=128, mem_len=128, batch=1036)
     elif name == "c5":
         gs = []
         for i, s in enumerate([1011, 1015]):
