@@ -231,6 +231,8 @@ gdp_status gdp_place(gdp_graph g, const gdp_config *c, const float *theta, const
  * the leader (lowest id in the group).  logprob[b] = sum over leaders of log p_v[D].
  *   logits      dev fp32 N x d (in);  placements dev uint8 B x N (out, placement-major)
  *   logprob     dev fp32 B (out)
+ * ws must be sized for at least B placements (gdp_workspace_size); log pi is summed in fp64 in a
+ * fixed order (per 128-node chunk, then the chunks in order): bit-identical across runs.
  * Errors: GDP_ERR_ARG (B < 1), GDP_ERR_WORKSPACE, GDP_ERR_CUDA. */
 gdp_status gdp_sample(gdp_graph g, const gdp_config *c, const float *logits, int32_t B, uint64_t seed,
                       uint64_t sample_offset, uint64_t step, uint8_t *placements, float *logprob,

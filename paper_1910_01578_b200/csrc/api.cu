@@ -216,6 +216,10 @@ bool ws_layout(const gdp_graph_s *g, int d, int B, char *base, WS *w) {
   const size_t Bc = (size_t)std::max(B, 1);
   // everything below depends on B (kept last so the offsets above never move)
   z.wb = reinterpret_cast<double *>(take(Bc * sizeof(double)));
+  {  // sampling: log pi partial sums per placement and 128-node warp chunk (k_sample)
+    const size_t nq = (N + 3) / 4, nwc = (nq + 255) / 256 * 8;
+    z.spart = reinterpret_cast<double *>(take(Bc * nwc * sizeof(double)));
+  }
   // cost scratch: one region per placement, large enough for either cost kernel
   size_t v1 = (2 + 2) * N * sizeof(int) + N * sizeof(int2) + E * sizeof(int4) + N * sizeof(int);
   size_t v2 = cost2_scratch_per_placement(g->N, g->E, g->nbig);
@@ -741,12 +745,11 @@ static gdp_status sample_impl(gdp_graph g, const gdp_config *c, const float *log
   if (st != GDP_OK) return st;
   if (B < 1) return fail(GDP_ERR_ARG, "B must be >= 1");
   WS w;
-  st = carve_any(g, c->num_devices, 1, ws, ws_bytes, &w);
+  st = carve_any(g, c->num_devices, B, ws, ws_bytes, &w);
   if (st != GDP_OK) return st;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   launch_sample(logits, c->num_devices, g->leader, g->has_coloc, g->N, active_devices(c), B, seed, sample_offset,
-                step, step_dev, w.cdf,
-                w.logp, w.lastpos, placements, logprob, s);
+                step, step_dev, w.cdf, w.logp, w.lastpos, w.spart, placements, logprob, s);
   GDP_LAUNCH_CHECK("gdp_sample");
   return GDP_OK;
 }

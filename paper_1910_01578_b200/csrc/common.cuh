@@ -112,7 +112,7 @@ struct WS {
   float *Etopo, *zsum, *z, *gam, *Wh, *dWh, *logits_topo;
   Layer L[3];  // 0 = conditioner, 1 = xl0, 2 = xl1
   // grad scratch
-  double *wb, *lpart;
+  double *wb, *lpart, *spart;
   float *dlog, *dlog_topo, *dy, *dx1, *dm, *dc, *dout, *dqkv, *dkvm, *dkvt, *da, *dam, *dxa, *dEt, *dE;
   float *dH, *dHn, *dAg, *dP, *dd;
   float *part;           // wgrad / column-sum partials
@@ -222,7 +222,7 @@ void launch_fill_rows(float *dst, const float *row, float scale, int N, int C, c
 // sampling / loss
 void launch_sample(const float *logits, int ld, const int *leader, bool has_coloc, int N, int d, int B, uint64_t seed,
                    uint64_t offset, uint64_t step, const uint64_t *step_ptr, float *cdf, float *logp, int *lastpos,
-                   uint8_t *D, float *logprob, cudaStream_t s);
+                   double *spart, uint8_t *D, float *logprob, cudaStream_t s);
 void launch_node_prep(const float *logits, int ld, int N, int d, float *cdf, float *logp, int *lastpos,
                       cudaStream_t s);
 // dL/dlogits (a14): part = kLogitChunks x N x kMaxD doubles of scratch (ws.lpart)

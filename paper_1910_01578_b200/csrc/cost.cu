@@ -385,17 +385,39 @@ __global__ void __launch_bounds__(32) k_cost(CostGraph G, TopoArgs T, const uint
   }
 }
 
-__global__ void k_advantage(const double *r, int B, double *sum, long long *cnt, double *adv) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+// A_b = r_b - (running sum before b) / (running count before b), the running state in the global
+// trial order (reading R22).  The running sum is one sequential chain of fp64 additions
+// (the oracle's order, bit-exact); only the chain runs on lane 0 -- the rewards are staged into
+// shared memory by the whole warp and the divisions run lane-parallel -- in chunks of AC.
+constexpr int AC = 2048;
+__global__ void __launch_bounds__(32) k_advantage(const double *__restrict__ r, int B, double *sum, long long *cnt,
+                                                  double *__restrict__ adv) {
+  __shared__ double sr[AC], sp[AC];
+  const int lane = threadIdx.x;
   double s = *sum;
-  long long c = *cnt;
-  for (int b = 0; b < B; b++) {
-    adv[b] = (c == 0) ? 0.0 : __dsub_rn(r[b], __ddiv_rn(s, (double)c));
-    s = __dadd_rn(s, r[b]);
-    c += 1;
+  const long long c0 = *cnt;
+  for (int b0 = 0; b0 < B; b0 += AC) {
+    const int n = min(AC, B - b0);
+    for (int i = lane; i < n; i += 32) sr[i] = r[b0 + i];
+    __syncwarp();
+    if (lane == 0) {
+      for (int i = 0; i < n; i++) {
+        sp[i] = s;
+        s = __dadd_rn(s, sr[i]);
+      }
+    }
+    s = __shfl_sync(0xffffffffu, s, 0);
+    __syncwarp();
+    for (int i = lane; i < n; i += 32) {
+      const long long c = c0 + b0 + i;
+      adv[b0 + i] = (c == 0) ? 0.0 : __dsub_rn(sr[i], __ddiv_rn(sp[i], (double)c));
+    }
+    __syncwarp();
   }
-  *sum = s;
-  *cnt = c;
+  if (lane == 0) {
+    *sum = s;
+    *cnt = c0 + B;
+  }
 }
 
 }  // namespace

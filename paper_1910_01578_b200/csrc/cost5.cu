@@ -186,6 +186,7 @@ __global__ void __launch_bounds__(512) k_cost5_pre(Cost5Graph G, TopoArgs T, con
                                                    unsigned char *scratch, size_t per_place) {
   __shared__ unsigned long long s_stat[8], s_busy[8], s_cross;
   __shared__ int s_cnt[8], s_ch[64], s_flag;
+  __shared__ int s_chw[16][64];   // per-warp channel counts (no contention on 64 addresses)
   const int N = G.N, d = T.d, b = blockIdx.x, tid = threadIdx.x, lane = tid & 31;
   const unsigned FULL = 0xffffffffu;
   const uint8_t *D = Dall + (size_t)b * N;
@@ -197,6 +198,7 @@ __global__ void __launch_bounds__(512) k_cost5_pre(Cost5Graph G, TopoArgs T, con
   int *gbig = reinterpret_cast<int *>(base + L.gbig);
   if (tid < 8) { s_stat[tid] = 0; s_busy[tid] = 0; s_cnt[tid] = 0; }
   if (tid < 64) s_ch[tid] = 0;
+  for (int i = tid; i < 16 * 64; i += blockDim.x) (&s_chw[0][0])[i] = 0;
   if (tid == 0) { s_cross = 0; s_flag = 0; }
   __syncthreads();
   {
@@ -205,7 +207,7 @@ __global__ void __launch_bounds__(512) k_cost5_pre(Cost5Graph G, TopoArgs T, con
 #pragma unroll
     for (int k = 0; k < 8; k++) { lm[k] = 0; lb[k] = 0; lc[k] = 0; }
     for (int v = tid; v < N; v += blockDim.x) {
-      int k = D[v];
+      int k = __ldg(D + v);
       if (k >= d) { flag |= 2; k = 0; }
       const long long mb = G.mem_bytes[v];
       const long long du = (long long)G.cost[v] * T.speed[k];
@@ -231,18 +233,30 @@ __global__ void __launch_bounds__(512) k_cost5_pre(Cost5Graph G, TopoArgs T, con
     long long lcross = 0;
     for (long long e = tid; e < G.E; e += blockDim.x) {
       const int u = G.out_src[e], w = G.out_idx[e];
-      const int su = D[u], tw = D[w];
+      const int su = __ldg(D + u), tw = __ldg(D + w);
       sdev[e] = (uint8_t)tw;
       if (su != tw && su < d && tw < d) {
-        atomicAdd(&s_ch[su * 8 + tw], 1);
+        atomicAdd(&s_chw[(tid >> 5) & 15][su * 8 + tw], 1);
         lcross += G.out_bytes[u];
       }
     }
     lcross = warp_sum_ll(lcross);
     if (lane == 0 && lcross) atomicAdd(&s_cross, (unsigned long long)lcross);
   }
-  for (int v = tid; v < N; v += blockDim.x) outcnt[v] = G.outdeg[v];
+  {  // consumer counters of the memory warp: a 16-byte vector copy of the out-degrees
+    const int n4 = N / 4;
+    const int4 *src = reinterpret_cast<const int4 *>(G.outdeg);
+    int4 *dst = reinterpret_cast<int4 *>(outcnt);
+    for (int i = tid; i < n4; i += blockDim.x) dst[i] = __ldg(src + i);
+    for (int v = 4 * n4 + tid; v < N; v += blockDim.x) outcnt[v] = G.outdeg[v];
+  }
   for (int i = tid; i < G.ngbig; i += blockDim.x) gbig[i] = G.gbig0[i];
+  __syncthreads();
+  if (tid < 64) {
+    int c = 0;
+    for (int w = 0; w < 16; w++) c += s_chw[w][tid];
+    s_ch[tid] = c;
+  }
   __syncthreads();
   if (tid < 8) {
     pre->stat[tid] = (long long)s_stat[tid];

@@ -48,64 +48,83 @@ __global__ void k_node_prep(const float *logits, int ld, int N, int d, float *cd
   lastpos[v] = last;
 }
 
+// a11.  Grid = (node chunks of 4 x 256 nodes, groups of SBG placements): a thread owns 4
+// consecutive nodes, keeps their CDF, log-probabilities and fallbacks in registers (read once, not
+// once per placement), and for each placement of its group draws its 4 uniforms from one
+// Philox4x32-10 call (counter (v>>2, gidx, step, gidx>>32), key = seed).  The inverse CDF is the
+// count of CDF entries <= u (the CDF is non-decreasing, so that count is the first k with
+// u < c_k; d -> the last k with p_k > 0).  The 4 device bytes leave as one 32-bit store (rows
+// 4-byte aligned) or 4 byte stores.  log pi_b: a fixed-order warp reduction per 128 nodes into
+// part[b][warp chunk], then k_sample_lp sums the warp chunks in order (deterministic).
 constexpr int ST = 256;
-// One CTA per placement; a thread draws 4 consecutive nodes from one Philox4x32-10 call.  The
-// inverse CDF is the count of CDF entries <= u (the CDF is non-decreasing, so that count is the
-// first k with u < c_k; d (none) -> the last k with p_k > 0); the 4 device bytes leave as one
-// 32-bit store when the placement row is 4-byte aligned.
+constexpr int SBG = 16;
 __global__ void __launch_bounds__(ST) k_sample(const float *__restrict__ cdf, const float *__restrict__ logp,
                                                const int *__restrict__ lastpos, const int *__restrict__ leader,
-                                               int has_coloc, int N, int d, uint64_t seed, uint64_t offset,
+                                               int has_coloc, int N, int d, int B, uint64_t seed, uint64_t offset,
                                                uint64_t step_val, const uint64_t *step_ptr, uint8_t *D,
-                                               float *logprob) {
+                                               double *part, int nwc) {
   const uint64_t step = step_ptr ? *step_ptr : step_val;   // device counter: graph replays advance it
-  __shared__ double red[ST / 32];
-  const int b = blockIdx.x;
-  const uint64_t gidx = offset + (uint64_t)b;
   const uint2 key = make_uint2((unsigned)(seed & 0xffffffffu), (unsigned)(seed >> 32));
-  double acc = 0.0;
-  const int nq = (N + 3) >> 2;
-  uint8_t *Db = D + (size_t)b * N;
-  const bool aligned = ((N & 3) == 0);
-  for (int q = threadIdx.x; q < nq; q += ST) {
-    const uint4 w = philox4x32_10(make_uint4((unsigned)q, (unsigned)(gidx & 0xffffffffu),
-                                             (unsigned)(step & 0xffffffffu), (unsigned)(gidx >> 32)),
-                                  key);
-    const unsigned ws[4] = {w.x, w.y, w.z, w.w};
-    unsigned packed = 0;
+  const int q = blockIdx.x * ST + threadIdx.x, lane = threadIdx.x & 31;
+  const int wc = q >> 5;                                   // warp chunk (128 nodes)
+  float c[4][kMaxD], lp[4][kMaxD];
+  int last[4];
+  bool lead[4];
 #pragma unroll
-    for (int j = 0; j < 4; j++) {
-      const int v = 4 * q + j;
-      if (v < N) {
-        const float u = (float)(ws[j] >> 8) * 5.9604644775390625e-08f;  // 2^-24
-        const float *cv = cdf + (size_t)v * d;
-        int k = 0;
-        if (d == 8) {
-          const float4 c0 = __ldg(reinterpret_cast<const float4 *>(cv)), c1 = __ldg(reinterpret_cast<const float4 *>(cv) + 1);
-          k = (c0.x <= u) + (c0.y <= u) + (c0.z <= u) + (c0.w <= u) + (c1.x <= u) + (c1.y <= u) + (c1.z <= u) +
-              (c1.w <= u);
-        } else {
-          for (int t = 0; t < d; t++) k += (__ldg(cv + t) <= u);
-        }
-        if (k >= d) k = __ldg(lastpos + v);
-        packed |= (unsigned)k << (8 * j);
-        if (!has_coloc || __ldg(leader + v) == v) acc += (double)__ldg(logp + (size_t)v * d + k);
-      }
+  for (int j = 0; j < 4; j++) {
+    const int v = 4 * q + j;
+    const bool ok = v < N;
+#pragma unroll
+    for (int t = 0; t < kMaxD; t++) {
+      c[j][t] = (ok && t < d) ? __ldg(cdf + (size_t)v * d + t) : __int_as_float(0x7f800000);
+      lp[j][t] = (ok && t < d) ? __ldg(logp + (size_t)v * d + t) : 0.f;
     }
-    if (aligned) *reinterpret_cast<unsigned *>(Db + 4 * q) = packed;
-    else
-      for (int j = 0; j < 4 && 4 * q + j < N; j++) Db[4 * q + j] = (uint8_t)(packed >> (8 * j));
+    last[j] = ok ? __ldg(lastpos + v) : 0;
+    lead[j] = ok && (!has_coloc || __ldg(leader + v) == v);
   }
-  // fixed-order block reduction
+  const bool any = 4 * q < N;
+  const bool aligned = ((N & 3) == 0) && 4 * q + 3 < N;
+  const int b1 = min(B, (int)(blockIdx.y + 1) * SBG);
+  for (int b = blockIdx.y * SBG; b < b1; b++) {
+    const uint64_t gidx = offset + (uint64_t)b;
+    double acc = 0.0;
+    if (any) {
+      const uint4 w = philox4x32_10(make_uint4((unsigned)q, (unsigned)(gidx & 0xffffffffu),
+                                               (unsigned)(step & 0xffffffffu), (unsigned)(gidx >> 32)),
+                                    key);
+      const unsigned ws[4] = {w.x, w.y, w.z, w.w};
+      unsigned packed = 0;
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double s = 0.0;
-    for (int i = 0; i < ST / 32; i++) s += red[i];
-    logprob[b] = (float)s;
+      for (int j = 0; j < 4; j++) {
+        const float u = (float)(ws[j] >> 8) * 5.9604644775390625e-08f;  // 2^-24
+        int k = 0;
+#pragma unroll
+        for (int t = 0; t < kMaxD; t++) k += (c[j][t] <= u);
+        if (k >= d) k = last[j];
+        float l = 0.f;
+#pragma unroll
+        for (int t = 0; t < kMaxD; t++) l = (t == k) ? lp[j][t] : l;
+        if (lead[j]) acc += (double)l;
+        packed |= (unsigned)k << (8 * j);
+      }
+      uint8_t *Db = D + (size_t)b * N;
+      if (aligned) *reinterpret_cast<unsigned *>(Db + 4 * q) = packed;
+      else
+        for (int j = 0; j < 4 && 4 * q + j < N; j++) Db[4 * q + j] = (uint8_t)(packed >> (8 * j));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0 && wc < nwc) part[(size_t)b * nwc + wc] = acc;
   }
+}
+
+// log pi_b = sum of the warp chunks' partial sums in chunk order
+__global__ void k_sample_lp(const double *__restrict__ part, int nwc, int B, float *logprob) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  double s = 0.0;
+  for (int i = 0; i < nwc; i++) s += part[(size_t)b * nwc + i];
+  logprob[b] = (float)s;
 }
 __global__ void k_colocate(const int *leader, int N, int B, uint8_t *D) {
   size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -216,12 +235,15 @@ __global__ void k_logit_fin(const float *__restrict__ logits, int ld, const int 
 
 void launch_sample(const float *logits, int ld, const int *leader, bool has_coloc, int N, int d, int B, uint64_t seed,
                    uint64_t offset, uint64_t step, const uint64_t *step_ptr, float *cdf, float *logp, int *lastpos,
-                   uint8_t *D, float *logprob, cudaStream_t s) {
+                   double *spart, uint8_t *D, float *logprob, cudaStream_t s) {
   note_launch("k_node_prep", s);
   k_node_prep<<<(N + 255) / 256, 256, 0, s>>>(logits, ld, N, d, cdf, logp, lastpos);
-  note_launch("k_sample", s, (double)B * N + 4.0 * (double)N * (2 * d + 1));
-  k_sample<<<B, ST, 0, s>>>(cdf, logp, lastpos, leader, has_coloc ? 1 : 0, N, d, seed, offset, step, step_ptr, D,
-                            logprob);
+  const int nq = (N + 3) / 4, nchunk = (nq + ST - 1) / ST, nwc = nchunk * (ST / 32);
+  note_launch("k_sample", s, (double)B * N + 4.0 * (double)N * (2 * d + 2) + 8.0 * B * nwc);
+  k_sample<<<dim3(nchunk, (B + SBG - 1) / SBG), ST, 0, s>>>(cdf, logp, lastpos, leader, has_coloc ? 1 : 0, N, d, B,
+                                                            seed, offset, step, step_ptr, D, spart, nwc);
+  note_launch("k_sample_lp", s, 8.0 * B * nwc + 4.0 * B);
+  k_sample_lp<<<(B + 127) / 128, 128, 0, s>>>(spart, nwc, B, logprob);
   if (has_coloc) {
     size_t n = (size_t)N * B;
     note_launch("k_colocate", s);
