@@ -270,6 +270,13 @@ gdp_status gdp_cost(gdp_graph g, gdp_topo t, const uint8_t *placements, int32_t 
  * model").  Returns 0 and sets the error for NULL handles. */
 int32_t gdp_cost_kernel(gdp_graph g, gdp_topo t);
 
+/* Diagnostic: placements the default cost kernel (5) runs at once on the current device --
+ * resident CTAs per SM (shared memory per placement grows with the ops' input counters) times
+ * the SMs.  A batch of that many placements costs about as long as one placement (the launch
+ * time is one placement's simulation latency); bench.py sizes its batch with it.  0 if kernel 5
+ * does not apply or for NULL handles. */
+int32_t gdp_cost_wave(gdp_graph g, gdp_topo t);
+
 /* Diagnostic (tests): the table of intermediates that gdp_embed / gdp_place / gdp_policy_grad
  * save in the workspace, as (name, byte offset from ws, rows, cols, is_int32) -- fp32 unless
  * is_int32.  GNN tensors (H0..H3, Z0..Z2, A0..A2 = max-pooled neighbourhoods, ARG0..ARG2 =

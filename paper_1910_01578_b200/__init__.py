@@ -24,7 +24,7 @@ STATUS = {0: "GDP_OK", 1: "GDP_ERR_ARG", 2: "GDP_ERR_GRAPH", 3: "GDP_ERR_CYCLE",
 P_COUNT = 90
 REPORT_BYTES = 24
 
-EXPORTS = ["gdp_default_config", "gdp_last_error", "gdp_launch_count", "gdp_build_info", "gdp_cost_kernel", "gdp_logprob", "gdp_clip_adam", "gdp_sample_at", "gdp_greedy", "gdp_graph_validate", "gdp_graph_create", "gdp_graph_destroy",
+EXPORTS = ["gdp_default_config", "gdp_last_error", "gdp_launch_count", "gdp_build_info", "gdp_cost_kernel", "gdp_cost_wave", "gdp_logprob", "gdp_clip_adam", "gdp_sample_at", "gdp_greedy", "gdp_graph_validate", "gdp_graph_create", "gdp_graph_destroy",
            "gdp_topo_create", "gdp_topo_destroy", "gdp_param_layout", "gdp_workspace_size", "gdp_embed",
            "gdp_place", "gdp_sample", "gdp_cost", "gdp_cost_with_kernel", "gdp_debug_tensors", "gdp_grad_check", "gdp_grad_buckets", "gdp_policy_grad_bucketed", "gdp_grad_sum", "gdp_advantage", "gdp_policy_grad", "gdp_profile_enable",
            "gdp_profile_mark", "gdp_profile_read"]
@@ -70,6 +70,7 @@ def lib():
             "gdp_cost_with_kernel": [P, P, P, I32, P, P, P, P, P, SZ, I32, P],
             "gdp_debug_tensors": [P, P, I32, ctypes.POINTER(ctypes.c_char_p), P, P, P, P],
             "gdp_grad_check": [P, P, I32, P, P],
+            "gdp_cost_wave": [P, P],
             "gdp_grad_buckets": [P, I32, P, P],
             "gdp_policy_grad_bucketed": [P, P, P, P, P, I32, P, P, P, F32, F32, F32, P, P, SZ, P, P],
             "gdp_grad_sum": [P, I32, I64, P, P],
@@ -274,6 +275,11 @@ def cost_kernel(g: Graph, t: Topo) -> int:
     if k == 0:
         raise RuntimeError("gdp_cost_kernel: " + last_error())
     return k
+
+
+def cost_wave(g: Graph, t: Topo) -> int:
+    """Placements k_cost5 runs at once (resident CTAs per SM x SMs); 0 if it does not apply."""
+    return int(lib().gdp_cost_wave(g.h, t.h))
 
 
 def gdp_cost(g: Graph, t: Topo, placements, B: int, rep, peak_mem, busy, reward, ws, stream=None, kernel: int = 0):

@@ -325,6 +325,11 @@ int32_t gdp_profile_read(int32_t max_names, const char **names, int32_t *launche
 
 const char *gdp_build_info(void) { return "libgdp sm_100a built " __DATE__ " " __TIME__; }
 
+int32_t gdp_cost_wave(gdp_graph g, gdp_topo t) {
+  if (!g || !t) { set_error("gdp_cost_wave: NULL handle"); return 0; }
+  return cost_wave(g, t);
+}
+
 int32_t gdp_cost_kernel(gdp_graph g, gdp_topo t) {
   if (!g || !t) { set_error("gdp_cost_kernel: NULL handle"); return 0; }
   return cost_kernel_choice(g, t, 0);

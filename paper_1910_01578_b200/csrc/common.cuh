@@ -250,6 +250,7 @@ void launch_clip_adam(const float *g, long long n, double max_norm, double lr, d
 // kernel gdp_cost runs (5, 3 or 1); `force` != 0 asks whether that kernel applies (it is
 // returned if so, else the automatic choice)
 int cost_kernel_choice(const gdp_graph_s *g, const gdp_topo_s *t, int force);
+int cost_wave(const gdp_graph_s *g, const gdp_topo_s *t);   // placements per full wave of k_cost5 (0: n/a)
 gdp_status launch_cost(const gdp_graph_s *g, const gdp_topo_s *t, const uint8_t *D, int B,
                        gdp_sim_report *rep, long long *peak, long long *busy, double *reward, const WS &w,
                        int force, cudaStream_t s);

@@ -460,6 +460,10 @@ int cost_kernel_choice(const gdp_graph_s *g, const gdp_topo_s *t, int force) {
   return ok5 ? 5 : (ok3 ? 3 : 1);
 }
 
+int cost_wave(const gdp_graph_s *g, const gdp_topo_s *t) {
+  return cost_kernel_choice(g, t, 0) == 5 ? cost5_wave(cost5_graph(g)) : 0;
+}
+
 gdp_status launch_cost(const gdp_graph_s *g, const gdp_topo_s *t, const uint8_t *D, int B, gdp_sim_report *rep,
                        long long *peak, long long *busy, double *reward, const WS &w, int force, cudaStream_t s) {
   const TopoArgs T = topo_args(t);

@@ -35,7 +35,7 @@ struct Cost2Graph {
 struct __align__(16) Q5 {     // an op in a queue (channel ring, FIFO, available list), 32 bytes
   int id, cost, ob, nn;       // id, compute cost, first out-edge slot, out-degree | in-degree << 16
   int cinfo;                  // input counter: kind (bits 0-1: 0 = at most one input, 1 = two inputs
-                              // (flag bit), 2 = byte counter, 3 = global counter) | index << 2
+                              // (flag bit), 2 = 4-bit counter (3..15 inputs), 3 = global counter) | index << 2
   int ib;                     // first in-edge slot
   int arr, u;                 // channel entries: arrival tick and producer id
 };
@@ -48,7 +48,7 @@ struct Cost5Host {            // host images built at graph creation (cost5_buil
   std::vector<Slot5> slots;
   std::vector<Q5> srcq;        // the sources, ascending id
   std::vector<int> gbig, outdeg;
-  std::vector<unsigned> bigb;  // byte counters (in-degree 3..254), 4 per word, 16-byte padded
+  std::vector<unsigned> bigb;  // 4-bit counters (in-degree 3..15), 8 per word, 16-byte padded
   int nflagw = 0;              // words of the two-input flag bitmap
 };
 struct Cost5Graph {
@@ -67,6 +67,7 @@ gdp_status cost5_build(int N, long long E, const int *optr, const int *oidx, con
                        const long long *out_bytes, Cost5Host *h);
 size_t cost5_smem_bytes(int nflagw, int nbigb);
 size_t cost5_scratch_per_placement(int N, long long E, int ngbig);
+int cost5_wave(const Cost5Graph &G);
 bool cost5_eligible(const TopoArgs &T, const Cost5Graph &G, int min_cost, long long min_edge_bytes);
 bool launch_cost5(const Cost5Graph &G, const TopoArgs &T, int min_cost, long long min_edge_bytes, const uint8_t *D,
                   int B, unsigned char *scratch, size_t per_place, gdp_sim_report *rep, long long *peak,

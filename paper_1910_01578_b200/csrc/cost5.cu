@@ -25,12 +25,12 @@
 //    an instant, the oracle's step (4)).
 //  * Per-op state in shared memory is only the input counters: ops with one input need none,
 //    ops with exactly two inputs one "first input arrived" bit (a compact bitmap), ops with
-//    3..254 inputs a byte counter, more a global counter (C4: 9.7 KB).  Device ids are not in
+//    3..15 inputs a 4-bit counter, more a global counter (C4: 6.9 KB).  Device ids are not in
 //    shared memory: a finishing op's consumers' devices come with its staged out-edge records
 //    (a per-placement byte per out-edge slot that k_cost5_pre writes), the memory warp reads the
 //    placement row from L2.  Static memory, busy time, channel sizes and the co-location check
-//    also come from k_cost5_pre (one CTA per placement, fully parallel).  With ~27 KB of shared
-//    memory per placement, eight CTAs (placements) share an SM at C4.
+//    also come from k_cost5_pre (one CTA per placement, fully parallel).  With 24 KB of shared
+//    memory per placement, nine CTAs (placements) share an SM at C4.
 // Requires (host-checked): every duration >= 1 and every transfer >= 1 tick (no same-instant
 // rounds), N and E < 2^25, degrees < 2^16.  Otherwise gdp_cost runs k_cost3 / k_cost (cost2.cu,
 // cost.cu).
@@ -47,10 +47,29 @@ namespace {
 using namespace cu;
 
 constexpr int KC5 = 4;      // channel entries kept in shared memory per channel (power of 2)
-constexpr int KF5 = 4;      // FIFO entries kept in shared memory per device (power of 2)
-constexpr int SO5 = 8;      // staged out-edge records per slot
-constexpr int NINC5 = 2;    // ops made available at one instant kept in shared memory per device
-constexpr int RI5 = 128;    // memory item ring (power of 2)
+#ifndef COST5_KF
+#define COST5_KF 4
+#endif
+#ifndef COST5_SO
+#define COST5_SO 8
+#endif
+#ifndef COST5_NINC
+#define COST5_NINC 2
+#endif
+constexpr int KF5 = COST5_KF;       // FIFO entries kept in shared memory per device (power of 2)
+constexpr int SO5 = COST5_SO;       // staged out-edge records per slot (more: read from global at the finish)
+constexpr int NINC5 = COST5_NINC;   // ops made available at one instant kept in shared memory per device
+#ifndef COST5_RI
+#define COST5_RI 128
+#endif
+#ifndef COST5_MB
+#define COST5_MB 32
+#endif
+#ifndef COST5_SLEEP
+#define COST5_SLEEP 1000
+#endif
+constexpr int RI5 = COST5_RI;       // memory item ring (power of 2)
+constexpr int MB5 = COST5_MB;       // the memory warp waits for this many items (or the end) before a batch
 
 #ifdef COST5_PROF   // per-phase cycle totals of the simulation warp (lane 0), printed by block 0
 #define P5(i)                                              \
@@ -81,19 +100,28 @@ struct Pre5 {   // per-placement results of k_cost5_pre
   int pad[3];
 };
 
+constexpr int NCH = 56;     // directed channels src != dst, compact index 7 src + dst - (dst > src)
+__host__ __device__ __forceinline__ int cidx(int src, int dst) { return 7 * src + dst - (dst > src ? 1 : 0); }
+__device__ __forceinline__ int cdst(int ci) {
+  const int s = ci / 7, r = ci - 7 * s;
+  return r + (r >= s ? 1 : 0);
+}
+
 struct Smem5 {
-  Q5 cc[64][KC5];                   // channel rings (arr, u set), c = 8 * src + dst
+  Q5 cc[NCH][KC5];                  // channel rings (arr, u set)
   Slot5 stage[8][2][SO5];           // out-edge slots of the running / next op of each device
   unsigned sdev[8][2][SO5];         // the 4 bytes of the placement's slot-device array holding each slot's
   Q5 fc[8][KF5];                    // FIFO rings
   Q5 inc[8][NINC5];                 // ops made available at this instant
   unsigned long long items[RI5];    // memory items: t | code << 32
   Q5 drun[8];                       // the op running on each device
-  int cfree[64], ctail[64], chead[64], coff[64];
-  int ca[64];                       // arrival time of each channel's head entry (INF: empty)
-  int dfin[8];                      // finish of each device's running op (INF: idle)
-  int fh[8], ft[8], cur[8], nxt[8]; // FIFO head / tail, staging slot of the running op, op staged in the other
-  int inc_n[8], doff[8];
+  int4 ch[NCH];                     // per channel: tail, free (transfer end), head
+  int ca[NCH];                      // arrival tick of each channel's head entry (INF: empty; contiguous: the
+                                    // next-event REDUX reads two per lane without bank conflicts)
+  int coff[NCH];
+  int4 dv[8];                       // per device: finish of the running op (INF: idle), FIFO head, tail, #available now
+  int4 dv2[8];                      // per device: staging slot of the running op, op staged in the other, speed
+  int doff[8];
   int mhead;                        // items consumed by the memory warp
   int mk, disp, oom;
 };
@@ -166,8 +194,8 @@ __device__ __forceinline__ bool arrive5(unsigned flag_s, unsigned bigb_s, int *g
     return (atoms_xor(flag_s + 4u * (unsigned)(ix >> 5), bit) & bit) != 0u;
   }
   if (kind == 2) {
-    const int sh = (ix & 3) * 8;
-    return ((atoms_add(bigb_s + 4u * (unsigned)(ix >> 2), 0u - (1u << sh)) >> sh) & 255u) == 1u;
+    const int sh = (ix & 7) * 4;
+    return ((atoms_add(bigb_s + 4u * (unsigned)(ix >> 3), 0u - (1u << sh)) >> sh) & 15u) == 1u;
   }
   return atomicSub(&gbig[ix], 1) == 1;
 }
@@ -295,14 +323,16 @@ __global__ void __launch_bounds__(64) k_cost5(Cost5Graph G, TopoArgs T, const ui
     for (int i = tid; i < G.nflagw; i += 64) flags[i] = 0u;
     for (int i = tid; i < G.nbigb; i += 64) bigb[i] = G.bigb0[i];
     for (int i = tid; i < RI5; i += 64) S.items[i] = 1ull << 32;   // lap parity 1: empty for lap 0
-    S.cfree[tid] = 0; S.ctail[tid] = 0; S.chead[tid] = 0;
-    if (tid < 8) S.inc_n[tid] = 0;
+    if (tid < NCH) { S.ch[tid] = make_int4(0, 0, 0, 0); S.ca[tid] = INF; }
+    if (tid < 8) { S.dv[tid] = make_int4(INF, 0, 0, 0); S.dv2[tid] = make_int4(0, -1, T.speed[tid], 0); }
     if (tid == 0) { S.mhead = 0; S.mk = 0; S.disp = 0; S.oom = 0; }
     if (tid == 32) {
       int o = 0;
       for (int k = 0; k < 8; k++) { S.doff[k] = o; o += pre->opcnt[k]; }
       o = 0;
-      for (int c = 0; c < 64; c++) { S.coff[c] = o; o += pre->chcnt[c]; }
+      for (int a = 0; a < 8; a++)
+        for (int b2 = 0; b2 < 8; b2++)
+          if (a != b2) { S.coff[cidx(a, b2)] = o; o += pre->chcnt[8 * a + b2]; }
     }
   }
   const int pflag = pre->flag;
@@ -349,10 +379,10 @@ __global__ void __launch_bounds__(64) k_cost5(Cost5Graph G, TopoArgs T, const ui
       itail++;
     };
     auto to_inc = [&](int q, const Q5 &r) {       // uniform
-      const int n = S.inc_n[q];
+      const int n = S.dv[q].w;
       if (n < NINC5) store_q5(&S.inc[q][n], r);
       else store_q5(ov_g + S.doff[q] + n, r);
-      S.inc_n[q] = n + 1;
+      S.dv[q].w = n + 1;
       incm |= 1u << q;
     };
     // uniform input arrival (no other lane touches the counters concurrently)
@@ -366,10 +396,10 @@ __global__ void __launch_bounds__(64) k_cost5(Cost5Graph G, TopoArgs T, const ui
         return (w & bit) != 0u;
       }
       if (kind == 2) {
-        const int sh = (ix & 3) * 8;
-        const unsigned w = bigb[ix >> 2];
-        bigb[ix >> 2] = w - (1u << sh);
-        return ((w >> sh) & 255u) == 1u;
+        const int sh = (ix & 7) * 4;
+        const unsigned w = bigb[ix >> 3];
+        bigb[ix >> 3] = w - (1u << sh);
+        return ((w >> sh) & 15u) == 1u;
       }
       const int o = gbig[ix];
       gbig[ix] = o - 1;
@@ -386,24 +416,23 @@ __global__ void __launch_bounds__(64) k_cost5(Cost5Graph G, TopoArgs T, const ui
       cp_commit();
     };
 
-    if (lane < 64 - 32) { S.ca[lane] = INF; S.ca[lane + 32] = INF; }
-    if (lane < 8) { S.dfin[lane] = INF; S.cur[lane] = 0; S.nxt[lane] = -1; S.fh[lane] = 0; S.ft[lane] = 0; }
     __syncwarp();
     // sources are available at t = 0: appended to their FIFO in ascending id (uniform)
     for (int i = 0; i < G.nsrc; i++) {
       Q5 r;
       load_q5(r, G.srcq + i);
       const int q = D[r.id];
-      const int f = S.ft[q];
+      const int f = S.dv[q].z;
       if (f < KF5) store_q5(&S.fc[q][f], r);
       else store_q5(fifo_g + S.doff[q] + f, r);
-      S.ft[q] = f + 1;
+      S.dv[q].z = f + 1;
     }
     unsigned att = (1u << d) - 1u;   // devices to dispatch at t = 0
     for (bool first = true;; first = false) {
       if (!first) {
         // ---------------------------------------------------------- next instant
-        const int ca0 = S.ca[2 * lane], ca1 = S.ca[2 * lane + 1], df = lane < 8 ? S.dfin[lane] : INF;
+        const int ca0 = lane < NCH / 2 ? S.ca[2 * lane] : INF, ca1 = lane < NCH / 2 ? S.ca[2 * lane + 1] : INF;
+        const int df = lane < 8 ? S.dv[lane].x : INF;
         t = (int)__reduce_min_sync(FULL, (unsigned)min(min(ca0, ca1), df));
         if (t == INF) break;
         const unsigned e0 = __ballot_sync(FULL, ca0 == t), e1 = __ballot_sync(FULL, ca1 == t);
@@ -415,18 +444,19 @@ __global__ void __launch_bounds__(64) k_cost5(Cost5Graph G, TopoArgs T, const ui
           int c;
           if (m0) { c = 2 * (__ffs(m0) - 1); m0 &= m0 - 1; }
           else { c = 2 * (__ffs(m1) - 1) + 1; m1 &= m1 - 1; }
-          const int h = S.chead[c], tail = S.ctail[c], s = h & (KC5 - 1);
+          const int4 cs = S.ch[c];
+          const int h = cs.z, tail = cs.x, s = h & (KC5 - 1), q = cdst(c);
           Q5 r;
           load_q5(r, &S.cc[c][s]);
-          S.chead[c] = h + 1;
+          S.ch[c].z = h + 1;
           if (h + KC5 < tail) {   // the slot takes position h + KC5 from the global overflow (rare)
             Q5 x;
             load_q5(x, chq_g + S.coff[c] + h + KC5);
             store_q5(&S.cc[c][s], x);
           }
           S.ca[c] = h + 1 < tail ? S.cc[c][(h + 1) & (KC5 - 1)].arr : INF;
-          item(IT_ALLOC_COPY, c & 7, r.u);
-          if (arrive_u(r.cinfo)) to_inc(c & 7, r);
+          item(IT_ALLOC_COPY, q, r.u);
+          if (arrive_u(r.cinfo)) to_inc(q, r);
         }
         P5(1);
         // ---------------------------------------------------------- (2) ops finishing now, ascending id
@@ -444,8 +474,8 @@ __global__ void __launch_bounds__(64) k_cost5(Cost5Graph G, TopoArgs T, const ui
           ef &= ~(1u << k);
           Q5 r;
           load_q5(r, &S.drun[k]);
-          const int sl = S.cur[k];
-          S.dfin[k] = INF;
+          const int sl = S.dv2[k].x;
+          S.dv[k].x = INF;
           const int nout = r.nn & 0xffff, nin = (int)((unsigned)r.nn >> 16);
           for (int j0 = 0; j0 < nin; j0 += 32) {   // frees of this finish -> memory warp, one item per lane
             const int n = min(32, nin - j0);
@@ -474,31 +504,31 @@ __global__ void __launch_bounds__(64) k_cost5(Cost5Graph G, TopoArgs T, const ui
             const unsigned am = __ballot_sync(FULL, av);
             const unsigned cm = __ballot_sync(FULL, cross);
             if (am) {   // ops made available now on device k, in lane (= id) order
-              const int n0 = S.inc_n[k];
+              const int n0 = S.dv[k].w;
               if (av) {
                 const int pos = n0 + __popc(am & lt);
                 if (pos < NINC5) store_q5(&S.inc[k][pos], q_of_slot(e, 0, r.id));
                 else store_q5(ov_g + S.doff[k] + pos, q_of_slot(e, 0, r.id));
               }
               __syncwarp();
-              S.inc_n[k] = n0 + __popc(am);
+              S.dv[k].w = n0 + __popc(am);
               incm |= 1u << k;
             }
             if (cm) {   // FIFO pushes on the directed channels k -> tw, ranked within each channel
               const unsigned grp = (cm & (cm - 1)) ? __match_any_sync(FULL, cross ? tw : -1) : cm;
               if (cross) {
                 const int rank = __popc(grp & lt), n = __popc(grp);
-                const int c = 8 * k + tw;
-                const int f = S.cfree[c], tail = S.ctail[c], hd = S.chead[c];
-                const int x = xfer_time3(e.bytes, c, T);
+                const int c = cidx(k, tw);
+                const int4 cs = S.ch[c];
+                const int tail = cs.x, f = cs.y, hd = cs.z;
+                const int x = xfer_time3(e.bytes, 8 * k + tw, T);
                 const int bt = max(t, f);
                 const int pos = tail + rank, arr = bt + (rank + 1) * x;
                 const Q5 q = q_of_slot(e, arr, r.id);
                 if (pos < hd + KC5) store_q5(&S.cc[c][pos & (KC5 - 1)], q);
                 else store_q5(chq_g + S.coff[c] + pos, q);
                 if (rank == 0) {
-                  S.cfree[c] = bt + n * x;
-                  S.ctail[c] = tail + n;
+                  *reinterpret_cast<int2 *>(&S.ch[c]) = make_int2(tail + n, bt + n * x);   // tail, free
                   if (tail == hd) S.ca[c] = bt + x;   // the channel was empty: a new head
                 }
               }
@@ -511,12 +541,13 @@ __global__ void __launch_bounds__(64) k_cost5(Cost5Graph G, TopoArgs T, const ui
       // ---------------------------------------------------------- (3) FIFO append + dispatch
       for (att |= incm, incm = 0; att; att &= att - 1) {
         const int k = __ffs(att) - 1;
-        const int n = S.inc_n[k];
-        bool running = S.dfin[k] != INF, go = false;
-        int fh = S.fh[k], ft = S.ft[k];
+        const int4 dvk = S.dv[k], dv2k = S.dv2[k];
+        const int n = dvk.w;
+        bool running = dvk.x != INF, go = false;
+        int fh = dvk.y, ft = dvk.z;
         Q5 run;
         if (n > 0) {
-          S.inc_n[k] = 0;
+          S.dv[k].w = 0;
           Q5 *Li = &S.inc[k][0];
           Q5 *Lo = ov_g + S.doff[k];
           if (n == 1 && !running && fh == ft) {   // common case: straight to dispatch
@@ -542,7 +573,7 @@ __global__ void __launch_bounds__(64) k_cost5(Cost5Graph G, TopoArgs T, const ui
               if (ft < fh + KF5) store_q5(&S.fc[k][ft & (KF5 - 1)], x);
               else store_q5(fifo_g + S.doff[k] + ft, x);
             }
-            S.ft[k] = ft;
+            S.dv[k].z = ft;
           }
         }
         if (!go && !running && fh < ft) {   // pop the FIFO head
@@ -553,30 +584,29 @@ __global__ void __launch_bounds__(64) k_cost5(Cost5Graph G, TopoArgs T, const ui
             load_q5(x, fifo_g + S.doff[k] + fh + KF5);
             store_q5(&S.fc[k][s], x);
           }
-          S.fh[k] = ++fh;
+          S.dv[k].y = ++fh;
           go = true;
         }
-        int cur = S.cur[k];
+        int cur = dv2k.x, nxt = dv2k.y;
         if (go) {
-          const int fin = t + run.cost * T.speed[k];
-          S.dfin[k] = fin;
+          const int fin = t + run.cost * dv2k.z;
+          S.dv[k].x = fin;
           store_q5(&S.drun[k], run);
           mk = max(mk, fin);
           disp++;
           item(IT_ALLOC_OP, k, run.id);
           cur ^= 1;   // the slot the head was staged into, or the one it is staged into now
-          S.cur[k] = cur;
-          const int staged = S.nxt[k];
-          S.nxt[k] = -1;
-          if (run.id != staged && (run.nn & 0xffff)) stage(k, cur, run);
+          if (run.id != nxt && (run.nn & 0xffff)) stage(k, cur, run);
+          nxt = -1;
           running = true;
         }
-        if (running && fh < ft && S.nxt[k] < 0) {   // stage the op now waiting at the head
+        if (running && fh < ft && nxt < 0) {   // stage the op now waiting at the head
           Q5 hr;
           load_q5(hr, &S.fc[k][fh & (KF5 - 1)]);
-          S.nxt[k] = hr.id;
+          nxt = hr.id;
           if (hr.nn & 0xffff) stage(k, cur ^ 1, hr);
         }
+        *reinterpret_cast<int2 *>(&S.dv2[k]) = make_int2(cur, nxt);
       }
       __syncwarp();
       P5(3);
@@ -609,14 +639,14 @@ __global__ void __launch_bounds__(64) k_cost5(Cost5Graph G, TopoArgs T, const ui
       const bool valid = (code & 1u) == ((pos / RI5) & 1u);
       const unsigned vm = __ballot_sync(FULL, valid);
       const int n = vm == FULL ? 32 : __ffs(~vm) - 1;
-      if (n < 32 && !__any_sync(FULL, valid && kind_end(it))) {
-        // wait for a full batch unless the simulation has ended: few, large batches leave the
-        // issue slots to the simulation warps
+      if (n < MB5 && !__any_sync(FULL, valid && kind_end(it))) {
+        // wait for a batch of MB5 items unless the simulation has ended: few, large batches
+        // leave the issue slots to the simulation warps
         if (n == 0 || ++nwait < 4) {
 #ifdef COST5_PROF
           nidle++;
 #endif
-          __nanosleep(1000);
+          __nanosleep(COST5_SLEEP);
           continue;
         }
       }
@@ -716,6 +746,19 @@ bool cost5_eligible(const TopoArgs &T, const Cost5Graph &G, int min_cost, long l
   return sizeof(Smem5) + cost5_smem_bytes(G.nflagw, G.nbigb) <= 227 * 1024;
 }
 
+// placements that run at once: resident k_cost5 CTAs per SM x SMs (0 if not eligible)
+int cost5_wave(const Cost5Graph &G) {
+  const size_t smem = cost5_smem_bytes(G.nflagw, G.nbigb);
+  if (sizeof(Smem5) + smem > 227 * 1024) return 0;
+  if (smem + sizeof(Smem5) > 48 * 1024)
+    cudaFuncSetAttribute(k_cost5, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int occ = 0, dev = 0, nsm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_cost5, 64, smem) != cudaSuccess) return 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  return occ * nsm;
+}
+
 bool launch_cost5(const Cost5Graph &G, const TopoArgs &T, int min_cost, long long min_edge_bytes, const uint8_t *D,
                   int B, unsigned char *scratch, size_t per_place, gdp_sim_report *rep, long long *peak,
                   long long *busy, double *reward, cudaStream_t s) {
@@ -745,7 +788,7 @@ gdp_status cost5_build(int N, long long E, const int *optr, const int *oidx, con
   h->outdeg.assign(N, 0);
   std::vector<Q5> q(N);
   int nb = 0, nf = 0;
-  std::vector<unsigned char> bytes;
+  std::vector<unsigned char> nibs;
   for (int v = 0; v < N; v++) {
     const int din = iptr[v + 1] - iptr[v], dout = optr[v + 1] - optr[v];
     if (din >= 65536 || dout >= 65536) h->ok = false;
@@ -754,7 +797,7 @@ gdp_status cost5_build(int N, long long E, const int *optr, const int *oidx, con
     r.nn = (dout & 0xffff) | ((din & 0xffff) << 16);
     if (din <= 1) r.cinfo = 0;
     else if (din == 2) r.cinfo = 1 | (nf++ << 2);
-    else if (din < 255) { r.cinfo = 2 | (nb << 2); bytes.push_back((unsigned char)din); nb++; }
+    else if (din <= 15) { r.cinfo = 2 | (nb << 2); nibs.push_back((unsigned char)din); nb++; }
     else { r.cinfo = 3 | ((int)h->gbig.size() << 2); h->gbig.push_back(din); }
     if (din == 0) h->srcq.push_back(r);
     h->outdeg[v] = dout;
@@ -767,9 +810,9 @@ gdp_status cost5_build(int N, long long E, const int *optr, const int *oidx, con
       s.bytes = out_bytes[v];   // the producer's output: the size of the copy on this edge
     }
   h->nflagw = (nf + 31) / 32;
-  while (bytes.size() % 16) bytes.push_back(0);
-  h->bigb.assign(bytes.size() / 4, 0u);
-  for (size_t i = 0; i < bytes.size(); i++) h->bigb[i / 4] |= (unsigned)bytes[i] << (8 * (i % 4));
+  while (nibs.size() % 32) nibs.push_back(0);
+  h->bigb.assign(nibs.size() / 8, 0u);
+  for (size_t i = 0; i < nibs.size(); i++) h->bigb[i / 8] |= (unsigned)nibs[i] << (4 * (i % 8));
   return GDP_OK;
 }
 

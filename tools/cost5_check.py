@@ -52,7 +52,12 @@ ok &= check("c2 d=1", W.graphs[0], 1, 4)
 g4 = workloads.config("c4").graphs[0]
 ok &= check("c4", g4, 8, 32)
 ok &= check("c4 d=3", g4, 3, 16, seed=5)
-for B in (296, 592, 888, 1184):
+G4 = gdp.Graph(g4, workloads.features(g4)); T4 = gdp.Topo(workloads.topology(g4, 8))
+print("cost wave (placements at once):", gdp.cost_wave(G4, T4), flush=True)
+W64 = workloads.config("c4_64k"); g64 = W64.graphs[0]
+print("c4_64k wave:", gdp.cost_wave(gdp.Graph(g64, workloads.features(g64)), gdp.Topo(workloads.topology(g64, 8))), flush=True)
+ok &= check("c4_64k", g64, 8, 16)
+for B in (296, 1332):
     D = np.random.default_rng(1).integers(0, 8, size=(B, g4.N)).astype(np.uint8)
     k, r, pk, bz, rw, args = run(g4, workloads.topology(g4, 8), D, 8)
     G, T, Dg, rep, peak, busy, rew, ws = args
