@@ -79,6 +79,13 @@ typedef struct {
   int32_t active_devices; /* mixed device counts: the head has num_devices (D_max)
                              outputs, sampling / log pi / greedy / the loss use the first
                              active_devices (the rest masked to -inf, zero gradient); 0 = all */
+  int32_t autoregressive; /* SURVEY NEXT-4 / SPEC.md:562, reading R35: 1 = the
+                             autoregressive-within-segment placer -- node i's logits add
+                             (gamma_h (.) mean of E[D_j] over the leaders j decided before it in
+                             its segment) W_h, E = GDP_P_AR_E (d x h); gdp_sample / gdp_logprob /
+                             gdp_greedy decode each segment position by position and
+                             gdp_policy_grad differentiates through it.  0 = per-node heads (R13).
+                             Requires active_devices = 0. */
 } gdp_config;
 
 /* One cost-model verdict per placement. */
@@ -123,7 +130,9 @@ typedef enum {
   GDP_P_GATE_HEAD_Q,    /* 64 */
   GDP_P_HEAD_W,         /* 64 x d   per-node device logits (Fig. 1 "d") */
   GDP_P_HEAD_B,         /* d */
-  GDP_P_COUNT           /* = 90 tensors */
+  GDP_P_AR_E,           /* d x 64    device embedding of the autoregressive placer (empty unless
+                           gdp_config.autoregressive) */
+  GDP_P_COUNT           /* = 91 tensors */
 } gdp_param_id;
 
 /* ------------------------------------------------------------------ setup (untimed) */

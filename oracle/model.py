@@ -28,8 +28,9 @@ GATED = ["q", "k", "v", "o", "f1", "f2"]
 
 
 # --------------------------------------------------------------------------- parameters
-def param_spec(F: int, d: int) -> List[Tuple[str, Tuple[int, ...]]]:
-    """Flat theta order, written from the GDP_P_* list in include/gdp.h."""
+def param_spec(F: int, d: int, autoregressive: bool = False) -> List[Tuple[str, Tuple[int, ...]]]:
+    """Flat theta order, written from the GDP_P_* list in include/gdp.h (GDP_P_AR_E, the device
+    embedding of the autoregressive placer, is empty unless `autoregressive`)."""
     s: List[Tuple[str, Tuple[int, ...]]] = [("gnn.in.W", (F, H)), ("gnn.in.b", (H,))]
     for l in range(L_GNN):
         s += [(f"gnn.{l}.W", (H, H)), (f"gnn.{l}.b", (H,)), (f"gnn.{l}.Wf", (2 * H, H)), (f"gnn.{l}.bf", (H,))]
@@ -43,12 +44,14 @@ def param_spec(F: int, d: int) -> List[Tuple[str, Tuple[int, ...]]]:
             w = FFN if j == "f2" else H
             s += [(f"gate{l}.{j}.P", (H, w)), (f"gate{l}.{j}.q", (w,))]
     s += [("gate.head.P", (H, H)), ("gate.head.q", (H,)), ("head.W", (H, d)), ("head.b", (d,))]
+    if autoregressive:
+        s += [("ar.E", (d, H))]
     return s
 
 
-def unflatten(theta: torch.Tensor, F: int, d: int) -> Dict[str, torch.Tensor]:
+def unflatten(theta: torch.Tensor, F: int, d: int, autoregressive: bool = False) -> Dict[str, torch.Tensor]:
     p, o = {}, 0
-    for name, shape in param_spec(F, d):
+    for name, shape in param_spec(F, d, autoregressive):
         n = int(np.prod(shape))
         p[name] = theta[o:o + n].view(*shape)
         o += n

@@ -21,7 +21,7 @@ _lib = None
 GDP_OK = 0
 STATUS = {0: "GDP_OK", 1: "GDP_ERR_ARG", 2: "GDP_ERR_GRAPH", 3: "GDP_ERR_CYCLE", 4: "GDP_ERR_SHAPE",
           5: "GDP_ERR_CUDA", 6: "GDP_ERR_OVERFLOW", 7: "GDP_ERR_NONFINITE", 8: "GDP_ERR_WORKSPACE"}
-P_COUNT = 90
+P_COUNT = 91
 REPORT_BYTES = 24
 
 EXPORTS = ["gdp_default_config", "gdp_last_error", "gdp_launch_count", "gdp_build_info", "gdp_cost_kernel", "gdp_cost_wave", "gdp_logprob", "gdp_clip_adam", "gdp_sample_at", "gdp_greedy", "gdp_graph_validate", "gdp_graph_create", "gdp_graph_destroy",
@@ -41,7 +41,7 @@ class Config(ctypes.Structure):
                 ("xl_layers", ctypes.c_int32), ("ffn", ctypes.c_int32), ("num_devices", ctypes.c_int32),
                 ("seg_len", ctypes.c_int32), ("mem_len", ctypes.c_int32), ("superposition", ctypes.c_int32),
                 ("tensor_cores", ctypes.c_int32), ("no_attention", ctypes.c_int32),
-                ("active_devices", ctypes.c_int32)]
+                ("active_devices", ctypes.c_int32), ("autoregressive", ctypes.c_int32)]
 
 
 def lib():
@@ -165,13 +165,15 @@ def _stream(stream=None):
 
 # --------------------------------------------------------------------------- setup objects
 def default_config(d: int, seg_len: int = 128, mem_len: int = 128, superposition: bool = True,
-                   tensor_cores: bool = False, no_attention: bool = False, active_devices: int = 0) -> Config:
+                   tensor_cores: bool = False, no_attention: bool = False, active_devices: int = 0,
+                   autoregressive: bool = False) -> Config:
     c = Config()
     _check(lib().gdp_default_config(d, ctypes.byref(c)), "gdp_default_config")
     c.seg_len, c.mem_len, c.superposition = seg_len, mem_len, int(bool(superposition))
     c.tensor_cores = int(tensor_cores) if not isinstance(tensor_cores, bool) else int(tensor_cores)
     c.no_attention = int(bool(no_attention))
     c.active_devices = int(active_devices)
+    c.autoregressive = int(bool(autoregressive))
     return c
 
 

@@ -85,10 +85,10 @@ static const char *const kParamNames[GDP_P_COUNT] = {
     "gate0.f1.P", "gate0.f1.q", "gate0.f2.P", "gate0.f2.q",
     "gate1.q.P", "gate1.q.q", "gate1.k.P", "gate1.k.q", "gate1.v.P", "gate1.v.q", "gate1.o.P", "gate1.o.q",
     "gate1.f1.P", "gate1.f1.q", "gate1.f2.P", "gate1.f2.q",
-    "gate.head.P", "gate.head.q", "head.W", "head.b"};
+    "gate.head.P", "gate.head.q", "head.W", "head.b", "ar.E"};
 
 // parameter tensor shapes in GDP_P_* order
-static void param_shapes(int F, int d, long long *sz) {
+static void param_shapes(int F, int d, bool ar, long long *sz) {
   const long long H = kH, FF = kFFN;
   int i = 0;
   sz[i++] = F * H; sz[i++] = H;
@@ -107,11 +107,12 @@ static void param_shapes(int F, int d, long long *sz) {
     }
   sz[i++] = H * H; sz[i++] = H;                     // head gate
   sz[i++] = H * d; sz[i++] = d;                     // head
+  sz[i++] = ar ? (long long)d * H : 0;              // autoregressive device embedding
 }
 
-void param_offsets(int F, int d, long long *off) {
+void param_offsets(int F, int d, long long *off, bool ar) {
   long long sz[GDP_P_COUNT];
-  param_shapes(F, d, sz);
+  param_shapes(F, d, ar, sz);
   off[0] = 0;
   for (int i = 0; i < GDP_P_COUNT; i++) off[i + 1] = off[i] + sz[i];
 }
@@ -123,6 +124,9 @@ static gdp_status check_config(const gdp_config *c) {
   if (c->num_devices < 1 || c->num_devices > kMaxD) return fail(GDP_ERR_ARG, "num_devices must be in 1..8");
   if (c->seg_len < 1) return fail(GDP_ERR_ARG, "seg_len must be >= 1");
   if (c->mem_len < -1) return fail(GDP_ERR_ARG, "mem_len must be >= -1");
+  if (c->autoregressive != 0 && c->autoregressive != 1) return fail(GDP_ERR_ARG, "autoregressive must be 0 or 1");
+  if (c->autoregressive && c->active_devices != 0 && c->active_devices != c->num_devices)
+    return fail(GDP_ERR_ARG, "the autoregressive placer needs active_devices = 0");
   if (c->tensor_cores < 0 || c->tensor_cores > 2) return fail(GDP_ERR_ARG, "tensor_cores must be 0, 1 or 2");
   if (c->no_attention != 0 && c->no_attention != 1) return fail(GDP_ERR_ARG, "no_attention must be 0 or 1");
   if (c->active_devices < 0 || c->active_devices > c->num_devices)
@@ -350,6 +354,7 @@ gdp_status gdp_default_config(int32_t d, gdp_config *out) {
   out->tensor_cores = 0;
   out->no_attention = 0;
   out->active_devices = 0;
+  out->autoregressive = 0;
   return GDP_OK;
 }
 
@@ -623,7 +628,7 @@ gdp_status gdp_param_layout(const gdp_config *c, int32_t F, int64_t *offsets, in
   if (st != GDP_OK) return st;
   if (F <= 0) return fail(GDP_ERR_ARG, "F must be > 0");
   long long off[GDP_P_COUNT + 1];
-  param_offsets(F, c->num_devices, off);
+  param_offsets(F, c->num_devices, off, c->autoregressive != 0);
   if (offsets)
     for (int i = 0; i <= GDP_P_COUNT; i++) offsets[i] = off[i];
   if (n_params) *n_params = off[GDP_P_COUNT];
@@ -836,7 +841,7 @@ gdp_status gdp_grad_check(const float *grad, const gdp_config *c, int32_t F, dou
   if (st != GDP_OK) return st;
   if (F < 1) return fail(GDP_ERR_ARG, "F must be >= 1");
   long long off[GDP_P_COUNT + 1];
-  param_offsets(F, c->num_devices, off);
+  param_offsets(F, c->num_devices, off, c->autoregressive != 0);
   const long long n = off[GDP_P_COUNT];
   const long long i = first_nonfinite(grad, n, reinterpret_cast<unsigned long long *>(scratch),
                                       static_cast<cudaStream_t>(stream));
@@ -941,7 +946,7 @@ gdp_status gdp_grad_buckets(const gdp_config *c, int32_t F, int64_t *first, int6
   if (st != GDP_OK) return st;
   if (F < 1) return fail(GDP_ERR_ARG, "F must be >= 1");
   long long off[GDP_P_COUNT + 1];
-  param_offsets(F, c->num_devices, off);
+  param_offsets(F, c->num_devices, off, c->autoregressive != 0);
   first[0] = off[GDP_P_XL0_LN1_G]; last[0] = off[GDP_P_COUNT];
   first[1] = off[GDP_P_COND_LN1_G]; last[1] = off[GDP_P_XL0_LN1_G];
   first[2] = 0; last[2] = off[GDP_P_COND_LN1_G];

@@ -7,7 +7,7 @@
 namespace gdp {
 
 // theta offsets (computed by gdp_param_layout in api.cu)
-extern void param_offsets(int F, int d, long long *off);
+extern void param_offsets(int F, int d, long long *off, bool ar);
 
 namespace {
 
@@ -297,7 +297,7 @@ void run_rows(const RowTable &T, const float *theta, float *grad, cudaStream_t s
 gdp_status run_embed(const gdp_graph_s *g, const float *theta, float *node_emb, const WS &w, int d,
                      cudaStream_t s) {
   Offs off;
-  param_offsets(g->F, d, off.o);
+  param_offsets(g->F, d, off.o, false);   // the GNN's offsets do not depend on the head
   const int N = g->N;
   // H0 = X W_in + b_in (affine input projection)
   GemmArgs a = gemm(N, g->F, kH, g->X, g->F, theta + off[GDP_P_GNN_IN_W], kH, 1, w.H[0], kH);
@@ -328,7 +328,7 @@ gdp_status run_place(const gdp_graph_s *g, const gdp_config *c, const float *the
                      float *logits, const WS &w, cudaStream_t s) {
   Offs off;
   const int d = c->num_devices, N = g->N, S = c->seg_len, M = c->mem_len;
-  param_offsets(g->F, d, off.o);
+  param_offsets(g->F, d, off.o, c->autoregressive != 0);
   if (g->perm_identity)
     GDP_CUDA_CHECK(cudaMemcpyAsync(w.Etopo, node_emb, (size_t)N * kH * sizeof(float), cudaMemcpyDeviceToDevice, s));
   else
@@ -373,7 +373,7 @@ gdp_status run_policy_grad(const gdp_graph_s *g, const gdp_config *c, const floa
   };
   Offs off;
   const int d = c->num_devices, N = g->N, S = c->seg_len, M = c->mem_len;
-  param_offsets(g->F, d, off.o);
+  param_offsets(g->F, d, off.o, c->autoregressive != 0);
   const bool sup = c->superposition != 0;
   const GateTable GT = gate_table(off);
   // a14: dL/dlogits (caller order) -> topological order

@@ -49,18 +49,20 @@ def test_profile_host_logic():
 
 def test_param_layout_matches_oracle_and_header():
     for d in (1, 2, 4, 8):
-        cfg = gdp.default_config(d)
-        off, n = gdp.param_layout(cfg, 37)
-        spec = Mo.param_spec(37, d)
-        assert len(spec) == gdp.P_COUNT
-        o = np.cumsum([0] + [int(np.prod(s)) for _, s in spec])
-        assert np.array_equal(off, o)
-        assert n == workloads.param_count(37, d)
+        for ar in (False, True):
+            cfg = gdp.default_config(d, autoregressive=ar)
+            off, n = gdp.param_layout(cfg, 37)
+            spec = Mo.param_spec(37, d, autoregressive=ar)
+            sizes = [int(np.prod(s)) for _, s in spec] + ([] if ar else [0])   # GDP_P_AR_E empty unless ar
+            assert len(sizes) == gdp.P_COUNT
+            o = np.cumsum([0] + sizes)
+            assert np.array_equal(off, o)
+            assert n == workloads.param_count(37, d) + (64 * d if ar else 0)
     # enum order in the header == oracle order
     txt = open(os.path.join(ROOT, "include", "gdp.h")).read()
     body = txt[txt.index("typedef enum {\n  GDP_P_GNN_IN_W"):txt.index("GDP_P_COUNT")]
     enum = re.findall(r"(GDP_P_\w+)", body)
-    want = ["GDP_P_" + n.upper().replace(".", "_") for n, _ in Mo.param_spec(37, 8)]
+    want = ["GDP_P_" + n.upper().replace(".", "_") for n, _ in Mo.param_spec(37, 8, autoregressive=True)]
     assert enum == want
 
 

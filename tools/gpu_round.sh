@@ -13,3 +13,10 @@ cp profiles/cost_kernel_ncu.json gpurun_out/cost_kernel_ncu.json
 timeout 900 python bench.py > gpurun_out/bench_line.json 2> gpurun_out/bench_err.log; head -c 1500 gpurun_out/bench_line.json
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv \
     python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e --no-kernels > gpurun_out/launches_bench.log 2>&1
+mkdir -p gpurun_out/rows
+for c in c1 c2 c3 c5; do timeout 600 python bench.py --config $c --no-cpu-baseline --no-e2e --steps 5 > gpurun_out/rows/$c.json 2>/dev/null; done
+timeout 600 python bench.py --config c4 --mem-len -1 --no-cpu-baseline --no-e2e --steps 3 > gpurun_out/rows/c4_mem_inf.json 2>/dev/null
+timeout 600 python bench.py --config c4_64k --no-cpu-baseline --no-e2e --steps 3 > gpurun_out/rows/c4_64k.json 2>/dev/null
+timeout 600 python bench.py --config c4 --batch 296 --no-cpu-baseline --no-e2e --steps 3 > gpurun_out/rows/c4_b296.json 2>/dev/null
+for f in gpurun_out/rows/*.json; do python -c "
+import json,sys; d=json.loads(open('$f').read().strip().splitlines()[-1]); print('$f', round(d['value'],1), round(d['ms_per_step'],2), d['config'].get('batch_per_gpu'), d.get('stages_ms'))"; done
