@@ -227,7 +227,10 @@ gdp_status gdp_embed(gdp_graph g, const gdp_config *c, const float *theta, float
  * stop-gradient cached states of the previous M positions; no positional terms,
  * P:144-148) -> logits = (gamma_head . y) W_head + b_head.
  *   node_emb  dev fp32 N x 64 (in, as written by gdp_embed)
- *   logits    dev fp32 N x d (out), caller node order
+ *   logits    dev fp32 N x d (out), caller node order.  With gdp_config.autoregressive the buffer
+ *             holds N + d rows: the N x d base logits, then the d x d table EW = (E . gamma_head) W_head
+ *             (row k: the logit shift a decided device k contributes, reading R35); every call that
+ *             takes `logits` below reads both parts in that mode.
  * Errors: GDP_ERR_ARG (d mismatch, S < 1, M < -1), GDP_ERR_WORKSPACE, GDP_ERR_CUDA. */
 gdp_status gdp_place(gdp_graph g, const gdp_config *c, const float *theta, const float *node_emb,
                      float *logits, void *ws, size_t ws_bytes, void *stream);
@@ -242,6 +245,10 @@ gdp_status gdp_place(gdp_graph g, const gdp_config *c, const float *theta, const
  *   logprob     dev fp32 B (out)
  * ws must be sized for at least B placements (gdp_workspace_size); log pi is summed in fp64 in a
  * fixed order (per 128-node chunk, then the chunks in order): bit-identical across runs.
+ * Autoregressive mode (R35): each segment (S positions of the Kahn order) is decoded position by
+ * position -- leader v of placement b takes z = base_v + mean of EW[D_bj] over the leaders j
+ * decided before it in its segment, then the same uniform and fp32 inverse CDF as above; log pi
+ * sums per (placement, segment group) in Kahn order, then the groups in order. */
  * Errors: GDP_ERR_ARG (B < 1), GDP_ERR_WORKSPACE, GDP_ERR_CUDA. */
 gdp_status gdp_sample(gdp_graph g, const gdp_config *c, const float *logits, int32_t B, uint64_t seed,
                       uint64_t sample_offset, uint64_t step, uint8_t *placements, float *logprob,
@@ -358,6 +365,8 @@ gdp_status gdp_advantage(const double *reward, int32_t B, double *run_sum, int64
  * The gradient flows end to end through the placer and the GNN; cached
  * Transformer-XL states are stop-gradient.  grad += dL/dtheta.
  * Must follow gdp_embed and gdp_place of the same theta with the same ws.
+ * Autoregressive mode (R35): p_v becomes the per-placement p_{b,v} of the decode, the entropy term
+ * the mean over placements and nodes, and the gradient also reaches GDP_P_AR_E through EW.
  *   logits dev fp32 N x d;  placements dev uint8 B x N;  adv dev fp64 B
  *   logprob dev fp32 B (used only when old_logprob != NULL);  old_logprob dev fp32 B or NULL
  *   grad dev fp32 [n_params] (accumulated)
@@ -373,14 +382,17 @@ gdp_status gdp_policy_grad(gdp_graph g, const gdp_config *c, const float *theta,
  * sum over co-location leaders of log softmax(logits_v)[D_b v], fp64 sum in a fixed order.
  * The PPO epochs need it to form rho = exp(log pi_new - log pi_old).
  *   logits dev fp32 N x d (in);  placements dev uint8 B x N (in);  logprob dev fp32 B (out)
- * Uses the sampling scratch of ws.  Errors: GDP_ERR_ARG, GDP_ERR_WORKSPACE, GDP_ERR_CUDA. */
+ * Uses the sampling scratch of ws (sized for B placements in autoregressive mode, where the
+ * logits of each leader follow the GIVEN devices of the earlier leaders of its segment).
+ * Errors: GDP_ERR_ARG, GDP_ERR_WORKSPACE, GDP_ERR_CUDA. */
 gdp_status gdp_logprob(gdp_graph g, const gdp_config *c, const float *logits, const uint8_t *placements, int32_t B,
                        float *logprob, void *ws, size_t ws_bytes, void *stream);
 
 /* Greedy decode for zero-shot placement: per node the
  * argmax of its co-location leader's logits, ties -> lowest device id; optional log pi of it.
  *   logits dev fp32 N x d (in);  placement dev uint8 N (out);  logprob dev fp32 [1] (out, nullable:
- *   then ws may be NULL).  Errors: GDP_ERR_ARG, GDP_ERR_WORKSPACE, GDP_ERR_CUDA. */
+ *   then ws may be NULL, except in autoregressive mode, where each segment is decoded greedily
+ *   position by position and ws is required).  Errors: GDP_ERR_ARG, GDP_ERR_WORKSPACE, GDP_ERR_CUDA. */
 gdp_status gdp_greedy(gdp_graph g, const gdp_config *c, const float *logits, uint8_t *placement, float *logprob,
                       void *ws, size_t ws_bytes, void *stream);
 

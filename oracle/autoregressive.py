@@ -62,6 +62,70 @@ def ar_logits(base: torch.Tensor, EW: torch.Tensor, D: np.ndarray, order: Sequen
     return torch.stack(rows)                                          # B x N x d
 
 
+def ar_logits_vec(base: torch.Tensor, EW: torch.Tensor, D: np.ndarray, order: Sequence[int], S: int,
+                  lead: np.ndarray) -> torch.Tensor:
+    """ar_logits with the position loop shared by all segments and samples (the same running
+    sums, position by position; pinned equal to ar_logits in tests/test_oracle_ar.py) -- for
+    full-size graphs, where the per-node Python loop would take minutes."""
+    B = D.shape[0]
+    N, d = base.shape
+    order = np.asarray(order, dtype=np.int64)
+    nseg = (N + S - 1) // S
+    P = np.full(nseg * S, -1, dtype=np.int64)
+    P[:N] = order
+    P = P.reshape(nseg, S)
+    Dt = torch.as_tensor(np.asarray(D, dtype=np.int64))
+    acc = torch.zeros(B, nseg, d, dtype=base.dtype)
+    c = np.zeros(nseg, dtype=np.int64)
+    zs, vs = [], []
+    for q in range(S):
+        v = P[:, q]
+        ok = v >= 0
+        sv = np.nonzero(ok)[0]
+        vv = v[ok]
+        cc = torch.as_tensor(np.maximum(c[sv], 1), dtype=base.dtype)[None, :, None]
+        shift = torch.where(torch.as_tensor(c[sv] > 0)[None, :, None], acc[:, sv] / cc, torch.zeros_like(acc[:, sv]))
+        zs.append(base[torch.as_tensor(vv)][None] + shift)
+        vs.append(vv)
+        isl = lead[vv] == vv
+        if isl.any():
+            sl, vl = sv[isl], vv[isl]
+            add = torch.zeros_like(acc)
+            add[:, torch.as_tensor(sl)] = EW[Dt[:, torch.as_tensor(vl)]]
+            acc = acc + add
+            c[sl] += 1
+    z = torch.cat(zs, 1)                                              # B x N x d, Kahn order
+    inv = np.empty(N, dtype=np.int64)
+    inv[np.concatenate(vs)] = np.arange(N)
+    return z[:, torch.as_tensor(inv)]
+
+
+def ar_greedy(base: np.ndarray, EW: np.ndarray, order: Sequence[int], S: int,
+              lead: np.ndarray) -> Tuple[np.ndarray, float, np.ndarray]:
+    """Greedy decode (NEXT-2 with R35): each leader takes the argmax of its z (ties -> lowest
+    device), the running sums follow those choices; non-leaders copy the leader.  Returns
+    (D, log pi, top-2 margin per node)."""
+    N, d = base.shape
+    D = np.zeros(N, dtype=np.uint8)
+    margin = np.full(N, np.inf)
+    lp = 0.0
+    for seg in segments_of(order, S):
+        acc = np.zeros(d)
+        c = 0
+        for v in seg:
+            if lead[v] != v:
+                continue
+            z = base[v].astype(np.float64) + (acc / c if c else 0.0)
+            k = int(np.argmax(z))
+            D[v] = k
+            if d > 1:
+                margin[v] = float(z[k] - np.sort(z)[-2])
+            lp += float(z[k] - (z.max() + math.log(np.exp(z - z.max()).sum())))
+            acc = acc + EW[k]
+            c += 1
+    return D[lead], lp, margin
+
+
 def ar_sample(base: np.ndarray, EW: np.ndarray, U: np.ndarray, order: Sequence[int], S: int,
               lead: np.ndarray, teacher: Optional[np.ndarray] = None) -> Tuple[np.ndarray, np.ndarray, np.ndarray]:
     """Decode B placements position by position (R35 with R17 inverse CDF in fp64).  Returns
@@ -98,7 +162,9 @@ def ar_policy_loss(base: torch.Tensor, EW: torch.Tensor, D, adv, lead: np.ndarra
                    old_logprob, clip_eps: float, entropy_coef: float, loss_scale: float) -> torch.Tensor:
     """model.policy_loss with per-sample logits z_{b,i} (R35): log pi over leaders; entropy the
     mean over samples and nodes."""
-    z = ar_logits(base, EW, np.asarray(D), order, S, lead)            # B x N x d
+    D = np.asarray(D)
+    big = D.shape[0] * base.shape[0] > 20000
+    z = (ar_logits_vec if big else ar_logits)(base, EW, D, order, S, lead)   # B x N x d
     B, N, d = z.shape
     logp = torch.log_softmax(z, 2)
     Dt = torch.as_tensor(np.asarray(D, dtype=np.int64))
@@ -132,10 +198,11 @@ def base_and_table(pg, theta: torch.Tensor, d: int, S: int, M_: int, superpositi
 
 
 def policy_grad(pg, theta, d: int, S: int, M_: int, superposition: bool, D, adv, old_logprob=None,
-                clip_eps: float = 0.2, entropy_coef: float = 0.01, loss_scale: float = 1.0):
-    """Gradient of ar_policy_loss w.r.t. the flat theta (with GDP_P_AR_E appended)."""
+                clip_eps: float = 0.2, entropy_coef: float = 0.01, loss_scale: float = 1.0, num=None):
+    """Gradient of ar_policy_loss w.r.t. the flat theta (with GDP_P_AR_E appended); `num` as in
+    model.policy_grad (tie import at the network's kinks)."""
     th = torch.as_tensor(np.asarray(theta, dtype=np.float64)).clone().requires_grad_(True)
-    base, EW = base_and_table(pg, th, d, S, M_, superposition)
+    base, EW = base_and_table(pg, th, d, S, M_, superposition, num=num)
     L = ar_policy_loss(base, EW, D, adv, pg.lead, pg.order, S, old_logprob, clip_eps, entropy_coef, loss_scale)
     (g,) = torch.autograd.grad(L, th)
     return g.numpy(), float(L.detach())

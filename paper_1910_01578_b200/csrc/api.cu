@@ -207,6 +207,7 @@ bool ws_layout(const gdp_graph_s *g, int d, int B, char *base, WS *w) {
   z.dAg = F32(N * kH);
   z.dP = F32(N * kH);
   z.dd = F32(N * kHeads);
+  z.dEW = F32(kMaxD * kMaxD);
   const size_t chunks = (N + 255) / 256 + 1;
   z.part_floats = chunks * 257 * 256;
   z.part = F32(z.part_floats);
@@ -758,8 +759,12 @@ static gdp_status sample_impl(gdp_graph g, const gdp_config *c, const float *log
   st = carve_any(g, c->num_devices, B, ws, ws_bytes, &w);
   if (st != GDP_OK) return st;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  launch_sample(logits, c->num_devices, g->leader, g->has_coloc, g->N, active_devices(c), B, seed, sample_offset,
-                step, step_dev, w.cdf, w.logp, w.lastpos, w.spart, placements, logprob, s);
+  if (c->autoregressive)
+    launch_ar_decode(kArDecodeSample, logits, g->perm, g->leader, g->has_coloc, g->N, c->num_devices, c->seg_len, B,
+                     seed, sample_offset, step, step_dev, placements, w.spart, logprob, s);
+  else
+    launch_sample(logits, c->num_devices, g->leader, g->has_coloc, g->N, active_devices(c), B, seed, sample_offset,
+                  step, step_dev, w.cdf, w.logp, w.lastpos, w.spart, placements, logprob, s);
   GDP_LAUNCH_CHECK("gdp_sample");
   return GDP_OK;
 }
@@ -787,9 +792,15 @@ gdp_status gdp_logprob(gdp_graph g, const gdp_config *c, const float *logits, co
   if (st != GDP_OK) return st;
   if (B < 1) return fail(GDP_ERR_ARG, "B must be >= 1");
   WS w;
-  st = carve_any(g, c->num_devices, 1, ws, ws_bytes, &w);
+  st = carve_any(g, c->num_devices, c->autoregressive ? B : 1, ws, ws_bytes, &w);
   if (st != GDP_OK) return st;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (c->autoregressive) {
+    launch_ar_decode(kArDecodeScore, logits, g->perm, g->leader, g->has_coloc, g->N, c->num_devices, c->seg_len, B,
+                     0, 0, 0, nullptr, const_cast<uint8_t *>(placements), w.spart, logprob, s);
+    GDP_LAUNCH_CHECK("gdp_logprob");
+    return GDP_OK;
+  }
   launch_node_prep(logits, c->num_devices, g->N, active_devices(c), w.cdf, w.logp, w.lastpos, s);
   launch_logprob(w.logp, g->leader, placements, g->N, active_devices(c), B, logprob, s);
   GDP_LAUNCH_CHECK("gdp_logprob");
@@ -803,6 +814,15 @@ gdp_status gdp_greedy(gdp_graph g, const gdp_config *c, const float *logits, uin
   gdp_status st = check_config(c);
   if (st != GDP_OK) return st;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (c->autoregressive) {   // the decode needs the log pi scratch whether or not it is returned
+    WS w;
+    st = carve_any(g, c->num_devices, 1, ws, ws_bytes, &w);
+    if (st != GDP_OK) return st;
+    launch_ar_decode(kArDecodeGreedy, logits, g->perm, g->leader, g->has_coloc, g->N, c->num_devices, c->seg_len, 1,
+                     0, 0, 0, nullptr, placement, w.spart, logprob, s);
+    GDP_LAUNCH_CHECK("gdp_greedy");
+    return GDP_OK;
+  }
   launch_greedy(logits, c->num_devices, g->leader, g->N, active_devices(c), placement, s);
   if (logprob) {
     WS w;

@@ -115,6 +115,7 @@ struct WS {
   double *wb, *lpart, *spart;
   float *dlog, *dlog_topo, *dy, *dx1, *dm, *dc, *dout, *dqkv, *dkvm, *dkvt, *da, *dam, *dxa, *dEt, *dE;
   float *dH, *dHn, *dAg, *dP, *dd;
+  float *dEW;            // autoregressive placer: dL/dEW (d x d)
   float *part;           // wgrad / column-sum partials
   float *dgam, *dz, *dzp;
   size_t part_floats;
@@ -237,6 +238,27 @@ int adam_parts();
 void launch_logprob(const float *logp, const int *leader, const uint8_t *D, int N, int d, int B, float *logprob,
                     cudaStream_t s);
 void launch_greedy(const float *logits, int ld, const int *leader, int N, int d, uint8_t *D, cudaStream_t s);
+// log pi_b = sum of part[b][0..nparts) in order; non-leaders copy their leader's device
+void launch_sum_parts(const double *part, int nparts, int B, float *logprob, cudaStream_t s);
+void launch_colocate(const int *leader, int N, int B, uint8_t *D, cudaStream_t s);
+// autoregressive-within-segment placer (ar.cu, reading R35).  EW (d x d)
+// follows the N x d base logits in the caller's logits buffer.
+constexpr int kArDecodeSample = 0, kArDecodeScore = 1, kArDecodeGreedy = 2;
+void launch_ar_table(const float *E, const float *Wh, int d, float *EW, cudaStream_t s);
+// groups of consecutive segments a decode / gradient warp walks (<= the k_sample chunk count, so
+// that ws.spart holds B x groups partial sums)
+int ar_groups(int N, int S);
+void launch_ar_decode(int mode, const float *logits, const int *perm, const int *leader, bool has_coloc, int N,
+                      int d, int S, int B, uint64_t seed, uint64_t offset, uint64_t step, const uint64_t *step_ptr,
+                      uint8_t *D, double *part, float *logprob, cudaStream_t s);
+// dL/dbase (topological rows, dlt) and dL/dEW (dEW, d x d) of the R35 loss; part / dewpart scratch
+void launch_ar_grad(const float *logits, const int *perm, const int *leader, int N, int d, int S, int B,
+                    const uint8_t *D, const double *adv, const float *logprob, const float *old_logprob, float eps,
+                    float beta, float scale, double *wb, double *lpart, float *dewpart, size_t dewpart_floats,
+                    float *dlt, float *dEW, cudaStream_t s);
+// dWh' += E^T dEW (rows 0..63 of the augmented head gradient), grad[E] += dEW Wh'^T
+void launch_ar_head_bwd(const float *E, const float *Wh, const float *dEW, int d, float *dWh, float *gE,
+                        cudaStream_t s);
 // devices a call samples / scores over: gdp_config.active_devices, or num_devices when 0
 int active_devices(const gdp_config *c);
 // synchronous: index of the first non-finite entry of g[0, n) (n if none, -1 on a CUDA error);

@@ -357,6 +357,8 @@ gdp_status run_place(const gdp_graph_s *g, const gdp_config *c, const float *the
   a.bias = theta + off[GDP_P_HEAD_B];
   launch_gemm(a, s);
   if (!g->perm_identity) launch_rows_scatter(w.logits_topo, g->perm, logits, N, d, false, s);
+  if (c->autoregressive)   // R35: EW = E Wh' behind the base logits
+    launch_ar_table(theta + off[GDP_P_AR_E], w.Wh, d, logits + (size_t)N * d, s);
   GDP_LAUNCH_CHECK("gdp_place");
   return GDP_OK;
 }
@@ -377,15 +379,24 @@ gdp_status run_policy_grad(const gdp_graph_s *g, const gdp_config *c, const floa
   const bool sup = c->superposition != 0;
   const GateTable GT = gate_table(off);
   // a14: dL/dlogits (caller order) -> topological order
-  launch_logit_grad(logits, d, D, g->leader, adv, logprob, old_logprob, eps, beta, scale, N, active_devices(c), B,
-                    w.wb, w.lpart, w.dlog, s);
+  const bool ar = c->autoregressive != 0;
   const float *dlt = w.dlog;
-  if (!g->perm_identity) {
-    launch_rows_gather(w.dlog, g->perm, w.dlog_topo, N, d, s);
+  if (ar) {   // R35: dL/dbase straight into topological rows, dL/dEW into w.dEW
+    launch_ar_grad(logits, g->perm, g->leader, N, d, S, B, D, adv, logprob, old_logprob, eps, beta, scale, w.wb,
+                   w.lpart, w.part, w.part_floats, w.dlog_topo, w.dEW, s);
     dlt = w.dlog_topo;
+  } else {
+    launch_logit_grad(logits, d, D, g->leader, adv, logprob, old_logprob, eps, beta, scale, N, active_devices(c), B,
+                      w.wb, w.lpart, w.dlog, s);
+    if (!g->perm_identity) {
+      launch_rows_gather(w.dlog, g->perm, w.dlog_topo, N, d, s);
+      dlt = w.dlog_topo;
+    }
   }
   // head: logits = y2 Wh' + bh
   launch_wgrad(N, kH, d, w.L[2].y, kH, kH, nullptr, 0, dlt, d, true, w.part, w.part_floats, w.dWh, false, s);
+  if (ar)   // EW = E Wh': dWh' += E^T dEW, grad[E] += dEW Wh'^T
+    launch_ar_head_bwd(theta + off[GDP_P_AR_E], w.Wh, w.dEW, d, w.dWh, grad + off[GDP_P_AR_E], s);
   GemmArgs a = gemm(N, d, kH, dlt, d, w.Wh, 1, d, w.dy, kH);
   launch_gemm(a, s);
   // placement layers (reverse order)

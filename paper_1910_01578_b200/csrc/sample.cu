@@ -7,21 +7,10 @@
 //  * k_logit_grad: thread per node: dL/dz_vk = -s sum_b w_b ([D_bv = k] - p_vk) [v leader]
 //                 + (beta/N) p_vk (log p_vk + H_v), with w_b = A_b rho_b [unclipped].
 #include "common.cuh"
+#include "philox.cuh"
 
 namespace gdp {
 namespace {
-
-__device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint2 k) {
-#pragma unroll
-  for (int r = 0; r < 10; r++) {
-    unsigned hi0 = __umulhi(0xD2511F53u, c.x), lo0 = 0xD2511F53u * c.x;
-    unsigned hi1 = __umulhi(0xCD9E8D57u, c.z), lo1 = 0xCD9E8D57u * c.z;
-    c = make_uint4(hi1 ^ c.y ^ k.x, lo1, hi0 ^ c.w ^ k.y, lo0);
-    k.x += 0x9E3779B9u;
-    k.y += 0xBB67AE85u;
-  }
-  return c;
-}
 
 // logits rows have stride ld >= d: a head padded to ld devices of which the first d are active
 // (mixed device counts); cdf / logp are stored with stride d
@@ -275,4 +264,16 @@ void launch_logit_grad(const float *logits, int ld, const uint8_t *D, const int 
   k_logit_fin<<<(N + 127) / 128, 128, 0, s>>>(logits, ld, leader, wb, part, nch, beta, scale, N, d, B, dlog);
 }
 
+}  // namespace gdp
+
+namespace gdp {
+void launch_sum_parts(const double *part, int nparts, int B, float *logprob, cudaStream_t s) {
+  note_launch("k_sample_lp", s, 8.0 * B * nparts + 4.0 * B);
+  k_sample_lp<<<(B + 127) / 128, 128, 0, s>>>(part, nparts, B, logprob);
+}
+void launch_colocate(const int *leader, int N, int B, uint8_t *D, cudaStream_t s) {
+  const size_t n = (size_t)N * B;
+  note_launch("k_colocate", s);
+  k_colocate<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(leader, N, B, D);
+}
 }  // namespace gdp

@@ -40,7 +40,8 @@ class _GraphState:
         d = cfg.num_devices
         self.ws = torch.empty(workspace_size(self.g, cfg, B_local), dtype=torch.uint8, device=device)
         self.node_emb = torch.empty(self.N, 64, dtype=torch.float32, device=device)
-        self.logits = torch.empty(self.N, d, dtype=torch.float32, device=device)
+        # autoregressive placer (R35): the d x d table EW = E Wh' follows the N x d base logits
+        self.logits = torch.empty(self.N + (d if cfg.autoregressive else 0), d, dtype=torch.float32, device=device)
         self.placements = torch.empty(B_local, self.N, dtype=torch.uint8, device=device)
         self.logprob = torch.empty(B_local, dtype=torch.float32, device=device)
         self.rep = torch.empty(B_local, REPORT_BYTES, dtype=torch.uint8, device=device)
@@ -66,11 +67,12 @@ class PolicyStep:
     def __init__(self, graphs: List, d: int, seg_len: int, mem_len: int, superposition: bool, batch: int,
                  seed: int = 42, clip_eps: float = 0.2, entropy_coef: float = 0.01, mode: str = "samples",
                  rank: int = 0, world: int = 1, device=None, tensor_cores: bool = False, cuda_graph: bool = False,
-                 no_attention: bool = False):
+                 no_attention: bool = False, autoregressive: bool = False):
         import torch
         self.torch = torch
         self.device = device if device is not None else torch.device("cuda", torch.cuda.current_device())
-        self.cfg = default_config(d, seg_len, mem_len, superposition, tensor_cores, no_attention)
+        self.cfg = default_config(d, seg_len, mem_len, superposition, tensor_cores, no_attention,
+                                  autoregressive=autoregressive)
         self.plan = make_plan(mode, rank, world, batch, len(graphs), entropy_coef,
                               [g[0].N * batch for g in graphs])
         self.seed, self.clip_eps = seed, clip_eps
@@ -225,12 +227,14 @@ class PPOTrainer:
     def __init__(self, gsrc, feat, topo_src, d: int, seg_len: int = 128, mem_len: int = 128,
                  superposition: bool = True, rollouts: int = 16, minibatch: int = 8, epochs: int = 4,
                  lr: float = 3e-4, clip_eps: float = 0.2, entropy_coef: float = 0.01, max_norm: float = 1.0,
-                 seed: int = 42, device=None, tensor_cores: bool = False, no_attention: bool = False):
+                 seed: int = 42, device=None, tensor_cores: bool = False, no_attention: bool = False,
+                 autoregressive: bool = False):
         import torch
         from . import ADAM_SCRATCH
         self.torch = torch
         self.device = device if device is not None else torch.device("cuda", torch.cuda.current_device())
-        self.cfg = default_config(d, seg_len, mem_len, superposition, tensor_cores, no_attention)
+        self.cfg = default_config(d, seg_len, mem_len, superposition, tensor_cores, no_attention,
+                                  autoregressive=autoregressive)
         self.R, self.mb, self.epochs = rollouts, minibatch, epochs
         self.lr, self.clip_eps, self.entropy_coef, self.max_norm, self.seed = lr, clip_eps, entropy_coef, max_norm, seed
         self.st = _GraphState(gsrc, feat, topo_src, self.cfg, rollouts, rollouts, self.device)
@@ -291,13 +295,14 @@ class PPOTrainer:
 
 def zero_shot(gsrc, feat, topo_src, theta, d: int, seg_len: int = 128, mem_len: int = 128,
               superposition: bool = True, tensor_cores: bool = False, device=None,
-              no_attention: bool = False) -> Dict[str, object]:
+              no_attention: bool = False, autoregressive: bool = False) -> Dict[str, object]:
     """Zero-shot placement: embed -> place -> greedy decode ->
     cost of that one placement, no update.  Returns the placement, its log-probability and the
     cost-model report (makespan, validity, reward, peaks)."""
     import torch
     device = device if device is not None else torch.device("cuda", torch.cuda.current_device())
-    cfg = default_config(d, seg_len, mem_len, superposition, tensor_cores, no_attention)
+    cfg = default_config(d, seg_len, mem_len, superposition, tensor_cores, no_attention,
+                         autoregressive=autoregressive)
     st = _GraphState(gsrc, feat, topo_src, cfg, 1, 1, device)
     gdp_embed(st.g, st.cfg, theta, st.node_emb, st.ws)
     gdp_place(st.g, st.cfg, theta, st.node_emb, st.logits, st.ws)
@@ -315,7 +320,8 @@ def finetune(gsrc, feat, topo_src, theta, d: int, updates: int = 50, **kw) -> Di
     in place), then the zero-shot placement of the result."""
     if updates > 50:
         raise ValueError("fine-tuning runs fewer than 50 updates (P:254)")
-    zs = {k: kw[k] for k in ("seg_len", "mem_len", "superposition", "tensor_cores", "no_attention") if k in kw}
+    zs = {k: kw[k] for k in ("seg_len", "mem_len", "superposition", "tensor_cores", "no_attention",
+                                   "autoregressive") if k in kw}
     tr = PPOTrainer(gsrc, feat, topo_src, d, **kw)
     for _ in range(updates):
         tr.update(theta)

@@ -117,3 +117,44 @@ def test_ar_gradient_finite_differences():
         tm[i] -= h
         fd = (loss(tp) - loss(tm)) / (2 * h)
         assert abs(fd - gr[i]) <= 1e-4 * max(1e-3, abs(gr[i])), (i, fd, gr[i])
+
+
+@pytest.mark.parametrize("S,coloc", [(4, False), (7, True), (64, True)])
+def test_vectorised_logits_equal_the_loop(S, coloc):
+    """ar_logits_vec (all segments advanced together) == ar_logits (node by node), exactly."""
+    rng = np.random.default_rng(S)
+    N, d, B = 45, 3, 4
+    base = torch.as_tensor(rng.normal(size=(N, d)))
+    EW = torch.as_tensor(rng.normal(size=(d, d)))
+    order = rng.permutation(N)
+    lead = np.arange(N)
+    if coloc:
+        lead[[5, 17, 30]] = 2
+        lead[[11, 40]] = 9
+    D = rng.integers(0, d, size=(B, N))
+    D = D[:, lead]
+    a = Ar.ar_logits(base, EW, D, order, S, lead)
+    b = Ar.ar_logits_vec(base, EW, D, order, S, lead)
+    assert torch.equal(a, b)
+
+
+def test_greedy_is_the_mode_of_each_conditional():
+    """ar_greedy: every leader's device is the argmax of its own conditional given the greedy
+    prefix, and its log pi is the log-probability ar_logits assigns to that placement."""
+    rng = np.random.default_rng(11)
+    N, d, S = 12, 4, 5
+    base = rng.normal(size=(N, d))
+    EW = rng.normal(size=(d, d)) * 2
+    lead = np.arange(N)
+    lead[7] = 3
+    D, lp, _ = Ar.ar_greedy(base, EW, list(range(N)), S, lead)
+    z = Ar.ar_logits(torch.as_tensor(base), torch.as_tensor(EW), D[None], list(range(N)), S, lead)[0].numpy()
+    isl = lead == np.arange(N)
+    assert np.array_equal(D[isl], z[isl].argmax(1))
+    assert D[7] == D[3]
+    ls = z - (z.max(1, keepdims=True) + np.log(np.exp(z - z.max(1, keepdims=True)).sum(1, keepdims=True)))
+    assert abs(lp - ls[np.arange(N), D][isl].sum()) < 1e-12
+    # E = 0: the plain per-node argmax (oracle.sampling.greedy)
+    D0, _, _ = Ar.ar_greedy(base, np.zeros((d, d)), list(range(N)), S, lead)
+    Dg, _ = Sa.greedy(base, lead)
+    assert np.array_equal(D0, Dg)
