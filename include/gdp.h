@@ -248,7 +248,7 @@ gdp_status gdp_place(gdp_graph g, const gdp_config *c, const float *theta, const
  * Autoregressive mode (R35): each segment (S positions of the Kahn order) is decoded position by
  * position -- leader v of placement b takes z = base_v + mean of EW[D_bj] over the leaders j
  * decided before it in its segment, then the same uniform and fp32 inverse CDF as above; log pi
- * sums per (placement, segment group) in Kahn order, then the groups in order. */
+ * sums per (placement, segment group) in Kahn order, then the groups in order.
  * Errors: GDP_ERR_ARG (B < 1), GDP_ERR_WORKSPACE, GDP_ERR_CUDA. */
 gdp_status gdp_sample(gdp_graph g, const gdp_config *c, const float *logits, int32_t B, uint64_t seed,
                       uint64_t sample_offset, uint64_t step, uint8_t *placements, float *logprob,
