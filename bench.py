@@ -216,7 +216,9 @@ def config_json(W, args, mode: str = "samples"):
             "mem_len": W.mem_len,
             "superposition": W.superposition, "batch_per_gpu": args.batch,
             "global_batch": args.batch * (args.gpus if mode == "samples" else 1), "parallelism": par,
-            "l2": "flushed between timed steps (512 MiB write)"}
+            "l2": "flushed between timed steps (512 MiB write)",
+            **({"placer": "autoregressive within segments (reading R35)"} if getattr(args, "autoregressive", False)
+               else {})}
 
 
 # ----------------------------------------------------------------------------- GPU arm
@@ -289,6 +291,8 @@ def main():
     ap.add_argument("--fp32", action="store_true", help="dense maps in fp32 SIMT instead of tcgen05 bf16")
     ap.add_argument("--no-attention", action="store_true", help="NEXT-3 ablation variant (reading R34)")
     ap.add_argument("--no-superposition", action="store_true", help="NEXT-3 ablation variant (gates == 1)")
+    ap.add_argument("--autoregressive", action="store_true",
+                    help="NEXT-4 autoregressive-within-segment placer (reading R35)")
     ap.add_argument("--cuda-graph", action="store_true",
                     help="replay the whole step as one CUDA graph (single process; no per-stage timings)")
     ap.add_argument("--zero-shot", action="store_true",
@@ -332,8 +336,11 @@ def main():
     mode = "graphs" if len(W.graphs) > 2 else "samples"
     ps = gdp.PolicyStep(graphs, W.d, W.seg_len, W.mem_len, W.superposition, W.batch, seed=W.seed,
                         mode=mode, rank=rank, world=world, device=dev, tensor_cores=not args.fp32,
-                        cuda_graph=args.cuda_graph, no_attention=args.no_attention)
+                        cuda_graph=args.cuda_graph, no_attention=args.no_attention,
+                        autoregressive=args.autoregressive)
     th = workloads.init_theta(workloads.F, W.d, seed=7)
+    if args.autoregressive:   # the device embedding E (GDP_P_AR_E), small random values
+        th = np.concatenate([th, np.random.default_rng(8).normal(scale=0.1, size=64 * W.d).astype(np.float32)])
     theta = torch.from_numpy(th).to(dev)
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
 

@@ -25,10 +25,10 @@ __global__ void k_node_prep(const float *logits, int ld, int N, int d, float *cd
     e[k] = expf(z[k] - mx);
     s += e[k];
   }
-  float ls = logf(s), c = 0.f;
+  float ls = logf(s), is = 1.f / s, c = 0.f;   // p = e / s as e * (1 / s), like the AR decode (ar.cu)
   int last = 0;
   for (int k = 0; k < d; k++) {
-    float p = e[k] / s;
+    float p = e[k] * is;
     c += p;
     cdf[(size_t)v * d + k] = c;
     logp[(size_t)v * d + k] = (z[k] - mx) - ls;
