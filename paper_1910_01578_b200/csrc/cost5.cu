@@ -68,6 +68,9 @@ constexpr int NINC5 = COST5_NINC;   // ops made available at one instant kept in
 #ifndef COST5_SLEEP
 #define COST5_SLEEP 1000
 #endif
+#ifndef COST5_SPIN
+#define COST5_SPIN 4
+#endif
 constexpr int RI5 = COST5_RI;       // memory item ring (power of 2)
 constexpr int MB5 = COST5_MB;       // the memory warp waits for this many items (or the end) before a batch
 
@@ -124,6 +127,7 @@ struct Smem5 {
   int doff[8];
   int mhead;                        // items consumed by the memory warp
   int mk, disp, oom;
+  int simw;                         // which of the two warps simulates (the other does the memory accounting)
 };
 
 struct Scratch5 {
@@ -296,6 +300,11 @@ __global__ void __launch_bounds__(512) k_cost5_pre(Cost5Graph G, TopoArgs T, con
 }
 
 // ------------------------------------------------------------------------ main kernel
+// The two warps of a 64-thread CTA occupy warp slots 2i, 2i + 1 of their SM, i.e. sub-partitions
+// (0, 1) or (2, 3) (slot mod 4; measured, tools/lat/smsp.cu).  With warp 0 always simulating, every
+// simulation warp would share sub-partitions 0 and 2 while 1 and 3 hold the mostly sleeping memory
+// warps; so successive CTAs on the same (SM, sub-partition pair) alternate the simulating warp.
+__device__ unsigned g_c5_pair[2 * 1024];
 __global__ void __launch_bounds__(64) k_cost5(Cost5Graph G, TopoArgs T, const uint8_t *__restrict__ Dall,
                                               unsigned char *scratch, size_t per_place, gdp_sim_report *rep,
                                               long long *peak_out, long long *busy_out, double *reward) {
@@ -325,7 +334,13 @@ __global__ void __launch_bounds__(64) k_cost5(Cost5Graph G, TopoArgs T, const ui
     for (int i = tid; i < RI5; i += 64) S.items[i] = 1ull << 32;   // lap parity 1: empty for lap 0
     if (tid < NCH) { S.ch[tid] = make_int4(0, 0, 0, 0); S.ca[tid] = INF; }
     if (tid < 8) { S.dv[tid] = make_int4(INF, 0, 0, 0); S.dv2[tid] = make_int4(0, -1, T.speed[tid], 0); }
-    if (tid == 0) { S.mhead = 0; S.mk = 0; S.disp = 0; S.oom = 0; }
+    if (tid == 0) {
+      S.mhead = 0; S.mk = 0; S.disp = 0; S.oom = 0;
+      unsigned wid, sm;
+      asm volatile("mov.u32 %0, %%warpid;" : "=r"(wid));
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+      S.simw = (int)(atomicAdd(&g_c5_pair[(2 * sm + ((wid >> 1) & 1u)) & 2047u], 1u) & 1u);
+    }
     if (tid == 32) {
       int o = 0;
       for (int k = 0; k < 8; k++) { S.doff[k] = o; o += pre->opcnt[k]; }
@@ -352,7 +367,7 @@ __global__ void __launch_bounds__(64) k_cost5(Cost5Graph G, TopoArgs T, const ui
     return;
   }
 
-  if (warp == 0) {
+  if (warp == S.simw) {
     // ============================================================ simulation warp
     // Warp-uniform serial event processing: every lane executes the same code on the same
     // values (so a lane reads back its own stores of the shared state and no lane diverges);
@@ -642,7 +657,7 @@ __global__ void __launch_bounds__(64) k_cost5(Cost5Graph G, TopoArgs T, const ui
       if (n < MB5 && !__any_sync(FULL, valid && kind_end(it))) {
         // wait for a batch of MB5 items unless the simulation has ended: few, large batches
         // leave the issue slots to the simulation warps
-        if (n == 0 || ++nwait < 4) {
+        if (n == 0 || ++nwait < COST5_SPIN) {
 #ifdef COST5_PROF
           nidle++;
 #endif
