@@ -29,8 +29,8 @@
 //    shared memory: a finishing op's consumers' devices come with its staged out-edge records
 //    (a per-placement byte per out-edge slot that k_cost5_pre writes), the memory warp reads the
 //    placement row from L2.  Static memory, busy time, channel sizes and the co-location check
-//    also come from k_cost5_pre (one CTA per placement, fully parallel).  With 24 KB of shared
-//    memory per placement, nine CTAs (placements) share an SM at C4.
+//    also come from k_cost5_pre (one CTA per placement, fully parallel).  With 22.2 KB of shared
+//    memory per placement, ten CTAs (placements) share an SM at C4.
 // Requires (host-checked): every duration >= 1 and every transfer >= 1 tick (no same-instant
 // rounds), N and E < 2^25, degrees < 2^16.  Otherwise gdp_cost runs k_cost3 / k_cost (cost2.cu,
 // cost.cu).
@@ -51,10 +51,10 @@ constexpr int KC5 = 4;      // channel entries kept in shared memory per channel
 #define COST5_KF 4
 #endif
 #ifndef COST5_SO
-#define COST5_SO 8
+#define COST5_SO 5
 #endif
 #ifndef COST5_NINC
-#define COST5_NINC 2
+#define COST5_NINC 1
 #endif
 constexpr int KF5 = COST5_KF;       // FIFO entries kept in shared memory per device (power of 2)
 constexpr int SO5 = COST5_SO;       // staged out-edge records per slot (more: read from global at the finish)
