@@ -67,10 +67,13 @@ typedef struct {
   int32_t mem_len;        /* M >= 0 cached positions before each segment, or -1 = every earlier segment */
   int32_t superposition;  /* 1: Eq. 4 gates on every placer dense map and the head; 0: gates == 1 */
   int32_t tensor_cores;   /* 0: every dense map in fp32 (SIMT, the 1e-4 parity mode); 1: dense maps
-                             Y = X W (forward and the backward dX = dY W^T) with 16 <= width <= 256 and
-                             >= 128 rows on tcgen05 tensor cores, bf16 operands, fp32 accumulation in
-                             TMEM, and the segment attention on tcgen05 tiles; weight gradients
-                             (reductions over nodes) stay fp32.  2 (diagnostic): as 1 but with the
+                             Y = X W (forward and the backward dX = dY W^T) with 16 <= width <= 256,
+                             1 <= K <= 256, ceil32(K) * ceil16(width) <= 40960 and >= 128 rows on
+                             tcgen05 tensor cores with tf32 operands -- the fp32 bit patterns of X and
+                             W truncated to their upper 19 bits (sign, exponent, 10 mantissa bits) --
+                             and fp32 accumulation in TMEM; the segment attention on tcgen05 tiles
+                             with bf16 Q, K, V and softmax numerators; weight gradients (reductions
+                             over nodes) stay fp32.  2 (diagnostic): as 1 but with the
                              SIMT attention kernels, so that tests compare the attention tiles inside
                              one tensor-core step */
   int32_t no_attention;   /* ablation: 1 replaces every attention

@@ -64,11 +64,11 @@ class Numerics:
     """How the oracle evaluates the network (SURVEY §8(c) parity metric).
 
     * exact (the default): float64 everywhere -- the definition of the method;
-    * bf16 = True: the tensor-core mode of the GPU path as include/gdp.h defines it
+    * tc = True: the tensor-core mode of the GPU path as include/gdp.h defines it
       (gdp_config.tensor_cores = 1): every dense map Y = X W whose shape the tensor cores take
-      (16 <= width <= 256, K <= 256, >= 128 rows), and its backward dX = dY W^T under the same
-      shape rule, multiplies X and W rounded to bfloat16 (round to nearest even) and
-      accumulates exactly; the segment attention multiplies bf16 Q, K, V and softmax numerators
+      (tc_shape), and its backward dX = dY W^T under the same shape rule, multiplies X and W
+      truncated to tf32 (the upper 19 bits of their fp32 patterns) and accumulates exactly; the
+      segment attention multiplies bf16 (round to nearest even) Q, K, V and softmax numerators
       P (and bf16 dO, dS, P in its backward); everything else (LayerNorm, activations, softmax,
       reductions, weight gradients, the head's forward of width d < 16) stays exact.  With the
       GPU's rounding points reproduced, what remains between the two is accumulation order.
@@ -79,9 +79,9 @@ class Numerics:
       `ties` = {"argmax": [3 x (N, 64) int], "relu": {layer name: bool mask (Kahn order)},
       "relu_v": {...}}; `imported` counts the adopted decisions."""
 
-    def __init__(self, bf16: bool = False, ties: Optional[dict] = None, tie_tol: float = 1e-5,
+    def __init__(self, tc: bool = False, ties: Optional[dict] = None, tie_tol: float = 1e-5,
                  attn_tc: bool = True):
-        self.bf16 = bf16
+        self.tc = tc
         self.attn_tc = attn_tc
         self.ties = ties or {}
         self.tie_tol = tie_tol
@@ -96,36 +96,46 @@ def bf(x: torch.Tensor) -> torch.Tensor:
     return x.to(torch.float32).to(torch.bfloat16).to(x.dtype)
 
 
+def tf32(x: torch.Tensor) -> torch.Tensor:
+    """The tensor core's tf32 operand (include/gdp.h): the value as the GPU holds it (float32)
+    with the low 13 of its 23 mantissa bits cleared -- truncation toward zero to 10 bits."""
+    f = x.to(torch.float32).contiguous()
+    i = f.view(torch.int32) & ~0x1FFF
+    return i.view(torch.float32).to(x.dtype)
+
+
 def tc_shape(M: int, K: int, Nout: int) -> bool:
-    """The tensor cores take Y (M x Nout) = X (M x K) W: 16 <= Nout <= 256, 1 <= K <= 256, M >= 128."""
-    return 16 <= Nout <= 256 and 1 <= K <= 256 and M >= 128
+    """The tensor cores take Y (M x Nout) = X (M x K) W: 16 <= Nout <= 256, 1 <= K <= 256,
+    M >= 128, and W's fp32 tile (K to 32, Nout to 16) fits the kernel's 160 KB."""
+    kp, np_ = -(-K // 32) * 32, -(-Nout // 16) * 16
+    return 16 <= Nout <= 256 and 1 <= K <= 256 and M >= 128 and kp * np_ <= 40960
 
 
-class _DenseBF16(torch.autograd.Function):
-    """y = bf(x) bf(W) + b when the forward shape is a tensor-core shape (fwd_tc); backward
-    dx = bf(dy) bf(W)^T when that shape is one (bwd_tc); dW = x^T dy, db = sum dy exact."""
+class _DenseTC(torch.autograd.Function):
+    """y = tf32(x) tf32(W) + b when the forward shape is a tensor-core shape (fwd_tc); backward
+    dx = tf32(dy) tf32(W)^T when that shape is one (bwd_tc); dW = x^T dy, db = sum dy exact."""
 
     @staticmethod
     def forward(ctx, x, W, b, fwd_tc, bwd_tc):
         ctx.save_for_backward(x, W)
         ctx.bwd_tc = bwd_tc
-        y = (bf(x) @ bf(W)) if fwd_tc else (x @ W)
+        y = (tf32(x) @ tf32(W)) if fwd_tc else (x @ W)
         return y + b
 
     @staticmethod
     def backward(ctx, dy):
         x, W = ctx.saved_tensors
-        dx = (bf(dy) @ bf(W).T) if ctx.bwd_tc else (dy @ W.T)
+        dx = (tf32(dy) @ tf32(W).T) if ctx.bwd_tc else (dy @ W.T)
         return dx, x.T @ dy, dy.sum(0), None, None
 
 
 def dense_map(x: torch.Tensor, W: torch.Tensor, b: torch.Tensor, rows: int, num: Numerics) -> torch.Tensor:
     """x W + b (Eq. 2-3, S:490 dense maps).  `rows` = the rows of the GPU's GEMM for this
-    map (all N nodes), which decides the tensor-core shape rule in bf16 mode."""
-    if not num.bf16:
+    map (all N nodes), which decides the tensor-core shape rule in the tensor-core mode."""
+    if not num.tc:
         return x @ W + b
     K, Nout = W.shape
-    return _DenseBF16.apply(x, W, b, tc_shape(rows, K, Nout), tc_shape(rows, Nout, K))
+    return _DenseTC.apply(x, W, b, tc_shape(rows, K, Nout), tc_shape(rows, Nout, K))
 
 
 class _AttnBF16(torch.autograd.Function):
@@ -351,7 +361,7 @@ def xl_layer(x: torch.Tensor, p: Dict[str, torch.Tensor], n: str, gam: Optional[
 
     def dense(inp, W, b, j):
         gj = g(j)
-        if not num.bf16:
+        if not num.tc:
             return (inp if gj is None else inp * gj) @ W + b
         # the GPU folds the gate into the weight (W' = diag(gamma) W, the same product) and
         # rounds W' for the tensor cores
@@ -371,7 +381,7 @@ def xl_layer(x: torch.Tensor, p: Dict[str, torch.Tensor], n: str, gam: Optional[
         Q = dense(aq, p[f"{n}.Wq"], p[f"{n}.bq"], "q")
         K = dense(ak, p[f"{n}.Wk"], p[f"{n}.bk"], "k")
         V = dense(ak, p[f"{n}.Wv"], p[f"{n}.bv"], "v")
-        if num.bf16 and num.attn_tc and S <= 128:      # the tcgen05 attention tiles take S <= 128
+        if num.tc and num.attn_tc and S <= 128:      # the tcgen05 attention tiles take S <= 128
             outs.append(_AttnBF16.apply(Q, K, V, M < 0 or M > S))
         else:
             outs.append(attention_heads(Q, K, V))
@@ -444,7 +454,7 @@ def place(E: torch.Tensor, p: Dict[str, torch.Tensor], order: Sequence[int], S: 
         gam, gh = [None, None], None
     for l in range(2):
         x = xl_layer(x, p, f"xl{l}", gam[l], S, M, keep, (mem_srcs or {}).get(f"xl{l}"), no_attention, num)
-    if num.bf16:   # the head's forward (width d < 16) is exact; its backward dX is a tensor-core shape
+    if num.tc:   # the head's forward (width d < 16) is exact; its backward dX is a tensor-core shape
         lt = dense_map(x, p["head.W"] if gh is None else gh[:, None] * p["head.W"], p["head.b"], x.shape[0], num)
     else:
         lt = (x if gh is None else x * gh) @ p["head.W"] + p["head.b"]

@@ -2,10 +2,11 @@
 tensor-core mode, fed with the kernel's own inputs.
 
 include/gdp.h defines gdp_config.tensor_cores = 1: every dense map Y = X W (and its backward
-dX = dY W^T) whose shape the tensor cores take multiplies bf16-rounded X and W and accumulates
-in fp32; the segment attention (O7) multiplies bf16 Q, K, V and softmax numerators.
-Given the same fp32 inputs the GPU kernel read, the functions below compute exactly that in
-float64: bf16 rounding of the operands (round to nearest even), exact products and sums.  What
+dX = dY W^T) whose shape the tensor cores take multiplies X and W truncated to tf32 and
+accumulates in fp32; the segment attention (O7) multiplies bf16 Q, K, V and softmax
+numerators.  Given the same fp32 inputs the GPU kernel read, the functions below compute exactly
+that in float64: tf32 truncation (dense maps) or bf16 rounding to nearest even (attention) of
+the operands, exact products and sums.  What
 remains between a kernel and its reference is the fp32 accumulation order -- except where an
 operand of a bf16 product is itself computed here rather than read from the GPU (the attention's
 softmax numerators P~ and its backward's dS, P): there the reference also returns the bound
@@ -20,7 +21,7 @@ from typing import Tuple
 import numpy as np
 import torch
 
-from .model import DH, HEADS, bf, key_range
+from .model import DH, HEADS, bf, key_range, tf32
 
 U_BF16 = 2.0 ** -8
 DT = torch.float64
@@ -31,9 +32,9 @@ def _t(x) -> torch.Tensor:
 
 
 def gemm(X, W, b=None, act: str = "none", R=None) -> np.ndarray:
-    """act(bf(X) bf(W) + b) (+ R): the fused epilogues of the dense maps -- sigmoid (Eq. 2),
+    """act(tf32(X) tf32(W) + b) (+ R): the fused epilogues of the dense maps -- sigmoid (Eq. 2),
     tanh (Eq. 3), relu (FFN, R12), residual add."""
-    y = bf(_t(X)) @ bf(_t(W))
+    y = tf32(_t(X)) @ tf32(_t(W))
     if b is not None:
         y = y + _t(b)
     if act == "sigmoid":

@@ -414,6 +414,7 @@ gdp_status gdp_graph_create(int32_t N, int32_t F, const float *feat, int64_t E, 
   auto *g = new gdp_graph_s();
   g->N = N;
   g->F = F;
+  g->ldX = (F + 3) / 4 * 4;
   g->E = E;
   GDP_CUDA_CHECK(cudaGetDevice(&g->device));
   // out / in CSR
@@ -530,7 +531,12 @@ gdp_status gdp_graph_create(int32_t N, int32_t F, const float *feat, int64_t E, 
     cudaError_t _e = up(reinterpret_cast<void **>(&g->field), (src), (bytes));  \
     if (_e != cudaSuccess) { gdp_graph_destroy(g); return cuda_status(_e, "graph upload"); } \
   } while (0)
-  UP(X, feat, (size_t)N * F * sizeof(float));
+  {
+    std::vector<float> xp((size_t)N * g->ldX, 0.f);   // rows padded to 16 bytes (TMA row stride)
+    for (int v = 0; v < N; v++)
+      for (int f = 0; f < F; f++) xp[(size_t)v * g->ldX + f] = feat[(size_t)v * F + f];
+    UP(X, xp.data(), xp.size() * sizeof(float));
+  }
   UP(nbr_ptr, nptr.data(), (N + 1) * sizeof(int));
   UP(nbr_idx, nidx.data(), nidx.size() * sizeof(int));
   {

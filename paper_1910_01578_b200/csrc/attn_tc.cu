@@ -18,6 +18,7 @@
 #include <cuda_bf16.h>
 
 #include "common.cuh"
+#include "tc_util.cuh"
 
 namespace gdp {
 namespace {
@@ -26,28 +27,8 @@ constexpr int TQ = 128;    // queries per tile (UMMA M)
 constexpr int TKEY = 256;  // keys per tile (UMMA N of Q K^T, K of P V)
 constexpr float kScaleTc = 0.25f;   // 1 / sqrt(16)
 
-__device__ __forceinline__ uint32_t su32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ uint64_t desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
-  uint64_t d = 0;
-  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
-  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
-  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
-  d |= (uint64_t)1 << 46;   // Blackwell descriptor version, SWIZZLE_NONE
-  return d;
-}
-// element (row r, col k) of a canonical K-major tile with Kp columns
-__device__ __forceinline__ uint32_t coff(int r, int k, int Kp) {
-  return (uint32_t)(((r >> 3) * (Kp >> 3) + (k >> 3)) * 128 + (r & 7) * 16 + (k & 7) * 2);
-}
-__device__ __forceinline__ void mbar_wait_parity(uint64_t *mb, uint32_t ph) {
-  uint32_t done = 0;
-  while (!done)
-    asm volatile("{\n\t.reg .pred P1;\n\tmbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
-                 "selp.b32 %0, 1, 0, P1;\n\t}\n"
-                 : "=r"(done)
-                 : "r"(su32(mb)), "r"(ph)
-                 : "memory");
-}
+using tc::su32;
+using tc::tmem_wait_ld;
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float *x) {
   uint32_t v[16];
   asm volatile(
@@ -75,7 +56,6 @@ __device__ __forceinline__ void tmem_ld16_nw(uint32_t taddr, uint32_t *v) {
         "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
       : "r"(taddr));
 }
-__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void reg_fence16(uint32_t *v) {
   asm volatile(""
                : "+r"(v[0]), "+r"(v[1]), "+r"(v[2]), "+r"(v[3]), "+r"(v[4]), "+r"(v[5]), "+r"(v[6]), "+r"(v[7]),
@@ -150,8 +130,8 @@ __global__ void __launch_bounds__(TQ, 4) k_attn_fwd_tc(const float *__restrict__
     }
     uint4 lo8 = make_uint4(pack2(a[0].x, a[0].y), pack2(a[0].z, a[0].w), pack2(a[1].x, a[1].y), pack2(a[1].z, a[1].w));
     uint4 hi8 = make_uint4(pack2(a[2].x, a[2].y), pack2(a[2].z, a[2].w), pack2(a[3].x, a[3].y), pack2(a[3].z, a[3].w));
-    *reinterpret_cast<uint4 *>(sQ + coff(tid, 0, 16)) = lo8;
-    *reinterpret_cast<uint4 *>(sQ + coff(tid, 8, 16)) = hi8;
+    *reinterpret_cast<uint4 *>(sQ + tc::canon_off(tid, 0, 16)) = lo8;
+    *reinterpret_cast<uint4 *>(sQ + tc::canon_off(tid, 8, 16)) = hi8;
   }
   const uint32_t trow_off = (uint32_t)(warp * 32) << 16;
   float m2 = -INFINITY, sum = 0.f, acc[16];
@@ -166,10 +146,10 @@ __global__ void __launch_bounds__(TQ, 4) k_attn_fwd_tc(const float *__restrict__
 #pragma unroll
     for (int h2 = 0; h2 < KR; h2++) {   // K / V rows tid and tid + 128 of this block -> bf16 tiles
       const int j = tid + h2 * TQ;
-      *reinterpret_cast<uint4 *>(sK + coff(j, 0, 16)) =
+      *reinterpret_cast<uint4 *>(sK + tc::canon_off(j, 0, 16)) =
           make_uint4(pack2(kk[h2][0].x, kk[h2][0].y), pack2(kk[h2][0].z, kk[h2][0].w), pack2(kk[h2][1].x, kk[h2][1].y),
                      pack2(kk[h2][1].z, kk[h2][1].w));
-      *reinterpret_cast<uint4 *>(sK + coff(j, 8, 16)) =
+      *reinterpret_cast<uint4 *>(sK + tc::canon_off(j, 8, 16)) =
           make_uint4(pack2(kk[h2][2].x, kk[h2][2].y), pack2(kk[h2][2].z, kk[h2][2].w), pack2(kk[h2][3].x, kk[h2][3].y),
                      pack2(kk[h2][3].z, kk[h2][3].w));
       const float vf[16] = {vv[h2][0].x, vv[h2][0].y, vv[h2][0].z, vv[h2][0].w, vv[h2][1].x, vv[h2][1].y,
@@ -177,7 +157,7 @@ __global__ void __launch_bounds__(TQ, 4) k_attn_fwd_tc(const float *__restrict__
                             vv[h2][3].x, vv[h2][3].y, vv[h2][3].z, vv[h2][3].w};
 #pragma unroll
       for (int c = 0; c < 16; c++)   // V^T: row = head dim c, column = key j
-        *reinterpret_cast<__nv_bfloat16 *>(sV + coff(c, j, TKF)) = __float2bfloat16_rn(vf[c]);
+        *reinterpret_cast<__nv_bfloat16 *>(sV + tc::canon_off(c, j, TKF)) = __float2bfloat16_rn(vf[c]);
     }
     if (kb + TKF < hi) ld_kv(qkv, kb + TKF, min(TKF, hi - kb - TKF), tid, hd, kk, vv);   // in flight meanwhile
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -189,14 +169,14 @@ __global__ void __launch_bounds__(TQ, 4) k_attn_fwd_tc(const float *__restrict__
     // S = Q K^T: M = 128, N = Np, K = 16
     if (tid == 0) {
       const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(Np >> 3) << 17) | ((uint32_t)(TQ >> 4) << 24);
-      const uint64_t ad = desc(su32(sQ), 128, 256), bd = desc(su32(sK), 128, 256);
+      const uint64_t ad = tc::desc_none(su32(sQ), 128, 256), bd = tc::desc_none(su32(sK), 128, 256);
       asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
                    "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem),
                    "l"(ad), "l"(bd), "r"(idesc), "r"(0u));
       asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(&mbar))
                    : "memory");
     }
-    mbar_wait_parity(&mbar, phase);
+    tc::mbar_wait(&mbar, phase);
     phase ^= 1u;
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     // row max of this block (64 columns per TMEM wait), then the rescale of the running sum / output
@@ -247,9 +227,9 @@ __global__ void __launch_bounds__(TQ, 4) k_attn_fwd_tc(const float *__restrict__
             p[jj] = ex2(fmaf(__uint_as_float(x[u][jj]), kC, -m2));
             sum += p[jj];
           }
-          *reinterpret_cast<uint4 *>(sP + coff(tid, c0 + 16 * u, TKF)) =
+          *reinterpret_cast<uint4 *>(sP + tc::canon_off(tid, c0 + 16 * u, TKF)) =
               make_uint4(pack2(p[0], p[1]), pack2(p[2], p[3]), pack2(p[4], p[5]), pack2(p[6], p[7]));
-          *reinterpret_cast<uint4 *>(sP + coff(tid, c0 + 16 * u + 8, TKF)) =
+          *reinterpret_cast<uint4 *>(sP + tc::canon_off(tid, c0 + 16 * u + 8, TKF)) =
               make_uint4(pack2(p[8], p[9]), pack2(p[10], p[11]), pack2(p[12], p[13]), pack2(p[14], p[15]));
         }
       }
@@ -263,9 +243,9 @@ __global__ void __launch_bounds__(TQ, 4) k_attn_fwd_tc(const float *__restrict__
           p[jj] = (c0 + jj < nk) ? ex2(fmaf(x[jj], kC, -m2)) : 0.f;
           sum += p[jj];
         }
-        *reinterpret_cast<uint4 *>(sP + coff(tid, c0, TKF)) =
+        *reinterpret_cast<uint4 *>(sP + tc::canon_off(tid, c0, TKF)) =
             make_uint4(pack2(p[0], p[1]), pack2(p[2], p[3]), pack2(p[4], p[5]), pack2(p[6], p[7]));
-        *reinterpret_cast<uint4 *>(sP + coff(tid, c0 + 8, TKF)) =
+        *reinterpret_cast<uint4 *>(sP + tc::canon_off(tid, c0 + 8, TKF)) =
             make_uint4(pack2(p[8], p[9]), pack2(p[10], p[11]), pack2(p[12], p[13]), pack2(p[14], p[15]));
       }
     }
@@ -278,7 +258,7 @@ __global__ void __launch_bounds__(TQ, 4) k_attn_fwd_tc(const float *__restrict__
       const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(16 >> 3) << 17) | ((uint32_t)(TQ >> 4) << 24);
       const uint32_t sbo = (TKF >> 3) * 128;
       for (int ks = 0; ks < Np / 16; ks++) {
-        const uint64_t ad = desc(su32(sP) + ks * 256, 128, sbo), bd = desc(su32(sV) + ks * 256, 128, sbo);
+        const uint64_t ad = tc::desc_none(su32(sP) + ks * 256, 128, sbo), bd = tc::desc_none(su32(sV) + ks * 256, 128, sbo);
         asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
                      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem),
                      "l"(ad), "l"(bd), "r"(idesc), "r"(ks > 0 ? 1u : 0u));
@@ -286,7 +266,7 @@ __global__ void __launch_bounds__(TQ, 4) k_attn_fwd_tc(const float *__restrict__
       asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(&mbar))
                    : "memory");
     }
-    mbar_wait_parity(&mbar, phase);
+    tc::mbar_wait(&mbar, phase);
     phase ^= 1u;
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     {
@@ -374,17 +354,17 @@ __global__ void __launch_bounds__(TQ, 1) k_attn_bwd_tc(const float *__restrict__
     }
 #pragma unroll
     for (int h8 = 0; h8 < 2; h8++) {
-      *reinterpret_cast<uint4 *>(sQ + coff(tid, 8 * h8, 16)) =
+      *reinterpret_cast<uint4 *>(sQ + tc::canon_off(tid, 8 * h8, 16)) =
           make_uint4(pack2(qf[8 * h8], qf[8 * h8 + 1]), pack2(qf[8 * h8 + 2], qf[8 * h8 + 3]),
                      pack2(qf[8 * h8 + 4], qf[8 * h8 + 5]), pack2(qf[8 * h8 + 6], qf[8 * h8 + 7]));
-      *reinterpret_cast<uint4 *>(sdO + coff(tid, 8 * h8, 16)) =
+      *reinterpret_cast<uint4 *>(sdO + tc::canon_off(tid, 8 * h8, 16)) =
           make_uint4(pack2(gf[8 * h8], gf[8 * h8 + 1]), pack2(gf[8 * h8 + 2], gf[8 * h8 + 3]),
                      pack2(gf[8 * h8 + 4], gf[8 * h8 + 5]), pack2(gf[8 * h8 + 6], gf[8 * h8 + 7]));
     }
 #pragma unroll
     for (int c = 0; c < 16; c++) {   // transposed: row = head dim, column = query
-      *reinterpret_cast<__nv_bfloat16 *>(sQt + coff(c, tid, TQ)) = __float2bfloat16_rn(qf[c]);
-      *reinterpret_cast<__nv_bfloat16 *>(sdOt + coff(c, tid, TQ)) = __float2bfloat16_rn(gf[c]);
+      *reinterpret_cast<__nv_bfloat16 *>(sQt + tc::canon_off(c, tid, TQ)) = __float2bfloat16_rn(qf[c]);
+      *reinterpret_cast<__nv_bfloat16 *>(sdOt + tc::canon_off(c, tid, TQ)) = __float2bfloat16_rn(gf[c]);
     }
   }
 #pragma unroll
@@ -399,13 +379,13 @@ __global__ void __launch_bounds__(TQ, 1) k_attn_bwd_tc(const float *__restrict__
     }
 #pragma unroll
     for (int t = 0; t < 4; t++) reinterpret_cast<float4 *>(sKf + j * 16)[t] = kk[t];
-    *reinterpret_cast<uint4 *>(sK + coff(j, 0, 16)) =
+    *reinterpret_cast<uint4 *>(sK + tc::canon_off(j, 0, 16)) =
         make_uint4(pack2(kk[0].x, kk[0].y), pack2(kk[0].z, kk[0].w), pack2(kk[1].x, kk[1].y), pack2(kk[1].z, kk[1].w));
-    *reinterpret_cast<uint4 *>(sK + coff(j, 8, 16)) =
+    *reinterpret_cast<uint4 *>(sK + tc::canon_off(j, 8, 16)) =
         make_uint4(pack2(kk[2].x, kk[2].y), pack2(kk[2].z, kk[2].w), pack2(kk[3].x, kk[3].y), pack2(kk[3].z, kk[3].w));
-    *reinterpret_cast<uint4 *>(sV + coff(j, 0, 16)) =
+    *reinterpret_cast<uint4 *>(sV + tc::canon_off(j, 0, 16)) =
         make_uint4(pack2(vv[0].x, vv[0].y), pack2(vv[0].z, vv[0].w), pack2(vv[1].x, vv[1].y), pack2(vv[1].z, vv[1].w));
-    *reinterpret_cast<uint4 *>(sV + coff(j, 8, 16)) =
+    *reinterpret_cast<uint4 *>(sV + tc::canon_off(j, 8, 16)) =
         make_uint4(pack2(vv[2].x, vv[2].y), pack2(vv[2].z, vv[2].w), pack2(vv[3].x, vv[3].y), pack2(vv[3].z, vv[3].w));
   }
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -417,14 +397,14 @@ __global__ void __launch_bounds__(TQ, 1) k_attn_bwd_tc(const float *__restrict__
     const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(Np >> 3) << 17) | ((uint32_t)(TQ >> 4) << 24);
     asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
                  "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem),
-                 "l"(desc(su32(sQ), 128, 256)), "l"(desc(su32(sK), 128, 256)), "r"(idesc), "r"(0u));
+                 "l"(tc::desc_none(su32(sQ), 128, 256)), "l"(tc::desc_none(su32(sK), 128, 256)), "r"(idesc), "r"(0u));
     asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
                  "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem + 256u),
-                 "l"(desc(su32(sdO), 128, 256)), "l"(desc(su32(sV), 128, 256)), "r"(idesc), "r"(0u));
+                 "l"(tc::desc_none(su32(sdO), 128, 256)), "l"(tc::desc_none(su32(sV), 128, 256)), "r"(idesc), "r"(0u));
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(&mbar))
                  : "memory");
   }
-  mbar_wait_parity(&mbar, 0);
+  tc::mbar_wait(&mbar, 0);
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
   float dq[16];
@@ -449,8 +429,8 @@ __global__ void __launch_bounds__(TQ, 1) k_attn_bwd_tc(const float *__restrict__
         dq[4 * t + 2] = fmaf(ds, k4.z, dq[4 * t + 2]);
         dq[4 * t + 3] = fmaf(ds, k4.w, dq[4 * t + 3]);
       }
-      *reinterpret_cast<__nv_bfloat16 *>(sPt + coff(j, tid, TQ)) = __float2bfloat16_rn(p);
-      *reinterpret_cast<__nv_bfloat16 *>(sdSt + coff(j, tid, TQ)) = __float2bfloat16_rn(ds);
+      *reinterpret_cast<__nv_bfloat16 *>(sPt + tc::canon_off(j, tid, TQ)) = __float2bfloat16_rn(p);
+      *reinterpret_cast<__nv_bfloat16 *>(sdSt + tc::canon_off(j, tid, TQ)) = __float2bfloat16_rn(ds);
     }
   }
   if (qv) {
@@ -471,18 +451,18 @@ __global__ void __launch_bounds__(TQ, 1) k_attn_bwd_tc(const float *__restrict__
       for (int ks = 0; ks < TQ / 16; ks++) {
         asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
                      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem + 16u * h),
-                     "l"(desc(su32(sdSt) + aoff + ks * 256, 128, sbo)), "l"(desc(su32(sQt) + ks * 256, 128, sbo)),
+                     "l"(tc::desc_none(su32(sdSt) + aoff + ks * 256, 128, sbo)), "l"(tc::desc_none(su32(sQt) + ks * 256, 128, sbo)),
                      "r"(idesc), "r"(ks > 0 ? 1u : 0u));
         asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
                      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem + 32u + 16u * h),
-                     "l"(desc(su32(sPt) + aoff + ks * 256, 128, sbo)), "l"(desc(su32(sdOt) + ks * 256, 128, sbo)),
+                     "l"(tc::desc_none(su32(sPt) + aoff + ks * 256, 128, sbo)), "l"(tc::desc_none(su32(sdOt) + ks * 256, 128, sbo)),
                      "r"(idesc), "r"(ks > 0 ? 1u : 0u));
       }
     }
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(&mbar))
                  : "memory");
   }
-  mbar_wait_parity(&mbar, 1);
+  tc::mbar_wait(&mbar, 1);
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   for (int h = 0; h < halves; h++) {
     float dk[16], dv[16];
@@ -542,14 +522,14 @@ __global__ void __launch_bounds__(TQ, 1) k_attn_bwd_tc(const float *__restrict__
 //     (stop-gradient for x), zeros where no later segment reaches the key.  Every output row is
 //     written exactly once, no atomics.
 __device__ __forceinline__ void st_row16(unsigned char *tile, int r, const float *f) {   // K-major row, Kp = 16
-  *reinterpret_cast<uint4 *>(tile + coff(r, 0, 16)) =
+  *reinterpret_cast<uint4 *>(tile + tc::canon_off(r, 0, 16)) =
       make_uint4(pack2(f[0], f[1]), pack2(f[2], f[3]), pack2(f[4], f[5]), pack2(f[6], f[7]));
-  *reinterpret_cast<uint4 *>(tile + coff(r, 8, 16)) =
+  *reinterpret_cast<uint4 *>(tile + tc::canon_off(r, 8, 16)) =
       make_uint4(pack2(f[8], f[9]), pack2(f[10], f[11]), pack2(f[12], f[13]), pack2(f[14], f[15]));
 }
 __device__ __forceinline__ void st_col16(unsigned char *tile, int r, const float *f) {   // transposed, Kp = 128
 #pragma unroll
-  for (int c = 0; c < 16; c++) *reinterpret_cast<__nv_bfloat16 *>(tile + coff(c, r, TQ)) = __float2bfloat16_rn(f[c]);
+  for (int c = 0; c < 16; c++) *reinterpret_cast<__nv_bfloat16 *>(tile + tc::canon_off(c, r, TQ)) = __float2bfloat16_rn(f[c]);
 }
 __device__ __forceinline__ void ld16(const float *p, float *f) {
 #pragma unroll
@@ -653,11 +633,11 @@ __global__ void __launch_bounds__(TQ, 4) k_attn_bwd_dq_tc(const float *__restric
     sync_for_mma();   // (also: the previous block's dQ has been drained by every warp)
     const uint32_t tmem = tmem_base, trow = tmem + trow_off;
     if (tid == 0) {
-      mma_f16(tmem, desc(su32(sQ), 128, 256), desc(su32(sK), 128, 256), idesc_f16(Np), 0u);
-      mma_f16(tmem + (uint32_t)TKQ, desc(su32(sdO), 128, 256), desc(su32(sV), 128, 256), idesc_f16(Np), 0u);
+      mma_f16(tmem, tc::desc_none(su32(sQ), 128, 256), tc::desc_none(su32(sK), 128, 256), idesc_f16(Np), 0u);
+      mma_f16(tmem + (uint32_t)TKQ, tc::desc_none(su32(sdO), 128, 256), tc::desc_none(su32(sV), 128, 256), idesc_f16(Np), 0u);
       mma_commit(&mbar);
     }
-    mbar_wait_parity(&mbar, phase);
+    tc::mbar_wait(&mbar, phase);
     phase ^= 1u;
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const bool full = nk == TKQ;
@@ -681,19 +661,19 @@ __global__ void __launch_bounds__(TQ, 4) k_attn_bwd_dq_tc(const float *__restric
           ds[jj] = c0 + jj < nk ? d : 0.f;
         }
       }
-      *reinterpret_cast<uint4 *>(sdS + coff(tid, c0, TQ)) =
+      *reinterpret_cast<uint4 *>(sdS + tc::canon_off(tid, c0, TQ)) =
           make_uint4(pack2(ds[0], ds[1]), pack2(ds[2], ds[3]), pack2(ds[4], ds[5]), pack2(ds[6], ds[7]));
-      *reinterpret_cast<uint4 *>(sdS + coff(tid, c0 + 8, TQ)) =
+      *reinterpret_cast<uint4 *>(sdS + tc::canon_off(tid, c0 + 8, TQ)) =
           make_uint4(pack2(ds[8], ds[9]), pack2(ds[10], ds[11]), pack2(ds[12], ds[13]), pack2(ds[14], ds[15]));
     }
     sync_for_mma();   // every row's S / dP read, dS written
     if (tid == 0) {   // dQ_block = dS K: M = 128, N = 16, K = Np keys
       for (int ks = 0; ks < Np / 16; ks++)
-        mma_f16(tmem, desc(su32(sdS) + ks * 256, 128, kSbo128), desc(su32(sKt) + ks * 256, 128, kSbo128),
+        mma_f16(tmem, tc::desc_none(su32(sdS) + ks * 256, 128, kSbo128), tc::desc_none(su32(sKt) + ks * 256, 128, kSbo128),
                 idesc_f16(16), ks > 0 ? 1u : 0u);
       mma_commit(&mbar);
     }
-    mbar_wait_parity(&mbar, phase);
+    tc::mbar_wait(&mbar, phase);
     phase ^= 1u;
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     {
@@ -804,12 +784,12 @@ __global__ void __launch_bounds__(TQ, 3) k_attn_bwd_dkv_tc(const float *__restri
       sync_for_mma();
       const uint32_t tmem = tmem_base, trow = tmem + trow_off;
       if (tid == 0) {   // S^T = K Q^T -> cols [0, Nqp); dP^T = V dO^T -> cols [64, 64 + Nqp)
-        mma_f16(tmem, desc(su32(sK), 128, 256), desc(su32(sQ) + (h0 >> 3) * 256, 128, 256), idesc_f16(Nqp), 0u);
-        mma_f16(tmem + (uint32_t)TQC, desc(su32(sV), 128, 256), desc(su32(sdO) + (h0 >> 3) * 256, 128, 256),
+        mma_f16(tmem, tc::desc_none(su32(sK), 128, 256), tc::desc_none(su32(sQ) + (h0 >> 3) * 256, 128, 256), idesc_f16(Nqp), 0u);
+        mma_f16(tmem + (uint32_t)TQC, tc::desc_none(su32(sV), 128, 256), tc::desc_none(su32(sdO) + (h0 >> 3) * 256, 128, 256),
                 idesc_f16(Nqp), 0u);
         mma_commit(&mbar);
       }
-      mbar_wait_parity(&mbar, phase);
+      tc::mbar_wait(&mbar, phase);
       phase ^= 1u;
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       for (int c0 = 0; c0 < Nqp; c0 += 16) {
@@ -838,27 +818,27 @@ __global__ void __launch_bounds__(TQ, 3) k_attn_bwd_dkv_tc(const float *__restri
 #pragma unroll
           for (int qq = 0; qq < 16; qq++) p[qq] = ds[qq] = 0.f;
         }
-        *reinterpret_cast<uint4 *>(sPt + coff(tid, c0, TQC)) =
+        *reinterpret_cast<uint4 *>(sPt + tc::canon_off(tid, c0, TQC)) =
             make_uint4(pack2(p[0], p[1]), pack2(p[2], p[3]), pack2(p[4], p[5]), pack2(p[6], p[7]));
-        *reinterpret_cast<uint4 *>(sPt + coff(tid, c0 + 8, TQC)) =
+        *reinterpret_cast<uint4 *>(sPt + tc::canon_off(tid, c0 + 8, TQC)) =
             make_uint4(pack2(p[8], p[9]), pack2(p[10], p[11]), pack2(p[12], p[13]), pack2(p[14], p[15]));
-        *reinterpret_cast<uint4 *>(sdSt + coff(tid, c0, TQC)) =
+        *reinterpret_cast<uint4 *>(sdSt + tc::canon_off(tid, c0, TQC)) =
             make_uint4(pack2(ds[0], ds[1]), pack2(ds[2], ds[3]), pack2(ds[4], ds[5]), pack2(ds[6], ds[7]));
-        *reinterpret_cast<uint4 *>(sdSt + coff(tid, c0 + 8, TQC)) =
+        *reinterpret_cast<uint4 *>(sdSt + tc::canon_off(tid, c0 + 8, TQC)) =
             make_uint4(pack2(ds[8], ds[9]), pack2(ds[10], ds[11]), pack2(ds[12], ds[13]), pack2(ds[14], ds[15]));
       }
       sync_for_mma();   // S^T / dP^T consumed, P^T and dS^T written
       if (tid == 0) {   // dK = dS^T Q -> cols [0, 16); dV = P^T dO -> cols [16, 32); K = this chunk's queries
         const uint32_t qt = (uint32_t)(h0 >> 3) * 128;
         for (int ks = 0; ks < Nqp / 16; ks++) {
-          mma_f16(tmem, desc(su32(sdSt) + ks * 256, 128, kSbo64), desc(su32(sQt) + qt + ks * 256, 128, kSbo128),
+          mma_f16(tmem, tc::desc_none(su32(sdSt) + ks * 256, 128, kSbo64), tc::desc_none(su32(sQt) + qt + ks * 256, 128, kSbo128),
                   idesc_f16(16), ks > 0 ? 1u : 0u);
-          mma_f16(tmem + 16u, desc(su32(sPt) + ks * 256, 128, kSbo64), desc(su32(sdOt) + qt + ks * 256, 128, kSbo128),
+          mma_f16(tmem + 16u, tc::desc_none(su32(sPt) + ks * 256, 128, kSbo64), tc::desc_none(su32(sdOt) + qt + ks * 256, 128, kSbo128),
                   idesc_f16(16), ks > 0 ? 1u : 0u);
         }
         mma_commit(&mbar);
       }
-      mbar_wait_parity(&mbar, phase);
+      tc::mbar_wait(&mbar, phase);
       phase ^= 1u;
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       float dk[16], dv[16];

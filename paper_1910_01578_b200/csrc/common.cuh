@@ -40,10 +40,11 @@ gdp_status cuda_status(cudaError_t e, const char *what);
 // ------------------------------------------------------------------ graph / topology
 struct gdp_graph_s {
   int N = 0, F = 0;
+  int ldX = 0;                                      // row stride of X: F rounded up to 4 (16-byte rows for TMA)
   int64_t E = 0, E_sym = 0;
   int device = 0;
   // device arrays (caller node ids)
-  float *X = nullptr;                               // N x F
+  float *X = nullptr;                               // N x ldX (columns F..ldX-1 zero)
   int *nbr_ptr = nullptr, *nbr_idx = nullptr;       // symmetric neighbour CSR (N+1, E_sym)
   int *heavy = nullptr;                             // nodes with more than kHeavyDeg neighbours, ascending
   int n_heavy = 0;

@@ -300,7 +300,7 @@ gdp_status run_embed(const gdp_graph_s *g, const float *theta, float *node_emb, 
   param_offsets(g->F, d, off.o, false);   // the GNN's offsets do not depend on the head
   const int N = g->N;
   // H0 = X W_in + b_in (affine input projection)
-  GemmArgs a = gemm(N, g->F, kH, g->X, g->F, theta + off[GDP_P_GNN_IN_W], kH, 1, w.H[0], kH);
+  GemmArgs a = gemm(N, g->F, kH, g->X, g->ldX, theta + off[GDP_P_GNN_IN_W], kH, 1, w.H[0], kH);
   a.bias = theta + off[GDP_P_GNN_IN_B];
   launch_gemm(a, s);
   for (int l = 0; l < kGNN; l++) {
@@ -461,7 +461,7 @@ gdp_status run_policy_grad(const gdp_graph_s *g, const gdp_config *c, const floa
     launch_gemm(a, s);
     dHn = dH;
   }
-  launch_wgrad(N, g->F, kH, g->X, g->F, g->F, nullptr, 0, dHn, kH, true, w.part, w.part_floats,
+  launch_wgrad(N, g->F, kH, g->X, g->ldX, g->F, nullptr, 0, dHn, kH, true, w.part, w.part_floats,
                grad + off[GDP_P_GNN_IN_W], true, s);
   mark(2);
   GDP_LAUNCH_CHECK("gdp_policy_grad");

@@ -209,3 +209,51 @@ def test_tensor_core_kernels_full_size_c4(gdp):
     W = workloads.config("c4")
     worst = run_kernel_checks(gdp, W.graphs[0], W.d, W.seg_len, W.mem_len, 8, seed=7)
     print({k: round(v, 4) for k, v in worst.items()})
+
+
+def _tf32_rn(x):
+    """tf32 by round-to-nearest-even (the alternative the truncation test rules out)."""
+    f = np.asarray(x, np.float32).copy()
+    i = f.view(np.int32).astype(np.int64)
+    i = (i + 0xFFF + ((i >> 13) & 1)) & ~0x1FFF
+    return i.astype(np.int32).view(np.float32).astype(np.float64)
+
+
+def test_tf32_operand_truncation(gdp):
+    """include/gdp.h defines the tensor-core dense maps' operands as the fp32 patterns truncated
+    to tf32 (upper 19 bits).  The input projection H0 = X W_in + b (N = 300: three row tiles,
+    ragged last, K = 37 = one full and one partial 32-column chunk) on features whose first 8
+    columns have every low mantissa bit set (1 + 2^-10 - 2^-23: truncation gives 1, rounding
+    1 + 2^-10) and W_in rows 0..7 = 1: the GPU must match the truncating reference to fp32
+    accumulation accuracy and miss the rounding one by the 2^-10 steps."""
+    g = workloads.random_dag(300, seed=5)
+    F = workloads.F
+    rng = np.random.default_rng(0)
+    X = rng.normal(size=(g.N, F)).astype(np.float32)
+    X[:, :8] = np.float32(1.0 + (2.0 ** -10 - 2.0 ** -23))
+    th = workloads.init_theta(F, 8, seed=3, mode="random")
+    off, names = 0, {}
+    for name, shape in workloads.param_spec(F, 8):
+        names[name] = (off, shape)
+        off += int(np.prod(shape))
+    o, _ = names["gnn.in.W"]
+    W = th[o:o + F * 64].reshape(F, 64).copy()
+    W[:8, :] = 1.0
+    th[o:o + F * 64] = W.reshape(-1)
+    ob, _ = names["gnn.in.b"]
+    b = th[ob:ob + 64].astype(np.float64)
+    G = gdp.Graph(g, X)
+    cfg = gdp.default_config(8, 128, 128, True, tensor_cores=True)
+    ws = torch.zeros(gdp.workspace_size(G, cfg, 1), dtype=torch.uint8, device="cuda")
+    views = gdp.debug_tensors(G, cfg, ws)
+    emb = torch.empty(g.N, 64, device="cuda")
+    gdp.gdp_embed(G, cfg, torch.from_numpy(th).cuda(), emb, ws)
+    torch.cuda.synchronize()
+    H0 = views["H0"].cpu().numpy().astype(np.float64)
+    tX = Mo.tf32(torch.as_tensor(X.astype(np.float64))).numpy()
+    tW = Mo.tf32(torch.as_tensor(W.astype(np.float64))).numpy()
+    terms = np.abs(tX) @ np.abs(tW) + np.abs(b)
+    e_tr = float((np.abs(H0 - (tX @ tW + b)) / terms).max())
+    e_rn = float((np.abs(H0 - (_tf32_rn(X) @ _tf32_rn(W) + b)) / terms).max())
+    assert e_tr <= 2.0 ** -17, (e_tr, e_rn)
+    assert e_rn > 2.0 ** -14, (e_tr, e_rn)

@@ -11,7 +11,7 @@ Tolerances (BASELINE.json north_star):
     (gdp_debug_tensors), counted in the assertion message;
   * bf16 tensor-core mode: every tcgen05 kernel elementwise at rtol 2e-2 on its own inputs
     (tests/test_gpu_kernels.py); the chained step against the oracle that reproduces the bf16
-    rounding points (oracle.Numerics(bf16=True), tie import at 2^-8) within a relative L2
+    rounding points (oracle.Numerics(tc=True), tie import at 2^-8) within a relative L2
     error of 2e-2 for embeddings, logits and gradient.
 """
 import numpy as np
@@ -28,7 +28,7 @@ pytestmark = pytest.mark.gpu
 
 RTOL = 1e-4
 TC_RTOL = 2e-2
-BF16_TIE = 2.0 ** -8   # tie-import margin in bf16 mode: one bf16 unit
+TC_TIE = 2.0 ** -8   # tie-import margin in bf16 mode: one bf16 unit
 
 
 def close_bound(x, r, bound, rtol=RTOL, floor=1e-2):
@@ -413,7 +413,7 @@ def test_full_size_c4_chain_tc(gdp):
     B = 8
     r = run_step(gdp, g, W.d, W.seg_len, W.mem_len, True, B, th, tc=True)
     pg = oracle.prepare(g, r["X"])
-    num = oracle.Numerics(bf16=True, ties=r["ties"], tie_tol=BF16_TIE)
+    num = oracle.Numerics(tc=True, ties=r["ties"], tie_tol=TC_TIE)
     assert rel_l2(r["emb"], oracle.embed(pg, th, W.d, num)) < TC_RTOL
     assert rel_l2(r["logits"], oracle.place(pg, th, r["emb"], W.d, W.seg_len, W.mem_len, True, num=num)) < TC_RTOL
     U = Osa.uniforms(g.N, B, 42, 0, 0)
@@ -421,7 +421,7 @@ def test_full_size_c4_chain_tc(gdp):
     assert not ((D != r["D"]) & (margin >= 1e-5)).any()
     t = workloads.topology(g, W.d)
     assert_cost_equal(g, t, r["D"], cost_gpu(gdp, g, t, r["D"]))
-    numg = oracle.Numerics(bf16=True, ties=r["ties"], tie_tol=BF16_TIE)
+    numg = oracle.Numerics(tc=True, ties=r["ties"], tie_tol=TC_TIE)
     grad, _ = oracle.policy_grad(pg, th, W.d, W.seg_len, W.mem_len, True, r["D"], r["adv"], loss_scale=1.0 / B,
                                  num=numg)
     e = rel_l2(r["grad"], grad)
@@ -432,7 +432,7 @@ def test_full_size_c4_chain_tc(gdp):
 @pytest.mark.parametrize("case", ["c2", "mem_inf_big", "seg_ragged", "short_mem"])
 def test_tensor_core_mode(gdp, case):
     """The chained step in tensor-core mode (bf16 operands, fp32 accumulation) against the oracle
-    that reproduces the mode's rounding points (oracle.Numerics(bf16=True)) with tie import at
+    that reproduces the mode's rounding points (oracle.Numerics(tc=True)) with tie import at
     one bf16 unit: embeddings, logits and gradient within a relative L2 error of 2e-2 (BASELINE
     north_star).  Elementwise, each kernel of this chain is held at 2e-2 on its own inputs in
     tests/test_gpu_kernels.py; chained, a rounding boundary that the oracle's float64 operand and
@@ -452,10 +452,10 @@ def test_tensor_core_mode(gdp, case):
     B = 16
     r = run_step(gdp, g, d, S, M, True, B, th, tc=True)
     pg = oracle.prepare(g, r["X"])
-    num = oracle.Numerics(bf16=True, ties=r["ties"], tie_tol=BF16_TIE)
+    num = oracle.Numerics(tc=True, ties=r["ties"], tie_tol=TC_TIE)
     e_emb = rel_l2(r["emb"], oracle.embed(pg, th, d, num))
     e_log = rel_l2(r["logits"], oracle.place(pg, th, r["emb"], d, S, M, True, num=num))
-    numg = oracle.Numerics(bf16=True, ties=r["ties"], tie_tol=BF16_TIE)
+    numg = oracle.Numerics(tc=True, ties=r["ties"], tie_tol=TC_TIE)
     grad, _ = oracle.policy_grad(pg, th, d, S, M, True, r["D"], r["adv"], loss_scale=1.0 / B, entropy_coef=0.01,
                                  num=numg)
     e_g = rel_l2(r["grad"], grad)
@@ -485,9 +485,9 @@ def test_tensor_core_attention_matches_simt(gdp, case):
     for tc, attn_tc in ((1, True), (2, False)):         # tensor_cores = 2: SIMT attention
         r = run_step(gdp, g, d, S, M, True, B, th, tc=tc)
         pg = oracle.prepare(g, r["X"])
-        num = oracle.Numerics(bf16=True, ties=r["ties"], tie_tol=BF16_TIE, attn_tc=attn_tc)
+        num = oracle.Numerics(tc=True, ties=r["ties"], tie_tol=TC_TIE, attn_tc=attn_tc)
         e_log = rel_l2(r["logits"], oracle.place(pg, th, r["emb"], d, S, M, True, num=num))
-        numg = oracle.Numerics(bf16=True, ties=r["ties"], tie_tol=BF16_TIE, attn_tc=attn_tc)
+        numg = oracle.Numerics(tc=True, ties=r["ties"], tie_tol=TC_TIE, attn_tc=attn_tc)
         grad, _ = oracle.policy_grad(pg, th, d, S, M, True, r["D"], r["adv"], loss_scale=1.0 / B,
                                      entropy_coef=0.01, num=numg)
         e_g = rel_l2(r["grad"], grad)

@@ -450,3 +450,17 @@ def test_kahn_order_with_id_ties():
     # no edges: ascending ids; two disjoint chains interleave by id
     assert Mo.topo_order(3, np.zeros((0, 2), dtype=np.int64)) == [0, 1, 2]
     assert Mo.topo_order(4, np.array([[2, 0], [3, 1]])) == [2, 0, 3, 1]
+
+
+def test_tf32_truncation_pins():
+    """The tensor-core mode's tf32 operand (include/gdp.h): the fp32 value with its low 13
+    mantissa bits cleared.  Pinned on hand values: representable values are unchanged, bits
+    below 2^-10 of the leading one are dropped toward zero for either sign, and tiny / large
+    exponents are kept (tf32 has fp32's 8-bit exponent)."""
+    x = torch.tensor([1.0, 1.0 + 2 ** -10, 1.0 + 2 ** -10 + 2 ** -11, 1.0 + 2 ** -11 + 2 ** -23,
+                      -(1.5 + 2 ** -12), 3.0 * 2 ** -120, 2.0 ** 100 * (1 + 2 ** -20), 0.0], dtype=torch.float64)
+    want = [1.0, 1.0 + 2 ** -10, 1.0 + 2 ** -10, 1.0, -1.5, 3.0 * 2 ** -120, 2.0 ** 100, 0.0]
+    assert Mo.tf32(x).tolist() == want
+    # the tensor-core shape rule: W's fp32 tile (K to 32, width to 16) must fit 160 KB
+    assert Mo.tc_shape(128, 256, 160) and not Mo.tc_shape(128, 256, 176)
+    assert Mo.tc_shape(128, 64, 256) and not Mo.tc_shape(127, 64, 256) and not Mo.tc_shape(128, 64, 8)

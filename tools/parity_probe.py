@@ -44,13 +44,13 @@ def probe(name, g, d, S, M, sup, B, th, tc, na=False, act=0):
     pg = oracle.prepare(g, r["X"])
     bf = bool(tc)
     tol = 4e-3 if bf else 1e-5
-    num = oracle.Numerics(bf16=bf, ties=r["ties"], tie_tol=tol, attn_tc=(tc == 1))
+    num = oracle.Numerics(tc=bf, ties=r["ties"], tie_tol=tol, attn_tc=(tc == 1))
     E = oracle.embed(pg, r_th := th, d, num)
     z = oracle.place(pg, th, r["emb"], d, S, M, sup, no_attention=na, num=num)
-    num2 = oracle.Numerics(bf16=bf, ties=r["ties"], tie_tol=tol, attn_tc=(tc == 1))
+    num2 = oracle.Numerics(tc=bf, ties=r["ties"], tie_tol=tol, attn_tc=(tc == 1))
     gr, _ = oracle.policy_grad(pg, th, d, S, M, sup, r["D"], r["adv"], loss_scale=1.0 / B, entropy_coef=0.01,
                                no_attention=na, active=act or None, num=num2)
-    num0 = oracle.Numerics(bf16=bf, attn_tc=(tc == 1))
+    num0 = oracle.Numerics(tc=bf, attn_tc=(tc == 1))
     gr0, _ = oracle.policy_grad(pg, th, d, S, M, sup, r["D"], r["adv"], loss_scale=1.0 / B, entropy_coef=0.01,
                                 no_attention=na, active=act or None, num=num0)
     print(f"{name:22s} tc={tc} N={g.N} embed {err(r['emb'], E)} logits {err(r['logits'], z)} "
