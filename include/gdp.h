@@ -71,9 +71,11 @@ typedef struct {
                              1 <= K <= 256, ceil32(K) * ceil16(width) <= 40960 and >= 128 rows on
                              tcgen05 tensor cores with tf32 operands -- the fp32 bit patterns of X and
                              W truncated to their upper 19 bits (sign, exponent, 10 mantissa bits) --
-                             and fp32 accumulation in TMEM; the segment attention on tcgen05 tiles
-                             with bf16 Q, K, V and softmax numerators; weight gradients (reductions
-                             over nodes) stay fp32.  2 (diagnostic): as 1 but with the
+                             and fp32 accumulation in TMEM; the weight gradients dW = X^T dY of the
+                             maps with 16 <= width <= 256, K <= 256 and >= 128 rows likewise (tf32
+                             X and dY, fp32 accumulation; the bias row an fp32 column sum); the
+                             segment attention on tcgen05 tiles with bf16 Q, K, V and softmax
+                             numerators.  2 (diagnostic): as 1 but with the
                              SIMT attention kernels, so that tests compare the attention tiles inside
                              one tensor-core step */
   int32_t no_attention;   /* ablation: 1 replaces every attention

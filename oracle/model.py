@@ -67,10 +67,11 @@ class Numerics:
     * tc = True: the tensor-core mode of the GPU path as include/gdp.h defines it
       (gdp_config.tensor_cores = 1): every dense map Y = X W whose shape the tensor cores take
       (tc_shape), and its backward dX = dY W^T under the same shape rule, multiplies X and W
-      truncated to tf32 (the upper 19 bits of their fp32 patterns) and accumulates exactly; the
-      segment attention multiplies bf16 (round to nearest even) Q, K, V and softmax numerators
+      truncated to tf32 (the upper 19 bits of their fp32 patterns) and accumulates exactly, and
+      so does the weight gradient dW = X^T dY under tc_wgrad_shape; the segment attention
+      multiplies bf16 (round to nearest even) Q, K, V and softmax numerators
       P (and bf16 dO, dS, P in its backward); everything else (LayerNorm, activations, softmax,
-      reductions, weight gradients, the head's forward of width d < 16) stays exact.  With the
+      the other reductions, the head's forward and weight gradient of width d < 16) stays exact.  With the
       GPU's rounding points reproduced, what remains between the two is accumulation order.
     * tie import (`ties`): where the oracle's own decision is within `tie_tol` of a kink -- a
       max-pool channel whose top-2 margin is below tie_tol * max(1, |top|), a ReLU input within
@@ -104,6 +105,12 @@ def tf32(x: torch.Tensor) -> torch.Tensor:
     return i.view(torch.float32).to(x.dtype)
 
 
+def tc_wgrad_shape(M: int, K: int, Nout: int) -> bool:
+    """The tensor cores take the weight gradient dW = X^T dY (X: M x K, dY: M x Nout):
+    16 <= Nout <= 256, 1 <= K <= 256, M >= 128."""
+    return 16 <= Nout <= 256 and 1 <= K <= 256 and M >= 128
+
+
 def tc_shape(M: int, K: int, Nout: int) -> bool:
     """The tensor cores take Y (M x Nout) = X (M x K) W: 16 <= Nout <= 256, 1 <= K <= 256,
     M >= 128, and W's fp32 tile (K to 32, Nout to 16) fits the kernel's 160 KB."""
@@ -113,12 +120,14 @@ def tc_shape(M: int, K: int, Nout: int) -> bool:
 
 class _DenseTC(torch.autograd.Function):
     """y = tf32(x) tf32(W) + b when the forward shape is a tensor-core shape (fwd_tc); backward
-    dx = tf32(dy) tf32(W)^T when that shape is one (bwd_tc); dW = x^T dy, db = sum dy exact."""
+    dx = tf32(dy) tf32(W)^T when that shape is one (bwd_tc); dW = tf32(x)^T tf32(dy) when the
+    weight-gradient shape is one (w_tc), else exact; db = sum dy exact."""
 
     @staticmethod
-    def forward(ctx, x, W, b, fwd_tc, bwd_tc):
+    def forward(ctx, x, W, b, fwd_tc, bwd_tc, w_tc):
         ctx.save_for_backward(x, W)
         ctx.bwd_tc = bwd_tc
+        ctx.w_tc = w_tc
         y = (tf32(x) @ tf32(W)) if fwd_tc else (x @ W)
         return y + b
 
@@ -126,7 +135,8 @@ class _DenseTC(torch.autograd.Function):
     def backward(ctx, dy):
         x, W = ctx.saved_tensors
         dx = (tf32(dy) @ tf32(W).T) if ctx.bwd_tc else (dy @ W.T)
-        return dx, x.T @ dy, dy.sum(0), None, None
+        dW = (tf32(x).T @ tf32(dy)) if ctx.w_tc else (x.T @ dy)
+        return dx, dW, dy.sum(0), None, None, None
 
 
 def dense_map(x: torch.Tensor, W: torch.Tensor, b: torch.Tensor, rows: int, num: Numerics) -> torch.Tensor:
@@ -135,7 +145,7 @@ def dense_map(x: torch.Tensor, W: torch.Tensor, b: torch.Tensor, rows: int, num:
     if not num.tc:
         return x @ W + b
     K, Nout = W.shape
-    return _DenseTC.apply(x, W, b, tc_shape(rows, K, Nout), tc_shape(rows, Nout, K))
+    return _DenseTC.apply(x, W, b, tc_shape(rows, K, Nout), tc_shape(rows, Nout, K), tc_wgrad_shape(rows, K, Nout))
 
 
 class _AttnBF16(torch.autograd.Function):

@@ -31,6 +31,11 @@ def _t(x) -> torch.Tensor:
     return torch.as_tensor(np.asarray(x, dtype=np.float64))
 
 
+def tf32_np(x) -> np.ndarray:
+    """tf32 truncation (model.tf32) of an array, as float64."""
+    return tf32(_t(x)).numpy()
+
+
 def gemm(X, W, b=None, act: str = "none", R=None) -> np.ndarray:
     """act(tf32(X) tf32(W) + b) (+ R): the fused epilogues of the dense maps -- sigmoid (Eq. 2),
     tanh (Eq. 3), relu (FFN, R12), residual add."""

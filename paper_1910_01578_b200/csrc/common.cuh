@@ -189,6 +189,11 @@ bool no_attention();
 void launch_wgrad(int M, int K, int Nout, const float *X1, int ldx1, int K1, const float *X2, int ldx2,
                   const float *dY, int ldy, bool with_bias, float *part, size_t part_floats, float *out,
                   bool accumulate, cudaStream_t s);
+// tensor-core mode (tc_wgrad.cu): the same partials by tcgen05 (tf32 X and dY, fp32 accumulation;
+// the bias row an fp32 column sum); returns the chunk count written to part, 0 if not launched
+bool wgrad_tc_eligible(int M, int K, int Nout);
+int launch_wgrad_tc(int M, int K, int Nout, const float *X1, int ldx1, int K1, const float *X2, int ldx2,
+                    const float *dY, int ldy, bool with_bias, float *part, size_t part_floats, cudaStream_t s);
 
 void launch_layernorm(const float *x, const float *g, const float *b, float *y, float *mu, float *rs, int N,
                       cudaStream_t s);

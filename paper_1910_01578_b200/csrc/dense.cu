@@ -344,6 +344,15 @@ void launch_wgrad(int M, int K, int Nout, const float *X1, int ldx1, int K1, con
                   const float *dY, int ldy, bool with_bias, float *part, size_t part_floats, float *out,
                   bool accumulate, cudaStream_t s) {
   const int Kaug = K + (with_bias ? 1 : 0);
+  if (t_tc && wgrad_tc_eligible(M, K, Nout)) {   // tensor-core mode: tcgen05 split-K (tc_wgrad.cu)
+    const int chunks = launch_wgrad_tc(M, K, Nout, X1, ldx1, K1, X2, ldx2, dY, ldy, with_bias, part, part_floats, s);
+    if (chunks > 0) {
+      const int count = Kaug * Nout;
+      note_launch("k_reduce_chunks", s);
+      k_reduce_chunks<<<nblk(count, 256), 256, 0, s>>>(part, chunks, count, out, accumulate ? 1 : 0);
+      return;
+    }
+  }
   const int gx = (K + BM - 1) / BM, gy = (Nout + BN - 1) / BN;
   // about 3 blocks per SM (the launch bound), within the partial buffer, at least WK rows per chunk
   long long want = (3LL * num_sms_dense() + gx * gy - 1) / (gx * gy);

@@ -94,13 +94,6 @@ template <int N>
 __device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory"); }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
-__device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, int x, int y, uint64_t *mb) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
-          su32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(su32(mb))
-      : "memory");
-}
 
 // one 8-column group of row m: bias, activation / mask, residual, store (or accumulate)
 template <int EPI>
@@ -523,32 +516,8 @@ int num_sms() {
   return n;
 }
 
-PFN_cuTensorMapEncodeTiled_v12000 encoder() {
-  static PFN_cuTensorMapEncodeTiled_v12000 f = nullptr;
-  static bool tried = false;
-  if (!tried) {
-    tried = true;
-    cudaDriverEntryPointQueryResult q;
-    void *p = nullptr;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      f = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-  }
-  return f;
-}
-
-// 2-D fp32 map over rows x cols (row stride ld floats), box brows rows x 32 columns, SWIZZLE_128B;
-// out-of-range rows / columns read as zero and are not written
 bool make_map(CUtensorMap *m, const float *base, int cols, int rows, int ld, int brows) {
-  PFN_cuTensorMapEncodeTiled_v12000 enc = encoder();
-  if (!enc || !base || (reinterpret_cast<uintptr_t>(base) & 15) || (ld % 4) || cols < 1 || rows < 1) return false;
-  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
-  cuuint64_t strides[1] = {(cuuint64_t)ld * 4};
-  cuuint32_t box[2] = {(cuuint32_t)KC, (cuuint32_t)brows};
-  cuuint32_t es[2] = {1, 1};
-  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(base), dims, strides, box, es,
-             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  return tc::tma_map_f32(m, base, cols, rows, ld, brows);
 }
 
 template <int EPI>
@@ -562,6 +531,37 @@ void launch_epi(const Maps &mp, const GemmArgs &a, const TfParams &p, int grid, 
 }
 
 }  // namespace
+
+namespace tc {
+namespace {
+PFN_cuTensorMapEncodeTiled_v12000 encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 f = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    cudaDriverEntryPointQueryResult q;
+    void *p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      f = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return f;
+}
+}  // namespace
+
+bool tma_map_f32(CUtensorMap *m, const float *base, int cols, int rows, int ld, int brows, bool atom32) {
+  PFN_cuTensorMapEncodeTiled_v12000 enc = encoder();
+  if (!enc || !base || (reinterpret_cast<uintptr_t>(base) & 15) || (ld % 4) || cols < 1 || rows < 1) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * 4};
+  cuuint32_t box[2] = {32u, (cuuint32_t)brows};
+  cuuint32_t es[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(base), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE,
+             atom32 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+}  // namespace tc
 
 bool tc_eligible(const GemmArgs &a) {
   const int Kp = (a.K + KC - 1) / KC * KC, Np = (a.Nout + 15) / 16 * 16;

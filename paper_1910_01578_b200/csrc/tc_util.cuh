@@ -1,6 +1,7 @@
 // Shared PTX helpers of the tcgen05 kernels (tc_gemm.cu, attn_tc.cu): shared-window addresses,
 // UMMA shared-memory descriptors, mbarriers, TMEM loads.
 #pragma once
+#include <cuda.h>
 #include <stdint.h>
 
 namespace gdp {
@@ -65,6 +66,22 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t *v) {
                : "r"(taddr));
 }
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+// TMA: one 2-D box of `map` at (column x, row y) into shared memory, completing on mbarrier mb
+__device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, int x, int y, uint64_t *mb) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          su32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(su32(mb))
+      : "memory");
+}
+
+// host: 2-D fp32 tensor map over rows x cols (row stride ld floats), box brows rows x 32 columns
+// (128 bytes), SWIZZLE_128B (16-byte granule g of row r at g ^ (r % 8)) or, with atom32,
+// SWIZZLE_128B_ATOM_32B (32-byte granule g of row r at g ^ (r % 4): the only MN-major layout the
+// tf32 MMA takes); out-of-range rows / columns read as zero and are not written.  False if TMA
+// cannot take the tensor (alignment) or the driver entry point is missing.
+bool tma_map_f32(CUtensorMap *m, const float *base, int cols, int rows, int ld, int brows, bool atom32 = false);
 
 }  // namespace tc
 }  // namespace gdp

@@ -1,16 +1,17 @@
 """Per-kernel parity of the tensor-core mode on the kernel's own inputs.
 
 After one embed -> place -> sample -> policy_grad step in tensor-core mode (gdp_config.tensor_cores
-= 1: tcgen05 GEMMs and attention tiles, bf16 operands), every intermediate the workspace holds
-(gdp_debug_tensors) is recomputed by oracle/tc.py from the GPU's own inputs to that kernel --
-the same fp32 operands, rounded to bf16 the same way -- and compared elementwise:
+= 1: tcgen05 GEMMs and weight gradients with tf32 operands, attention tiles with bf16 operands),
+every intermediate the workspace holds (gdp_debug_tensors) is recomputed by oracle/tc.py from
+the GPU's own inputs to that kernel -- the same fp32 operands, truncated to tf32 / rounded to
+bf16 the same way -- and compared elementwise:
 
-    |x - r| <= rtol * max(|r|, 1e-2 * max|r|) + bound,     rtol = 2e-2 (BASELINE north_star, bf16)
+    |x - r| <= rtol * max(|r|, 1e-2 * max|r|) + bound,     rtol = 2e-2 (BASELINE north_star, tensor cores)
 
 where `bound` = 2^-8 * sum |terms| only for products whose bf16 operand the oracle computes itself
 (attention P~, dS, P; SURVEY §8(c) "c u sum|terms|"), else 0.  fp32 SIMT kernels in the same
-step (LayerNorm, gates, folding, the head, weight gradients, max-pool) use rtol 1e-4; the
-max-pool values and argmax indices are bit-exact.  Cases: C2 (79 row tiles per map) and C4 at
+step (LayerNorm, gates, folding, the head, bias rows, max-pool) use rtol 1e-4; the max-pool
+values and argmax indices are bit-exact.  Cases: C2 (79 row tiles per map) and C4 at
 full size (408 tiles of the 192/256-wide maps for 296 CTA slots: the persistent multi-tile loop
 of k_gemm_tc).
 """
@@ -25,7 +26,7 @@ import workloads
 
 pytestmark = pytest.mark.gpu
 
-RT = 2e-2      # bf16 tensor-core kernels
+RT = 2e-2      # tensor-core kernels (tf32 dense maps, bf16 attention)
 RS = 1e-4      # fp32 SIMT kernels
 FLOOR = 1e-2
 
@@ -168,14 +169,22 @@ def run_kernel_checks(gdp, g, d, S, M, B, seed=13):
         worst[k] = check(k, v, ref[k], RT, bound=bnd[k])
     worst["da"] = check("da", b["da"], Otc.gemm(b["dqkv"], f["L0.Wqkv"].T), RT)
     worst["dam"] = check("dam", b["dam"], Otc.gemm(b["dkvm"], f["L0.Wqkv"][:, 64:].T), RT)
-    # weight gradients of the conditioner's folded maps (fp32 SIMT k_wgrad, bias row last)
-    aug = lambda a: np.concatenate([a.astype(np.float64), np.ones((N, 1))], 1)
-    worst["dW2"] = check("dW2", b["L0.dW2"], aug(f["L0.m"]).T @ dy.astype(np.float64), RS)
-    worst["dW1"] = check("dW1", b["L0.dW1"], aug(f["L0.c"]).T @ b["dm"].astype(np.float64), RS)
-    worst["dWo"] = check("dWo", b["L0.dWo"], aug(f["L0.o"]).T @ b["dx1"].astype(np.float64), RS)
+    # weight gradients of the conditioner's folded maps (k_wgrad_tc: tf32 X and dY, fp32
+    # accumulation; the bias row -- last -- an fp32 column sum)
+    def wgrad(name, got, X, dY):
+        X = np.asarray(X, np.float64)
+        dY = np.asarray(dY, np.float64)
+        if Mo.tc_wgrad_shape(N, X.shape[1], dY.shape[1]):
+            w = check(name, got[:-1], Otc.tf32_np(X).T @ Otc.tf32_np(dY), RT)
+        else:
+            w = check(name, got[:-1], X.T @ dY, RS)
+        return max(w, check(name + ".b", got[-1], dY.sum(0), RS))
+    worst["dW2"] = wgrad("dW2", b["L0.dW2"], f["L0.m"], dy)
+    worst["dW1"] = wgrad("dW1", b["L0.dW1"], f["L0.c"], b["dm"])
+    worst["dWo"] = wgrad("dWo", b["L0.dWo"], f["L0.o"], b["dx1"])
     dkvt = b["dqkv"].astype(np.float64).copy()
     dkvt[:, 64:] += b["dkvm"]
-    worst["dWqkv"] = check("dWqkv", b["L0.dWqkv"], aug(f["L0.a"]).T @ dkvt, RS)
+    worst["dWqkv"] = wgrad("dWqkv", b["L0.dWqkv"], f["L0.a"], dkvt)
     return worst
 
 
