@@ -111,7 +111,10 @@ __device__ __forceinline__ int cdst(int ci) {
 }
 
 struct Smem5 {
-  Q5 cc[NCH][KC5];                  // channel rings (arr, u set)
+  Q5 chd[NCH];                      // each channel's head entry in full (the consumer's queue fields;
+                                    // fetched by a bulk copy of its out-edge slot when it becomes the head)
+  int2 cq[NCH][KC5];                // channel rings, compact: (out-edge slot, arrival tick)
+  unsigned long long hbar[NCH];     // mbarrier of each channel's head fetch
   Slot5 stage[8][2][SO5];           // out-edge slots of the running / next op of each device
   unsigned sdev[8][2][SO5];         // the 4 bytes of the placement's slot-device array holding each slot's
   Q5 fc[8][KF5];                    // FIFO rings
@@ -143,7 +146,7 @@ __host__ __device__ inline Scratch5 scratch5_layout(int N, long long E, int ngbi
   s.fifo = s.gbig + al(4 * (size_t)(ngbig > 0 ? ngbig : 1));
   s.ov = s.fifo + al(sizeof(Q5) * (size_t)N);
   s.chq = s.ov + al(sizeof(Q5) * (size_t)N);
-  s.total = s.chq + al(sizeof(Q5) * (size_t)(E > 0 ? E : 1));
+  s.total = s.chq + al(sizeof(int2) * (size_t)(E > 0 ? E : 1));
   return s;
 }
 
@@ -176,6 +179,26 @@ __device__ __forceinline__ void cp_32(void *s, const void *g) {
 __device__ __forceinline__ void cp_4(void *s, const void *g) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"((unsigned)__cvta_generic_to_shared(s)), "l"(g)
                : "memory");
+}
+// a channel's new head: its out-edge slot (32 bytes) copied by the bulk-copy engine, completing
+// on the channel's mbarrier (independent of the cp.async groups of the staging copies)
+__device__ __forceinline__ void head_fetch(Q5 *dst, const Slot5 *src, unsigned long long *mb) {
+  const unsigned m = (unsigned)__cvta_generic_to_shared(mb);
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], 32;" ::"r"(m) : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 32, [%2];" ::"r"(
+                   (unsigned)__cvta_generic_to_shared(dst)),
+               "l"(src), "r"(m)
+               : "memory");
+}
+__device__ __forceinline__ void head_wait(unsigned long long *mb, unsigned ph) {
+  unsigned done = 0;
+  const unsigned m = (unsigned)__cvta_generic_to_shared(mb);
+  while (!done)
+    asm volatile("{\n\t.reg .pred P1;\n\tmbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+                 "selp.b32 %0, 1, 0, P1;\n\t}\n"
+                 : "=r"(done)
+                 : "r"(m), "r"(ph)
+                 : "memory");
 }
 // shared-memory words addressed by their 32-bit shared-window address (computed once per kernel)
 __device__ __forceinline__ unsigned atoms_xor(unsigned a, unsigned x) {
@@ -305,7 +328,10 @@ __global__ void __launch_bounds__(512) k_cost5_pre(Cost5Graph G, TopoArgs T, con
 // simulation warp would share sub-partitions 0 and 2 while 1 and 3 hold the mostly sleeping memory
 // warps; so successive CTAs on the same (SM, sub-partition pair) alternate the simulating warp.
 __device__ unsigned g_c5_pair[2 * 1024];
-__global__ void __launch_bounds__(64) k_cost5(Cost5Graph G, TopoArgs T, const uint8_t *__restrict__ Dall,
+#ifndef COST5_MINB
+#define COST5_MINB 12
+#endif
+__global__ void __launch_bounds__(64, COST5_MINB) k_cost5(Cost5Graph G, TopoArgs T, const uint8_t *__restrict__ Dall,
                                               unsigned char *scratch, size_t per_place, gdp_sim_report *rep,
                                               long long *peak_out, long long *busy_out, double *reward) {
   __shared__ Smem5 S;                                       // fixed state (static: direct addressing)
@@ -325,14 +351,19 @@ __global__ void __launch_bounds__(64) k_cost5(Cost5Graph G, TopoArgs T, const ui
   int *gbig = reinterpret_cast<int *>(base + L.gbig);
   Q5 *fifo_g = reinterpret_cast<Q5 *>(base + L.fifo);
   Q5 *ov_g = reinterpret_cast<Q5 *>(base + L.ov);
-  Q5 *chq_g = reinterpret_cast<Q5 *>(base + L.chq);
+  int2 *chq_g = reinterpret_cast<int2 *>(base + L.chq);
 
   // ------------------------------------------------------------ prologue (both warps)
   {
     for (int i = tid; i < G.nflagw; i += 64) flags[i] = 0u;
     for (int i = tid; i < G.nbigb; i += 64) bigb[i] = G.bigb0[i];
     for (int i = tid; i < RI5; i += 64) S.items[i] = 1ull << 32;   // lap parity 1: empty for lap 0
-    if (tid < NCH) { S.ch[tid] = make_int4(0, 0, 0, 0); S.ca[tid] = INF; }
+    if (tid < NCH) {
+      S.ch[tid] = make_int4(0, 0, 0, 0);
+      S.ca[tid] = INF;
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((unsigned)__cvta_generic_to_shared(&S.hbar[tid])));
+    }
+    if (tid == 0) asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     if (tid < 8) { S.dv[tid] = make_int4(INF, 0, 0, 0); S.dv2[tid] = make_int4(0, -1, T.speed[tid], 0); }
     if (tid == 0) {
       S.mhead = 0; S.mk = 0; S.disp = 0; S.oom = 0;
@@ -378,6 +409,7 @@ __global__ void __launch_bounds__(64) k_cost5(Cost5Graph G, TopoArgs T, const ui
     unsigned spend = 0;                 // this lane's staging copies in flight (bit 2k + slot)
     unsigned itail = 0, mcache = 0;     // items appended; memory-warp head as last read
     unsigned incm = 0;                  // devices with ops made available at this instant
+    unsigned long long hpn = 0, hph = 0;  // channels with a head fetch in flight; their mbarrier phases
 #ifdef COST5_PROF
     long long prof[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0}, plast = clock64();
 #endif
@@ -461,16 +493,27 @@ __global__ void __launch_bounds__(64) k_cost5(Cost5Graph G, TopoArgs T, const ui
           else { c = 2 * (__ffs(m1) - 1) + 1; m1 &= m1 - 1; }
           const int4 cs = S.ch[c];
           const int h = cs.z, tail = cs.x, s = h & (KC5 - 1), q = cdst(c);
-          Q5 r;
-          load_q5(r, &S.cc[c][s]);
-          S.ch[c].z = h + 1;
-          if (h + KC5 < tail) {   // the slot takes position h + KC5 from the global overflow (rare)
-            Q5 x;
-            load_q5(x, chq_g + S.coff[c] + h + KC5);
-            store_q5(&S.cc[c][s], x);
+          const unsigned long long cb = 1ull << c;
+          if (hpn & cb) {   // the head's record was fetched when it became the head (>= 1 instant ago)
+            head_wait(&S.hbar[c], (unsigned)((hph >> c) & 1ull));
+            hph ^= cb;
+            hpn &= ~cb;
           }
-          S.ca[c] = h + 1 < tail ? S.cc[c][(h + 1) & (KC5 - 1)].arr : INF;
-          item(IT_ALLOC_COPY, q, r.u);
+          Q5 r;
+          load_q5(r, &S.chd[c]);   // queue fields (arr / u are not used: the slot's bytes)
+          const int e = S.cq[c][s].x;
+          S.ch[c].z = h + 1;
+          if (h + KC5 < tail) S.cq[c][s] = chq_g[S.coff[c] + h + KC5];   // from the global overflow (rare)
+          if (h + 1 < tail) {   // a new head: its arrival, and its record from the out-edge slot
+            const int2 nx = S.cq[c][(h + 1) & (KC5 - 1)];
+            S.ca[c] = nx.y;
+            __syncwarp();   // every lane has read chd[c] before the copy overwrites it
+            if (lane == 0) head_fetch(&S.chd[c], G.slots + nx.x, &S.hbar[c]);
+            hpn |= cb;
+          } else {
+            S.ca[c] = INF;
+          }
+          item(IT_ALLOC_COPY, q, e);   // the memory warp reads the copy's bytes from slot e
           if (arrive_u(r.cinfo)) to_inc(q, r);
         }
         P5(1);
@@ -539,9 +582,10 @@ __global__ void __launch_bounds__(64) k_cost5(Cost5Graph G, TopoArgs T, const ui
                 const int x = xfer_time3(e.bytes, 8 * k + tw, T);
                 const int bt = max(t, f);
                 const int pos = tail + rank, arr = bt + (rank + 1) * x;
-                const Q5 q = q_of_slot(e, arr, r.id);
-                if (pos < hd + KC5) store_q5(&S.cc[c][pos & (KC5 - 1)], q);
-                else store_q5(chq_g + S.coff[c] + pos, q);
+                const int2 ce = make_int2(r.ob + j, arr);
+                if (pos < hd + KC5) S.cq[c][pos & (KC5 - 1)] = ce;
+                else chq_g[S.coff[c] + pos] = ce;
+                if (pos == hd) store_q5(&S.chd[c], q_of_slot(e, arr, r.id));   // an empty channel's new head
                 if (rank == 0) {
                   *reinterpret_cast<int2 *>(&S.ch[c]) = make_int2(tail + n, bt + n * x);   // tail, free
                   if (tail == hd) S.ca[c] = bt + x;   // the channel was empty: a new head
@@ -677,7 +721,8 @@ __global__ void __launch_bounds__(64) k_cost5(Cost5Graph G, TopoArgs T, const ui
       long long xA = 0, xB = 0, bu = 0;
       int du = 0;
       if (mine) {
-        if (kind == IT_ALLOC_OP || kind == IT_ALLOC_COPY) { dA = dev; xA = G.out_bytes[idx]; }
+        if (kind == IT_ALLOC_OP) { dA = dev; xA = G.out_bytes[idx]; }
+        else if (kind == IT_ALLOC_COPY) { dA = dev; xA = G.slots[idx].bytes; }   // idx = the copy's out-edge slot
         else if (kind == IT_SINK) { dA = dev; xA = -G.out_bytes[idx]; }
         else if (kind == IT_INEDGE) {
           const IRec ir = G.irec[idx];
@@ -765,6 +810,7 @@ bool cost5_eligible(const TopoArgs &T, const Cost5Graph &G, int min_cost, long l
 int cost5_wave(const Cost5Graph &G) {
   const size_t smem = cost5_smem_bytes(G.nflagw, G.nbigb);
   if (sizeof(Smem5) + smem > 227 * 1024) return 0;
+  cudaFuncSetAttribute(k_cost5, cudaFuncAttributePreferredSharedMemoryCarveout, 100);   // all of it shared
   if (smem + sizeof(Smem5) > 48 * 1024)
     cudaFuncSetAttribute(k_cost5, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int occ = 0, dev = 0, nsm = 0;
@@ -781,6 +827,11 @@ bool launch_cost5(const Cost5Graph &G, const TopoArgs &T, int min_cost, long lon
   if (per_place < cost5_scratch_per_placement(G.N, G.E, G.ngbig)) return false;
   const size_t smem = cost5_smem_bytes(G.nflagw, G.nbigb);
   static size_t configured = 0;
+  static bool carve = false;
+  if (!carve) {
+    cudaFuncSetAttribute(k_cost5, cudaFuncAttributePreferredSharedMemoryCarveout, 100);   // all of it shared
+    carve = true;
+  }
   if (smem + sizeof(Smem5) > 48 * 1024 && smem > configured) {
     cudaFuncSetAttribute(k_cost5, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     configured = smem;

@@ -9,7 +9,7 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --c
     python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e --no-kernels > gpurun_out/launches_bench.log 2>&1
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:'k_cost5$' -s 1 -c 1 -o gpurun_out/prof_cost \
     python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e --no-kernels > gpurun_out/prof_cost.log 2>&1
-python tools/ncu_to_json.py gpurun_out/prof_cost.ncu-rep gpurun_out/cost_kernel_ncu.json k_cost5 c4_gnmt52k_d8 1480 \
+python tools/ncu_to_json.py gpurun_out/prof_cost.ncu-rep gpurun_out/cost_kernel_ncu.json k_cost5 c4_gnmt52k_d8 1776 \
   "ncu --set full --import-source on --clock-control none -k regex:k_cost5$ -s 1 -c 1 python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e (tools/_g9.sh, round 2)" > gpurun_out/ncu_json.log 2>&1
 timeout 600 python bench.py --config c4_64k --no-cpu-baseline --no-e2e --steps 3 > gpurun_out/rows/c4_64k.json 2>/dev/null
 timeout 600 python bench.py --config c4 --mem-len -1 --no-cpu-baseline --no-e2e --steps 3 > gpurun_out/rows/c4_mem_inf.json 2>/dev/null
