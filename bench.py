@@ -245,7 +245,7 @@ def run_train(args, W, gdp, dev):
     print(json.dumps({"metric": "GDP-one PPO training updates/s (16 rollouts, 4 epochs x 2 minibatches)",
                       "value": 1000.0 / ms, "unit": "updates/s", "n_gpus": 1, "steps": args.steps,
                       "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-                      "dtype": "f32" if args.fp32 else "bf16xbf16->f32 dense maps / f32",
+                      "dtype": "f32" if args.fp32 else "tf32->f32 dense maps + weight grads / bf16 attention / f32",
                       "data": "synthetic", "gpu_launches": (gdp.launch_count() - l0) // args.steps,
                       "config": {"workload": W.name, "graph": g.name, "nodes": g.N, "devices_d": W.d}}))
 
@@ -474,7 +474,8 @@ def main():
         out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
                "scaling": "weak" if mode == "samples" else "strong", "vs_baseline": None,
-               "dtype": ("f32" if args.fp32 else "bf16xbf16->f32 (tcgen05 dense maps) / f32") + " policy, i32 cost model", "data": "synthetic",
+               "dtype": ("f32" if args.fp32 else "tf32->f32 (tcgen05 dense maps, weight grads) / bf16 (tcgen05 attention) / f32")
+               + " policy, i32 cost model", "data": "synthetic",
                "config": config_json(W, argparse.Namespace(batch=W.batch, gpus=world), mode),
                "clocks": clk.summary(), "gpu_launches": int(launches), "roofline": roof, "e2e": e2e,
                "cpu_baseline": cpu, "kernels": kernels,
