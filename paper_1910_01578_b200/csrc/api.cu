@@ -573,6 +573,7 @@ gdp_status gdp_graph_create(int32_t N, int32_t F, const float *feat, int64_t E, 
     g->ngbig5 = (int)h5.gbig.size();
     g->nflagw5 = h5.nflagw;
     UP(slots5, h5.slots.data(), h5.slots.size() * sizeof(Slot5));
+    UP(ebytes5, h5.ebytes.data(), h5.ebytes.size() * sizeof(long long));
     UP(srcq5, h5.srcq.data(), h5.srcq.size() * sizeof(Q5));
     UP(gbig5, h5.gbig.data(), h5.gbig.size() * sizeof(int));
     UP(outdeg5, h5.outdeg.data(), h5.outdeg.size() * sizeof(int));
@@ -587,7 +588,7 @@ gdp_status gdp_graph_destroy(gdp_graph g) {
   if (!g) return GDP_OK;
   void *ptrs[] = {g->X, g->nbr_ptr, g->nbr_idx, g->heavy, g->out_ptr, g->out_idx, g->out_src, g->in_ptr, g->in_idx,
                   g->cost, g->out_bytes, g->mem_bytes, g->perm, g->leader, g->nrec, g->erec, g->irec,
-                  g->cnt0, g->bigid, g->big_in, g->big_out, g->slots5, g->srcq5, g->gbig5, g->outdeg5,
+                  g->cnt0, g->bigid, g->big_in, g->big_out, g->slots5, g->srcq5, g->ebytes5, g->gbig5, g->outdeg5,
                   g->bigb5};
   for (void *p : ptrs)
     if (p) cudaFree(p);

@@ -69,7 +69,7 @@ struct gdp_graph_s {
   int nbig = 0;
   // k_cost5 records (cost5.cu)
   bool c5_ok = false;
-  void *slots5 = nullptr, *srcq5 = nullptr;
+  void *slots5 = nullptr, *srcq5 = nullptr, *ebytes5 = nullptr;
   int *gbig5 = nullptr, *outdeg5 = nullptr;
   unsigned *bigb5 = nullptr;
   int nsrc5 = 0, nbigb5 = 0, ngbig5 = 0, nflagw5 = 0;
@@ -172,10 +172,7 @@ bool tensor_cores_on();
 bool tensor_core_attention_on();
 bool attn_fwd_tc_eligible(int S, int M);
 void launch_attn_fwd_tc(const float *qkv, float *o, float *lse, int N, int S, int M, cudaStream_t s);
-bool attn_bwd_tc_eligible(int S, int M);
-void launch_attn_bwd_tc(const float *qkv, const float *o, const float *lse, const float *dout, float *dqkv,
-                        float *dkvm, int N, int S, int M, cudaStream_t s);
-bool attn_bwd_tc_long_eligible(int S, int M);   // M > S or M = inf: query-major dQ + key-major dK / dV
+bool attn_bwd_tc_long_eligible(int S, int M);   // any M: query-major dQ + key-major dK / dV
 void launch_attn_bwd_dq_tc(const float *qkv, const float *o, const float *lse, const float *dout, float *dqkv, int N,
                            int S, int M, cudaStream_t s);
 void launch_attn_bwd_dkv_tc(const float *qkv, const float *o, const float *lse, const float *dout, float *dqkv,
@@ -197,11 +194,13 @@ int launch_wgrad_tc(int M, int K, int Nout, const float *X1, int ldx1, int K1, c
 
 void launch_layernorm(const float *x, const float *g, const float *b, float *y, float *mu, float *rs, int N,
                       cudaStream_t s);
-// dx (+)= LN backward of da; param grads from (da + da_extra) accumulated into dgb[0..63] (gain) and
-// dgb[64..127] (bias).
+// dx (+)= LN backward of da (+ res, nullable: the residual branch); param grads from (da + da_extra)
+// accumulated into dgb[0..63] (gain) and dgb[64..127] (bias).
 void launch_layernorm_bwd(const float *x, const float *mu, const float *rs, const float *g, const float *da,
-                          const float *da_extra, float *dx, bool dx_accumulate, float *dgb, float *part,
-                          int N, cudaStream_t s);
+                          const float *da_extra, float *dx, bool dx_accumulate, const float *res, float *dgb,
+                          float *part, int N, cudaStream_t s);
+// dkvt = [dQ | dK_own + dK_mem | dV_own + dV_mem] (16-byte aligned rows)
+void launch_dkvt(const float *dqkv, const float *dkvm, float *dkvt, int N, cudaStream_t s);
 void launch_colsum(const float *x, int N, int C, float scale, float *out, float *part, cudaStream_t s);
 
 // nnz = ptr[N] (symmetric neighbour entries), used only for the algorithmic byte count;
@@ -222,8 +221,6 @@ void launch_rows_gather(const float *src, const int *perm, float *dst, int N, in
 void launch_rows_scatter(const float *src, const int *perm, float *dst, int N, int C, bool accumulate,
                          cudaStream_t s);
 void launch_tanh_grad(const float *dHn, const float *Hn, float *dP, int n, cudaStream_t s);
-void launch_add(const float *a, int lda, const float *b, int ldb, float *c, int ldc, int rows, int cols,
-                cudaStream_t s);
 void launch_fill_rows(float *dst, const float *row, float scale, int N, int C, cudaStream_t s);
 
 // sampling / loss

@@ -438,6 +438,7 @@ static Cost5Graph cost5_graph(const gdp_graph_s *g) {
   Cost5Graph C;
   C.N = g->N; C.E = g->E; C.ok = g->c5_ok ? 1 : 0;
   C.slots = static_cast<const Slot5 *>(g->slots5); C.srcq = static_cast<const Q5 *>(g->srcq5);
+  C.ebytes = static_cast<const long long *>(g->ebytes5);
   C.irec = static_cast<const IRec *>(g->irec);
   C.out_idx = g->out_idx; C.out_src = g->out_src; C.cost = g->cost; C.leader = g->leader;
   C.outdeg = g->outdeg5; C.gbig0 = g->gbig5; C.bigb0 = g->bigb5;

@@ -46,6 +46,7 @@ struct __align__(16) Slot5 {  // out-edge slot e = (v -> w), out-CSR order, 32 b
 struct Cost5Host {            // host images built at graph creation (cost5_build)
   bool ok = false;
   std::vector<Slot5> slots;
+  std::vector<long long> ebytes;   // per out-edge slot: the producer's output bytes (k_cost5_pre, contiguous)
   std::vector<Q5> srcq;        // the sources, ascending id
   std::vector<int> gbig, outdeg;
   std::vector<unsigned> bigb;  // 4-bit counters (in-degree 3..15), 8 per word, 16-byte padded
@@ -56,6 +57,7 @@ struct Cost5Graph {
   long long E;
   int ok;
   const Slot5 *slots;
+  const long long *ebytes;
   const Q5 *srcq;
   const IRec *irec;
   const int *out_idx, *out_src, *cost, *leader, *outdeg, *gbig0;

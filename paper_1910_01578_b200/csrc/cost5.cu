@@ -236,15 +236,20 @@ __device__ __forceinline__ unsigned long long item5(int t, int kind, int dev, in
 // One CTA per placement: static memory / busy time / op count per device, co-location and
 // malformed flags, the device of every out-edge slot's consumer (one byte per slot, out-CSR
 // order), cross bytes and per-channel transfer counts (the sizes of the global overflow
-// regions), consumer counters of the memory warp, global input counters.
+// regions), consumer counters of the memory warp, global input counters.  The placement row
+// (N bytes) is staged in shared memory with 16-byte loads when it fits (dynamic shared memory
+// = N rounded to 16; 0 = read from global), so the random D[u] / D[w] reads of the edge pass hit
+// shared memory; the edge pass takes 4 consecutive slots per thread (16-byte loads of the
+// producer / consumer ids, one 32-bit store of their 4 device bytes).
 __global__ void __launch_bounds__(512) k_cost5_pre(Cost5Graph G, TopoArgs T, const uint8_t *__restrict__ Dall,
-                                                   unsigned char *scratch, size_t per_place) {
+                                                   unsigned char *scratch, size_t per_place, int dsm) {
+  extern __shared__ __align__(16) uint8_t sD[];
   __shared__ unsigned long long s_stat[8], s_busy[8], s_cross;
   __shared__ int s_cnt[8], s_ch[64], s_flag;
   __shared__ int s_chw[16][64];   // per-warp channel counts (no contention on 64 addresses)
   const int N = G.N, d = T.d, b = blockIdx.x, tid = threadIdx.x, lane = tid & 31;
   const unsigned FULL = 0xffffffffu;
-  const uint8_t *D = Dall + (size_t)b * N;
+  const uint8_t *Dg = Dall + (size_t)b * N;
   const Scratch5 L = scratch5_layout(N, G.E, G.ngbig);
   unsigned char *base = scratch + (size_t)b * per_place;
   Pre5 *pre = reinterpret_cast<Pre5 *>(base + L.pre);
@@ -255,14 +260,24 @@ __global__ void __launch_bounds__(512) k_cost5_pre(Cost5Graph G, TopoArgs T, con
   if (tid < 64) s_ch[tid] = 0;
   for (int i = tid; i < 16 * 64; i += blockDim.x) (&s_chw[0][0])[i] = 0;
   if (tid == 0) { s_cross = 0; s_flag = 0; }
+  if (dsm) {   // the row into shared memory (B x N rows are 16-byte aligned when N % 16 == 0)
+    if ((reinterpret_cast<uintptr_t>(Dg) & 15) == 0) {
+      const int n16 = N / 16;
+      for (int i = tid; i < n16; i += blockDim.x) reinterpret_cast<uint4 *>(sD)[i] = __ldg(reinterpret_cast<const uint4 *>(Dg) + i);
+      for (int v = 16 * n16 + tid; v < N; v += blockDim.x) sD[v] = Dg[v];
+    } else {
+      for (int v = tid; v < N; v += blockDim.x) sD[v] = Dg[v];
+    }
+  }
   __syncthreads();
+  const uint8_t *D = dsm ? sD : Dg;
   {
     long long lm[8], lb[8];
     int lc[8], flag = 0;
 #pragma unroll
     for (int k = 0; k < 8; k++) { lm[k] = 0; lb[k] = 0; lc[k] = 0; }
     for (int v = tid; v < N; v += blockDim.x) {
-      int k = __ldg(D + v);
+      int k = D[v];
       if (k >= d) { flag |= 2; k = 0; }
       const long long mb = G.mem_bytes[v];
       const long long du = (long long)G.cost[v] * T.speed[k];
@@ -286,15 +301,25 @@ __global__ void __launch_bounds__(512) k_cost5_pre(Cost5Graph G, TopoArgs T, con
   }
   {
     long long lcross = 0;
-    for (long long e = tid; e < G.E; e += blockDim.x) {
-      const int u = G.out_src[e], w = G.out_idx[e];
-      const int su = __ldg(D + u), tw = __ldg(D + w);
-      sdev[e] = (uint8_t)tw;
+    int *chw = s_chw[(tid >> 5) & 15];
+    auto edge = [&](long long e, int u, int w) -> unsigned {
+      const int su = D[u], tw = D[w];
       if (su != tw && su < d && tw < d) {
-        atomicAdd(&s_chw[(tid >> 5) & 15][su * 8 + tw], 1);
-        lcross += G.out_bytes[u];
+        atomicAdd(&chw[su * 8 + tw], 1);
+        lcross += __ldg(G.ebytes + e);
       }
+      return (unsigned)tw;
+    };
+    const long long E4 = G.E / 4;
+    const int4 *src4 = reinterpret_cast<const int4 *>(G.out_src), *idx4 = reinterpret_cast<const int4 *>(G.out_idx);
+    for (long long q = tid; q < E4; q += blockDim.x) {   // 4 slots per thread
+      const int4 u = __ldg(src4 + q), w = __ldg(idx4 + q);
+      const long long e = 4 * q;
+      const unsigned b0 = edge(e, u.x, w.x), b1 = edge(e + 1, u.y, w.y), b2 = edge(e + 2, u.z, w.z),
+                     b3 = edge(e + 3, u.w, w.w);
+      reinterpret_cast<unsigned *>(sdev)[q] = b0 | (b1 << 8) | (b2 << 16) | (b3 << 24);
     }
+    for (long long e = 4 * E4 + tid; e < G.E; e += blockDim.x) sdev[e] = (uint8_t)edge(e, G.out_src[e], G.out_idx[e]);
     lcross = warp_sum_ll(lcross);
     if (lane == 0 && lcross) atomicAdd(&s_cross, (unsigned long long)lcross);
   }
@@ -836,8 +861,15 @@ bool launch_cost5(const Cost5Graph &G, const TopoArgs &T, int min_cost, long lon
     cudaFuncSetAttribute(k_cost5, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     configured = smem;
   }
+  // the pre-pass stages the placement row in shared memory when it fits (up to 160 KB)
+  const int dsm = G.N <= 160 * 1024 ? (G.N + 15) / 16 * 16 : 0;
+  static int pre_configured = 0;
+  if (dsm > 48 * 1024 && dsm > pre_configured) {
+    cudaFuncSetAttribute(k_cost5_pre, cudaFuncAttributeMaxDynamicSharedMemorySize, dsm);
+    pre_configured = dsm;
+  }
   note_launch("k_cost5_pre", s);
-  k_cost5_pre<<<B, 512, 0, s>>>(G, T, D, scratch, per_place);
+  k_cost5_pre<<<B, 512, dsm, s>>>(G, T, D, scratch, per_place, dsm);
   note_launch("k_cost5", s);
   k_cost5<<<B, 64, smem, s>>>(G, T, D, scratch, per_place, rep, peak, busy, reward);
   return true;
@@ -848,6 +880,7 @@ gdp_status cost5_build(int N, long long E, const int *optr, const int *oidx, con
                        const long long *out_bytes, Cost5Host *h) {
   h->ok = N < (1 << 25) && E < (1LL << 25);
   h->slots.assign((size_t)std::max<long long>(E, 1), Slot5{});
+  h->ebytes.assign((size_t)std::max<long long>(E, 1), 0);
   h->srcq.clear();
   h->bigb.clear();
   h->gbig.clear();
@@ -874,6 +907,7 @@ gdp_status cost5_build(int N, long long E, const int *optr, const int *oidx, con
       Slot5 &s = h->slots[(size_t)e];
       s.w = w.id; s.cost = w.cost; s.ob = w.ob; s.nn = w.nn; s.cinfo = w.cinfo; s.ib = w.ib;
       s.bytes = out_bytes[v];   // the producer's output: the size of the copy on this edge
+      h->ebytes[(size_t)e] = out_bytes[v];
     }
   h->nflagw = (nf + 31) / 32;
   while (nibs.size() % 32) nibs.push_back(0);

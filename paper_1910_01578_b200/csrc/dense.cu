@@ -177,12 +177,16 @@ __global__ void __launch_bounds__(NT, 3) k_wgrad(int M, int K, int Kaug, int Nou
   }
 }
 
+// out[e] (+)= sum over chunks of part[c][e]: one warp per output, lane l sums chunks l, l + 32, ...
+// in order, then a fixed xor butterfly (deterministic; every chunk's load in flight at once)
 __global__ void k_reduce_chunks(const float *part, int chunks, int count, float *out, int accumulate) {
-  int e = blockIdx.x * blockDim.x + threadIdx.x;
+  const int e = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (e >= count) return;
   float s = 0.f;
-  for (int c = 0; c < chunks; c++) s += part[(size_t)c * count + e];
-  out[e] = accumulate ? out[e] + s : s;
+  for (int c = lane; c < chunks; c += 32) s += part[(size_t)c * count + e];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) out[e] = accumulate ? out[e] + s : s;
 }
 
 // ---- LayerNorm: one warp per row of 64 (2 values per lane)
@@ -210,9 +214,10 @@ __global__ void k_layernorm(const float *x, const float *g, const float *b, floa
   }
 }
 
-constexpr int LN_ROWS = 256;  // rows per block (fixed => deterministic partials)
+constexpr int LN_ROWS = 64;   // rows per block (fixed => deterministic partials; ~5 blocks per SM at C4)
 __global__ void k_layernorm_bwd(const float *x, const float *mu, const float *rs, const float *g,
-                                const float *da, const float *dae, float *dx, int dx_acc, float *part, int N) {
+                                const float *da, const float *dae, float *dx, int dx_acc, const float *res,
+                                float *part, int N) {
   __shared__ float red[8][128];
   int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   int r0 = blockIdx.x * LN_ROWS, r1 = min(N, r0 + LN_ROWS);
@@ -237,6 +242,10 @@ __global__ void k_layernorm_bwd(const float *x, const float *mu, const float *rs
       float s1 = warp_sum(dh0 + dh1) * (1.0f / kH);
       float s2 = warp_sum(dh0 * xh0 + dh1 * xh1) * (1.0f / kH);
       float r0v = rr * (dh0 - s1 - xh0 * s2), r1v = rr * (dh1 - s1 - xh1 * s2);
+      if (res) {   // the residual branch's gradient (x1 = x + ..., y = x1 + ...)
+        r0v += res[o + lane];
+        r1v += res[o + lane + 32];
+      }
       if (dx_acc) {
         dx[o + lane] += r0v;
         dx[o + lane + 32] += r1v;
@@ -295,11 +304,19 @@ __global__ void k_tanh_grad(const float *dHn, const float *Hn, float *dP, size_t
   float h = Hn[e];
   dP[e] = dHn[e] * (1.f - h * h);
 }
-__global__ void k_add(const float *a, int lda, const float *b, int ldb, float *c, int ldc, int rows, int cols) {
-  size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= (size_t)rows * cols) return;
-  int r = (int)(e / cols), k = (int)(e % cols);
-  c[(size_t)r * ldc + k] = a[(size_t)r * lda + k] + b[(size_t)r * ldb + k];
+// dkvt = [dQ | dK_own + dK_mem | dV_own + dV_mem] (N x 192) from dqkv (N x 192) and dkvm (N x 128),
+// one float4 per thread
+__global__ void k_dkvt(const float4 *dqkv, const float4 *dkvm, float4 *dkvt, int N) {
+  const size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (size_t)N * 48) return;
+  const size_t r = e / 48;
+  const int c = (int)(e % 48);
+  float4 v = dqkv[e];
+  if (c >= 16) {
+    const float4 m = dkvm[r * 32 + (c - 16)];
+    v.x += m.x; v.y += m.y; v.z += m.z; v.w += m.w;
+  }
+  dkvt[e] = v;
 }
 __global__ void k_fill_rows(float *dst, const float *row, float scale, int N, int C) {
   size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -349,7 +366,7 @@ void launch_wgrad(int M, int K, int Nout, const float *X1, int ldx1, int K1, con
     if (chunks > 0) {
       const int count = Kaug * Nout;
       note_launch("k_reduce_chunks", s);
-      k_reduce_chunks<<<nblk(count, 256), 256, 0, s>>>(part, chunks, count, out, accumulate ? 1 : 0);
+      k_reduce_chunks<<<nblk((size_t)count * 32, 256), 256, 0, s>>>(part, chunks, count, out, accumulate ? 1 : 0);
       return;
     }
   }
@@ -365,7 +382,7 @@ void launch_wgrad(int M, int K, int Nout, const float *X1, int ldx1, int K1, con
   k_wgrad<<<grid, NT, 0, s>>>(M, K, Kaug, Nout, X1, ldx1, K1, X2, ldx2, dY, ldy, part, rpc);
   int count = Kaug * Nout;
   note_launch("k_reduce_chunks", s);
-  k_reduce_chunks<<<nblk(count, 256), 256, 0, s>>>(part, chunks, count, out, accumulate ? 1 : 0);
+  k_reduce_chunks<<<nblk((size_t)count * 32, 256), 256, 0, s>>>(part, chunks, count, out, accumulate ? 1 : 0);
 }
 
 void launch_layernorm(const float *x, const float *g, const float *b, float *y, float *mu, float *rs, int N,
@@ -375,13 +392,13 @@ void launch_layernorm(const float *x, const float *g, const float *b, float *y, 
 }
 
 void launch_layernorm_bwd(const float *x, const float *mu, const float *rs, const float *g, const float *da,
-                          const float *da_extra, float *dx, bool dx_accumulate, float *dgb, float *part,
-                          int N, cudaStream_t s) {
+                          const float *da_extra, float *dx, bool dx_accumulate, const float *res, float *dgb,
+                          float *part, int N, cudaStream_t s) {
   int chunks = (N + LN_ROWS - 1) / LN_ROWS;
   note_launch("k_layernorm_bwd", s);
-  k_layernorm_bwd<<<chunks, 256, 0, s>>>(x, mu, rs, g, da, da_extra, dx, dx_accumulate ? 1 : 0, part, N);
+  k_layernorm_bwd<<<chunks, 256, 0, s>>>(x, mu, rs, g, da, da_extra, dx, dx_accumulate ? 1 : 0, res, part, N);
   note_launch("k_reduce_chunks", s);
-  k_reduce_chunks<<<1, 128, 0, s>>>(part, chunks, 128, dgb, 1);
+  k_reduce_chunks<<<nblk(128 * 32, 256), 256, 0, s>>>(part, chunks, 128, dgb, 1);
 }
 
 void launch_colsum(const float *x, int N, int C, float scale, float *out, float *part, cudaStream_t s) {
@@ -405,10 +422,11 @@ void launch_tanh_grad(const float *dHn, const float *Hn, float *dP, int n, cudaS
   note_launch("k_tanh_grad", s);
   k_tanh_grad<<<nblk(n, 256), 256, 0, s>>>(dHn, Hn, dP, (size_t)n);
 }
-void launch_add(const float *a, int lda, const float *b, int ldb, float *c, int ldc, int rows, int cols,
-                cudaStream_t s) {
-  note_launch("k_add", s);
-  k_add<<<nblk((size_t)rows * cols, 256), 256, 0, s>>>(a, lda, b, ldb, c, ldc, rows, cols);
+void launch_dkvt(const float *dqkv, const float *dkvm, float *dkvt, int N, cudaStream_t s) {
+  note_launch("k_dkvt", s);
+  k_dkvt<<<nblk((size_t)N * 48, 256), 256, 0, s>>>(reinterpret_cast<const float4 *>(dqkv),
+                                                    reinterpret_cast<const float4 *>(dkvm),
+                                                    reinterpret_cast<float4 *>(dkvt), N);
 }
 void launch_fill_rows(float *dst, const float *row, float scale, int N, int C, cudaStream_t s) {
   note_launch("k_fill_rows", s);

@@ -454,12 +454,7 @@ void launch_attn_fwd(const float *qkv, float *o, float *lse, int N, int S, int M
 void launch_attn_bwd(const float *qkv, const float *o, const float *lse, const float *dout, float *dqkv,
                      float *dkvm, float *Dd, int N, int S, int M, cudaStream_t s) {
   int nseg = (N + S - 1) / S;
-  if (tensor_core_attention_on() && attn_bwd_tc_eligible(S, M) && attn_tc_grid_ok(N, S)) {   // tensor-core mode, M <= S (attn_tc.cu)
-    note_launch("k_attn_bwd_tc", s, 4.0 * (double)N * (192 + 64 + 64 + kHeads + 192 + 128), 2.5 * attn_flops(N, S, M));
-    launch_attn_bwd_tc(qkv, o, lse, dout, dqkv, dkvm, N, S, M, s);
-    return;
-  }
-  if (tensor_core_attention_on() && attn_bwd_tc_long_eligible(S, M) && attn_tc_grid_ok(N, S)) {   // M > S (attn_tc.cu)
+  if (tensor_core_attention_on() && attn_bwd_tc_long_eligible(S, M) && attn_tc_grid_ok(N, S)) {   // tensor-core mode (attn_tc.cu)
     note_launch("k_attn_bwd_dq_tc", s, 4.0 * (double)N * (192 + 64 + 64 + kHeads + 64), attn_flops(N, S, M));
     launch_attn_bwd_dq_tc(qkv, o, lse, dout, dqkv, N, S, M, s);
     note_launch("k_attn_bwd_dkv_tc", s, 4.0 * (double)N * (192 + 64 + 64 + kHeads + 128 + 128), 1.5 * attn_flops(N, S, M));

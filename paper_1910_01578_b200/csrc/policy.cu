@@ -18,18 +18,21 @@ struct GateMap {            // one gated dense map
 };
 struct GateTable { GateMap m[kGateCount]; };
 
+// one thread per gate entry (kGamTotal of them over the 13 maps): gamma = 2 sigma(q + z P)
 __global__ void k_gates(const float *theta, const float *z, GateTable T, float *gam) {
   __shared__ float sz[kH];
   if (threadIdx.x < kH) sz[threadIdx.x] = z[threadIdx.x];
   __syncthreads();
-  for (int j = 0; j < kGateCount; j++) {
-    const GateMap g = T.m[j];
-    for (int i = threadIdx.x; i < g.width; i += blockDim.x) {
-      float s = theta[g.offq + i];
-      for (int k = 0; k < kH; k++) s = fmaf(sz[k], theta[g.offP + k * g.width + i], s);
-      gam[g.goff + i] = 2.f / (1.f + expf(-s));
-    }
-  }
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= kGamTotal) return;
+  int j = 0;
+  while (j + 1 < kGateCount && T.m[j + 1].goff <= t) j++;
+  const GateMap g = T.m[j];
+  const int i = t - g.goff;
+  float s = theta[g.offq + i];
+#pragma unroll 16
+  for (int k = 0; k < kH; k++) s = fmaf(sz[k], theta[g.offP + k * g.width + i], s);
+  gam[t] = 2.f / (1.f + expf(-s));
 }
 
 // W' = diag(gamma) W for one Transformer-XL layer (gamma pointers nullable -> 1).
@@ -81,25 +84,29 @@ struct RowMap {
   float *dpre;       // nullable
 };
 struct RowTable { RowMap m[16]; int count; };
+// one warp per row (lanes over the row's columns, coalesced); dgamma_i summed lane-strided then by
+// a fixed xor butterfly (deterministic)
 __global__ void k_gate_bwd_rows(const float *theta, RowTable T, float *grad) {
   int j = blockIdx.y;
   if (j >= T.count) return;
   const RowMap r = T.m[j];
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (i > r.fan_in) return;
   const float *src = r.dW + (size_t)i * r.ld + r.col0;
   if (i == r.fan_in) {   // bias row
-    for (int c = 0; c < r.ncols; c++) grad[r.offb + c] += src[c];
+    for (int c = lane; c < r.ncols; c += 32) grad[r.offb + c] += src[c];
     return;
   }
-  float g = r.gam ? r.gam[i] : 1.f;
+  const float g = r.gam ? r.gam[i] : 1.f;
   float dg = 0.f;
-  for (int c = 0; c < r.ncols; c++) {
-    float dw = src[c];
+  for (int c = lane; c < r.ncols; c += 32) {
+    const float dw = src[c];
     dg = fmaf(theta[r.offW + i * r.ncols + c], dw, dg);
     grad[r.offW + i * r.ncols + c] += g * dw;
   }
-  if (r.gam && r.dpre) r.dpre[i] = dg * g * (1.f - 0.5f * g);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) dg += __shfl_xor_sync(0xffffffffu, dg, o);
+  if (lane == 0 && r.gam && r.dpre) r.dpre[i] = dg * g * (1.f - 0.5f * g);
 }
 
 // step 2: grad P_j[k,i] += z_k dpre_j[i], grad q_j[i] += dpre_j[i]
@@ -115,22 +122,25 @@ __global__ void k_gate_bwd_P(const float *z, const float *dpre, GateTable T, flo
 }
 
 // step 3: dz_k = sum_j sum_i P_j[k,i] dpre_j[i] (fixed order), then scaled by 1/N
+// one block per k: threads take gate entries t, t + 256, ... (fixed), then a fixed smem tree
 __global__ void k_gate_bwd_z(const float *theta, const float *dpre, GateTable T, float invN, float *dzN) {
-  int k = threadIdx.x;
-  if (k >= kH) return;
+  __shared__ float red[256];
+  const int k = blockIdx.x;
   float s = 0.f;
-  for (int j = 0; j < kGateCount; j++) {
+  for (int t = threadIdx.x; t < kGamTotal; t += blockDim.x) {
+    int j = 0;
+    while (j + 1 < kGateCount && T.m[j + 1].goff <= t) j++;
     const GateMap g = T.m[j];
-    for (int i = 0; i < g.width; i++) s = fmaf(theta[g.offP + k * g.width + i], dpre[g.goff + i], s);
+    const int i = t - g.goff;
+    s = fmaf(theta[g.offP + k * g.width + i], dpre[t], s);
   }
-  dzN[k] = s * invN;
-}
-
-__global__ void k_copy_cols(const float *src, int lds, float *dst, int ldd, int rows, int cols) {
-  size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= (size_t)rows * cols) return;
-  int r = (int)(e / cols), c = (int)(e % cols);
-  dst[(size_t)r * ldd + c] = src[(size_t)r * lds + c];
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) dzN[k] = red[0] * invN;
 }
 
 inline unsigned nblk(size_t n, int t) { return (unsigned)((n + t - 1) / t); }
@@ -241,9 +251,8 @@ void layer_bwd(const WS &w, const Offs &off, const float *theta, int l, const fl
   launch_gemm(g, s);
   launch_wgrad(N, kH, kFFN, L.c, kH, kH, nullptr, 0, w.dm, kFFN, true, w.part, w.part_floats, L.dW1, false, s);
   // x1 -> LN2 -> c: dx1 = dy + LN2_bwd(dc)
-  launch_layernorm_bwd(L.x1, L.mu2, L.rs2, theta + off[b + LN2G], w.dc, nullptr, w.dx1, false,
+  launch_layernorm_bwd(L.x1, L.mu2, L.rs2, theta + off[b + LN2G], w.dc, nullptr, w.dx1, false, dy,
                        grad + off[b + LN2G], w.part, N, s);
-  launch_add(w.dx1, kH, dy, kH, w.dx1, kH, N, kH, s);
   // x1 = x + o Wo' + bo
   g = gemm(N, kH, kH, w.dx1, kH, L.Wo, 1, kH, w.dout, kH);          // do = dx1 Wo'^T
   launch_gemm(g, s);
@@ -252,18 +261,15 @@ void layer_bwd(const WS &w, const Offs &off, const float *theta, int l, const fl
   if (no_attention()) launch_relu_v_bwd(L.qkv, w.dout, w.dqkv, w.dkvm, N, s);
   else launch_attn_bwd(L.qkv, L.o, L.lse, w.dout, w.dqkv, w.dkvm, w.dd, N, S, M, s);
   // totals for the parameter gradients: dkvt = [dQ | dK_own + dK_mem | dV_own + dV_mem]
-  note_launch("k_copy_cols", s);
-  k_copy_cols<<<nblk((size_t)N * 64, 256), 256, 0, s>>>(w.dqkv, 192, w.dkvt, 192, N, 64);
-  launch_add(w.dqkv + 64, 192, w.dkvm, 128, w.dkvt + 64, 192, N, 128, s);
+  launch_dkvt(w.dqkv, w.dkvm, w.dkvt, N, s);
   launch_wgrad(N, kH, 192, L.a, kH, kH, nullptr, 0, w.dkvt, 192, true, w.part, w.part_floats, L.dWqkv, false, s);
   // da (own rows, flows into x) and dam (memory rows: parameters only, stop-gradient)
   g = gemm(N, 192, kH, w.dqkv, 192, L.Wqkv, 1, 192, w.da, kH);
   launch_gemm(g, s);
   g = gemm(N, 128, kH, w.dkvm, 128, L.Wqkv + 64, 1, 192, w.dam, kH);
   launch_gemm(g, s);
-  launch_layernorm_bwd(x, L.mu1, L.rs1, theta + off[b + LN1G], w.da, w.dam, dx, dx_acc, grad + off[b + LN1G],
-                       w.part, N, s);
-  launch_add(dx, kH, w.dx1, kH, dx, kH, N, kH, s);
+  launch_layernorm_bwd(x, L.mu1, L.rs1, theta + off[b + LN1G], w.da, w.dam, dx, dx_acc, w.dx1,
+                       grad + off[b + LN1G], w.part, N, s);
 }
 
 void add_layer_rows(RowTable &T, const WS &w, const Offs &off, int l, const float *const *g, float *dpre_base,
@@ -286,9 +292,9 @@ void add_layer_rows(RowTable &T, const WS &w, const Offs &off, int l, const floa
 
 void run_rows(const RowTable &T, const float *theta, float *grad, cudaStream_t s) {
   if (T.count == 0) return;
-  dim3 grid(nblk(257, 128), T.count);
+  dim3 grid(nblk(257, 8), T.count);   // 8 rows (warps) per block, fan-in + bias row <= 257
   note_launch("k_gate_bwd_rows", s);
-  k_gate_bwd_rows<<<grid, 128, 0, s>>>(theta, T, grad);
+  k_gate_bwd_rows<<<grid, 256, 0, s>>>(theta, T, grad);
 }
 
 }  // namespace
@@ -343,7 +349,7 @@ gdp_status run_place(const gdp_graph_s *g, const gdp_config *c, const float *the
     layer_fwd(w, off, theta, 0, w.Etopo, N, S, M, s);
     launch_colsum(w.L[0].y, N, kH, 1.0f / (float)N, w.z, w.part, s);
     note_launch("k_gates", s);
-    k_gates<<<1, 256, 0, s>>>(theta, w.z, GT, w.gam);
+    k_gates<<<nblk(kGamTotal, 128), 128, 0, s>>>(theta, w.z, GT, w.gam);
     for (int j = 0; j < 6; j++) { g0[j] = gam_of(w, GT, 0, j); g1[j] = gam_of(w, GT, 1, j); }
     gh = w.gam + GT.m[12].goff;
   }
@@ -424,7 +430,7 @@ gdp_status run_policy_grad(const gdp_graph_s *g, const gdp_config *c, const floa
     k_gate_bwd_P<<<gp, 256, 0, s>>>(w.z, w.dgam, GT, grad);
     mark(0);
     note_launch("k_gate_bwd_z", s);
-    k_gate_bwd_z<<<1, 64, 0, s>>>(theta, w.dgam, GT, 1.0f / (float)N, w.dz);
+    k_gate_bwd_z<<<kH, 256, 0, s>>>(theta, w.dgam, GT, 1.0f / (float)N, w.dz);
     // conditioner: z = mean_v C_v -> dC_v = dz / N for every node
     launch_fill_rows(w.dy, w.dz, 1.0f, N, kH, s);
     layer_bwd(w, off, theta, 0, w.Etopo, w.dy, w.dEt, true, grad, N, S, M, s);

@@ -465,7 +465,7 @@ def test_tensor_core_mode(gdp, case):
 @pytest.mark.parametrize("case", ["c1", "seg", "short_mem", "ragged", "mem_inf", "long_mem", "one_chunk_inf",
                                   "ragged_chunk"])
 def test_tensor_core_attention_matches_simt(gdp, case):
-    """The tcgen05 attention tiles (forward k_attn_fwd_tc, backward k_attn_bwd_tc) and the SIMT
+    """The tcgen05 attention tiles (forward k_attn_fwd_tc, backward k_attn_bwd_dq_tc / _dkv_tc) and the SIMT
     attention kernels inside a tensor-core-mode step (gdp_config.tensor_cores = 2), each against
     the bf16-emulating oracle of its own mode (relative L2 <= 2e-2) for logits and gradient.
     mem_inf / long_mem: more than 256 keys per segment (several key blocks in the forward; the

@@ -33,10 +33,10 @@ def test_profile_covers_the_step():
     launches = gdp.launch_count() - l0
     assert sum(r["launches"] for r in rec.values()) == launches
     # tensor-core mode: the attention runs on the tcgen05 tiles (attn_tc.cu)
-    for k in ("k_gather_max", "k_sample", "k_logit_grad", "k_attn_fwd_tc", "k_attn_bwd_tc"):
+    for k in ("k_gather_max", "k_sample", "k_logit_grad", "k_attn_fwd_tc", "k_attn_bwd_dq_tc", "k_attn_bwd_dkv_tc"):
         assert k in rec, k
         assert rec[k]["bytes"] > 0 and rec[k]["ms"] > 0
-    assert rec["k_attn_fwd_tc"]["flops"] > 0 and rec["k_attn_bwd_tc"]["flops"] > 0
+    assert rec["k_attn_fwd_tc"]["flops"] > 0 and rec["k_attn_bwd_dq_tc"]["flops"] > 0
     total = sum(r["ms"] for r in rec.values())
     step = e0.elapsed_time(e1)
     assert total <= step * 1.05 + 0.05
