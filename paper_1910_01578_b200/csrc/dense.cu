@@ -177,16 +177,27 @@ __global__ void __launch_bounds__(NT, 3) k_wgrad(int M, int K, int Kaug, int Nou
   }
 }
 
-// out[e] (+)= sum over chunks of part[c][e]: one warp per output, lane l sums chunks l, l + 32, ...
-// in order, then a fixed xor butterfly (deterministic; every chunk's load in flight at once)
-__global__ void k_reduce_chunks(const float *part, int chunks, int count, float *out, int accumulate) {
-  const int e = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
-  if (e >= count) return;
+// out[e] (+)= sum over chunks of part[c][e]: a block takes 32 consecutive outputs (lanes:
+// coalesced 128-byte loads) x 8 warps; warp w sums chunks w, w + 8, ... in order, then the 8
+// partial sums are added in warp order (deterministic)
+__global__ void __launch_bounds__(256) k_reduce_chunks(const float *part, int chunks, int count, float *out,
+                                                       int accumulate) {
+  __shared__ float red[8][33];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int e = blockIdx.x * 32 + lane;
   float s = 0.f;
-  for (int c = lane; c < chunks; c += 32) s += part[(size_t)c * count + e];
+  if (e < count) {
+#pragma unroll 4
+    for (int c = w; c < chunks; c += 8) s += part[(size_t)c * count + e];
+  }
+  red[w][lane] = s;
+  __syncthreads();
+  if (w == 0 && e < count) {
+    float t = red[0][lane];
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-  if (lane == 0) out[e] = accumulate ? out[e] + s : s;
+    for (int k = 1; k < 8; k++) t += red[k][lane];
+    out[e] = accumulate ? out[e] + t : t;
+  }
 }
 
 // ---- LayerNorm: one warp per row of 64 (2 values per lane)
@@ -366,7 +377,7 @@ void launch_wgrad(int M, int K, int Nout, const float *X1, int ldx1, int K1, con
     if (chunks > 0) {
       const int count = Kaug * Nout;
       note_launch("k_reduce_chunks", s);
-      k_reduce_chunks<<<nblk((size_t)count * 32, 256), 256, 0, s>>>(part, chunks, count, out, accumulate ? 1 : 0);
+      k_reduce_chunks<<<nblk(count, 32), 256, 0, s>>>(part, chunks, count, out, accumulate ? 1 : 0);
       return;
     }
   }
@@ -382,7 +393,7 @@ void launch_wgrad(int M, int K, int Nout, const float *X1, int ldx1, int K1, con
   k_wgrad<<<grid, NT, 0, s>>>(M, K, Kaug, Nout, X1, ldx1, K1, X2, ldx2, dY, ldy, part, rpc);
   int count = Kaug * Nout;
   note_launch("k_reduce_chunks", s);
-  k_reduce_chunks<<<nblk((size_t)count * 32, 256), 256, 0, s>>>(part, chunks, count, out, accumulate ? 1 : 0);
+  k_reduce_chunks<<<nblk(count, 32), 256, 0, s>>>(part, chunks, count, out, accumulate ? 1 : 0);
 }
 
 void launch_layernorm(const float *x, const float *g, const float *b, float *y, float *mu, float *rs, int N,
@@ -398,7 +409,7 @@ void launch_layernorm_bwd(const float *x, const float *mu, const float *rs, cons
   note_launch("k_layernorm_bwd", s);
   k_layernorm_bwd<<<chunks, 256, 0, s>>>(x, mu, rs, g, da, da_extra, dx, dx_accumulate ? 1 : 0, res, part, N);
   note_launch("k_reduce_chunks", s);
-  k_reduce_chunks<<<nblk(128 * 32, 256), 256, 0, s>>>(part, chunks, 128, dgb, 1);
+  k_reduce_chunks<<<nblk(128, 32), 256, 0, s>>>(part, chunks, 128, dgb, 1);
 }
 
 void launch_colsum(const float *x, int N, int C, float scale, float *out, float *part, cudaStream_t s) {
