@@ -65,11 +65,15 @@ constexpr int NINC5 = COST5_NINC;   // ops made available at one instant kept in
 #ifndef COST5_MB
 #define COST5_MB 32
 #endif
+#ifndef COST5_MBAR
+#define COST5_MBAR 0   // 1: the memory warp sleeps on an mbarrier the simulation warp arrives on per 32 items
+                       // (measured 162.8 ms vs 142.3 ms polling at C4 B = 1776: kept off)
+#endif
 #ifndef COST5_SLEEP
-#define COST5_SLEEP 1000
+#define COST5_SLEEP 3000
 #endif
 #ifndef COST5_SPIN
-#define COST5_SPIN 4
+#define COST5_SPIN 8
 #endif
 constexpr int RI5 = COST5_RI;       // memory item ring (power of 2)
 constexpr int MB5 = COST5_MB;       // the memory warp waits for this many items (or the end) before a batch
@@ -120,6 +124,7 @@ struct Smem5 {
   Q5 fc[8][KF5];                    // FIFO rings
   Q5 inc[8][NINC5];                 // ops made available at this instant
   unsigned long long items[RI5];    // memory items: t | code << 32
+  unsigned long long ibar;          // mbarrier: one phase per 32 items appended (and one at the end)
   Q5 drun[8];                       // the op running on each device
   int4 ch[NCH];                     // per channel: tail, free (transfer end), head
   int ca[NCH];                      // arrival tick of each channel's head entry (INF: empty; contiguous: the
@@ -189,6 +194,22 @@ __device__ __forceinline__ void head_fetch(Q5 *dst, const Slot5 *src, unsigned l
                    (unsigned)__cvta_generic_to_shared(dst)),
                "l"(src), "r"(m)
                : "memory");
+}
+__device__ __forceinline__ void mbar_arrive5(unsigned long long *mb) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"((unsigned)__cvta_generic_to_shared(mb)) : "memory");
+}
+// sleep (suspended in hardware, not polling) until the phase of parity ph completes or ~20 us
+// pass; the caller re-reads the ring either way (if the simulation warp ran an even number of
+// batches ahead the parity alone cannot tell, so the time limit is what keeps that case live)
+__device__ __forceinline__ void mbar_sleep5(unsigned long long *mb, unsigned ph) {
+  unsigned done;
+  const unsigned m = (unsigned)__cvta_generic_to_shared(mb);
+  asm volatile("{\n\t.reg .pred P1;\n\tmbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2, 20000;\n\t"
+               "selp.b32 %0, 1, 0, P1;\n\t}\n"
+               : "=r"(done)
+               : "r"(m), "r"(ph)
+               : "memory");
+  (void)done;
 }
 __device__ __forceinline__ void head_wait(unsigned long long *mb, unsigned ph) {
   unsigned done = 0;
@@ -388,7 +409,10 @@ __global__ void __launch_bounds__(64, COST5_MINB) k_cost5(Cost5Graph G, TopoArgs
       S.ca[tid] = INF;
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((unsigned)__cvta_generic_to_shared(&S.hbar[tid])));
     }
-    if (tid == 0) asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (tid == 0) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((unsigned)__cvta_generic_to_shared(&S.ibar)));
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
     if (tid < 8) { S.dv[tid] = make_int4(INF, 0, 0, 0); S.dv2[tid] = make_int4(0, -1, T.speed[tid], 0); }
     if (tid == 0) {
       S.mhead = 0; S.mk = 0; S.disp = 0; S.oom = 0;
@@ -449,6 +473,9 @@ __global__ void __launch_bounds__(64, COST5_MINB) k_cost5(Cost5Graph G, TopoArgs
       ensure(1);
       S.items[itail & (RI5 - 1)] = item5(t, kind, dev, idx, itail);
       itail++;
+#if COST5_MBAR
+      if ((itail & 31u) == 0u && lane == 0) mbar_arrive5(&S.ibar);   // a batch of 32 is complete
+#endif
     };
     auto to_inc = [&](int q, const Q5 &r) {       // uniform
       const int n = S.dv[q].w;
@@ -564,6 +591,12 @@ __global__ void __launch_bounds__(64, COST5_MINB) k_cost5(Cost5Graph G, TopoArgs
             const int n = min(32, nin - j0);
             ensure((unsigned)n);
             if (lane < n) S.items[(itail + lane) & (RI5 - 1)] = item5(t, IT_INEDGE, k, r.ib + j0 + lane, itail + lane);
+#if COST5_MBAR
+            if ((itail >> 5) != ((itail + n) >> 5)) {   // a batch of 32 is complete
+              __syncwarp();
+              if (lane == 0) mbar_arrive5(&S.ibar);
+            }
+#endif
             itail += n;
           }
           if (nout == 0) item(IT_SINK, k, r.id);
@@ -702,6 +735,9 @@ __global__ void __launch_bounds__(64, COST5_MINB) k_cost5(Cost5Graph G, TopoArgs
 #endif
     // ---------------------------------------------------------- end of the simulation
     item(IT_END, 0, 0);
+#if COST5_MBAR
+    if (lane == 0) mbar_arrive5(&S.ibar);   // the last (partial) batch
+#endif
     cp_wait0();
     if (lane == 0) { S.mk = mk; S.disp = disp; }
   } else {
@@ -723,6 +759,14 @@ __global__ void __launch_bounds__(64, COST5_MINB) k_cost5(Cost5Graph G, TopoArgs
       const bool valid = (code & 1u) == ((pos / RI5) & 1u);
       const unsigned vm = __ballot_sync(FULL, valid);
       const int n = vm == FULL ? 32 : __ffs(~vm) - 1;
+#if COST5_MBAR
+      if (n < 32 && !__any_sync(FULL, valid && kind_end(it))) {
+        // sleep until the simulation warp completes the batch starting at mh (mh is a multiple
+        // of 32 until the end): no polling instructions on the simulation warps' issue slots
+        mbar_sleep5(&S.ibar, (mh >> 5) & 1u);
+        continue;
+      }
+#endif
       if (n < MB5 && !__any_sync(FULL, valid && kind_end(it))) {
         // wait for a batch of MB5 items unless the simulation has ended: few, large batches
         // leave the issue slots to the simulation warps

@@ -11,7 +11,8 @@
 // fan-in (K <= 256: at most two halves, the unused 32-column blocks of a half stay zero),
 // N = width padded to 16.
 //
-// One CTA per row chunk (<= one per SM): warp 0 streams the chunk's 64-row stages by TMA,
+// One CTA per row chunk (<= one per SM): warp 0 streams the chunk's 64-row stages by TMA
+// (up to 4 in flight),
 // warp 1 issues 8 x (halves) MMAs per stage (K = 8 nodes each), warps 2-5 sum the bias row
 // (column sums of dY) from the same shared-memory stages and, at the end, drain TMEM into the
 // chunk's partial [K + 1 x width] (the k_wgrad layout); k_reduce_chunks adds the partials in
