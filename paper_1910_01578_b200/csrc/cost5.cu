@@ -26,11 +26,13 @@
 //  * Per-op state in shared memory is only the input counters: ops with one input need none,
 //    ops with exactly two inputs one "first input arrived" bit (a compact bitmap), ops with
 //    3..15 inputs a 4-bit counter, more a global counter (C4: 6.9 KB).  Device ids are not in
-//    shared memory: a finishing op's consumers' devices come with its staged out-edge records
-//    (a per-placement byte per out-edge slot that k_cost5_pre writes), the memory warp reads the
+//    shared memory: a finishing op's consumers' devices -- and each cross edge's transfer time,
+//    so no division is on the critical path -- come with its staged out-edge records (a
+//    per-placement word per out-edge slot that k_cost5_pre writes), the memory warp reads the
 //    placement row from L2.  Static memory, busy time, channel sizes and the co-location check
-//    also come from k_cost5_pre (one CTA per placement, fully parallel).  With 22.2 KB of shared
-//    memory per placement, ten CTAs (placements) share an SM at C4.
+//    also come from k_cost5_pre (one CTA per placement, fully parallel).  With 18.1 KB of shared
+//    memory per placement (compact channel rings, heads fetched by bulk copies), twelve CTAs
+//    (placements) share an SM at C4.
 // Requires (host-checked): every duration >= 1 and every transfer >= 1 tick (no same-instant
 // rounds), N and E < 2^25, degrees < 2^16.  Otherwise gdp_cost runs k_cost3 / k_cost (cost2.cu,
 // cost.cu).
@@ -120,7 +122,7 @@ struct Smem5 {
   int2 cq[NCH][KC5];                // channel rings, compact: (out-edge slot, arrival tick)
   unsigned long long hbar[NCH];     // mbarrier of each channel's head fetch
   Slot5 stage[8][2][SO5];           // out-edge slots of the running / next op of each device
-  unsigned sdev[8][2][SO5];         // the 4 bytes of the placement's slot-device array holding each slot's
+  unsigned sdev[8][2][SO5];         // each staged slot's word from k_cost5_pre: consumer device | transfer time << 3
   Q5 fc[8][KF5];                    // FIFO rings
   Q5 inc[8][NINC5];                 // ops made available at this instant
   unsigned long long items[RI5];    // memory items: t | code << 32
@@ -146,7 +148,7 @@ __host__ __device__ inline Scratch5 scratch5_layout(int N, long long E, int ngbi
   Scratch5 s;
   s.pre = 0;
   s.sdev = al(sizeof(Pre5));
-  s.outcnt = s.sdev + al((size_t)(E > 0 ? E : 1) + 16);
+  s.outcnt = s.sdev + al(4 * (size_t)(E > 0 ? E : 1) + 16);
   s.gbig = s.outcnt + al(4 * (size_t)N);
   s.fifo = s.gbig + al(4 * (size_t)(ngbig > 0 ? ngbig : 1));
   s.ov = s.fifo + al(sizeof(Q5) * (size_t)N);
@@ -255,7 +257,7 @@ __device__ __forceinline__ unsigned long long item5(int t, int kind, int dev, in
 
 // ------------------------------------------------------------------------ pre-pass
 // One CTA per placement: static memory / busy time / op count per device, co-location and
-// malformed flags, the device of every out-edge slot's consumer (one byte per slot, out-CSR
+// malformed flags, per out-edge slot the consumer's device and the transfer time (one word per slot, out-CSR
 // order), cross bytes and per-channel transfer counts (the sizes of the global overflow
 // regions), consumer counters of the memory warp, global input counters.  The placement row
 // (N bytes) is staged in shared memory with 16-byte loads when it fits (dynamic shared memory
@@ -274,7 +276,7 @@ __global__ void __launch_bounds__(512) k_cost5_pre(Cost5Graph G, TopoArgs T, con
   const Scratch5 L = scratch5_layout(N, G.E, G.ngbig);
   unsigned char *base = scratch + (size_t)b * per_place;
   Pre5 *pre = reinterpret_cast<Pre5 *>(base + L.pre);
-  uint8_t *sdev = base + L.sdev;
+  unsigned *sdev = reinterpret_cast<unsigned *>(base + L.sdev);
   int *outcnt = reinterpret_cast<int *>(base + L.outcnt);
   int *gbig = reinterpret_cast<int *>(base + L.gbig);
   if (tid < 8) { s_stat[tid] = 0; s_busy[tid] = 0; s_cnt[tid] = 0; }
@@ -323,13 +325,18 @@ __global__ void __launch_bounds__(512) k_cost5_pre(Cost5Graph G, TopoArgs T, con
   {
     long long lcross = 0;
     int *chw = s_chw[(tid >> 5) & 15];
+    // per slot: the consumer's device (3 bits) and, for a cross edge, its transfer time (the
+    // simulation warp stages the word with the slot: no division on its critical path)
     auto edge = [&](long long e, int u, int w) -> unsigned {
       const int su = D[u], tw = D[w];
+      unsigned x = 0;
       if (su != tw && su < d && tw < d) {
         atomicAdd(&chw[su * 8 + tw], 1);
-        lcross += __ldg(G.ebytes + e);
+        const long long by = __ldg(G.ebytes + e);
+        lcross += by;
+        x = (unsigned)xfer_time3(by, 8 * su + tw, T);
       }
-      return (unsigned)tw;
+      return (x << 3) | ((unsigned)tw & 7u);
     };
     const long long E4 = G.E / 4;
     const int4 *src4 = reinterpret_cast<const int4 *>(G.out_src), *idx4 = reinterpret_cast<const int4 *>(G.out_idx);
@@ -338,9 +345,9 @@ __global__ void __launch_bounds__(512) k_cost5_pre(Cost5Graph G, TopoArgs T, con
       const long long e = 4 * q;
       const unsigned b0 = edge(e, u.x, w.x), b1 = edge(e + 1, u.y, w.y), b2 = edge(e + 2, u.z, w.z),
                      b3 = edge(e + 3, u.w, w.w);
-      reinterpret_cast<unsigned *>(sdev)[q] = b0 | (b1 << 8) | (b2 << 16) | (b3 << 24);
+      reinterpret_cast<uint4 *>(sdev)[q] = make_uint4(b0, b1, b2, b3);
     }
-    for (long long e = 4 * E4 + tid; e < G.E; e += blockDim.x) sdev[e] = (uint8_t)edge(e, G.out_src[e], G.out_idx[e]);
+    for (long long e = 4 * E4 + tid; e < G.E; e += blockDim.x) sdev[e] = edge(e, G.out_src[e], G.out_idx[e]);
     lcross = warp_sum_ll(lcross);
     if (lane == 0 && lcross) atomicAdd(&s_cross, (unsigned long long)lcross);
   }
@@ -392,7 +399,7 @@ __global__ void __launch_bounds__(64, COST5_MINB) k_cost5(Cost5Graph G, TopoArgs
   const Scratch5 L = scratch5_layout(N, G.E, G.ngbig);
   unsigned char *base = scratch + (size_t)b * per_place;
   const Pre5 *pre = reinterpret_cast<const Pre5 *>(base + L.pre);
-  const uint8_t *sdev_g = base + L.sdev;
+  const unsigned *sdev_g = reinterpret_cast<const unsigned *>(base + L.sdev);
   int *outcnt = reinterpret_cast<int *>(base + L.outcnt);
   int *gbig = reinterpret_cast<int *>(base + L.gbig);
   Q5 *fifo_g = reinterpret_cast<Q5 *>(base + L.fifo);
@@ -509,7 +516,7 @@ __global__ void __launch_bounds__(64, COST5_MINB) k_cost5(Cost5Graph G, TopoArgs
       if (lane < no) {
         const int e = r.ob + lane;
         cp_32(&S.stage[k][sl][lane], G.slots + e);
-        cp_4(&S.sdev[k][sl][lane], sdev_g + (e & ~3));
+        cp_4(&S.sdev[k][sl][lane], sdev_g + e);
         spend |= 1u << (2 * k + sl);
       }
       cp_commit();
@@ -605,15 +612,17 @@ __global__ void __launch_bounds__(64, COST5_MINB) k_cost5(Cost5Graph G, TopoArgs
             const bool valid = j < nout;
             Slot5 e;
             int tw = k;
+            unsigned sw = 0;
             if (valid) {
               if (j < SO5) {
                 if (spend & (1u << (2 * k + sl))) { cp_wait0(); spend = 0; }
                 load_slot5(e, &S.stage[k][sl][j]);
-                tw = (S.sdev[k][sl][j] >> (8 * ((r.ob + j) & 3))) & 0xff;
+                sw = S.sdev[k][sl][j];
               } else {
                 load_slot5(e, G.slots + r.ob + j);
-                tw = sdev_g[r.ob + j];
+                sw = sdev_g[r.ob + j];
               }
+              tw = (int)(sw & 7u);
             }
             const bool same = valid && tw == k, cross = valid && tw != k;
             const bool av = same && arrive5(flag_s, bigb_s, gbig, e.cinfo);
@@ -637,7 +646,7 @@ __global__ void __launch_bounds__(64, COST5_MINB) k_cost5(Cost5Graph G, TopoArgs
                 const int c = cidx(k, tw);
                 const int4 cs = S.ch[c];
                 const int tail = cs.x, f = cs.y, hd = cs.z;
-                const int x = xfer_time3(e.bytes, 8 * k + tw, T);
+                const int x = (int)(sw >> 3);   // the transfer time k_cost5_pre computed
                 const int bt = max(t, f);
                 const int pos = tail + rank, arr = bt + (rank + 1) * x;
                 const int2 ce = make_int2(r.ob + j, arr);
