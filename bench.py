@@ -369,10 +369,18 @@ def main():
             times.append(e0.elapsed_time(e1))
     launches = (gdp.launch_count() - launches0) // args.steps
     total_ms = sum(times)
+    step_ms = list(times)
     if distributed:
         t = torch.tensor([total_ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
+        ts_t = torch.tensor(times, device=dev, dtype=torch.float64)   # per-step max over ranks
+        dist.all_reduce(ts_t, op=dist.ReduceOp.MAX)
+        step_ms = [float(x) for x in ts_t.cpu()]
+    step_sorted = sorted(step_ms)
+    step_stats = {"median": statistics.median(step_ms),
+                  "p90": step_sorted[min(len(step_sorted) - 1, int(0.9 * (len(step_sorted) - 1) + 0.999))],
+                  "min": step_sorted[0], "max": step_sorted[-1]}
     # placements per step over all ranks: samples mode adds B per rank per graph (weak scaling);
     # graphs mode splits the fixed set of graphs (strong scaling)
     placements = W.batch * (world if mode == "samples" else 1) * len(W.graphs) * args.steps
@@ -479,7 +487,7 @@ def main():
                "config": config_json(W, argparse.Namespace(batch=W.batch, gpus=world), mode),
                "clocks": clk.summary(), "gpu_launches": int(launches), "roofline": roof, "e2e": e2e,
                "cpu_baseline": cpu, "kernels": kernels,
-               "stages_ms": stage, "cuda_graph": bool(ps.cuda_graph),
+               "stages_ms": stage, "step_ms": step_stats, "cuda_graph": bool(ps.cuda_graph),
                "valid_frac": float(np.mean(rep["valid"])), "makespan_mean_ticks": float(np.mean(rep["makespan"]))}
         print(json.dumps(out), flush=True)
     if distributed:
