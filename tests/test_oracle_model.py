@@ -464,3 +464,21 @@ def test_tf32_truncation_pins():
     # the tensor-core shape rule: W's fp32 tile (K to 32, width to 16) must fit 160 KB
     assert Mo.tc_shape(128, 256, 160) and not Mo.tc_shape(128, 256, 176)
     assert Mo.tc_shape(128, 64, 256) and not Mo.tc_shape(127, 64, 256) and not Mo.tc_shape(128, 64, 8)
+
+
+def test_layer_norm_closed_form():
+    """R12 (pre-LN, biased variance, eps 1e-5), pinned by hand: x = (a, -a, a, -a, ...) has mean 0
+    and biased variance a^2, so LN(x) = +-a / sqrt(a^2 + 1e-5) * g + b.  At a = 0.01 the eps term
+    moves the value from 1 to 0.9534626 (an unbiased variance, another eps or a dropped eps would
+    all fail); a constant row maps to the bias exactly."""
+    a = 0.01
+    x = torch.tensor([[a if i % 2 == 0 else -a for i in range(64)]], dtype=torch.float64)
+    g = torch.full((64,), 2.0, dtype=torch.float64)
+    b = torch.full((64,), 0.5, dtype=torch.float64)
+    y = Mo.layer_norm(x, g, b)
+    v = a / math.sqrt(a * a + 1e-5)
+    assert abs(v - 0.9534625892455922) < 1e-15
+    want = torch.tensor([[0.5 + 2 * v if i % 2 == 0 else 0.5 - 2 * v for i in range(64)]], dtype=torch.float64)
+    assert torch.allclose(y, want, rtol=0, atol=1e-14)
+    c = Mo.layer_norm(torch.full((1, 64), 3.7, dtype=torch.float64), g, b)
+    assert torch.equal(c, torch.full((1, 64), 0.5, dtype=torch.float64))
