@@ -392,6 +392,10 @@ __global__ void __launch_bounds__(64, COST5_MINB) k_cost5(Cost5Graph G, TopoArgs
   const int N = G.N, d = T.d, b = blockIdx.x;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const unsigned FULL = 0xffffffffu, lt = (1u << lane) - 1u;
+#ifdef COST5_TIMING   // per-placement wall time (us) and SM in the report's padding (tools/cost5_spread.py)
+  unsigned long long t_beg;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_beg));
+#endif
   unsigned *flags = reinterpret_cast<unsigned *>(smem_raw);
   unsigned *bigb = flags + G.nflagw;
   const unsigned flag_s = (unsigned)__cvta_generic_to_shared(flags), bigb_s = flag_s + 4u * (unsigned)G.nflagw;
@@ -854,6 +858,17 @@ __global__ void __launch_bounds__(64, COST5_MINB) k_cost5(Cost5Graph G, TopoArgs
     gdp_sim_report R;
     R.makespan = S.mk; R.cross_bytes = pre->cross;
     for (int i = 0; i < 6; i++) R.pad[i] = 0;
+#ifdef COST5_TIMING
+    {
+      unsigned long long t_end;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+      const unsigned us = (unsigned)((t_end - t_beg) / 1000ull);
+      unsigned sm;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+      R.pad[0] = us & 255u; R.pad[1] = (us >> 8) & 255u; R.pad[2] = (us >> 16) & 255u; R.pad[3] = us >> 24;
+      R.pad[4] = (uint8_t)sm; R.pad[5] = (uint8_t)S.simw;
+    }
+#endif
     R.violation = (pflag & 1) ? 1 : (S.oom ? 2 : 0);
     if (S.disp != N) R.violation = 3;   // cannot happen for a validated DAG
     R.valid = R.violation == 0;
