@@ -270,6 +270,9 @@ __global__ void __launch_bounds__(512) k_cost5_pre(Cost5Graph G, TopoArgs T, con
   __shared__ unsigned long long s_stat[8], s_busy[8], s_cross;
   __shared__ int s_cnt[8], s_ch[64], s_flag;
   __shared__ int s_chw[16][64];   // per-warp channel counts (no contention on 64 addresses)
+  __shared__ long long s_bpt[64];
+  __shared__ double s_ibpt[64];
+  __shared__ int s_lat[64];
   const int N = G.N, d = T.d, b = blockIdx.x, tid = threadIdx.x, lane = tid & 31;
   const unsigned FULL = 0xffffffffu;
   const uint8_t *Dg = Dall + (size_t)b * N;
@@ -280,7 +283,12 @@ __global__ void __launch_bounds__(512) k_cost5_pre(Cost5Graph G, TopoArgs T, con
   int *outcnt = reinterpret_cast<int *>(base + L.outcnt);
   int *gbig = reinterpret_cast<int *>(base + L.gbig);
   if (tid < 8) { s_stat[tid] = 0; s_busy[tid] = 0; s_cnt[tid] = 0; }
-  if (tid < 64) s_ch[tid] = 0;
+  if (tid < 64) {
+    s_ch[tid] = 0;
+    s_bpt[tid] = T.bpt[tid];   // the channel tables in shared memory: the edge pass indexes them per lane
+    s_ibpt[tid] = T.inv_bpt[tid];
+    s_lat[tid] = T.lat[tid];
+  }
   for (int i = tid; i < 16 * 64; i += blockDim.x) (&s_chw[0][0])[i] = 0;
   if (tid == 0) { s_cross = 0; s_flag = 0; }
   if (dsm) {   // the row into shared memory (B x N rows are 16-byte aligned when N % 16 == 0)
@@ -334,7 +342,15 @@ __global__ void __launch_bounds__(512) k_cost5_pre(Cost5Graph G, TopoArgs T, con
         atomicAdd(&chw[su * 8 + tw], 1);
         const long long by = __ldg(G.ebytes + e);
         lcross += by;
-        x = (unsigned)xfer_time3(by, 8 * su + tw, T);
+        {   // = xfer_time3(by, 8 su + tw, T) on the shared-memory tables
+          const int c = 8 * su + tw;
+          const long long bw = s_bpt[c];
+          long long qq = (long long)((double)by * s_ibpt[c]);
+          long long rr = by - qq * bw;
+          while (rr < 0) { qq--; rr += bw; }
+          while (rr >= bw) { qq++; rr -= bw; }
+          x = (unsigned)((int)(qq + (rr > 0)) + s_lat[c]);
+        }
       }
       return (x << 3) | ((unsigned)tw & 7u);
     };
