@@ -299,14 +299,18 @@ def main():
                     help="time NEXT-2 zero-shot placement (embed, place, greedy, cost of one placement)")
     ap.add_argument("--train", action="store_true",
                     help="time the NEXT-1 training update (PPOTrainer.update) instead of the policy step")
+    ap.add_argument("--global-batch", type=int, default=None,
+                    help="strong scaling (SURVEY 8(d)): this many placements in total, split over the ranks")
     args = ap.parse_args()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.global_batch:   # placements per rank = ceil(global / ranks); reported as strong scaling
+        args.batch = -(-args.global_batch // world)
     W = workloads.config(args.config, batch=args.batch, mem_len=args.mem_len)
     if args.no_superposition:
         W.superposition = False
     args.batch = W.batch
-    rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
         run_reference(args, W, rank)
         return
@@ -481,7 +485,7 @@ def main():
         rep = st0.reports()
         out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
-               "scaling": "weak" if mode == "samples" else "strong", "vs_baseline": None,
+               "scaling": "weak" if (mode == "samples" and not args.global_batch) else "strong", "vs_baseline": None,
                "dtype": ("f32" if args.fp32 else "tf32->f32 (tcgen05 dense maps, weight grads) / bf16 (tcgen05 attention) / f32")
                + " policy, i32 cost model", "data": "synthetic",
                "config": config_json(W, argparse.Namespace(batch=W.batch, gpus=world), mode),
