@@ -554,15 +554,16 @@ __global__ void __launch_bounds__(64, COST5_MINB) k_cost5(Cost5Graph G, TopoArgs
       S.dv[q].z = f + 1;
     }
     unsigned att = (1u << d) - 1u;   // devices to dispatch at t = 0
+    int ca0 = INF, ca1 = INF, cmin = INF, dfr = INF;   // next-event operands (see "next instant")
     for (bool first = true;; first = false) {
       if (!first) {
         // ---------------------------------------------------------- next instant
-        const int ca0 = lane < NCH / 2 ? S.ca[2 * lane] : INF, ca1 = lane < NCH / 2 ? S.ca[2 * lane + 1] : INF;
-        const int df = lane < 8 ? S.dv[lane].x : INF;
-        t = (int)__reduce_min_sync(FULL, (unsigned)min(min(ca0, ca1), df));
+        // the channel heads' minimum was taken before the previous dispatch (which does not
+        // touch them); the running finishes are lane-held registers (lane k: device k)
+        t = min(cmin, (int)__reduce_min_sync(FULL, (unsigned)dfr));
         if (t == INF) break;
         const unsigned e0 = __ballot_sync(FULL, ca0 == t), e1 = __ballot_sync(FULL, ca1 == t);
-        unsigned ef = __ballot_sync(FULL, df == t);
+        unsigned ef = __ballot_sync(FULL, dfr == t);
         P5C(9);
         P5(0);
         // ---------------------------------------------------------- (1) copies arriving now
@@ -613,6 +614,7 @@ __global__ void __launch_bounds__(64, COST5_MINB) k_cost5(Cost5Graph G, TopoArgs
           load_q5(r, &S.drun[k]);
           const int sl = S.dv2[k].x;
           S.dv[k].x = INF;
+          if (lane == k) dfr = INF;
           const int nout = r.nn & 0xffff, nin = (int)((unsigned)r.nn >> 16);
           for (int j0 = 0; j0 < nin; j0 += 32) {   // frees of this finish -> memory warp, one item per lane
             const int n = min(32, nin - j0);
@@ -684,6 +686,11 @@ __global__ void __launch_bounds__(64, COST5_MINB) k_cost5(Cost5Graph G, TopoArgs
         }
         P5(2);
       }
+      // the channel heads are final for the next instant: their minimum now, its latency hidden
+      // behind the dispatch below
+      ca0 = lane < NCH / 2 ? S.ca[2 * lane] : INF;
+      ca1 = lane < NCH / 2 ? S.ca[2 * lane + 1] : INF;
+      cmin = (int)__reduce_min_sync(FULL, (unsigned)min(ca0, ca1));
       // ---------------------------------------------------------- (3) FIFO append + dispatch
       for (att |= incm, incm = 0; att; att &= att - 1) {
         const int k = __ffs(att) - 1;
@@ -737,6 +744,7 @@ __global__ void __launch_bounds__(64, COST5_MINB) k_cost5(Cost5Graph G, TopoArgs
         if (go) {
           const int fin = t + run.cost * dv2k.z;
           S.dv[k].x = fin;
+          if (lane == k) dfr = fin;
           store_q5(&S.drun[k], run);
           mk = max(mk, fin);
           disp++;
