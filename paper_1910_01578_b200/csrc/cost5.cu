@@ -554,14 +554,16 @@ __global__ void __launch_bounds__(64, COST5_MINB) k_cost5(Cost5Graph G, TopoArgs
       S.dv[q].z = f + 1;
     }
     unsigned att = (1u << d) - 1u;   // devices to dispatch at t = 0
-    int ca0 = INF, ca1 = INF, cmin = INF, dfr = INF;   // next-event operands (see "next instant")
+    int cmin = INF, dfr = INF;   // next-event operands (see "next instant")
     for (bool first = true;; first = false) {
       if (!first) {
         // ---------------------------------------------------------- next instant
         // the channel heads' minimum was taken before the previous dispatch (which does not
-        // touch them); the running finishes are lane-held registers (lane k: device k)
+        // touch them); the running finishes are lane-held registers (lane k: device k); the heads
+        // are re-read for the ballots (off the minimum's critical path)
         t = min(cmin, (int)__reduce_min_sync(FULL, (unsigned)dfr));
         if (t == INF) break;
+        const int ca0 = lane < NCH / 2 ? S.ca[2 * lane] : INF, ca1 = lane < NCH / 2 ? S.ca[2 * lane + 1] : INF;
         const unsigned e0 = __ballot_sync(FULL, ca0 == t), e1 = __ballot_sync(FULL, ca1 == t);
         unsigned ef = __ballot_sync(FULL, dfr == t);
         P5C(9);
@@ -688,9 +690,8 @@ __global__ void __launch_bounds__(64, COST5_MINB) k_cost5(Cost5Graph G, TopoArgs
       }
       // the channel heads are final for the next instant: their minimum now, its latency hidden
       // behind the dispatch below
-      ca0 = lane < NCH / 2 ? S.ca[2 * lane] : INF;
-      ca1 = lane < NCH / 2 ? S.ca[2 * lane + 1] : INF;
-      cmin = (int)__reduce_min_sync(FULL, (unsigned)min(ca0, ca1));
+      cmin = (int)__reduce_min_sync(FULL, (unsigned)min(lane < NCH / 2 ? S.ca[2 * lane] : INF,
+                                                        lane < NCH / 2 ? S.ca[2 * lane + 1] : INF));
       // ---------------------------------------------------------- (3) FIFO append + dispatch
       for (att |= incm, incm = 0; att; att &= att - 1) {
         const int k = __ffs(att) - 1;
