@@ -554,14 +554,14 @@ __global__ void __launch_bounds__(64, COST5_MINB) k_cost5(Cost5Graph G, TopoArgs
       S.dv[q].z = f + 1;
     }
     unsigned att = (1u << d) - 1u;   // devices to dispatch at t = 0
-    int cmin = INF, dfr = INF;   // next-event operands (see "next instant")
+    int cmin = INF, dmin = INF, dfr = INF;   // next-event operands (see "next instant")
     for (bool first = true;; first = false) {
       if (!first) {
         // ---------------------------------------------------------- next instant
-        // the channel heads' minimum was taken before the previous dispatch (which does not
-        // touch them); the running finishes are lane-held registers (lane k: device k); the heads
-        // are re-read for the ballots (off the minimum's critical path)
-        t = min(cmin, (int)__reduce_min_sync(FULL, (unsigned)dfr));
+        // both minima were taken before the previous dispatch (which never touches the channel
+        // heads and only lowers the running finishes' minimum); the running finishes are
+        // lane-held registers (lane k: device k); the heads are re-read for the ballots
+        t = min(cmin, dmin);
         if (t == INF) break;
         const int ca0 = lane < NCH / 2 ? S.ca[2 * lane] : INF, ca1 = lane < NCH / 2 ? S.ca[2 * lane + 1] : INF;
         const unsigned e0 = __ballot_sync(FULL, ca0 == t), e1 = __ballot_sync(FULL, ca1 == t);
@@ -692,6 +692,8 @@ __global__ void __launch_bounds__(64, COST5_MINB) k_cost5(Cost5Graph G, TopoArgs
       // behind the dispatch below
       cmin = (int)__reduce_min_sync(FULL, (unsigned)min(lane < NCH / 2 ? S.ca[2 * lane] : INF,
                                                         lane < NCH / 2 ? S.ca[2 * lane + 1] : INF));
+      // the running finishes' minimum likewise; the dispatch below lowers it with each new finish
+      dmin = (int)__reduce_min_sync(FULL, (unsigned)dfr);
       // ---------------------------------------------------------- (3) FIFO append + dispatch
       for (att |= incm, incm = 0; att; att &= att - 1) {
         const int k = __ffs(att) - 1;
@@ -746,6 +748,7 @@ __global__ void __launch_bounds__(64, COST5_MINB) k_cost5(Cost5Graph G, TopoArgs
           const int fin = t + run.cost * dv2k.z;
           S.dv[k].x = fin;
           if (lane == k) dfr = fin;
+          dmin = min(dmin, fin);
           store_q5(&S.drun[k], run);
           mk = max(mk, fin);
           disp++;
