@@ -481,7 +481,7 @@ __global__ void __launch_bounds__(64, COST5_MINB) k_cost5(Cost5Graph G, TopoArgs
     // lane parallelism only where it pays -- the next-event minimum (one REDUX over the 64
     // channel heads and 8 running finishes), the out-edges of a finish, the in-edge items and
     // the staging copies (those sections end with __syncwarp).
-    int mk = 0, disp = 0, t = 0;
+    int t = 0;   // the instant; after the loop the last one = the makespan (the last event is a finish)
     unsigned spend = 0;                 // this lane's staging copies in flight (bit 2k + slot)
     unsigned itail = 0, mcache = 0;     // items appended; memory-warp head as last read
     unsigned incm = 0;                  // devices with ops made available at this instant
@@ -555,16 +555,19 @@ __global__ void __launch_bounds__(64, COST5_MINB) k_cost5(Cost5Graph G, TopoArgs
     }
     unsigned att = (1u << d) - 1u;   // devices to dispatch at t = 0
     int cmin = INF, dmin = INF, dfr = INF;   // next-event operands (see "next instant")
+    unsigned ce0 = 0, ce1 = 0;
     for (bool first = true;; first = false) {
       if (!first) {
         // ---------------------------------------------------------- next instant
-        // both minima were taken before the previous dispatch (which never touches the channel
-        // heads and only lowers the running finishes' minimum); the running finishes are
-        // lane-held registers (lane k: device k); the heads are re-read for the ballots
-        t = min(cmin, dmin);
-        if (t == INF) break;
-        const int ca0 = lane < NCH / 2 ? S.ca[2 * lane] : INF, ca1 = lane < NCH / 2 ? S.ca[2 * lane + 1] : INF;
-        const unsigned e0 = __ballot_sync(FULL, ca0 == t), e1 = __ballot_sync(FULL, ca1 == t);
+        // both minima (and the channels at the heads' minimum) were taken before the previous
+        // dispatch, which never touches the channel heads and only lowers the running finishes'
+        // minimum; the running finishes are lane-held registers (lane k: device k)
+        {
+          const int tn = min(cmin, dmin);
+          if (tn == INF) break;
+          t = tn;
+        }
+        const unsigned e0 = cmin == t ? ce0 : 0u, e1 = cmin == t ? ce1 : 0u;
         unsigned ef = __ballot_sync(FULL, dfr == t);
         P5C(9);
         P5(0);
@@ -690,8 +693,12 @@ __global__ void __launch_bounds__(64, COST5_MINB) k_cost5(Cost5Graph G, TopoArgs
       }
       // the channel heads are final for the next instant: their minimum now, its latency hidden
       // behind the dispatch below
-      cmin = (int)__reduce_min_sync(FULL, (unsigned)min(lane < NCH / 2 ? S.ca[2 * lane] : INF,
-                                                        lane < NCH / 2 ? S.ca[2 * lane + 1] : INF));
+      {
+        const int ca0 = lane < NCH / 2 ? S.ca[2 * lane] : INF, ca1 = lane < NCH / 2 ? S.ca[2 * lane + 1] : INF;
+        cmin = (int)__reduce_min_sync(FULL, (unsigned)min(ca0, ca1));
+        ce0 = __ballot_sync(FULL, ca0 == cmin);   // the channels whose head arrives at cmin
+        ce1 = __ballot_sync(FULL, ca1 == cmin);
+      }
       // the running finishes' minimum likewise; the dispatch below lowers it with each new finish
       dmin = (int)__reduce_min_sync(FULL, (unsigned)dfr);
       // ---------------------------------------------------------- (3) FIFO append + dispatch
@@ -750,8 +757,6 @@ __global__ void __launch_bounds__(64, COST5_MINB) k_cost5(Cost5Graph G, TopoArgs
           if (lane == k) dfr = fin;
           dmin = min(dmin, fin);
           store_q5(&S.drun[k], run);
-          mk = max(mk, fin);
-          disp++;
           item(IT_ALLOC_OP, k, run.id);
           cur ^= 1;   // the slot the head was staged into, or the one it is staged into now
           if (run.id != nxt && (run.nn & 0xffff)) stage(k, cur, run);
@@ -780,12 +785,12 @@ __global__ void __launch_bounds__(64, COST5_MINB) k_cost5(Cost5Graph G, TopoArgs
     if (lane == 0) mbar_arrive5(&S.ibar);   // the last (partial) batch
 #endif
     cp_wait0();
-    if (lane == 0) { S.mk = mk; S.disp = disp; }
+    if (lane == 0) S.mk = t;
   } else {
     // ============================================================ memory warp
     const bool dl = lane < d;
     long long mem = dl ? pre->stat[lane] : 0, pk = mem;
-    int last_t = -1;
+    int last_t = -1, ndisp = 0;
     unsigned mh = 0;
     int nwait = 0;
     bool done = false;
@@ -827,6 +832,7 @@ __global__ void __launch_bounds__(64, COST5_MINB) k_cost5(Cost5Graph G, TopoArgs
       const bool mine = lane < n;
       const int ti = (int)(unsigned)(it & 0xffffffffull);
       const int kind = (int)((code >> 1) & 7u), dev = (int)((code >> 4) & 7u), idx = (int)(code >> 7);
+      ndisp += __popc(__ballot_sync(FULL, mine && kind == IT_ALLOC_OP));   // one item per dispatch
       int dA = -1, dB = -1, u = -1;
       long long xA = 0, xB = 0, bu = 0;
       int du = 0;
@@ -871,6 +877,7 @@ __global__ void __launch_bounds__(64, COST5_MINB) k_cost5(Cost5Graph G, TopoArgs
       }
     }
     pk = max(pk, mem);
+    if (lane == 0) S.disp = ndisp;
 #ifdef COST5_PROF
     if (b == 0 && lane == 0)
       printf("C5MEM batches=%lld items=%lld idle_polls=%lld cycles=%lld\n", nbatch, nitems, nidle, clock64() - m0);
