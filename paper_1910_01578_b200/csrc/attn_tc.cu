@@ -72,6 +72,13 @@ __device__ __forceinline__ float ex2(float x) {
   return y;
 }
 
+// B = a row-major [K rows x 16] bf16 tile (canon_off with Kp = 16) read MN-major (N = its 16
+// columns, K = its rows): that K-major canonical layout is already the MN-major interleaved layout
+// of the transpose (core matrix = 8 rows x 16 bytes), so no transposed copy is staged.
+// SWIZZLE_NONE, MN-major: SBO = next 8 columns (128 B), LBO = next 8 rows (256 B); a K step of 16
+// rows is 512 B; instruction-descriptor bit 16 = B MN-major.
+__device__ __forceinline__ uint64_t desc_bmn(uint32_t saddr) { return tc::desc_none(saddr, 256, 128); }
+
 // Forward key block: 128 keys, so S needs 128 TMEM columns and the tiles 45 KB of shared memory:
 // 4 CTAs (16 warps) per SM instead of 2 with 256-key blocks.
 constexpr int TKF = 128;
@@ -100,7 +107,7 @@ __global__ void __launch_bounds__(TQ, 4) k_attn_fwd_tc(const float *__restrict__
   __shared__ uint32_t tmem_base;
   unsigned char *sQ = sm;                        // 128 x 16 bf16
   unsigned char *sK = sm + TQ * 16 * 2;          // 256 x 16
-  unsigned char *sV = sK + TKF * 16 * 2;        // V^T: 16 x 128
+  unsigned char *sV = sK + TKF * 16 * 2;        // 128 keys x 16 (MN-major B of P V)
   unsigned char *sP = sV + 16 * TKF * 2;        // 128 x 128
   const int tid = threadIdx.x, warp = tid >> 5;
   const int nseg = gridDim.y;
@@ -152,12 +159,12 @@ __global__ void __launch_bounds__(TQ, 4) k_attn_fwd_tc(const float *__restrict__
       *reinterpret_cast<uint4 *>(sK + tc::canon_off(j, 8, 16)) =
           make_uint4(pack2(kk[h2][2].x, kk[h2][2].y), pack2(kk[h2][2].z, kk[h2][2].w), pack2(kk[h2][3].x, kk[h2][3].y),
                      pack2(kk[h2][3].z, kk[h2][3].w));
-      const float vf[16] = {vv[h2][0].x, vv[h2][0].y, vv[h2][0].z, vv[h2][0].w, vv[h2][1].x, vv[h2][1].y,
-                            vv[h2][1].z, vv[h2][1].w, vv[h2][2].x, vv[h2][2].y, vv[h2][2].z, vv[h2][2].w,
-                            vv[h2][3].x, vv[h2][3].y, vv[h2][3].z, vv[h2][3].w};
-#pragma unroll
-      for (int c = 0; c < 16; c++)   // V^T: row = head dim c, column = key j
-        *reinterpret_cast<__nv_bfloat16 *>(sV + tc::canon_off(c, j, TKF)) = __float2bfloat16_rn(vf[c]);
+      *reinterpret_cast<uint4 *>(sV + tc::canon_off(j, 0, 16)) =
+          make_uint4(pack2(vv[h2][0].x, vv[h2][0].y), pack2(vv[h2][0].z, vv[h2][0].w), pack2(vv[h2][1].x, vv[h2][1].y),
+                     pack2(vv[h2][1].z, vv[h2][1].w));
+      *reinterpret_cast<uint4 *>(sV + tc::canon_off(j, 8, 16)) =
+          make_uint4(pack2(vv[h2][2].x, vv[h2][2].y), pack2(vv[h2][2].z, vv[h2][2].w), pack2(vv[h2][3].x, vv[h2][3].y),
+                     pack2(vv[h2][3].z, vv[h2][3].w));
     }
     if (kb + TKF < hi) ld_kv(qkv, kb + TKF, min(TKF, hi - kb - TKF), tid, hd, kk, vv);   // in flight meanwhile
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -255,10 +262,11 @@ __global__ void __launch_bounds__(TQ, 4) k_attn_fwd_tc(const float *__restrict__
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     // P V: M = 128, N = 16, K = 256 keys (16 steps), into TMEM columns 0..15
     if (tid == 0) {
-      const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(16 >> 3) << 17) | ((uint32_t)(TQ >> 4) << 24);
+      const uint32_t idesc =
+          (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) | ((uint32_t)(16 >> 3) << 17) | ((uint32_t)(TQ >> 4) << 24);
       const uint32_t sbo = (TKF >> 3) * 128;
       for (int ks = 0; ks < Np / 16; ks++) {
-        const uint64_t ad = tc::desc_none(su32(sP) + ks * 256, 128, sbo), bd = tc::desc_none(su32(sV) + ks * 256, 128, sbo);
+        const uint64_t ad = tc::desc_none(su32(sP) + ks * 256, 128, sbo), bd = desc_bmn(su32(sV) + ks * 512);
         asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
                      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem),
                      "l"(ad), "l"(bd), "r"(idesc), "r"(ks > 0 ? 1u : 0u));
@@ -314,10 +322,6 @@ __device__ __forceinline__ void st_row16(unsigned char *tile, int r, const float
   *reinterpret_cast<uint4 *>(tile + tc::canon_off(r, 8, 16)) =
       make_uint4(pack2(f[8], f[9]), pack2(f[10], f[11]), pack2(f[12], f[13]), pack2(f[14], f[15]));
 }
-__device__ __forceinline__ void st_col16(unsigned char *tile, int r, const float *f) {   // transposed, Kp = 128
-#pragma unroll
-  for (int c = 0; c < 16; c++) *reinterpret_cast<__nv_bfloat16 *>(tile + tc::canon_off(c, r, TQ)) = __float2bfloat16_rn(f[c]);
-}
 __device__ __forceinline__ void ld16(const float *p, float *f) {
 #pragma unroll
   for (int t = 0; t < 4; t++) {
@@ -344,6 +348,7 @@ __device__ __forceinline__ uint32_t idesc_f16(int n) {   // bf16 x bf16 -> fp32,
   return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(TQ >> 4) << 24);
 }
 constexpr uint32_t kSbo128 = (TQ >> 3) * 128;   // next 8-row group of a K-major tile with 128 columns
+__device__ __forceinline__ uint32_t idesc_f16_bmn(int n) { return idesc_f16(n) | (1u << 16); }
 
 // dQ key block: 64 keys, so S and dP take 128 TMEM columns together: 4 CTAs per SM.  The shared
 // tiles keep their 128-key layouts (Kp = 128); only the first 64 rows / K columns are used.
@@ -359,8 +364,7 @@ __global__ void __launch_bounds__(TQ, 4) k_attn_bwd_dq_tc(const float *__restric
   unsigned char *sdO = sQ + TQ * 32;      // 128 x 16 (A of dP)
   unsigned char *sK = sdO + TQ * 32;      // 128 keys x 16 (B of S)
   unsigned char *sV = sK + TQ * 32;       // 128 keys x 16 (B of dP)
-  unsigned char *sKt = sV + TQ * 32;      // 16 x 128 keys (B of dQ)
-  unsigned char *sdS = sKt + TQ * 32;     // 128 queries x 128 keys (A of dQ)
+  unsigned char *sdS = sV + TQ * 32;      // 128 queries x 128 keys (A of dQ; its B is sK read MN-major)
   const int tid = threadIdx.x, warp = tid >> 5;
   // blockIdx.x = head (fastest in dispatch order), so the four heads' longest key ranges go first
   const int tau = gridDim.y - 1 - blockIdx.y, hd = blockIdx.x;
@@ -414,7 +418,6 @@ __global__ void __launch_bounds__(TQ, 4) k_attn_bwd_dq_tc(const float *__restric
     if (tid < TKQ) {
       st_row16(sK, tid, kf);
       st_row16(sV, tid, vf);
-      st_col16(sKt, tid, kf);
     }
     if (kb + TKQ < hi) ld_kv_row(kb + TKQ);   // in flight during this block
     sync_for_mma();   // (also: the previous block's dQ has been drained by every warp)
@@ -456,8 +459,8 @@ __global__ void __launch_bounds__(TQ, 4) k_attn_bwd_dq_tc(const float *__restric
     sync_for_mma();   // every row's S / dP read, dS written
     if (tid == 0) {   // dQ_block = dS K: M = 128, N = 16, K = Np keys
       for (int ks = 0; ks < Np / 16; ks++)
-        mma_f16(tmem, tc::desc_none(su32(sdS) + ks * 256, 128, kSbo128), tc::desc_none(su32(sKt) + ks * 256, 128, kSbo128),
-                idesc_f16(16), ks > 0 ? 1u : 0u);
+        mma_f16(tmem, tc::desc_none(su32(sdS) + ks * 256, 128, kSbo128), desc_bmn(su32(sK) + ks * 512),
+                idesc_f16_bmn(16), ks > 0 ? 1u : 0u);
       mma_commit(&mbar);
     }
     tc::mbar_wait(&mbar, phase);
@@ -481,9 +484,11 @@ __global__ void __launch_bounds__(TQ, 4) k_attn_bwd_dq_tc(const float *__restric
 }
 
 // dK / dV query chunk: 64 queries, so S^T and dP^T take 128 TMEM columns together and P^T / dS^T
-// 16 KB each (56 KB of shared memory): 3 CTAs per SM instead of 2.  A query segment is staged
-// whole (Q, dO and their transposes) and processed as up to two chunks; the chunks' dK / dV are
-// summed in fp32 registers.
+// 16 KB each (48 KB of shared memory: Q and dO are read MN-major as the B of dK / dV, no transposed
+// copies; 13.95 ms per C4 M = inf step against 15.6 with the copies).  3 CTAs per SM: 4 (128
+// registers) spill the next segment's prefetched rows or, loading them at staging time, expose
+// their latency (15.5 ms measured).  A query segment is staged whole and processed as up to two
+// chunks; the chunks' dK / dV are summed in fp32 registers.
 constexpr int TQC = 64;
 constexpr uint32_t kSbo64 = (TQC >> 3) * 128;   // next 8-row group of a K-major tile with 64 columns
 __global__ void __launch_bounds__(TQ, 3) k_attn_bwd_dkv_tc(const float *__restrict__ qkv, const float *__restrict__ o,
@@ -496,11 +501,9 @@ __global__ void __launch_bounds__(TQ, 3) k_attn_bwd_dkv_tc(const float *__restri
   __shared__ __align__(16) float sL[TQ], sD[TQ];
   unsigned char *sK = sm;                 // 128 keys x 16 (A of S^T)
   unsigned char *sV = sK + TQ * 32;       // 128 keys x 16 (A of dP^T)
-  unsigned char *sQ = sV + TQ * 32;       // 128 queries x 16 (B of S^T; chunk c from row 64c)
-  unsigned char *sdO = sQ + TQ * 32;      // 128 queries x 16 (B of dP^T)
-  unsigned char *sQt = sdO + TQ * 32;     // 16 x 128 queries (B of dK; chunk c from column 64c)
-  unsigned char *sdOt = sQt + TQ * 32;    // 16 x 128 queries (B of dV)
-  unsigned char *sPt = sdOt + TQ * 32;    // 128 keys x 64 queries (A of dV)
+  unsigned char *sQ = sV + TQ * 32;       // 128 queries x 16 (B of S^T, and MN-major B of dK; chunk c from row 64c)
+  unsigned char *sdO = sQ + TQ * 32;      // 128 queries x 16 (B of dP^T, and MN-major B of dV)
+  unsigned char *sPt = sdO + TQ * 32;     // 128 keys x 64 queries (A of dV)
   unsigned char *sdSt = sPt + TQ * TQC * 2;   // 128 keys x 64 queries (A of dK)
   const int tid = threadIdx.x, warp = tid >> 5;
   // sigma = 0 has the most query segments; blockIdx.x = head, so every head's heaviest CTAs go first
@@ -559,8 +562,6 @@ __global__ void __launch_bounds__(TQ, 3) k_attn_bwd_dkv_tc(const float *__restri
       for (int c = 0; c < 16; c++) D = fmaf(gf[c], of[c], D);
       st_row16(sQ, tid, qf);
       st_row16(sdO, tid, gf);
-      st_col16(sQt, tid, qf);
-      st_col16(sdOt, tid, gf);
       sL[tid] = Lr * 1.4426950408889634f;   // LSE in log2 units, +inf past the segment (p = 0 there)
       sD[tid] = D;
     }
@@ -616,12 +617,12 @@ __global__ void __launch_bounds__(TQ, 3) k_attn_bwd_dkv_tc(const float *__restri
       }
       sync_for_mma();   // S^T / dP^T consumed, P^T and dS^T written
       if (tid == 0) {   // dK = dS^T Q -> cols [0, 16); dV = P^T dO -> cols [16, 32); K = this chunk's queries
-        const uint32_t qt = (uint32_t)(h0 >> 3) * 128;
+        const uint32_t qt = (uint32_t)(h0 >> 3) * 256;
         for (int ks = 0; ks < Nqp / 16; ks++) {
-          mma_f16(tmem, tc::desc_none(su32(sdSt) + ks * 256, 128, kSbo64), tc::desc_none(su32(sQt) + qt + ks * 256, 128, kSbo128),
-                  idesc_f16(16), ks > 0 ? 1u : 0u);
-          mma_f16(tmem + 16u, tc::desc_none(su32(sPt) + ks * 256, 128, kSbo64), tc::desc_none(su32(sdOt) + qt + ks * 256, 128, kSbo128),
-                  idesc_f16(16), ks > 0 ? 1u : 0u);
+          mma_f16(tmem, tc::desc_none(su32(sdSt) + ks * 256, 128, kSbo64), desc_bmn(su32(sQ) + qt + ks * 512),
+                  idesc_f16_bmn(16), ks > 0 ? 1u : 0u);
+          mma_f16(tmem + 16u, tc::desc_none(su32(sPt) + ks * 256, 128, kSbo64), desc_bmn(su32(sdO) + qt + ks * 512),
+                  idesc_f16_bmn(16), ks > 0 ? 1u : 0u);
         }
         mma_commit(&mbar);
       }
@@ -670,8 +671,8 @@ bool attn_fwd_tc_eligible(int S, int M) { return S >= 1 && S <= TQ && M >= -1; }
 // 0.46 ms for these two)
 bool attn_bwd_tc_long_eligible(int S, int M) { return S >= 1 && S <= TQ && M >= -1; }
 
-static const size_t kSmemDq = (size_t)5 * TQ * 32 + (size_t)TQ * TQ * 2;         // 52 KB
-static const size_t kSmemDkv = (size_t)6 * TQ * 32 + (size_t)2 * TQ * TQC * 2;   // 56 KB
+static const size_t kSmemDq = (size_t)4 * TQ * 32 + (size_t)TQ * TQ * 2;         // 48 KB
+static const size_t kSmemDkv = (size_t)4 * TQ * 32 + (size_t)2 * TQ * TQC * 2;   // 48 KB
 void launch_attn_bwd_dq_tc(const float *qkv, const float *o, const float *lse, const float *dout, float *dqkv, int N,
                            int S, int M, cudaStream_t s) {
   const int nseg = (N + S - 1) / S;
