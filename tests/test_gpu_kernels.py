@@ -205,9 +205,11 @@ def test_tensor_core_kernels_c2(gdp):
     print({k: round(v, 4) for k, v in worst.items()})
 
 
-@pytest.mark.parametrize("S,M", [(96, 160), (100, 60), (100, -1)])
+@pytest.mark.parametrize("S,M", [(96, 160), (100, 60), (100, -1), (8, 24), (20, -1), (33, 33), (1, 5)])
 def test_tensor_core_kernels_memory_lengths(gdp, S, M):
-    """Ragged segments, M > S (several key blocks, the dQ / dK-dV kernels), M < S, M = inf."""
+    """Ragged segments, M > S (several key blocks, the dQ / dK-dV kernels), M < S, M = inf; short
+    segments (S = 1, 8, 20, 33: one 16-row K step of the MN-major Q / dO / K / V operands, mostly
+    zero padding rows)."""
     g = workloads.random_dag(1000, p_edge=0.05, max_back=60, seed=21)
     run_kernel_checks(gdp, g, 4, S, M, 16)
 
