@@ -700,9 +700,13 @@ __global__ void __launch_bounds__(64, COST5_MINB) k_cost5(Cost5Graph G, TopoArgs
         ce1 = __ballot_sync(FULL, ca1 == cmin);
       }
       // the running finishes' minimum likewise; the dispatch below lowers it with each new finish
+      // (recomputed every instant: skipping it on instants without a finish, where it cannot have
+      // risen, measured 1 % slower -- the branch costs more than the REDUX)
       dmin = (int)__reduce_min_sync(FULL, (unsigned)dfr);
       // ---------------------------------------------------------- (3) FIFO append + dispatch
       for (att |= incm, incm = 0; att; att &= att - 1) {
+        P5(3);
+        P5C(11);
         const int k = __ffs(att) - 1;
         const int4 dvk = S.dv[k], dv2k = S.dv2[k];
         const int n = dvk.w;
@@ -750,8 +754,10 @@ __global__ void __launch_bounds__(64, COST5_MINB) k_cost5(Cost5Graph G, TopoArgs
           S.dv[k].y = ++fh;
           go = true;
         }
+        P5(4);
         int cur = dv2k.x, nxt = dv2k.y;
         if (go) {
+          P5C(7);
           const int fin = t + run.cost * dv2k.z;
           S.dv[k].x = fin;
           if (lane == k) dfr = fin;
@@ -763,6 +769,7 @@ __global__ void __launch_bounds__(64, COST5_MINB) k_cost5(Cost5Graph G, TopoArgs
           nxt = -1;
           running = true;
         }
+        P5(5);
         if (running && fh < ft && nxt < 0) {   // stage the op now waiting at the head
           Q5 hr;
           load_q5(hr, &S.fc[k][fh & (KF5 - 1)]);
@@ -770,6 +777,7 @@ __global__ void __launch_bounds__(64, COST5_MINB) k_cost5(Cost5Graph G, TopoArgs
           if (hr.nn & 0xffff) stage(k, cur ^ 1, hr);
         }
         *reinterpret_cast<int2 *>(&S.dv2[k]) = make_int2(cur, nxt);
+        P5(6);
       }
       __syncwarp();
       P5(3);
@@ -778,6 +786,9 @@ __global__ void __launch_bounds__(64, COST5_MINB) k_cost5(Cost5Graph G, TopoArgs
     if (b == 0 && lane == 0)
       printf("C5PROF inst=%lld fin_inst=%lld ensure_waits=%lld next=%lld arr=%lld fin=%lld disp=%lld\n", prof[9],
              prof[10], prof[8], prof[0], prof[1], prof[2], prof[3]);
+    if (b == 0 && lane == 0)
+      printf("C5DISP iters=%lld go=%lld top+redux=%lld decide=%lld goblk=%lld look=%lld\n", prof[11], prof[7], prof[3],
+             prof[4], prof[5], prof[6]);
 #endif
     // ---------------------------------------------------------- end of the simulation
     item(IT_END, 0, 0);
