@@ -440,6 +440,7 @@ static Cost5Graph cost5_graph(const gdp_graph_s *g) {
   C.slots = static_cast<const Slot5 *>(g->slots5); C.srcq = static_cast<const Q5 *>(g->srcq5);
   C.ebytes = static_cast<const long long *>(g->ebytes5);
   C.irec = static_cast<const IRec *>(g->irec);
+  C.in_ptr = g->in_ptr;
   C.out_idx = g->out_idx; C.out_src = g->out_src; C.cost = g->cost; C.leader = g->leader;
   C.outdeg = g->outdeg5; C.gbig0 = g->gbig5; C.bigb0 = g->bigb5;
   C.out_bytes = g->out_bytes; C.mem_bytes = g->mem_bytes;

@@ -61,6 +61,7 @@ struct Cost5Graph {
   const Q5 *srcq;
   const IRec *irec;
   const int *out_idx, *out_src, *cost, *leader, *outdeg, *gbig0;
+  const int *in_ptr;   // N + 1: in-CSR offsets (the memory warp expands a finish into its in-edges)
   const unsigned *bigb0;
   const long long *out_bytes, *mem_bytes;
   int nsrc, nbigb, ngbig, nflagw, has_coloc;

@@ -97,7 +97,8 @@ constexpr int MB5 = COST5_MB;       // the memory warp waits for this many items
   } while (0)
 #endif
 
-enum { IT_ALLOC_OP = 0, IT_ALLOC_COPY = 1, IT_INEDGE = 2, IT_SINK = 3, IT_END = 4 };
+// IT_FIN: an op with inputs finished (idx = its id); the memory warp expands it into its in-edges
+enum { IT_ALLOC_OP = 0, IT_ALLOC_COPY = 1, IT_INEDGE = 2, IT_SINK = 3, IT_END = 4, IT_FIN = 5 };
 
 
 struct Pre5 {   // per-placement results of k_cost5_pre
@@ -123,11 +124,11 @@ struct Smem5 {
   unsigned long long hbar[NCH];     // mbarrier of each channel's head fetch
   Slot5 stage[8][2][SO5];           // out-edge slots of the running / next op of each device
   unsigned sdev[8][2][SO5];         // each staged slot's word from k_cost5_pre: consumer device | transfer time << 3
-  Q5 fc[8][KF5];                    // FIFO rings
-  Q5 inc[8][NINC5];                 // ops made available at this instant
+  int4 fc[8][KF5];                  // FIFO rings: id, cost, ob, nn (the queue fields a dispatch reads)
+  int4 inc[8][NINC5];               // ops made available at this instant (same fields)
   unsigned long long items[RI5];    // memory items: t | code << 32
   unsigned long long ibar;          // mbarrier: one phase per 32 items appended (and one at the end)
-  int4 drun[8];                     // the op running on each device: id, ob, nn, ib -- what its finish
+  int4 drun[8];                     // the op running on each device: id, ob, nn -- what its finish
                                     // reads (one 16-byte load / store instead of a 32-byte Q5: -1.7 %)
   int4 ch[NCH];                     // per channel: tail, free (transfer end), head
   int ca[NCH];                      // arrival tick of each channel's head entry (INF: empty; contiguous: the
@@ -423,8 +424,8 @@ __global__ void __launch_bounds__(64, COST5_MINB) k_cost5(Cost5Graph G, TopoArgs
   const unsigned *sdev_g = reinterpret_cast<const unsigned *>(base + L.sdev);
   int *outcnt = reinterpret_cast<int *>(base + L.outcnt);
   int *gbig = reinterpret_cast<int *>(base + L.gbig);
-  Q5 *fifo_g = reinterpret_cast<Q5 *>(base + L.fifo);
-  Q5 *ov_g = reinterpret_cast<Q5 *>(base + L.ov);
+  int4 *fifo_g = reinterpret_cast<int4 *>(base + L.fifo);
+  int4 *ov_g = reinterpret_cast<int4 *>(base + L.ov);
   int2 *chq_g = reinterpret_cast<int2 *>(base + L.chq);
 
   // ------------------------------------------------------------ prologue (both warps)
@@ -507,8 +508,9 @@ __global__ void __launch_bounds__(64, COST5_MINB) k_cost5(Cost5Graph G, TopoArgs
     };
     auto to_inc = [&](int q, const Q5 &r) {       // uniform
       const int n = S.dv[q].w;
-      if (n < NINC5) store_q5(&S.inc[q][n], r);
-      else store_q5(ov_g + S.doff[q] + n, r);
+      const int4 x = make_int4(r.id, r.cost, r.ob, r.nn);
+      if (n < NINC5) S.inc[q][n] = x;
+      else ov_g[S.doff[q] + n] = x;
       S.dv[q].w = n + 1;
       incm |= 1u << q;
     };
@@ -532,10 +534,10 @@ __global__ void __launch_bounds__(64, COST5_MINB) k_cost5(Cost5Graph G, TopoArgs
       gbig[ix] = o - 1;
       return o == 1;
     };
-    auto stage = [&](int k, int sl, const Q5 &r) {   // lane j copies out-edge slot j and its device byte
-      const int no = min(r.nn & 0xffff, SO5);
+    auto stage = [&](int k, int sl, const int4 &r) {   // lane j copies out-edge slot j and its device byte
+      const int no = min(r.w & 0xffff, SO5);
       if (lane < no) {
-        const int e = r.ob + lane;
+        const int e = r.z + lane;
         cp_32(&S.stage[k][sl][lane], G.slots + e);
         cp_4(&S.sdev[k][sl][lane], sdev_g + e);
         spend |= 1u << (2 * k + sl);
@@ -546,12 +548,11 @@ __global__ void __launch_bounds__(64, COST5_MINB) k_cost5(Cost5Graph G, TopoArgs
     __syncwarp();
     // sources are available at t = 0: appended to their FIFO in ascending id (uniform)
     for (int i = 0; i < G.nsrc; i++) {
-      Q5 r;
-      load_q5(r, G.srcq + i);
-      const int q = D[r.id];
+      const int4 r = reinterpret_cast<const int4 *>(G.srcq + i)[0];   // id, cost, ob, nn
+      const int q = D[r.x];
       const int f = S.dv[q].z;
-      if (f < KF5) store_q5(&S.fc[q][f], r);
-      else store_q5(fifo_g + S.doff[q] + f, r);
+      if (f < KF5) S.fc[q][f] = r;
+      else fifo_g[S.doff[q] + f] = r;
       S.dv[q].z = f + 1;
     }
     unsigned att = (1u << d) - 1u;   // devices to dispatch at t = 0
@@ -616,27 +617,16 @@ __global__ void __launch_bounds__(64, COST5_MINB) k_cost5(Cost5Graph G, TopoArgs
             }
           }
           ef &= ~(1u << k);
-          Q5 r;   // id, ob, nn, ib
+          Q5 r;   // id, ob, nn
           {
             const int4 rr = S.drun[k];
-            r.id = rr.x; r.ob = rr.y; r.nn = rr.z; r.ib = rr.w;
+            r.id = rr.x; r.ob = rr.y; r.nn = rr.z;
           }
           const int sl = S.dv2[k].x;
           S.dv[k].x = INF;
           if (lane == k) dfr = INF;
           const int nout = r.nn & 0xffff, nin = (int)((unsigned)r.nn >> 16);
-          for (int j0 = 0; j0 < nin; j0 += 32) {   // frees of this finish -> memory warp, one item per lane
-            const int n = min(32, nin - j0);
-            ensure((unsigned)n);
-            if (lane < n) S.items[(itail + lane) & (RI5 - 1)] = item5(t, IT_INEDGE, k, r.ib + j0 + lane, itail + lane);
-#if COST5_MBAR
-            if ((itail >> 5) != ((itail + n) >> 5)) {   // a batch of 32 is complete
-              __syncwarp();
-              if (lane == 0) mbar_arrive5(&S.ibar);
-            }
-#endif
-            itail += n;
-          }
+          if (nin) item(IT_FIN, k, r.id);   // its frees: the memory warp expands it into the in-edges
           if (nout == 0) item(IT_SINK, k, r.id);
           for (int j0 = 0; j0 < nout; j0 += 32) {   // out-edges, one per lane
             const int j = j0 + lane;
@@ -663,8 +653,9 @@ __global__ void __launch_bounds__(64, COST5_MINB) k_cost5(Cost5Graph G, TopoArgs
               const int n0 = S.dv[k].w;
               if (av) {
                 const int pos = n0 + __popc(am & lt);
-                if (pos < NINC5) store_q5(&S.inc[k][pos], q_of_slot(e, 0, r.id));
-                else store_q5(ov_g + S.doff[k] + pos, q_of_slot(e, 0, r.id));
+                const int4 x = make_int4(e.w, e.cost, e.ob, e.nn);
+                if (pos < NINC5) S.inc[k][pos] = x;
+                else ov_g[S.doff[k] + pos] = x;
               }
               __syncwarp();
               S.dv[k].w = n0 + __popc(am);
@@ -716,45 +707,38 @@ __global__ void __launch_bounds__(64, COST5_MINB) k_cost5(Cost5Graph G, TopoArgs
         const int n = dvk.w;
         bool running = dvk.x != INF, go = false;
         int fh = dvk.y, ft = dvk.z;
-        Q5 run;
+        int4 run;   // id, cost, ob, nn
         if (n > 0) {
           S.dv[k].w = 0;
-          Q5 *Li = &S.inc[k][0];
-          Q5 *Lo = ov_g + S.doff[k];
+          int4 *Li = &S.inc[k][0];
+          int4 *Lo = ov_g + S.doff[k];
           if (n == 1 && !running && fh == ft) {   // common case: straight to dispatch
-            load_q5(run, Li);
+            run = Li[0];
             go = true;
           } else {
             for (int i = 1; i < n; i++) {   // insertion sort by id (n is small except after wide fan-outs)
-              Q5 key;
-              load_q5(key, i < NINC5 ? &Li[i] : &Lo[i]);
+              const int4 key = i < NINC5 ? Li[i] : Lo[i];
               int j = i - 1;
               while (j >= 0) {
-                Q5 pj;
-                load_q5(pj, j < NINC5 ? &Li[j] : &Lo[j]);
-                if (pj.id <= key.id) break;
-                store_q5(j + 1 < NINC5 ? &Li[j + 1] : &Lo[j + 1], pj);
+                const int4 pj = j < NINC5 ? Li[j] : Lo[j];
+                if (pj.x <= key.x) break;
+                (j + 1 < NINC5 ? Li[j + 1] : Lo[j + 1]) = pj;
                 j--;
               }
-              store_q5(j + 1 < NINC5 ? &Li[j + 1] : &Lo[j + 1], key);
+              (j + 1 < NINC5 ? Li[j + 1] : Lo[j + 1]) = key;
             }
             for (int i = 0; i < n; i++, ft++) {
-              Q5 x;
-              load_q5(x, i < NINC5 ? &Li[i] : &Lo[i]);
-              if (ft < fh + KF5) store_q5(&S.fc[k][ft & (KF5 - 1)], x);
-              else store_q5(fifo_g + S.doff[k] + ft, x);
+              const int4 x = i < NINC5 ? Li[i] : Lo[i];
+              if (ft < fh + KF5) S.fc[k][ft & (KF5 - 1)] = x;
+              else fifo_g[S.doff[k] + ft] = x;
             }
             S.dv[k].z = ft;
           }
         }
         if (!go && !running && fh < ft) {   // pop the FIFO head
           const int s = fh & (KF5 - 1);
-          load_q5(run, &S.fc[k][s]);
-          if (fh + KF5 < ft) {   // the slot takes position fh + KF5 from the global overflow (rare)
-            Q5 x;
-            load_q5(x, fifo_g + S.doff[k] + fh + KF5);
-            store_q5(&S.fc[k][s], x);
-          }
+          run = S.fc[k][s];
+          if (fh + KF5 < ft) S.fc[k][s] = fifo_g[S.doff[k] + fh + KF5];   // position fh + KF5 from the overflow (rare)
           S.dv[k].y = ++fh;
           go = true;
         }
@@ -762,23 +746,22 @@ __global__ void __launch_bounds__(64, COST5_MINB) k_cost5(Cost5Graph G, TopoArgs
         int cur = dv2k.x, nxt = dv2k.y;
         if (go) {
           P5C(7);
-          const int fin = t + run.cost * dv2k.z;
+          const int fin = t + run.y * dv2k.z;
           S.dv[k].x = fin;
           if (lane == k) dfr = fin;
           dmin = min(dmin, fin);
-          S.drun[k] = make_int4(run.id, run.ob, run.nn, run.ib);
-          item(IT_ALLOC_OP, k, run.id);
+          S.drun[k] = make_int4(run.x, run.z, run.w, 0);
+          item(IT_ALLOC_OP, k, run.x);
           cur ^= 1;   // the slot the head was staged into, or the one it is staged into now
-          if (run.id != nxt && (run.nn & 0xffff)) stage(k, cur, run);
+          if (run.x != nxt && (run.w & 0xffff)) stage(k, cur, run);
           nxt = -1;
           running = true;
         }
         P5(5);
         if (running && fh < ft && nxt < 0) {   // stage the op now waiting at the head
-          Q5 hr;
-          load_q5(hr, &S.fc[k][fh & (KF5 - 1)]);
-          nxt = hr.id;
-          if (hr.nn & 0xffff) stage(k, cur ^ 1, hr);
+          const int4 hr = S.fc[k][fh & (KF5 - 1)];
+          nxt = hr.x;
+          if (hr.w & 0xffff) stage(k, cur ^ 1, hr);
         }
         *reinterpret_cast<int2 *>(&S.dv2[k]) = make_int2(cur, nxt);
         P5(6);
@@ -845,43 +828,73 @@ __global__ void __launch_bounds__(64, COST5_MINB) k_cost5(Cost5Graph G, TopoArgs
       nitems += n;
 #endif
       const bool mine = lane < n;
-      const int ti = (int)(unsigned)(it & 0xffffffffull);
-      const int kind = (int)((code >> 1) & 7u), dev = (int)((code >> 4) & 7u), idx = (int)(code >> 7);
-      ndisp += __popc(__ballot_sync(FULL, mine && kind == IT_ALLOC_OP));   // one item per dispatch
-      int dA = -1, dB = -1, u = -1;
-      long long xA = 0, xB = 0, bu = 0;
-      int du = 0;
+      const int ti0 = (int)(unsigned)(it & 0xffffffffull);
+      const int kind0 = (int)((code >> 1) & 7u), dev0 = (int)((code >> 4) & 7u), idx0 = (int)(code >> 7);
+      ndisp += __popc(__ballot_sync(FULL, mine && kind0 == IT_ALLOC_OP));   // one item per dispatch
+      // the batch expanded in order: an IT_FIN item becomes its op's in-edges (in-CSR order), every
+      // other item stays one; processed 32 expanded items at a time
+      int ib0 = 0, cnt = 0;
       if (mine) {
-        if (kind == IT_ALLOC_OP) { dA = dev; xA = G.out_bytes[idx]; }
-        else if (kind == IT_ALLOC_COPY) { dA = dev; xA = G.slots[idx].bytes; }   // idx = the copy's out-edge slot
-        else if (kind == IT_SINK) { dA = dev; xA = -G.out_bytes[idx]; }
-        else if (kind == IT_INEDGE) {
-          const IRec ir = G.irec[idx];
-          u = ir.u;
-          bu = ir.bytes;
-          du = D[u];
-          if (du != dev) { dA = dev; xA = -bu; }   // the copy this op held
-        } else {
-          done = true;
+        if (kind0 == IT_FIN) { ib0 = G.in_ptr[idx0]; cnt = G.in_ptr[idx0 + 1] - ib0; }
+        else cnt = 1;
+      }
+      int iend = cnt;   // inclusive prefix sum: item i covers expanded positions [iend - cnt, iend)
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(FULL, iend, o);
+        if (lane >= o) iend += y;
+      }
+      const int total = __shfl_sync(FULL, iend, 31);
+      for (int w0 = 0; w0 < total; w0 += 32) {
+        const int w = w0 + lane;
+        int src = 0;   // the item covering position w: the number of items whose range ends at or before w
+#pragma unroll
+        for (int step = 16; step; step >>= 1) {
+          const int e = __shfl_sync(FULL, iend, src + step - 1);
+          if (e <= w) src += step;
         }
-      }
-      done = __any_sync(FULL, done);
-      {  // producers whose last consumer finishes: one counter update per producer and batch
-        const unsigned grp = __match_any_sync(FULL, u);
-        const int leader = __ffs(grp) - 1, last = 31 - __clz(grp), cnt = __popc(grp);
-        int old = 0;
-        if (u >= 0 && lane == leader) old = atomicSub(&outcnt[u], cnt);
-        old = __shfl_sync(FULL, old, leader);
-        if (u >= 0 && lane == last && old == cnt) { dB = du; xB = -bu; }
-      }
-      // apply in item order; sample the peak whenever the instant changes
-      for (int i = 0; i < n; i++) {
-        const int tI = __shfl_sync(FULL, ti, i);
-        const int aD = __shfl_sync(FULL, dA, i), bD = __shfl_sync(FULL, dB, i);
-        const long long aX = __shfl_sync(FULL, xA, i), bX = __shfl_sync(FULL, xB, i);
-        if (tI != last_t) { pk = max(pk, mem); last_t = tI; }
-        if (aD == lane) mem += aX;
-        if (bD == lane) mem += bX;
+        const bool vmine = w < total;
+        const int ti = __shfl_sync(FULL, ti0, src), kind_s = __shfl_sync(FULL, kind0, src);
+        const int dev = __shfl_sync(FULL, dev0, src), idx_s = __shfl_sync(FULL, idx0, src);
+        const int sbeg = __shfl_sync(FULL, iend - cnt, src), sib = __shfl_sync(FULL, ib0, src);
+        const int kind = kind_s == IT_FIN ? IT_INEDGE : kind_s;
+        const int idx = kind_s == IT_FIN ? sib + (w - sbeg) : idx_s;
+        int dA = -1, dB = -1, u = -1;
+        long long xA = 0, xB = 0, bu = 0;
+        int du = 0;
+        if (vmine) {
+          if (kind == IT_ALLOC_OP) { dA = dev; xA = G.out_bytes[idx]; }
+          else if (kind == IT_ALLOC_COPY) { dA = dev; xA = G.slots[idx].bytes; }   // idx = the copy's out-edge slot
+          else if (kind == IT_SINK) { dA = dev; xA = -G.out_bytes[idx]; }
+          else if (kind == IT_INEDGE) {
+            const IRec ir = G.irec[idx];
+            u = ir.u;
+            bu = ir.bytes;
+            du = D[u];
+            if (du != dev) { dA = dev; xA = -bu; }   // the copy this op held
+          } else {
+            done = true;
+          }
+        }
+        done = __any_sync(FULL, done);
+        {  // producers whose last consumer finishes: one counter update per producer and round
+          const unsigned grp = __match_any_sync(FULL, u);
+          const int leader = __ffs(grp) - 1, last = 31 - __clz(grp), cnt2 = __popc(grp);
+          int old = 0;
+          if (u >= 0 && lane == leader) old = atomicSub(&outcnt[u], cnt2);
+          old = __shfl_sync(FULL, old, leader);
+          if (u >= 0 && lane == last && old == cnt2) { dB = du; xB = -bu; }
+        }
+        // apply in item order; sample the peak whenever the instant changes
+        const int nv = min(32, total - w0);
+        for (int i = 0; i < nv; i++) {
+          const int tI = __shfl_sync(FULL, ti, i);
+          const int aD = __shfl_sync(FULL, dA, i), bD = __shfl_sync(FULL, dB, i);
+          const long long aX = __shfl_sync(FULL, xA, i), bX = __shfl_sync(FULL, xB, i);
+          if (tI != last_t) { pk = max(pk, mem); last_t = tI; }
+          if (aD == lane) mem += aX;
+          if (bD == lane) mem += bX;
+        }
       }
       mh += n;
       __syncwarp();
