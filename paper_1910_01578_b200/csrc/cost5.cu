@@ -625,9 +625,10 @@ __global__ void __launch_bounds__(64, COST5_MINB) k_cost5(Cost5Graph G, TopoArgs
           const int sl = S.dv2[k].x;
           S.dv[k].x = INF;
           if (lane == k) dfr = INF;
-          const int nout = r.nn & 0xffff, nin = (int)((unsigned)r.nn >> 16);
-          if (nin) item(IT_FIN, k, r.id);   // its frees: the memory warp expands it into the in-edges
-          if (nout == 0) item(IT_SINK, k, r.id);
+          const int nout = r.nn & 0xffff;
+          // its frees, one item: the memory warp expands it into the in-edges (the copies this op
+          // held, producers it was the last consumer of) and, for a sink, its own output
+          item(IT_FIN, k, r.id);
           for (int j0 = 0; j0 < nout; j0 += 32) {   // out-edges, one per lane
             const int j = j0 + lane;
             const bool valid = j < nout;
@@ -833,10 +834,15 @@ __global__ void __launch_bounds__(64, COST5_MINB) k_cost5(Cost5Graph G, TopoArgs
       ndisp += __popc(__ballot_sync(FULL, mine && kind0 == IT_ALLOC_OP));   // one item per dispatch
       // the batch expanded in order: an IT_FIN item becomes its op's in-edges (in-CSR order), every
       // other item stays one; processed 32 expanded items at a time
-      int ib0 = 0, cnt = 0;
+      int ib0 = 0, cnt = 0, sink = 0;
       if (mine) {
-        if (kind0 == IT_FIN) { ib0 = G.in_ptr[idx0]; cnt = G.in_ptr[idx0 + 1] - ib0; }
-        else cnt = 1;
+        if (kind0 == IT_FIN) {
+          ib0 = G.in_ptr[idx0];
+          sink = G.outdeg[idx0] == 0;
+          cnt = G.in_ptr[idx0 + 1] - ib0 + sink;   // its in-edges, then (a sink) its output
+        } else {
+          cnt = 1;
+        }
       }
       int iend = cnt;   // inclusive prefix sum: item i covers expanded positions [iend - cnt, iend)
 #pragma unroll
@@ -857,8 +863,10 @@ __global__ void __launch_bounds__(64, COST5_MINB) k_cost5(Cost5Graph G, TopoArgs
         const int ti = __shfl_sync(FULL, ti0, src), kind_s = __shfl_sync(FULL, kind0, src);
         const int dev = __shfl_sync(FULL, dev0, src), idx_s = __shfl_sync(FULL, idx0, src);
         const int sbeg = __shfl_sync(FULL, iend - cnt, src), sib = __shfl_sync(FULL, ib0, src);
-        const int kind = kind_s == IT_FIN ? IT_INEDGE : kind_s;
-        const int idx = kind_s == IT_FIN ? sib + (w - sbeg) : idx_s;
+        const int ssink = __shfl_sync(FULL, sink, src), send = __shfl_sync(FULL, iend, src);
+        const bool fsink = kind_s == IT_FIN && ssink && w == send - 1;   // the last position of a sink's FIN
+        const int kind = kind_s == IT_FIN ? (fsink ? IT_SINK : IT_INEDGE) : kind_s;
+        const int idx = kind_s == IT_FIN ? (fsink ? idx_s : sib + (w - sbeg)) : idx_s;
         int dA = -1, dB = -1, u = -1;
         long long xA = 0, xB = 0, bu = 0;
         int du = 0;
