@@ -574,7 +574,7 @@ gdp_status gdp_graph_create(int32_t N, int32_t F, const float *feat, int64_t E, 
     g->nflagw5 = h5.nflagw;
     UP(slots5, h5.slots.data(), h5.slots.size() * sizeof(Slot5));
     UP(ebytes5, h5.ebytes.data(), h5.ebytes.size() * sizeof(long long));
-    UP(srcq5, h5.srcq.data(), h5.srcq.size() * sizeof(Q5));
+    UP(srcq5, h5.srcq.data(), h5.srcq.size() * sizeof(Slot5));
     UP(gbig5, h5.gbig.data(), h5.gbig.size() * sizeof(int));
     UP(outdeg5, h5.outdeg.data(), h5.outdeg.size() * sizeof(int));
     UP(bigb5, h5.bigb.data(), h5.bigb.size() * sizeof(unsigned));

@@ -437,7 +437,7 @@ static TopoArgs topo_args(const gdp_topo_s *t) {
 static Cost5Graph cost5_graph(const gdp_graph_s *g) {
   Cost5Graph C;
   C.N = g->N; C.E = g->E; C.ok = g->c5_ok ? 1 : 0;
-  C.slots = static_cast<const Slot5 *>(g->slots5); C.srcq = static_cast<const Q5 *>(g->srcq5);
+  C.slots = static_cast<const Slot5 *>(g->slots5); C.srcq = static_cast<const Slot5 *>(g->srcq5);
   C.ebytes = static_cast<const long long *>(g->ebytes5);
   C.irec = static_cast<const IRec *>(g->irec);
   C.in_ptr = g->in_ptr;

@@ -39,15 +39,31 @@ struct __align__(16) Q5 {     // an op in a queue (channel ring, FIFO, available
   int ib;                     // first in-edge slot
   int arr, u;                 // channel entries: arrival tick and producer id
 };
-struct __align__(16) Slot5 {  // out-edge slot e = (v -> w), out-CSR order, 32 bytes
-  int w, cost, ob, nn, cinfo, ib;   // the consumer's queue fields
-  long long bytes;                  // the producer's output bytes (the copy on this edge)
+// The 16-byte queue record of an op (the consumer w of an out-edge slot e = (v -> w), out-CSR
+// order; a source; a FIFO / available / channel-head entry): its id, compute cost, first out-edge
+// slot, out-degree and input-counter info (kind + index, 27 bits) packed into the spare high bits
+// (N, E < 2^25, degrees < 2^16):
+//   x = id | ix[18:25) << 25      y = cost
+//   z = ob | kind << 25 | ix[16:18) << 27      w = out-degree | ix[0:16) << 16
+// where cinfo = kind | ix << 2 (kind 0: at most one input, 1: two inputs (flag bit), 2: 4-bit
+// counter (3..15 inputs), 3: global counter).  The copy's bytes are in ebytes (per slot).
+struct __align__(16) Slot5 {
+  int x, cost, z, w;
 };
+__host__ __device__ __forceinline__ Slot5 pack_slot5(int id, int cost, int ob, int nout, int cinfo) {
+  const unsigned kind = (unsigned)cinfo & 3u, ix = (unsigned)cinfo >> 2;
+  Slot5 s;
+  s.x = (int)((unsigned)id | ((ix >> 18) << 25));
+  s.cost = cost;
+  s.z = (int)((unsigned)ob | (kind << 25) | (((ix >> 16) & 3u) << 27));
+  s.w = (int)(((unsigned)nout & 0xffffu) | ((ix & 0xffffu) << 16));
+  return s;
+}
 struct Cost5Host {            // host images built at graph creation (cost5_build)
   bool ok = false;
   std::vector<Slot5> slots;
   std::vector<long long> ebytes;   // per out-edge slot: the producer's output bytes (k_cost5_pre, contiguous)
-  std::vector<Q5> srcq;        // the sources, ascending id
+  std::vector<Slot5> srcq;     // the sources, ascending id
   std::vector<int> gbig, outdeg;
   std::vector<unsigned> bigb;  // 4-bit counters (in-degree 3..15), 8 per word, 16-byte padded
   int nflagw = 0;              // words of the two-input flag bitmap
@@ -58,7 +74,7 @@ struct Cost5Graph {
   int ok;
   const Slot5 *slots;
   const long long *ebytes;
-  const Q5 *srcq;
+  const Slot5 *srcq;
   const IRec *irec;
   const int *out_idx, *out_src, *cost, *leader, *outdeg, *gbig0;
   const int *in_ptr;   // N + 1: in-CSR offsets (the memory warp expands a finish into its in-edges)

@@ -118,11 +118,11 @@ __device__ __forceinline__ int cdst(int ci) {
 }
 
 struct Smem5 {
-  Q5 chd[NCH];                      // each channel's head entry in full (the consumer's queue fields;
+  int4 chd[NCH];                    // each channel's head entry: the consumer's packed record (Slot5;
                                     // fetched by a bulk copy of its out-edge slot when it becomes the head)
   int2 cq[NCH][KC5];                // channel rings, compact: (out-edge slot, arrival tick)
   unsigned long long hbar[NCH];     // mbarrier of each channel's head fetch
-  Slot5 stage[8][2][SO5];           // out-edge slots of the running / next op of each device
+  int4 stage[8][2][SO5];            // out-edge slots (packed Slot5) of the running / next op of each device
   unsigned sdev[8][2][SO5];         // each staged slot's word from k_cost5_pre: consumer device | transfer time << 3
   int4 fc[8][KF5];                  // FIFO rings: id, cost, ob, nn (the queue fields a dispatch reads)
   int4 inc[8][NINC5];               // ops made available at this instant (same fields)
@@ -159,42 +159,24 @@ __host__ __device__ inline Scratch5 scratch5_layout(int N, long long E, int ngbi
   return s;
 }
 
-__device__ __forceinline__ void load_q5(Q5 &r, const Q5 *src) {
-  const int4 *s = reinterpret_cast<const int4 *>(src);
-  const int4 a = s[0], b = s[1];
-  r.id = a.x; r.cost = a.y; r.ob = a.z; r.nn = a.w; r.cinfo = b.x; r.ib = b.y; r.arr = b.z; r.u = b.w;
-}
-__device__ __forceinline__ void store_q5(Q5 *dst, const Q5 &r) {
-  int4 *d = reinterpret_cast<int4 *>(dst);
-  d[0] = make_int4(r.id, r.cost, r.ob, r.nn);
-  d[1] = make_int4(r.cinfo, r.ib, r.arr, r.u);
-}
-// the queue fields of an out-edge slot's consumer (+ arrival and producer for a channel entry)
-__device__ __forceinline__ Q5 q_of_slot(const Slot5 &e, int arr, int u) {
-  Q5 r;
-  r.id = e.w; r.cost = e.cost; r.ob = e.ob; r.nn = e.nn; r.cinfo = e.cinfo; r.ib = e.ib; r.arr = arr; r.u = u;
-  return r;
-}
-__device__ __forceinline__ void load_slot5(Slot5 &e, const Slot5 *src) {
-  const int4 *s = reinterpret_cast<const int4 *>(src);
-  const int4 a = s[0], b = s[1];
-  e.w = a.x; e.cost = a.y; e.ob = a.z; e.nn = a.w; e.cinfo = b.x; e.ib = b.y;
-  e.bytes = ((long long)(unsigned)b.z) | ((long long)b.w << 32);
-}
-__device__ __forceinline__ void cp_32(void *s, const void *g) {
-  cp16(reinterpret_cast<int4 *>(s), g);
-  cp16(reinterpret_cast<int4 *>(s) + 1, reinterpret_cast<const int4 *>(g) + 1);
+// fields of a packed record (Slot5 layout, held as int4)
+constexpr int M25 = (1 << 25) - 1;
+__device__ __forceinline__ int rec_id(const int4 &r) { return r.x & M25; }
+__device__ __forceinline__ int rec_ob(const int4 &r) { return r.z & M25; }
+__device__ __forceinline__ int rec_cinfo(const int4 &r) {
+  const unsigned ix = ((unsigned)r.w >> 16) | ((((unsigned)r.z >> 27) & 3u) << 16) | (((unsigned)r.x >> 25) << 18);
+  return (int)((((unsigned)r.z >> 25) & 3u) | (ix << 2));
 }
 __device__ __forceinline__ void cp_4(void *s, const void *g) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"((unsigned)__cvta_generic_to_shared(s)), "l"(g)
                : "memory");
 }
-// a channel's new head: its out-edge slot (32 bytes) copied by the bulk-copy engine, completing
+// a channel's new head: its out-edge slot (16 bytes) copied by the bulk-copy engine, completing
 // on the channel's mbarrier (independent of the cp.async groups of the staging copies)
-__device__ __forceinline__ void head_fetch(Q5 *dst, const Slot5 *src, unsigned long long *mb) {
+__device__ __forceinline__ void head_fetch(int4 *dst, const Slot5 *src, unsigned long long *mb) {
   const unsigned m = (unsigned)__cvta_generic_to_shared(mb);
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], 32;" ::"r"(m) : "memory");
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 32, [%2];" ::"r"(
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], 16;" ::"r"(m) : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 16, [%2];" ::"r"(
                    (unsigned)__cvta_generic_to_shared(dst)),
                "l"(src), "r"(m)
                : "memory");
@@ -400,7 +382,7 @@ __global__ void __launch_bounds__(512) k_cost5_pre(Cost5Graph G, TopoArgs T, con
 // warps; so successive CTAs on the same (SM, sub-partition pair) alternate the simulating warp.
 __device__ unsigned g_c5_pair[2 * 1024];
 #ifndef COST5_MINB
-#define COST5_MINB 12
+#define COST5_MINB 14
 #endif
 __global__ void __launch_bounds__(64, COST5_MINB) k_cost5(Cost5Graph G, TopoArgs T, const uint8_t *__restrict__ Dall,
                                               unsigned char *scratch, size_t per_place, gdp_sim_report *rep,
@@ -506,9 +488,8 @@ __global__ void __launch_bounds__(64, COST5_MINB) k_cost5(Cost5Graph G, TopoArgs
       if ((itail & 31u) == 0u && lane == 0) mbar_arrive5(&S.ibar);   // a batch of 32 is complete
 #endif
     };
-    auto to_inc = [&](int q, const Q5 &r) {       // uniform
+    auto to_inc = [&](int q, const int4 &x) {     // uniform; x: the op's packed record
       const int n = S.dv[q].w;
-      const int4 x = make_int4(r.id, r.cost, r.ob, r.nn);
       if (n < NINC5) S.inc[q][n] = x;
       else ov_g[S.doff[q] + n] = x;
       S.dv[q].w = n + 1;
@@ -537,8 +518,8 @@ __global__ void __launch_bounds__(64, COST5_MINB) k_cost5(Cost5Graph G, TopoArgs
     auto stage = [&](int k, int sl, const int4 &r) {   // lane j copies out-edge slot j and its device byte
       const int no = min(r.w & 0xffff, SO5);
       if (lane < no) {
-        const int e = r.z + lane;
-        cp_32(&S.stage[k][sl][lane], G.slots + e);
+        const int e = rec_ob(r) + lane;
+        cp16(&S.stage[k][sl][lane], G.slots + e);
         cp_4(&S.sdev[k][sl][lane], sdev_g + e);
         spend |= 1u << (2 * k + sl);
       }
@@ -548,8 +529,8 @@ __global__ void __launch_bounds__(64, COST5_MINB) k_cost5(Cost5Graph G, TopoArgs
     __syncwarp();
     // sources are available at t = 0: appended to their FIFO in ascending id (uniform)
     for (int i = 0; i < G.nsrc; i++) {
-      const int4 r = reinterpret_cast<const int4 *>(G.srcq + i)[0];   // id, cost, ob, nn
-      const int q = D[r.x];
+      const int4 r = reinterpret_cast<const int4 *>(G.srcq)[i];   // packed record
+      const int q = D[rec_id(r)];
       const int f = S.dv[q].z;
       if (f < KF5) S.fc[q][f] = r;
       else fifo_g[S.doff[q] + f] = r;
@@ -586,8 +567,7 @@ __global__ void __launch_bounds__(64, COST5_MINB) k_cost5(Cost5Graph G, TopoArgs
             hph ^= cb;
             hpn &= ~cb;
           }
-          Q5 r;
-          load_q5(r, &S.chd[c]);   // queue fields (arr / u are not used: the slot's bytes)
+          const int4 r = S.chd[c];   // the consumer's packed record
           const int e = S.cq[c][s].x;
           S.ch[c].z = h + 1;
           if (h + KC5 < tail) S.cq[c][s] = chq_g[S.coff[c] + h + KC5];   // from the global overflow (rare)
@@ -601,7 +581,7 @@ __global__ void __launch_bounds__(64, COST5_MINB) k_cost5(Cost5Graph G, TopoArgs
             S.ca[c] = INF;
           }
           item(IT_ALLOC_COPY, q, e);   // the memory warp reads the copy's bytes from slot e
-          if (arrive_u(r.cinfo)) to_inc(q, r);
+          if (arrive_u(rec_cinfo(r))) to_inc(q, r);
         }
         P5(1);
         // ---------------------------------------------------------- (2) ops finishing now, ascending id
@@ -617,7 +597,7 @@ __global__ void __launch_bounds__(64, COST5_MINB) k_cost5(Cost5Graph G, TopoArgs
             }
           }
           ef &= ~(1u << k);
-          Q5 r;   // id, ob, nn
+          Q5 r;   // id, ob, nn (unpacked at the dispatch)
           {
             const int4 rr = S.drun[k];
             r.id = rr.x; r.ob = rr.y; r.nn = rr.z;
@@ -632,31 +612,30 @@ __global__ void __launch_bounds__(64, COST5_MINB) k_cost5(Cost5Graph G, TopoArgs
           for (int j0 = 0; j0 < nout; j0 += 32) {   // out-edges, one per lane
             const int j = j0 + lane;
             const bool valid = j < nout;
-            Slot5 e;
+            int4 e = make_int4(0, 0, 0, 0);   // the consumer's packed record
             int tw = k;
             unsigned sw = 0;
             if (valid) {
               if (j < SO5) {
                 if (spend & (1u << (2 * k + sl))) { cp_wait0(); spend = 0; }
-                load_slot5(e, &S.stage[k][sl][j]);
+                e = S.stage[k][sl][j];
                 sw = S.sdev[k][sl][j];
               } else {
-                load_slot5(e, G.slots + r.ob + j);
+                e = reinterpret_cast<const int4 *>(G.slots)[r.ob + j];
                 sw = sdev_g[r.ob + j];
               }
               tw = (int)(sw & 7u);
             }
             const bool same = valid && tw == k, cross = valid && tw != k;
-            const bool av = same && arrive5(flag_s, bigb_s, gbig, e.cinfo);
+            const bool av = same && arrive5(flag_s, bigb_s, gbig, rec_cinfo(e));
             const unsigned am = __ballot_sync(FULL, av);
             const unsigned cm = __ballot_sync(FULL, cross);
             if (am) {   // ops made available now on device k, in lane (= id) order
               const int n0 = S.dv[k].w;
               if (av) {
                 const int pos = n0 + __popc(am & lt);
-                const int4 x = make_int4(e.w, e.cost, e.ob, e.nn);
-                if (pos < NINC5) S.inc[k][pos] = x;
-                else ov_g[S.doff[k] + pos] = x;
+                if (pos < NINC5) S.inc[k][pos] = e;
+                else ov_g[S.doff[k] + pos] = e;
               }
               __syncwarp();
               S.dv[k].w = n0 + __popc(am);
@@ -675,7 +654,7 @@ __global__ void __launch_bounds__(64, COST5_MINB) k_cost5(Cost5Graph G, TopoArgs
                 const int2 ce = make_int2(r.ob + j, arr);
                 if (pos < hd + KC5) S.cq[c][pos & (KC5 - 1)] = ce;
                 else chq_g[S.coff[c] + pos] = ce;
-                if (pos == hd) store_q5(&S.chd[c], q_of_slot(e, arr, r.id));   // an empty channel's new head
+                if (pos == hd) S.chd[c] = e;   // an empty channel's new head
                 if (rank == 0) {
                   *reinterpret_cast<int2 *>(&S.ch[c]) = make_int2(tail + n, bt + n * x);   // tail, free
                   if (tail == hd) S.ca[c] = bt + x;   // the channel was empty: a new head
@@ -708,7 +687,7 @@ __global__ void __launch_bounds__(64, COST5_MINB) k_cost5(Cost5Graph G, TopoArgs
         const int n = dvk.w;
         bool running = dvk.x != INF, go = false;
         int fh = dvk.y, ft = dvk.z;
-        int4 run;   // id, cost, ob, nn
+        int4 run;   // packed record
         if (n > 0) {
           S.dv[k].w = 0;
           int4 *Li = &S.inc[k][0];
@@ -722,7 +701,7 @@ __global__ void __launch_bounds__(64, COST5_MINB) k_cost5(Cost5Graph G, TopoArgs
               int j = i - 1;
               while (j >= 0) {
                 const int4 pj = j < NINC5 ? Li[j] : Lo[j];
-                if (pj.x <= key.x) break;
+                if ((pj.x & M25) <= (key.x & M25)) break;
                 (j + 1 < NINC5 ? Li[j + 1] : Lo[j + 1]) = pj;
                 j--;
               }
@@ -751,8 +730,8 @@ __global__ void __launch_bounds__(64, COST5_MINB) k_cost5(Cost5Graph G, TopoArgs
           S.dv[k].x = fin;
           if (lane == k) dfr = fin;
           dmin = min(dmin, fin);
-          S.drun[k] = make_int4(run.x, run.z, run.w, 0);
-          item(IT_ALLOC_OP, k, run.x);
+          S.drun[k] = make_int4(rec_id(run), rec_ob(run), run.w, 0);
+          item(IT_ALLOC_OP, k, rec_id(run));
           cur ^= 1;   // the slot the head was staged into, or the one it is staged into now
           if (run.x != nxt && (run.w & 0xffff)) stage(k, cur, run);
           nxt = -1;
@@ -761,7 +740,7 @@ __global__ void __launch_bounds__(64, COST5_MINB) k_cost5(Cost5Graph G, TopoArgs
         P5(5);
         if (running && fh < ft && nxt < 0) {   // stage the op now waiting at the head
           const int4 hr = S.fc[k][fh & (KF5 - 1)];
-          nxt = hr.x;
+          nxt = hr.x;   // packed: compared with run.x
           if (hr.w & 0xffff) stage(k, cur ^ 1, hr);
         }
         *reinterpret_cast<int2 *>(&S.dv2[k]) = make_int2(cur, nxt);
@@ -872,7 +851,7 @@ __global__ void __launch_bounds__(64, COST5_MINB) k_cost5(Cost5Graph G, TopoArgs
         int du = 0;
         if (vmine) {
           if (kind == IT_ALLOC_OP) { dA = dev; xA = G.out_bytes[idx]; }
-          else if (kind == IT_ALLOC_COPY) { dA = dev; xA = G.slots[idx].bytes; }   // idx = the copy's out-edge slot
+          else if (kind == IT_ALLOC_COPY) { dA = dev; xA = G.ebytes[idx]; }   // idx = the copy's out-edge slot
           else if (kind == IT_SINK) { dA = dev; xA = -G.out_bytes[idx]; }
           else if (kind == IT_INEDGE) {
             const IRec ir = G.irec[idx];
@@ -1037,16 +1016,14 @@ gdp_status cost5_build(int N, long long E, const int *optr, const int *oidx, con
     else if (din == 2) r.cinfo = 1 | (nf++ << 2);
     else if (din <= 15) { r.cinfo = 2 | (nb << 2); nibs.push_back((unsigned char)din); nb++; }
     else { r.cinfo = 3 | ((int)h->gbig.size() << 2); h->gbig.push_back(din); }
-    if (din == 0) h->srcq.push_back(r);
+    if (din == 0) h->srcq.push_back(pack_slot5(r.id, r.cost, r.ob, dout, r.cinfo));
     h->outdeg[v] = dout;
   }
   for (int v = 0; v < N; v++)
     for (int e = optr[v]; e < optr[v + 1]; e++) {
       const Q5 &w = q[oidx[e]];
-      Slot5 &s = h->slots[(size_t)e];
-      s.w = w.id; s.cost = w.cost; s.ob = w.ob; s.nn = w.nn; s.cinfo = w.cinfo; s.ib = w.ib;
-      s.bytes = out_bytes[v];   // the producer's output: the size of the copy on this edge
-      h->ebytes[(size_t)e] = out_bytes[v];
+      h->slots[(size_t)e] = pack_slot5(w.id, w.cost, w.ob, w.nn & 0xffff, w.cinfo);
+      h->ebytes[(size_t)e] = out_bytes[v];   // the producer's output: the size of the copy on this edge
     }
   h->nflagw = (nf + 31) / 32;
   while (nibs.size() % 32) nibs.push_back(0);
