@@ -50,7 +50,7 @@ using namespace cu;
 
 constexpr int KC5 = 4;      // channel entries kept in shared memory per channel (power of 2)
 #ifndef COST5_KF
-#define COST5_KF 4
+#define COST5_KF 2
 #endif
 #ifndef COST5_SO
 #define COST5_SO 5
@@ -62,7 +62,7 @@ constexpr int KF5 = COST5_KF;       // FIFO entries kept in shared memory per de
 constexpr int SO5 = COST5_SO;       // staged out-edge records per slot (more: read from global at the finish)
 constexpr int NINC5 = COST5_NINC;   // ops made available at one instant kept in shared memory per device
 #ifndef COST5_RI
-#define COST5_RI 128
+#define COST5_RI 64
 #endif
 #ifndef COST5_MB
 #define COST5_MB 32
@@ -130,10 +130,9 @@ struct Smem5 {
   unsigned long long ibar;          // mbarrier: one phase per 32 items appended (and one at the end)
   int4 drun[8];                     // the op running on each device: id, ob, nn -- what its finish
                                     // reads (one 16-byte load / store instead of a 32-byte Q5: -1.7 %)
-  int4 ch[NCH];                     // per channel: tail, free (transfer end), head
+  int4 ch[NCH];                     // per channel: tail, free (transfer end), head, overflow offset
   int ca[NCH];                      // arrival tick of each channel's head entry (INF: empty; contiguous: the
                                     // next-event REDUX reads two per lane without bank conflicts)
-  int coff[NCH];
   int4 dv[8];                       // per device: finish of the running op (INF: idle), FIFO head, tail, #available now
   int4 dv2[8];                      // per device: staging slot of the running op, op staged in the other, speed
   int doff[8];
@@ -382,7 +381,7 @@ __global__ void __launch_bounds__(512) k_cost5_pre(Cost5Graph G, TopoArgs T, con
 // warps; so successive CTAs on the same (SM, sub-partition pair) alternate the simulating warp.
 __device__ unsigned g_c5_pair[2 * 1024];
 #ifndef COST5_MINB
-#define COST5_MINB 14
+#define COST5_MINB 15
 #endif
 __global__ void __launch_bounds__(64, COST5_MINB) k_cost5(Cost5Graph G, TopoArgs T, const uint8_t *__restrict__ Dall,
                                               unsigned char *scratch, size_t per_place, gdp_sim_report *rep,
@@ -416,7 +415,6 @@ __global__ void __launch_bounds__(64, COST5_MINB) k_cost5(Cost5Graph G, TopoArgs
     for (int i = tid; i < G.nbigb; i += 64) bigb[i] = G.bigb0[i];
     for (int i = tid; i < RI5; i += 64) S.items[i] = 1ull << 32;   // lap parity 1: empty for lap 0
     if (tid < NCH) {
-      S.ch[tid] = make_int4(0, 0, 0, 0);
       S.ca[tid] = INF;
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((unsigned)__cvta_generic_to_shared(&S.hbar[tid])));
     }
@@ -438,7 +436,7 @@ __global__ void __launch_bounds__(64, COST5_MINB) k_cost5(Cost5Graph G, TopoArgs
       o = 0;
       for (int a = 0; a < 8; a++)
         for (int b2 = 0; b2 < 8; b2++)
-          if (a != b2) { S.coff[cidx(a, b2)] = o; o += pre->chcnt[8 * a + b2]; }
+          if (a != b2) { S.ch[cidx(a, b2)] = make_int4(0, 0, 0, o); o += pre->chcnt[8 * a + b2]; }
     }
   }
   const int pflag = pre->flag;
@@ -570,7 +568,7 @@ __global__ void __launch_bounds__(64, COST5_MINB) k_cost5(Cost5Graph G, TopoArgs
           const int4 r = S.chd[c];   // the consumer's packed record
           const int e = S.cq[c][s].x;
           S.ch[c].z = h + 1;
-          if (h + KC5 < tail) S.cq[c][s] = chq_g[S.coff[c] + h + KC5];   // from the global overflow (rare)
+          if (h + KC5 < tail) S.cq[c][s] = chq_g[cs.w + h + KC5];   // from the global overflow (rare)
           if (h + 1 < tail) {   // a new head: its arrival, and its record from the out-edge slot
             const int2 nx = S.cq[c][(h + 1) & (KC5 - 1)];
             S.ca[c] = nx.y;
@@ -653,7 +651,7 @@ __global__ void __launch_bounds__(64, COST5_MINB) k_cost5(Cost5Graph G, TopoArgs
                 const int pos = tail + rank, arr = bt + (rank + 1) * x;
                 const int2 ce = make_int2(r.ob + j, arr);
                 if (pos < hd + KC5) S.cq[c][pos & (KC5 - 1)] = ce;
-                else chq_g[S.coff[c] + pos] = ce;
+                else chq_g[cs.w + pos] = ce;
                 if (pos == hd) S.chd[c] = e;   // an empty channel's new head
                 if (rank == 0) {
                   *reinterpret_cast<int2 *>(&S.ch[c]) = make_int2(tail + n, bt + n * x);   // tail, free
