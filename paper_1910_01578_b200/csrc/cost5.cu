@@ -71,6 +71,9 @@ constexpr int NINC5 = COST5_NINC;   // ops made available at one instant kept in
 #define COST5_MBAR 0   // 1: the memory warp sleeps on an mbarrier the simulation warp arrives on per 32 items
                        // (measured 162.8 ms vs 142.3 ms polling at C4 B = 1776: kept off)
 #endif
+#ifndef COST5_TRI
+#define COST5_TRI 1   // three-input ops count in 2-bit fields (4-bit fields for 4..15 inputs)
+#endif
 #ifndef COST5_SLEEP
 #define COST5_SLEEP 3000
 #endif
@@ -219,9 +222,19 @@ __device__ __forceinline__ unsigned atoms_add(unsigned a, unsigned x) {
 }
 // an input of op (cinfo) arrived now: true iff it was the last one (the op becomes available now)
 __device__ __forceinline__ bool arrive5(unsigned flag_s, unsigned bigb_s, int *gbig, int cinfo) {
+#if COST5_TRI
+  if (cinfo == 0) return true;
+  const int kind = cinfo & 3;
+  const int ix = cinfo >> 2;
+  if (kind == 0) {   // three inputs: a 2-bit count (from 3) at field ix - 1 of the counter words
+    const int p = ix - 1, sh = (p & 15) * 2;
+    return ((atoms_add(bigb_s + 4u * (unsigned)(p >> 4), 0u - (1u << sh)) >> sh) & 3u) == 1u;
+  }
+#else
   const int kind = cinfo & 3;
   if (kind == 0) return true;
   const int ix = cinfo >> 2;
+#endif
   if (kind == 1) {
     const unsigned bit = 1u << (ix & 31);
     return (atoms_xor(flag_s + 4u * (unsigned)(ix >> 5), bit) & bit) != 0u;
@@ -381,7 +394,7 @@ __global__ void __launch_bounds__(512) k_cost5_pre(Cost5Graph G, TopoArgs T, con
 // warps; so successive CTAs on the same (SM, sub-partition pair) alternate the simulating warp.
 __device__ unsigned g_c5_pair[2 * 1024];
 #ifndef COST5_MINB
-#define COST5_MINB 15
+#define COST5_MINB 16
 #endif
 __global__ void __launch_bounds__(64, COST5_MINB) k_cost5(Cost5Graph G, TopoArgs T, const uint8_t *__restrict__ Dall,
                                               unsigned char *scratch, size_t per_place, gdp_sim_report *rep,
@@ -495,9 +508,21 @@ __global__ void __launch_bounds__(64, COST5_MINB) k_cost5(Cost5Graph G, TopoArgs
     };
     // uniform input arrival (no other lane touches the counters concurrently)
     auto arrive_u = [&](int cinfo) -> bool {
+#if COST5_TRI
+      if (cinfo == 0) return true;
+      const int kind = cinfo & 3;
+      const int ix = cinfo >> 2;
+      if (kind == 0) {
+        const int p = ix - 1, sh = (p & 15) * 2;
+        const unsigned w = bigb[p >> 4];
+        bigb[p >> 4] = w - (1u << sh);
+        return ((w >> sh) & 3u) == 1u;
+      }
+#else
       const int kind = cinfo & 3;
       if (kind == 0) return true;
       const int ix = cinfo >> 2;
+#endif
       if (kind == 1) {
         const unsigned bit = 1u << (ix & 31), w = flags[ix >> 5];
         flags[ix >> 5] = w ^ bit;
@@ -1004,6 +1029,7 @@ gdp_status cost5_build(int N, long long E, const int *optr, const int *oidx, con
   std::vector<Q5> q(N);
   int nb = 0, nf = 0;
   std::vector<unsigned char> nibs;
+  std::vector<int> tri;   // three-input ops (COST5_TRI): 2-bit counts after the 4-bit ones
   for (int v = 0; v < N; v++) {
     const int din = iptr[v + 1] - iptr[v], dout = optr[v + 1] - optr[v];
     if (din >= 65536 || dout >= 65536) h->ok = false;
@@ -1012,11 +1038,16 @@ gdp_status cost5_build(int N, long long E, const int *optr, const int *oidx, con
     r.nn = (dout & 0xffff) | ((din & 0xffff) << 16);
     if (din <= 1) r.cinfo = 0;
     else if (din == 2) r.cinfo = 1 | (nf++ << 2);
+    else if (COST5_TRI && din == 3) { r.cinfo = 0; tri.push_back(v); }   // encoded below
     else if (din <= 15) { r.cinfo = 2 | (nb << 2); nibs.push_back((unsigned char)din); nb++; }
     else { r.cinfo = 3 | ((int)h->gbig.size() << 2); h->gbig.push_back(din); }
     if (din == 0) h->srcq.push_back(pack_slot5(r.id, r.cost, r.ob, dout, r.cinfo));
     h->outdeg[v] = dout;
   }
+  while (nibs.size() % 32) nibs.push_back(0);
+  const int nibw = (int)(nibs.size() / 8);
+  for (size_t i = 0; i < tri.size(); i++)   // kind 0 with index 1 + (2-bit field position in the counter words)
+    q[tri[i]].cinfo = (int)((1 + (size_t)nibw * 16 + i) << 2);
   for (int v = 0; v < N; v++)
     for (int e = optr[v]; e < optr[v + 1]; e++) {
       const Q5 &w = q[oidx[e]];
@@ -1024,8 +1055,8 @@ gdp_status cost5_build(int N, long long E, const int *optr, const int *oidx, con
       h->ebytes[(size_t)e] = out_bytes[v];   // the producer's output: the size of the copy on this edge
     }
   h->nflagw = (nf + 31) / 32;
-  while (nibs.size() % 32) nibs.push_back(0);
-  h->bigb.assign(nibs.size() / 8, 0u);
+  h->bigb.assign((size_t)nibw + (tri.size() + 15) / 16, 0xffffffffu);   // 2-bit fields start at 3
+  for (int i = 0; i < nibw; i++) h->bigb[(size_t)i] = 0u;
   for (size_t i = 0; i < nibs.size(); i++) h->bigb[i / 8] |= (unsigned)nibs[i] << (4 * (i % 8));
   return GDP_OK;
 }

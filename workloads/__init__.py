@@ -511,14 +511,14 @@ def config(name: str, batch: Optional[int] = None, mem_len: Optional[int] = None
         w = Workload("c3_txl20k_wavenet20k_d8", [transformer_xl(seed=1003), wavenet(seed=1004)],
                      d=8, seg_len=128, mem_len=128, batch=64)
     elif name == "c4":
-        # B = 2220 = 148 SMs x 15 resident k_cost5 CTAs: one full wave of the cost kernel (one CTA
-        # per placement, 14.1 KB of shared memory and 64 registers x 64 threads each at N = 52 k;
+        # B = 2368 = 148 SMs x 16 resident k_cost5 CTAs: one full wave of the cost kernel (one CTA
+        # per placement, 13.2 KB of shared memory and 64 registers x 64 threads each at N = 52 k;
         # gdp_cost_wave)
-        w = Workload("c4_gnmt52k_d8", [gnmt(seed=1005)], d=8, seg_len=128, mem_len=128, batch=2220)
+        w = Workload("c4_gnmt52k_d8", [gnmt(seed=1005)], d=8, seg_len=128, mem_len=128, batch=2368)
     elif name == "c4_64k":
         # PAPER.md:181 "over 60k nodes": the same GNMT shape unrolled over 148 steps (64 274 ops);
-        # its cost-kernel state still fits thirteen CTAs per SM: B = 1924 = one wave (gdp_cost_wave)
-        w = Workload("c4_gnmt64k_d8", [gnmt(steps=148, seed=1005)], d=8, seg_len=128, mem_len=128, batch=1924)
+        # its cost-kernel state still fits fourteen CTAs per SM: B = 2072 = one wave (gdp_cost_wave)
+        w = Workload("c4_gnmt64k_d8", [gnmt(steps=148, seed=1005)], d=8, seg_len=128, mem_len=128, batch=2072)
     elif name == "c5":
         gs = []
         for i, s in enumerate([1011, 1015]):
