@@ -525,6 +525,36 @@ def test_cost_overflow_paths(gdp):
         assert_cost_equal(g, t, D, cost_gpu(gdp, g, t, D))
 
 
+def test_cost_counter_kinds_and_wide_frees(gdp):
+    """k_cost5's input-counter kinds side by side (one input: none; two: a flag bit; three: a 2-bit
+    field, 16 per word; 4..15: a 4-bit field; 16+: a global counter) and finishes whose frees the
+    memory warp expands over several 32-wide rounds (in-degrees 40 and 100), sinks among them;
+    bit-exact against the oracle on 1, 3 and 8 devices, with kernel 5 checked to be the one run."""
+    rng = np.random.default_rng(29)
+    n_src = 100
+    edges, nxt = [], n_src
+    kinds = []
+    for din in [1] * 20 + [2] * 40 + [3] * 70 + [5] * 20 + [15] * 4 + [16] * 3 + [40, 100]:
+        for s in rng.choice(n_src, size=din, replace=False):
+            edges.append((int(s), nxt))
+        kinds.append(nxt)
+        nxt += 1
+    # a second layer so that the 3-input ops also feed later ops (their counters reset per placement)
+    for m in range(60):
+        for s in rng.choice(kinds, size=3, replace=False):
+            edges.append((int(s), nxt))
+        nxt += 1
+    N = nxt
+    cost = rng.integers(1, 7, size=N)
+    g = mkgraph(N, edges, cost, out=rng.integers(0, 3000, size=N), mem=rng.integers(0, 200, size=N))
+    for d in (1, 3, 8):
+        t = mktopo(d, bw=500, lat=2, cap=10 ** 9)
+        assert gdp.cost_kernel(gdp.Graph(g, workloads.features(g)), gdp.Topo(t)) == 5
+        D = rng.integers(0, d, size=(12, N)).astype(np.uint8)
+        D[0] = 0
+        assert_cost_equal(g, t, D, cost_gpu(gdp, g, t, D))
+
+
 @pytest.mark.parametrize("d", [1, 2])
 def test_cost_full_size_c4_few_devices(gdp, d):
     g = workloads.config("c4").graphs[0]
