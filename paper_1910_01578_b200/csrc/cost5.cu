@@ -826,6 +826,13 @@ __global__ void __launch_bounds__(64, COST5_MINB) k_cost5(Cost5Graph G, TopoArgs
         }
       }
       nwait = 0;
+#ifdef COST5_NOMEM   // experiment: consume the items without the accounting (peaks wrong)
+      done = __any_sync(FULL, lane < n && kind_end(it));
+      mh += n;
+      __syncwarp();
+      if (lane == 0) asm volatile("st.release.cta.shared::cta.b32 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(&S.mhead)), "r"(mh) : "memory");
+      continue;
+#endif
 #ifdef COST5_PROF
       nbatch++;
       nitems += n;
@@ -895,15 +902,30 @@ __global__ void __launch_bounds__(64, COST5_MINB) k_cost5(Cost5Graph G, TopoArgs
           old = __shfl_sync(FULL, old, leader);
           if (u >= 0 && lane == last && old == cnt2) { dB = du; xB = -bu; }
         }
-        // apply in item order; sample the peak whenever the instant changes
-        const int nv = min(32, total - w0);
-        for (int i = 0; i < nv; i++) {
+        // apply in item order; sample the peak whenever the instant changes.  Each device lane
+        // walks only its own contributions of the round, in item order, and samples its peak when
+        // the instant changes between them: exact, since a device's bytes only change at its own
+        // contributions (an instant boundary between two of them sees the value the earlier
+        // sample already took).  Walking all 32 items on every lane instead (7 shuffles each)
+        // measured 3.6 % slower on the whole kernel: the memory warps' issue slots and shuffles
+        // compete with the simulation warps at sixteen placements per SM.
+        unsigned myA = 0u, myB = 0u;
+#pragma unroll
+        for (int k = 0; k < 8; k++) {
+          const unsigned ma = __ballot_sync(FULL, dA == k), mb = __ballot_sync(FULL, dB == k);
+          if (lane == k) { myA = ma; myB = mb; }
+        }
+        unsigned my = myA | myB;
+        const int iters = (int)__reduce_max_sync(FULL, (unsigned)__popc(my));
+        for (int r2 = 0; r2 < iters; r2++) {
+          const int i = my ? __ffs(my) - 1 : 0;
           const int tI = __shfl_sync(FULL, ti, i);
-          const int aD = __shfl_sync(FULL, dA, i), bD = __shfl_sync(FULL, dB, i);
           const long long aX = __shfl_sync(FULL, xA, i), bX = __shfl_sync(FULL, xB, i);
-          if (tI != last_t) { pk = max(pk, mem); last_t = tI; }
-          if (aD == lane) mem += aX;
-          if (bD == lane) mem += bX;
+          if (my) {
+            if (tI != last_t) { pk = max(pk, mem); last_t = tI; }
+            mem += (((myA >> i) & 1u) ? aX : 0ll) + (((myB >> i) & 1u) ? bX : 0ll);
+            my &= my - 1;
+          }
         }
       }
       mh += n;
