@@ -860,6 +860,9 @@ __global__ void __launch_bounds__(64, COST5_MINB) k_cost5(Cost5Graph G, TopoArgs
         if (lane >= o) iend += y;
       }
       const int total = __shfl_sync(FULL, iend, 31);
+      // per item, what an expanded position needs: kind | device << 3 | sink << 6, and for a
+      // finish the in-edge index of position 0 (in-edge slot = base + position)
+      const int code0 = kind0 | (dev0 << 3) | (sink << 6), base0 = ib0 - (iend - cnt);
       for (int w0 = 0; w0 < total; w0 += 32) {
         const int w = w0 + lane;
         int src = 0;   // the item covering position w: the number of items whose range ends at or before w
@@ -869,13 +872,13 @@ __global__ void __launch_bounds__(64, COST5_MINB) k_cost5(Cost5Graph G, TopoArgs
           if (e <= w) src += step;
         }
         const bool vmine = w < total;
-        const int ti = __shfl_sync(FULL, ti0, src), kind_s = __shfl_sync(FULL, kind0, src);
-        const int dev = __shfl_sync(FULL, dev0, src), idx_s = __shfl_sync(FULL, idx0, src);
-        const int sbeg = __shfl_sync(FULL, iend - cnt, src), sib = __shfl_sync(FULL, ib0, src);
-        const int ssink = __shfl_sync(FULL, sink, src), send = __shfl_sync(FULL, iend, src);
-        const bool fsink = kind_s == IT_FIN && ssink && w == send - 1;   // the last position of a sink's FIN
+        const int ti = __shfl_sync(FULL, ti0, src), code = __shfl_sync(FULL, code0, src);
+        const int base = __shfl_sync(FULL, base0, src), idx_s = __shfl_sync(FULL, idx0, src);
+        const int send = __shfl_sync(FULL, iend, src);
+        const int kind_s = code & 7, dev = (code >> 3) & 7;
+        const bool fsink = kind_s == IT_FIN && (code >> 6) && w == send - 1;   // the last position of a sink's FIN
         const int kind = kind_s == IT_FIN ? (fsink ? IT_SINK : IT_INEDGE) : kind_s;
-        const int idx = kind_s == IT_FIN ? (fsink ? idx_s : sib + (w - sbeg)) : idx_s;
+        const int idx = kind_s == IT_FIN ? (fsink ? idx_s : base + w) : idx_s;
         int dA = -1, dB = -1, u = -1;
         long long xA = 0, xB = 0, bu = 0;
         int du = 0;
