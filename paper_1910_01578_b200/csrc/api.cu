@@ -572,6 +572,7 @@ gdp_status gdp_graph_create(int32_t N, int32_t F, const float *feat, int64_t E, 
     g->nbigb5 = (int)h5.bigb.size();
     g->ngbig5 = (int)h5.gbig.size();
     g->nflagw5 = h5.nflagw;
+    g->bytes32_5 = h5.bytes32 ? 1 : 0;
     UP(slots5, h5.slots.data(), h5.slots.size() * sizeof(Slot5));
     UP(ebytes5, h5.ebytes.data(), h5.ebytes.size() * sizeof(long long));
     UP(srcq5, h5.srcq.data(), h5.srcq.size() * sizeof(Slot5));

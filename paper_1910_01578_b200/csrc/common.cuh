@@ -72,7 +72,7 @@ struct gdp_graph_s {
   void *slots5 = nullptr, *srcq5 = nullptr, *ebytes5 = nullptr;
   int *gbig5 = nullptr, *outdeg5 = nullptr;
   unsigned *bigb5 = nullptr;
-  int nsrc5 = 0, nbigb5 = 0, ngbig5 = 0, nflagw5 = 0;
+  int nsrc5 = 0, nbigb5 = 0, ngbig5 = 0, nflagw5 = 0, bytes32_5 = 0;
 };
 
 struct gdp_topo_s {

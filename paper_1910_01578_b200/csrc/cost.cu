@@ -445,6 +445,7 @@ static Cost5Graph cost5_graph(const gdp_graph_s *g) {
   C.outdeg = g->outdeg5; C.gbig0 = g->gbig5; C.bigb0 = g->bigb5;
   C.out_bytes = g->out_bytes; C.mem_bytes = g->mem_bytes;
   C.nsrc = g->nsrc5; C.nbigb = g->nbigb5; C.ngbig = g->ngbig5; C.nflagw = g->nflagw5;
+  C.bytes32 = g->bytes32_5;
   C.has_coloc = g->has_coloc ? 1 : 0;
   return C;
 }

@@ -61,6 +61,7 @@ __host__ __device__ __forceinline__ Slot5 pack_slot5(int id, int cost, int ob, i
 }
 struct Cost5Host {            // host images built at graph creation (cost5_build)
   bool ok = false;
+  bool bytes32 = false;        // every output < 2^31 bytes: the memory warp applies 32-bit deltas
   std::vector<Slot5> slots;
   std::vector<long long> ebytes;   // per out-edge slot: the producer's output bytes (k_cost5_pre, contiguous)
   std::vector<Slot5> srcq;     // the sources, ascending id
@@ -81,6 +82,7 @@ struct Cost5Graph {
   const unsigned *bigb0;
   const long long *out_bytes, *mem_bytes;
   int nsrc, nbigb, ngbig, nflagw, has_coloc;
+  int bytes32;                 // Cost5Host::bytes32
 };
 gdp_status cost5_build(int N, long long E, const int *optr, const int *oidx, const int *iptr, const int *cost,
                        const long long *out_bytes, Cost5Host *h);

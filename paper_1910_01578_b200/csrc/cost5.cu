@@ -396,6 +396,9 @@ __device__ unsigned g_c5_pair[2 * 1024];
 #ifndef COST5_MINB
 #define COST5_MINB 16
 #endif
+// B32: every output < 2^31 bytes (Cost5Graph::bytes32), so the memory warp broadcasts 32-bit
+// deltas; a template parameter rather than a branch, which costs registers in the shared budget
+template <bool B32>
 __global__ void __launch_bounds__(64, COST5_MINB) k_cost5(Cost5Graph G, TopoArgs T, const uint8_t *__restrict__ Dall,
                                               unsigned char *scratch, size_t per_place, gdp_sim_report *rep,
                                               long long *peak_out, long long *busy_out, double *reward) {
@@ -923,11 +926,20 @@ __global__ void __launch_bounds__(64, COST5_MINB) k_cost5(Cost5Graph G, TopoArgs
         for (int r2 = 0; r2 < iters; r2++) {
           const int i = my ? __ffs(my) - 1 : 0;
           const int tI = __shfl_sync(FULL, ti, i);
-          const long long aX = __shfl_sync(FULL, xA, i), bX = __shfl_sync(FULL, xB, i);
-          if (my) {
-            if (tI != last_t) { pk = max(pk, mem); last_t = tI; }
-            mem += (((myA >> i) & 1u) ? aX : 0ll) + (((myB >> i) & 1u) ? bX : 0ll);
-            my &= my - 1;
+          if (B32) {   // every delta is one output's bytes, < 2^31: one 32-bit broadcast each
+            const int aX = __shfl_sync(FULL, (int)xA, i), bX = __shfl_sync(FULL, (int)xB, i);
+            if (my) {
+              if (tI != last_t) { pk = max(pk, mem); last_t = tI; }
+              mem += ((myA >> i) & 1u) ? aX : bX;   // an item's two deltas go to different devices
+              my &= my - 1;
+            }
+          } else {
+            const long long aX = __shfl_sync(FULL, xA, i), bX = __shfl_sync(FULL, xB, i);
+            if (my) {
+              if (tI != last_t) { pk = max(pk, mem); last_t = tI; }
+              mem += (((myA >> i) & 1u) ? aX : 0ll) + (((myB >> i) & 1u) ? bX : 0ll);
+              my &= my - 1;
+            }
           }
         }
       }
@@ -1001,11 +1013,12 @@ bool cost5_eligible(const TopoArgs &T, const Cost5Graph &G, int min_cost, long l
 int cost5_wave(const Cost5Graph &G) {
   const size_t smem = cost5_smem_bytes(G.nflagw, G.nbigb);
   if (sizeof(Smem5) + smem > 227 * 1024) return 0;
-  cudaFuncSetAttribute(k_cost5, cudaFuncAttributePreferredSharedMemoryCarveout, 100);   // all of it shared
+  const void *fn = G.bytes32 ? (const void *)k_cost5<true> : (const void *)k_cost5<false>;
+  cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);   // all of it shared
   if (smem + sizeof(Smem5) > 48 * 1024)
-    cudaFuncSetAttribute(k_cost5, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int occ = 0, dev = 0, nsm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_cost5, 64, smem) != cudaSuccess) return 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, 64, smem) != cudaSuccess) return 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   return occ * nsm;
@@ -1017,15 +1030,17 @@ bool launch_cost5(const Cost5Graph &G, const TopoArgs &T, int min_cost, long lon
   if (!cost5_eligible(T, G, min_cost, min_edge_bytes)) return false;
   if (per_place < cost5_scratch_per_placement(G.N, G.E, G.ngbig)) return false;
   const size_t smem = cost5_smem_bytes(G.nflagw, G.nbigb);
-  static size_t configured = 0;
-  static bool carve = false;
-  if (!carve) {
-    cudaFuncSetAttribute(k_cost5, cudaFuncAttributePreferredSharedMemoryCarveout, 100);   // all of it shared
-    carve = true;
+  static size_t configured[2] = {0, 0};
+  static bool carve[2] = {false, false};
+  const int b32 = G.bytes32 ? 1 : 0;
+  const void *fn = b32 ? (const void *)k_cost5<true> : (const void *)k_cost5<false>;
+  if (!carve[b32]) {
+    cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);   // all of it shared
+    carve[b32] = true;
   }
-  if (smem + sizeof(Smem5) > 48 * 1024 && smem > configured) {
-    cudaFuncSetAttribute(k_cost5, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    configured = smem;
+  if (smem + sizeof(Smem5) > 48 * 1024 && smem > configured[b32]) {
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    configured[b32] = smem;
   }
   // the pre-pass stages the placement row in shared memory when it fits (up to 160 KB)
   const int dsm = G.N <= 160 * 1024 ? (G.N + 15) / 16 * 16 : 0;
@@ -1037,7 +1052,8 @@ bool launch_cost5(const Cost5Graph &G, const TopoArgs &T, int min_cost, long lon
   note_launch("k_cost5_pre", s);
   k_cost5_pre<<<B, 512, dsm, s>>>(G, T, D, scratch, per_place, dsm);
   note_launch("k_cost5", s);
-  k_cost5<<<B, 64, smem, s>>>(G, T, D, scratch, per_place, rep, peak, busy, reward);
+  if (b32) k_cost5<true><<<B, 64, smem, s>>>(G, T, D, scratch, per_place, rep, peak, busy, reward);
+  else k_cost5<false><<<B, 64, smem, s>>>(G, T, D, scratch, per_place, rep, peak, busy, reward);
   return true;
 }
 
@@ -1080,6 +1096,9 @@ gdp_status cost5_build(int N, long long E, const int *optr, const int *oidx, con
       h->ebytes[(size_t)e] = out_bytes[v];   // the producer's output: the size of the copy on this edge
     }
   h->nflagw = (nf + 31) / 32;
+  h->bytes32 = true;
+  for (int v = 0; v < N; v++)
+    if (out_bytes[v] >= (1LL << 31)) h->bytes32 = false;
   h->bigb.assign((size_t)nibw + (tri.size() + 15) / 16, 0xffffffffu);   // 2-bit fields start at 3
   for (int i = 0; i < nibw; i++) h->bigb[(size_t)i] = 0u;
   for (size_t i = 0; i < nibs.size(); i++) h->bigb[i / 8] |= (unsigned)nibs[i] << (4 * (i % 8));

@@ -555,6 +555,20 @@ def test_cost_counter_kinds_and_wide_frees(gdp):
         assert_cost_equal(g, t, D, cost_gpu(gdp, g, t, D))
 
 
+def test_cost_large_outputs(gdp):
+    """Outputs of 2^31 bytes and more: the memory warp's 64-bit delta path (below that it
+    broadcasts 32-bit deltas), bit-exact peaks on 1, 2 and 4 devices."""
+    rng = np.random.default_rng(31)
+    g = workloads.random_dag(400, p_edge=0.05, max_back=40, seed=31, cost_max=9)
+    big = rng.random(g.N) < 0.1
+    g.output_bytes[big] = g.output_bytes[big] + (3 << 31)
+    for d in (1, 2, 4):
+        t = mktopo(d, bw=1 << 40, lat=1, cap=1 << 62)
+        assert gdp.cost_kernel(gdp.Graph(g, workloads.features(g)), gdp.Topo(t)) == 5
+        D = rng.integers(0, d, size=(8, g.N)).astype(np.uint8)
+        assert_cost_equal(g, t, D, cost_gpu(gdp, g, t, D))
+
+
 @pytest.mark.parametrize("d", [1, 2])
 def test_cost_full_size_c4_few_devices(gdp, d):
     g = workloads.config("c4").graphs[0]

@@ -5,10 +5,10 @@ mkdir -p gpurun_out/rows
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1
 timeout 1800 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu.log 2>&1; tail -4 gpurun_out/pytest_gpu.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; tail -2 gpurun_out/smoke.log
-timeout 900 ncu --set full --import-source on --clock-control none -k regex:'k_cost5$' -s 1 -c 1 -o gpurun_out/prof_cost \
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:'k_cost5(<|$)' -s 1 -c 1 -o gpurun_out/prof_cost \
     python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e --no-kernels > gpurun_out/prof_cost.log 2>&1
 python tools/ncu_to_json.py gpurun_out/prof_cost.ncu-rep profiles/cost_kernel_ncu.json k_cost5 c4_gnmt52k_d8 2368 \
-  "ncu --set full --import-source on --clock-control none -k regex:k_cost5$ -s 1 -c 1 python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e (tools/evidence.sh, round 2)" > gpurun_out/ncu_json.log 2>&1
+  "ncu --set full --import-source on --clock-control none -k regex:k_cost5(<|$) -s 1 -c 1 python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e (tools/evidence.sh, round 2)" > gpurun_out/ncu_json.log 2>&1
 cp profiles/cost_kernel_ncu.json gpurun_out/cost_kernel_ncu.json
 timeout 900 python bench.py > gpurun_out/bench_line.json 2> gpurun_out/bench_err.log; head -c 1200 gpurun_out/bench_line.json
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv \
