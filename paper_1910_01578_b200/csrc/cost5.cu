@@ -915,11 +915,16 @@ __global__ void __launch_bounds__(64, COST5_MINB) k_cost5(Cost5Graph G, TopoArgs
         // sample already took).  Walking all 32 items on every lane instead (7 shuffles each)
         // measured 3.6 % slower on the whole kernel: the memory warps' issue slots and shuffles
         // compete with the simulation warps at sixteen placements per SM.
-        unsigned myA = 0u, myB = 0u;
-#pragma unroll
-        for (int k = 0; k < 8; k++) {
-          const unsigned ma = __ballot_sync(FULL, dA == k), mb = __ballot_sync(FULL, dB == k);
-          if (lane == k) { myA = ma; myB = mb; }
+        // device masks from four ballots each (valid + the device's three bits)
+        unsigned myA, myB;
+        {
+          const unsigned va = __ballot_sync(FULL, dA >= 0), a0 = __ballot_sync(FULL, dA & 1),
+                         a1 = __ballot_sync(FULL, (dA >> 1) & 1), a2 = __ballot_sync(FULL, (dA >> 2) & 1);
+          const unsigned vb = __ballot_sync(FULL, dB >= 0), b0 = __ballot_sync(FULL, dB & 1),
+                         b1 = __ballot_sync(FULL, (dB >> 1) & 1), b2 = __ballot_sync(FULL, (dB >> 2) & 1);
+          const unsigned s0 = (lane & 1) ? 0u : ~0u, s1 = (lane & 2) ? 0u : ~0u, s2 = (lane & 4) ? 0u : ~0u;
+          myA = lane < 8 ? va & (a0 ^ s0) & (a1 ^ s1) & (a2 ^ s2) : 0u;
+          myB = lane < 8 ? vb & (b0 ^ s0) & (b1 ^ s1) & (b2 ^ s2) : 0u;
         }
         unsigned my = myA | myB;
         const int iters = (int)__reduce_max_sync(FULL, (unsigned)__popc(my));
