@@ -75,7 +75,7 @@ constexpr int NINC5 = COST5_NINC;   // ops made available at one instant kept in
 #define COST5_TRI 1   // three-input ops count in 2-bit fields (4-bit fields for 4..15 inputs)
 #endif
 #ifndef COST5_SLEEP
-#define COST5_SLEEP 3000
+#define COST5_SLEEP 4500
 #endif
 #ifndef COST5_SPIN
 #define COST5_SPIN 8
