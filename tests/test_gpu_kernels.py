@@ -214,6 +214,29 @@ def test_tensor_core_kernels_memory_lengths(gdp, S, M):
     run_kernel_checks(gdp, g, 4, S, M, 16)
 
 
+def test_tensor_core_mode_beyond_65535_segments(gdp):
+    """ADVICE r1: the tensor-core attention kernels put the segments on gridDim.y (<= 65 535);
+    with S = 1 on a 66 000-node graph the tensor-core step must take the SIMT attention kernels
+    (segments on gridDim.x, fp32 operands, not bf16): each layer's attention output on sampled
+    rows -- including segments past 65 535 -- against the oracle's plain segment attention
+    (oracle/model.py attention_heads over key_range) on the step's own Q, K, V."""
+    import oracle.model as Mo
+    g = workloads.random_dag(66000, p_edge=0.0005, max_back=8, seed=41)
+    N, S, M = g.N, 1, 1
+    th = workloads.init_theta(workloads.F, 2, seed=13, mode="random")
+    _, f, _, logits = tc_step(gdp, g, 2, S, M, 4, th)
+    assert np.isfinite(logits).all()
+    rows = np.unique(np.concatenate([np.arange(0, 40), np.arange(N - 40, N),
+                                     np.random.default_rng(0).integers(0, N, size=400)]))
+    for l in range(3):
+        qkv = torch.from_numpy(f[f"L{l}.qkv"].astype(np.float64))
+        ref = np.stack([Mo.attention_heads(qkv[i:i + 1, 0:64], qkv[lo:hi, 64:128], qkv[lo:hi, 128:192])[0].numpy()
+                        for i in rows for lo, hi in [Mo.key_range(int(i), N, S, M)]])
+        got = f[f"L{l}.o"][rows].astype(np.float64)
+        err = np.abs(got - ref) / (np.abs(ref) + 1e-3 * np.abs(ref).max())
+        assert err.max() < 1e-4, (l, float(err.max()))
+
+
 def test_tensor_core_kernels_full_size_c4(gdp):
     """C4 at full size (52 122 rows: 408 row tiles of the 192 / 256-wide maps for 296 CTA
     slots, so every persistent k_gemm_tc CTA runs several tiles), B = 8."""
