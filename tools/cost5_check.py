@@ -57,7 +57,7 @@ print("cost wave (placements at once):", gdp.cost_wave(G4, T4), flush=True)
 W64 = workloads.config("c4_64k"); g64 = W64.graphs[0]
 print("c4_64k wave:", gdp.cost_wave(gdp.Graph(g64, workloads.features(g64)), gdp.Topo(workloads.topology(g64, 8))), flush=True)
 ok &= check("c4_64k", g64, 8, 16)
-for B in (296, 1332):
+for B in (296, 2368):
     D = np.random.default_rng(1).integers(0, 8, size=(B, g4.N)).astype(np.uint8)
     k, r, pk, bz, rw, args = run(g4, workloads.topology(g4, 8), D, 8)
     G, T, Dg, rep, peak, busy, rew, ws = args

@@ -10,7 +10,7 @@ __graft_entry__.build()
 import paper_1910_01578_b200 as gdp
 g = workloads.config("c4").graphs[0]
 G = gdp.Graph(g, workloads.features(g)); T = gdp.Topo(workloads.topology(g, 8))
-B = int(sys.argv[1]) if len(sys.argv) > 1 else 1776
+B = int(sys.argv[1]) if len(sys.argv) > 1 else 2368
 ws = torch.empty(gdp.workspace_size(G, gdp.default_config(8), B), dtype=torch.uint8, device="cuda")
 D = torch.from_numpy(np.random.default_rng(1).integers(0, 8, size=(B, g.N)).astype(np.uint8)).cuda()
 rep = torch.empty(B, 24, dtype=torch.uint8, device="cuda")

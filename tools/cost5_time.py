@@ -11,7 +11,7 @@ g = workloads.config(os.environ.get("CFG", "c4")).graphs[0]
 topo = workloads.topology(g, 8)
 G = gdp.Graph(g, workloads.features(g)); T = gdp.Topo(topo)
 cfg = gdp.default_config(8)
-for B in [int(x) for x in sys.argv[1:]] or [1332]:
+for B in [int(x) for x in sys.argv[1:]] or [2368]:
     ws = torch.empty(gdp.workspace_size(G, cfg, B), dtype=torch.uint8, device="cuda")
     Dg = torch.from_numpy(np.random.default_rng(1).integers(0, 8, size=(B, g.N)).astype(np.uint8)).cuda()
     rep = torch.empty(B, 24, dtype=torch.uint8, device="cuda")
